@@ -1,0 +1,196 @@
+/*
+ * csaw.h — C ABI of the B200-native C-SAW hot path (arXiv 2009.09103).
+ *
+ * "P:n" cites line n of the paper's LaTeX; "R<n>" cites reading n
+ * in DESIGN.md §3 (where the paper is silent or garbled).
+ *
+ * The library implements the paper's data-parallel hot path -- bias-based
+ * vertex selection (§2.2, §4) inside the sampling / random-walk main loop
+ * (Fig. 2(b)) -- as hand-written sm_100a CUDA kernels.  There is no
+ * CPU fallback: every entry point that computes needs a CUDA device and fails
+ * with CSAW_ERR_CUDA otherwise.
+ *
+ * Conventions shared by all entry points
+ *  - Pointers are plain host or device pointers; the library detects which with
+ *    cudaPointerGetAttributes.  Device pointers must live on the graph's device.
+ *    Host pointers are staged through library-owned device scratch inside the
+ *    call (copies on `stream`), and the call then synchronises `stream`.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  With device
+ *    buffers, csaw_walk is stream-ordered and returns after enqueue;
+ *    csaw_sample synchronises `stream` once (it must return *num_edges).
+ *  - Ownership: callers own every buffer they pass.  csaw_graph_create copies
+ *    the CSR; the graph owns its device copy and its internal scratch (reused
+ *    across calls, freed by csaw_graph_destroy).  A graph may be used by one
+ *    host thread at a time.
+ *  - Errors: every entry point returns a csaw_status, never aborts or prints;
+ *    csaw_last_error() returns a thread-local message for the last failure.
+ *  - Determinism (R7): every output is a pure function of (graph bytes, bias,
+ *    fanout / length, seeds, rng_seed, instance_base + i).  It does not depend
+ *    on the stream, GPU count, launch configuration or OOM partitioning.  Draws
+ *    are Philox4x32-10 with key (rng_seed lo, rng_seed hi) and counter
+ *    (instance, step|depth, slot, purpose<<28 | j<<14 | attempt).
+ *  - Vertex ids are uint32; CSAW_NONE (0xFFFFFFFF) marks "no vertex".
+ */
+#ifndef CSAW_H
+#define CSAW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CSAW_NONE 0xFFFFFFFFu
+#define CSAW_API __attribute__((visibility("default")))
+
+typedef enum {
+    CSAW_OK = 0,
+    CSAW_ERR_INVALID_ARG = 1,     /* bad parameter (null pointer, k >= 2^14, depth > 255, ...) */
+    CSAW_ERR_OUT_OF_RANGE = 2,    /* a seed vertex >= V */
+    CSAW_ERR_BAD_GRAPH = 3,       /* CSR validation failed (see csaw_last_error) */
+    CSAW_ERR_DEGENERATE_POOL = 4, /* reserved: walks end (pad CSAW_NONE) instead, R20 */
+    CSAW_ERR_CAPACITY = 5,        /* output capacity too small; *num_edges = required */
+    CSAW_ERR_NO_MEMORY = 6,       /* device / pinned allocation failed or budget exceeded */
+    CSAW_ERR_CUDA = 7,            /* CUDA runtime error, or no CUDA device */
+    CSAW_ERR_UNSUPPORTED = 8      /* combination not implemented (message says which) */
+} csaw_status;
+
+/* Bias selectors: the closed set of VERTEXBIAS / EDGEBIAS / UPDATE triples
+ * (Eq. 2-4) the library implements. */
+typedef enum {
+    CSAW_BIAS_UNIFORM = 0,      /* EdgeBias = 1: unbiased neighbor sampling / simple walk */
+    CSAW_BIAS_DEGREE = 1,       /* EdgeBias = deg(u): biased neighbor sampling (Fig. 1) / biased DeepWalk */
+    CSAW_BIAS_NODE2VEC = 2,     /* EdgeBias = alpha(prev, u) (R16); walks only */
+    CSAW_BIAS_FOREST_FIRE = 3,  /* uniform EdgeBias, per-vertex burn count with P_f (R15); sampling only */
+    CSAW_BIAS_LAYER = 4,        /* EdgeBias = deg(u) over the union pool of the frontier (R14); sampling only */
+    CSAW_BIAS_MDRW = 5          /* VertexBias = deg(v), EdgeBias = 1, Update = replace (Fig. 4); walks only */
+} csaw_bias_kind;
+
+typedef struct {
+    int32_t kind;       /* csaw_bias_kind */
+    double p, q;        /* node2vec return / in-out parameters, > 0 */
+    double pf;          /* forest-fire burning probability, in [0, 1) */
+    int32_t pool_size;  /* MDRW FrontierSize m (2,000), >= 1 */
+    int32_t a_max;      /* BRS attempt cap before exact updated sampling (R2); 0 = default 64; even, 2..16382 */
+} csaw_bias;
+
+/* A CSR graph: row_ptr int64[V+1] (row_ptr[0] = 0, non-decreasing, row_ptr[V] = E),
+ * col_idx uint32[E] with values < V.  Rows should be sorted ascending without
+ * duplicates (node2vec's N(prev) membership test relies on sorted rows; the
+ * library checks and reports csaw_graph_info.rows_sorted).  Host or device
+ * pointers; copied, never retained.  weights: reserved, must be NULL. */
+typedef struct {
+    int64_t num_vertices;
+    int64_t num_edges;
+    const int64_t *row_ptr;
+    const uint32_t *col_idx;
+    const float *weights;
+} csaw_csr;
+
+typedef struct {
+    int32_t device;                 /* CUDA device ordinal */
+    int64_t device_budget_bytes;    /* 0 = in-memory; > 0 = out-of-memory mode (§5) under this budget */
+    int32_t num_partitions;         /* OOM: equal contiguous vertex ranges; 0 = default 4 */
+    int32_t max_resident;           /* OOM: partitions resident at once; 0 = default 2 */
+    int32_t num_streams;            /* OOM: streams (one kernel per active partition); 0 = default 2 */
+    uint32_t flags;                 /* reserved, 0 */
+} csaw_graph_opts;
+
+typedef struct {
+    int64_t num_vertices, num_edges;
+    int64_t max_degree;
+    int64_t nonisolated;            /* vertices with degree > 0 */
+    int32_t rows_sorted;            /* 1 if every row is strictly ascending */
+    int32_t oom_mode;               /* 1 if created with a device budget */
+    int64_t device_bytes;           /* device memory held by the graph (CSR + degree + scratch) */
+} csaw_graph_info_t;
+
+typedef struct csaw_graph csaw_graph;  /* opaque */
+
+/* Counters of the last csaw_sample / csaw_walk on a graph (SURVEY §5 "metrics"). */
+typedef struct {
+    uint64_t sampled_edges;         /* SEPS numerator (R30) */
+    uint64_t pools;                 /* selection pools processed (frontier entries / walk steps) */
+    uint64_t neighbours_scanned;    /* candidates whose bias was evaluated (pass 1 of the CTPS build) */
+    uint64_t partition_loads;       /* OOM: partition transfers (Fig. 15) */
+    uint64_t h2d_bytes;             /* OOM: bytes copied host -> device for partitions */
+    double kernel_ms;               /* device time of the call's kernels (CUDA events) */
+    double transfer_ms;             /* OOM: partition-transfer time */
+} csaw_run_stats;
+
+/* Create a graph on opt->device (opt may be NULL: device 0, in-memory).
+ * Validates the CSR (row_ptr monotone, row_ptr[V] = E, col < V) on the device,
+ * builds deg[v] = row_ptr[v+1]-row_ptr[v] (u32).  Errors: INVALID_ARG (null /
+ * negative sizes / V >= 2^32-1 / weights != NULL), BAD_GRAPH, NO_MEMORY, CUDA. */
+CSAW_API csaw_status csaw_graph_create(const csaw_csr *csr, const csaw_graph_opts *opt, csaw_graph **out);
+CSAW_API csaw_status csaw_graph_destroy(csaw_graph *g);
+CSAW_API csaw_status csaw_graph_info(const csaw_graph *g, csaw_graph_info_t *out);
+
+/* Upper bound on the number of sampled edges csaw_sample can emit for
+ * neighbor / layer sampling: n * sum_d prod_{d'<=d} fanout[d'] (neighbor) or
+ * n * sum_d fanout[d] (layer).  Forest fire has no fixed bound: returns an
+ * estimate from the burn law, and csaw_sample reports CSAW_ERR_CAPACITY with
+ * the exact requirement if it is too small. */
+CSAW_API csaw_status csaw_sample_capacity(const csaw_bias *bias, const int32_t *fanout, int32_t depth,
+                                          int64_t n_instances, int64_t *capacity);
+
+/*
+ * Traversal sampling (neighbor / forest fire / layer), Fig. 2(b) main loop
+ * with Select = ITS over an integer CTPS (Eq. 1) and
+ * without-replacement collision migration by bipartite region search (§4.2,
+ * P:514-565) with bitmap collision detection.  UPDATE appends every
+ * not-yet-visited pick to the instance's next frontier (R9).
+ *
+ *   bias          kind UNIFORM, DEGREE, FOREST_FIRE or LAYER (host pointer)
+ *   fanout        host int32[depth]: NeighborSize per depth (ignored for FOREST_FIRE), 0 <= fanout < 2^14
+ *   depth         1..255
+ *   seeds         uint32[n_instances]: one seed vertex per instance (host or device)
+ *   instance_base global id of seeds[0] (multi-GPU sharding, R7)
+ *   offsets       uint64[n_instances+1]: instance i's edges are [offsets[i], offsets[i+1])
+ *   src,dst       uint32[capacity]; edge_depth uint8[capacity] (1..depth)
+ *                 per instance in canonical order (depth, src, dst) (R11)
+ *   num_edges     host int64*: total edges written (or required, on CAPACITY)
+ * Returns OUT_OF_RANGE if a seed >= V (nothing written), CAPACITY if the
+ * output does not fit (offsets written, edges not written).
+ */
+CSAW_API csaw_status csaw_sample(const csaw_graph *g, const csaw_bias *bias, const int32_t *fanout, int32_t depth,
+                                 const uint32_t *seeds, int64_t n_instances, uint64_t instance_base,
+                                 uint64_t rng_seed, uint64_t *offsets, uint32_t *src, uint32_t *dst,
+                                 uint8_t *edge_depth, int64_t capacity, int64_t *num_edges, void *stream);
+
+/*
+ * Random walks, with replacement: DEGREE (biased DeepWalk),
+ * UNIFORM (DeepWalk), NODE2VEC (step 0 uniform, R16), MDRW
+ * (multi-dimensional random walk, Fig. 4).
+ *   DEGREE / UNIFORM / NODE2VEC: seeds uint32[n_walkers]; path uint32[n_walkers][length+1],
+ *     path[w][0] = seeds[w]; a walker at a vertex with no positive-bias
+ *     neighbour stops and the rest of its row is CSAW_NONE (R20).
+ *   MDRW: seeds uint32[n_walkers][pool_size] (the instance's initial pool, slot
+ *     order); path uint32[n_walkers][length][2] = the (v, u) edge sampled at each step.
+ */
+CSAW_API csaw_status csaw_walk(const csaw_graph *g, const csaw_bias *bias, int32_t length,
+                               const uint32_t *seeds, int64_t n_walkers, uint64_t instance_base,
+                               uint64_t rng_seed, uint32_t *path, void *stream);
+
+/* Counters of the last run on g (valid after the stream completed). */
+CSAW_API csaw_status csaw_stats(const csaw_graph *g, csaw_run_stats *out);
+
+/* Thread-local description of the last error ("" if none). */
+CSAW_API const char *csaw_last_error(void);
+
+/* Library version string, e.g. "csaw-b200 0.1 sm_100a". */
+CSAW_API const char *csaw_version(void);
+
+/* Test hook: Philox4x32-10 on the device for n counters (ctr uint32[n][4],
+ * key uint32[2], out uint32[n][4]; host or device pointers).  Lets tests pin
+ * the device generator against the Random123 KATs and cuRAND's device Philox. */
+CSAW_API csaw_status csaw_philox(const uint32_t *ctr, const uint32_t *key, uint32_t *out, int64_t n);
+
+/* Test hook: compares the library's device Philox with cuRAND's
+ * curand_Philox4x32_10 on n pseudo-random counters; *mismatches = count. */
+CSAW_API csaw_status csaw_selftest_curand(int64_t n, int64_t *mismatches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CSAW_H */

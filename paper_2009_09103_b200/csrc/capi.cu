@@ -1,0 +1,527 @@
+// capi.cu — C ABI entry points, graph creation / validation, error plumbing.
+//
+// csaw_graph_create copies and validates a CSR on the device (the paper's L0
+// graph storage, §5.1 P:808-813 / Table 2 "Size (of CSR)") and precomputes the
+// degree array used by every degree bias (one 4-byte gather per neighbour
+// instead of two row_ptr reads).
+#include <cuda_runtime.h>
+#include <curand_kernel.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace csaw {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void clear_error() { g_last_error.clear(); }
+
+csaw_status cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+    char buf[512];
+    std::snprintf(buf, sizeof(buf), "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+                  cudaGetErrorString(e), what, file, line);
+    set_error(buf);
+    if (e == cudaErrorMemoryAllocation) return CSAW_ERR_NO_MEMORY;
+    return CSAW_ERR_CUDA;
+}
+
+Scratch::~Scratch() { release_all(); }
+
+void Scratch::release_all() {
+    for (auto& b : bufs_)
+        if (b.p) cudaFree(b.p);
+    bufs_.clear();
+}
+
+csaw_status Scratch::get(int slot, size_t bytes, void** out) {
+    if (slot < 0) return fail(CSAW_ERR_INVALID_ARG, "bad scratch slot");
+    if (static_cast<size_t>(slot) >= bufs_.size()) bufs_.resize(slot + 1);
+    Buf& b = bufs_[slot];
+    if (bytes == 0) bytes = 16;
+    if (b.n < bytes) {
+        if (b.p) {
+            CSAW_CUDA(cudaDeviceSynchronize());   // buffer may still be in use by queued work
+            CSAW_CUDA(cudaFree(b.p));
+            b.p = nullptr;
+            b.n = 0;
+        }
+        const size_t want = std::max(bytes, b.n + b.n / 2);
+        cudaError_t e = cudaMalloc(&b.p, want);
+        if (e != cudaSuccess) {
+            e = cudaMalloc(&b.p, bytes);
+            if (e != cudaSuccess) { b.p = nullptr; return cuda_fail(e, "cudaMalloc(scratch)", __FILE__, __LINE__); }
+            b.n = bytes;
+        } else {
+            b.n = want;
+        }
+    }
+    *out = b.p;
+    return CSAW_OK;
+}
+
+size_t Scratch::bytes_held() const {
+    size_t s = 0;
+    for (auto& b : bufs_) s += b.n;
+    return s;
+}
+
+PinnedBuf::~PinnedBuf() {
+    if (p_) cudaFreeHost(p_);
+}
+
+csaw_status PinnedBuf::get(size_t bytes, void** out) {
+    if (n_ < bytes) {
+        if (p_) cudaFreeHost(p_);
+        p_ = nullptr;
+        n_ = 0;
+        CSAW_CUDA(cudaMallocHost(&p_, bytes));
+        n_ = bytes;
+    }
+    *out = p_;
+    return CSAW_OK;
+}
+
+bool is_device_ptr(const void* p, int device) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    (void)device;
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+csaw_status begin_call(const csaw_graph* g) {
+    clear_error();
+    if (!g) return fail(CSAW_ERR_INVALID_ARG, "graph is NULL");
+    CSAW_CUDA(cudaSetDevice(g->device));
+    return CSAW_OK;
+}
+
+// ---------------------------------------------------------------- validation kernels
+struct ValidateOut {
+    unsigned long long bad_rowptr;     // first v with row_ptr[v+1] < row_ptr[v] (+1), 0 = ok
+    unsigned long long bad_col;        // first e with col[e] >= V (+1)
+    unsigned long long unsorted;       // count of rows not strictly ascending
+    unsigned long long max_deg;
+    unsigned long long nonisolated;
+};
+
+__global__ void k_validate_rows(const int64_t* __restrict__ rp, int64_t V, uint32_t* __restrict__ deg,
+                                ValidateOut* out) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = rp[v], b = rp[v + 1];
+        if (b < a) atomicMin(&out->bad_rowptr, static_cast<unsigned long long>(v + 1));
+        const int64_t d = b - a;
+        deg[v] = d > 0 ? static_cast<uint32_t>(d) : 0u;
+        if (d > 0) {
+            atomicMax(&out->max_deg, static_cast<unsigned long long>(d));
+            atomicAdd(&out->nonisolated, 1ull);
+        }
+    }
+}
+
+__global__ void k_validate_cols(const uint32_t* __restrict__ col, int64_t E, int64_t V, ValidateOut* out) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+        if (static_cast<int64_t>(col[e]) >= V) atomicMin(&out->bad_col, static_cast<unsigned long long>(e + 1));
+}
+
+// warp per row: strictly ascending check
+__global__ void k_validate_sorted(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col, int64_t V,
+                                  ValidateOut* out) {
+    const int lane = lane_id();
+    for (uint64_t v = global_warp_id(); v < static_cast<uint64_t>(V); v += total_warps()) {
+        const int64_t a = rp[v], b = rp[v + 1];
+        bool bad = false;
+        for (int64_t e = a + lane; e + 1 < b; e += 32) bad |= col[e] >= col[e + 1];
+        if (__any_sync(FULL, bad) && lane == 0) atomicAdd(&out->unsorted, 1ull);
+    }
+}
+
+}  // namespace csaw
+
+using namespace csaw;
+
+extern "C" {
+
+CSAW_API const char* csaw_last_error(void) { return g_last_error.c_str(); }
+
+CSAW_API const char* csaw_version(void) { return "csaw-b200 0.1 sm_100a"; }
+
+CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opts* opt, csaw_graph** out) {
+    clear_error();
+    if (!csr || !out) return fail(CSAW_ERR_INVALID_ARG, "csr/out is NULL");
+    *out = nullptr;
+    if (csr->num_vertices < 0 || csr->num_edges < 0) return fail(CSAW_ERR_INVALID_ARG, "negative size");
+    if (csr->num_vertices >= static_cast<int64_t>(NONE)) return fail(CSAW_ERR_INVALID_ARG, "num_vertices must be < 2^32-1");
+    if (!csr->row_ptr || (csr->num_edges > 0 && !csr->col_idx)) return fail(CSAW_ERR_INVALID_ARG, "row_ptr/col_idx is NULL");
+    if (csr->weights) return fail(CSAW_ERR_UNSUPPORTED, "edge weights are reserved (must be NULL)");
+    csaw_graph_opts o{};
+    if (opt) o = *opt;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(CSAW_ERR_CUDA, "no CUDA device: the C-SAW library has no CPU fallback");
+    }
+    if (o.device < 0 || o.device >= ndev) return fail(CSAW_ERR_INVALID_ARG, "bad device ordinal");
+    CSAW_CUDA(cudaSetDevice(o.device));
+
+    csaw_graph* g = new csaw_graph();
+    g->device = o.device;
+    g->V = csr->num_vertices;
+    g->E = csr->num_edges;
+    cudaDeviceProp prop;
+    CSAW_CUDA(cudaGetDeviceProperties(&prop, o.device));
+    g->num_sms = prop.multiProcessorCount;
+    g->oom = o.device_budget_bytes > 0;
+
+    const int64_t V = g->V, E = g->E;
+    auto cleanup = [&](csaw_status s) {
+        csaw_graph_destroy(g);
+        return s;
+    };
+    cudaError_t e;
+    e = cudaMalloc(&g->row_ptr, sizeof(int64_t) * (V + 1));
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(row_ptr)", __FILE__, __LINE__));
+    e = cudaMalloc(&g->deg, sizeof(uint32_t) * std::max<int64_t>(V, 1));
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(deg)", __FILE__, __LINE__));
+    // col: device copy in-memory; in OOM mode a temporary device copy is used for validation only
+    uint32_t* dcol = nullptr;
+    e = cudaMalloc(&dcol, sizeof(uint32_t) * std::max<int64_t>(E, 1));
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(col)", __FILE__, __LINE__));
+    e = cudaMemcpy(g->row_ptr, csr->row_ptr, sizeof(int64_t) * (V + 1), cudaMemcpyDefault);
+    if (e != cudaSuccess) { cudaFree(dcol); return cleanup(cuda_fail(e, "copy row_ptr", __FILE__, __LINE__)); }
+    if (E > 0) {
+        e = cudaMemcpy(dcol, csr->col_idx, sizeof(uint32_t) * E, cudaMemcpyDefault);
+        if (e != cudaSuccess) { cudaFree(dcol); return cleanup(cuda_fail(e, "copy col_idx", __FILE__, __LINE__)); }
+    }
+    int64_t rp_first = -1, rp_last = -1;
+    cudaMemcpy(&rp_first, g->row_ptr, sizeof(int64_t), cudaMemcpyDeviceToHost);
+    cudaMemcpy(&rp_last, g->row_ptr + V, sizeof(int64_t), cudaMemcpyDeviceToHost);
+    if (rp_first != 0 || rp_last != E) {
+        cudaFree(dcol);
+        return cleanup(fail(CSAW_ERR_BAD_GRAPH, "row_ptr[0] must be 0 and row_ptr[V] must equal num_edges"));
+    }
+    ValidateOut* dv = nullptr;
+    e = cudaMalloc(&dv, sizeof(ValidateOut));
+    if (e != cudaSuccess) { cudaFree(dcol); return cleanup(cuda_fail(e, "cudaMalloc", __FILE__, __LINE__)); }
+    ValidateOut hv{~0ull, ~0ull, 0, 0, 0};
+    cudaMemcpy(dv, &hv, sizeof(hv), cudaMemcpyHostToDevice);
+    const int blocks = g->num_sms * 8;
+    if (V > 0) k_validate_rows<<<blocks, 256>>>(g->row_ptr, V, g->deg, dv);
+    cudaMemcpy(&hv, dv, sizeof(hv), cudaMemcpyDeviceToHost);
+    if (hv.bad_rowptr != ~0ull) {
+        cudaFree(dv); cudaFree(dcol);
+        return cleanup(fail(CSAW_ERR_BAD_GRAPH, "row_ptr decreases at vertex " + std::to_string(hv.bad_rowptr - 1)));
+    }
+    if (E > 0) k_validate_cols<<<blocks, 256>>>(dcol, E, V, dv);
+    if (V > 0) k_validate_sorted<<<blocks, 256>>>(g->row_ptr, dcol, V, dv);
+    e = cudaMemcpy(&hv, dv, sizeof(hv), cudaMemcpyDeviceToHost);
+    cudaFree(dv);
+    if (e != cudaSuccess) { cudaFree(dcol); return cleanup(cuda_fail(e, "validate", __FILE__, __LINE__)); }
+    if (hv.bad_col != ~0ull) {
+        cudaFree(dcol);
+        return cleanup(fail(CSAW_ERR_BAD_GRAPH, "col_idx[" + std::to_string(hv.bad_col - 1) + "] >= num_vertices"));
+    }
+    g->max_deg = static_cast<int64_t>(hv.max_deg);
+    g->nonisolated = static_cast<int64_t>(hv.nonisolated);
+    g->rows_sorted = hv.unsorted == 0;
+    if (g->max_deg >= static_cast<int64_t>(NONE) - 64) {
+        cudaFree(dcol);
+        return cleanup(fail(CSAW_ERR_UNSUPPORTED, "max degree must be < 2^32-64"));
+    }
+    if (!g->oom) {
+        g->col = dcol;
+    } else {
+        // Out-of-memory mode (§5): the full CSR lives in pinned host memory;
+        // the device keeps row_ptr + deg and an arena of partition slots.
+        auto& st = g->oomst;
+        st.budget = o.device_budget_bytes;
+        st.P = o.num_partitions > 0 ? o.num_partitions : 4;
+        st.R = o.max_resident > 0 ? o.max_resident : 2;
+        st.S = o.num_streams > 0 ? o.num_streams : 2;
+        if (st.R > st.P) st.R = st.P;
+        e = cudaMallocHost(&st.h_col, sizeof(uint32_t) * std::max<int64_t>(E, 1));
+        if (e != cudaSuccess) { cudaFree(dcol); return cleanup(cuda_fail(e, "cudaMallocHost(col)", __FILE__, __LINE__)); }
+        e = cudaMallocHost(&st.h_row, sizeof(int64_t) * (V + 1));
+        if (e != cudaSuccess) { cudaFree(dcol); return cleanup(cuda_fail(e, "cudaMallocHost(row)", __FILE__, __LINE__)); }
+        cudaMemcpy(st.h_col, dcol, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost);
+        cudaMemcpy(st.h_row, g->row_ptr, sizeof(int64_t) * (V + 1), cudaMemcpyDeviceToHost);
+        cudaFree(dcol);
+        // equal contiguous vertex ranges, remainder to the lowest partitions (R23)
+        st.bounds.assign(st.P + 1, 0);
+        const int64_t base = V / st.P, rem = V % st.P;
+        for (int p = 0; p < st.P; ++p) st.bounds[p + 1] = st.bounds[p] + base + (p < rem ? 1 : 0);
+        st.ebeg.assign(st.P + 1, 0);
+        int64_t maxpe = 0;
+        for (int p = 0; p <= st.P; ++p) st.ebeg[p] = st.h_row[st.bounds[p]];
+        for (int p = 0; p < st.P; ++p) maxpe = std::max(maxpe, st.ebeg[p + 1] - st.ebeg[p]);
+        st.slot_edges = maxpe;
+        const int64_t resident_bytes = sizeof(int64_t) * (V + 1) + sizeof(uint32_t) * V;
+        const int64_t arena = static_cast<int64_t>(st.R) * maxpe * static_cast<int64_t>(sizeof(uint32_t));
+        if (resident_bytes + arena > st.budget) {
+            return cleanup(fail(CSAW_ERR_NO_MEMORY,
+                                "OOM mode: row_ptr+deg (" + std::to_string(resident_bytes) + " B) + " +
+                                std::to_string(st.R) + " partition slots (" + std::to_string(arena) +
+                                " B) exceed the device budget " + std::to_string(st.budget) + " B"));
+        }
+        e = cudaMalloc(&st.d_slots, std::max<int64_t>(arena, 4));
+        if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(arena)", __FILE__, __LINE__));
+        st.resident.assign(st.R, -1);
+        st.streams.resize(st.S);
+        for (auto& s : st.streams) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    }
+    cudaEventCreate(&g->ev0);
+    cudaEventCreate(&g->ev1);
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "graph_create", __FILE__, __LINE__));
+    *out = g;
+    return CSAW_OK;
+}
+
+CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
+    if (!g) return CSAW_OK;
+    cudaSetDevice(g->device);
+    cudaDeviceSynchronize();
+    if (g->row_ptr) cudaFree(g->row_ptr);
+    if (g->col) cudaFree(g->col);
+    if (g->deg) cudaFree(g->deg);
+    auto& st = g->oomst;
+    if (st.h_col) cudaFreeHost(st.h_col);
+    if (st.h_row) cudaFreeHost(st.h_row);
+    if (st.d_slots) cudaFree(st.d_slots);
+    for (auto s : st.streams) cudaStreamDestroy(s);
+    if (g->ev0) cudaEventDestroy(g->ev0);
+    if (g->ev1) cudaEventDestroy(g->ev1);
+    g->scratch.release_all();
+    delete g;
+    return CSAW_OK;
+}
+
+CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out) {
+    clear_error();
+    if (!g || !out) return fail(CSAW_ERR_INVALID_ARG, "graph/out is NULL");
+    out->num_vertices = g->V;
+    out->num_edges = g->E;
+    out->max_degree = g->max_deg;
+    out->nonisolated = g->nonisolated;
+    out->rows_sorted = g->rows_sorted;
+    out->oom_mode = g->oom ? 1 : 0;
+    out->device_bytes = sizeof(int64_t) * (g->V + 1) + sizeof(uint32_t) * g->V +
+                        (g->col ? sizeof(uint32_t) * g->E : 0) + static_cast<int64_t>(g->scratch.bytes_held()) +
+                        (g->oom ? static_cast<int64_t>(g->oomst.R) * g->oomst.slot_edges * 4 : 0);
+    return CSAW_OK;
+}
+
+CSAW_API csaw_status csaw_stats(const csaw_graph* g, csaw_run_stats* out) {
+    clear_error();
+    if (!g || !out) return fail(CSAW_ERR_INVALID_ARG, "graph/out is NULL");
+    *out = g->stats;
+    return CSAW_OK;
+}
+
+CSAW_API csaw_status csaw_sample_capacity(const csaw_bias* bias, const int32_t* fanout, int32_t depth,
+                                          int64_t n, int64_t* cap) {
+    clear_error();
+    if (!bias || !cap || n < 0 || depth < 0) return fail(CSAW_ERR_INVALID_ARG, "bad argument");
+    double total = 0;
+    if (bias->kind == CSAW_BIAS_FOREST_FIRE) {
+        // mean burn count pf/(1-pf) per expanded vertex; 4x headroom + slack
+        const double m = bias->pf / std::max(1e-9, 1.0 - bias->pf);
+        double level = 1.0;
+        for (int d = 0; d < depth; ++d) { level *= m; total += level; }
+        total = 4.0 * total * n + 1024;
+    } else if (bias->kind == CSAW_BIAS_LAYER) {
+        if (!fanout) return fail(CSAW_ERR_INVALID_ARG, "fanout is NULL");
+        for (int d = 0; d < depth; ++d) total += fanout[d];
+        total *= n;
+    } else {
+        if (!fanout) return fail(CSAW_ERR_INVALID_ARG, "fanout is NULL");
+        double level = 1.0;
+        for (int d = 0; d < depth; ++d) { level *= fanout[d]; total += level; }
+        total *= n;
+    }
+    *cap = total > 9.0e18 ? INT64_MAX : static_cast<int64_t>(total);
+    return CSAW_OK;
+}
+
+static csaw_status check_bias(const csaw_bias* b) {
+    if (!b) return fail(CSAW_ERR_INVALID_ARG, "bias is NULL");
+    if (b->kind < CSAW_BIAS_UNIFORM || b->kind > CSAW_BIAS_MDRW) return fail(CSAW_ERR_INVALID_ARG, "unknown bias kind");
+    if (b->a_max != 0 && (b->a_max < 2 || b->a_max > 16382 || (b->a_max & 1)))
+        return fail(CSAW_ERR_INVALID_ARG, "a_max must be 0 (default 64) or even in [2, 16382]");
+    return CSAW_OK;
+}
+
+CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32_t length, const uint32_t* seeds,
+                               int64_t n, uint64_t instance_base, uint64_t rng_seed, uint32_t* path, void* stream) {
+    CSAW_TRY(begin_call(g));
+    CSAW_TRY(check_bias(bias));
+    const csaw_bias b = *bias;
+    if (b.kind == CSAW_BIAS_FOREST_FIRE || b.kind == CSAW_BIAS_LAYER)
+        return fail(CSAW_ERR_INVALID_ARG, "forest fire / layer are sampling selectors (use csaw_sample)");
+    if (length < 0 || n < 0) return fail(CSAW_ERR_INVALID_ARG, "negative length / n_walkers");
+    if (b.kind == CSAW_BIAS_NODE2VEC && !(b.p > 0 && b.q > 0 && std::isfinite(b.p) && std::isfinite(b.q)))
+        return fail(CSAW_ERR_INVALID_ARG, "node2vec needs finite p, q > 0");
+    if (b.kind == CSAW_BIAS_MDRW && b.pool_size < 1) return fail(CSAW_ERR_INVALID_ARG, "MDRW needs pool_size >= 1");
+    if (instance_base + static_cast<uint64_t>(n) > 0xFFFFFFFFull)
+        return fail(CSAW_ERR_INVALID_ARG, "instance ids must fit in 32 bits");
+    if (n == 0 || (b.kind != CSAW_BIAS_MDRW && length < 0)) return CSAW_OK;
+    if (!seeds || !path) return fail(CSAW_ERR_INVALID_ARG, "seeds/path is NULL");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t nseeds = b.kind == CSAW_BIAS_MDRW ? n * static_cast<int64_t>(b.pool_size) : n;
+    const int64_t nout = b.kind == CSAW_BIAS_MDRW ? n * static_cast<int64_t>(length) * 2
+                                                  : n * (static_cast<int64_t>(length) + 1);
+    const bool seeds_dev = is_device_ptr(seeds, g->device);
+    const bool path_dev = is_device_ptr(path, g->device);
+    const uint32_t* d_seeds = seeds;
+    uint32_t* d_path = path;
+    if (!seeds_dev) {
+        void* p;
+        CSAW_TRY(g->scratch.get(SL_SEEDS, sizeof(uint32_t) * nseeds, &p));
+        CSAW_CUDA(cudaMemcpyAsync(p, seeds, sizeof(uint32_t) * nseeds, cudaMemcpyHostToDevice, st));
+        d_seeds = static_cast<const uint32_t*>(p);
+    }
+    if (!path_dev) {
+        void* p;
+        CSAW_TRY(g->scratch.get(SL_OUT, sizeof(uint32_t) * std::max<int64_t>(nout, 1), &p));
+        d_path = static_cast<uint32_t*>(p);
+    }
+    csaw_status s;
+    if (g->oom) {
+        if (b.kind != CSAW_BIAS_MDRW && b.kind != CSAW_BIAS_UNIFORM && b.kind != CSAW_BIAS_DEGREE)
+            return fail(CSAW_ERR_UNSUPPORTED, "OOM mode supports MDRW and degree/uniform walks");
+        s = run_mdrw_oom(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
+    } else {
+        s = run_walk(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
+    }
+    if (s != CSAW_OK) return s;
+    if (!path_dev) {
+        CSAW_CUDA(cudaMemcpyAsync(path, d_path, sizeof(uint32_t) * nout, cudaMemcpyDeviceToHost, st));
+    }
+    if (!seeds_dev || !path_dev) CSAW_CUDA(cudaStreamSynchronize(st));
+    return CSAW_OK;
+}
+
+CSAW_API csaw_status csaw_sample(const csaw_graph* g, const csaw_bias* bias, const int32_t* fanout, int32_t depth,
+                                 const uint32_t* seeds, int64_t n, uint64_t instance_base, uint64_t rng_seed,
+                                 uint64_t* offsets, uint32_t* src, uint32_t* dst, uint8_t* edge_depth,
+                                 int64_t capacity, int64_t* num_edges, void* stream) {
+    CSAW_TRY(begin_call(g));
+    CSAW_TRY(check_bias(bias));
+    const csaw_bias b = *bias;
+    if (b.kind == CSAW_BIAS_NODE2VEC || b.kind == CSAW_BIAS_MDRW)
+        return fail(CSAW_ERR_INVALID_ARG, "node2vec / MDRW are walk selectors (use csaw_walk)");
+    if (!num_edges) return fail(CSAW_ERR_INVALID_ARG, "num_edges is NULL");
+    *num_edges = 0;
+    if (depth < 1 || depth > 255) return fail(CSAW_ERR_INVALID_ARG, "depth must be in [1, 255]");
+    if (n < 0 || capacity < 0) return fail(CSAW_ERR_INVALID_ARG, "negative n_instances / capacity");
+    if (b.kind == CSAW_BIAS_FOREST_FIRE && !(b.pf >= 0.0 && b.pf < 1.0))
+        return fail(CSAW_ERR_INVALID_ARG, "forest fire needs pf in [0, 1)");
+    if (b.kind != CSAW_BIAS_FOREST_FIRE) {
+        if (!fanout) return fail(CSAW_ERR_INVALID_ARG, "fanout is NULL");
+        for (int d = 0; d < depth; ++d)
+            if (fanout[d] < 0 || fanout[d] >= (1 << 14)) return fail(CSAW_ERR_INVALID_ARG, "fanout must be in [0, 2^14)");
+    }
+    if (instance_base + static_cast<uint64_t>(n) > 0xFFFFFFFFull)
+        return fail(CSAW_ERR_INVALID_ARG, "instance ids must fit in 32 bits");
+    if (g->oom) return fail(CSAW_ERR_UNSUPPORTED, "OOM-mode traversal sampling is not implemented yet");
+    if (!offsets) return fail(CSAW_ERR_INVALID_ARG, "offsets is NULL");
+    if (n > 0 && !seeds) return fail(CSAW_ERR_INVALID_ARG, "seeds is NULL");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const bool seeds_dev = n == 0 || is_device_ptr(seeds, g->device);
+    const bool offs_dev = is_device_ptr(offsets, g->device);
+    const bool out_dev = capacity == 0 || is_device_ptr(dst, g->device);
+    if (capacity > 0 && (!src || !dst || !edge_depth)) return fail(CSAW_ERR_INVALID_ARG, "src/dst/edge_depth is NULL");
+    const uint32_t* d_seeds = seeds;
+    if (!seeds_dev) {
+        void* p;
+        CSAW_TRY(g->scratch.get(SL_SEEDS, sizeof(uint32_t) * n, &p));
+        CSAW_CUDA(cudaMemcpyAsync(p, seeds, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
+        d_seeds = static_cast<const uint32_t*>(p);
+    }
+    uint64_t* d_offs = offsets;
+    if (!offs_dev) {
+        void* p;
+        CSAW_TRY(g->scratch.get(SL_OFFS, sizeof(uint64_t) * (n + 1), &p));
+        d_offs = static_cast<uint64_t*>(p);
+    }
+    csaw_status s = run_sample(g, b, fanout, depth, d_seeds, n, instance_base, rng_seed, d_offs, src, dst,
+                               edge_depth, capacity, num_edges, out_dev, st);
+    if (s != CSAW_OK && s != CSAW_ERR_CAPACITY) return s;
+    if (!offs_dev) {
+        CSAW_CUDA(cudaMemcpyAsync(offsets, d_offs, sizeof(uint64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+        CSAW_CUDA(cudaStreamSynchronize(st));
+    }
+    return s;
+}
+
+// ---------------------------------------------------------------- test hooks
+__global__ void k_philox(const uint4* __restrict__ ctr, uint2 key, uint4* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = philox4x32_10(ctr[i], key);
+}
+
+CSAW_API csaw_status csaw_philox(const uint32_t* ctr, const uint32_t* key, uint32_t* out, int64_t n) {
+    clear_error();
+    if (n <= 0) return CSAW_OK;
+    if (!ctr || !key || !out) return fail(CSAW_ERR_INVALID_ARG, "NULL argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(CSAW_ERR_CUDA, "no CUDA device");
+    }
+    uint32_t hk[2];
+    CSAW_CUDA(cudaMemcpy(hk, key, sizeof(hk), cudaMemcpyDefault));
+    uint4 *dc = nullptr, *doo = nullptr;
+    CSAW_CUDA(cudaMalloc(&dc, sizeof(uint4) * n));
+    CSAW_CUDA(cudaMalloc(&doo, sizeof(uint4) * n));
+    cudaMemcpy(dc, ctr, sizeof(uint4) * n, cudaMemcpyDefault);
+    k_philox<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256>>>(dc, make_uint2(hk[0], hk[1]), doo, n);
+    cudaError_t e = cudaMemcpy(out, doo, sizeof(uint4) * n, cudaMemcpyDefault);
+    cudaFree(dc);
+    cudaFree(doo);
+    if (e != cudaSuccess) return cuda_fail(e, "csaw_philox", __FILE__, __LINE__);
+    return CSAW_OK;
+}
+
+__global__ void k_selftest_curand(int64_t n, unsigned long long* mism) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = static_cast<uint32_t>(i * 2654435761ull), b = static_cast<uint32_t>(i >> 3) ^ 0x5bd1e995u;
+        const uint4 c = make_uint4(a, b, a ^ 0xdeadbeefu, static_cast<uint32_t>(i));
+        const uint2 k = make_uint2(b * 7u + 1u, a + 12345u);
+        const uint4 mine = philox4x32_10(c, k);
+        const uint4 ref = curand_Philox4x32_10(c, k);
+        if (mine.x != ref.x || mine.y != ref.y || mine.z != ref.z || mine.w != ref.w) atomicAdd(mism, 1ull);
+    }
+}
+
+CSAW_API csaw_status csaw_selftest_curand(int64_t n, int64_t* mismatches) {
+    clear_error();
+    if (!mismatches) return fail(CSAW_ERR_INVALID_ARG, "NULL argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(CSAW_ERR_CUDA, "no CUDA device");
+    }
+    unsigned long long* d = nullptr;
+    CSAW_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
+    cudaMemset(d, 0, sizeof(unsigned long long));
+    k_selftest_curand<<<1024, 256>>>(n, d);
+    unsigned long long h = 0;
+    cudaError_t e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "selftest", __FILE__, __LINE__);
+    *mismatches = static_cast<int64_t>(h);
+    return CSAW_OK;
+}
+
+}  // extern "C"

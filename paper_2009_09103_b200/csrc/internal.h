@@ -1,0 +1,125 @@
+// internal.h — host runtime shared by the C ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/csaw.h"
+
+namespace csaw {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+void clear_error();
+
+struct Status {
+    csaw_status code;
+    Status(csaw_status c = CSAW_OK) : code(c) {}
+    bool ok() const { return code == CSAW_OK; }
+};
+
+csaw_status cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define CSAW_CUDA(call)                                                         \
+    do {                                                                        \
+        cudaError_t e_ = (call);                                                \
+        if (e_ != cudaSuccess) return ::csaw::cuda_fail(e_, #call, __FILE__, __LINE__); \
+    } while (0)
+
+#define CSAW_TRY(expr)                                                          \
+    do {                                                                        \
+        csaw_status s_ = (expr);                                                \
+        if (s_ != CSAW_OK) return s_;                                           \
+    } while (0)
+
+inline csaw_status fail(csaw_status s, const std::string& msg) {
+    set_error(msg);
+    return s;
+}
+
+// ---------------------------------------------------------------- device scratch
+// Named growable device buffers owned by a graph, reused across calls.  Growth
+// frees + re-allocates (stream-ordered alloc is avoided to keep the memory
+// footprint predictable under an OOM budget).
+class Scratch {
+public:
+    ~Scratch();
+    // Returns a device buffer of at least `bytes` for slot `slot`.
+    csaw_status get(int slot, size_t bytes, void** out);
+    size_t bytes_held() const;
+    void release_all();
+private:
+    struct Buf { void* p = nullptr; size_t n = 0; };
+    std::vector<Buf> bufs_;
+};
+
+// A pinned host staging buffer (for host-pointer arguments).
+class PinnedBuf {
+public:
+    ~PinnedBuf();
+    csaw_status get(size_t bytes, void** out);
+private:
+    void* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+// ---------------------------------------------------------------- out-of-memory state
+struct OomState {
+    int32_t P = 0;                 // partitions
+    int32_t R = 0;                 // resident slots
+    int32_t S = 0;                 // streams
+    int64_t budget = 0;
+    std::vector<int64_t> bounds;   // vertex bounds [P+1]
+    std::vector<int64_t> ebeg;     // first edge of partition p
+    int64_t slot_edges = 0;        // capacity of an arena slot in col entries
+    uint32_t* h_col = nullptr;     // pinned host col_idx (full graph)
+    int64_t* h_row = nullptr;      // pinned host row_ptr
+    uint32_t* d_slots = nullptr;   // R arena slots of col entries
+    std::vector<int32_t> resident; // partition id per slot (-1 = empty)
+    std::vector<cudaStream_t> streams;
+};
+
+}  // namespace csaw
+
+struct csaw_graph {
+    int device = 0;
+    int64_t V = 0, E = 0;
+    int64_t* row_ptr = nullptr;   // device [V+1] (in OOM mode: full row_ptr stays resident)
+    uint32_t* col = nullptr;      // device [E] (nullptr in OOM mode)
+    uint32_t* deg = nullptr;      // device [V]
+    int64_t max_deg = 0;
+    int64_t nonisolated = 0;
+    int32_t rows_sorted = 0;
+    int num_sms = 148;
+    bool oom = false;
+    csaw::OomState oomst;
+    mutable csaw::Scratch scratch;
+    mutable csaw::PinnedBuf pinned;
+    mutable csaw_run_stats stats{};
+    mutable cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace csaw {
+// scratch slot ids
+enum Slot : int {
+    SL_SEEDS = 0, SL_OUT, SL_OFFS, SL_SRC, SL_DST, SL_DEP, SL_COUNTS, SL_GLIST, SL_TMP0, SL_TMP1, SL_TMP2,
+    SL_LEVEL_BASE = 16,          // per-level arrays: SL_LEVEL_BASE + level * 16 + k
+    SL_MAX = 16 + 256 * 16
+};
+
+bool is_device_ptr(const void* p, int device);
+csaw_status begin_call(const csaw_graph* g);
+
+// walk.cu / sample.cu entry points
+csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds,
+                     int64_t n, uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st);
+csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
+                       const uint32_t* d_seeds, int64_t n, uint64_t base, uint64_t seed, uint64_t* d_offsets,
+                       uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
+                       bool out_on_device, cudaStream_t st);
+csaw_status run_mdrw_oom(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds,
+                         int64_t n, uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st);
+}  // namespace csaw

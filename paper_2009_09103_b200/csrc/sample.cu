@@ -1,0 +1,665 @@
+// sample.cu — traversal sampling: neighbor sampling (degree / uniform bias,
+// P:153-154), forest fire and layer sampling.
+//
+// Level-synchronous driver over ONE batched frontier queue that mixes all
+// instances (batched multi-instance sampling): a queue entry is
+// (VertexID, InstanceID) with CurrDepth implicit in the level.
+// Per level:
+//   bound   ub = min(k, deg) per work item (k = NeighborSize, or the burn count)
+//   scan    staging offsets
+//   select  one warp per pool: EDGEBIAS -> CTPS -> Philox -> ITS -> bitmap/BRS
+//           (select.cuh), picks written in canonical (src, dst) order
+//   update  UPDATE = visited post-filter (reading R9): candidate keys
+//           (instance, vertex) for unvisited picks, LSD radix sort, unique ->
+//           next queue sorted by (instance, vertex) (set semantics, R10)
+// Finally per-instance offsets are scanned and edges scattered in canonical
+// (depth, src, dst) order (R11).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+#include "select.cuh"
+#include "util.cuh"
+
+namespace csaw {
+
+constexpr int SEL_WARPS = 8;
+constexpr uint64_t SENT = ~0ull;
+
+enum ErrFlag : unsigned { ERR_SEED_RANGE = 1u, ERR_POOL_TOO_BIG = 2u, ERR_K_TOO_BIG = 4u };
+
+struct LevelDesc {                 // device-side view of one level
+    const uint32_t* qv;            // queue vertices (sorted within instance)
+    const uint64_t* inst_off;      // [n+1] instance segments of the queue
+    const uint64_t* eoff;          // [nwork+1] staging offsets
+    const uint64_t* rank;          // [total+1] exclusive scan of valid staged entries
+    uint64_t* lvlbase;             // [n] edges of this instance in earlier levels
+    int layer;                     // work item = instance (layer) or queue entry
+};
+
+// ---------------------------------------------------------------- kernels
+__global__ void k_init_queue(const uint32_t* __restrict__ seeds, uint64_t n, int64_t V, uint32_t* qv, uint32_t* qi,
+                             uint64_t* inst_off, unsigned* err) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n; i += (uint64_t)gridDim.x * blockDim.x) {
+        inst_off[i] = i;
+        if (i < n) {
+            const uint32_t s = seeds[i];
+            if (static_cast<int64_t>(s) >= V) atomicOr(err, ERR_SEED_RANGE);
+            qv[i] = s;
+            qi[i] = static_cast<uint32_t>(i);
+        }
+    }
+}
+
+// Forest-fire burn count: consecutive successes of o0 < theta, truncated at deg (R15).
+__device__ __forceinline__ uint32_t ff_burn(uint2 key, uint32_t inst, uint32_t d, uint32_t v, uint32_t deg,
+                                            uint64_t theta) {
+    uint32_t x = 0;
+    while (x < deg) {
+        const uint4 o = philox4x32_10(make_uint4(inst, d, v, (PURPOSE_BURN << 28) | x), key);
+        if (static_cast<uint64_t>(o.x) < theta) ++x; else break;
+    }
+    return x;
+}
+
+__global__ void k_ns_bound(const int64_t* __restrict__ rp, const uint32_t* __restrict__ qv,
+                           const uint32_t* __restrict__ qi, uint64_t nq, int ff, uint32_t fanout, uint64_t theta,
+                           uint32_t d, uint32_t base, uint2 key, uint32_t* __restrict__ ub, uint32_t* __restrict__ kq,
+                           unsigned* kmax) {
+    uint32_t mk = 0;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = qv[q];
+        const uint32_t deg = static_cast<uint32_t>(rp[v + 1] - rp[v]);
+        const uint32_t k = ff ? ff_burn(key, base + qi[q], d, v, deg, theta) : fanout;
+        kq[q] = k;
+        ub[q] = min(k, deg);
+        mk = max(mk, min(k, deg));
+    }
+    mk = __reduce_max_sync(FULL, mk);
+    if ((threadIdx.x & 31) == 0 && mk) atomicMax(kmax, mk);
+}
+
+struct U32Val {
+    const uint32_t* a;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return a[i]; }
+};
+
+template <class Pool>
+struct StageEmit {
+    uint32_t* s_inst;
+    uint32_t* s_src;
+    uint32_t* s_dst;
+    uint64_t e0;
+    uint32_t inst;
+    uint32_t src;
+    __device__ __forceinline__ void operator()(uint32_t rank, uint32_t, uint32_t item) const {
+        s_inst[e0 + rank] = inst;
+        s_src[e0 + rank] = src;
+        s_dst[e0 + rank] = item;
+    }
+};
+
+struct SelArgs {
+    const int64_t* __restrict__ rp;
+    const uint32_t* __restrict__ col;
+    const uint32_t* __restrict__ deg;
+    const uint32_t* __restrict__ qv;
+    const uint32_t* __restrict__ qi;
+    uint64_t nq;
+    const uint32_t* __restrict__ kq;
+    const uint32_t* __restrict__ ub;
+    const uint64_t* __restrict__ eoff;
+    uint32_t* s_inst;
+    uint32_t* s_src;
+    uint32_t* s_dst;
+    uint32_t d;
+    uint32_t base;
+    uint2 key;
+    uint32_t a_max;
+    PickRec* glist;
+    uint32_t kmax;
+    unsigned long long* counters;   // [0] scanned, [1] pools
+};
+
+// Neighbor sampling / forest fire: one warp per queue entry.
+template <bool kDegree>
+__global__ void __launch_bounds__(SEL_WARPS * 32) k_ns_select(SelArgs a) {
+    __shared__ uint64_t tab_all[SEL_WARPS][TAB];
+    __shared__ uint32_t bm_all[SEL_WARPS][BM_WORDS];
+    const int wib = threadIdx.x >> 5;
+    uint64_t* tab = tab_all[wib];
+    uint32_t* bm = bm_all[wib];
+    const int lane = lane_id();
+    PickRec* gl = a.glist ? a.glist + global_warp_id() * a.kmax : nullptr;
+    unsigned long long scanned = 0, pools = 0;
+    for (uint64_t q = global_warp_id(); q < a.nq; q += total_warps()) {
+        const uint32_t v = a.qv[q];
+        const uint32_t inst = a.qi[q];
+        const int64_t b0 = __ldg(a.rp + v);
+        const uint32_t n = static_cast<uint32_t>(__ldg(a.rp + v + 1) - b0);
+        const uint32_t k = a.kq[q];
+        const uint64_t e0 = a.eoff[q];
+        const uint32_t ub = a.ub[q];
+        DrawKey dk{a.key, a.base + inst, a.d, v};
+        StageEmit<int> emit{a.s_inst, a.s_src, a.s_dst, e0, inst, v};
+        uint32_t cnt = 0;
+        if (n > 0 && k > 0) {
+            if constexpr (kDegree) {
+                DegreePool P{a.col, a.deg, static_cast<uint64_t>(b0), n};
+                const Ctps C = build_ctps(P, tab);
+                cnt = select_wor(P, C, tab, bm, k, dk, a.a_max, gl, emit);
+                scanned += n;
+            } else {
+                UniformPool P{a.col, static_cast<uint64_t>(b0), n};
+                const Ctps C = build_ctps(P, tab);
+                cnt = select_wor(P, C, tab, bm, k, dk, a.a_max, gl, emit);
+            }
+            ++pools;
+        }
+        for (uint32_t r = cnt + lane; r < ub; r += 32) {
+            a.s_inst[e0 + r] = inst;
+            a.s_src[e0 + r] = v;
+            a.s_dst[e0 + r] = NONE;
+        }
+    }
+    if (lane == 0) {
+        if (scanned) atomicAdd(a.counters + 0, scanned);
+        if (pools) atomicAdd(a.counters + 1, pools);
+    }
+}
+
+// ---------------------------------------------------------------- layer sampling
+// Pool = multiset union of N(v) over the instance's sorted frontier, in that
+// order (reading R14); EDGEBIAS = deg(u).  seg_pref[j] = sum of frontier
+// degrees before segment j (relative to the instance).
+struct LayerPool {
+    static constexpr bool kClosedForm = false;
+    const int64_t* __restrict__ rp;
+    const uint32_t* __restrict__ col;
+    const uint32_t* __restrict__ deg;
+    const uint32_t* __restrict__ fv;     // frontier vertices of the instance
+    const uint64_t* __restrict__ pref;   // global exclusive prefix of frontier degrees
+    uint64_t pbase;                      // pref at the instance's first segment
+    uint32_t nf;                         // frontier size
+    uint32_t n;                          // pool size
+    // per-lane cursor
+    uint32_t seg;
+    uint64_t seg_lo, seg_hi;             // pool range of segment seg
+    int64_t seg_row;                     // rp[fv[seg]]
+
+    __device__ __forceinline__ uint32_t find_seg(uint64_t i) const {   // last j with pref_rel[j] <= i
+        uint32_t lo = 0, hi = nf;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(pref + mid) - pbase <= i) lo = mid; else hi = mid;
+        }
+        return lo;
+    }
+    __device__ __forceinline__ void set_seg(uint32_t j) {
+        seg = j;
+        seg_lo = __ldg(pref + j) - pbase;
+        seg_hi = (j + 1 < nf) ? __ldg(pref + j + 1) - pbase : n;
+        seg_row = __ldg(rp + __ldg(fv + j));
+    }
+    __device__ __forceinline__ void seek(uint32_t row0) {
+        const uint64_t i = static_cast<uint64_t>(row0) * 32 + lane_id();
+        set_seg(i < n ? find_seg(i) : nf - 1);
+    }
+    template <int NR>
+    __device__ __forceinline__ void load_rows(uint32_t row0, uint32_t (&key)[NR], uint32_t (&b)[NR]) {
+        const int lane = lane_id();
+#pragma unroll
+        for (int u = 0; u < NR; ++u) {
+            const uint64_t i = static_cast<uint64_t>(row0 + u) * 32 + lane;
+            if (i < n) {
+                while (i >= seg_hi) set_seg(seg + 1);
+                key[u] = __ldg(col + seg_row + (i - seg_lo));
+            } else {
+                key[u] = NONE;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < NR; ++u) b[u] = (key[u] != NONE) ? __ldg(deg + key[u]) : 0u;
+    }
+    __device__ __forceinline__ uint32_t item(uint32_t i) const {
+        const uint32_t j = find_seg(i);
+        const uint32_t v = __ldg(fv + j);
+        return __ldg(col + __ldg(rp + v) + (i - (__ldg(pref + j) - pbase)));
+    }
+    __device__ __forceinline__ uint32_t src_of(uint32_t i) const { return __ldg(fv + find_seg(i)); }
+};
+
+struct LayerEmit {
+    const LayerPool* P;
+    uint32_t* s_inst;
+    uint32_t* s_src;
+    uint32_t* s_dst;
+    uint64_t e0;
+    uint32_t inst;
+    __device__ __forceinline__ void operator()(uint32_t rank, uint32_t s, uint32_t item) const {
+        s_inst[e0 + rank] = inst;
+        s_src[e0 + rank] = P->src_of(s);
+        s_dst[e0 + rank] = item;
+    }
+};
+
+struct DegOfQueue {
+    const int64_t* rp;
+    const uint32_t* qv;
+    __device__ __forceinline__ uint64_t operator()(uint64_t q) const {
+        const uint32_t v = qv[q];
+        return static_cast<uint64_t>(rp[v + 1] - rp[v]);
+    }
+};
+
+__global__ void k_layer_bound(const uint64_t* __restrict__ inst_off, const uint64_t* __restrict__ qpref, uint64_t n,
+                              uint32_t fanout, uint32_t* __restrict__ ub, unsigned* err, unsigned* kmax) {
+    uint32_t mk = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t P = qpref[inst_off[i + 1]] - qpref[inst_off[i]];
+        if (P >= static_cast<uint64_t>(NONE) - 64) atomicOr(err, ERR_POOL_TOO_BIG);
+        ub[i] = static_cast<uint32_t>(min(static_cast<uint64_t>(fanout), P));
+        mk = max(mk, ub[i]);
+    }
+    mk = __reduce_max_sync(FULL, mk);
+    if ((threadIdx.x & 31) == 0 && mk) atomicMax(kmax, mk);
+}
+
+struct LayerArgs {
+    const int64_t* __restrict__ rp;
+    const uint32_t* __restrict__ col;
+    const uint32_t* __restrict__ deg;
+    const uint32_t* __restrict__ qv;
+    const uint64_t* __restrict__ inst_off;
+    const uint64_t* __restrict__ qpref;
+    uint64_t n;
+    uint32_t fanout;
+    const uint32_t* __restrict__ ub;
+    const uint64_t* __restrict__ eoff;
+    uint32_t* s_inst;
+    uint32_t* s_src;
+    uint32_t* s_dst;
+    uint32_t d;
+    uint32_t base;
+    uint2 key;
+    uint32_t a_max;
+    PickRec* glist;
+    uint32_t kmax;
+    unsigned long long* counters;
+};
+
+// one warp per instance (its layer pool)
+__global__ void __launch_bounds__(SEL_WARPS * 32) k_layer_select(LayerArgs a) {
+    __shared__ uint64_t tab_all[SEL_WARPS][TAB];
+    __shared__ uint32_t bm_all[SEL_WARPS][BM_WORDS];
+    const int wib = threadIdx.x >> 5;
+    uint64_t* tab = tab_all[wib];
+    uint32_t* bm = bm_all[wib];
+    const int lane = lane_id();
+    PickRec* gl = a.glist ? a.glist + global_warp_id() * a.kmax : nullptr;
+    unsigned long long scanned = 0, pools = 0;
+    for (uint64_t i = global_warp_id(); i < a.n; i += total_warps()) {
+        const uint64_t qb = a.inst_off[i], qe = a.inst_off[i + 1];
+        const uint64_t e0 = a.eoff[i];
+        const uint32_t ub = a.ub[i];
+        uint32_t cnt = 0;
+        if (qe > qb && ub > 0) {
+            LayerPool P;
+            P.rp = a.rp; P.col = a.col; P.deg = a.deg;
+            P.fv = a.qv + qb;
+            P.pref = a.qpref + qb;
+            P.pbase = a.qpref[qb];
+            P.nf = static_cast<uint32_t>(qe - qb);
+            P.n = static_cast<uint32_t>(a.qpref[qe] - P.pbase);
+            DrawKey dk{a.key, a.base + static_cast<uint32_t>(i), a.d, NONE};
+            LayerEmit emit{&P, a.s_inst, a.s_src, a.s_dst, e0, static_cast<uint32_t>(i)};
+            const Ctps C = build_ctps(P, tab);
+            cnt = select_wor(P, C, tab, bm, a.fanout, dk, a.a_max, gl, emit);
+            scanned += P.n;
+            ++pools;
+        }
+        for (uint32_t r = cnt + lane; r < ub; r += 32) {
+            a.s_inst[e0 + r] = static_cast<uint32_t>(i);
+            a.s_src[e0 + r] = NONE;
+            a.s_dst[e0 + r] = NONE;
+        }
+    }
+    if (lane == 0) {
+        if (scanned) atomicAdd(a.counters + 0, scanned);
+        if (pools) atomicAdd(a.counters + 1, pools);
+    }
+}
+
+// ---------------------------------------------------------------- UPDATE: next frontier
+struct VisitedArgs {
+    const uint32_t* seeds;
+    const LevelDesc* levels;   // levels[1..l] have queues; level 0 = seeds
+    int nlev;                  // number of queue levels to check beyond the seed (1..l)
+};
+
+__device__ __forceinline__ bool in_sorted(const uint32_t* a, uint64_t lo, uint64_t hi, uint32_t x) {
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        const uint32_t y = a[mid];
+        if (y == x) return true;
+        if (y < x) lo = mid + 1; else hi = mid;
+    }
+    return false;
+}
+
+__global__ void k_cand(const uint32_t* __restrict__ s_inst, const uint32_t* __restrict__ s_dst, uint64_t total,
+                       VisitedArgs va, int vbits, uint64_t* __restrict__ keys) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = s_dst[e];
+        uint64_t key = SENT;
+        if (u != NONE) {
+            const uint32_t i = s_inst[e];
+            bool vis = va.seeds[i] == u;
+            for (int l = 1; l <= va.nlev && !vis; ++l) {
+                const LevelDesc& L = va.levels[l];
+                vis = in_sorted(L.qv, L.inst_off[i], L.inst_off[i + 1], u);
+            }
+            if (!vis) key = (static_cast<uint64_t>(i) << vbits) | u;
+        }
+        keys[e] = key;
+    }
+}
+
+struct UniqueFlag {
+    const uint64_t* k;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+        const uint64_t x = k[i];
+        return (x != SENT && (i == 0 || x != k[i - 1])) ? 1u : 0u;
+    }
+};
+
+struct CompactQueue {
+    const uint64_t* k;
+    uint32_t* qv;
+    uint32_t* qi;
+    uint64_t* count;
+    int vbits;
+    __device__ __forceinline__ void operator()(uint64_t i, uint64_t e, uint64_t v) const {
+        if (v) {
+            const uint64_t x = k[i];
+            qv[e] = static_cast<uint32_t>(x & ((1ull << vbits) - 1));
+            qi[e] = static_cast<uint32_t>(x >> vbits);
+        }
+    }
+    __device__ __forceinline__ void total(uint64_t, uint64_t t) const { *count = t; }
+};
+
+__global__ void k_inst_off(const uint32_t* __restrict__ qi, uint64_t nq, uint64_t n, uint64_t* __restrict__ off) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t lo = 0, hi = nq;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (qi[mid] < i) lo = mid + 1; else hi = mid;
+        }
+        off[i] = lo;
+    }
+}
+
+struct ValidVal {
+    const uint32_t* s_dst;
+    __device__ __forceinline__ uint64_t operator()(uint64_t e) const { return s_dst[e] != NONE ? 1u : 0u; }
+};
+
+// ---------------------------------------------------------------- final assembly
+__device__ __forceinline__ uint64_t stage_begin(const LevelDesc& L, uint64_t i) {
+    return L.layer ? L.eoff[i] : L.eoff[L.inst_off[i]];
+}
+
+__global__ void k_counts(const LevelDesc* __restrict__ levels, int nlev, uint64_t n, uint64_t* __restrict__ tot) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t run = 0;
+        for (int l = 0; l < nlev; ++l) {
+            const LevelDesc& L = levels[l];
+            const uint64_t c = L.rank[stage_begin(L, i + 1)] - L.rank[stage_begin(L, i)];
+            L.lvlbase[i] = run;
+            run += c;
+        }
+        tot[i] = run;
+    }
+}
+
+struct U64Val {
+    const uint64_t* a;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const { return a[i]; }
+};
+
+__global__ void k_write(LevelDesc L, int depth1, const uint32_t* __restrict__ s_inst, const uint32_t* __restrict__ s_src,
+                        const uint32_t* __restrict__ s_dst, uint64_t total, const uint64_t* __restrict__ offsets,
+                        uint32_t* __restrict__ src, uint32_t* __restrict__ dst, uint8_t* __restrict__ dep) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = s_dst[e];
+        if (u == NONE) continue;
+        const uint32_t i = s_inst[e];
+        const uint64_t pos = offsets[i] + L.lvlbase[i] + L.rank[e] - L.rank[stage_begin(L, i)];
+        src[pos] = s_src[e];
+        dst[pos] = u;
+        dep[pos] = static_cast<uint8_t>(depth1);
+    }
+}
+
+// ---------------------------------------------------------------- host driver
+static int grid_for(const csaw_graph* g, uint64_t n, int per_block = 256) {
+    const uint64_t b = (n + per_block - 1) / per_block;
+    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(b, static_cast<uint64_t>(g->num_sms) * 16)));
+}
+
+static int sel_grid(const csaw_graph* g, uint64_t nwork) {
+    const uint64_t warps = std::min<uint64_t>(std::max<uint64_t>(nwork, 1), static_cast<uint64_t>(g->num_sms) * 64);
+    return static_cast<int>((warps + SEL_WARPS - 1) / SEL_WARPS);
+}
+
+template <class T>
+static csaw_status lvl_buf(const csaw_graph* g, int l, int k, uint64_t count, T** out) {
+    void* p;
+    CSAW_TRY(g->scratch.get(SL_LEVEL_BASE + l * 16 + k, sizeof(T) * std::max<uint64_t>(count, 1), &p));
+    *out = static_cast<T*>(p);
+    return CSAW_OK;
+}
+
+csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
+                       const uint32_t* d_seeds, int64_t n_i64, uint64_t base, uint64_t seed, uint64_t* d_offsets,
+                       uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
+                       bool out_on_device, cudaStream_t st) {
+    g->stats = csaw_run_stats{};
+    const uint64_t n = static_cast<uint64_t>(n_i64);
+    const bool layer = b.kind == CSAW_BIAS_LAYER;
+    const bool ff = b.kind == CSAW_BIAS_FOREST_FIRE;
+    const bool degree_bias = b.kind == CSAW_BIAS_DEGREE;
+    const uint32_t a_max = b.a_max ? static_cast<uint32_t>(b.a_max) : 64u;
+    const uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+    const uint64_t theta = ff ? static_cast<uint64_t>(std::floor(b.pf * 4294967296.0)) : 0;
+    const int vbits = std::max(1, bits_for(static_cast<uint64_t>(std::max<int64_t>(g->V, 1) - 1)));
+    const int ibits = std::max(1, bits_for(n > 0 ? n - 1 : 0));
+    if (vbits + ibits + 1 > 64) return fail(CSAW_ERR_UNSUPPORTED, "instance/vertex key does not fit 64 bits");
+    const int nbits = vbits + ibits + 1;
+
+    // small pinned host mailbox for per-level counts
+    void* hmb;
+    CSAW_TRY(g->pinned.get(4096, &hmb));
+    volatile uint64_t* hbox = static_cast<volatile uint64_t*>(hmb);
+
+    void *cnt_v, *part_v, *err_v;
+    CSAW_TRY(g->scratch.get(SL_COUNTS, 256, &cnt_v));
+    unsigned long long* counters = static_cast<unsigned long long*>(cnt_v);
+    unsigned* err = reinterpret_cast<unsigned*>(counters + 8);
+    unsigned* kmaxd = reinterpret_cast<unsigned*>(counters + 9);
+    uint64_t* nq_next = reinterpret_cast<uint64_t*>(counters + 10);
+    CSAW_TRY(g->scratch.get(SL_TMP2, sizeof(uint64_t) * (SCAN_MAX_GRID + 8), &part_v));
+    uint64_t* part = static_cast<uint64_t*>(part_v);
+    (void)err_v;
+    CSAW_CUDA(cudaMemsetAsync(counters, 0, 256, st));
+    CSAW_CUDA(cudaEventRecord(g->ev0, st));
+
+    std::vector<LevelDesc> hlev(depth + 1);
+    std::vector<uint64_t> totals(depth, 0);
+    std::vector<uint32_t*> sinst(depth), ssrc(depth), sdst(depth);
+
+    // level 0 queue = seeds
+    uint32_t *qv, *qi;
+    uint64_t* inst_off;
+    CSAW_TRY(lvl_buf(g, 0, 0, n, &qv));
+    CSAW_TRY(lvl_buf(g, 0, 1, n, &qi));
+    CSAW_TRY(lvl_buf(g, 0, 2, n + 1, &inst_off));
+    k_init_queue<<<grid_for(g, n + 1), 256, 0, st>>>(d_seeds, n, g->V, qv, qi, inst_off, err);
+    CSAW_CUDA(cudaGetLastError());
+    uint64_t nq = n;
+
+    // device copy of level descriptors (for the visited test / counts)
+    LevelDesc* dlev;
+    CSAW_TRY(lvl_buf(g, 255, 15, depth + 1, &dlev));
+
+    for (int l = 0; l < depth; ++l) {
+        hlev[l].qv = qv;
+        hlev[l].inst_off = inst_off;
+        hlev[l].layer = layer ? 1 : 0;
+        const uint64_t nwork = layer ? n : nq;
+        uint32_t *ub, *kq = nullptr;
+        uint64_t* eoff;
+        CSAW_TRY(lvl_buf(g, l, 3, nwork, &ub));
+        CSAW_TRY(lvl_buf(g, l, 4, nwork + 1, &eoff));
+        uint64_t* qpref = nullptr;
+        const uint32_t fan = ff ? 0u : static_cast<uint32_t>(fanout[l]);
+        CSAW_CUDA(cudaMemsetAsync(kmaxd, 0, sizeof(unsigned), st));
+        if (layer) {
+            CSAW_TRY(lvl_buf(g, l, 5, nq + 1, &qpref));
+            CSAW_TRY(device_scan(DegOfQueue{g->row_ptr, qv}, nq, ScanToArray{qpref}, part, st));
+            k_layer_bound<<<grid_for(g, n), 256, 0, st>>>(inst_off, qpref, n, fan, ub, err, kmaxd);
+        } else {
+            CSAW_TRY(lvl_buf(g, l, 5, nq, &kq));
+            if (nq > 0)
+                k_ns_bound<<<grid_for(g, nq), 256, 0, st>>>(g->row_ptr, qv, qi, nq, ff ? 1 : 0, fan, theta,
+                                                            static_cast<uint32_t>(l), static_cast<uint32_t>(base), key,
+                                                            ub, kq, kmaxd);
+        }
+        CSAW_CUDA(cudaGetLastError());
+        CSAW_TRY(device_scan(U32Val{ub}, nwork, ScanToArray{eoff}, part, st));
+        // read total staged entries + kmax + error flags
+        hbox[1] = 0; hbox[2] = 0;
+        CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[0], eoff + nwork, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[1], kmaxd, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[2], err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        CSAW_CUDA(cudaStreamSynchronize(st));
+        const uint64_t total = hbox[0];
+        const uint32_t kmax = static_cast<uint32_t>(hbox[1] & 0xFFFFFFFFu);
+        const unsigned errs = static_cast<unsigned>(hbox[2] & 0xFFFFFFFFu);
+        if (errs & ERR_SEED_RANGE) return fail(CSAW_ERR_OUT_OF_RANGE, "a seed vertex is >= num_vertices");
+        if (errs & ERR_POOL_TOO_BIG) return fail(CSAW_ERR_UNSUPPORTED, "a layer pool has >= 2^32-64 candidates");
+        if (kmax >= (1u << 14)) return fail(CSAW_ERR_UNSUPPORTED, "a pool needs >= 2^14 picks (draw counter field)");
+        totals[l] = total;
+        uint32_t *s_inst, *s_src, *s_dst;
+        CSAW_TRY(lvl_buf(g, l, 6, total, &s_inst));
+        CSAW_TRY(lvl_buf(g, l, 7, total, &s_src));
+        CSAW_TRY(lvl_buf(g, l, 8, total, &s_dst));
+        sinst[l] = s_inst; ssrc[l] = s_src; sdst[l] = s_dst;
+        PickRec* glist = nullptr;
+        const int sgrid = sel_grid(g, nwork);
+        if (kmax > 32) {
+            void* p;
+            CSAW_TRY(g->scratch.get(SL_GLIST, sizeof(PickRec) * kmax * static_cast<uint64_t>(sgrid) * SEL_WARPS, &p));
+            glist = static_cast<PickRec*>(p);
+        }
+        if (nwork > 0 && total > 0) {
+            if (layer) {
+                LayerArgs la{g->row_ptr, g->col, g->deg, qv, inst_off, qpref, n, fan, ub, eoff, s_inst, s_src, s_dst,
+                             static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters};
+                k_layer_select<<<sgrid, SEL_WARPS * 32, 0, st>>>(la);
+            } else {
+                SelArgs sa{g->row_ptr, g->col, g->deg, qv, qi, nq, kq, ub, eoff, s_inst, s_src, s_dst,
+                           static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters};
+                if (degree_bias) k_ns_select<true><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
+                else k_ns_select<false><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
+            }
+            CSAW_CUDA(cudaGetLastError());
+        }
+        // rank of valid staged entries (final assembly)
+        uint64_t* rank;
+        CSAW_TRY(lvl_buf(g, l, 9, total + 1, &rank));
+        CSAW_TRY(device_scan(ValidVal{s_dst}, total, ScanToArray{rank}, part, st));
+        hlev[l].eoff = eoff;
+        hlev[l].rank = rank;
+        uint64_t* lvlbase;
+        CSAW_TRY(lvl_buf(g, l, 10, n, &lvlbase));
+        hlev[l].lvlbase = lvlbase;
+
+        if (l + 1 == depth) break;
+        // ---- UPDATE: next frontier (visited post-filter, set semantics)
+        CSAW_CUDA(cudaMemcpyAsync(dlev, hlev.data(), sizeof(LevelDesc) * (l + 1), cudaMemcpyHostToDevice, st));
+        uint64_t *keys, *alt, *hist, *hoffs;
+        CSAW_TRY(lvl_buf(g, l, 11, total, &keys));
+        CSAW_TRY(lvl_buf(g, l, 12, total, &alt));
+        const int rg = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(512, (total + 4095) / 4096)));
+        CSAW_TRY(lvl_buf(g, l, 13, static_cast<uint64_t>(256) * rg, &hist));
+        CSAW_TRY(lvl_buf(g, l, 14, static_cast<uint64_t>(256) * rg + 1, &hoffs));
+        VisitedArgs va{d_seeds, dlev, l};
+        if (total > 0) k_cand<<<grid_for(g, total), 256, 0, st>>>(s_inst, s_dst, total, va, vbits, keys);
+        CSAW_CUDA(cudaGetLastError());
+        uint64_t* sorted = keys;
+        CSAW_TRY(radix_sort_u64(keys, alt, total, nbits, hist, hoffs, part, &sorted, st));
+        uint32_t *nqv, *nqi;
+        uint64_t* noff;
+        CSAW_TRY(lvl_buf(g, l + 1, 0, total, &nqv));
+        CSAW_TRY(lvl_buf(g, l + 1, 1, total, &nqi));
+        CSAW_TRY(lvl_buf(g, l + 1, 2, n + 1, &noff));
+        CSAW_TRY(device_scan(UniqueFlag{sorted}, total, CompactQueue{sorted, nqv, nqi, nq_next, vbits}, part, st));
+        CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[3], nq_next, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        CSAW_CUDA(cudaStreamSynchronize(st));
+        nq = hbox[3];
+        k_inst_off<<<grid_for(g, n + 1), 256, 0, st>>>(nqi, nq, n, noff);
+        CSAW_CUDA(cudaGetLastError());
+        qv = nqv; qi = nqi; inst_off = noff;
+    }
+
+    // ---- final assembly: per-instance offsets in canonical (depth, src, dst) order
+    CSAW_CUDA(cudaMemcpyAsync(dlev, hlev.data(), sizeof(LevelDesc) * depth, cudaMemcpyHostToDevice, st));
+    uint64_t* tot;
+    CSAW_TRY(lvl_buf(g, 254, 0, n, &tot));
+    if (n > 0) k_counts<<<grid_for(g, n), 256, 0, st>>>(dlev, depth, n, tot);
+    CSAW_TRY(device_scan(U64Val{tot}, n, ScanToArray{d_offsets}, part, st));
+    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[4], d_offsets + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[5], counters, sizeof(uint64_t) * 2, cudaMemcpyDeviceToHost, st));
+    CSAW_CUDA(cudaStreamSynchronize(st));
+    const uint64_t nedges = hbox[4];
+    *num_edges = static_cast<int64_t>(nedges);
+    g->stats.sampled_edges = nedges;
+    g->stats.neighbours_scanned = hbox[5];
+    g->stats.pools = hbox[6];
+    if (static_cast<int64_t>(nedges) > capacity) {
+        CSAW_CUDA(cudaEventRecord(g->ev1, st));
+        return fail(CSAW_ERR_CAPACITY, "output capacity " + std::to_string(capacity) + " < required " +
+                                           std::to_string(nedges));
+    }
+    uint32_t *osrc = src, *odst = dst;
+    uint8_t* odep = dep;
+    if (!out_on_device && nedges > 0) {
+        void *p0, *p1, *p2;
+        CSAW_TRY(g->scratch.get(SL_SRC, sizeof(uint32_t) * nedges, &p0));
+        CSAW_TRY(g->scratch.get(SL_DST, sizeof(uint32_t) * nedges, &p1));
+        CSAW_TRY(g->scratch.get(SL_DEP, nedges, &p2));
+        osrc = static_cast<uint32_t*>(p0); odst = static_cast<uint32_t*>(p1); odep = static_cast<uint8_t*>(p2);
+    }
+    for (int l = 0; l < depth; ++l) {
+        if (totals[l] == 0) continue;
+        k_write<<<grid_for(g, totals[l]), 256, 0, st>>>(hlev[l], l + 1, sinst[l], ssrc[l], sdst[l], totals[l],
+                                                         d_offsets, osrc, odst, odep);
+    }
+    CSAW_CUDA(cudaGetLastError());
+    CSAW_CUDA(cudaEventRecord(g->ev1, st));
+    if (!out_on_device && nedges > 0) {
+        CSAW_CUDA(cudaMemcpyAsync(src, osrc, sizeof(uint32_t) * nedges, cudaMemcpyDeviceToHost, st));
+        CSAW_CUDA(cudaMemcpyAsync(dst, odst, sizeof(uint32_t) * nedges, cudaMemcpyDeviceToHost, st));
+        CSAW_CUDA(cudaMemcpyAsync(dep, odep, nedges, cudaMemcpyDeviceToHost, st));
+    }
+    CSAW_CUDA(cudaStreamSynchronize(st));
+    return CSAW_OK;
+}
+
+}  // namespace csaw

@@ -1,0 +1,489 @@
+// walk.cu — random-walk kernels (with replacement): biased DeepWalk
+// (degree), simple walk (uniform), node2vec and
+// multi-dimensional random walk (Fig. 4).
+//
+// One warp owns one walker for its whole walk: the step loop runs inside the
+// kernel (persistent; no host round trip per step).  Each step is
+// one Select over N(cur) (§4.1): bias evaluation + Kogge-Stone CTPS in shared
+// memory, one Philox draw keyed (instance, step), inverse transform search.
+// Path entries are buffered one per lane and flushed as coalesced 128 B stores.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "internal.h"
+#include "select.cuh"
+
+namespace csaw {
+
+constexpr int WALK_WARPS = 8;   // warps per block
+
+struct WalkArgs {
+    const int64_t* __restrict__ rp;
+    const uint32_t* __restrict__ col;
+    const uint32_t* __restrict__ deg;
+    const uint32_t* __restrict__ seeds;
+    uint64_t n;
+    int32_t L;
+    uint32_t base;
+    uint2 key;
+    uint32_t* __restrict__ path;
+    unsigned long long* __restrict__ counters;   // [0] = neighbours scanned, [1] = steps
+};
+
+// path[w][pi] buffered in lane (pi & 31); flushed when a 32-block completes.
+struct PathWriter {
+    uint32_t* row;
+    uint32_t buf;
+    int32_t L;
+    __device__ __forceinline__ void put(int32_t pi, uint32_t v) {
+        const int lane = lane_id();
+        if ((pi & 31) == lane) buf = v;
+        if ((pi & 31) == 31 || pi == L) {
+            const int32_t idx = (pi & ~31) + lane;
+            if (idx <= pi) row[idx] = buf;
+        }
+    }
+};
+
+template <bool kUniform>
+__global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkArgs a) {
+    __shared__ uint64_t tab_all[WALK_WARPS][TAB];
+    uint64_t* tab = tab_all[threadIdx.x >> 5];
+    const int lane = lane_id();
+    unsigned long long scanned = 0, steps = 0;
+    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+        uint32_t cur = a.seeds[w];
+        const uint32_t inst = a.base + static_cast<uint32_t>(w);
+        PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
+        pw.put(0, cur);
+        for (int32_t t = 0; t < a.L; ++t) {
+            uint32_t nxt = NONE;
+            if (cur != NONE) {
+                const int64_t b0 = __ldg(a.rp + cur);
+                const uint32_t d = static_cast<uint32_t>(__ldg(a.rp + cur + 1) - b0);
+                if (d > 0) {
+                    const uint64_t U = draw_u64(a.key, inst, static_cast<uint32_t>(t), 0u, word3(PURPOSE_EDGE, 0, 0));
+                    if constexpr (kUniform) {
+                        nxt = __ldg(a.col + b0 + below(U, d));
+                    } else {
+                        DegreePool P{a.col, a.deg, static_cast<uint64_t>(b0), d};
+                        const Ctps C = build_ctps(P, tab);
+                        nxt = select_wr(P, C, tab, U);
+                        scanned += d;
+                    }
+                    ++steps;
+                }
+            }
+            cur = nxt;
+            pw.put(t + 1, cur);
+        }
+    }
+    if (lane == 0) {
+        if (scanned) atomicAdd(a.counters + 0, scanned);
+        if (steps) atomicAdd(a.counters + 1, steps);
+    }
+}
+
+// ---------------------------------------------------------------- node2vec
+// EdgeBias of u in N(v) with predecessor prev: class 0 (u == prev, alpha 1/p),
+// class 1 (u in N(prev), alpha 1), class 2 (otherwise, alpha 1/q) -- Grover &
+// Leskovec's second-order bias (reading R16).  Membership in the
+// sorted N(prev) is a warp-cooperative merge: rows of N(v) (ascending) are
+// matched against a 32-entry window of N(prev) held one per lane, searched
+// with 5 shuffle steps; the window only moves forward (32-ary jumps).
+struct Node2vecPool {
+    static constexpr bool kClosedForm = false;
+    const uint32_t* __restrict__ col;
+    uint64_t beg;       // N(v) = col[beg, beg + n)
+    uint32_t n;
+    const uint32_t* __restrict__ nprev;   // N(prev) = nprev[0, np)
+    uint64_t np;
+    uint32_t prev;
+    uint32_t w[3];      // bias per class (integer path), or class codes {0,1,2} (float path)
+    // merge state
+    uint64_t wp;        // window start in N(prev)
+    uint32_t W;         // lane's window element (NONE beyond np)
+    bool wvalid;
+
+    __device__ __forceinline__ void seek(uint32_t) { wvalid = false; wp = 0; }
+
+    __device__ __forceinline__ void load_window(uint64_t at) {
+        wp = at;
+        const uint64_t p = at + lane_id();
+        W = p < np ? __ldg(nprev + p) : NONE;
+        wvalid = true;
+    }
+
+    // membership of each lane's u (ascending across lanes; NONE = invalid lane)
+    __device__ __forceinline__ bool member_row(uint32_t u) {
+        const bool valid = u != NONE;
+        const unsigned vm = __ballot_sync(FULL, valid);
+        if (!vm || np == 0) return false;
+        const uint32_t umin = __shfl_sync(FULL, u, __ffs(vm) - 1);
+        if (!wvalid || __shfl_sync(FULL, W, 31) < umin)
+            load_window(warp_lower_bound(nprev, wvalid ? wp + 32 : 0, np, umin));
+        bool mem = false, open = valid;
+        for (;;) {
+            // lower_bound of u in the 32-entry window by shuffle binary search
+            int idx = 0;
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+                const uint32_t wv = __shfl_sync(FULL, W, idx + s - 1);
+                if (wv < u) idx += s;
+            }
+            const bool found = __shfl_sync(FULL, W, idx) == u;
+            const uint32_t w31 = __shfl_sync(FULL, W, 31);
+            if (open && u <= w31) { mem = found; open = false; }
+            const unsigned om = __ballot_sync(FULL, open);
+            if (!om) break;
+            const uint32_t un = __shfl_sync(FULL, u, __ffs(om) - 1);
+            load_window(warp_lower_bound(nprev, wp + 32, np, un));
+        }
+        return mem;
+    }
+
+    template <int NR>
+    __device__ __forceinline__ void load_rows(uint32_t row0, uint32_t (&key)[NR], uint32_t (&b)[NR]) {
+        const int lane = lane_id();
+#pragma unroll
+        for (int u = 0; u < NR; ++u) {
+            const uint32_t i = (row0 + u) * 32 + lane;
+            key[u] = (i < n) ? __ldg(col + beg + i) : NONE;
+        }
+#pragma unroll
+        for (int u = 0; u < NR; ++u) {
+            const bool mem = member_row(key[u]);
+            b[u] = key[u] == NONE ? 0u : (key[u] == prev ? w[0] : (mem ? w[1] : w[2]));
+        }
+    }
+    __device__ __forceinline__ uint32_t item(uint32_t i) const { return __ldg(col + beg + i); }
+};
+
+struct N2vArgs {
+    WalkArgs wa;
+    uint32_t wint[3];    // integer biases {m/p, m, m/q} (R16); unused on the float path
+    float wf[3];         // float biases {(float)(1/p), 1, (float)(1/q)}
+};
+
+// Float CTPS (general p, q): fp32 biases summed in fp64 (north star; R28).
+__device__ __forceinline__ double warp_incl_scan_f64(double v) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(FULL, v, o);
+        if (lane >= o) v += y;
+    }
+    return v;
+}
+
+// One float-path step: x = r*T with r = (U >> 11) 2^-53; s = first i with S_{i+1} > x
+// (clamped to n-1).  Two passes: totals per chunk of U rows, then a rescan.
+__device__ uint32_t n2v_float_step(Node2vecPool& P, const float (&wf)[3], double* ftab, uint64_t U64) {
+    const int lane = lane_id();
+    const uint32_t n = P.n;
+    const uint32_t nrows = (n + 31) >> 5;
+    const uint32_t m = max(static_cast<uint32_t>(U), ((nrows + TAB - 1) / TAB + U - 1) / U * U);
+    double carry = 0.0;
+    uint32_t chunk = 0;
+    P.seek(0);
+    for (uint32_t c0 = 0; c0 < nrows; c0 += m) {
+        const uint32_t c1 = min(c0 + m, nrows);
+        for (uint32_t r0 = c0; r0 < c1; r0 += U) {
+            uint32_t key[U], b[U];
+            P.template load_rows<U>(r0, key, b);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const double bv = key[u] == NONE ? 0.0 : static_cast<double>(wf[b[u]]);
+                carry += __shfl_sync(FULL, warp_incl_scan_f64(bv), 31);
+            }
+        }
+        if (lane == 0) ftab[chunk] = carry;
+        ++chunk;
+    }
+    __syncwarp();
+    const double T = carry;
+    const double r = static_cast<double>(U64 >> 11) * (1.0 / 9007199254740992.0);
+    const double x = r * T;
+    uint32_t c = 0;
+    while (c + 1 < chunk && ftab[c] <= x) ++c;   // chunk containing x (clamped to the last)
+    double base = c ? ftab[c - 1] : 0.0;
+    const uint32_t rbeg = c * m, rend = min(rbeg + m, nrows);
+    P.seek(rbeg);
+    uint32_t last_item = NONE;
+    for (uint32_t r0 = rbeg; r0 < rend; r0 += U) {
+        uint32_t key[U], b[U];
+        P.template load_rows<U>(r0, key, b);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const double bv = key[u] == NONE ? 0.0 : static_cast<double>(wf[b[u]]);
+            const double incl = warp_incl_scan_f64(bv) + base;
+            const unsigned hit = __ballot_sync(FULL, key[u] != NONE && incl > x);
+            const unsigned vm = __ballot_sync(FULL, key[u] != NONE);
+            if (vm) last_item = __shfl_sync(FULL, key[u], 31 - __clz(vm));
+            if (hit) return __shfl_sync(FULL, key[u], __ffs(hit) - 1);
+            base = __shfl_sync(FULL, incl, 31);
+        }
+    }
+    return last_item;   // x >= T after rounding: the last candidate
+}
+
+template <bool kFloat>
+__global__ void __launch_bounds__(WALK_WARPS * 32) k_node2vec(N2vArgs na) {
+    __shared__ uint64_t tab_all[WALK_WARPS][TAB];
+    uint64_t* tab = tab_all[threadIdx.x >> 5];
+    const WalkArgs& a = na.wa;
+    const int lane = lane_id();
+    unsigned long long scanned = 0, steps = 0;
+    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+        uint32_t cur = a.seeds[w], prev = NONE;
+        const uint32_t inst = a.base + static_cast<uint32_t>(w);
+        PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
+        pw.put(0, cur);
+        for (int32_t t = 0; t < a.L; ++t) {
+            uint32_t nxt = NONE;
+            if (cur != NONE) {
+                const int64_t b0 = __ldg(a.rp + cur);
+                const uint32_t d = static_cast<uint32_t>(__ldg(a.rp + cur + 1) - b0);
+                if (d > 0) {
+                    const uint64_t U64 = draw_u64(a.key, inst, static_cast<uint32_t>(t), 0u, word3(PURPOSE_EDGE, 0, 0));
+                    if (prev == NONE) {
+                        nxt = __ldg(a.col + b0 + below(U64, d));     // step 0: uniform (R16)
+                    } else {
+                        const int64_t p0 = __ldg(a.rp + prev);
+                        Node2vecPool P;
+                        P.col = a.col; P.beg = static_cast<uint64_t>(b0); P.n = d;
+                        P.nprev = a.col + p0;
+                        P.np = static_cast<uint64_t>(__ldg(a.rp + prev + 1) - p0);
+                        P.prev = prev;
+                        P.wp = 0; P.W = NONE; P.wvalid = false;
+                        if constexpr (kFloat) {
+                            P.w[0] = 0; P.w[1] = 1; P.w[2] = 2;
+                            nxt = n2v_float_step(P, na.wf, reinterpret_cast<double*>(tab), U64);
+                        } else {
+                            P.w[0] = na.wint[0]; P.w[1] = na.wint[1]; P.w[2] = na.wint[2];
+                            const Ctps C = build_ctps(P, tab);
+                            nxt = select_wr(P, C, tab, U64);
+                        }
+                        scanned += d;
+                    }
+                    ++steps;
+                }
+            }
+            prev = cur;
+            cur = nxt;
+            pw.put(t + 1, cur);
+        }
+    }
+    if (lane == 0) {
+        if (scanned) atomicAdd(a.counters + 0, scanned);
+        if (steps) atomicAdd(a.counters + 1, steps);
+    }
+}
+
+// Host twin of the oracle's reading R16 (independent code): smallest m in
+// [1, 2^16] with m/p and m/q integers in [1, 2^32); 0 = float path.
+static uint32_t n2v_integer_scale(double p, double q) {
+    for (uint32_t m = 1; m <= 65536u; ++m) {
+        const double a = static_cast<double>(m) / p, c = static_cast<double>(m) / q;
+        if (a == std::floor(a) && c == std::floor(c) && a >= 1.0 && c >= 1.0 && a < 4294967296.0 && c < 4294967296.0)
+            return m;
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------- MDRW
+// Multi-dimensional random walk (frontier sampling; Fig. 4): per
+// instance a pool of m vertices in slot order (R18).  VertexBias = degree:
+// the warp keeps the m biases and per-32-slot block totals (shared memory),
+// so a draw is located by a warp scan over block totals then one over a block
+// -- exactly ITS over the slot-order CTPS.  EdgeBias = 1 (closed form, one col
+// load), Update replaces the picked slot in place.
+struct MdrwArgs {
+    const int64_t* __restrict__ rp;
+    const uint32_t* __restrict__ col;
+    const uint32_t* __restrict__ seeds;   // [n][m]
+    uint64_t n;
+    int32_t m;
+    int32_t L;
+    uint32_t base;
+    uint2 key;
+    uint32_t* __restrict__ out;           // [n][L][2]
+    uint32_t* __restrict__ pool_v;        // scratch [n][m]
+    uint64_t* __restrict__ pool_rb;       // scratch [n][m]
+    uint32_t* __restrict__ gbias;         // scratch [n_warps][m] when shared memory is too small
+    uint64_t* __restrict__ gblk;          // scratch [n_warps][nblk]
+    int smem_ok;
+    int warps_per_block;
+};
+
+__global__ void k_mdrw(MdrwArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = lane_id();
+    const int wib = threadIdx.x >> 5;
+    const uint32_t m = static_cast<uint32_t>(a.m);
+    const uint32_t nblk = (m + 31) / 32;
+    uint32_t* bias;
+    uint64_t* blk;
+    if (a.smem_ok) {
+        const size_t per = ((static_cast<size_t>(m) * 4 + 15) / 16) * 16 + static_cast<size_t>(nblk) * 8;
+        unsigned char* base = smem_raw + per * wib;
+        blk = reinterpret_cast<uint64_t*>(base);
+        bias = reinterpret_cast<uint32_t*>(base + static_cast<size_t>(nblk) * 8);
+    } else {
+        const uint64_t gw = global_warp_id();
+        bias = a.gbias + gw * m;
+        blk = a.gblk + gw * nblk;
+    }
+    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+        const uint32_t inst = a.base + static_cast<uint32_t>(w);
+        uint32_t* pv = a.pool_v + w * m;
+        uint64_t* prb = a.pool_rb + w * m;
+        // init pool (slot order = seeds order)
+        for (uint32_t s = lane; s < m; s += 32) {
+            const uint32_t v = a.seeds[w * m + s];
+            const int64_t r0 = __ldg(a.rp + v);
+            pv[s] = v;
+            prb[s] = static_cast<uint64_t>(r0);
+            bias[s] = static_cast<uint32_t>(__ldg(a.rp + v + 1) - r0);
+        }
+        __syncwarp();
+        uint64_t T = 0;
+        for (uint32_t b = 0; b < nblk; ++b) {
+            const uint32_t s = b * 32 + lane;
+            const uint64_t tot = warp_sum(s < m ? bias[s] : 0u);
+            if (lane == 0) blk[b] = tot;
+            T += tot;
+        }
+        __syncwarp();
+        uint32_t* orow = a.out + w * static_cast<uint64_t>(a.L) * 2;
+        uint2 ebuf = make_uint2(NONE, NONE);
+        for (int32_t t = 0; t < a.L; ++t) {
+            uint32_t v = NONE, u = NONE;
+            if (T > 0) {
+                const uint64_t x = below(draw_u64(a.key, inst, static_cast<uint32_t>(t), 0u, word3(PURPOSE_VERTEX, 0, 0)), T);
+                // block containing x
+                uint64_t base = 0;
+                uint32_t bsel = 0;
+                uint64_t blo = 0;
+                for (uint32_t g0 = 0; g0 < nblk; g0 += 32) {
+                    const uint64_t vb = (g0 + lane < nblk) ? blk[g0 + lane] : 0;
+                    const uint64_t incl = warp_incl_scan(vb) + base;
+                    const unsigned hit = __ballot_sync(FULL, incl > x);
+                    if (hit) {
+                        const int f = __ffs(hit) - 1;
+                        bsel = g0 + f;
+                        blo = __shfl_sync(FULL, incl - vb, f);
+                        break;
+                    }
+                    base = __shfl_sync(FULL, incl, 31);
+                }
+                const uint32_t s0 = bsel * 32 + lane;
+                const uint32_t e = s0 < m ? bias[s0] : 0u;
+                const uint64_t incl2 = warp_incl_scan(static_cast<uint64_t>(e)) + blo;
+                const unsigned hit2 = __ballot_sync(FULL, incl2 > x);
+                const uint32_t slot = bsel * 32 + (__ffs(hit2) - 1);
+                const uint32_t d = bias[slot];
+                if (lane == 0) {
+                    v = pv[slot];
+                    const uint64_t rb = prb[slot];
+                    const uint64_t j = below(draw_u64(a.key, inst, static_cast<uint32_t>(t), 0u, word3(PURPOSE_EDGE, 0, 0)), d);
+                    u = __ldg(a.col + rb + j);
+                    const int64_t ru = __ldg(a.rp + u);
+                    const uint32_t du = static_cast<uint32_t>(__ldg(a.rp + u + 1) - ru);
+                    pv[slot] = u;
+                    prb[slot] = static_cast<uint64_t>(ru);
+                    bias[slot] = du;
+                    blk[bsel] = blk[bsel] + du - d;
+                    T = T + du - d;
+                }
+                __syncwarp();
+                T = __shfl_sync(FULL, T, 0);
+                v = __shfl_sync(FULL, v, 0);
+                u = __shfl_sync(FULL, u, 0);
+            }
+            // buffer 16 steps (2 words each) per 32 lanes, flush coalesced
+            const int k = t & 15;
+            if (lane == 2 * k) ebuf.x = v;
+            if (lane == 2 * k + 1) ebuf.x = u;
+            if (k == 15 || t == a.L - 1) {
+                const int32_t t0 = t & ~15;
+                const int32_t idx = t0 * 2 + lane;
+                if (idx < (t + 1) * 2) orow[idx] = ebuf.x;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------- host launchers
+static int walk_grid(const csaw_graph* g, int64_t n) {
+    const int64_t warps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 64);
+    return static_cast<int>(std::max<int64_t>(1, (warps + WALK_WARPS - 1) / WALK_WARPS));
+}
+
+csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds, int64_t n,
+                     uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st) {
+    g->stats = csaw_run_stats{};
+    void* cnt;
+    CSAW_TRY(g->scratch.get(SL_COUNTS, 64, &cnt));
+    CSAW_CUDA(cudaMemsetAsync(cnt, 0, 64, st));
+    CSAW_CUDA(cudaEventRecord(g->ev0, st));
+    const uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+    WalkArgs a{g->row_ptr, g->col, g->deg, d_seeds, static_cast<uint64_t>(n), length,
+               static_cast<uint32_t>(base), key, d_path, static_cast<unsigned long long*>(cnt)};
+    if (b.kind == CSAW_BIAS_DEGREE) {
+        k_walk<false><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a);
+    } else if (b.kind == CSAW_BIAS_UNIFORM) {
+        k_walk<true><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a);
+    } else if (b.kind == CSAW_BIAS_NODE2VEC) {
+        if (!g->rows_sorted) return fail(CSAW_ERR_BAD_GRAPH, "node2vec needs sorted CSR rows (N(prev) membership)");
+        N2vArgs na;
+        na.wa = a;
+        const uint32_t m = n2v_integer_scale(b.p, b.q);
+        na.wint[0] = m ? static_cast<uint32_t>(static_cast<double>(m) / b.p) : 0;
+        na.wint[1] = m;
+        na.wint[2] = m ? static_cast<uint32_t>(static_cast<double>(m) / b.q) : 0;
+        na.wf[0] = static_cast<float>(1.0 / b.p);
+        na.wf[1] = 1.0f;
+        na.wf[2] = static_cast<float>(1.0 / b.q);
+        if (m) k_node2vec<false><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(na);
+        else k_node2vec<true><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(na);
+    } else if (b.kind == CSAW_BIAS_MDRW) {
+        const uint32_t m = static_cast<uint32_t>(b.pool_size);
+        const uint32_t nblk = (m + 31) / 32;
+        const size_t per = ((static_cast<size_t>(m) * 4 + 15) / 16) * 16 + static_cast<size_t>(nblk) * 8;
+        int wpb = static_cast<int>(std::min<size_t>(8, (200 * 1024) / std::max<size_t>(per, 1)));
+        const bool smem_ok = wpb >= 1;
+        if (!smem_ok) wpb = 4;
+        const int64_t max_warps = static_cast<int64_t>(g->num_sms) * 48;
+        const int64_t warps = std::min<int64_t>(n, max_warps);
+        const int grid = static_cast<int>((warps + wpb - 1) / wpb);
+        void *pv, *prb, *gb = nullptr, *gk = nullptr;
+        CSAW_TRY(g->scratch.get(SL_TMP0, sizeof(uint32_t) * n * m, &pv));
+        CSAW_TRY(g->scratch.get(SL_TMP1, sizeof(uint64_t) * n * m, &prb));
+        const size_t smem = smem_ok ? per * wpb : 0;
+        if (!smem_ok) {
+            CSAW_TRY(g->scratch.get(SL_TMP2, (sizeof(uint32_t) * m + sizeof(uint64_t) * nblk) * grid * wpb, &gb));
+            gk = static_cast<char*>(gb) + sizeof(uint32_t) * m * grid * wpb;
+        } else {
+            CSAW_CUDA(cudaFuncSetAttribute(k_mdrw, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        }
+        MdrwArgs ma{g->row_ptr, g->col, d_seeds, static_cast<uint64_t>(n), b.pool_size, length,
+                    static_cast<uint32_t>(base), key, d_path, static_cast<uint32_t*>(pv),
+                    static_cast<uint64_t*>(prb), static_cast<uint32_t*>(gb), static_cast<uint64_t*>(gk),
+                    smem_ok ? 1 : 0, wpb};
+        k_mdrw<<<grid, wpb * 32, smem, st>>>(ma);
+    } else {
+        return fail(CSAW_ERR_INVALID_ARG, "bias kind is not a walk selector");
+    }
+    CSAW_CUDA(cudaGetLastError());
+    CSAW_CUDA(cudaEventRecord(g->ev1, st));
+    g->stats.sampled_edges = b.kind == CSAW_BIAS_MDRW ? static_cast<uint64_t>(n) * length
+                                                      : static_cast<uint64_t>(n) * length;
+    return CSAW_OK;
+}
+
+}  // namespace csaw
