@@ -1,0 +1,531 @@
+#!/usr/bin/env python
+"""bench.py — C-SAW hot path on B200: sampled edges per second (SEPS) + roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+A "step" is one pass of the whole hot path over one batch: for the default
+config (cfg2, BASELINE.json configs[1]) every walker of the 4,000-walker,
+2,000-step degree-biased random walk on the LJ-shaped R-MAT graph.  Inputs are
+synthetic (synth/, seeded), resident in HBM when the timed region starts; L2 is
+flushed (256 MB write) before every timed step, and each step is timed with
+CUDA events on the launching stream.  Multi-GPU: one process per GPU
+(torchrun), weak scaling (each rank runs the config's workload on its own
+disjoint instance-id range), max-over-ranks time, NCCL used only for the
+optional output gather after timing.  The oracle (oracle/) is executed only by
+the cpu_baseline leg and by --impl reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from synth import CONFIGS, degree_stats, instance_seeds, mdrw_seeds, nonisolated_vertices, rmat_csr  # noqa: E402
+
+METRIC = "sampled edges/sec (SEPS) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "sampled_edges/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rng-seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle CPU-baseline budget (wall s)")
+    ap.add_argument("--gather", action="store_true", help="NCCL-gather outputs after timing (reported apart)")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ workload description
+def workload_of(cfg):
+    """(kind, bias name, csaw entry) for a config."""
+    return {"walk": "walk", "node2vec": "walk", "mdrw": "walk",
+            "neighbor": "sample", "layer": "sample", "forest_fire": "sample"}[cfg.workload]
+
+
+def make_graph(cfg, device):
+    t0 = time.perf_counter()
+    g = rmat_csr(cfg.graph_vertices, cfg.graph_entries, cfg.graph_seed, device=device)
+    torch.cuda.synchronize(device) if device.type == "cuda" else None
+    return g, time.perf_counter() - t0
+
+
+def make_seeds(cfg, g, rank, world):
+    """This rank's instance ids [base, base+n) and seeds (weak scaling: n per rank)."""
+    if cfg.workload == "node2vec":
+        verts = nonisolated_vertices(g)
+        n = verts.numel() if cfg.n_instances == 0 else cfg.n_instances
+        return rank * n, verts[:n].to(torch.int32)
+    n = cfg.n_instances
+    if cfg.workload == "mdrw":
+        s = mdrw_seeds(g, n * world, cfg.pool_size)
+        return rank * n, s[rank * n:(rank + 1) * n].contiguous()
+    s = instance_seeds(g, n * world)
+    return rank * n, s[rank * n:(rank + 1) * n].contiguous()
+
+
+def bias_of(cs, cfg):
+    return {"walk": cs.make_bias(cfg.bias), "node2vec": cs.make_bias("node2vec", p=cfg.p, q=cfg.q),
+            "mdrw": cs.make_bias("mdrw", pool_size=cfg.pool_size), "neighbor": cs.make_bias(cfg.bias),
+            "layer": cs.make_bias("layer"), "forest_fire": cs.make_bias("forest_fire", pf=cfg.pf)}[cfg.workload]
+
+
+def algorithmic_bytes(cfg, st, n, edges):
+    """Bytes the method must move (element granularity), DESIGN.md §6:
+    degree pool: 16 (row_ptr pair) + 8 d (col + deg) per pool, + output;
+    uniform: 16 + 4 per step; node2vec: 16 + 4 d(v) + 4 d(prev); MDRW: 32 per step;
+    sampling select kernel: 16 per pool + 8 per scanned candidate + 12 per staged edge."""
+    scanned, pools = st["neighbours_scanned"], st["pools"]
+    if cfg.workload == "walk":
+        out = 4 * n * (cfg.length + 1) + 4 * n
+        if cfg.bias == "degree":
+            return 16 * pools + 8 * scanned + out
+        return 20 * pools + out
+    if cfg.workload == "node2vec":
+        return 16 * pools + 8 * scanned + 4 * n * (cfg.length + 1) + 4 * n
+    if cfg.workload == "mdrw":
+        return 32 * n * cfg.length + 16 * n * cfg.pool_size
+    if cfg.workload == "forest_fire":
+        return 16 * pools + 16 * edges
+    return 16 * pools + 8 * scanned + 12 * edges
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[6]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+# ------------------------------------------------------------------ oracle CPU baseline
+def _oracle_job(args):
+    import oracle as O
+    cfg_name, lo, hi, base, seeds, rng_seed = args
+    cfg = CONFIGS[cfg_name]
+    g = O._G
+    edges = 0
+    for j, i in enumerate(range(lo, hi)):
+        gi = base + i
+        s = seeds[j]
+        if cfg.workload == "walk":
+            O.walk(g, O.KIND_DEGREE if cfg.bias == "degree" else O.KIND_UNIFORM, cfg.length, int(s), gi, rng_seed)
+            edges += cfg.length
+        elif cfg.workload == "node2vec":
+            O.node2vec(g, cfg.p, cfg.q, cfg.length, int(s), gi, rng_seed)
+            edges += cfg.length
+        elif cfg.workload == "mdrw":
+            O.mdrw(g, s, cfg.length, gi, rng_seed)
+            edges += cfg.length
+        elif cfg.workload == "layer":
+            edges += O.layer_sample(g, list(cfg.fanout), cfg.depth, int(s), gi, rng_seed)[0].size
+        elif cfg.workload == "forest_fire":
+            edges += O.neighbor_sample(g, O.KIND_FF, [], cfg.depth, int(s), gi, rng_seed, cfg.pf)[0].size
+        else:
+            edges += O.neighbor_sample(g, O.KIND_DEGREE if cfg.bias == "degree" else O.KIND_UNIFORM,
+                                       list(cfg.fanout), cfg.depth, int(s), gi, rng_seed)[0].size
+    return edges
+
+
+def oracle_timed_sample(cfg, og, seeds_np, base, rng_seed, budget_s, workers=None):
+    """Time the oracle (as it stands) over a bounded prefix of this config's instances on
+    all host cores (independent instances).  Returns (SEPS, cores, sample text)."""
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+
+    import oracle as O
+    workers = workers or os.cpu_count() or 1
+    n = len(seeds_np)
+    O._G = og
+    # calibrate single-instance cost
+    t0 = time.perf_counter()
+    _oracle_job((cfg.name, 0, 1, base, seeds_np[:1], rng_seed))
+    t1 = max(time.perf_counter() - t0, 1e-4)
+    per_worker = max(1, int(budget_s / t1))
+    m = int(min(n, per_worker * workers))
+    m = max(m, min(n, workers))
+    chunks = np.array_split(np.arange(m), workers * 2)
+    jobs = [(cfg.name, int(c[0]), int(c[-1]) + 1, base, seeds_np[int(c[0]):int(c[-1]) + 1], rng_seed)
+            for c in chunks if c.size]
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("fork")) as ex:
+        edges = sum(ex.map(_oracle_job, jobs))
+    wall = time.perf_counter() - t0
+    sample = f"{m} of {n} instances of {cfg.name} (full length/depth each), {workers} processes"
+    return edges / wall, workers, sample, edges, wall
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    import oracle as O
+    O.build()
+    dev = torch.device("cuda:0") if torch.cuda.is_available() else torch.device("cpu")
+    g, _ = make_graph(cfg, dev)
+    base, seeds = make_seeds(cfg, g, 0, 1)
+    og = O.Graph.from_torch(g)
+    seeds_np = seeds.cpu().numpy().view(np.uint32)
+    del g
+    if dev.type == "cuda":
+        torch.cuda.empty_cache()
+    per_step = max(2.0, 120.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        oracle_timed_sample(cfg, og, seeds_np, base, args.rng_seed, min(per_step, 3.0))
+    vals, walls, samples = [], [], []
+    for _ in range(args.steps):
+        v, cores, sample, edges, wall = oracle_timed_sample(cfg, og, seeds_np, base, args.rng_seed, per_step)
+        vals.append(v)
+        walls.append(wall)
+        samples.append(sample)
+    value = statistics.mean(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(walls),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (seeded R-MAT, synth/)",
+            "config": config_block(cfg, 1, None),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": samples[-1]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(cfg, world, stats_g):
+    c = {"workload": f"{cfg.name}: {cfg.description}", "instances_per_gpu": cfg.n_instances or "all non-isolated",
+         "graph": {"V": cfg.graph_vertices, "E_target": cfg.graph_entries, "generator": "R-MAT Graph500 (0.57,0.19,0.19,0.05), symmetrised, dedup"},
+         "parallelism": f"instances sharded over {world} GPU(s), CSR replicated",
+         "l2": "flushed (256 MB write) before every timed step; CSR also larger than L2"}
+    if cfg.workload in ("walk", "node2vec", "mdrw"):
+        c["length"] = cfg.length
+    if cfg.fanout:
+        c["fanout"] = list(cfg.fanout)
+    if cfg.depth:
+        c["depth"] = cfg.depth
+    if cfg.workload == "node2vec":
+        c["p"], c["q"] = cfg.p, cfg.q
+    if cfg.workload == "forest_fire":
+        c["pf"] = cfg.pf
+    if cfg.workload == "mdrw":
+        c["pool_size"] = cfg.pool_size
+    if stats_g:
+        c["graph_stats"] = stats_g
+    return c
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    import paper_2009_09103_b200 as cs
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        print(json.dumps({"metric": METRIC, "error": "no CUDA device: the library has no CPU fallback"}))
+        return 1
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    kind = workload_of(cfg)
+
+    g, gen_s = make_graph(cfg, dev)
+    gstats = degree_stats(g)
+    base, seeds = make_seeds(cfg, g, rank, world)
+    seeds = seeds.to(dev).contiguous()
+    n = seeds.shape[0]
+    G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local)
+    bias = bias_of(cs, cfg)
+    stream = torch.cuda.current_stream(dev)
+
+    # output buffers (device) for the device-resident timed region
+    if kind == "walk":
+        shape = (n, cfg.length, 2) if cfg.workload == "mdrw" else (n, cfg.length + 1)
+        out_dev = torch.empty(shape, dtype=torch.int32, device=dev)
+
+        def step():
+            cs.csaw_walk(G, bias, seeds, cfg.length, instance_base=base, rng_seed=args.rng_seed, out=out_dev,
+                         stream=stream)
+            return n * cfg.length
+    else:
+        cap = cs.csaw_sample_capacity(bias, list(cfg.fanout), cfg.depth, n)
+        bufs = [torch.empty(n + 1, dtype=torch.int64, device=dev), torch.empty(cap, dtype=torch.int32, device=dev),
+                torch.empty(cap, dtype=torch.int32, device=dev), torch.empty(cap, dtype=torch.uint8, device=dev)]
+
+        def step():
+            nonlocal bufs, cap
+            try:
+                r = cs.csaw_sample(G, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth, instance_base=base,
+                                   rng_seed=args.rng_seed, out=bufs, stream=stream)
+            except cs.CsawError as e:
+                if e.status != 5:
+                    raise
+                cap = int(cap * 2)
+                bufs = [bufs[0]] + [torch.empty(cap, dtype=t.dtype, device=dev) for t in bufs[1:]]
+                r = cs.csaw_sample(G, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth, instance_base=base,
+                                   rng_seed=args.rng_seed, out=bufs, stream=stream)
+            return int(r[1].numel())
+
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---------------- timed region (device-resident inputs)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    evs = []
+    edges = 0
+    launches = 0
+    hot_ms, hot_launches = 0.0, 0
+    alg_bytes = 0
+    st_last = None
+    for _ in range(args.steps):
+        flush.fill_(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        edges += step()
+        e1.record(stream)
+        evs.append((e0, e1))
+        st = cs.csaw_stats(G)
+        st_last = st
+        launches += st["kernel_launches"]
+        hot_ms += st["hot_kernel_ms"]
+        hot_launches += st["hot_launches"]
+        alg_bytes += algorithmic_bytes(cfg, st, n, st["sampled_edges"])
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(step_ms)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        e = torch.tensor([edges], dtype=torch.int64, device=dev)
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+        edges_all = int(e.item())
+    else:
+        edges_all = edges
+    value = edges_all / (total_ms / 1000.0)
+
+    # ---------------- optional NCCL gather of the sampled outputs (not on the SEPS clock, G31)
+    gather_ms = None
+    if args.gather and world > 1:
+        from paper_2009_09103_b200 import dist as cdist
+        t0 = time.perf_counter()
+        if kind == "walk":
+            cdist.gather_walks(out_dev)
+        else:
+            cdist.gather_samples(*r_last(cs, G, bias, seeds, cfg, base, args, stream))
+        torch.cuda.synchronize(dev)
+        gather_ms = 1000 * (time.perf_counter() - t0)
+
+    # ---------------- end-to-end through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(cs, G, bias, seeds, cfg, base, args, kind, n, dev, world)
+
+    # ---------------- roofline of the hot kernel
+    peaks = load_peaks()
+    hot_avg_ms = hot_ms / max(hot_launches, 1)
+    bytes_per_launch = alg_bytes / max(hot_launches, 1)
+    achieved = bytes_per_launch / (hot_avg_ms / 1000.0) / 1e9 if hot_avg_ms > 0 else None
+    peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = load_traffic(cfg.name)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "kernel": hot_kernel_name(cfg), "alg_bytes_per_launch": bytes_per_launch,
+            "hot_ms_per_launch": hot_avg_ms, "hot_share_of_step": (hot_ms / total_ms) if total_ms else None,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
+
+    # ---------------- oracle CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle as O
+            O.build()
+            og = O.Graph.from_torch(g)
+            sv = seeds.cpu().numpy()
+            sv = sv.view(np.uint32) if sv.dtype == np.int32 else sv.astype(np.uint32)
+            v, cores, sample, _, _ = oracle_timed_sample(cfg, og, sv, base, args.rng_seed, args.cpu_seconds)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+        except Exception as ex:  # report, never hide
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / max(args.steps, 1), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+                "data": "synthetic (seeded R-MAT + seeds from synth/; no datasets)",
+                "config": config_block(cfg, world, gstats), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk,
+                "detail": {"edges_per_step_per_gpu": edges / max(args.steps, 1), "step_ms": step_ms,
+                           "graph_gen_s": gen_s, "gather_ms": gather_ms,
+                           "neighbours_scanned_per_step": st_last["neighbours_scanned"] if st_last else None,
+                           "pools_per_step": st_last["pools"] if st_last else None}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    G.close()
+    return 0
+
+
+def r_last(cs, G, bias, seeds, cfg, base, args, stream):
+    return cs.csaw_sample(G, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth, instance_base=base,
+                          rng_seed=args.rng_seed, stream=stream)
+
+
+def run_e2e(cs, G, bias, seeds, cfg, base, args, kind, n, dev, world):
+    """Same metric through the C ABI with pinned HOST buffers: the library copies the
+    step's seeds host->device and the step's result device->host inside the call."""
+    seeds_h = seeds.cpu().pin_memory()
+    steps = max(1, min(args.steps, 3))
+    times = []
+    edges = 0
+    if kind == "walk":
+        shape = (n, cfg.length, 2) if cfg.workload == "mdrw" else (n, cfg.length + 1)
+        out_h = torch.empty(shape, dtype=torch.int32).pin_memory()
+        cs.csaw_walk(G, bias, seeds_h, cfg.length, instance_base=base, rng_seed=args.rng_seed, out=out_h)
+        for _ in range(steps):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            cs.csaw_walk(G, bias, seeds_h, cfg.length, instance_base=base, rng_seed=args.rng_seed, out=out_h)
+            times.append(time.perf_counter() - t0)
+            edges += n * cfg.length
+        h2d = seeds_h.numel() * 4
+        d2h = out_h.numel() * 4
+    else:
+        cap = cs.csaw_sample_capacity(bias, list(cfg.fanout), cfg.depth, n) * 2
+        out_h = [torch.empty(n + 1, dtype=torch.int64).pin_memory(), torch.empty(cap, dtype=torch.int32).pin_memory(),
+                 torch.empty(cap, dtype=torch.int32).pin_memory(), torch.empty(cap, dtype=torch.uint8).pin_memory()]
+        r = cs.csaw_sample(G, bias, seeds_h, fanout=list(cfg.fanout), depth=cfg.depth, instance_base=base,
+                           rng_seed=args.rng_seed, out=out_h)
+        m = r[1].numel()
+        for _ in range(steps):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            r = cs.csaw_sample(G, bias, seeds_h, fanout=list(cfg.fanout), depth=cfg.depth, instance_base=base,
+                               rng_seed=args.rng_seed, out=out_h)
+            times.append(time.perf_counter() - t0)
+            edges += r[1].numel()
+        h2d = seeds_h.numel() * 4
+        d2h = (n + 1) * 8 + m * 9
+    t = sum(times)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ee = torch.tensor([edges], dtype=torch.int64, device=dev)
+        dist.all_reduce(ee, op=dist.ReduceOp.SUM)
+        t, edges = float(tt.item()), int(ee.item())
+    return {"value": edges / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "steps": steps, "timing": "host wall clock around the synchronous C-ABI call (max over ranks)"}
+
+
+def hot_kernel_name(cfg):
+    return {"walk": "k_walk<degree>" if cfg.bias == "degree" else "k_walk<uniform>", "node2vec": "k_node2vec<int>",
+            "mdrw": "k_mdrw", "neighbor": "k_ns_select<degree>", "layer": "k_layer_select",
+            "forest_fire": "k_ns_select<uniform>"}[cfg.workload]
+
+
+def load_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def load_traffic(cfg_name):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the hot kernel, from the
+    committed ncu --set full capture summary (profiles/ncu_traffic.json), else null."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        v = d.get(cfg_name)
+        return v.get("dram_bytes_per_launch") if isinstance(v, dict) else v
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    sys.exit(main())

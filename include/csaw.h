@@ -114,7 +114,10 @@ typedef struct {
     uint64_t neighbours_scanned;    /* candidates whose bias was evaluated (pass 1 of the CTPS build) */
     uint64_t partition_loads;       /* OOM: partition transfers (Fig. 15) */
     uint64_t h2d_bytes;             /* OOM: bytes copied host -> device for partitions */
-    double kernel_ms;               /* device time of the call's kernels (CUDA events) */
+    uint64_t kernel_launches;       /* kernels this library launched for the call */
+    uint64_t hot_launches;          /* launches of the selection ("hot") kernel */
+    double kernel_ms;               /* device time, first launch -> last completion (CUDA events) */
+    double hot_kernel_ms;           /* summed device time of the hot-kernel launches (CUDA events) */
     double transfer_ms;             /* OOM: partition-transfer time */
 } csaw_run_stats;
 
@@ -172,7 +175,7 @@ CSAW_API csaw_status csaw_walk(const csaw_graph *g, const csaw_bias *bias, int32
                                const uint32_t *seeds, int64_t n_walkers, uint64_t instance_base,
                                uint64_t rng_seed, uint32_t *path, void *stream);
 
-/* Counters of the last run on g (valid after the stream completed). */
+/* Counters of the last run on g.  Synchronises on the call's completion event. */
 CSAW_API csaw_status csaw_stats(const csaw_graph *g, csaw_run_stats *out);
 
 /* Thread-local description of the last error ("" if none). */

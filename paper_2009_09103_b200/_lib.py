@@ -75,7 +75,8 @@ class csaw_graph_info_t(C.Structure):
 
 class csaw_run_stats(C.Structure):
     _fields_ = [("sampled_edges", C.c_uint64), ("pools", C.c_uint64), ("neighbours_scanned", C.c_uint64),
-                ("partition_loads", C.c_uint64), ("h2d_bytes", C.c_uint64), ("kernel_ms", C.c_double),
+                ("partition_loads", C.c_uint64), ("h2d_bytes", C.c_uint64), ("kernel_launches", C.c_uint64),
+                ("hot_launches", C.c_uint64), ("kernel_ms", C.c_double), ("hot_kernel_ms", C.c_double),
                 ("transfer_ms", C.c_double)]
 
 

@@ -106,6 +106,41 @@ csaw_status begin_call(const csaw_graph* g) {
     return CSAW_OK;
 }
 
+thread_local uint64_t tl_launches = 0;
+
+csaw_status stats_begin(const csaw_graph* g, cudaStream_t st) {
+    g->stats = csaw_run_stats{};
+    g->hot_used = 0;
+    g->pending_counters = nullptr;
+    tl_launches = 0;
+    CSAW_CUDA(cudaEventRecord(g->ev0, st));
+    return CSAW_OK;
+}
+
+csaw_status hot_begin(const csaw_graph* g, cudaStream_t st) {
+    const size_t need = static_cast<size_t>(g->hot_used) * 2 + 2;
+    while (g->hot_ev.size() < need) {
+        cudaEvent_t e;
+        CSAW_CUDA(cudaEventCreate(&e));
+        g->hot_ev.push_back(e);
+    }
+    CSAW_CUDA(cudaEventRecord(g->hot_ev[g->hot_used * 2], st));
+    return CSAW_OK;
+}
+
+csaw_status hot_end(const csaw_graph* g, cudaStream_t st) {
+    CSAW_CUDA(cudaEventRecord(g->hot_ev[g->hot_used * 2 + 1], st));
+    ++g->hot_used;
+    return CSAW_OK;
+}
+
+csaw_status stats_end(const csaw_graph* g, cudaStream_t st) {
+    g->stats.kernel_launches = tl_launches;
+    g->stats.hot_launches = static_cast<uint64_t>(g->hot_used);
+    CSAW_CUDA(cudaEventRecord(g->ev1, st));
+    return CSAW_OK;
+}
+
 // ---------------------------------------------------------------- validation kernels
 struct ValidateOut {
     unsigned long long bad_rowptr;     // first v with row_ptr[v+1] < row_ptr[v] (+1), 0 = ok
@@ -324,6 +359,25 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
 CSAW_API csaw_status csaw_stats(const csaw_graph* g, csaw_run_stats* out) {
     clear_error();
     if (!g || !out) return fail(CSAW_ERR_INVALID_ARG, "graph/out is NULL");
+    CSAW_CUDA(cudaSetDevice(g->device));
+    CSAW_CUDA(cudaEventSynchronize(g->ev1));
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, g->ev0, g->ev1) == cudaSuccess) g->stats.kernel_ms = ms;
+    else cudaGetLastError();
+    double hot = 0.0;
+    for (int i = 0; i < g->hot_used; ++i) {
+        float h = 0.f;
+        if (cudaEventElapsedTime(&h, g->hot_ev[2 * i], g->hot_ev[2 * i + 1]) == cudaSuccess) hot += h;
+        else cudaGetLastError();
+    }
+    g->stats.hot_kernel_ms = hot;
+    if (g->pending_counters) {
+        unsigned long long c[2] = {0, 0};
+        CSAW_CUDA(cudaMemcpy(c, g->pending_counters, sizeof(c), cudaMemcpyDeviceToHost));
+        g->stats.neighbours_scanned = c[0];
+        g->stats.pools = c[1];
+        g->pending_counters = nullptr;
+    }
     *out = g->stats;
     return CSAW_OK;
 }

@@ -100,6 +100,11 @@ struct csaw_graph {
     mutable csaw::PinnedBuf pinned;
     mutable csaw_run_stats stats{};
     mutable cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // hot-kernel timing: event pairs recorded around each selection-kernel launch
+    mutable std::vector<cudaEvent_t> hot_ev;
+    mutable int hot_used = 0;
+    // device counters still to be folded into `stats` ([0] scanned, [1] pools/steps)
+    mutable const unsigned long long* pending_counters = nullptr;
 };
 
 namespace csaw {
@@ -112,6 +117,17 @@ enum Slot : int {
 
 bool is_device_ptr(const void* p, int device);
 csaw_status begin_call(const csaw_graph* g);
+
+// kernels launched by the current call (per host thread)
+extern thread_local uint64_t tl_launches;
+inline void note_launch(uint64_t k = 1) { tl_launches += k; }
+// start a call's statistics: resets counters, records ev0 on st
+csaw_status stats_begin(const csaw_graph* g, cudaStream_t st);
+// bracket one hot-kernel launch with events
+csaw_status hot_begin(const csaw_graph* g, cudaStream_t st);
+csaw_status hot_end(const csaw_graph* g, cudaStream_t st);
+// end a call: records ev1, stores the launch count
+csaw_status stats_end(const csaw_graph* g, cudaStream_t st);
 
 // walk.cu / sample.cu entry points
 csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds,

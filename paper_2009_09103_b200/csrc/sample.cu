@@ -469,7 +469,6 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
                        const uint32_t* d_seeds, int64_t n_i64, uint64_t base, uint64_t seed, uint64_t* d_offsets,
                        uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
                        bool out_on_device, cudaStream_t st) {
-    g->stats = csaw_run_stats{};
     const uint64_t n = static_cast<uint64_t>(n_i64);
     const bool layer = b.kind == CSAW_BIAS_LAYER;
     const bool ff = b.kind == CSAW_BIAS_FOREST_FIRE;
@@ -497,7 +496,7 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
     uint64_t* part = static_cast<uint64_t*>(part_v);
     (void)err_v;
     CSAW_CUDA(cudaMemsetAsync(counters, 0, 256, st));
-    CSAW_CUDA(cudaEventRecord(g->ev0, st));
+    CSAW_TRY(stats_begin(g, st));
 
     std::vector<LevelDesc> hlev(depth + 1);
     std::vector<uint64_t> totals(depth, 0);
@@ -510,6 +509,7 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
     CSAW_TRY(lvl_buf(g, 0, 1, n, &qi));
     CSAW_TRY(lvl_buf(g, 0, 2, n + 1, &inst_off));
     k_init_queue<<<grid_for(g, n + 1), 256, 0, st>>>(d_seeds, n, g->V, qv, qi, inst_off, err);
+    note_launch();
     CSAW_CUDA(cudaGetLastError());
     uint64_t nq = n;
 
@@ -533,12 +533,15 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
             CSAW_TRY(lvl_buf(g, l, 5, nq + 1, &qpref));
             CSAW_TRY(device_scan(DegOfQueue{g->row_ptr, qv}, nq, ScanToArray{qpref}, part, st));
             k_layer_bound<<<grid_for(g, n), 256, 0, st>>>(inst_off, qpref, n, fan, ub, err, kmaxd);
+            note_launch();
         } else {
             CSAW_TRY(lvl_buf(g, l, 5, nq, &kq));
-            if (nq > 0)
+            if (nq > 0) {
+                note_launch();
                 k_ns_bound<<<grid_for(g, nq), 256, 0, st>>>(g->row_ptr, qv, qi, nq, ff ? 1 : 0, fan, theta,
                                                             static_cast<uint32_t>(l), static_cast<uint32_t>(base), key,
                                                             ub, kq, kmaxd);
+            }
         }
         CSAW_CUDA(cudaGetLastError());
         CSAW_TRY(device_scan(U32Val{ub}, nwork, ScanToArray{eoff}, part, st));
@@ -568,6 +571,8 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
             glist = static_cast<PickRec*>(p);
         }
         if (nwork > 0 && total > 0) {
+            CSAW_TRY(hot_begin(g, st));
+            note_launch();
             if (layer) {
                 LayerArgs la{g->row_ptr, g->col, g->deg, qv, inst_off, qpref, n, fan, ub, eoff, s_inst, s_src, s_dst,
                              static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters};
@@ -579,6 +584,7 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
                 else k_ns_select<false><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
             }
             CSAW_CUDA(cudaGetLastError());
+            CSAW_TRY(hot_end(g, st));
         }
         // rank of valid staged entries (final assembly)
         uint64_t* rank;
@@ -600,7 +606,7 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
         CSAW_TRY(lvl_buf(g, l, 13, static_cast<uint64_t>(256) * rg, &hist));
         CSAW_TRY(lvl_buf(g, l, 14, static_cast<uint64_t>(256) * rg + 1, &hoffs));
         VisitedArgs va{d_seeds, dlev, l};
-        if (total > 0) k_cand<<<grid_for(g, total), 256, 0, st>>>(s_inst, s_dst, total, va, vbits, keys);
+        if (total > 0) { k_cand<<<grid_for(g, total), 256, 0, st>>>(s_inst, s_dst, total, va, vbits, keys); note_launch(); }
         CSAW_CUDA(cudaGetLastError());
         uint64_t* sorted = keys;
         CSAW_TRY(radix_sort_u64(keys, alt, total, nbits, hist, hoffs, part, &sorted, st));
@@ -614,6 +620,7 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
         CSAW_CUDA(cudaStreamSynchronize(st));
         nq = hbox[3];
         k_inst_off<<<grid_for(g, n + 1), 256, 0, st>>>(nqi, nq, n, noff);
+        note_launch();
         CSAW_CUDA(cudaGetLastError());
         qv = nqv; qi = nqi; inst_off = noff;
     }
@@ -622,7 +629,7 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
     CSAW_CUDA(cudaMemcpyAsync(dlev, hlev.data(), sizeof(LevelDesc) * depth, cudaMemcpyHostToDevice, st));
     uint64_t* tot;
     CSAW_TRY(lvl_buf(g, 254, 0, n, &tot));
-    if (n > 0) k_counts<<<grid_for(g, n), 256, 0, st>>>(dlev, depth, n, tot);
+    if (n > 0) { k_counts<<<grid_for(g, n), 256, 0, st>>>(dlev, depth, n, tot); note_launch(); }
     CSAW_TRY(device_scan(U64Val{tot}, n, ScanToArray{d_offsets}, part, st));
     CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[4], d_offsets + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[5], counters, sizeof(uint64_t) * 2, cudaMemcpyDeviceToHost, st));
@@ -633,7 +640,7 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
     g->stats.neighbours_scanned = hbox[5];
     g->stats.pools = hbox[6];
     if (static_cast<int64_t>(nedges) > capacity) {
-        CSAW_CUDA(cudaEventRecord(g->ev1, st));
+        CSAW_TRY(stats_end(g, st));
         return fail(CSAW_ERR_CAPACITY, "output capacity " + std::to_string(capacity) + " < required " +
                                            std::to_string(nedges));
     }
@@ -650,9 +657,10 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
         if (totals[l] == 0) continue;
         k_write<<<grid_for(g, totals[l]), 256, 0, st>>>(hlev[l], l + 1, sinst[l], ssrc[l], sdst[l], totals[l],
                                                          d_offsets, osrc, odst, odep);
+        note_launch();
     }
     CSAW_CUDA(cudaGetLastError());
-    CSAW_CUDA(cudaEventRecord(g->ev1, st));
+    CSAW_TRY(stats_end(g, st));
     if (!out_on_device && nedges > 0) {
         CSAW_CUDA(cudaMemcpyAsync(src, osrc, sizeof(uint32_t) * nedges, cudaMemcpyDeviceToHost, st));
         CSAW_CUDA(cudaMemcpyAsync(dst, odst, sizeof(uint32_t) * nedges, cudaMemcpyDeviceToHost, st));

@@ -93,10 +93,11 @@ csaw_status device_scan(Val val, uint64_t n, Out out, uint64_t* part, cudaStream
     int g = static_cast<int>(std::min<uint64_t>(SCAN_MAX_GRID, (n + 8 * SCAN_BLOCK - 1) / (8 * SCAN_BLOCK)));
     if (g < 1) g = 1;
     const uint64_t chunk = (n + g - 1) / g;
-    if (n > 0) k_scan_partials<<<g, SCAN_BLOCK, 0, st>>>(val, n, chunk, part);
+    if (n > 0) { k_scan_partials<<<g, SCAN_BLOCK, 0, st>>>(val, n, chunk, part); note_launch(); }
     else CSAW_CUDA(cudaMemsetAsync(part, 0, sizeof(uint64_t) * g, st));
     k_scan_top<<<1, SCAN_BLOCK, 0, st>>>(part, g);
     k_scan_final<<<g, SCAN_BLOCK, 0, st>>>(val, n, chunk, part, g, out);
+    note_launch(2);
     CSAW_CUDA(cudaGetLastError());
     return CSAW_OK;
 }
@@ -174,6 +175,7 @@ inline csaw_status radix_sort_u64(uint64_t* keys, uint64_t* alt, uint64_t n, int
             k_rs_hist<<<g, RS_BLOCK, 0, st>>>(a, n, chunk, shift, hist, g);
             CSAW_TRY(device_scan(HistVal{hist}, static_cast<uint64_t>(256) * g, ScanToArray{hoffs}, part, st));
             k_rs_scatter<<<g, RS_BLOCK, 0, st>>>(a, b, n, chunk, shift, hoffs, g);
+            note_launch(2);
             uint64_t* t = a; a = b; b = t;
         }
         CSAW_CUDA(cudaGetLastError());

@@ -426,11 +426,12 @@ static int walk_grid(const csaw_graph* g, int64_t n) {
 
 csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds, int64_t n,
                      uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st) {
-    g->stats = csaw_run_stats{};
     void* cnt;
     CSAW_TRY(g->scratch.get(SL_COUNTS, 64, &cnt));
     CSAW_CUDA(cudaMemsetAsync(cnt, 0, 64, st));
-    CSAW_CUDA(cudaEventRecord(g->ev0, st));
+    CSAW_TRY(stats_begin(g, st));
+    CSAW_TRY(hot_begin(g, st));
+    note_launch();
     const uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     WalkArgs a{g->row_ptr, g->col, g->deg, d_seeds, static_cast<uint64_t>(n), length,
                static_cast<uint32_t>(base), key, d_path, static_cast<unsigned long long*>(cnt)};
@@ -480,9 +481,10 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         return fail(CSAW_ERR_INVALID_ARG, "bias kind is not a walk selector");
     }
     CSAW_CUDA(cudaGetLastError());
-    CSAW_CUDA(cudaEventRecord(g->ev1, st));
-    g->stats.sampled_edges = b.kind == CSAW_BIAS_MDRW ? static_cast<uint64_t>(n) * length
-                                                      : static_cast<uint64_t>(n) * length;
+    CSAW_TRY(hot_end(g, st));
+    CSAW_TRY(stats_end(g, st));
+    g->stats.sampled_edges = static_cast<uint64_t>(n) * length;   // L edges per walker / instance (R30)
+    g->pending_counters = static_cast<const unsigned long long*>(cnt);
     return CSAW_OK;
 }
 
