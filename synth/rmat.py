@@ -109,13 +109,29 @@ def _rmat_edges(first: int, count: int, scale: int, graph_seed: int, device) -> 
 
 
 def rmat_csr(num_vertices: int, target_entries: int, graph_seed: int, device="cpu",
-             chunk: int = 1 << 26) -> RmatGraph:
-    """Symmetric, deduplicated R-MAT CSR with ~target_entries entries (see module doc)."""
+             chunk: int = 1 << 26, fill: bool = True) -> RmatGraph:
+    """Symmetric, deduplicated R-MAT CSR with ~target_entries entries (see module doc).
+
+    fill=True keeps drawing (a longer prefix of the same edge stream) until the
+    deduplicated CSR has >= 97 % of target_entries, so rejection of ids >= V and
+    duplicate edges do not shrink the graph below the paper's Table 2 size."""
+    n_draw = target_entries // 2
+    g = None
+    for _ in range(4 if fill else 1):
+        g = _rmat_once(num_vertices, target_entries, n_draw, graph_seed, device, chunk)
+        got = g.num_edges
+        if not fill or got >= 0.97 * target_entries or got == 0:
+            break
+        n_draw = int(n_draw * min(4.0, target_entries / got) * 1.01) + 1
+    return g
+
+
+def _rmat_once(num_vertices: int, target_entries: int, n_undirected: int, graph_seed: int, device,
+               chunk: int) -> RmatGraph:
     V = int(num_vertices)
     if V < 2:
         raise ValueError("need at least 2 vertices")
     scale = max(1, math.ceil(math.log2(V)))
-    n_undirected = target_entries // 2
     # label permutation: sort (hash << 32 | v) -> unique, deterministic keys
     v = torch.arange(V, dtype=torch.int64, device=device)
     pkey = (hash_stream(v, stream_key(graph_seed, 2)) << 32) | v
