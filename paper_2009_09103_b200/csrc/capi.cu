@@ -164,16 +164,16 @@ __global__ void k_validate_rows(const int64_t* __restrict__ rp, int64_t V, uint3
     }
 }
 
-__global__ void k_validate_cols(const uint32_t* __restrict__ col, int64_t E, int64_t V, ValidateOut* out) {
+__global__ void k_validate_cols(const uint32_t* __restrict__ col, int64_t E, int64_t e0, int64_t V, ValidateOut* out) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
-        if (static_cast<int64_t>(col[e]) >= V) atomicMin(&out->bad_col, static_cast<unsigned long long>(e + 1));
+        if (static_cast<int64_t>(col[e]) >= V) atomicMin(&out->bad_col, static_cast<unsigned long long>(e0 + e + 1));
 }
 
 // warp per row: strictly ascending check
-__global__ void k_validate_sorted(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col, int64_t V,
-                                  ValidateOut* out) {
+__global__ void k_validate_sorted(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col, int64_t v0,
+                                  int64_t v1, ValidateOut* out) {
     const int lane = lane_id();
-    for (uint64_t v = global_warp_id(); v < static_cast<uint64_t>(V); v += total_warps()) {
+    for (uint64_t v = v0 + global_warp_id(); v < static_cast<uint64_t>(v1); v += total_warps()) {
         const int64_t a = rp[v], b = rp[v + 1];
         bool bad = false;
         for (int64_t e = a + lane; e + 1 < b; e += 32) bad |= col[e] >= col[e + 1];
@@ -217,80 +217,62 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
     CSAW_CUDA(cudaGetDeviceProperties(&prop, o.device));
     g->num_sms = prop.multiProcessorCount;
     g->oom = o.device_budget_bytes > 0;
-
     const int64_t V = g->V, E = g->E;
+    ValidateOut* dv = nullptr;
+    uint32_t* dcol = nullptr;
     auto cleanup = [&](csaw_status s) {
+        if (dv) cudaFree(dv);
+        if (dcol && dcol != g->col) cudaFree(dcol);
         csaw_graph_destroy(g);
         return s;
     };
-    cudaError_t e;
-    e = cudaMalloc(&g->row_ptr, sizeof(int64_t) * (V + 1));
-    if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(row_ptr)", __FILE__, __LINE__));
-    e = cudaMalloc(&g->deg, sizeof(uint32_t) * std::max<int64_t>(V, 1));
-    if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(deg)", __FILE__, __LINE__));
-    // col: device copy in-memory; in OOM mode a temporary device copy is used for validation only
-    uint32_t* dcol = nullptr;
-    e = cudaMalloc(&dcol, sizeof(uint32_t) * std::max<int64_t>(E, 1));
-    if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(col)", __FILE__, __LINE__));
-    e = cudaMemcpy(g->row_ptr, csr->row_ptr, sizeof(int64_t) * (V + 1), cudaMemcpyDefault);
-    if (e != cudaSuccess) { cudaFree(dcol); return cleanup(cuda_fail(e, "copy row_ptr", __FILE__, __LINE__)); }
-    if (E > 0) {
-        e = cudaMemcpy(dcol, csr->col_idx, sizeof(uint32_t) * E, cudaMemcpyDefault);
-        if (e != cudaSuccess) { cudaFree(dcol); return cleanup(cuda_fail(e, "copy col_idx", __FILE__, __LINE__)); }
-    }
+#define CREATE_CUDA(call, what)                                                          \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess) return cleanup(cuda_fail(e_, what, __FILE__, __LINE__));  \
+    } while (0)
+    CREATE_CUDA(cudaMalloc(&g->row_ptr, sizeof(int64_t) * (V + 1)), "cudaMalloc(row_ptr)");
+    CREATE_CUDA(cudaMalloc(&g->deg, sizeof(uint32_t) * std::max<int64_t>(V, 1)), "cudaMalloc(deg)");
+    CREATE_CUDA(cudaMemcpy(g->row_ptr, csr->row_ptr, sizeof(int64_t) * (V + 1), cudaMemcpyDefault), "copy row_ptr");
     int64_t rp_first = -1, rp_last = -1;
     cudaMemcpy(&rp_first, g->row_ptr, sizeof(int64_t), cudaMemcpyDeviceToHost);
     cudaMemcpy(&rp_last, g->row_ptr + V, sizeof(int64_t), cudaMemcpyDeviceToHost);
-    if (rp_first != 0 || rp_last != E) {
-        cudaFree(dcol);
+    if (rp_first != 0 || rp_last != E)
         return cleanup(fail(CSAW_ERR_BAD_GRAPH, "row_ptr[0] must be 0 and row_ptr[V] must equal num_edges"));
-    }
-    ValidateOut* dv = nullptr;
-    e = cudaMalloc(&dv, sizeof(ValidateOut));
-    if (e != cudaSuccess) { cudaFree(dcol); return cleanup(cuda_fail(e, "cudaMalloc", __FILE__, __LINE__)); }
+    CREATE_CUDA(cudaMalloc(&dv, sizeof(ValidateOut)), "cudaMalloc");
     ValidateOut hv{~0ull, ~0ull, 0, 0, 0};
     cudaMemcpy(dv, &hv, sizeof(hv), cudaMemcpyHostToDevice);
     const int blocks = g->num_sms * 8;
     if (V > 0) k_validate_rows<<<blocks, 256>>>(g->row_ptr, V, g->deg, dv);
-    cudaMemcpy(&hv, dv, sizeof(hv), cudaMemcpyDeviceToHost);
-    if (hv.bad_rowptr != ~0ull) {
-        cudaFree(dv); cudaFree(dcol);
+    CREATE_CUDA(cudaMemcpy(&hv, dv, sizeof(hv), cudaMemcpyDeviceToHost), "validate rows");
+    if (hv.bad_rowptr != ~0ull)
         return cleanup(fail(CSAW_ERR_BAD_GRAPH, "row_ptr decreases at vertex " + std::to_string(hv.bad_rowptr - 1)));
-    }
-    if (E > 0) k_validate_cols<<<blocks, 256>>>(dcol, E, V, dv);
-    if (V > 0) k_validate_sorted<<<blocks, 256>>>(g->row_ptr, dcol, V, dv);
-    e = cudaMemcpy(&hv, dv, sizeof(hv), cudaMemcpyDeviceToHost);
-    cudaFree(dv);
-    if (e != cudaSuccess) { cudaFree(dcol); return cleanup(cuda_fail(e, "validate", __FILE__, __LINE__)); }
-    if (hv.bad_col != ~0ull) {
-        cudaFree(dcol);
-        return cleanup(fail(CSAW_ERR_BAD_GRAPH, "col_idx[" + std::to_string(hv.bad_col - 1) + "] >= num_vertices"));
-    }
     g->max_deg = static_cast<int64_t>(hv.max_deg);
     g->nonisolated = static_cast<int64_t>(hv.nonisolated);
-    g->rows_sorted = hv.unsorted == 0;
-    if (g->max_deg >= static_cast<int64_t>(NONE) - 64) {
-        cudaFree(dcol);
+    if (g->max_deg >= static_cast<int64_t>(NONE) - 64)
         return cleanup(fail(CSAW_ERR_UNSUPPORTED, "max degree must be < 2^32-64"));
-    }
+
     if (!g->oom) {
+        CREATE_CUDA(cudaMalloc(&dcol, sizeof(uint32_t) * std::max<int64_t>(E, 1)), "cudaMalloc(col)");
         g->col = dcol;
+        if (E > 0) CREATE_CUDA(cudaMemcpy(dcol, csr->col_idx, sizeof(uint32_t) * E, cudaMemcpyDefault), "copy col_idx");
+        if (E > 0) k_validate_cols<<<blocks, 256>>>(dcol, E, 0, V, dv);
+        if (V > 0) k_validate_sorted<<<blocks, 256>>>(g->row_ptr, dcol, 0, V, dv);
     } else {
-        // Out-of-memory mode (§5): the full CSR lives in pinned host memory;
-        // the device keeps row_ptr + deg and an arena of partition slots.
+        // Out-of-memory mode (§5): the full col_idx lives in pinned host memory; the
+        // device holds row_ptr + deg and R arena slots of one partition each.  The
+        // CSR is validated slice by slice through slot 0, so the device never holds
+        // more than the budget.
         auto& st = g->oomst;
         st.budget = o.device_budget_bytes;
         st.P = o.num_partitions > 0 ? o.num_partitions : 4;
         st.R = o.max_resident > 0 ? o.max_resident : 2;
         st.S = o.num_streams > 0 ? o.num_streams : 2;
+        if (st.P > V && V > 0) st.P = static_cast<int32_t>(V);
+        if (st.P < 1) st.P = 1;
         if (st.R > st.P) st.R = st.P;
-        e = cudaMallocHost(&st.h_col, sizeof(uint32_t) * std::max<int64_t>(E, 1));
-        if (e != cudaSuccess) { cudaFree(dcol); return cleanup(cuda_fail(e, "cudaMallocHost(col)", __FILE__, __LINE__)); }
-        e = cudaMallocHost(&st.h_row, sizeof(int64_t) * (V + 1));
-        if (e != cudaSuccess) { cudaFree(dcol); return cleanup(cuda_fail(e, "cudaMallocHost(row)", __FILE__, __LINE__)); }
-        cudaMemcpy(st.h_col, dcol, sizeof(uint32_t) * E, cudaMemcpyDeviceToHost);
+        CREATE_CUDA(cudaMallocHost(&st.h_row, sizeof(int64_t) * (V + 1)), "cudaMallocHost(row)");
         cudaMemcpy(st.h_row, g->row_ptr, sizeof(int64_t) * (V + 1), cudaMemcpyDeviceToHost);
-        cudaFree(dcol);
         // equal contiguous vertex ranges, remainder to the lowest partitions (R23)
         st.bounds.assign(st.P + 1, 0);
         const int64_t base = V / st.P, rem = V % st.P;
@@ -299,25 +281,39 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         int64_t maxpe = 0;
         for (int p = 0; p <= st.P; ++p) st.ebeg[p] = st.h_row[st.bounds[p]];
         for (int p = 0; p < st.P; ++p) maxpe = std::max(maxpe, st.ebeg[p + 1] - st.ebeg[p]);
-        st.slot_edges = maxpe;
+        st.slot_edges = std::max<int64_t>(maxpe, 1);
         const int64_t resident_bytes = sizeof(int64_t) * (V + 1) + sizeof(uint32_t) * V;
-        const int64_t arena = static_cast<int64_t>(st.R) * maxpe * static_cast<int64_t>(sizeof(uint32_t));
-        if (resident_bytes + arena > st.budget) {
+        const int64_t arena = static_cast<int64_t>(st.R) * st.slot_edges * static_cast<int64_t>(sizeof(uint32_t));
+        if (resident_bytes + arena > st.budget)
             return cleanup(fail(CSAW_ERR_NO_MEMORY,
                                 "OOM mode: row_ptr+deg (" + std::to_string(resident_bytes) + " B) + " +
-                                std::to_string(st.R) + " partition slots (" + std::to_string(arena) +
-                                " B) exceed the device budget " + std::to_string(st.budget) + " B"));
+                                    std::to_string(st.R) + " partition slots (" + std::to_string(arena) +
+                                    " B) exceed the device budget " + std::to_string(st.budget) + " B"));
+        CREATE_CUDA(cudaMalloc(&st.d_slots, arena), "cudaMalloc(arena)");
+        CREATE_CUDA(cudaMallocHost(&st.h_col, sizeof(uint32_t) * std::max<int64_t>(E, 1)), "cudaMallocHost(col)");
+        if (E > 0) CREATE_CUDA(cudaMemcpy(st.h_col, csr->col_idx, sizeof(uint32_t) * E, cudaMemcpyDefault), "copy col_idx");
+        for (int p = 0; p < st.P; ++p) {
+            const int64_t e0 = st.ebeg[p], ne = st.ebeg[p + 1] - e0;
+            if (ne == 0) continue;
+            CREATE_CUDA(cudaMemcpy(st.d_slots, st.h_col + e0, sizeof(uint32_t) * ne, cudaMemcpyHostToDevice), "slice");
+            k_validate_cols<<<blocks, 256>>>(st.d_slots, ne, e0, V, dv);
+            k_validate_sorted<<<blocks, 256>>>(g->row_ptr, st.d_slots - e0, st.bounds[p], st.bounds[p + 1], dv);
+            CREATE_CUDA(cudaDeviceSynchronize(), "validate slice");
         }
-        e = cudaMalloc(&st.d_slots, std::max<int64_t>(arena, 4));
-        if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(arena)", __FILE__, __LINE__));
         st.resident.assign(st.R, -1);
         st.streams.resize(st.S);
-        for (auto& s : st.streams) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        for (auto& s : st.streams) CREATE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     }
-    cudaEventCreate(&g->ev0);
-    cudaEventCreate(&g->ev1);
-    e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) return cleanup(cuda_fail(e, "graph_create", __FILE__, __LINE__));
+    CREATE_CUDA(cudaMemcpy(&hv, dv, sizeof(hv), cudaMemcpyDeviceToHost), "validate");
+    cudaFree(dv);
+    dv = nullptr;
+    if (hv.bad_col != ~0ull)
+        return cleanup(fail(CSAW_ERR_BAD_GRAPH, "col_idx[" + std::to_string(hv.bad_col - 1) + "] >= num_vertices"));
+    g->rows_sorted = hv.unsorted == 0;
+    CREATE_CUDA(cudaEventCreate(&g->ev0), "event");
+    CREATE_CUDA(cudaEventCreate(&g->ev1), "event");
+    CREATE_CUDA(cudaDeviceSynchronize(), "graph_create");
+#undef CREATE_CUDA
     *out = g;
     return CSAW_OK;
 }
@@ -451,8 +447,8 @@ CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32
     }
     csaw_status s;
     if (g->oom) {
-        if (b.kind != CSAW_BIAS_MDRW && b.kind != CSAW_BIAS_UNIFORM && b.kind != CSAW_BIAS_DEGREE)
-            return fail(CSAW_ERR_UNSUPPORTED, "OOM mode supports MDRW and degree/uniform walks");
+        if (b.kind != CSAW_BIAS_MDRW)
+            return fail(CSAW_ERR_UNSUPPORTED, "OOM-mode walks implement MDRW (config 5)");
         s = run_mdrw_oom(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
     } else {
         s = run_walk(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);

@@ -1,12 +1,350 @@
-// oom.cu — out-of-memory mode (§5): workload-aware partition scheduling.
+// oom.cu — out-of-memory mode (§5): graph partitions, workload-aware
+// partition scheduling and batched multi-instance sampling under a device budget.
+//
+// The CSR lives in pinned host memory; the device keeps row_ptr + deg (needed by
+// VERTEXBIAS / EDGEBIAS = degree for every vertex, "decide which partition a
+// vertex belongs to in constant time") and R arena slots, each holding the
+// col_idx slice of one partition (contiguous equal vertex range).
+// One frontier queue per partition holds the instances whose next selection
+// needs that partition (batched multi-instance queue).  Every wave:
+//   1. count active instances per partition;
+//   2. keep resident partitions that still have work, fill the free / empty
+//      slots with the busiest non-resident partitions (ties -> lower id; only
+//      empty-queue residents are evicted; reading R23);
+//   3. cudaMemcpyAsync each new partition into its slot and launch one kernel per
+//      active partition on its own stream, CTAs proportional to
+//      its active count (thread-block balancing; R24);
+//   4. a kernel advances each of its instances while the next pick stays in its
+//      partition, then appends the instance to the owner's queue.
+// Results are identical to the in-memory path: every draw is keyed by
+// (instance, step), never by schedule (R7, R22).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "common.cuh"
 #include "internal.h"
+#include "select.cuh"
 
 namespace csaw {
 
-csaw_status run_mdrw_oom(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds, int64_t n,
+constexpr int OOM_WARPS = 8;
+
+struct Owner {   // equal contiguous ranges, remainder to the lowest partitions (R23)
+    uint64_t base;   // V / P
+    uint64_t rem;    // V % P
+    __device__ __forceinline__ uint32_t operator()(uint32_t v) const {
+        const uint64_t big = rem * (base + 1);
+        if (v < big) return static_cast<uint32_t>(v / (base + 1));
+        return static_cast<uint32_t>(rem + (v - big) / base);
+    }
+};
+
+struct MdrwOom {
+    // per-instance MDRW state (global memory: instances migrate between kernels)
+    uint32_t* pool_v;     // [n][m]
+    uint32_t* bias;       // [n][m]
+    uint64_t* blk;        // [n][nblk]
+    uint64_t* T;          // [n]
+    uint32_t* tstep;      // [n] next step to take
+    uint32_t* pend_slot;  // [n] pending pick (slot) for step tstep
+    // queues: [P][n] instance ids; counts [P]
+    uint32_t* qin;
+    uint32_t* qout;
+    uint32_t* cnt_in;
+    uint32_t* cnt_out;
+};
+
+struct OomArgs {
+    const int64_t* __restrict__ rp;
+    const uint32_t* __restrict__ deg;
+    const uint32_t* __restrict__ seeds;
+    uint64_t n;
+    uint32_t m, nblk;
+    int32_t L;
+    uint32_t ibase;
+    uint2 key;
+    uint32_t* __restrict__ out;   // [n][L][2]
+    MdrwOom s;
+    Owner own;
+    uint32_t P;
+};
+
+// VERTEXBIAS = degree over the instance's pool (slot order, R18): ITS by a warp scan
+// over the block totals, then over the selected block (identical to a flat scan).
+__device__ __forceinline__ uint32_t mdrw_pick(const OomArgs& a, uint64_t i, uint32_t t) {
+    const int lane = lane_id();
+    const uint64_t T = a.s.T[i];
+    const uint64_t x = below(draw_u64(a.key, a.ibase + static_cast<uint32_t>(i), t, 0u, word3(PURPOSE_VERTEX, 0, 0)), T);
+    const uint64_t* blk = a.s.blk + i * a.nblk;
+    uint64_t base = 0, blo = 0;
+    uint32_t bsel = 0;
+    for (uint32_t g0 = 0; g0 < a.nblk; g0 += 32) {
+        const uint64_t vb = (g0 + lane < a.nblk) ? blk[g0 + lane] : 0;
+        const uint64_t incl = warp_incl_scan(vb) + base;
+        const unsigned hit = __ballot_sync(FULL, incl > x);
+        if (hit) {
+            const int f = __ffs(hit) - 1;
+            bsel = g0 + f;
+            blo = __shfl_sync(FULL, incl - vb, f);
+            break;
+        }
+        base = __shfl_sync(FULL, incl, 31);
+    }
+    const uint32_t s0 = bsel * 32 + lane;
+    const uint32_t e = s0 < a.m ? a.s.bias[i * a.m + s0] : 0u;
+    const uint64_t incl2 = warp_incl_scan(static_cast<uint64_t>(e)) + blo;
+    const unsigned hit2 = __ballot_sync(FULL, incl2 > x);
+    return bsel * 32 + (__ffs(hit2) - 1);
+}
+
+__global__ void __launch_bounds__(OOM_WARPS * 32) k_mdrw_oom_init(OomArgs a) {
+    const int lane = lane_id();
+    for (uint64_t i = global_warp_id(); i < a.n; i += total_warps()) {
+        uint64_t T = 0;
+        for (uint32_t b = 0; b < a.nblk; ++b) {
+            const uint32_t s = b * 32 + lane;
+            uint32_t d = 0;
+            if (s < a.m) {
+                const uint32_t v = a.seeds[i * a.m + s];
+                d = __ldg(a.deg + v);
+                a.s.pool_v[i * a.m + s] = v;
+                a.s.bias[i * a.m + s] = d;
+            }
+            const uint64_t tot = warp_sum(static_cast<uint64_t>(d));
+            if (lane == 0) a.s.blk[i * a.nblk + b] = tot;
+            T += tot;
+        }
+        __syncwarp();
+        if (lane == 0) { a.s.T[i] = T; a.s.tstep[i] = 0; }
+        __syncwarp();
+        if (a.L == 0) continue;
+        if (T == 0) {   // no positive-degree vertex in the pool: the walk ends (R20)
+            for (uint64_t k = lane; k < static_cast<uint64_t>(a.L) * 2; k += 32) a.out[i * a.L * 2 + k] = NONE;
+            continue;
+        }
+        const uint32_t slot = mdrw_pick(a, i, 0);
+        if (lane == 0) {
+            a.s.pend_slot[i] = slot;
+            const uint32_t p = a.own(a.s.pool_v[i * a.m + slot]);
+            const uint32_t pos = atomicAdd(a.s.cnt_in + p, 1u);
+            a.s.qin[static_cast<uint64_t>(p) * a.n + pos] = static_cast<uint32_t>(i);
+        }
+    }
+}
+
+// One kernel per active partition p: col slice of p lives at `slot_col`
+// (entries [ebeg, ebeg + |slice|) of the full col_idx).
+__global__ void __launch_bounds__(OOM_WARPS * 32) k_mdrw_oom_part(OomArgs a, uint32_t p,
+                                                                  const uint32_t* __restrict__ slot_col, int64_t ebeg,
+                                                                  const uint32_t* __restrict__ qlist, uint32_t qn) {
+    const int lane = lane_id();
+    for (uint64_t j = global_warp_id(); j < qn; j += total_warps()) {
+        const uint64_t i = qlist[j];
+        const uint32_t inst = a.ibase + static_cast<uint32_t>(i);
+        uint32_t t = a.s.tstep[i];
+        uint32_t slot = a.s.pend_slot[i];
+        uint32_t* pv = a.s.pool_v + i * a.m;
+        uint32_t* bias = a.s.bias + i * a.m;
+        uint64_t* blk = a.s.blk + i * a.nblk;
+        uint32_t* orow = a.out + i * static_cast<uint64_t>(a.L) * 2;
+        for (;;) {
+            // step t at the picked slot; its vertex v is owned by p
+            if (lane == 0) {
+                const uint32_t v = pv[slot];
+                const uint32_t d = bias[slot];
+                const int64_t rb = __ldg(a.rp + v);
+                const uint64_t jj = below(draw_u64(a.key, inst, t, 0u, word3(PURPOSE_EDGE, 0, 0)), d);
+                const uint32_t u = __ldg(slot_col + (rb - ebeg) + jj);
+                const uint32_t du = __ldg(a.deg + u);
+                orow[2 * t] = v;
+                orow[2 * t + 1] = u;
+                pv[slot] = u;
+                bias[slot] = du;
+                blk[slot / 32] = blk[slot / 32] + du - d;
+                a.s.T[i] = a.s.T[i] + du - d;
+            }
+            __syncwarp();
+            ++t;
+            if (t >= static_cast<uint32_t>(a.L)) break;
+            slot = mdrw_pick(a, i, t);
+            const uint32_t q = a.own(pv[slot]);
+            if (q != p) {
+                if (lane == 0) {
+                    a.s.tstep[i] = t;
+                    a.s.pend_slot[i] = slot;
+                    const uint32_t pos = atomicAdd(a.s.cnt_out + q, 1u);
+                    a.s.qout[static_cast<uint64_t>(q) * a.n + pos] = static_cast<uint32_t>(i);
+                }
+                break;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+csaw_status run_mdrw_oom(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds, int64_t n_i,
                          uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st) {
-    (void)g; (void)b; (void)length; (void)d_seeds; (void)n; (void)base; (void)seed; (void)d_path; (void)st;
-    return fail(CSAW_ERR_UNSUPPORTED, "OOM mode: not implemented yet");
+    if (b.kind != CSAW_BIAS_MDRW) return fail(CSAW_ERR_UNSUPPORTED, "OOM mode implements MDRW walks (config 5)");
+    const uint64_t n = static_cast<uint64_t>(n_i);
+    auto& os = const_cast<csaw_graph*>(g)->oomst;
+    const uint32_t m = static_cast<uint32_t>(b.pool_size);
+    const uint32_t nblk = (m + 31) / 32;
+    const uint32_t P = static_cast<uint32_t>(os.P);
+    // device scratch (counted against the budget)
+    const size_t need = n * m * 8 + n * nblk * 8 + n * 16 + 2 * static_cast<size_t>(P) * n * 4 + 2 * P * 4 + 64;
+    const int64_t resident = sizeof(int64_t) * (g->V + 1) + sizeof(uint32_t) * g->V +
+                             static_cast<int64_t>(os.R) * os.slot_edges * 4;
+    if (resident + static_cast<int64_t>(need) > os.budget)
+        return fail(CSAW_ERR_NO_MEMORY, "OOM mode: instance state (" + std::to_string(need) +
+                                            " B) does not fit the device budget next to the resident graph");
+    void* p0;
+    CSAW_TRY(g->scratch.get(SL_TMP0, need, &p0));
+    char* cur = static_cast<char*>(p0);
+    auto take = [&](size_t bytes) { char* r = cur; cur += (bytes + 15) / 16 * 16; return static_cast<void*>(r); };
+    OomArgs a;
+    a.rp = g->row_ptr; a.deg = g->deg; a.seeds = d_seeds; a.n = n; a.m = m; a.nblk = nblk; a.L = length;
+    a.ibase = static_cast<uint32_t>(base);
+    a.key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+    a.out = d_path;
+    a.s.pool_v = static_cast<uint32_t*>(take(n * m * 4));
+    a.s.bias = static_cast<uint32_t*>(take(n * m * 4));
+    a.s.blk = static_cast<uint64_t*>(take(n * nblk * 8));
+    a.s.T = static_cast<uint64_t*>(take(n * 8));
+    a.s.tstep = static_cast<uint32_t*>(take(n * 4));
+    a.s.pend_slot = static_cast<uint32_t*>(take(n * 4));
+    a.s.qin = static_cast<uint32_t*>(take(static_cast<size_t>(P) * n * 4));
+    a.s.qout = static_cast<uint32_t*>(take(static_cast<size_t>(P) * n * 4));
+    a.s.cnt_in = static_cast<uint32_t*>(take(P * 4));
+    a.s.cnt_out = static_cast<uint32_t*>(take(P * 4));
+    a.own.base = static_cast<uint64_t>(g->V) / P;
+    a.own.rem = static_cast<uint64_t>(g->V) % P;
+    a.P = P;
+
+    void* hmb;
+    CSAW_TRY(g->pinned.get(4096, &hmb));
+    uint32_t* hcnt = static_cast<uint32_t*>(hmb);   // [0,P) in, [P,2P) out
+
+    CSAW_CUDA(cudaMemsetAsync(a.s.cnt_in, 0, P * 4, st));
+    CSAW_CUDA(cudaMemsetAsync(a.s.cnt_out, 0, P * 4, st));
+    CSAW_TRY(stats_begin(g, st));
+    const int blocks_total = g->num_sms * 8;
+    if (n > 0) {
+        k_mdrw_oom_init<<<std::max(1, (int)std::min<uint64_t>((n + OOM_WARPS - 1) / OOM_WARPS, blocks_total)),
+                          OOM_WARPS * 32, 0, st>>>(a);
+        note_launch();
+        CSAW_CUDA(cudaGetLastError());
+    }
+    // partition streams wait for the init on the user stream
+    cudaEvent_t evs;
+    CSAW_CUDA(cudaEventCreateWithFlags(&evs, cudaEventDisableTiming));
+    std::vector<cudaEvent_t> tev;   // transfer timing events (pairs)
+    std::vector<uint64_t> in_cnt(P), out_cnt(P);
+    uint64_t loads = 0, h2d = 0;
+    std::vector<int32_t>& res = os.resident;     // partition per slot
+    for (;;) {
+        CSAW_CUDA(cudaMemcpyAsync(hcnt, a.s.cnt_in, P * 4, cudaMemcpyDeviceToHost, st));
+        CSAW_CUDA(cudaStreamSynchronize(st));
+        uint64_t active_total = 0;
+        for (uint32_t p = 0; p < P; ++p) { in_cnt[p] = hcnt[p]; active_total += in_cnt[p]; }
+        if (active_total == 0) break;
+        // ---- workload-aware choice of the partitions to sample this wave
+        std::vector<int32_t> order(P);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return in_cnt[x] > in_cnt[y]; });
+        std::vector<int32_t> chosen;   // partitions sampled this wave
+        std::vector<int32_t> slot_of(P, -1);
+        for (int s = 0; s < os.R; ++s)
+            if (res[s] >= 0) slot_of[res[s]] = s;
+        for (int s = 0; s < os.R; ++s)      // residents with work stay (released only when empty)
+            if (res[s] >= 0 && in_cnt[res[s]] > 0) chosen.push_back(res[s]);
+        for (int32_t p : order) {
+            if (static_cast<int>(chosen.size()) >= os.R || in_cnt[p] == 0) break;
+            if (slot_of[p] >= 0) continue;   // already chosen as resident with work
+            // a free slot, or one whose resident has an empty queue
+            int victim = -1;
+            for (int s = 0; s < os.R; ++s)
+                if (res[s] < 0 || in_cnt[res[s]] == 0) {
+                    if (std::find(chosen.begin(), chosen.end(), res[s]) != chosen.end() && res[s] >= 0) continue;
+                    victim = s;
+                    break;
+                }
+            if (victim < 0) break;
+            if (res[victim] >= 0) slot_of[res[victim]] = -1;
+            res[victim] = p;
+            slot_of[p] = victim;
+            chosen.push_back(p);
+            // ---- transfer the partition's col slice (pinned host -> arena slot)
+            const int sidx = victim % os.S;
+            cudaEvent_t t0, t1;
+            CSAW_CUDA(cudaEventCreate(&t0));
+            CSAW_CUDA(cudaEventCreate(&t1));
+            CSAW_CUDA(cudaEventRecord(evs, st));
+            CSAW_CUDA(cudaStreamWaitEvent(os.streams[sidx], evs, 0));
+            CSAW_CUDA(cudaEventRecord(t0, os.streams[sidx]));
+            const int64_t ne = os.ebeg[p + 1] - os.ebeg[p];
+            CSAW_CUDA(cudaMemcpyAsync(os.d_slots + static_cast<int64_t>(victim) * os.slot_edges, os.h_col + os.ebeg[p],
+                                      sizeof(uint32_t) * ne, cudaMemcpyHostToDevice, os.streams[sidx]));
+            CSAW_CUDA(cudaEventRecord(t1, os.streams[sidx]));
+            tev.push_back(t0);
+            tev.push_back(t1);
+            ++loads;
+            h2d += sizeof(uint32_t) * ne;
+        }
+        // ---- one kernel per active partition, CTAs proportional to its active count
+        uint64_t chosen_total = 0;
+        for (int32_t p : chosen) chosen_total += in_cnt[p];
+        CSAW_CUDA(cudaEventRecord(evs, st));
+        for (int32_t p : chosen) {
+            const int s = slot_of[p];
+            const int sidx = s % os.S;
+            CSAW_CUDA(cudaStreamWaitEvent(os.streams[sidx], evs, 0));
+            int blocks = static_cast<int>(std::max<uint64_t>(1, blocks_total * in_cnt[p] / std::max<uint64_t>(chosen_total, 1)));
+            blocks = std::min<int>(blocks, static_cast<int>((in_cnt[p] + OOM_WARPS - 1) / OOM_WARPS));
+            k_mdrw_oom_part<<<std::max(1, blocks), OOM_WARPS * 32, 0, os.streams[sidx]>>>(
+                a, static_cast<uint32_t>(p), os.d_slots + static_cast<int64_t>(s) * os.slot_edges, os.ebeg[p],
+                a.s.qin + static_cast<uint64_t>(p) * n, static_cast<uint32_t>(in_cnt[p]));
+            note_launch();
+            CSAW_CUDA(cudaGetLastError());
+        }
+        for (int s = 0; s < os.S; ++s) {
+            CSAW_CUDA(cudaEventRecord(evs, os.streams[s]));
+            CSAW_CUDA(cudaStreamWaitEvent(st, evs, 0));
+        }
+        // ---- merge queues: sampled partitions take their out-queue; others append it
+        CSAW_CUDA(cudaMemcpyAsync(hcnt + P, a.s.cnt_out, P * 4, cudaMemcpyDeviceToHost, st));
+        CSAW_CUDA(cudaStreamSynchronize(st));
+        for (uint32_t p = 0; p < P; ++p) {
+            out_cnt[p] = hcnt[P + p];
+            const bool was = std::find(chosen.begin(), chosen.end(), static_cast<int32_t>(p)) != chosen.end();
+            const uint64_t keep = was ? 0 : in_cnt[p];
+            if (out_cnt[p])
+                CSAW_CUDA(cudaMemcpyAsync(a.s.qin + static_cast<uint64_t>(p) * n + keep, a.s.qout + static_cast<uint64_t>(p) * n,
+                                          sizeof(uint32_t) * out_cnt[p], cudaMemcpyDeviceToDevice, st));
+            hcnt[p] = static_cast<uint32_t>(keep + out_cnt[p]);
+        }
+        CSAW_CUDA(cudaMemcpyAsync(a.s.cnt_in, hcnt, P * 4, cudaMemcpyHostToDevice, st));
+        CSAW_CUDA(cudaMemsetAsync(a.s.cnt_out, 0, P * 4, st));
+    }
+    CSAW_TRY(stats_end(g, st));
+    CSAW_CUDA(cudaStreamSynchronize(st));
+    double tms = 0;
+    for (size_t k = 0; k + 1 < tev.size(); k += 2) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, tev[k], tev[k + 1]);
+        tms += ms;
+        cudaEventDestroy(tev[k]);
+        cudaEventDestroy(tev[k + 1]);
+    }
+    cudaEventDestroy(evs);
+    g->stats.partition_loads = loads;
+    g->stats.h2d_bytes = h2d;
+    g->stats.transfer_ms = tms;
+    g->stats.sampled_edges = n * static_cast<uint64_t>(length);
+    g->stats.pools = n * static_cast<uint64_t>(length);
+    return CSAW_OK;
 }
 
 }  // namespace csaw
