@@ -51,6 +51,8 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle CPU-baseline budget (wall s)")
     ap.add_argument("--gather", action="store_true", help="NCCL-gather outputs after timing (reported apart)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--in-memory", action="store_true", help="cfg5: ignore the OOM budget (in-memory MDRW)")
+    ap.add_argument("--no-cache", action="store_true", help="disable the static-bias CTPS cache (scan every pool)")
     return ap.parse_args()
 
 
@@ -94,6 +96,12 @@ def algorithmic_bytes(cfg, st, n, edges):
     uniform: 16 + 4 per step; node2vec: 16 + 4 d(v) + 4 d(prev); MDRW: 32 per step;
     sampling select kernel: 16 per pool + 8 per scanned candidate + 12 per staged edge."""
     scanned, pools = st["neighbours_scanned"], st["pools"]
+    probes = st.get("cache_probes", 0)
+    if probes and cfg.workload == "walk":
+        # cached CTPS: row_ptr pair 16 + T 8 + col 4 per step, 8 per cache probe, + path
+        return 28 * pools + 8 * probes + 4 * n * (cfg.length + 1) + 4 * n
+    if probes:
+        return 24 * pools + 8 * probes + 12 * edges
     if cfg.workload == "walk":
         out = 4 * n * (cfg.length + 1) + 4 * n
         if cfg.bias == "degree":
@@ -208,14 +216,17 @@ def oracle_timed_sample(cfg, og, seeds_np, base, rng_seed, budget_s, workers=Non
     per_worker = max(1, int(budget_s / t1))
     m = int(min(n, per_worker * workers))
     m = max(m, min(n, workers))
+    # tiny workloads (e.g. cfg1): repeat whole passes so the sample is ~budget_s of CPU work
+    passes = max(1, min(1000, int(budget_s * workers / max(t1 * n, 1e-9)))) if m == n else 1
     chunks = np.array_split(np.arange(m), workers * 2)
     jobs = [(cfg.name, int(c[0]), int(c[-1]) + 1, base, seeds_np[int(c[0]):int(c[-1]) + 1], rng_seed)
-            for c in chunks if c.size]
+            for c in chunks if c.size] * passes
     t0 = time.perf_counter()
     with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("fork")) as ex:
         edges = sum(ex.map(_oracle_job, jobs))
     wall = time.perf_counter() - t0
-    sample = f"{m} of {n} instances of {cfg.name} (full length/depth each), {workers} processes"
+    sample = (f"{m} of {n} instances of {cfg.name} (full length/depth each)"
+              + (f" x {passes} passes" if passes > 1 else "") + f", {workers} processes")
     return edges / wall, workers, sample, edges, wall
 
 
@@ -273,6 +284,9 @@ def config_block(cfg, world, stats_g):
         c["pf"] = cfg.pf
     if cfg.workload == "mdrw":
         c["pool_size"] = cfg.pool_size
+    if cfg.oom_budget_bytes:
+        c["oom"] = {"device_budget_bytes": cfg.oom_budget_bytes, "partitions": cfg.oom_partitions,
+                    "resident": cfg.oom_resident, "streams": cfg.oom_resident}
     if stats_g:
         c["graph_stats"] = stats_g
     return c
@@ -303,7 +317,20 @@ def main():
     base, seeds = make_seeds(cfg, g, rank, world)
     seeds = seeds.to(dev).contiguous()
     n = seeds.shape[0]
-    G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local)
+    oom = cfg.oom_budget_bytes > 0 and not args.in_memory
+    if oom:
+        # out-of-memory mode (§5): the device holds only what the imposed budget
+        # allows -- move the generated graph to host memory first
+        g = g.to("cpu")
+        torch.cuda.empty_cache()
+        G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, budget_bytes=cfg.oom_budget_bytes,
+                                 num_partitions=cfg.oom_partitions, max_resident=cfg.oom_resident,
+                                 num_streams=cfg.oom_resident)
+    else:
+        # static-bias CTPS cache (§8(f) NEXT-1, bit-identical) for degree-biased selections
+        use_cache = (not args.no_cache) and cfg.bias in ("degree", "layer")
+        G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache)
+    ginfo = G.info()
     bias = bias_of(cs, cfg)
     stream = torch.cuda.current_stream(dev)
 
@@ -411,7 +438,7 @@ def main():
     traffic = load_traffic(cfg.name)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": hot_kernel_name(cfg), "alg_bytes_per_launch": bytes_per_launch,
+            "kernel": hot_kernel_name(cfg, bool(ginfo.get("ctps_cache")), bool(ginfo.get("oom_mode"))), "alg_bytes_per_launch": bytes_per_launch,
             "hot_ms_per_launch": hot_avg_ms, "hot_share_of_step": (hot_ms / total_ms) if total_ms else None,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
 
@@ -438,6 +465,12 @@ def main():
                 "gpu_launches": launches, "clocks": clk,
                 "detail": {"edges_per_step_per_gpu": edges / max(args.steps, 1), "step_ms": step_ms,
                            "graph_gen_s": gen_s, "gather_ms": gather_ms,
+                           "ctps_cache": bool(ginfo.get("ctps_cache")), "cache_build_ms": ginfo.get("cache_build_ms"),
+                           "oom": bool(ginfo.get("oom_mode")),
+                           "partition_loads_per_step": st_last["partition_loads"] if st_last else None,
+                           "h2d_bytes_per_step": st_last["h2d_bytes"] if st_last else None,
+                           "transfer_ms_per_step": st_last["transfer_ms"] if st_last else None,
+                           "cache_probes_per_step": st_last["cache_probes"] if st_last else None,
                            "neighbours_scanned_per_step": st_last["neighbours_scanned"] if st_last else None,
                            "pools_per_step": st_last["pools"] if st_last else None}}
         print(json.dumps(line), flush=True)
@@ -501,10 +534,16 @@ def run_e2e(cs, G, bias, seeds, cfg, base, args, kind, n, dev, world):
             "steps": steps, "timing": "host wall clock around the synchronous C-ABI call (max over ranks)"}
 
 
-def hot_kernel_name(cfg):
-    return {"walk": "k_walk<degree>" if cfg.bias == "degree" else "k_walk<uniform>", "node2vec": "k_node2vec<int>",
-            "mdrw": "k_mdrw", "neighbor": "k_ns_select<degree>", "layer": "k_layer_select",
-            "forest_fire": "k_ns_select<uniform>"}[cfg.workload]
+def hot_kernel_name(cfg, cached=False, oom=False):
+    if cfg.workload == "walk":
+        return "k_walk_cached" if (cfg.bias == "degree" and cached) else f"k_walk<{cfg.bias}>"
+    if cfg.workload == "mdrw":
+        return "k_mdrw_oom_part" if oom else "k_mdrw"
+    if cfg.workload == "neighbor":
+        return "k_ns_select<2: cached degree>" if cached else f"k_ns_select<{cfg.bias}>"
+    if cfg.workload == "layer":
+        return "k_layer_select<cached>" if cached else "k_layer_select<scan>"
+    return {"node2vec": "k_node2vec<int>", "forest_fire": "k_ns_select<0: uniform>"}[cfg.workload]
 
 
 def load_peaks() -> dict:

@@ -93,8 +93,17 @@ typedef struct {
     int32_t num_partitions;         /* OOM: equal contiguous vertex ranges; 0 = default 4 */
     int32_t max_resident;           /* OOM: partitions resident at once; 0 = default 2 */
     int32_t num_streams;            /* OOM: streams (one kernel per active partition); 0 = default 2 */
-    uint32_t flags;                 /* reserved, 0 */
+    uint32_t flags;                 /* CSAW_GRAPH_* bits */
 } csaw_graph_opts;
+
+/* csaw_graph_opts.flags: build the static-bias CTPS cache at creation (in-memory
+ * graphs).  cps[e] = sum of deg(col[e']) over e' in [row_ptr[v], e], u64 per CSR
+ * entry, plus the per-row count of positive-bias neighbours.  This is the
+ * paper's "caching transition probability" (in \begin{comment}; reading
+ * R25): degree-biased selections then search the cached prefix (O(log d) reads)
+ * instead of re-scanning the neighbour list.  Results are bit-identical (same
+ * integer S, same draws). */
+#define CSAW_GRAPH_CTPS_CACHE 0x1u
 
 typedef struct {
     int64_t num_vertices, num_edges;
@@ -103,6 +112,9 @@ typedef struct {
     int32_t rows_sorted;            /* 1 if every row is strictly ascending */
     int32_t oom_mode;               /* 1 if created with a device budget */
     int64_t device_bytes;           /* device memory held by the graph (CSR + degree + scratch) */
+    int32_t ctps_cache;             /* 1 if the static-bias CTPS cache was built */
+    int32_t reserved;
+    double cache_build_ms;          /* device time of the cache build */
 } csaw_graph_info_t;
 
 typedef struct csaw_graph csaw_graph;  /* opaque */
@@ -114,6 +126,7 @@ typedef struct {
     uint64_t neighbours_scanned;    /* candidates whose bias was evaluated (pass 1 of the CTPS build) */
     uint64_t partition_loads;       /* OOM: partition transfers (Fig. 15) */
     uint64_t h2d_bytes;             /* OOM: bytes copied host -> device for partitions */
+    uint64_t cache_probes;          /* CTPS-cache entries read by the searches (CSAW_GRAPH_CTPS_CACHE) */
     uint64_t kernel_launches;       /* kernels this library launched for the call */
     uint64_t hot_launches;          /* launches of the selection ("hot") kernel */
     double kernel_ms;               /* device time, first launch -> last completion (CUDA events) */

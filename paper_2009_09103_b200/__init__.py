@@ -73,12 +73,17 @@ class Graph:
         return csaw_graph_info(self)
 
 
+CSAW_GRAPH_CTPS_CACHE = 0x1
+
+
 def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, num_partitions: int = 0,
-                      max_resident: int = 0, num_streams: int = 0) -> Graph:
-    """row_ptr int64[V+1], col_idx int32/uint32[E] (torch tensors, host or device)."""
+                      max_resident: int = 0, num_streams: int = 0, ctps_cache: bool = False) -> Graph:
+    """row_ptr int64[V+1], col_idx int32/uint32[E] (torch tensors, host or device).
+    ctps_cache=True builds the static-bias CTPS cache (CSAW_GRAPH_CTPS_CACHE)."""
     V = row_ptr.numel() - 1
     csr = csaw_csr(V, col_idx.numel(), _ptr(row_ptr), _ptr(col_idx), None)
-    opt = csaw_graph_opts(device, budget_bytes, num_partitions, max_resident, num_streams, 0)
+    opt = csaw_graph_opts(device, budget_bytes, num_partitions, max_resident, num_streams,
+                          CSAW_GRAPH_CTPS_CACHE if ctps_cache else 0)
     out = C.c_void_p()
     check(lib().csaw_graph_create(C.byref(csr), C.byref(opt), C.byref(out)))
     return Graph(out.value, device)

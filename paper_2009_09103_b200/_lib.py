@@ -70,12 +70,13 @@ class csaw_graph_opts(C.Structure):
 class csaw_graph_info_t(C.Structure):
     _fields_ = [("num_vertices", C.c_int64), ("num_edges", C.c_int64), ("max_degree", C.c_int64),
                 ("nonisolated", C.c_int64), ("rows_sorted", C.c_int32), ("oom_mode", C.c_int32),
-                ("device_bytes", C.c_int64)]
+                ("device_bytes", C.c_int64), ("ctps_cache", C.c_int32), ("reserved", C.c_int32),
+                ("cache_build_ms", C.c_double)]
 
 
 class csaw_run_stats(C.Structure):
     _fields_ = [("sampled_edges", C.c_uint64), ("pools", C.c_uint64), ("neighbours_scanned", C.c_uint64),
-                ("partition_loads", C.c_uint64), ("h2d_bytes", C.c_uint64), ("kernel_launches", C.c_uint64),
+                ("partition_loads", C.c_uint64), ("h2d_bytes", C.c_uint64), ("cache_probes", C.c_uint64), ("kernel_launches", C.c_uint64),
                 ("hot_launches", C.c_uint64), ("kernel_ms", C.c_double), ("hot_kernel_ms", C.c_double),
                 ("transfer_ms", C.c_double)]
 

@@ -181,6 +181,28 @@ __global__ void k_validate_sorted(const int64_t* __restrict__ rp, const uint32_t
     }
 }
 
+// Static-bias CTPS cache ("caching transition probability", R25): warp per
+// row, the same Kogge-Stone u64 scan the select kernels run per step.
+__global__ void k_build_cps(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                            const uint32_t* __restrict__ deg, int64_t V, uint64_t* __restrict__ cps,
+                            uint32_t* __restrict__ npos) {
+    const int lane = lane_id();
+    for (uint64_t v = global_warp_id(); v < static_cast<uint64_t>(V); v += total_warps()) {
+        const int64_t a = rp[v], b = rp[v + 1];
+        uint64_t carry = 0;
+        uint32_t pos = 0;
+        for (int64_t e0 = a; e0 < b; e0 += 32) {
+            const int64_t e = e0 + lane;
+            const uint32_t bias = e < b ? __ldg(deg + __ldg(col + e)) : 0u;
+            const uint64_t incl = warp_incl_scan(static_cast<uint64_t>(bias)) + carry;
+            if (e < b) cps[e] = incl;
+            carry = __shfl_sync(FULL, incl, 31);
+            pos += __popc(__ballot_sync(FULL, bias > 0));
+        }
+        if (lane == 0) npos[v] = pos;
+    }
+}
+
 }  // namespace csaw
 
 using namespace csaw;
@@ -310,6 +332,22 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
     if (hv.bad_col != ~0ull)
         return cleanup(fail(CSAW_ERR_BAD_GRAPH, "col_idx[" + std::to_string(hv.bad_col - 1) + "] >= num_vertices"));
     g->rows_sorted = hv.unsorted == 0;
+    if ((o.flags & CSAW_GRAPH_CTPS_CACHE) && !g->oom) {
+        CREATE_CUDA(cudaMalloc(&g->cps, sizeof(uint64_t) * std::max<int64_t>(E, 1)), "cudaMalloc(cps)");
+        CREATE_CUDA(cudaMalloc(&g->npos, sizeof(uint32_t) * std::max<int64_t>(V, 1)), "cudaMalloc(npos)");
+        cudaEvent_t c0, c1;
+        CREATE_CUDA(cudaEventCreate(&c0), "event");
+        CREATE_CUDA(cudaEventCreate(&c1), "event");
+        cudaEventRecord(c0);
+        if (V > 0) k_build_cps<<<blocks, 256>>>(g->row_ptr, g->col, g->deg, V, g->cps, g->npos);
+        cudaEventRecord(c1);
+        CREATE_CUDA(cudaEventSynchronize(c1), "build cps");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c0, c1);
+        g->cache_build_ms = ms;
+        cudaEventDestroy(c0);
+        cudaEventDestroy(c1);
+    }
     CREATE_CUDA(cudaEventCreate(&g->ev0), "event");
     CREATE_CUDA(cudaEventCreate(&g->ev1), "event");
     CREATE_CUDA(cudaDeviceSynchronize(), "graph_create");
@@ -325,6 +363,8 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->row_ptr) cudaFree(g->row_ptr);
     if (g->col) cudaFree(g->col);
     if (g->deg) cudaFree(g->deg);
+    if (g->cps) cudaFree(g->cps);
+    if (g->npos) cudaFree(g->npos);
     auto& st = g->oomst;
     if (st.h_col) cudaFreeHost(st.h_col);
     if (st.h_row) cudaFreeHost(st.h_row);
@@ -348,7 +388,11 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
     out->oom_mode = g->oom ? 1 : 0;
     out->device_bytes = sizeof(int64_t) * (g->V + 1) + sizeof(uint32_t) * g->V +
                         (g->col ? sizeof(uint32_t) * g->E : 0) + static_cast<int64_t>(g->scratch.bytes_held()) +
-                        (g->oom ? static_cast<int64_t>(g->oomst.R) * g->oomst.slot_edges * 4 : 0);
+                        (g->oom ? static_cast<int64_t>(g->oomst.R) * g->oomst.slot_edges * 4 : 0) +
+                        (g->cps ? static_cast<int64_t>(sizeof(uint64_t) * g->E + sizeof(uint32_t) * g->V) : 0);
+    out->ctps_cache = g->cps ? 1 : 0;
+    out->reserved = 0;
+    out->cache_build_ms = g->cache_build_ms;
     return CSAW_OK;
 }
 
@@ -368,10 +412,11 @@ CSAW_API csaw_status csaw_stats(const csaw_graph* g, csaw_run_stats* out) {
     }
     g->stats.hot_kernel_ms = hot;
     if (g->pending_counters) {
-        unsigned long long c[2] = {0, 0};
+        unsigned long long c[3] = {0, 0, 0};
         CSAW_CUDA(cudaMemcpy(c, g->pending_counters, sizeof(c), cudaMemcpyDeviceToHost));
         g->stats.neighbours_scanned = c[0];
         g->stats.pools = c[1];
+        g->stats.cache_probes = c[2];
         g->pending_counters = nullptr;
     }
     *out = g->stats;

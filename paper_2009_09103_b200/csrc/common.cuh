@@ -116,6 +116,38 @@ __device__ __forceinline__ uint64_t warp_lower_bound(const uint32_t* __restrict_
     return b ? lo + (__ffs(b) - 1) : hi;
 }
 
+// First index in a[lo, hi) with a[idx] > x (hi if none), for a sorted non-decreasing u64
+// array.  Warp-collective 32-ary search: ceil(log32(hi - lo)) rounds of 32 parallel
+// probes (one round trip each) instead of log2 dependent loads.  *probes counts loads.
+__device__ __forceinline__ uint64_t warp_upper_bound_u64(const uint64_t* __restrict__ a, uint64_t lo, uint64_t hi,
+                                                         uint64_t x, uint32_t* probes) {
+    const int lane = lane_id();
+    while (hi - lo > 32) {
+        const uint64_t step = (hi - lo + 31) / 32;
+        const uint64_t p = lo + static_cast<uint64_t>(lane) * step;
+        const bool inr = p < hi;
+        const bool ok = inr && __ldg(a + p) > x;
+        const unsigned b = __ballot_sync(FULL, ok);
+        const unsigned inb = __ballot_sync(FULL, inr);
+        *probes += __popc(inb);
+        if (b == 0) {
+            const int last = 31 - __clz(inb);
+            lo = lo + static_cast<uint64_t>(last) * step + 1;
+        } else {
+            const int f = __ffs(b) - 1;
+            if (f == 0) return lo;
+            const uint64_t pf = lo + static_cast<uint64_t>(f) * step;
+            lo = lo + static_cast<uint64_t>(f - 1) * step + 1;
+            hi = pf;
+        }
+    }
+    const uint64_t p = lo + lane;
+    const bool ok = p < hi && __ldg(a + p) > x;
+    *probes += static_cast<uint32_t>(min(static_cast<uint64_t>(32), hi - lo));
+    const unsigned b = __ballot_sync(FULL, ok);
+    return b ? lo + (__ffs(b) - 1) : hi;
+}
+
 // Grid helpers
 __device__ __forceinline__ uint64_t global_warp_id() {
     return (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;

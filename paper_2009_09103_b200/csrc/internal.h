@@ -93,6 +93,9 @@ struct csaw_graph {
     int64_t max_deg = 0;
     int64_t nonisolated = 0;
     int32_t rows_sorted = 0;
+    uint64_t* cps = nullptr;      // static-bias CTPS cache [E] (CSAW_GRAPH_CTPS_CACHE), inclusive per row
+    uint32_t* npos = nullptr;     // [V] positive-bias neighbours per row (cache builds only)
+    double cache_build_ms = 0.0;
     int num_sms = 148;
     bool oom = false;
     csaw::OomState oomst;

@@ -31,6 +31,18 @@
 namespace csaw {
 
 constexpr int OOM_WARPS = 8;
+constexpr int OOM_MAXP = 64;   // partitions supported by the scheduler
+
+// Partitions whose col slice is resident and complete when a kernel starts.
+struct ReadyMap {
+    int32_t slot[OOM_MAXP];     // arena slot, or -1
+    int64_t ebeg[OOM_MAXP];     // first CSR entry of the partition
+    const uint32_t* slots;      // arena base
+    int64_t slot_edges;
+    __device__ __forceinline__ const uint32_t* col_of(uint32_t q) const {   // col[] view for partition q
+        return slot[q] < 0 ? nullptr : slots + static_cast<int64_t>(slot[q]) * slot_edges - ebeg[q];
+    }
+};
 
 struct Owner {   // equal contiguous ranges, remainder to the lowest partitions (R23)
     uint64_t base;   // V / P
@@ -135,10 +147,10 @@ __global__ void __launch_bounds__(OOM_WARPS * 32) k_mdrw_oom_init(OomArgs a) {
     }
 }
 
-// One kernel per active partition p: col slice of p lives at `slot_col`
-// (entries [ebeg, ebeg + |slice|) of the full col_idx).
-__global__ void __launch_bounds__(OOM_WARPS * 32) k_mdrw_oom_part(OomArgs a, uint32_t p,
-                                                                  const uint32_t* __restrict__ slot_col, int64_t ebeg,
+// One kernel per active partition p (its queue); an instance keeps stepping while
+// its next pick lies in a partition that is resident and ready (rm), then joins the
+// queue of the partition it needs.
+__global__ void __launch_bounds__(OOM_WARPS * 32) k_mdrw_oom_part(OomArgs a, uint32_t p, ReadyMap rm,
                                                                   const uint32_t* __restrict__ qlist, uint32_t qn) {
     const int lane = lane_id();
     for (uint64_t j = global_warp_id(); j < qn; j += total_warps()) {
@@ -150,6 +162,7 @@ __global__ void __launch_bounds__(OOM_WARPS * 32) k_mdrw_oom_part(OomArgs a, uin
         uint32_t* bias = a.s.bias + i * a.m;
         uint64_t* blk = a.s.blk + i * a.nblk;
         uint32_t* orow = a.out + i * static_cast<uint64_t>(a.L) * 2;
+        const uint32_t* colq = rm.col_of(p);
         for (;;) {
             // step t at the picked slot; its vertex v is owned by p
             if (lane == 0) {
@@ -157,7 +170,7 @@ __global__ void __launch_bounds__(OOM_WARPS * 32) k_mdrw_oom_part(OomArgs a, uin
                 const uint32_t d = bias[slot];
                 const int64_t rb = __ldg(a.rp + v);
                 const uint64_t jj = below(draw_u64(a.key, inst, t, 0u, word3(PURPOSE_EDGE, 0, 0)), d);
-                const uint32_t u = __ldg(slot_col + (rb - ebeg) + jj);
+                const uint32_t u = __ldg(colq + rb + jj);
                 const uint32_t du = __ldg(a.deg + u);
                 orow[2 * t] = v;
                 orow[2 * t + 1] = u;
@@ -171,7 +184,8 @@ __global__ void __launch_bounds__(OOM_WARPS * 32) k_mdrw_oom_part(OomArgs a, uin
             if (t >= static_cast<uint32_t>(a.L)) break;
             slot = mdrw_pick(a, i, t);
             const uint32_t q = a.own(pv[slot]);
-            if (q != p) {
+            colq = rm.col_of(q);
+            if (colq == nullptr) {
                 if (lane == 0) {
                     a.s.tstep[i] = t;
                     a.s.pend_slot[i] = slot;
@@ -194,7 +208,8 @@ csaw_status run_mdrw_oom(const csaw_graph* g, const csaw_bias& b, int32_t length
     const uint32_t nblk = (m + 31) / 32;
     const uint32_t P = static_cast<uint32_t>(os.P);
     // device scratch (counted against the budget)
-    const size_t need = n * m * 8 + n * nblk * 8 + n * 16 + 2 * static_cast<size_t>(P) * n * 4 + 2 * P * 4 + 64;
+    if (P > static_cast<uint32_t>(OOM_MAXP)) return fail(CSAW_ERR_UNSUPPORTED, "OOM mode supports at most 64 partitions");
+    const size_t need = n * m * 8 + n * nblk * 8 + n * 16 + 2 * static_cast<size_t>(P) * n * 4 + 2 * P * 4 + 16 * 16;
     const int64_t resident = sizeof(int64_t) * (g->V + 1) + sizeof(uint32_t) * g->V +
                              static_cast<int64_t>(os.R) * os.slot_edges * 4;
     if (resident + static_cast<int64_t>(need) > os.budget)
@@ -255,6 +270,7 @@ csaw_status run_mdrw_oom(const csaw_graph* g, const csaw_bias& b, int32_t length
         std::iota(order.begin(), order.end(), 0);
         std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return in_cnt[x] > in_cnt[y]; });
         std::vector<int32_t> chosen;   // partitions sampled this wave
+        std::vector<int32_t> fresh;    // partitions transferred this wave
         std::vector<int32_t> slot_of(P, -1);
         for (int s = 0; s < os.R; ++s)
             if (res[s] >= 0) slot_of[res[s]] = s;
@@ -276,6 +292,7 @@ csaw_status run_mdrw_oom(const csaw_graph* g, const csaw_bias& b, int32_t length
             res[victim] = p;
             slot_of[p] = victim;
             chosen.push_back(p);
+            fresh.push_back(p);
             // ---- transfer the partition's col slice (pinned host -> arena slot)
             const int sidx = victim % os.S;
             cudaEvent_t t0, t1;
@@ -294,6 +311,13 @@ csaw_status run_mdrw_oom(const csaw_graph* g, const csaw_bias& b, int32_t length
             h2d += sizeof(uint32_t) * ne;
         }
         // ---- one kernel per active partition, CTAs proportional to its active count
+        ReadyMap rm;
+        rm.slots = os.d_slots;
+        rm.slot_edges = os.slot_edges;
+        for (int q = 0; q < OOM_MAXP; ++q) { rm.slot[q] = -1; rm.ebeg[q] = 0; }
+        for (uint32_t q = 0; q < P; ++q) rm.ebeg[q] = os.ebeg[q];
+        for (int s = 0; s < os.R; ++s)
+            if (res[s] >= 0 && std::find(fresh.begin(), fresh.end(), res[s]) == fresh.end()) rm.slot[res[s]] = s;
         uint64_t chosen_total = 0;
         for (int32_t p : chosen) chosen_total += in_cnt[p];
         CSAW_CUDA(cudaEventRecord(evs, st));
@@ -303,11 +327,14 @@ csaw_status run_mdrw_oom(const csaw_graph* g, const csaw_bias& b, int32_t length
             CSAW_CUDA(cudaStreamWaitEvent(os.streams[sidx], evs, 0));
             int blocks = static_cast<int>(std::max<uint64_t>(1, blocks_total * in_cnt[p] / std::max<uint64_t>(chosen_total, 1)));
             blocks = std::min<int>(blocks, static_cast<int>((in_cnt[p] + OOM_WARPS - 1) / OOM_WARPS));
+            ReadyMap rmp = rm;
+            rmp.slot[p] = s;
+            CSAW_TRY(hot_begin(g, os.streams[sidx]));
             k_mdrw_oom_part<<<std::max(1, blocks), OOM_WARPS * 32, 0, os.streams[sidx]>>>(
-                a, static_cast<uint32_t>(p), os.d_slots + static_cast<int64_t>(s) * os.slot_edges, os.ebeg[p],
-                a.s.qin + static_cast<uint64_t>(p) * n, static_cast<uint32_t>(in_cnt[p]));
+                a, static_cast<uint32_t>(p), rmp, a.s.qin + static_cast<uint64_t>(p) * n, static_cast<uint32_t>(in_cnt[p]));
             note_launch();
             CSAW_CUDA(cudaGetLastError());
+            CSAW_TRY(hot_end(g, os.streams[sidx]));
         }
         for (int s = 0; s < os.S; ++s) {
             CSAW_CUDA(cudaEventRecord(evs, os.streams[s]));

@@ -122,11 +122,14 @@ struct SelArgs {
     uint32_t a_max;
     PickRec* glist;
     uint32_t kmax;
-    unsigned long long* counters;   // [0] scanned, [1] pools
+    unsigned long long* counters;   // [0] scanned, [1] pools, [2] cache probes
+    const uint64_t* __restrict__ cps;    // static-bias CTPS cache (nullptr if not built)
+    const uint32_t* __restrict__ npos;
 };
 
 // Neighbor sampling / forest fire: one warp per queue entry.
-template <bool kDegree>
+// kMode: 0 = uniform (closed form), 1 = degree (scanned CTPS), 2 = degree (cached CTPS)
+template <int kMode>
 __global__ void __launch_bounds__(SEL_WARPS * 32) k_ns_select(SelArgs a) {
     __shared__ uint64_t tab_all[SEL_WARPS][TAB];
     __shared__ uint32_t bm_all[SEL_WARPS][BM_WORDS];
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) k_ns_select(SelArgs a) {
     uint32_t* bm = bm_all[wib];
     const int lane = lane_id();
     PickRec* gl = a.glist ? a.glist + global_warp_id() * a.kmax : nullptr;
-    unsigned long long scanned = 0, pools = 0;
+    unsigned long long scanned = 0, pools = 0, probes = 0;
     for (uint64_t q = global_warp_id(); q < a.nq; q += total_warps()) {
         const uint32_t v = a.qv[q];
         const uint32_t inst = a.qi[q];
@@ -148,7 +151,12 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) k_ns_select(SelArgs a) {
         StageEmit<int> emit{a.s_inst, a.s_src, a.s_dst, e0, inst, v};
         uint32_t cnt = 0;
         if (n > 0 && k > 0) {
-            if constexpr (kDegree) {
+            if constexpr (kMode == 2) {
+                CachedDegreePool P{a.col, a.cps, static_cast<uint64_t>(b0), n, __ldg(a.npos + v), 0};
+                const Ctps C = build_ctps(P, tab);
+                cnt = select_wor(P, C, tab, bm, k, dk, a.a_max, gl, emit);
+                probes += P.probes;
+            } else if constexpr (kMode == 1) {
                 DegreePool P{a.col, a.deg, static_cast<uint64_t>(b0), n};
                 const Ctps C = build_ctps(P, tab);
                 cnt = select_wor(P, C, tab, bm, k, dk, a.a_max, gl, emit);
@@ -169,6 +177,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) k_ns_select(SelArgs a) {
     if (lane == 0) {
         if (scanned) atomicAdd(a.counters + 0, scanned);
         if (pools) atomicAdd(a.counters + 1, pools);
+        if (probes) atomicAdd(a.counters + 2, probes);
     }
 }
 
@@ -176,16 +185,21 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) k_ns_select(SelArgs a) {
 // Pool = multiset union of N(v) over the instance's sorted frontier, in that
 // order (reading R14); EDGEBIAS = deg(u).  seg_pref[j] = sum of frontier
 // degrees before segment j (relative to the instance).
-struct LayerPool {
+template <bool kCache>
+struct LayerPoolT {
     static constexpr bool kClosedForm = false;
+    static constexpr bool kCached = kCache;
     const int64_t* __restrict__ rp;
     const uint32_t* __restrict__ col;
     const uint32_t* __restrict__ deg;
+    const uint64_t* __restrict__ cps;    // static-bias CTPS cache (kCache)
+    const uint32_t* __restrict__ npos;   // positive-bias neighbours per row (kCache)
     const uint32_t* __restrict__ fv;     // frontier vertices of the instance
     const uint64_t* __restrict__ pref;   // global exclusive prefix of frontier degrees
     uint64_t pbase;                      // pref at the instance's first segment
     uint32_t nf;                         // frontier size
     uint32_t n;                          // pool size
+    uint32_t probes;
     // per-lane cursor
     uint32_t seg;
     uint64_t seg_lo, seg_hi;             // pool range of segment seg
@@ -212,18 +226,33 @@ struct LayerPool {
     template <int NR>
     __device__ __forceinline__ void load_rows(uint32_t row0, uint32_t (&key)[NR], uint32_t (&b)[NR]) {
         const int lane = lane_id();
+        int64_t eidx[NR], rs[NR];
 #pragma unroll
         for (int u = 0; u < NR; ++u) {
             const uint64_t i = static_cast<uint64_t>(row0 + u) * 32 + lane;
+            eidx[u] = -1;
+            rs[u] = 0;
             if (i < n) {
                 while (i >= seg_hi) set_seg(seg + 1);
-                key[u] = __ldg(col + seg_row + (i - seg_lo));
+                eidx[u] = seg_row + static_cast<int64_t>(i - seg_lo);
+                rs[u] = seg_row;
+                key[u] = __ldg(col + eidx[u]);
             } else {
                 key[u] = NONE;
             }
         }
 #pragma unroll
-        for (int u = 0; u < NR; ++u) b[u] = (key[u] != NONE) ? __ldg(deg + key[u]) : 0u;
+        for (int u = 0; u < NR; ++u) {
+            if constexpr (kCache) {
+                b[u] = 0;
+                if (eidx[u] >= 0) {
+                    const int64_t e = eidx[u];
+                    b[u] = static_cast<uint32_t>(__ldg(cps + e) - (e == rs[u] ? 0 : __ldg(cps + e - 1)));
+                }
+            } else {
+                b[u] = (key[u] != NONE) ? __ldg(deg + key[u]) : 0u;
+            }
+        }
     }
     __device__ __forceinline__ uint32_t item(uint32_t i) const {
         const uint32_t j = find_seg(i);
@@ -231,10 +260,62 @@ struct LayerPool {
         return __ldg(col + __ldg(rp + v) + (i - (__ldg(pref + j) - pbase)));
     }
     __device__ __forceinline__ uint32_t src_of(uint32_t i) const { return __ldg(fv + find_seg(i)); }
-};
 
+    // ---- cached CTPS of the union pool: segment j contributes [O_j, O_j + T_j)
+    __device__ __forceinline__ uint64_t seg_total(uint32_t j) const {
+        const uint32_t v = __ldg(fv + j);
+        const int64_t a = __ldg(rp + v), b = __ldg(rp + v + 1);
+        return b > a ? __ldg(cps + b - 1) : 0;
+    }
+    __device__ __forceinline__ uint64_t total() const {
+        uint64_t t = 0;
+        for (uint32_t j0 = 0; j0 < nf; j0 += 32) {
+            const uint32_t j = j0 + lane_id();
+            t += warp_sum(j < nf ? seg_total(j) : 0);
+        }
+        return t;
+    }
+    __device__ __forceinline__ uint32_t npos_count() const {
+        uint32_t t = 0;
+        for (uint32_t j0 = 0; j0 < nf; j0 += 32) {
+            const uint32_t j = j0 + lane_id();
+            t += __reduce_add_sync(FULL, j < nf ? __ldg(npos + __ldg(fv + j)) : 0u);
+        }
+        return t;
+    }
+    __device__ __forceinline__ Region search(uint64_t x) {   // x warp-uniform
+        uint64_t base = 0, O = 0;
+        uint32_t js = 0;
+        for (uint32_t j0 = 0; j0 < nf; j0 += 32) {
+            const uint32_t j = j0 + lane_id();
+            const uint64_t tj = j < nf ? seg_total(j) : 0;
+            const uint64_t incl = warp_incl_scan(tj) + base;
+            const unsigned hit = __ballot_sync(FULL, j < nf && incl > x);
+            if (hit) {
+                const int f = __ffs(hit) - 1;
+                js = j0 + f;
+                O = __shfl_sync(FULL, incl - tj, f);
+                break;
+            }
+            base = __shfl_sync(FULL, incl, 31);
+        }
+        const uint32_t v = __ldg(fv + js);
+        const int64_t ra = __ldg(rp + v), rb = __ldg(rp + v + 1);
+        const uint64_t e = warp_upper_bound_u64(cps, static_cast<uint64_t>(ra), static_cast<uint64_t>(rb), x - O, &probes);
+        Region r;
+        const uint64_t before = e > static_cast<uint64_t>(ra) ? __ldg(cps + e - 1) : 0;
+        r.s = static_cast<uint32_t>((__ldg(pref + js) - pbase) + (e - static_cast<uint64_t>(ra)));
+        r.lo = O + before;
+        r.b = static_cast<uint32_t>(__ldg(cps + e) - before);
+        r.item = __ldg(col + e);
+        return r;
+    }
+};
+using LayerPool = LayerPoolT<false>;
+
+template <class LP>
 struct LayerEmit {
-    const LayerPool* P;
+    const LP* P;
     uint32_t* s_inst;
     uint32_t* s_src;
     uint32_t* s_dst;
@@ -290,9 +371,12 @@ struct LayerArgs {
     PickRec* glist;
     uint32_t kmax;
     unsigned long long* counters;
+    const uint64_t* __restrict__ cps;
+    const uint32_t* __restrict__ npos;
 };
 
-// one warp per instance (its layer pool)
+// one warp per instance (its layer pool); kCache: union CTPS from the static-bias cache
+template <bool kCache>
 __global__ void __launch_bounds__(SEL_WARPS * 32) k_layer_select(LayerArgs a) {
     __shared__ uint64_t tab_all[SEL_WARPS][TAB];
     __shared__ uint32_t bm_all[SEL_WARPS][BM_WORDS];
@@ -301,25 +385,26 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) k_layer_select(LayerArgs a) {
     uint32_t* bm = bm_all[wib];
     const int lane = lane_id();
     PickRec* gl = a.glist ? a.glist + global_warp_id() * a.kmax : nullptr;
-    unsigned long long scanned = 0, pools = 0;
+    unsigned long long scanned = 0, pools = 0, probes = 0;
     for (uint64_t i = global_warp_id(); i < a.n; i += total_warps()) {
         const uint64_t qb = a.inst_off[i], qe = a.inst_off[i + 1];
         const uint64_t e0 = a.eoff[i];
         const uint32_t ub = a.ub[i];
         uint32_t cnt = 0;
         if (qe > qb && ub > 0) {
-            LayerPool P;
-            P.rp = a.rp; P.col = a.col; P.deg = a.deg;
+            LayerPoolT<kCache> P;
+            P.rp = a.rp; P.col = a.col; P.deg = a.deg; P.cps = a.cps; P.npos = a.npos; P.probes = 0;
             P.fv = a.qv + qb;
             P.pref = a.qpref + qb;
             P.pbase = a.qpref[qb];
             P.nf = static_cast<uint32_t>(qe - qb);
             P.n = static_cast<uint32_t>(a.qpref[qe] - P.pbase);
             DrawKey dk{a.key, a.base + static_cast<uint32_t>(i), a.d, NONE};
-            LayerEmit emit{&P, a.s_inst, a.s_src, a.s_dst, e0, static_cast<uint32_t>(i)};
+            LayerEmit<LayerPoolT<kCache>> emit{&P, a.s_inst, a.s_src, a.s_dst, e0, static_cast<uint32_t>(i)};
             const Ctps C = build_ctps(P, tab);
             cnt = select_wor(P, C, tab, bm, a.fanout, dk, a.a_max, gl, emit);
-            scanned += P.n;
+            if (!kCache) scanned += P.n;
+            probes += P.probes;
             ++pools;
         }
         for (uint32_t r = cnt + lane; r < ub; r += 32) {
@@ -331,6 +416,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) k_layer_select(LayerArgs a) {
     if (lane == 0) {
         if (scanned) atomicAdd(a.counters + 0, scanned);
         if (pools) atomicAdd(a.counters + 1, pools);
+        if (probes) atomicAdd(a.counters + 2, probes);
     }
 }
 
@@ -575,13 +661,17 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
             note_launch();
             if (layer) {
                 LayerArgs la{g->row_ptr, g->col, g->deg, qv, inst_off, qpref, n, fan, ub, eoff, s_inst, s_src, s_dst,
-                             static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters};
-                k_layer_select<<<sgrid, SEL_WARPS * 32, 0, st>>>(la);
+                             static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters,
+                             g->cps, g->npos};
+                if (g->cps) k_layer_select<true><<<sgrid, SEL_WARPS * 32, 0, st>>>(la);
+                else k_layer_select<false><<<sgrid, SEL_WARPS * 32, 0, st>>>(la);
             } else {
                 SelArgs sa{g->row_ptr, g->col, g->deg, qv, qi, nq, kq, ub, eoff, s_inst, s_src, s_dst,
-                           static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters};
-                if (degree_bias) k_ns_select<true><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
-                else k_ns_select<false><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
+                           static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters,
+                           g->cps, g->npos};
+                if (degree_bias && g->cps) k_ns_select<2><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
+                else if (degree_bias) k_ns_select<1><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
+                else k_ns_select<0><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
             }
             CSAW_CUDA(cudaGetLastError());
             CSAW_TRY(hot_end(g, st));
@@ -632,13 +722,14 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
     if (n > 0) { k_counts<<<grid_for(g, n), 256, 0, st>>>(dlev, depth, n, tot); note_launch(); }
     CSAW_TRY(device_scan(U64Val{tot}, n, ScanToArray{d_offsets}, part, st));
     CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[4], d_offsets + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[5], counters, sizeof(uint64_t) * 2, cudaMemcpyDeviceToHost, st));
+    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[5], counters, sizeof(uint64_t) * 3, cudaMemcpyDeviceToHost, st));
     CSAW_CUDA(cudaStreamSynchronize(st));
     const uint64_t nedges = hbox[4];
     *num_edges = static_cast<int64_t>(nedges);
     g->stats.sampled_edges = nedges;
     g->stats.neighbours_scanned = hbox[5];
     g->stats.pools = hbox[6];
+    g->stats.cache_probes = hbox[7];
     if (static_cast<int64_t>(nedges) > capacity) {
         CSAW_TRY(stats_end(g, st));
         return fail(CSAW_ERR_CAPACITY, "output capacity " + std::to_string(capacity) + " < required " +

@@ -27,6 +27,7 @@ constexpr int TAB = 256;          // chunk-table entries per warp (2 KB of u64)
 constexpr int BM_WORDS = 256;     // strided bitmap words per warp
 constexpr uint32_t BM_BITS = BM_WORDS * 32u;
 constexpr int U = 8;              // rows (of 32 candidates) in flight per warp
+constexpr uint32_t CACHED = 0xFFFFFFFFu;   // Ctps::m marker: the pool searches a cached CTPS
 
 struct Region {
     uint32_t s;      // pool index
@@ -64,6 +65,10 @@ __device__ __forceinline__ Ctps build_ctps(Pool& P, uint64_t* __restrict__ tab) 
     c.n = P.n;
     if constexpr (Pool::kClosedForm) {
         c.m = 0; c.nch = 0; c.npos = P.n; c.T = P.n;
+        return c;
+    }
+    if constexpr (Pool::kCached) {   // static-bias CTPS cache: T and npos are read, not scanned
+        c.m = CACHED; c.nch = 0; c.T = P.total(); c.npos = P.npos_count();
         return c;
     }
     const uint32_t n = P.n;
@@ -144,6 +149,8 @@ __device__ __forceinline__ Region its_uniform(Pool& P, const Ctps& C, const uint
         Region r;
         r.s = static_cast<uint32_t>(x); r.lo = x; r.b = 1; r.item = NONE;
         return r;
+    } else if constexpr (Pool::kCached) {
+        return P.search(x);
     } else {
         if (C.m == 0) return its_table(tab, C.n, x);
         // chunk: first c with tab[c] > x (all lanes search redundantly: broadcast reads)
@@ -412,6 +419,7 @@ __device__ uint32_t select_wor(Pool& P, const Ctps& C, uint64_t* __restrict__ ta
 // 128 B col load); U rows are loaded before the dependent deg gathers.
 struct DegreePool {
     static constexpr bool kClosedForm = false;
+    static constexpr bool kCached = false;
     const uint32_t* __restrict__ col;
     const uint32_t* __restrict__ deg;
     uint64_t beg;
@@ -435,6 +443,7 @@ struct DegreePool {
 // col entries are ever read.
 struct UniformPool {
     static constexpr bool kClosedForm = true;
+    static constexpr bool kCached = false;
     const uint32_t* __restrict__ col;
     uint64_t beg;
     uint32_t n;
@@ -447,6 +456,50 @@ struct UniformPool {
             const uint32_t i = (row0 + u) * 32 + lane;
             key[u] = (i < n) ? __ldg(col + beg + i) : NONE;
             b[u] = i < n ? 1u : 0u;
+        }
+    }
+    __device__ __forceinline__ uint32_t item(uint32_t i) const { return __ldg(col + beg + i); }
+};
+
+// N(v) with EdgeBias = deg(u) read from the static-bias CTPS cache (P:779-789,
+// reading R25): cps[beg + i] = S_{i+1}.  T is one load; a draw is located by a
+// 32-ary warp search of the cached prefix (O(log32 d) round trips) -- the same
+// integer S as DegreePool's scan, hence the same picks.
+struct CachedDegreePool {
+    static constexpr bool kClosedForm = false;
+    static constexpr bool kCached = true;
+    const uint32_t* __restrict__ col;
+    const uint64_t* __restrict__ cps;
+    uint64_t beg;
+    uint32_t n;
+    uint32_t np;          // positive-bias candidates of the row
+    uint32_t probes;      // cache loads issued (statistics)
+    __device__ __forceinline__ uint64_t total() const { return n ? __ldg(cps + beg + n - 1) : 0; }
+    __device__ __forceinline__ uint32_t npos_count() const { return np; }
+    __device__ __forceinline__ Region search(uint64_t x) {
+        const uint64_t e = warp_upper_bound_u64(cps, beg, beg + n, x, &probes);
+        Region r;
+        r.s = static_cast<uint32_t>(e - beg);
+        const uint64_t hi = __ldg(cps + e);
+        r.lo = e > beg ? __ldg(cps + e - 1) : 0;
+        r.b = static_cast<uint32_t>(hi - r.lo);
+        r.item = NONE;
+        return r;
+    }
+    __device__ __forceinline__ void seek(uint32_t) {}
+    template <int NR>
+    __device__ __forceinline__ void load_rows(uint32_t row0, uint32_t (&key)[NR], uint32_t (&b)[NR]) {
+        const int lane = lane_id();
+#pragma unroll
+        for (int u = 0; u < NR; ++u) {
+            const uint32_t i = (row0 + u) * 32 + lane;
+            key[u] = NONE;
+            b[u] = 0;
+            if (i < n) {
+                key[u] = __ldg(col + beg + i);
+                const uint64_t prev = i ? __ldg(cps + beg + i - 1) : 0;
+                b[u] = static_cast<uint32_t>(__ldg(cps + beg + i) - prev);
+            }
         }
     }
     __device__ __forceinline__ uint32_t item(uint32_t i) const { return __ldg(col + beg + i); }

@@ -48,6 +48,45 @@ struct PathWriter {
     }
 };
 
+// Degree-biased walk over the static-bias CTPS cache (NEXT-1): per step one row_ptr
+// pair, one cache load for T, a 32-ary warp search of the cached prefix, one col
+// load -- O(log32 d) round trips instead of an 8 d-byte rescan.  Bit-identical.
+__global__ void __launch_bounds__(WALK_WARPS * 32) k_walk_cached(WalkArgs a, const uint64_t* __restrict__ cps) {
+    const int lane = lane_id();
+    unsigned long long probes = 0, steps = 0;
+    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+        uint32_t cur = a.seeds[w];
+        const uint32_t inst = a.base + static_cast<uint32_t>(w);
+        PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
+        pw.put(0, cur);
+        for (int32_t t = 0; t < a.L; ++t) {
+            uint32_t nxt = NONE;
+            if (cur != NONE) {
+                const int64_t b0 = __ldg(a.rp + cur);
+                const int64_t b1 = __ldg(a.rp + cur + 1);
+                if (b1 > b0) {
+                    const uint64_t T = __ldg(cps + b1 - 1);
+                    if (T > 0) {
+                        const uint64_t U = draw_u64(a.key, inst, static_cast<uint32_t>(t), 0u, word3(PURPOSE_EDGE, 0, 0));
+                        uint32_t pr = 0;
+                        const uint64_t e = warp_upper_bound_u64(cps, static_cast<uint64_t>(b0), static_cast<uint64_t>(b1),
+                                                                below(U, T), &pr);
+                        nxt = __ldg(a.col + e);
+                        probes += pr;
+                        ++steps;
+                    }
+                }
+            }
+            cur = nxt;
+            pw.put(t + 1, cur);
+        }
+    }
+    if (lane == 0) {
+        if (probes) atomicAdd(a.counters + 2, probes);
+        if (steps) atomicAdd(a.counters + 1, steps);
+    }
+}
+
 template <bool kUniform>
 __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkArgs a) {
     __shared__ uint64_t tab_all[WALK_WARPS][TAB];
@@ -96,6 +135,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkArgs a) {
 // with 5 shuffle steps; the window only moves forward (32-ary jumps).
 struct Node2vecPool {
     static constexpr bool kClosedForm = false;
+    static constexpr bool kCached = false;
     const uint32_t* __restrict__ col;
     uint64_t beg;       // N(v) = col[beg, beg + n)
     uint32_t n;
@@ -117,14 +157,29 @@ struct Node2vecPool {
         wvalid = true;
     }
 
+    // Move the window forward so that it contains lower_bound(N(prev), key): first
+    // the adjacent window (one coalesced load; the common case when merging lists
+    // of similar size), else a 32-ary search of the remainder.
+    __device__ __forceinline__ void advance_to(uint32_t key) {
+        if (!wvalid) {
+            load_window(warp_lower_bound(nprev, 0, np, key));
+            return;
+        }
+        if (wp + 32 >= np) {   // window already covers the tail
+            load_window(np);
+            return;
+        }
+        load_window(wp + 32);
+        if (__shfl_sync(FULL, W, 31) < key && wp + 32 < np) load_window(warp_lower_bound(nprev, wp + 32, np, key));
+    }
+
     // membership of each lane's u (ascending across lanes; NONE = invalid lane)
     __device__ __forceinline__ bool member_row(uint32_t u) {
         const bool valid = u != NONE;
         const unsigned vm = __ballot_sync(FULL, valid);
         if (!vm || np == 0) return false;
         const uint32_t umin = __shfl_sync(FULL, u, __ffs(vm) - 1);
-        if (!wvalid || __shfl_sync(FULL, W, 31) < umin)
-            load_window(warp_lower_bound(nprev, wvalid ? wp + 32 : 0, np, umin));
+        if (!wvalid || __shfl_sync(FULL, W, 31) < umin) advance_to(umin);
         bool mem = false, open = valid;
         for (;;) {
             // lower_bound of u in the 32-entry window by shuffle binary search
@@ -140,7 +195,7 @@ struct Node2vecPool {
             const unsigned om = __ballot_sync(FULL, open);
             if (!om) break;
             const uint32_t un = __shfl_sync(FULL, u, __ffs(om) - 1);
-            load_window(warp_lower_bound(nprev, wp + 32, np, un));
+            advance_to(un);
         }
         return mem;
     }
@@ -435,7 +490,9 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
     const uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     WalkArgs a{g->row_ptr, g->col, g->deg, d_seeds, static_cast<uint64_t>(n), length,
                static_cast<uint32_t>(base), key, d_path, static_cast<unsigned long long*>(cnt)};
-    if (b.kind == CSAW_BIAS_DEGREE) {
+    if (b.kind == CSAW_BIAS_DEGREE && g->cps) {
+        k_walk_cached<<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a, g->cps);
+    } else if (b.kind == CSAW_BIAS_DEGREE) {
         k_walk<false><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a);
     } else if (b.kind == CSAW_BIAS_UNIFORM) {
         k_walk<true><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a);
