@@ -53,6 +53,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--in-memory", action="store_true", help="cfg5: ignore the OOM budget (in-memory MDRW)")
     ap.add_argument("--no-cache", action="store_true", help="disable the static-bias CTPS cache (scan every pool)")
+    ap.add_argument("--no-zerocopy", action="store_true", help="cfg5: skip the zero-copy OOM variant")
     return ap.parse_args()
 
 
@@ -424,6 +425,33 @@ def main():
         torch.cuda.synchronize(dev)
         gather_ms = 1000 * (time.perf_counter() - t0)
 
+    # ---------------- cfg5: the B200-native zero-copy OOM variant (NEXT-4), reported apart
+    zc = None
+    if oom and cfg.workload == "mdrw" and not args.no_zerocopy:
+        try:
+            Gz = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, budget_bytes=cfg.oom_budget_bytes,
+                                      num_partitions=cfg.oom_partitions, max_resident=1, zerocopy=True)
+            outz = torch.empty((n, cfg.length, 2), dtype=torch.int32, device=dev)
+            cs.csaw_walk(Gz, bias, seeds, cfg.length, instance_base=base, rng_seed=args.rng_seed, out=outz, stream=stream)
+            torch.cuda.synchronize(dev)
+            zt = []
+            for _ in range(max(1, args.steps)):
+                flush.fill_(1)
+                z0 = torch.cuda.Event(enable_timing=True)
+                z1 = torch.cuda.Event(enable_timing=True)
+                z0.record(stream)
+                cs.csaw_walk(Gz, bias, seeds, cfg.length, instance_base=base, rng_seed=args.rng_seed, out=outz,
+                             stream=stream)
+                z1.record(stream)
+                torch.cuda.synchronize(dev)
+                zt.append(z0.elapsed_time(z1))
+            zc = {"value": n * cfg.length / (sum(zt) / len(zt) / 1000.0), "unit": UNIT, "ms_per_step": sum(zt) / len(zt),
+                  "identical_to_partitioned": bool(torch.equal(outz, out_dev)),
+                  "what": "OOM zero-copy: col_idx read in place from pinned host memory, same 8 GB budget (NEXT-4)"}
+            Gz.close()
+        except Exception as ex:
+            zc = {"error": str(ex)}
+
     # ---------------- end-to-end through the C ABI with host buffers
     e2e = None
     if not args.no_e2e:
@@ -471,6 +499,7 @@ def main():
                            "h2d_bytes_per_step": st_last["h2d_bytes"] if st_last else None,
                            "transfer_ms_per_step": st_last["transfer_ms"] if st_last else None,
                            "cache_probes_per_step": st_last["cache_probes"] if st_last else None,
+                           "oom_zerocopy": zc,
                            "neighbours_scanned_per_step": st_last["neighbours_scanned"] if st_last else None,
                            "pools_per_step": st_last["pools"] if st_last else None}}
         print(json.dumps(line), flush=True)

@@ -104,6 +104,12 @@ typedef struct {
  * instead of re-scanning the neighbour list.  Results are bit-identical (same
  * integer S, same draws). */
 #define CSAW_GRAPH_CTPS_CACHE 0x1u
+/* csaw_graph_opts.flags, out-of-memory mode only: instead of staging partitions
+ * (§5.2 workload-aware scheduling, the default), kernels read col_idx in place
+ * from pinned, mapped host memory (zero-copy).  Useful
+ * when a step needs one neighbour entry (MDRW, uniform walks); the device then
+ * holds only row_ptr + deg + run state.  Other selectors return UNSUPPORTED. */
+#define CSAW_GRAPH_OOM_ZEROCOPY 0x2u
 
 typedef struct {
     int64_t num_vertices, num_edges;

@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "util.cuh"
 
 namespace csaw {
 
@@ -203,6 +204,43 @@ __global__ void k_build_cps(const int64_t* __restrict__ rp, const uint32_t* __re
     }
 }
 
+// B-tree index over the cached prefix (select.cuh CpsTree): sizes, then levels.
+__device__ __forceinline__ uint64_t bt_size_of(uint64_t d) {
+    uint64_t s = 0, nk = d;
+    while (nk > 32) { nk = (nk + 31) / 32; s += nk; }
+    return s;
+}
+
+struct BtSize {
+    const int64_t* rp;
+    __device__ __forceinline__ uint64_t operator()(uint64_t v) const { return bt_size_of(rp[v + 1] - rp[v]); }
+};
+
+__global__ void k_build_bt(const int64_t* __restrict__ rp, const uint64_t* __restrict__ cps,
+                           const uint64_t* __restrict__ bt_off, int64_t V, uint64_t* __restrict__ bt) {
+    const int lane = lane_id();
+    for (uint64_t v = global_warp_id(); v < static_cast<uint64_t>(V); v += total_warps()) {
+        const int64_t beg = rp[v];
+        const uint64_t d = static_cast<uint64_t>(rp[v + 1] - beg);
+        if (d <= 32) continue;
+        uint64_t n[8];
+        int K = 0;
+        n[0] = d;
+        while (n[K] > 32 && K < 7) { n[K + 1] = (n[K] + 31) / 32; ++K; }
+        uint64_t off[8];
+        uint64_t acc = 0;
+        for (int k = K; k >= 1; --k) { off[k] = acc; acc += n[k]; }
+        const uint64_t base = bt_off[v];
+        for (int k = 1; k <= K; ++k) {
+            for (uint64_t j = lane; j < n[k]; j += 32) {
+                const uint64_t src = min(j * 32 + 31, n[k - 1] - 1);
+                bt[base + off[k] + j] = (k == 1) ? cps[beg + src] : bt[base + off[k - 1] + src];
+            }
+            __syncwarp();
+        }
+    }
+}
+
 }  // namespace csaw
 
 using namespace csaw;
@@ -287,6 +325,7 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         // more than the budget.
         auto& st = g->oomst;
         st.budget = o.device_budget_bytes;
+        st.zerocopy = (o.flags & CSAW_GRAPH_OOM_ZEROCOPY) != 0;
         st.P = o.num_partitions > 0 ? o.num_partitions : 4;
         st.R = o.max_resident > 0 ? o.max_resident : 2;
         st.S = o.num_streams > 0 ? o.num_streams : 2;
@@ -305,7 +344,9 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         for (int p = 0; p < st.P; ++p) maxpe = std::max(maxpe, st.ebeg[p + 1] - st.ebeg[p]);
         st.slot_edges = std::max<int64_t>(maxpe, 1);
         const int64_t resident_bytes = sizeof(int64_t) * (V + 1) + sizeof(uint32_t) * V;
-        const int64_t arena = static_cast<int64_t>(st.R) * st.slot_edges * static_cast<int64_t>(sizeof(uint32_t));
+        // the arena holds R partitions; zero-copy mode validates through a 1-partition slot only
+        const int64_t arena = static_cast<int64_t>(st.zerocopy ? 1 : st.R) * st.slot_edges *
+                              static_cast<int64_t>(sizeof(uint32_t));
         if (resident_bytes + arena > st.budget)
             return cleanup(fail(CSAW_ERR_NO_MEMORY,
                                 "OOM mode: row_ptr+deg (" + std::to_string(resident_bytes) + " B) + " +
@@ -323,6 +364,10 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
             CREATE_CUDA(cudaDeviceSynchronize(), "validate slice");
         }
         st.resident.assign(st.R, -1);
+        if (st.zerocopy) {   // no partition staging: release the validation slot
+            cudaFree(st.d_slots);
+            st.d_slots = nullptr;
+        }
         st.streams.resize(st.S);
         for (auto& s : st.streams) CREATE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
     }
@@ -340,6 +385,16 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         CREATE_CUDA(cudaEventCreate(&c1), "event");
         cudaEventRecord(c0);
         if (V > 0) k_build_cps<<<blocks, 256>>>(g->row_ptr, g->col, g->deg, V, g->cps, g->npos);
+        // B-tree index over the cached prefix
+        CREATE_CUDA(cudaMalloc(&g->bt_off, sizeof(uint64_t) * (V + 1)), "cudaMalloc(bt_off)");
+        uint64_t* part = nullptr;
+        CREATE_CUDA(cudaMalloc(&part, sizeof(uint64_t) * (SCAN_MAX_GRID + 8)), "cudaMalloc");
+        device_scan(BtSize{g->row_ptr}, static_cast<uint64_t>(V), ScanToArray{g->bt_off}, part, nullptr);
+        uint64_t btn = 0;
+        CREATE_CUDA(cudaMemcpy(&btn, g->bt_off + V, sizeof(uint64_t), cudaMemcpyDeviceToHost), "bt size");
+        cudaFree(part);
+        CREATE_CUDA(cudaMalloc(&g->bt, sizeof(uint64_t) * std::max<uint64_t>(btn, 1)), "cudaMalloc(bt)");
+        if (V > 0) k_build_bt<<<blocks, 256>>>(g->row_ptr, g->cps, g->bt_off, V, g->bt);
         cudaEventRecord(c1);
         CREATE_CUDA(cudaEventSynchronize(c1), "build cps");
         float ms = 0.f;
@@ -365,6 +420,8 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->deg) cudaFree(g->deg);
     if (g->cps) cudaFree(g->cps);
     if (g->npos) cudaFree(g->npos);
+    if (g->bt) cudaFree(g->bt);
+    if (g->bt_off) cudaFree(g->bt_off);
     auto& st = g->oomst;
     if (st.h_col) cudaFreeHost(st.h_col);
     if (st.h_row) cudaFreeHost(st.h_row);
@@ -491,7 +548,11 @@ CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32
         d_path = static_cast<uint32_t*>(p);
     }
     csaw_status s;
-    if (g->oom) {
+    if (g->oom && g->oomst.zerocopy) {
+        if (b.kind != CSAW_BIAS_MDRW && b.kind != CSAW_BIAS_UNIFORM)
+            return fail(CSAW_ERR_UNSUPPORTED, "zero-copy OOM mode implements MDRW and uniform walks");
+        s = run_walk(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
+    } else if (g->oom) {
         if (b.kind != CSAW_BIAS_MDRW)
             return fail(CSAW_ERR_UNSUPPORTED, "OOM-mode walks implement MDRW (config 5)");
         s = run_mdrw_oom(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);

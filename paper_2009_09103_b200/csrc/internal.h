@@ -72,6 +72,7 @@ struct OomState {
     int32_t R = 0;                 // resident slots
     int32_t S = 0;                 // streams
     int64_t budget = 0;
+    bool zerocopy = false;         // CSAW_GRAPH_OOM_ZEROCOPY: kernels read h_col in place
     std::vector<int64_t> bounds;   // vertex bounds [P+1]
     std::vector<int64_t> ebeg;     // first edge of partition p
     int64_t slot_edges = 0;        // capacity of an arena slot in col entries
@@ -95,6 +96,8 @@ struct csaw_graph {
     int32_t rows_sorted = 0;
     uint64_t* cps = nullptr;      // static-bias CTPS cache [E] (CSAW_GRAPH_CTPS_CACHE), inclusive per row
     uint32_t* npos = nullptr;     // [V] positive-bias neighbours per row (cache builds only)
+    uint64_t* bt = nullptr;       // fanout-32 B-tree index levels over cps (rows with d > 32)
+    uint64_t* bt_off = nullptr;   // [V] start of a row's index segment in bt
     double cache_build_ms = 0.0;
     int num_sms = 148;
     bool oom = false;

@@ -125,12 +125,14 @@ struct SelArgs {
     unsigned long long* counters;   // [0] scanned, [1] pools, [2] cache probes
     const uint64_t* __restrict__ cps;    // static-bias CTPS cache (nullptr if not built)
     const uint32_t* __restrict__ npos;
+    const uint64_t* __restrict__ bt;
+    const uint64_t* __restrict__ bt_off;
 };
 
 // Neighbor sampling / forest fire: one warp per queue entry.
 // kMode: 0 = uniform (closed form), 1 = degree (scanned CTPS), 2 = degree (cached CTPS)
 template <int kMode>
-__global__ void __launch_bounds__(SEL_WARPS * 32) k_ns_select(SelArgs a) {
+__global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_ns_select(SelArgs a) {
     __shared__ uint64_t tab_all[SEL_WARPS][TAB];
     __shared__ uint32_t bm_all[SEL_WARPS][BM_WORDS];
     const int wib = threadIdx.x >> 5;
@@ -152,7 +154,8 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) k_ns_select(SelArgs a) {
         uint32_t cnt = 0;
         if (n > 0 && k > 0) {
             if constexpr (kMode == 2) {
-                CachedDegreePool P{a.col, a.cps, static_cast<uint64_t>(b0), n, __ldg(a.npos + v), 0};
+                CachedDegreePool P{a.col, a.cps, static_cast<uint64_t>(b0), n, __ldg(a.npos + v), 0, a.bt,
+                                   __ldg(a.bt_off + v)};
                 const Ctps C = build_ctps(P, tab);
                 cnt = select_wor(P, C, tab, bm, k, dk, a.a_max, gl, emit);
                 probes += P.probes;
@@ -194,6 +197,8 @@ struct LayerPoolT {
     const uint32_t* __restrict__ deg;
     const uint64_t* __restrict__ cps;    // static-bias CTPS cache (kCache)
     const uint32_t* __restrict__ npos;   // positive-bias neighbours per row (kCache)
+    const uint64_t* __restrict__ bt;     // B-tree index over cps (kCache)
+    const uint64_t* __restrict__ bt_off;
     const uint32_t* __restrict__ fv;     // frontier vertices of the instance
     const uint64_t* __restrict__ pref;   // global exclusive prefix of frontier degrees
     uint64_t pbase;                      // pref at the instance's first segment
@@ -301,13 +306,15 @@ struct LayerPoolT {
         }
         const uint32_t v = __ldg(fv + js);
         const int64_t ra = __ldg(rp + v), rb = __ldg(rp + v + 1);
-        const uint64_t e = warp_upper_bound_u64(cps, static_cast<uint64_t>(ra), static_cast<uint64_t>(rb), x - O, &probes);
+        CpsTree t{cps, bt, col, static_cast<uint64_t>(ra), static_cast<uint32_t>(rb - ra), __ldg(bt_off + v)};
+        uint64_t xl = x - O, T = 0, e = 0, lo = 0, hi = 0;
+        uint32_t item = NONE;
+        t.template search<false>(0, xl, T, e, lo, hi, item, probes);
         Region r;
-        const uint64_t before = e > static_cast<uint64_t>(ra) ? __ldg(cps + e - 1) : 0;
         r.s = static_cast<uint32_t>((__ldg(pref + js) - pbase) + (e - static_cast<uint64_t>(ra)));
-        r.lo = O + before;
-        r.b = static_cast<uint32_t>(__ldg(cps + e) - before);
-        r.item = __ldg(col + e);
+        r.lo = O + lo;
+        r.b = static_cast<uint32_t>(hi - lo);
+        r.item = item;
         return r;
     }
 };
@@ -373,11 +380,13 @@ struct LayerArgs {
     unsigned long long* counters;
     const uint64_t* __restrict__ cps;
     const uint32_t* __restrict__ npos;
+    const uint64_t* __restrict__ bt;
+    const uint64_t* __restrict__ bt_off;
 };
 
 // one warp per instance (its layer pool); kCache: union CTPS from the static-bias cache
 template <bool kCache>
-__global__ void __launch_bounds__(SEL_WARPS * 32) k_layer_select(LayerArgs a) {
+__global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_layer_select(LayerArgs a) {
     __shared__ uint64_t tab_all[SEL_WARPS][TAB];
     __shared__ uint32_t bm_all[SEL_WARPS][BM_WORDS];
     const int wib = threadIdx.x >> 5;
@@ -394,6 +403,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) k_layer_select(LayerArgs a) {
         if (qe > qb && ub > 0) {
             LayerPoolT<kCache> P;
             P.rp = a.rp; P.col = a.col; P.deg = a.deg; P.cps = a.cps; P.npos = a.npos; P.probes = 0;
+            P.bt = a.bt; P.bt_off = a.bt_off;
             P.fv = a.qv + qb;
             P.pref = a.qpref + qb;
             P.pbase = a.qpref[qb];
@@ -487,6 +497,100 @@ __global__ void k_inst_off(const uint32_t* __restrict__ qi, uint64_t nq, uint64_
             if (qi[mid] < i) lo = mid + 1; else hi = mid;
         }
         off[i] = lo;
+    }
+}
+
+// ---- segmented UPDATE (common case): one warp per instance sorts + dedups its own
+// candidates in shared memory (they are contiguous in the staging array), applies
+// the visited post-filter, and writes its next-frontier segment; a scan of the
+// per-instance counts gives the next queue's instance offsets directly.
+constexpr uint32_t FSEG = 1024;   // max staged picks per instance handled by the segmented path
+constexpr int FSEG_WARPS = 4;
+
+__device__ __forceinline__ uint64_t stage_begin_l(const uint64_t* eoff, const uint64_t* inst_off, int layer, uint64_t i) {
+    return layer ? eoff[i] : eoff[inst_off[i]];
+}
+
+__global__ void k_segmax(const uint64_t* __restrict__ eoff, const uint64_t* __restrict__ inst_off, int layer,
+                         uint64_t n, unsigned* segmax) {
+    uint32_t mk = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t c = stage_begin_l(eoff, inst_off, layer, i + 1) - stage_begin_l(eoff, inst_off, layer, i);
+        mk = max(mk, static_cast<uint32_t>(min(c, static_cast<uint64_t>(0xFFFFFFFFu))));
+    }
+    mk = __reduce_max_sync(FULL, mk);
+    if ((threadIdx.x & 31) == 0 && mk) atomicMax(segmax, mk);
+}
+
+__global__ void __launch_bounds__(FSEG_WARPS * 32) k_frontier_seg(const uint64_t* __restrict__ eoff,
+                                                                  const uint64_t* __restrict__ inst_off, int layer,
+                                                                  const uint32_t* __restrict__ s_dst, VisitedArgs va,
+                                                                  uint64_t n, uint32_t* __restrict__ tmp,
+                                                                  uint64_t* __restrict__ cnt) {
+    __shared__ uint32_t buf_all[FSEG_WARPS][FSEG];
+    uint32_t* buf = buf_all[threadIdx.x >> 5];
+    const int lane = lane_id();
+    for (uint64_t i = global_warp_id(); i < n; i += total_warps()) {
+        const uint64_t sb = stage_begin_l(eoff, inst_off, layer, i);
+        const uint32_t c = static_cast<uint32_t>(stage_begin_l(eoff, inst_off, layer, i + 1) - sb);
+        uint32_t P = 32;
+        while (P < c) P <<= 1;
+        for (uint32_t j = lane; j < P; j += 32) {
+            uint32_t u = NONE;
+            if (j < c) {
+                u = s_dst[sb + j];
+                if (u != NONE) {   // UPDATE: drop vertices this instance already visited (R9)
+                    bool vis = va.seeds[i] == u;
+                    for (int l = 1; l <= va.nlev && !vis; ++l) {
+                        const LevelDesc& L = va.levels[l];
+                        vis = in_sorted(L.qv, L.inst_off[i], L.inst_off[i + 1], u);
+                    }
+                    if (vis) u = NONE;
+                }
+            }
+            buf[j] = u;
+        }
+        __syncwarp();
+        // bitonic sort of buf[0, P) ascending (NONE sorts last)
+        for (uint32_t k = 2; k <= P; k <<= 1) {
+            for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+                for (uint32_t idx = lane; idx < P; idx += 32) {
+                    const uint32_t pr = idx ^ jj;
+                    if (pr > idx) {
+                        const uint32_t a = buf[idx], b = buf[pr];
+                        const bool up = (idx & k) == 0;
+                        if ((a > b) == up) { buf[idx] = b; buf[pr] = a; }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        // unique, compacted into tmp[sb ...) (set semantics, R10)
+        uint32_t w = 0;
+        for (uint32_t j0 = 0; j0 < c; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            const uint32_t u = j < c ? buf[j] : NONE;
+            const bool keep = u != NONE && (j == 0 || buf[j - 1] != u);
+            const unsigned bal = __ballot_sync(FULL, keep);
+            if (keep) tmp[sb + w + __popc(bal & lanemask_lt())] = u;
+            w += __popc(bal);
+        }
+        if (lane == 0) cnt[i] = w;
+        __syncwarp();
+    }
+}
+
+__global__ void k_frontier_compact(const uint64_t* __restrict__ eoff, const uint64_t* __restrict__ inst_off, int layer,
+                                   const uint32_t* __restrict__ tmp, const uint64_t* __restrict__ noff, uint64_t n,
+                                   uint32_t* __restrict__ nqv, uint32_t* __restrict__ nqi) {
+    const int lane = lane_id();
+    for (uint64_t i = global_warp_id(); i < n; i += total_warps()) {
+        const uint64_t sb = stage_begin_l(eoff, inst_off, layer, i);
+        const uint64_t o = noff[i], c = noff[i + 1] - o;
+        for (uint64_t j = lane; j < c; j += 32) {
+            nqv[o + j] = tmp[sb + j];
+            nqi[o + j] = static_cast<uint32_t>(i);
+        }
     }
 }
 
@@ -631,8 +735,15 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
         }
         CSAW_CUDA(cudaGetLastError());
         CSAW_TRY(device_scan(U32Val{ub}, nwork, ScanToArray{eoff}, part, st));
-        // read total staged entries + kmax + error flags
-        hbox[1] = 0; hbox[2] = 0;
+        unsigned* segmaxd = kmaxd + 1;
+        CSAW_CUDA(cudaMemsetAsync(segmaxd, 0, sizeof(unsigned), st));
+        if (l + 1 < depth && n > 0) {
+            k_segmax<<<grid_for(g, n), 256, 0, st>>>(eoff, inst_off, layer ? 1 : 0, n, segmaxd);
+            note_launch();
+        }
+        // read total staged entries + kmax + error flags + largest per-instance segment
+        hbox[1] = 0; hbox[2] = 0; hbox[8] = 0;
+        CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[8], segmaxd, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[0], eoff + nwork, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
         CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[1], kmaxd, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[2], err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
@@ -640,6 +751,7 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
         const uint64_t total = hbox[0];
         const uint32_t kmax = static_cast<uint32_t>(hbox[1] & 0xFFFFFFFFu);
         const unsigned errs = static_cast<unsigned>(hbox[2] & 0xFFFFFFFFu);
+        const uint32_t segmax = static_cast<uint32_t>(hbox[8] & 0xFFFFFFFFu);
         if (errs & ERR_SEED_RANGE) return fail(CSAW_ERR_OUT_OF_RANGE, "a seed vertex is >= num_vertices");
         if (errs & ERR_POOL_TOO_BIG) return fail(CSAW_ERR_UNSUPPORTED, "a layer pool has >= 2^32-64 candidates");
         if (kmax >= (1u << 14)) return fail(CSAW_ERR_UNSUPPORTED, "a pool needs >= 2^14 picks (draw counter field)");
@@ -662,13 +774,13 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
             if (layer) {
                 LayerArgs la{g->row_ptr, g->col, g->deg, qv, inst_off, qpref, n, fan, ub, eoff, s_inst, s_src, s_dst,
                              static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters,
-                             g->cps, g->npos};
+                             g->cps, g->npos, g->bt, g->bt_off};
                 if (g->cps) k_layer_select<true><<<sgrid, SEL_WARPS * 32, 0, st>>>(la);
                 else k_layer_select<false><<<sgrid, SEL_WARPS * 32, 0, st>>>(la);
             } else {
                 SelArgs sa{g->row_ptr, g->col, g->deg, qv, qi, nq, kq, ub, eoff, s_inst, s_src, s_dst,
                            static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters,
-                           g->cps, g->npos};
+                           g->cps, g->npos, g->bt, g->bt_off};
                 if (degree_bias && g->cps) k_ns_select<2><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
                 else if (degree_bias) k_ns_select<1><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
                 else k_ns_select<0><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
@@ -689,6 +801,35 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
         if (l + 1 == depth) break;
         // ---- UPDATE: next frontier (visited post-filter, set semantics)
         CSAW_CUDA(cudaMemcpyAsync(dlev, hlev.data(), sizeof(LevelDesc) * (l + 1), cudaMemcpyHostToDevice, st));
+        if (segmax <= FSEG) {
+            // segmented path: per-instance shared-memory sort / dedup (no global sort)
+            VisitedArgs va{d_seeds, dlev, l};
+            uint32_t *tmpq, *nqv, *nqi;
+            uint64_t *cntv, *noff;
+            CSAW_TRY(lvl_buf(g, l, 11, total, &tmpq));
+            CSAW_TRY(lvl_buf(g, l, 12, n, &cntv));
+            CSAW_TRY(lvl_buf(g, l + 1, 2, n + 1, &noff));
+            const int fg = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((n + FSEG_WARPS - 1) / FSEG_WARPS,
+                                                                                      static_cast<uint64_t>(g->num_sms) * 16)));
+            if (n > 0) {
+                k_frontier_seg<<<fg, FSEG_WARPS * 32, 0, st>>>(eoff, inst_off, layer ? 1 : 0, s_dst, va, n, tmpq, cntv);
+                note_launch();
+            }
+            CSAW_TRY(device_scan(U64Val{cntv}, n, ScanToArray{noff}, part, st));
+            CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[3], noff + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+            CSAW_CUDA(cudaStreamSynchronize(st));
+            nq = hbox[3];
+            CSAW_TRY(lvl_buf(g, l + 1, 0, nq, &nqv));
+            CSAW_TRY(lvl_buf(g, l + 1, 1, nq, &nqi));
+            if (n > 0 && nq > 0) {
+                k_frontier_compact<<<fg, FSEG_WARPS * 32, 0, st>>>(eoff, inst_off, layer ? 1 : 0, tmpq, noff, n, nqv, nqi);
+                note_launch();
+            }
+            CSAW_CUDA(cudaGetLastError());
+            qv = nqv; qi = nqi; inst_off = noff;
+            continue;
+        }
+        // general path (an instance staged > FSEG picks): global LSD radix sort of (instance, vertex)
         uint64_t *keys, *alt, *hist, *hoffs;
         CSAW_TRY(lvl_buf(g, l, 11, total, &keys));
         CSAW_TRY(lvl_buf(g, l, 12, total, &alt));

@@ -461,6 +461,74 @@ struct UniformPool {
     __device__ __forceinline__ uint32_t item(uint32_t i) const { return __ldg(col + beg + i); }
 };
 
+// ---------------------------------------------------------------- CTPS-cache B-tree
+// Static fanout-32 index over one row's cached inclusive prefix cps[beg, beg+d):
+// level 0 = the row itself; level k+1 entry j = max of level-k block j (its last
+// entry); levels until <= 32 entries.  Stored top level first at bt[boff...].
+// A search reads one coalesced 32-entry block per level (256 B) instead of 32
+// scattered probes, and the top level's last entry is T.
+struct CpsTree {
+    const uint64_t* __restrict__ cps;
+    const uint64_t* __restrict__ bt;
+    const uint32_t* __restrict__ col;
+    uint64_t beg;
+    uint32_t d;
+    uint64_t boff;
+
+    struct Levels {
+        int K;                 // number of index levels (0 if d <= 32)
+        uint32_t n[8];         // n[0] = d, n[k] = ceil(n[k-1] / 32)
+        uint64_t off[8];       // offset of level k (k >= 1) inside the row's bt segment
+    };
+    __device__ __forceinline__ Levels levels() const {
+        Levels L;
+        L.K = 0;
+        L.n[0] = d;
+        while (L.n[L.K] > 32 && L.K < 7) { L.n[L.K + 1] = (L.n[L.K] + 31) / 32; ++L.K; }
+        uint64_t acc = 0;
+        for (int k = L.K; k >= 1; --k) { L.off[k] = acc; acc += L.n[k]; }
+        return L;
+    }
+    // Warp-collective.  kDraw: x = below(U, T) with T from the top level (returned);
+    // else x is given.  Result: CSR index e of the pick, S_s = lo, S_{s+1} = hi, col[e].
+    template <bool kDraw>
+    __device__ __forceinline__ void search(uint64_t U, uint64_t& x, uint64_t& T, uint64_t& e, uint64_t& lo,
+                                           uint64_t& hi, uint32_t& item, uint32_t& probes) const {
+        const int lane = lane_id();
+        const Levels L = levels();
+        uint64_t j = 0;          // block index at the current level
+        uint64_t left = 0;       // value just left of the current block (S before it)
+        for (int k = L.K; k >= 0; --k) {
+            const uint64_t idx = j * 32 + lane;
+            const bool valid = idx < L.n[k];
+            uint64_t v = 0;
+            uint32_t it = NONE;
+            if (valid) {
+                if (k == 0) { v = __ldg(cps + beg + idx); it = __ldg(col + beg + idx); }
+                else v = __ldg(bt + boff + L.off[k] + idx);
+            }
+            probes += static_cast<uint32_t>(min(static_cast<uint64_t>(32), L.n[k] - j * 32));
+            if (kDraw && k == L.K) {   // top level: its last entry is the row total
+                const unsigned vm = __ballot_sync(FULL, valid);
+                T = __shfl_sync(FULL, v, 31 - __clz(vm));
+                if (T == 0) { e = ~0ull; item = NONE; lo = hi = 0; return; }
+                x = below(U, T);
+            }
+            const unsigned hit = __ballot_sync(FULL, valid && v > x);
+            const int f = __ffs(hit) - 1;   // exists for x < T
+            const uint64_t prev = __shfl_sync(FULL, v, f > 0 ? f - 1 : 0);
+            if (f > 0) left = prev;
+            if (k == 0) {
+                e = beg + j * 32 + f;
+                hi = __shfl_sync(FULL, v, f);
+                lo = left;
+                item = __shfl_sync(FULL, it, f);
+            }
+            j = j * 32 + f;
+        }
+    }
+};
+
 // N(v) with EdgeBias = deg(u) read from the static-bias CTPS cache (P:779-789,
 // reading R25): cps[beg + i] = S_{i+1}.  T is one load; a draw is located by a
 // 32-ary warp search of the cached prefix (O(log32 d) round trips) -- the same
@@ -474,16 +542,20 @@ struct CachedDegreePool {
     uint32_t n;
     uint32_t np;          // positive-bias candidates of the row
     uint32_t probes;      // cache loads issued (statistics)
+    const uint64_t* __restrict__ bt;   // B-tree index (CpsTree)
+    uint64_t boff;
     __device__ __forceinline__ uint64_t total() const { return n ? __ldg(cps + beg + n - 1) : 0; }
     __device__ __forceinline__ uint32_t npos_count() const { return np; }
     __device__ __forceinline__ Region search(uint64_t x) {
-        const uint64_t e = warp_upper_bound_u64(cps, beg, beg + n, x, &probes);
+        CpsTree t{cps, bt, col, beg, n, boff};
+        uint64_t T = 0, e = 0, lo = 0, hi = 0;
+        uint32_t item = NONE;
+        t.template search<false>(0, x, T, e, lo, hi, item, probes);
         Region r;
         r.s = static_cast<uint32_t>(e - beg);
-        const uint64_t hi = __ldg(cps + e);
-        r.lo = e > beg ? __ldg(cps + e - 1) : 0;
-        r.b = static_cast<uint32_t>(hi - r.lo);
-        r.item = NONE;
+        r.lo = lo;
+        r.b = static_cast<uint32_t>(hi - lo);
+        r.item = item;
         return r;
     }
     __device__ __forceinline__ void seek(uint32_t) {}

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_partials(Val val, uint64_t 
     }
 }
 
-__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_top(uint64_t* part, int g) {
+static __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_top(uint64_t* part, int g) {
     __shared__ uint64_t wsum[SCAN_BLOCK / 32];
     __shared__ uint64_t total;
     const uint64_t v = threadIdx.x < g ? part[threadIdx.x] : 0;
@@ -106,7 +106,7 @@ csaw_status device_scan(Val val, uint64_t n, Out out, uint64_t* part, cudaStream
 constexpr int RS_BLOCK = 256;
 constexpr int RS_WARPS = RS_BLOCK / 32;
 
-__global__ void __launch_bounds__(RS_BLOCK) k_rs_hist(const uint64_t* __restrict__ keys, uint64_t n, uint64_t chunk,
+static __global__ void __launch_bounds__(RS_BLOCK) k_rs_hist(const uint64_t* __restrict__ keys, uint64_t n, uint64_t chunk,
                                                       int shift, uint64_t* __restrict__ hist, int g) {
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(RS_BLOCK) k_rs_hist(const uint64_t* __restrict
     hist[static_cast<uint64_t>(threadIdx.x) * g + blockIdx.x] = h[threadIdx.x];   // digit-major
 }
 
-__global__ void __launch_bounds__(RS_BLOCK) k_rs_scatter(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
+static __global__ void __launch_bounds__(RS_BLOCK) k_rs_scatter(const uint64_t* __restrict__ in, uint64_t* __restrict__ out,
                                                          uint64_t n, uint64_t chunk, int shift,
                                                          const uint64_t* __restrict__ offs, int g) {
     __shared__ uint32_t wcnt[RS_WARPS][256];

@@ -51,7 +51,9 @@ struct PathWriter {
 // Degree-biased walk over the static-bias CTPS cache (NEXT-1): per step one row_ptr
 // pair, one cache load for T, a 32-ary warp search of the cached prefix, one col
 // load -- O(log32 d) round trips instead of an 8 d-byte rescan.  Bit-identical.
-__global__ void __launch_bounds__(WALK_WARPS * 32) k_walk_cached(WalkArgs a, const uint64_t* __restrict__ cps) {
+__global__ void __launch_bounds__(WALK_WARPS * 32) k_walk_cached(WalkArgs a, const uint64_t* __restrict__ cps,
+                                                                  const uint64_t* __restrict__ bt,
+                                                                  const uint64_t* __restrict__ bt_off) {
     const int lane = lane_id();
     unsigned long long probes = 0, steps = 0;
     for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
@@ -64,17 +66,17 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk_cached(WalkArgs a, con
             if (cur != NONE) {
                 const int64_t b0 = __ldg(a.rp + cur);
                 const int64_t b1 = __ldg(a.rp + cur + 1);
+                const uint64_t boff = __ldg(bt_off + cur);
+                const uint64_t U = draw_u64(a.key, inst, static_cast<uint32_t>(t), 0u, word3(PURPOSE_EDGE, 0, 0));
                 if (b1 > b0) {
-                    const uint64_t T = __ldg(cps + b1 - 1);
-                    if (T > 0) {
-                        const uint64_t U = draw_u64(a.key, inst, static_cast<uint32_t>(t), 0u, word3(PURPOSE_EDGE, 0, 0));
-                        uint32_t pr = 0;
-                        const uint64_t e = warp_upper_bound_u64(cps, static_cast<uint64_t>(b0), static_cast<uint64_t>(b1),
-                                                                below(U, T), &pr);
-                        nxt = __ldg(a.col + e);
-                        probes += pr;
-                        ++steps;
-                    }
+                    // B-tree over the cached prefix: T from the top level, one coalesced
+                    // block per level, col read together with the last block
+                    CpsTree tr{cps, bt, a.col, static_cast<uint64_t>(b0), static_cast<uint32_t>(b1 - b0), boff};
+                    uint64_t x = 0, T = 0, e = 0, lo = 0, hi = 0;
+                    uint32_t pr = 0;
+                    tr.template search<true>(U, x, T, e, lo, hi, nxt, pr);
+                    probes += pr;
+                    if (T > 0) ++steps;
                 }
             }
             cur = nxt;
@@ -285,10 +287,185 @@ __device__ uint32_t n2v_float_step(Node2vecPool& P, const float (&wf)[3], double
     return last_item;   // x >= T after rounding: the last candidate
 }
 
+// Integer node2vec step with an implicit CTPS.  The bias of u in N(v) takes only
+// three values -- w[0] (u == prev), w[1] (u in N(prev)), w[2] (otherwise) -- so
+// S_i = w2 * (#regular before i) + sum of the special weights before i.  One merge
+// pass over N(v) x N(prev) records the "special" positions (prev and the common
+// neighbours) in shared memory; T and the region of x follow in closed form
+// between consecutive specials.  Same integers as the scanned CTPS, so the same
+// pick.  Returns false if more than SPEC_CAP specials (caller uses the scan).
+constexpr uint32_t SPEC_CAP = 1024;
+
+// Membership of each lane's x (ascending over valid lanes) in big[lo0, nb), by
+// narrowing: [lo, hi) = the big-list range of the row's value span (two 32-ary
+// searches), then one shuffle search if it fits a window, else a per-lane binary
+// search.  lo0 advances monotonically (rows are processed in ascending order).
+__device__ __forceinline__ bool n2v_find(const uint32_t* __restrict__ big, uint64_t& lo0, uint64_t nb, uint32_t x,
+                                         bool valid, uint64_t& idx) {
+    const int lane = lane_id();
+    const unsigned vm = __ballot_sync(FULL, valid);
+    idx = 0;
+    if (!vm || lo0 >= nb) return false;
+    const uint32_t xmin = __shfl_sync(FULL, x, __ffs(vm) - 1);
+    const uint32_t xmax = __shfl_sync(FULL, x, 31 - __clz(vm));
+    const uint64_t lo = warp_lower_bound(big, lo0, nb, xmin);
+    const uint64_t hi = warp_lower_bound(big, lo, nb, xmax + 1u);
+    lo0 = hi;
+    bool found = false;
+    if (hi - lo <= 32) {
+        const uint32_t W = (lo + lane < hi) ? __ldg(big + lo + lane) : NONE;
+        int k = 0;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+            const uint32_t wv = __shfl_sync(FULL, W, k + s - 1);
+            if (wv < x) k += s;
+        }
+        found = valid && __shfl_sync(FULL, W, k) == x;
+        idx = lo + k;
+    } else {
+        uint64_t l = lo, h = hi;
+        while (l < h) {   // same trip count on every lane (same range)
+            const uint64_t mid = (l + h) >> 1;
+            if (__ldg(big + mid) < x) l = mid + 1; else h = mid;
+        }
+        found = valid && l < hi && __ldg(big + l) == x;
+        idx = l;
+    }
+    return found;
+}
+
+__device__ bool n2v_implicit_step(Node2vecPool& P, uint32_t* spec, uint64_t U64, uint32_t& out) {
+    const int lane = lane_id();
+    const uint32_t n = P.n;
+    const uint32_t nrows = (n + 31) >> 5;
+    const uint64_t wp = P.w[0], w1 = P.w[1], wq = P.w[2];
+    uint32_t cnt = 0;
+    bool has_prev = false;
+    const uint64_t dv = n, dp = P.np;
+    if (dp <= 8 * dv && dv <= 8 * dp) {
+        // balanced sizes: stream N(v) rows against a forward-moving window of N(prev)
+        P.seek(0);
+        for (uint32_t r0 = 0; r0 < nrows; r0 += U) {
+            uint32_t key[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = (r0 + u) * 32 + lane;
+                key[u] = (i < n) ? __ldg(P.col + P.beg + i) : NONE;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (r0 + u < nrows) {
+                    const bool mem = P.member_row(key[u]);
+                    const bool isp = key[u] == P.prev;
+                    const bool sp = key[u] != NONE && (isp || mem);
+                    const unsigned bal = __ballot_sync(FULL, sp);
+                    if (sp) {
+                        const uint32_t idx = cnt + __popc(bal & lanemask_lt());
+                        if (idx < SPEC_CAP) spec[idx] = ((r0 + u) * 32 + lane) | (isp ? 0x80000000u : 0u);
+                    }
+                    has_prev |= __any_sync(FULL, isp);
+                    cnt += __popc(bal);
+                }
+            }
+        }
+    } else {
+        // imbalanced: iterate the smaller list, narrowed search in the larger one
+        const uint32_t* A = P.col + P.beg;    // N(v)
+        const uint64_t pp = warp_lower_bound(A, 0, dv, P.prev);
+        has_prev = pp < dv && __ldg(A + pp) == P.prev;
+        const bool small_is_v = dv < dp;
+        const uint32_t* small = small_is_v ? A : P.nprev;
+        const uint32_t* big = small_is_v ? P.nprev : A;
+        const uint64_t ns = small_is_v ? dv : dp, nb = small_is_v ? dp : dv;
+        uint64_t lo0 = 0;
+        bool prev_done = !has_prev;
+        for (uint64_t r0 = 0; r0 < ns; r0 += 32) {
+            const uint64_t i = r0 + lane;
+            const bool valid = i < ns;
+            const uint32_t xv = valid ? __ldg(small + i) : NONE;
+            uint64_t bi = 0;
+            const bool f = n2v_find(big, lo0, nb, xv, valid, bi);
+            const bool mem = f && xv != P.prev;
+            const uint64_t posA = small_is_v ? i : bi;      // position in N(v)
+            // insert prev's own position in order (it is not in N(prev): no self-loops)
+            if (!prev_done) {
+                const unsigned before = __ballot_sync(FULL, mem && posA < pp);
+                const unsigned after = __ballot_sync(FULL, mem && posA > pp);
+                (void)before;
+                if (after || r0 + 32 >= ns) {
+                    // emit members < pp first, then prev, then the rest of this row
+                    const unsigned bal0 = __ballot_sync(FULL, mem && posA < pp);
+                    if (mem && posA < pp) {
+                        const uint32_t idx = cnt + __popc(bal0 & lanemask_lt());
+                        if (idx < SPEC_CAP) spec[idx] = static_cast<uint32_t>(posA);
+                    }
+                    cnt += __popc(bal0);
+                    if (lane == 0 && cnt < SPEC_CAP) spec[cnt] = static_cast<uint32_t>(pp) | 0x80000000u;
+                    ++cnt;
+                    prev_done = true;
+                    const unsigned bal1 = __ballot_sync(FULL, mem && posA > pp);
+                    if (mem && posA > pp) {
+                        const uint32_t idx = cnt + __popc(bal1 & lanemask_lt());
+                        if (idx < SPEC_CAP) spec[idx] = static_cast<uint32_t>(posA);
+                    }
+                    cnt += __popc(bal1);
+                    continue;
+                }
+            }
+            const unsigned bal = __ballot_sync(FULL, mem);
+            if (mem) {
+                const uint32_t idx = cnt + __popc(bal & lanemask_lt());
+                if (idx < SPEC_CAP) spec[idx] = static_cast<uint32_t>(posA);
+            }
+            cnt += __popc(bal);
+        }
+        if (!prev_done) {   // empty small list
+            if (lane == 0 && cnt < SPEC_CAP) spec[cnt] = static_cast<uint32_t>(pp) | 0x80000000u;
+            ++cnt;
+        }
+    }
+    __syncwarp();
+    if (cnt > SPEC_CAP) return false;
+    const uint64_t np_ = has_prev ? 1 : 0;
+    const uint64_t T = wq * (n - cnt) + w1 * (cnt - np_) + wp * np_;
+    const uint64_t x = below(U64, T);
+    // largest special j with S(p_j) = wq * (p_j - j) + sum_{j' < j} w_j' <= x
+    bool found = false;
+    uint64_t Ssel = 0, wsel = 0, psel = 0, base = 0;
+    for (uint32_t j0 = 0; j0 < cnt; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const bool valid = j < cnt;
+        const uint32_t e = valid ? spec[j] : 0u;
+        const uint64_t pos = e & 0x7FFFFFFFu;
+        const uint64_t wj = valid ? ((e >> 31) ? wp : w1) : 0;
+        const uint64_t incl = warp_incl_scan(wj);
+        const uint64_t Sj = wq * (pos - j) + base + incl - wj;
+        const unsigned vm = __ballot_sync(FULL, valid);
+        const unsigned le = __ballot_sync(FULL, valid && Sj <= x);
+        if (le) {
+            const int f = 31 - __clz(le);
+            found = true;
+            Ssel = __shfl_sync(FULL, Sj, f);
+            wsel = __shfl_sync(FULL, wj, f);
+            psel = __shfl_sync(FULL, pos, f);
+        }
+        if (le != vm) break;
+        base += __shfl_sync(FULL, incl, 31);
+    }
+    uint64_t i;
+    if (!found) i = x / wq;
+    else if (x < Ssel + wsel) i = psel;
+    else i = psel + 1 + (x - Ssel - wsel) / wq;
+    out = __ldg(P.col + P.beg + i);
+    return true;
+}
+
 template <bool kFloat>
-__global__ void __launch_bounds__(WALK_WARPS * 32) k_node2vec(N2vArgs na) {
+__global__ void __launch_bounds__(WALK_WARPS * 32, 3) k_node2vec(N2vArgs na) {
     __shared__ uint64_t tab_all[WALK_WARPS][TAB];
+    __shared__ uint32_t spec_all[kFloat ? 1 : WALK_WARPS][kFloat ? 1 : SPEC_CAP];
     uint64_t* tab = tab_all[threadIdx.x >> 5];
+    uint32_t* spec = spec_all[kFloat ? 0 : (threadIdx.x >> 5)];
     const WalkArgs& a = na.wa;
     const int lane = lane_id();
     unsigned long long scanned = 0, steps = 0;
@@ -319,8 +496,10 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_node2vec(N2vArgs na) {
                             nxt = n2v_float_step(P, na.wf, reinterpret_cast<double*>(tab), U64);
                         } else {
                             P.w[0] = na.wint[0]; P.w[1] = na.wint[1]; P.w[2] = na.wint[2];
-                            const Ctps C = build_ctps(P, tab);
-                            nxt = select_wr(P, C, tab, U64);
+                            if (!n2v_implicit_step(P, spec, U64, nxt)) {
+                                const Ctps C = build_ctps(P, tab);   // > SPEC_CAP common neighbours
+                                nxt = select_wr(P, C, tab, U64);
+                            }
                         }
                         scanned += d;
                     }
@@ -368,8 +547,8 @@ struct MdrwArgs {
     uint32_t* __restrict__ out;           // [n][L][2]
     uint32_t* __restrict__ pool_v;        // scratch [n][m]
     uint64_t* __restrict__ pool_rb;       // scratch [n][m]
-    uint32_t* __restrict__ gbias;         // scratch [n_warps][m] when shared memory is too small
-    uint64_t* __restrict__ gblk;          // scratch [n_warps][nblk]
+    uint32_t* __restrict__ gbias;         // scratch [n][m]: per-slot VertexBias (degree)
+    uint64_t* __restrict__ gblk;          // scratch [n_warps][nblk] when shared memory is too small
     int smem_ok;
     int warps_per_block;
 };
@@ -380,20 +559,13 @@ __global__ void k_mdrw(MdrwArgs a) {
     const int wib = threadIdx.x >> 5;
     const uint32_t m = static_cast<uint32_t>(a.m);
     const uint32_t nblk = (m + 31) / 32;
-    uint32_t* bias;
-    uint64_t* blk;
-    if (a.smem_ok) {
-        const size_t per = ((static_cast<size_t>(m) * 4 + 15) / 16) * 16 + static_cast<size_t>(nblk) * 8;
-        unsigned char* base = smem_raw + per * wib;
-        blk = reinterpret_cast<uint64_t*>(base);
-        bias = reinterpret_cast<uint32_t*>(base + static_cast<size_t>(nblk) * 8);
-    } else {
-        const uint64_t gw = global_warp_id();
-        bias = a.gbias + gw * m;
-        blk = a.gblk + gw * nblk;
-    }
+    // block totals in shared memory (small: all instances fit in one wave); the
+    // per-slot biases stay in global memory (one coalesced 128 B read per step)
+    uint64_t* blk = a.smem_ok ? reinterpret_cast<uint64_t*>(smem_raw) + static_cast<size_t>(nblk) * wib
+                              : a.gblk + global_warp_id() * nblk;
     for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
+        uint32_t* bias = a.gbias + w * m;
         uint32_t* pv = a.pool_v + w * m;
         uint64_t* prb = a.pool_rb + w * m;
         // init pool (slot order = seeds order)
@@ -488,10 +660,12 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
     CSAW_TRY(hot_begin(g, st));
     note_launch();
     const uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
-    WalkArgs a{g->row_ptr, g->col, g->deg, d_seeds, static_cast<uint64_t>(n), length,
+    // zero-copy OOM mode: col_idx is read in place from pinned host memory (UVA)
+    const uint32_t* colp = g->col ? g->col : g->oomst.h_col;
+    WalkArgs a{g->row_ptr, colp, g->deg, d_seeds, static_cast<uint64_t>(n), length,
                static_cast<uint32_t>(base), key, d_path, static_cast<unsigned long long*>(cnt)};
     if (b.kind == CSAW_BIAS_DEGREE && g->cps) {
-        k_walk_cached<<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a, g->cps);
+        k_walk_cached<<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a, g->cps, g->bt, g->bt_off);
     } else if (b.kind == CSAW_BIAS_DEGREE) {
         k_walk<false><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a);
     } else if (b.kind == CSAW_BIAS_UNIFORM) {
@@ -512,24 +686,24 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
     } else if (b.kind == CSAW_BIAS_MDRW) {
         const uint32_t m = static_cast<uint32_t>(b.pool_size);
         const uint32_t nblk = (m + 31) / 32;
-        const size_t per = ((static_cast<size_t>(m) * 4 + 15) / 16) * 16 + static_cast<size_t>(nblk) * 8;
+        const size_t per = static_cast<size_t>(nblk) * 8;
         int wpb = static_cast<int>(std::min<size_t>(8, (200 * 1024) / std::max<size_t>(per, 1)));
         const bool smem_ok = wpb >= 1;
-        if (!smem_ok) wpb = 4;
-        const int64_t max_warps = static_cast<int64_t>(g->num_sms) * 48;
+        if (!smem_ok) wpb = 8;
+        const int64_t max_warps = static_cast<int64_t>(g->num_sms) * 64;
         const int64_t warps = std::min<int64_t>(n, max_warps);
         const int grid = static_cast<int>((warps + wpb - 1) / wpb);
         void *pv, *prb, *gb = nullptr, *gk = nullptr;
         CSAW_TRY(g->scratch.get(SL_TMP0, sizeof(uint32_t) * n * m, &pv));
         CSAW_TRY(g->scratch.get(SL_TMP1, sizeof(uint64_t) * n * m, &prb));
+        CSAW_TRY(g->scratch.get(SL_TMP2, sizeof(uint32_t) * n * m, &gb));
         const size_t smem = smem_ok ? per * wpb : 0;
         if (!smem_ok) {
-            CSAW_TRY(g->scratch.get(SL_TMP2, (sizeof(uint32_t) * m + sizeof(uint64_t) * nblk) * grid * wpb, &gb));
-            gk = static_cast<char*>(gb) + sizeof(uint32_t) * m * grid * wpb;
+            CSAW_TRY(g->scratch.get(SL_GLIST, sizeof(uint64_t) * nblk * grid * wpb, &gk));
         } else {
             CSAW_CUDA(cudaFuncSetAttribute(k_mdrw, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         }
-        MdrwArgs ma{g->row_ptr, g->col, d_seeds, static_cast<uint64_t>(n), b.pool_size, length,
+        MdrwArgs ma{g->row_ptr, colp, d_seeds, static_cast<uint64_t>(n), b.pool_size, length,
                     static_cast<uint32_t>(base), key, d_path, static_cast<uint32_t*>(pv),
                     static_cast<uint64_t*>(prb), static_cast<uint32_t*>(gb), static_cast<uint64_t*>(gk),
                     smem_ok ? 1 : 0, wpb};

@@ -83,3 +83,22 @@ def test_oom_budget_enforced(medium):
         cs.csaw_walk(Go, cs.make_bias("mdrw"), seeds, 10)
     assert ei.value.status == 6
     Go.close()
+
+
+def test_oom_zerocopy_equals_in_memory(medium):
+    """NEXT-4(ii): col_idx read in place from pinned host memory under the budget."""
+    g = medium
+    n, m, L = 64, 200, 300
+    seeds = mdrw_seeds(g, n, m).to(DEV)
+    Gm = cs.csaw_graph_create(g.row_ptr.to(DEV), g.col_idx.to(DEV))
+    Gz = cs.csaw_graph_create(g.row_ptr, g.col_idx, budget_bytes=budget_for(g, 4, 1, n, m), num_partitions=4,
+                              max_resident=1, zerocopy=True)
+    assert torch.equal(cs.csaw_walk(Gm, cs.make_bias("mdrw"), seeds, L, rng_seed=5),
+                       cs.csaw_walk(Gz, cs.make_bias("mdrw"), seeds, L, rng_seed=5))
+    s1 = seeds[:, 0].contiguous()
+    assert torch.equal(cs.csaw_walk(Gm, "uniform", s1, L, rng_seed=6), cs.csaw_walk(Gz, "uniform", s1, L, rng_seed=6))
+    with pytest.raises(cs.CsawError) as ei:
+        cs.csaw_walk(Gz, "degree", s1, 10)
+    assert ei.value.status == 8
+    Gm.close()
+    Gz.close()
