@@ -110,6 +110,11 @@ typedef struct {
  * when a step needs one neighbour entry (MDRW, uniform walks); the device then
  * holds only row_ptr + deg + run state.  Other selectors return UNSUPPORTED. */
 #define CSAW_GRAPH_OOM_ZEROCOPY 0x2u
+/* csaw_graph_opts.flags: csaw_sample always uses the level-synchronous batched
+ * driver (one frontier queue mixing all instances) instead of the
+ * fused one-warp-per-instance path chosen for small per-instance frontiers.
+ * Outputs are identical either way (R7); this flag exists for tests/ablation. */
+#define CSAW_GRAPH_SAMPLE_BATCHED 0x4u
 
 typedef struct {
     int64_t num_vertices, num_edges;

@@ -277,6 +277,7 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
     CSAW_CUDA(cudaGetDeviceProperties(&prop, o.device));
     g->num_sms = prop.multiProcessorCount;
     g->oom = o.device_budget_bytes > 0;
+    g->force_batched = (o.flags & CSAW_GRAPH_SAMPLE_BATCHED) != 0;
     const int64_t V = g->V, E = g->E;
     ValidateOut* dv = nullptr;
     uint32_t* dcol = nullptr;

@@ -111,6 +111,8 @@ struct csaw_graph {
     mutable int hot_used = 0;
     // device counters still to be folded into `stats` ([0] scanned, [1] pools/steps)
     mutable const unsigned long long* pending_counters = nullptr;
+    // testing / ablation: always use the level-synchronous batched sampling driver
+    bool force_batched = false;
 };
 
 namespace csaw {
@@ -142,6 +144,10 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
                        const uint32_t* d_seeds, int64_t n, uint64_t base, uint64_t seed, uint64_t* d_offsets,
                        uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
                        bool out_on_device, cudaStream_t st);
+csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
+                              const uint32_t* d_seeds, int64_t n, uint64_t base, uint64_t seed, uint64_t* d_offsets,
+                              uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
+                              bool out_on_device, cudaStream_t st);
 csaw_status run_mdrw_oom(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds,
                          int64_t n, uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st);
 }  // namespace csaw

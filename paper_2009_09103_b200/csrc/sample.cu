@@ -199,8 +199,8 @@ struct LayerPoolT {
     const uint32_t* __restrict__ npos;   // positive-bias neighbours per row (kCache)
     const uint64_t* __restrict__ bt;     // B-tree index over cps (kCache)
     const uint64_t* __restrict__ bt_off;
-    const uint32_t* __restrict__ fv;     // frontier vertices of the instance
-    const uint64_t* __restrict__ pref;   // global exclusive prefix of frontier degrees
+    const uint32_t* fv;                  // frontier vertices of the instance (global or shared)
+    const uint64_t* pref;                // exclusive prefix of frontier degrees (global or shared)
     uint64_t pbase;                      // pref at the instance's first segment
     uint32_t nf;                         // frontier size
     uint32_t n;                          // pool size
@@ -214,15 +214,15 @@ struct LayerPoolT {
         uint32_t lo = 0, hi = nf;
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) >> 1;
-            if (__ldg(pref + mid) - pbase <= i) lo = mid; else hi = mid;
+            if (pref[mid] - pbase <= i) lo = mid; else hi = mid;
         }
         return lo;
     }
     __device__ __forceinline__ void set_seg(uint32_t j) {
         seg = j;
-        seg_lo = __ldg(pref + j) - pbase;
-        seg_hi = (j + 1 < nf) ? __ldg(pref + j + 1) - pbase : n;
-        seg_row = __ldg(rp + __ldg(fv + j));
+        seg_lo = pref[j] - pbase;
+        seg_hi = (j + 1 < nf) ? pref[j + 1] - pbase : n;
+        seg_row = __ldg(rp + fv[j]);
     }
     __device__ __forceinline__ void seek(uint32_t row0) {
         const uint64_t i = static_cast<uint64_t>(row0) * 32 + lane_id();
@@ -261,14 +261,14 @@ struct LayerPoolT {
     }
     __device__ __forceinline__ uint32_t item(uint32_t i) const {
         const uint32_t j = find_seg(i);
-        const uint32_t v = __ldg(fv + j);
-        return __ldg(col + __ldg(rp + v) + (i - (__ldg(pref + j) - pbase)));
+        const uint32_t v = fv[j];
+        return __ldg(col + __ldg(rp + v) + (i - (pref[j] - pbase)));
     }
-    __device__ __forceinline__ uint32_t src_of(uint32_t i) const { return __ldg(fv + find_seg(i)); }
+    __device__ __forceinline__ uint32_t src_of(uint32_t i) const { return fv[find_seg(i)]; }
 
     // ---- cached CTPS of the union pool: segment j contributes [O_j, O_j + T_j)
     __device__ __forceinline__ uint64_t seg_total(uint32_t j) const {
-        const uint32_t v = __ldg(fv + j);
+        const uint32_t v = fv[j];
         const int64_t a = __ldg(rp + v), b = __ldg(rp + v + 1);
         return b > a ? __ldg(cps + b - 1) : 0;
     }
@@ -284,7 +284,7 @@ struct LayerPoolT {
         uint32_t t = 0;
         for (uint32_t j0 = 0; j0 < nf; j0 += 32) {
             const uint32_t j = j0 + lane_id();
-            t += __reduce_add_sync(FULL, j < nf ? __ldg(npos + __ldg(fv + j)) : 0u);
+            t += __reduce_add_sync(FULL, j < nf ? __ldg(npos + fv[j]) : 0u);
         }
         return t;
     }
@@ -304,14 +304,14 @@ struct LayerPoolT {
             }
             base = __shfl_sync(FULL, incl, 31);
         }
-        const uint32_t v = __ldg(fv + js);
+        const uint32_t v = fv[js];
         const int64_t ra = __ldg(rp + v), rb = __ldg(rp + v + 1);
         CpsTree t{cps, bt, col, static_cast<uint64_t>(ra), static_cast<uint32_t>(rb - ra), __ldg(bt_off + v)};
         uint64_t xl = x - O, T = 0, e = 0, lo = 0, hi = 0;
         uint32_t item = NONE;
         t.template search<false>(0, xl, T, e, lo, hi, item, probes);
         Region r;
-        r.s = static_cast<uint32_t>((__ldg(pref + js) - pbase) + (e - static_cast<uint64_t>(ra)));
+        r.s = static_cast<uint32_t>((pref[js] - pbase) + (e - static_cast<uint64_t>(ra)));
         r.lo = O + lo;
         r.b = static_cast<uint32_t>(hi - lo);
         r.item = item;
@@ -636,6 +636,251 @@ __global__ void k_write(LevelDesc L, int depth1, const uint32_t* __restrict__ s_
     }
 }
 
+// ---------------------------------------------------------------- fused per-instance sampler
+// For small per-instance frontiers (the paper's NeighborSize = Depth = 2 setups,
+// P:972-974) the whole traversal of one instance runs in ONE warp: frontier,
+// next frontier and visited set live in shared memory, each level's pools are
+// selected in frontier order, and the edges go to a per-instance staging row.
+// One launch instead of ~15 per level and no host round trip between levels;
+// the results are identical to the level-synchronous batched driver because
+// every draw is keyed by (instance, depth, vertex) (R7).  Anything that does not
+// fit (frontier > F_CAP, visited > VIS_CAP, more staged edges than ecap, or a
+// pool needing > 32 picks) raises the overflow flag and the host reruns the call
+// with the batched driver.
+constexpr int FUSED_WARPS = 4;
+constexpr uint32_t F_CAP = 256;
+constexpr uint32_t VIS_CAP = 512;
+
+struct FusedArgs {
+    const int64_t* __restrict__ rp;
+    const uint32_t* __restrict__ col;
+    const uint32_t* __restrict__ deg;
+    const uint64_t* __restrict__ cps;
+    const uint32_t* __restrict__ npos;
+    const uint64_t* __restrict__ bt;
+    const uint64_t* __restrict__ bt_off;
+    const uint32_t* __restrict__ seeds;
+    uint64_t n;
+    int32_t depth;
+    const int32_t* __restrict__ fanout;   // device [depth]
+    uint64_t theta;                       // forest fire
+    uint32_t base;
+    uint2 key;
+    uint32_t a_max;
+    uint32_t ecap;                        // staged edges per instance
+    uint32_t* __restrict__ s_src;         // [n][ecap]
+    uint32_t* __restrict__ s_dst;
+    uint8_t* __restrict__ s_dep;
+    uint64_t* __restrict__ cnt;           // [n]
+    unsigned* overflow;                   // bit 0: fall back to the batched driver; bit 1: seed out of range
+    unsigned long long* counters;
+    int64_t V;
+};
+
+struct FusedEmit {
+    uint32_t* s_src;
+    uint32_t* s_dst;
+    uint8_t* s_dep;
+    uint64_t e0;
+    uint32_t src;
+    uint8_t d1;
+    __device__ __forceinline__ void operator()(uint32_t rank, uint32_t, uint32_t item) const {
+        s_src[e0 + rank] = src;
+        s_dst[e0 + rank] = item;
+        s_dep[e0 + rank] = d1;
+    }
+};
+
+template <class LP>
+struct FusedLayerEmit {
+    const LP* P;
+    uint32_t* s_src;
+    uint32_t* s_dst;
+    uint8_t* s_dep;
+    uint64_t e0;
+    uint8_t d1;
+    __device__ __forceinline__ void operator()(uint32_t rank, uint32_t s, uint32_t item) const {
+        s_src[e0 + rank] = P->src_of(s);
+        s_dst[e0 + rank] = item;
+        s_dep[e0 + rank] = d1;
+    }
+};
+
+// kMode: 0 uniform NS, 1 degree NS (scan), 2 degree NS (cache), 3 forest fire,
+//        4 layer (scan), 5 layer (cache)
+template <int kMode>
+__global__ void __launch_bounds__(FUSED_WARPS * 32, 4) k_sample_fused(FusedArgs a) {
+    __shared__ uint64_t tab_all[FUSED_WARPS][TAB];
+    __shared__ uint32_t bm_all[FUSED_WARPS][BM_WORDS];
+    __shared__ uint32_t F_all[FUSED_WARPS][F_CAP];
+    __shared__ uint32_t NX_all[FUSED_WARPS][F_CAP];
+    __shared__ uint32_t VIS_all[FUSED_WARPS][VIS_CAP];
+    __shared__ uint64_t PF_all[FUSED_WARPS][F_CAP];
+    const int wib = threadIdx.x >> 5;
+    uint64_t* tab = tab_all[wib];
+    uint32_t* bm = bm_all[wib];
+    uint32_t* F = F_all[wib];
+    uint32_t* NX = NX_all[wib];
+    uint32_t* VIS = VIS_all[wib];
+    uint64_t* PF = PF_all[wib];
+    const int lane = lane_id();
+    constexpr bool kLayer = kMode >= 4;
+    unsigned long long scanned = 0, pools = 0, probes = 0;
+    for (uint64_t i = global_warp_id(); i < a.n; i += total_warps()) {
+        const uint32_t inst = a.base + static_cast<uint32_t>(i);
+        const uint32_t seed = a.seeds[i];
+        const uint64_t e_base = i * a.ecap;
+        if (static_cast<int64_t>(seed) >= a.V) {
+            if (lane == 0) { atomicOr(a.overflow, 2u); a.cnt[i] = 0; }
+            continue;
+        }
+        if (lane == 0) { F[0] = seed; VIS[0] = seed; }
+        __syncwarp();
+        uint32_t nf = 1, nv = 1;
+        uint32_t ec = 0;
+        bool ovf = false;
+        for (int32_t d = 0; d < a.depth && nf > 0 && !ovf; ++d) {
+            uint32_t nnx = 0;
+            const uint32_t ec0 = ec;
+            if constexpr (kLayer) {
+                // union pool over the sorted frontier: exclusive degree prefix in PF
+                uint64_t carry = 0;
+                for (uint32_t j0 = 0; j0 < nf; j0 += 32) {
+                    const uint32_t j = j0 + lane;
+                    const uint64_t dj = j < nf ? static_cast<uint64_t>(__ldg(a.rp + F[j] + 1) - __ldg(a.rp + F[j])) : 0;
+                    const uint64_t incl = warp_incl_scan(dj) + carry;
+                    if (j < nf) PF[j] = incl - dj;
+                    carry = __shfl_sync(FULL, incl, 31);
+                }
+                __syncwarp();
+                const uint32_t k = static_cast<uint32_t>(a.fanout[d]);
+                if (carry >= static_cast<uint64_t>(NONE) - 64 || k > 32) { ovf = true; break; }
+                const uint32_t pn = static_cast<uint32_t>(carry);
+                if (pn > 0 && k > 0) {
+                    if (ec + min(k, pn) > a.ecap) { ovf = true; break; }
+                    LayerPoolT<kMode == 5> P;
+                    P.rp = a.rp; P.col = a.col; P.deg = a.deg; P.cps = a.cps; P.npos = a.npos; P.probes = 0;
+                    P.bt = a.bt; P.bt_off = a.bt_off;
+                    P.fv = F; P.pref = PF; P.pbase = 0; P.nf = nf; P.n = pn;
+                    DrawKey dk{a.key, inst, static_cast<uint32_t>(d), NONE};
+                    FusedLayerEmit<LayerPoolT<kMode == 5>> emit{&P, a.s_src, a.s_dst, a.s_dep, e_base + ec,
+                                                                 static_cast<uint8_t>(d + 1)};
+                    const Ctps C = build_ctps(P, tab);
+                    ec += select_wor(P, C, tab, bm, k, dk, a.a_max, nullptr, emit);
+                    if (kMode == 4) scanned += pn;
+                    probes += P.probes;
+                    ++pools;
+                }
+            } else {
+                for (uint32_t fj = 0; fj < nf && !ovf; ++fj) {
+                    const uint32_t v = F[fj];
+                    const int64_t b0 = __ldg(a.rp + v);
+                    const uint32_t nd = static_cast<uint32_t>(__ldg(a.rp + v + 1) - b0);
+                    uint32_t k;
+                    if constexpr (kMode == 3) k = ff_burn(a.key, inst, static_cast<uint32_t>(d), v, nd, a.theta);
+                    else k = static_cast<uint32_t>(a.fanout[d]);
+                    if (nd == 0 || k == 0) continue;
+                    if (k > 32 || ec + min(k, nd) > a.ecap) { ovf = true; break; }
+                    DrawKey dk{a.key, inst, static_cast<uint32_t>(d), v};
+                    FusedEmit emit{a.s_src, a.s_dst, a.s_dep, e_base + ec, v, static_cast<uint8_t>(d + 1)};
+                    uint32_t c;
+                    if constexpr (kMode == 2) {
+                        CachedDegreePool P{a.col, a.cps, static_cast<uint64_t>(b0), nd, __ldg(a.npos + v), 0, a.bt,
+                                           __ldg(a.bt_off + v)};
+                        const Ctps C = build_ctps(P, tab);
+                        c = select_wor(P, C, tab, bm, k, dk, a.a_max, nullptr, emit);
+                        probes += P.probes;
+                    } else if constexpr (kMode == 1) {
+                        DegreePool P{a.col, a.deg, static_cast<uint64_t>(b0), nd};
+                        const Ctps C = build_ctps(P, tab);
+                        c = select_wor(P, C, tab, bm, k, dk, a.a_max, nullptr, emit);
+                        scanned += nd;
+                    } else {
+                        UniformPool P{a.col, static_cast<uint64_t>(b0), nd};
+                        const Ctps C = build_ctps(P, tab);
+                        c = select_wor(P, C, tab, bm, k, dk, a.a_max, nullptr, emit);
+                    }
+                    ec += c;
+                    ++pools;
+                }
+                if (ovf) break;
+            }
+            __syncwarp();
+            if (d + 1 == a.depth) break;
+            // UPDATE (R9): unvisited picks of this level -> next frontier
+            for (uint32_t e0 = ec0; e0 < ec; e0 += 32) {
+                const uint32_t e = e0 + lane;
+                uint32_t u = e < ec ? a.s_dst[e_base + e] : NONE;
+                if (u != NONE)
+                    for (uint32_t q = 0; q < nv; ++q)
+                        if (VIS[q] == u) { u = NONE; break; }
+                const unsigned bal = __ballot_sync(FULL, u != NONE);
+                const uint32_t pos = nnx + __popc(bal & lanemask_lt());
+                if (u != NONE && pos < F_CAP) NX[pos] = u;
+                nnx += __popc(bal);
+            }
+            __syncwarp();
+            if (nnx > F_CAP) { ovf = true; break; }
+            // sort + unique (set semantics, R10)
+            uint32_t P2 = 32;
+            while (P2 < nnx) P2 <<= 1;
+            for (uint32_t j = nnx + lane; j < P2; j += 32) NX[j] = NONE;
+            __syncwarp();
+            for (uint32_t kk = 2; kk <= P2; kk <<= 1) {
+                for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+                    for (uint32_t idx = lane; idx < P2; idx += 32) {
+                        const uint32_t pr = idx ^ jj;
+                        if (pr > idx) {
+                            const uint32_t x0 = NX[idx], x1 = NX[pr];
+                            if ((x0 > x1) == ((idx & kk) == 0)) { NX[idx] = x1; NX[pr] = x0; }
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+            uint32_t w = 0;
+            for (uint32_t j0 = 0; j0 < nnx; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const uint32_t u = j < nnx ? NX[j] : NONE;
+                const bool keep = u != NONE && (j == 0 || NX[j - 1] != u);
+                const unsigned bal = __ballot_sync(FULL, keep);
+                if (keep) F[w + __popc(bal & lanemask_lt())] = u;
+                w += __popc(bal);
+            }
+            __syncwarp();
+            nf = w;
+            if (nv + nf > VIS_CAP) { ovf = true; break; }
+            for (uint32_t j = lane; j < nf; j += 32) VIS[nv + j] = F[j];
+            nv += nf;
+            __syncwarp();
+        }
+        if (lane == 0) {
+            a.cnt[i] = ec;
+            if (ovf) atomicOr(a.overflow, 1u);
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if (scanned) atomicAdd(a.counters + 0, scanned);
+        if (pools) atomicAdd(a.counters + 1, pools);
+        if (probes) atomicAdd(a.counters + 2, probes);
+    }
+}
+
+__global__ void k_fused_copy(const uint32_t* __restrict__ s_src, const uint32_t* __restrict__ s_dst,
+                             const uint8_t* __restrict__ s_dep, uint32_t ecap, const uint64_t* __restrict__ offs,
+                             uint64_t n, uint32_t* __restrict__ src, uint32_t* __restrict__ dst, uint8_t* __restrict__ dep) {
+    const int lane = lane_id();
+    for (uint64_t i = global_warp_id(); i < n; i += total_warps()) {
+        const uint64_t o = offs[i], c = offs[i + 1] - o;
+        for (uint64_t j = lane; j < c; j += 32) {
+            src[o + j] = s_src[i * ecap + j];
+            dst[o + j] = s_dst[i * ecap + j];
+            dep[o + j] = s_dep[i * ecap + j];
+        }
+    }
+}
+
 // ---------------------------------------------------------------- host driver
 static int grid_for(const csaw_graph* g, uint64_t n, int per_block = 256) {
     const uint64_t b = (n + per_block - 1) / per_block;
@@ -655,7 +900,137 @@ static csaw_status lvl_buf(const csaw_graph* g, int l, int k, uint64_t count, T*
     return CSAW_OK;
 }
 
+// Fused path: returns CSAW_OK when done, CSAW_ERR_CAPACITY / OUT_OF_RANGE as usual, and
+// FUSED_FALLBACK when the batched level-synchronous driver must run instead.
+constexpr csaw_status FUSED_FALLBACK = static_cast<csaw_status>(-1);
+
+static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
+                                    const uint32_t* d_seeds, uint64_t n, uint64_t base, uint64_t seed,
+                                    uint64_t* d_offsets, uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity,
+                                    int64_t* num_edges, bool out_on_device, cudaStream_t st) {
+    const bool layer = b.kind == CSAW_BIAS_LAYER;
+    const bool ff = b.kind == CSAW_BIAS_FOREST_FIRE;
+    // per-instance staging capacity from the fanouts (forest fire: a fixed budget)
+    double ecap_d = 0;
+    if (ff) {
+        ecap_d = 512;
+    } else {
+        double level = 1;
+        for (int d = 0; d < depth; ++d) {
+            if (fanout[d] > 32) return FUSED_FALLBACK;
+            level = layer ? fanout[d] : level * fanout[d];
+            ecap_d += level;
+        }
+    }
+    if (ecap_d > 2048 || n == 0) return FUSED_FALLBACK;
+    const uint32_t ecap = std::max<uint32_t>(1, static_cast<uint32_t>(ecap_d));
+    void *pc, *ps, *pd, *pe, *pk, *pf, *pp;
+    CSAW_TRY(g->scratch.get(SL_COUNTS, 256, &pc));
+    unsigned long long* counters = static_cast<unsigned long long*>(pc);
+    unsigned* ovf = reinterpret_cast<unsigned*>(counters + 12);
+    CSAW_TRY(g->scratch.get(SL_SRC + 200, sizeof(uint32_t) * n * ecap, &ps));
+    CSAW_TRY(g->scratch.get(SL_SRC + 201, sizeof(uint32_t) * n * ecap, &pd));
+    CSAW_TRY(g->scratch.get(SL_SRC + 202, static_cast<size_t>(n) * ecap, &pe));
+    CSAW_TRY(g->scratch.get(SL_SRC + 203, sizeof(uint64_t) * n, &pk));
+    CSAW_TRY(g->scratch.get(SL_SRC + 204, sizeof(int32_t) * std::max(depth, 1), &pf));
+    CSAW_TRY(g->scratch.get(SL_TMP2, sizeof(uint64_t) * (SCAN_MAX_GRID + 8), &pp));
+    void* hmb;
+    CSAW_TRY(g->pinned.get(4096, &hmb));
+    volatile uint64_t* hbox = static_cast<volatile uint64_t*>(hmb);
+    int32_t* hfan = reinterpret_cast<int32_t*>(const_cast<uint64_t*>(hbox) + 64);
+    for (int d = 0; d < depth; ++d) hfan[d] = ff ? 0 : fanout[d];
+    CSAW_CUDA(cudaMemsetAsync(counters, 0, 256, st));
+    CSAW_CUDA(cudaMemcpyAsync(pf, hfan, sizeof(int32_t) * depth, cudaMemcpyHostToDevice, st));
+    CSAW_TRY(stats_begin(g, st));
+    FusedArgs a;
+    a.rp = g->row_ptr; a.col = g->col; a.deg = g->deg; a.cps = g->cps; a.npos = g->npos; a.bt = g->bt;
+    a.bt_off = g->bt_off; a.seeds = d_seeds; a.n = n; a.depth = depth; a.fanout = static_cast<int32_t*>(pf);
+    a.theta = ff ? static_cast<uint64_t>(std::floor(b.pf * 4294967296.0)) : 0;
+    a.base = static_cast<uint32_t>(base);
+    a.key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+    a.a_max = b.a_max ? static_cast<uint32_t>(b.a_max) : 64u;
+    a.ecap = ecap;
+    a.s_src = static_cast<uint32_t*>(ps); a.s_dst = static_cast<uint32_t*>(pd); a.s_dep = static_cast<uint8_t*>(pe);
+    a.cnt = static_cast<uint64_t*>(pk);
+    a.overflow = ovf;
+    a.counters = counters;
+    a.V = g->V;
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((n + FUSED_WARPS - 1) / FUSED_WARPS,
+                                                                                static_cast<uint64_t>(g->num_sms) * 16)));
+    CSAW_TRY(hot_begin(g, st));
+    if (layer) {
+        if (g->cps) k_sample_fused<5><<<grid, FUSED_WARPS * 32, 0, st>>>(a);
+        else k_sample_fused<4><<<grid, FUSED_WARPS * 32, 0, st>>>(a);
+    } else if (ff) {
+        k_sample_fused<3><<<grid, FUSED_WARPS * 32, 0, st>>>(a);
+    } else if (b.kind == CSAW_BIAS_DEGREE) {
+        if (g->cps) k_sample_fused<2><<<grid, FUSED_WARPS * 32, 0, st>>>(a);
+        else k_sample_fused<1><<<grid, FUSED_WARPS * 32, 0, st>>>(a);
+    } else {
+        k_sample_fused<0><<<grid, FUSED_WARPS * 32, 0, st>>>(a);
+    }
+    note_launch();
+    CSAW_CUDA(cudaGetLastError());
+    CSAW_TRY(hot_end(g, st));
+    CSAW_TRY(device_scan(U64Val{a.cnt}, n, ScanToArray{d_offsets}, static_cast<uint64_t*>(pp), st));
+    hbox[0] = 0;
+    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[0], ovf, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[1], d_offsets + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[2], counters, sizeof(uint64_t) * 3, cudaMemcpyDeviceToHost, st));
+    CSAW_CUDA(cudaStreamSynchronize(st));
+    const unsigned flags = static_cast<unsigned>(hbox[0] & 0xFFFFFFFFu);
+    if (flags & 2u) return fail(CSAW_ERR_OUT_OF_RANGE, "a seed vertex is >= num_vertices");
+    if (flags & 1u) return FUSED_FALLBACK;
+    const uint64_t nedges = hbox[1];
+    *num_edges = static_cast<int64_t>(nedges);
+    g->stats.sampled_edges = nedges;
+    g->stats.neighbours_scanned = hbox[2];
+    g->stats.pools = hbox[3];
+    g->stats.cache_probes = hbox[4];
+    if (static_cast<int64_t>(nedges) > capacity) {
+        CSAW_TRY(stats_end(g, st));
+        return fail(CSAW_ERR_CAPACITY, "output capacity " + std::to_string(capacity) + " < required " +
+                                           std::to_string(nedges));
+    }
+    uint32_t *osrc = src, *odst = dst;
+    uint8_t* odep = dep;
+    if (!out_on_device && nedges > 0) {
+        void *p0, *p1, *p2;
+        CSAW_TRY(g->scratch.get(SL_SRC, sizeof(uint32_t) * nedges, &p0));
+        CSAW_TRY(g->scratch.get(SL_DST, sizeof(uint32_t) * nedges, &p1));
+        CSAW_TRY(g->scratch.get(SL_DEP, nedges, &p2));
+        osrc = static_cast<uint32_t*>(p0); odst = static_cast<uint32_t*>(p1); odep = static_cast<uint8_t*>(p2);
+    }
+    if (nedges > 0) {
+        k_fused_copy<<<grid, FUSED_WARPS * 32, 0, st>>>(a.s_src, a.s_dst, a.s_dep, ecap, d_offsets, n, osrc, odst, odep);
+        note_launch();
+        CSAW_CUDA(cudaGetLastError());
+    }
+    CSAW_TRY(stats_end(g, st));
+    if (!out_on_device && nedges > 0) {
+        CSAW_CUDA(cudaMemcpyAsync(src, osrc, sizeof(uint32_t) * nedges, cudaMemcpyDeviceToHost, st));
+        CSAW_CUDA(cudaMemcpyAsync(dst, odst, sizeof(uint32_t) * nedges, cudaMemcpyDeviceToHost, st));
+        CSAW_CUDA(cudaMemcpyAsync(dep, odep, nedges, cudaMemcpyDeviceToHost, st));
+    }
+    CSAW_CUDA(cudaStreamSynchronize(st));
+    return CSAW_OK;
+}
+
 csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
+                       const uint32_t* d_seeds, int64_t n_i64, uint64_t base, uint64_t seed, uint64_t* d_offsets,
+                       uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
+                       bool out_on_device, cudaStream_t st) {
+    if (!g->force_batched) {
+        const csaw_status s = run_sample_fused(g, b, fanout, depth, d_seeds, static_cast<uint64_t>(n_i64), base, seed,
+                                               d_offsets, src, dst, dep, capacity, num_edges, out_on_device, st);
+        if (s != FUSED_FALLBACK) return s;
+    }
+    return run_sample_levels(g, b, fanout, depth, d_seeds, n_i64, base, seed, d_offsets, src, dst, dep, capacity,
+                             num_edges, out_on_device, st);
+}
+
+// Level-synchronous batched driver (general path).
+csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
                        const uint32_t* d_seeds, int64_t n_i64, uint64_t base, uint64_t seed, uint64_t* d_offsets,
                        uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
                        bool out_on_device, cudaStream_t st) {

@@ -475,19 +475,10 @@ struct CpsTree {
     uint32_t d;
     uint64_t boff;
 
-    struct Levels {
-        int K;                 // number of index levels (0 if d <= 32)
-        uint32_t n[8];         // n[0] = d, n[k] = ceil(n[k-1] / 32)
-        uint64_t off[8];       // offset of level k (k >= 1) inside the row's bt segment
-    };
-    __device__ __forceinline__ Levels levels() const {
-        Levels L;
-        L.K = 0;
-        L.n[0] = d;
-        while (L.n[L.K] > 32 && L.K < 7) { L.n[L.K + 1] = (L.n[L.K] + 31) / 32; ++L.K; }
-        uint64_t acc = 0;
-        for (int k = L.K; k >= 1; --k) { L.off[k] = acc; acc += L.n[k]; }
-        return L;
+    // levels: n_k = ceil(d / 32^k) entries at level k; K = first k with n_k <= 32
+    // (closed form, no per-step loop over arrays).
+    __device__ __forceinline__ static int num_levels(uint32_t d) {
+        return d <= 32 ? 0 : (31 - __clz(d - 1)) / 5;   // (bits(d-1) - 1) / 5
     }
     // Warp-collective.  kDraw: x = below(U, T) with T from the top level (returned);
     // else x is given.  Result: CSR index e of the pick, S_s = lo, S_{s+1} = hi, col[e].
@@ -495,35 +486,37 @@ struct CpsTree {
     __device__ __forceinline__ void search(uint64_t U, uint64_t& x, uint64_t& T, uint64_t& e, uint64_t& lo,
                                            uint64_t& hi, uint32_t& item, uint32_t& probes) const {
         const int lane = lane_id();
-        const Levels L = levels();
-        uint64_t j = 0;          // block index at the current level
-        uint64_t left = 0;       // value just left of the current block (S before it)
-        for (int k = L.K; k >= 0; --k) {
-            const uint64_t idx = j * 32 + lane;
-            const bool valid = idx < L.n[k];
+        const int K = num_levels(d);
+        uint32_t j = 0;          // block index at the current level
+        uint64_t left = 0;       // S just left of the current block
+        uint64_t off = 0;        // offset of level k inside the row's bt segment (top level first)
+        for (int k = K; k >= 0; --k) {
+            const uint32_t nk = k == 0 ? d : ((d - 1) >> (5 * k)) + 1;
+            const uint32_t idx = j * 32 + lane;
+            const bool valid = idx < nk;
             uint64_t v = 0;
             uint32_t it = NONE;
             if (valid) {
                 if (k == 0) { v = __ldg(cps + beg + idx); it = __ldg(col + beg + idx); }
-                else v = __ldg(bt + boff + L.off[k] + idx);
+                else v = __ldg(bt + boff + off + idx);
             }
-            probes += static_cast<uint32_t>(min(static_cast<uint64_t>(32), L.n[k] - j * 32));
-            if (kDraw && k == L.K) {   // top level: its last entry is the row total
-                const unsigned vm = __ballot_sync(FULL, valid);
-                T = __shfl_sync(FULL, v, 31 - __clz(vm));
+            probes += min(32u, nk - j * 32);
+            if (kDraw && k == K) {   // top level: its last entry is the row total
+                T = __shfl_sync(FULL, v, nk - 1);
                 if (T == 0) { e = ~0ull; item = NONE; lo = hi = 0; return; }
                 x = below(U, T);
             }
             const unsigned hit = __ballot_sync(FULL, valid && v > x);
             const int f = __ffs(hit) - 1;   // exists for x < T
-            const uint64_t prev = __shfl_sync(FULL, v, f > 0 ? f - 1 : 0);
-            if (f > 0) left = prev;
+            const uint64_t pv = __shfl_sync(FULL, v, f > 0 ? f - 1 : 0);
+            if (f > 0) left = pv;
             if (k == 0) {
-                e = beg + j * 32 + f;
+                e = beg + idx - lane + f;
                 hi = __shfl_sync(FULL, v, f);
                 lo = left;
                 item = __shfl_sync(FULL, it, f);
             }
+            off += nk;
             j = j * 32 + f;
         }
     }

@@ -51,7 +51,7 @@ struct PathWriter {
 // Degree-biased walk over the static-bias CTPS cache (NEXT-1): per step one row_ptr
 // pair, one cache load for T, a 32-ary warp search of the cached prefix, one col
 // load -- O(log32 d) round trips instead of an 8 d-byte rescan.  Bit-identical.
-__global__ void __launch_bounds__(WALK_WARPS * 32) k_walk_cached(WalkArgs a, const uint64_t* __restrict__ cps,
+__global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_cached(WalkArgs a, const uint64_t* __restrict__ cps,
                                                                   const uint64_t* __restrict__ bt,
                                                                   const uint64_t* __restrict__ bt_off) {
     const int lane = lane_id();
@@ -320,7 +320,8 @@ __device__ __forceinline__ bool n2v_find(const uint32_t* __restrict__ big, uint6
             const uint32_t wv = __shfl_sync(FULL, W, k + s - 1);
             if (wv < x) k += s;
         }
-        found = valid && __shfl_sync(FULL, W, k) == x;
+        const uint32_t wk = __shfl_sync(FULL, W, k);   // all lanes shuffle (no short-circuit)
+        found = valid && wk == x;
         idx = lo + k;
     } else {
         uint64_t l = lo, h = hi;
