@@ -72,6 +72,9 @@ typedef struct {
     double pf;          /* forest-fire burning probability, in [0, 1) */
     int32_t pool_size;  /* MDRW FrontierSize m (2,000), >= 1 */
     int32_t a_max;      /* BRS attempt cap before exact updated sampling (R2); 0 = default 64; even, 2..16382 */
+    int32_t migration;  /* collision migration without replacement (§4.2): 0 = bipartite region search
+                           (the method), 1 = repeated sampling (Fig. 6(a)), 2 = updated sampling
+                           (Fig. 6(b)); 1 and 2 are the paper's baselines, for the Fig. 10-11 ablation */
 } csaw_bias;
 
 /* A CSR graph: row_ptr int64[V+1] (row_ptr[0] = 0, non-decreasing, row_ptr[V] = E),
@@ -138,6 +141,7 @@ typedef struct {
     uint64_t partition_loads;       /* OOM: partition transfers (Fig. 15) */
     uint64_t h2d_bytes;             /* OOM: bytes copied host -> device for partitions */
     uint64_t cache_probes;          /* CTPS-cache entries read by the searches (CSAW_GRAPH_CTPS_CACHE) */
+    uint64_t draws;                 /* random draws consumed by without-replacement selections (Fig. 11) */
     uint64_t kernel_launches;       /* kernels this library launched for the call */
     uint64_t hot_launches;          /* launches of the selection ("hot") kernel */
     double kernel_ms;               /* device time, first launch -> last completion (CUDA events) */

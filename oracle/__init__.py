@@ -48,6 +48,7 @@ def lib():
             "oracle_its": (i64, [P, i64, u64]),
             "oracle_brs_step": (i64, [P, P, i64, i64, u64]),
             "oracle_select_wor": (i64, [P, i64, i64, u64, u32, u32, u32, i32, P, P]),
+            "oracle_set_migration": (None, [i32]),
             "oracle_ff_theta": (u64, [f64]),
             "oracle_ff_burn": (i64, [u64, u32, u32, u32, i64, f64]),
             "oracle_neighbor_sample": (i64, [P, P, i64, i32, P, i32, f64, u32, u32, u64, i32, P, P, P, i64, P]),
@@ -130,6 +131,14 @@ def select_wor(b, k, seed, inst, t, slot, a_max=A_MAX_DEFAULT, with_attempts=Fal
     n = lib().oracle_select_wor(_p(b), b.size, k, seed, inst, t, slot, a_max, _p(picks), _p(att))
     r = [int(x) for x in picks[:n]]
     return (r, int(att[0])) if with_attempts else r
+
+
+MIGRATION = {"brs": 0, "repeated": 1, "updated": 2}
+
+
+def set_migration(mode) -> None:
+    """Collision-migration mode of every later selection in this process (0 BRS, 1 repeated, 2 updated)."""
+    lib().oracle_set_migration(MIGRATION[mode] if isinstance(mode, str) else int(mode))
 
 
 def ff_theta(pf: float) -> int:

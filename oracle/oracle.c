@@ -152,6 +152,46 @@ ORACLE_EXPORT int64_t oracle_brs_step(const uint64_t *S, const uint32_t *b, int6
  * If k >= #positive-bias candidates: all of them, ascending (R8).
  * attempts_out (nullable) accumulates the number of draws used.
  */
+/* Collision migration mode (§4.2): 0 = bipartite region search (the method),
+ * 1 = repeated sampling (Fig. 6(a)), 2 = updated sampling (Fig. 6(b),
+ * P:508-511).  The baselines exist for the Fig. 10-11 ablation. Single-threaded
+ * oracle: a process-wide setting. */
+static int g_migration = 0;
+ORACLE_EXPORT void oracle_set_migration(int32_t mode) { g_migration = mode; }
+
+/* Exact updated sampling (Fig. 6(b)): rebuild the CTPS over the positive-bias,
+ * untaken candidates (ascending) and search it with U. */
+static int64_t updated_pick(const uint32_t *b, int64_t n, const int64_t *picks, int64_t taken, uint64_t U)
+{
+    int64_t nsv = 0;
+    int64_t *sv = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    uint32_t *b2 = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; i++)
+        if (b[i] > 0 && !in_list(picks, taken, i)) { sv[nsv] = i; b2[nsv] = b[i]; nsv++; }
+    uint64_t *S2 = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(nsv + 1));
+    oracle_prefix(b2, nsv, S2);
+    int64_t s = sv[oracle_its(S2, nsv, oracle_below(U, S2[nsv]))];
+    free(S2); free(b2); free(sv);
+    return s;
+}
+
+/*
+ * select_wor: k distinct picks from b[0..n), in pick order j = 0..k-1.
+ * Returns the number of picks.  Sequential semantics: pick j sees picks < j
+ * (R3).  Steps (mode 0, bipartite region search):
+ *   (1)(2) s = its(S, below(U(j,a), T)); accept if not taken
+ *   (3)    fresh x' = below(U(j,a+1), T - b[s]) over the space with the
+ *          taken region [S[s], S[s+1]) removed (R1 fresh draw, Theorem 2)
+ *   (4)(5) y = x' if x' < S[s] (left part (0,l)) else x' + b[s] (right part
+ *          (h,1), "r + delta"); s = its(S, y); accept if not taken, else
+ *          back to (1)
+ *   after a_max attempts: exact updated sampling (Fig. 6(b)) over
+ *   the untaken positive-bias candidates with draw U(j, a_max) (R2).
+ * Mode 1 (repeated sampling): redraw (1)(2) until untaken, same cap.
+ * Mode 2 (updated sampling): every pick is updated sampling with U(j, 0).
+ * If k >= #positive-bias candidates: all of them, ascending (R8).
+ * attempts_out (nullable) accumulates the number of draws used.
+ */
 ORACLE_EXPORT int64_t oracle_select_wor(const uint32_t *b, int64_t n, int64_t k,
                                         uint64_t seed, uint32_t inst, uint32_t t, uint32_t slot,
                                         int32_t a_max, int64_t *picks, int64_t *attempts_out)
@@ -171,28 +211,26 @@ ORACLE_EXPORT int64_t oracle_select_wor(const uint32_t *b, int64_t n, int64_t k,
     for (int64_t j = 0; j < k; j++) {
         uint32_t a = 0;
         int64_t s;
-        for (;;) {
-            s = oracle_its(S, n, oracle_below(draw_u64(seed, inst, t, slot, word3_of(P_EDGE, (uint32_t)j, a), 0), T));
-            a += 1;
-            if (!in_list(picks, taken, s)) break;
-            uint64_t x2 = oracle_below(draw_u64(seed, inst, t, slot, word3_of(P_EDGE, (uint32_t)j, a), 0), T - (uint64_t)b[s]);
-            a += 1;
-            s = oracle_brs_step(S, b, n, s, x2);
-            if (!in_list(picks, taken, s)) break;
-            if ((int32_t)a >= a_max) {
-                /* updated sampling: survivors sv = positive-bias, untaken, ascending */
-                int64_t nsv = 0;
-                int64_t *sv = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
-                uint32_t *b2 = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)n);
-                for (int64_t i = 0; i < n; i++)
-                    if (b[i] > 0 && !in_list(picks, taken, i)) { sv[nsv] = i; b2[nsv] = b[i]; nsv++; }
-                uint64_t *S2 = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(nsv + 1));
-                oracle_prefix(b2, nsv, S2);
-                uint64_t x = oracle_below(draw_u64(seed, inst, t, slot, word3_of(P_EDGE, (uint32_t)j, (uint32_t)a_max), 0), S2[nsv]);
-                s = sv[oracle_its(S2, nsv, x)];
+        if (g_migration == 2) {
+            s = updated_pick(b, n, picks, taken, draw_u64(seed, inst, t, slot, word3_of(P_EDGE, (uint32_t)j, 0), 0));
+            a = 1;
+        } else {
+            for (;;) {
+                s = oracle_its(S, n, oracle_below(draw_u64(seed, inst, t, slot, word3_of(P_EDGE, (uint32_t)j, a), 0), T));
                 a += 1;
-                free(S2); free(b2); free(sv);
-                break;
+                if (!in_list(picks, taken, s)) break;
+                if (g_migration == 0) {
+                    uint64_t x2 = oracle_below(draw_u64(seed, inst, t, slot, word3_of(P_EDGE, (uint32_t)j, a), 0), T - (uint64_t)b[s]);
+                    a += 1;
+                    s = oracle_brs_step(S, b, n, s, x2);
+                    if (!in_list(picks, taken, s)) break;
+                }
+                if ((int32_t)a >= a_max) {
+                    s = updated_pick(b, n, picks, taken,
+                                     draw_u64(seed, inst, t, slot, word3_of(P_EDGE, (uint32_t)j, (uint32_t)a_max), 0));
+                    a += 1;
+                    break;
+                }
             }
         }
         if (attempts_out) *attempts_out += a;

@@ -46,9 +46,13 @@ def _stream_ptr(stream) -> int:
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
-def make_bias(kind, p=1.0, q=1.0, pf=0.0, pool_size=0, a_max=0) -> csaw_bias:
+MIGRATION = {"brs": 0, "repeated": 1, "updated": 2}
+
+
+def make_bias(kind, p=1.0, q=1.0, pf=0.0, pool_size=0, a_max=0, migration="brs") -> csaw_bias:
     k = BIAS[kind] if isinstance(kind, str) else int(kind)
-    return csaw_bias(k, float(p), float(q), float(pf), int(pool_size), int(a_max))
+    mig = MIGRATION[migration] if isinstance(migration, str) else int(migration)
+    return csaw_bias(k, float(p), float(q), float(pf), int(pool_size), int(a_max), mig)
 
 
 class Graph:

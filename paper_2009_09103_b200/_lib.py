@@ -54,7 +54,7 @@ BIAS = {"uniform": 0, "degree": 1, "node2vec": 2, "forest_fire": 3, "layer": 4, 
 
 class csaw_bias(C.Structure):
     _fields_ = [("kind", C.c_int32), ("p", C.c_double), ("q", C.c_double), ("pf", C.c_double),
-                ("pool_size", C.c_int32), ("a_max", C.c_int32)]
+                ("pool_size", C.c_int32), ("a_max", C.c_int32), ("migration", C.c_int32)]
 
 
 class csaw_csr(C.Structure):
@@ -76,7 +76,8 @@ class csaw_graph_info_t(C.Structure):
 
 class csaw_run_stats(C.Structure):
     _fields_ = [("sampled_edges", C.c_uint64), ("pools", C.c_uint64), ("neighbours_scanned", C.c_uint64),
-                ("partition_loads", C.c_uint64), ("h2d_bytes", C.c_uint64), ("cache_probes", C.c_uint64), ("kernel_launches", C.c_uint64),
+                ("partition_loads", C.c_uint64), ("h2d_bytes", C.c_uint64), ("cache_probes", C.c_uint64), ("draws", C.c_uint64),
+                ("kernel_launches", C.c_uint64),
                 ("hot_launches", C.c_uint64), ("kernel_ms", C.c_double), ("hot_kernel_ms", C.c_double),
                 ("transfer_ms", C.c_double)]
 

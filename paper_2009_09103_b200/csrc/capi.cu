@@ -509,6 +509,7 @@ CSAW_API csaw_status csaw_sample_capacity(const csaw_bias* bias, const int32_t* 
 static csaw_status check_bias(const csaw_bias* b) {
     if (!b) return fail(CSAW_ERR_INVALID_ARG, "bias is NULL");
     if (b->kind < CSAW_BIAS_UNIFORM || b->kind > CSAW_BIAS_MDRW) return fail(CSAW_ERR_INVALID_ARG, "unknown bias kind");
+    if (b->migration < 0 || b->migration > 2) return fail(CSAW_ERR_INVALID_ARG, "migration must be 0, 1 or 2");
     if (b->a_max != 0 && (b->a_max < 2 || b->a_max > 16382 || (b->a_max & 1)))
         return fail(CSAW_ERR_INVALID_ARG, "a_max must be 0 (default 64) or even in [2, 16382]");
     return CSAW_OK;

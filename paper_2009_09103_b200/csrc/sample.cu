@@ -122,11 +122,12 @@ struct SelArgs {
     uint32_t a_max;
     PickRec* glist;
     uint32_t kmax;
-    unsigned long long* counters;   // [0] scanned, [1] pools, [2] cache probes
+    unsigned long long* counters;   // [0] scanned, [1] pools, [2] cache probes, [3] draws
     const uint64_t* __restrict__ cps;    // static-bias CTPS cache (nullptr if not built)
     const uint32_t* __restrict__ npos;
     const uint64_t* __restrict__ bt;
     const uint64_t* __restrict__ bt_off;
+    uint32_t mode;                   // collision migration (MIGRATE_*)
 };
 
 // Neighbor sampling / forest fire: one warp per queue entry.
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_ns_select(SelArgs a) {
     uint32_t* bm = bm_all[wib];
     const int lane = lane_id();
     PickRec* gl = a.glist ? a.glist + global_warp_id() * a.kmax : nullptr;
-    unsigned long long scanned = 0, pools = 0, probes = 0;
+    unsigned long long scanned = 0, pools = 0, probes = 0, draws = 0;
     for (uint64_t q = global_warp_id(); q < a.nq; q += total_warps()) {
         const uint32_t v = a.qv[q];
         const uint32_t inst = a.qi[q];
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_ns_select(SelArgs a) {
         const uint32_t k = a.kq[q];
         const uint64_t e0 = a.eoff[q];
         const uint32_t ub = a.ub[q];
-        DrawKey dk{a.key, a.base + inst, a.d, v};
+        DrawKey dk{a.key, a.base + inst, a.d, v, a.mode, 0};
         StageEmit<int> emit{a.s_inst, a.s_src, a.s_dst, e0, inst, v};
         uint32_t cnt = 0;
         if (n > 0 && k > 0) {
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_ns_select(SelArgs a) {
                 cnt = select_wor(P, C, tab, bm, k, dk, a.a_max, gl, emit);
             }
             ++pools;
+            draws += dk.draws;
         }
         for (uint32_t r = cnt + lane; r < ub; r += 32) {
             a.s_inst[e0 + r] = inst;
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_ns_select(SelArgs a) {
         if (scanned) atomicAdd(a.counters + 0, scanned);
         if (pools) atomicAdd(a.counters + 1, pools);
         if (probes) atomicAdd(a.counters + 2, probes);
+        if (draws) atomicAdd(a.counters + 3, draws);
     }
 }
 
@@ -382,6 +385,7 @@ struct LayerArgs {
     const uint32_t* __restrict__ npos;
     const uint64_t* __restrict__ bt;
     const uint64_t* __restrict__ bt_off;
+    uint32_t mode;
 };
 
 // one warp per instance (its layer pool); kCache: union CTPS from the static-bias cache
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_layer_select(LayerArgs a)
     uint32_t* bm = bm_all[wib];
     const int lane = lane_id();
     PickRec* gl = a.glist ? a.glist + global_warp_id() * a.kmax : nullptr;
-    unsigned long long scanned = 0, pools = 0, probes = 0;
+    unsigned long long scanned = 0, pools = 0, probes = 0, draws = 0;
     for (uint64_t i = global_warp_id(); i < a.n; i += total_warps()) {
         const uint64_t qb = a.inst_off[i], qe = a.inst_off[i + 1];
         const uint64_t e0 = a.eoff[i];
@@ -409,13 +413,14 @@ __global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_layer_select(LayerArgs a)
             P.pbase = a.qpref[qb];
             P.nf = static_cast<uint32_t>(qe - qb);
             P.n = static_cast<uint32_t>(a.qpref[qe] - P.pbase);
-            DrawKey dk{a.key, a.base + static_cast<uint32_t>(i), a.d, NONE};
+            DrawKey dk{a.key, a.base + static_cast<uint32_t>(i), a.d, NONE, a.mode, 0};
             LayerEmit<LayerPoolT<kCache>> emit{&P, a.s_inst, a.s_src, a.s_dst, e0, static_cast<uint32_t>(i)};
             const Ctps C = build_ctps(P, tab);
             cnt = select_wor(P, C, tab, bm, a.fanout, dk, a.a_max, gl, emit);
             if (!kCache) scanned += P.n;
             probes += P.probes;
             ++pools;
+            draws += dk.draws;
         }
         for (uint32_t r = cnt + lane; r < ub; r += 32) {
             a.s_inst[e0 + r] = static_cast<uint32_t>(i);
@@ -427,6 +432,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_layer_select(LayerArgs a)
         if (scanned) atomicAdd(a.counters + 0, scanned);
         if (pools) atomicAdd(a.counters + 1, pools);
         if (probes) atomicAdd(a.counters + 2, probes);
+        if (draws) atomicAdd(a.counters + 3, draws);
     }
 }
 
@@ -675,6 +681,7 @@ struct FusedArgs {
     unsigned* overflow;                   // bit 0: fall back to the batched driver; bit 1: seed out of range
     unsigned long long* counters;
     int64_t V;
+    uint32_t mode;
 };
 
 struct FusedEmit {
@@ -725,7 +732,7 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, 4) k_sample_fused(FusedArgs 
     uint64_t* PF = PF_all[wib];
     const int lane = lane_id();
     constexpr bool kLayer = kMode >= 4;
-    unsigned long long scanned = 0, pools = 0, probes = 0;
+    unsigned long long scanned = 0, pools = 0, probes = 0, draws = 0;
     for (uint64_t i = global_warp_id(); i < a.n; i += total_warps()) {
         const uint32_t inst = a.base + static_cast<uint32_t>(i);
         const uint32_t seed = a.seeds[i];
@@ -762,7 +769,7 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, 4) k_sample_fused(FusedArgs 
                     P.rp = a.rp; P.col = a.col; P.deg = a.deg; P.cps = a.cps; P.npos = a.npos; P.probes = 0;
                     P.bt = a.bt; P.bt_off = a.bt_off;
                     P.fv = F; P.pref = PF; P.pbase = 0; P.nf = nf; P.n = pn;
-                    DrawKey dk{a.key, inst, static_cast<uint32_t>(d), NONE};
+                    DrawKey dk{a.key, inst, static_cast<uint32_t>(d), NONE, a.mode, 0};
                     FusedLayerEmit<LayerPoolT<kMode == 5>> emit{&P, a.s_src, a.s_dst, a.s_dep, e_base + ec,
                                                                  static_cast<uint8_t>(d + 1)};
                     const Ctps C = build_ctps(P, tab);
@@ -770,6 +777,7 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, 4) k_sample_fused(FusedArgs 
                     if (kMode == 4) scanned += pn;
                     probes += P.probes;
                     ++pools;
+            draws += dk.draws;
                 }
             } else {
                 for (uint32_t fj = 0; fj < nf && !ovf; ++fj) {
@@ -781,7 +789,7 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, 4) k_sample_fused(FusedArgs 
                     else k = static_cast<uint32_t>(a.fanout[d]);
                     if (nd == 0 || k == 0) continue;
                     if (k > 32 || ec + min(k, nd) > a.ecap) { ovf = true; break; }
-                    DrawKey dk{a.key, inst, static_cast<uint32_t>(d), v};
+                    DrawKey dk{a.key, inst, static_cast<uint32_t>(d), v, a.mode, 0};
                     FusedEmit emit{a.s_src, a.s_dst, a.s_dep, e_base + ec, v, static_cast<uint8_t>(d + 1)};
                     uint32_t c;
                     if constexpr (kMode == 2) {
@@ -802,6 +810,7 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, 4) k_sample_fused(FusedArgs 
                     }
                     ec += c;
                     ++pools;
+            draws += dk.draws;
                 }
                 if (ovf) break;
             }
@@ -864,6 +873,7 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, 4) k_sample_fused(FusedArgs 
         if (scanned) atomicAdd(a.counters + 0, scanned);
         if (pools) atomicAdd(a.counters + 1, pools);
         if (probes) atomicAdd(a.counters + 2, probes);
+        if (draws) atomicAdd(a.counters + 3, draws);
     }
 }
 
@@ -955,6 +965,7 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     a.overflow = ovf;
     a.counters = counters;
     a.V = g->V;
+    a.mode = static_cast<uint32_t>(b.migration);
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((n + FUSED_WARPS - 1) / FUSED_WARPS,
                                                                                 static_cast<uint64_t>(g->num_sms) * 16)));
     CSAW_TRY(hot_begin(g, st));
@@ -976,7 +987,7 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     hbox[0] = 0;
     CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[0], ovf, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[1], d_offsets + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[2], counters, sizeof(uint64_t) * 3, cudaMemcpyDeviceToHost, st));
+    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[2], counters, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost, st));
     CSAW_CUDA(cudaStreamSynchronize(st));
     const unsigned flags = static_cast<unsigned>(hbox[0] & 0xFFFFFFFFu);
     if (flags & 2u) return fail(CSAW_ERR_OUT_OF_RANGE, "a seed vertex is >= num_vertices");
@@ -987,6 +998,7 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     g->stats.neighbours_scanned = hbox[2];
     g->stats.pools = hbox[3];
     g->stats.cache_probes = hbox[4];
+    g->stats.draws = hbox[5];
     if (static_cast<int64_t>(nedges) > capacity) {
         CSAW_TRY(stats_end(g, st));
         return fail(CSAW_ERR_CAPACITY, "output capacity " + std::to_string(capacity) + " < required " +
@@ -1149,13 +1161,13 @@ csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int
             if (layer) {
                 LayerArgs la{g->row_ptr, g->col, g->deg, qv, inst_off, qpref, n, fan, ub, eoff, s_inst, s_src, s_dst,
                              static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters,
-                             g->cps, g->npos, g->bt, g->bt_off};
+                             g->cps, g->npos, g->bt, g->bt_off, static_cast<uint32_t>(b.migration)};
                 if (g->cps) k_layer_select<true><<<sgrid, SEL_WARPS * 32, 0, st>>>(la);
                 else k_layer_select<false><<<sgrid, SEL_WARPS * 32, 0, st>>>(la);
             } else {
                 SelArgs sa{g->row_ptr, g->col, g->deg, qv, qi, nq, kq, ub, eoff, s_inst, s_src, s_dst,
                            static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters,
-                           g->cps, g->npos, g->bt, g->bt_off};
+                           g->cps, g->npos, g->bt, g->bt_off, static_cast<uint32_t>(b.migration)};
                 if (degree_bias && g->cps) k_ns_select<2><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
                 else if (degree_bias) k_ns_select<1><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
                 else k_ns_select<0><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
@@ -1238,7 +1250,7 @@ csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int
     if (n > 0) { k_counts<<<grid_for(g, n), 256, 0, st>>>(dlev, depth, n, tot); note_launch(); }
     CSAW_TRY(device_scan(U64Val{tot}, n, ScanToArray{d_offsets}, part, st));
     CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[4], d_offsets + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[5], counters, sizeof(uint64_t) * 3, cudaMemcpyDeviceToHost, st));
+    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[5], counters, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost, st));
     CSAW_CUDA(cudaStreamSynchronize(st));
     const uint64_t nedges = hbox[4];
     *num_edges = static_cast<int64_t>(nedges);
@@ -1246,6 +1258,7 @@ csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int
     g->stats.neighbours_scanned = hbox[5];
     g->stats.pools = hbox[6];
     g->stats.cache_probes = hbox[7];
+    g->stats.draws = hbox[8];
     if (static_cast<int64_t>(nedges) > capacity) {
         CSAW_TRY(stats_end(g, st));
         return fail(CSAW_ERR_CAPACITY, "output capacity " + std::to_string(capacity) + " < required " +

@@ -203,11 +203,18 @@ __device__ __forceinline__ uint32_t select_wr(Pool& P, const Ctps& C, const uint
 }
 
 // ---------------------------------------------------------------- selection without replacement
+// Collision migration (§4.2): BRS is the method; the naive baselines of Fig. 6(a)
+// (repeated sampling) and Fig. 6(b) (updated sampling) exist for the ablation
+// of Fig. 10-11.
+enum : uint32_t { MIGRATE_BRS = 0, MIGRATE_REPEATED = 1, MIGRATE_UPDATED = 2 };
+
 struct DrawKey {
     uint2 key;       // Philox key (rng_seed)
     uint32_t inst;   // global instance id
     uint32_t t;      // depth
     uint32_t slot;   // frontier vertex id / 0xFFFFFFFF (layer pool)
+    uint32_t mode;   // MIGRATE_*
+    uint32_t draws;  // accumulated number of draws (statistics, Fig. 11 "#iterations")
 };
 
 __device__ __forceinline__ uint64_t wor_draw(const DrawKey& dk, uint32_t j, uint32_t a) {
@@ -226,7 +233,7 @@ __device__ __forceinline__ bool bm_test(const uint32_t* bm, uint32_t s) {
 // glist: per-warp global scratch of >= k PickRecs, used only when k > 32.
 template <class Pool, class Emit>
 __device__ uint32_t select_wor(Pool& P, const Ctps& C, uint64_t* __restrict__ tab, uint32_t* __restrict__ bm,
-                               uint32_t k, const DrawKey& dk, uint32_t a_max, PickRec* __restrict__ glist,
+                               uint32_t k, DrawKey& dk, uint32_t a_max, PickRec* __restrict__ glist,
                                Emit&& emit) {
     const int lane = lane_id();
     const uint32_t n = C.n;
@@ -291,19 +298,25 @@ __device__ uint32_t select_wor(Pool& P, const Ctps& C, uint64_t* __restrict__ ta
         // ---- attempt 0 for every lane of the pass (one lane per pick)
         Region reg;
         reg.s = NONE; reg.b = 0; reg.lo = 0; reg.item = NONE;
-        const uint64_t x0 = below(wor_draw(dk, j0 + lane, 0), T);
-        if constexpr (Pool::kClosedForm) {
-            reg.s = static_cast<uint32_t>(x0); reg.lo = x0; reg.b = 1;
-        } else if (C.m == 0) {
-            if (static_cast<uint32_t>(lane) < kp) reg = its_table(tab, n, x0);
-        } else {
-            for (uint32_t l = 0; l < kp; ++l) {
-                const uint64_t xl = __shfl_sync(FULL, x0, l);
-                const Region rl = its_uniform(P, C, tab, xl);
-                if (static_cast<uint32_t>(lane) == l) reg = rl;
+        const bool updated_mode = dk.mode == MIGRATE_UPDATED;
+        if (!updated_mode) {
+            const uint64_t x0 = below(wor_draw(dk, j0 + lane, 0), T);
+            dk.draws += kp;
+            if constexpr (Pool::kClosedForm) {
+                reg.s = static_cast<uint32_t>(x0); reg.lo = x0; reg.b = 1;
+            } else if (C.m == 0) {
+                if (static_cast<uint32_t>(lane) < kp) reg = its_table(tab, n, x0);
+            } else {
+                for (uint32_t l = 0; l < kp; ++l) {
+                    const uint64_t xl = __shfl_sync(FULL, x0, l);
+                    const Region rl = its_uniform(P, C, tab, xl);
+                    if (static_cast<uint32_t>(lane) == l) reg = rl;
+                }
             }
         }
-        uint32_t cand = (static_cast<uint32_t>(lane) < kp) ? reg.s : NONE;
+        // updated sampling: no independent attempt-0 candidates (every pick depends
+        // on the survivors), so every lane resolves serially below
+        uint32_t cand = (static_cast<uint32_t>(lane) < kp && !updated_mode) ? reg.s : NONE;
         fin = NONE; fin_b = 0; fin_lo = 0;
 
         uint32_t r = 0;   // lanes [0, r) are final
@@ -312,8 +325,8 @@ __device__ uint32_t select_wor(Pool& P, const Ctps& C, uint64_t* __restrict__ ta
             const uint32_t v = static_cast<uint32_t>(lane) < r ? fin : (active ? cand : (NONE - lane));
             const unsigned peers = __match_any_sync(FULL, v);
             const unsigned below_r = (r >= 32) ? FULL : ((1u << r) - 1u);
-            bool bad = false;
-            if (active) {
+            bool bad = updated_mode && active;
+            if (active && !updated_mode) {
                 bad = (peers & below_r) != 0                          // equals a final of this pass
                       || (peers & lanemask_lt() & ~below_r) != 0      // same candidate as an earlier open lane
                       || taken_prev(cand);                            // taken in an earlier pass
@@ -338,39 +351,55 @@ __device__ uint32_t select_wor(Pool& P, const Ctps& C, uint64_t* __restrict__ ta
                 if (__ballot_sync(FULL, static_cast<uint32_t>(lane) < rr && fin == q)) return true;
                 return taken_prev(q);
             };
+            // exact updated sampling over the survivors (Fig. 6(b)) with draw U(jr, aidx):
+            // survivor position xs, mapped back to the original CTPS by skipping the
+            // taken regions (least fixpoint of y = xs + sum{b_q : taken q, S_q <= y})
+            auto updated_pick = [&](uint32_t aidx) -> Region {
+                uint64_t tmass = warp_sum(static_cast<uint32_t>(lane) < rr ? fin_b : 0u);
+                for (uint32_t q = 0; q < nprev; ++q) tmass += glist[q].b;
+                const uint64_t xs = below(wor_draw(dk, jr, aidx), T - tmass);
+                uint64_t yy = xs;
+                for (;;) {
+                    uint64_t add = warp_sum((static_cast<uint32_t>(lane) < rr && fin_lo <= yy) ? fin_b : 0u);
+                    for (uint32_t q = 0; q < nprev; ++q)
+                        if (glist[q].lo <= yy) add += glist[q].b;
+                    const uint64_t ny = xs + add;
+                    if (ny == yy) break;
+                    yy = ny;
+                }
+                return its_uniform(P, C, tab, yy);
+            };
             Region res;
             uint32_t a = 1;
-            for (;;) {
-                // (3) fresh draw over the space without [S_s, S_s + b_s); (4)/(5) map back
-                const uint64_t x2 = below(wor_draw(dk, jr, a), T - sb);
-                ++a;
-                const uint64_t y = (x2 < slo) ? x2 : x2 + sb;
-                res = its_uniform(P, C, tab, y);
-                if (!taken(res.s)) break;
-                if (a >= a_max) {
-                    // exact updated sampling over the survivors (Fig. 6(b); R2)
-                    uint64_t tmass = warp_sum(static_cast<uint32_t>(lane) < rr ? fin_b : 0u);
-                    for (uint32_t q = 0; q < nprev; ++q) tmass += glist[q].b;
-                    const uint64_t xs = below(wor_draw(dk, jr, a_max), T - tmass);
-                    uint64_t yy = xs;
-                    for (;;) {   // least fixpoint of y = xs + sum{b_q : taken q with S_q <= y}
-                        uint64_t add = warp_sum((static_cast<uint32_t>(lane) < rr && fin_lo <= yy) ? fin_b : 0u);
-                        for (uint32_t q = 0; q < nprev; ++q)
-                            if (glist[q].lo <= yy) add += glist[q].b;
-                        const uint64_t ny = xs + add;
-                        if (ny == yy) break;
-                        yy = ny;
-                    }
-                    res = its_uniform(P, C, tab, yy);
-                    break;
+            if (updated_mode) {
+                res = updated_pick(0);
+            } else if (dk.mode == MIGRATE_REPEATED) {
+                // Fig. 6(a): redraw over the original CTPS until an untaken region is hit
+                for (;;) {
+                    if (a >= a_max) { res = updated_pick(a_max); ++a; break; }
+                    const uint64_t x = below(wor_draw(dk, jr, a), T);
+                    ++a;
+                    res = its_uniform(P, C, tab, x);
+                    if (!taken(res.s)) break;
                 }
-                // (1)(2) plain draw over [0, T)
-                const uint64_t x = below(wor_draw(dk, jr, a), T);
-                ++a;
-                res = its_uniform(P, C, tab, x);
-                if (!taken(res.s)) break;
-                s = res.s; sb = res.b; slo = res.lo;
+            } else {
+                for (;;) {
+                    // (3) fresh draw over the space without [S_s, S_s + b_s); (4)/(5) map back
+                    const uint64_t x2 = below(wor_draw(dk, jr, a), T - sb);
+                    ++a;
+                    const uint64_t y = (x2 < slo) ? x2 : x2 + sb;
+                    res = its_uniform(P, C, tab, y);
+                    if (!taken(res.s)) break;
+                    if (a >= a_max) { res = updated_pick(a_max); ++a; break; }   // R2
+                    // (1)(2) plain draw over [0, T)
+                    const uint64_t x = below(wor_draw(dk, jr, a), T);
+                    ++a;
+                    res = its_uniform(P, C, tab, x);
+                    if (!taken(res.s)) break;
+                    s = res.s; sb = res.b; slo = res.lo;
+                }
             }
+            dk.draws += updated_mode ? 1u : a - 1u;
             if (static_cast<uint32_t>(lane) == r) {
                 fin = res.s; fin_b = res.b; fin_lo = res.lo;
                 cand = res.s;

@@ -24,18 +24,29 @@ def graph_pair(row_ptr, col):
 
 
 def check_sample(G, og, workload, seeds, fanout=(), depth=None, rng_seed=1, instance_base=0, pf=0.0,
-                 a_max=0, instances=None):
+                 a_max=0, instances=None, migration="brs"):
     """Run csaw_sample and compare every instance (or `instances`) with the oracle, element by element."""
     depth = len(fanout) if depth is None else depth
     kind = {"degree": "degree", "uniform": "uniform", "forest_fire": "forest_fire", "layer": "layer"}[workload]
     seeds_t = torch.as_tensor(np.asarray(seeds).astype(np.uint32).view(np.int32)).to(DEV)
-    b = cs.make_bias(kind, pf=pf, a_max=a_max)
+    b = cs.make_bias(kind, pf=pf, a_max=a_max, migration=migration)
     offs, src, dst, dep = cs.csaw_sample(G, b, seeds_t, fanout=fanout, depth=depth, rng_seed=rng_seed,
                                          instance_base=instance_base)
     offs = offs.cpu().numpy().astype(np.int64)
     src, dst, dep = u32(src), u32(dst), dep.cpu().numpy()
     am = a_max or O.A_MAX_DEFAULT
     ids = range(len(seeds)) if instances is None else instances
+    total = 0
+    O.set_migration(migration)
+    try:
+        total = _compare_instances(og, workload, seeds, fanout, depth, rng_seed, instance_base, pf, am, ids,
+                                   offs, src, dst, dep)
+    finally:
+        O.set_migration("brs")
+    return offs, total
+
+
+def _compare_instances(og, workload, seeds, fanout, depth, rng_seed, instance_base, pf, am, ids, offs, src, dst, dep):
     total = 0
     for i in ids:
         gi = instance_base + i
@@ -50,7 +61,7 @@ def check_sample(G, og, workload, seeds, fanout=(), depth=None, rng_seed=1, inst
         assert np.array_equal(dst[a:bnd], ed), f"instance {i}: dst differs"
         assert np.array_equal(dep[a:bnd], ee), f"instance {i}: depth differs"
         total += es.size
-    return offs, total
+    return total
 
 
 def check_walk(G, og, kind, seeds, length, rng_seed=1, instance_base=0, walkers=None, p=1.0, q=1.0):

@@ -69,3 +69,24 @@ def test_fused_equals_batched_medium(cache):
         assert torch.equal(x, y)
     A.close()
     B.close()
+
+
+@pytest.mark.parametrize("migration", ["repeated", "updated"])
+@pytest.mark.parametrize("batched", [False, True])
+def test_migration_baselines_parity(migration, batched):
+    """NEXT-2 ablation modes (Fig. 6(a)/(b)) are bit-exact with the oracle too."""
+    g = rmat_csr(1024, 16384, 1)
+    rp = g.row_ptr.to(DEV)
+    G = cs.csaw_graph_create(rp, g.col_idx.to(DEV), batched_only=batched)
+    og = O.Graph.from_torch(g)
+    seeds = instance_seeds(g, 300, set_id=6).numpy()
+    check_sample(G, og, "degree", seeds, fanout=[8, 4], rng_seed=3, migration=migration)
+    check_sample(G, og, "layer", seeds, fanout=[4, 3], rng_seed=3, migration=migration)
+    check_sample(G, og, "uniform", seeds, fanout=[40, 3], rng_seed=3, migration=migration, a_max=4)
+    G.close()
+    rp_t, col_t = gtoy()
+    G2 = cs.csaw_graph_create(torch.tensor(rp_t).to(DEV), torch.tensor(col_t.view(np.int32)).to(DEV),
+                              batched_only=batched)
+    check_sample(G2, O.Graph(rp_t, col_t), "degree", np.tile(np.arange(12, dtype=np.uint32), 50), fanout=[3, 2],
+                 rng_seed=5, migration=migration, a_max=2)
+    G2.close()

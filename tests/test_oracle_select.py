@@ -170,3 +170,37 @@ def test_brs_fewer_attempts_than_repeated_sampling():
             exp_rep += p * T / (T - taken)
             taken += b[s]
     assert brs / N < exp_rep
+
+
+@pytest.mark.parametrize("mode", ["repeated", "updated"])
+@pytest.mark.parametrize("b,k", [([3, 6, 2, 2, 2], 3), ([90, 5, 3, 1, 1], 3), ([0, 7, 0, 1, 3, 0, 2], 3)])
+def test_baseline_migrations_have_the_same_law(mode, b, k):
+    """Repeated sampling (Fig. 6(a)) and updated sampling (Fig. 6(b)) are the
+    paper's baselines: same successive-sampling law, different draw usage."""
+    O.set_migration(mode)
+    try:
+        N = 20000
+        counts = {}
+        draws = 0
+        for inst in range(N):
+            picks, att = O.select_wor(b, k, 99, inst, 0, 0, with_attempts=True)
+            assert len(set(picks)) == k
+            counts[tuple(picks)] = counts.get(tuple(picks), 0) + 1
+            draws += att
+        assert chi2_pvalue(counts, successive_probs(b, k), N) > 1e-4
+        if mode == "updated":
+            assert draws == N * k          # one draw per pick, never a collision
+    finally:
+        O.set_migration("brs")
+
+
+def test_fig11_direction_brs_vs_repeated():
+    """Fig. 11: BRS reduces the draws per pick vs repeated sampling."""
+    b = [400, 40, 20, 10, 5, 5, 3, 1, 1]
+    k = 4
+    tot = {}
+    for mode in ("brs", "repeated"):
+        O.set_migration(mode)
+        tot[mode] = sum(O.select_wor(b, k, 5, i, 0, 0, with_attempts=True)[1] for i in range(5000))
+    O.set_migration("brs")
+    assert tot["brs"] < tot["repeated"]
