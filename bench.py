@@ -568,11 +568,13 @@ def hot_kernel_name(cfg, cached=False, oom=False):
         return "k_walk_cached" if (cfg.bias == "degree" and cached) else f"k_walk<{cfg.bias}>"
     if cfg.workload == "mdrw":
         return "k_mdrw_oom_part" if oom else "k_mdrw"
-    if cfg.workload == "neighbor":
-        return "k_ns_select<2: cached degree>" if cached else f"k_ns_select<{cfg.bias}>"
-    if cfg.workload == "layer":
-        return "k_layer_select<cached>" if cached else "k_layer_select<scan>"
-    return {"node2vec": "k_node2vec<int>", "forest_fire": "k_ns_select<0: uniform>"}[cfg.workload]
+    if cfg.workload == "node2vec":
+        return "k_node2vec<int>"
+    # sampling: the fused one-warp-per-instance kernel (small per-instance frontiers)
+    mode = {"neighbor": 2 if cached else 1, "forest_fire": 3, "layer": 5 if cached else 4}[cfg.workload]
+    if cfg.workload == "neighbor" and cfg.bias == "uniform":
+        mode = 0
+    return f"k_sample_fused<{mode}>"
 
 
 def load_peaks() -> dict:

@@ -877,9 +877,14 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, 4) k_sample_fused(FusedArgs 
     }
 }
 
+// Compacts the staging rows into the caller's arrays.  Guarded on the device so the
+// host need not wait between the fused kernel and the copy: nothing is written if
+// the fused pass overflowed or the output does not fit `capacity`.
 __global__ void k_fused_copy(const uint32_t* __restrict__ s_src, const uint32_t* __restrict__ s_dst,
                              const uint8_t* __restrict__ s_dep, uint32_t ecap, const uint64_t* __restrict__ offs,
-                             uint64_t n, uint32_t* __restrict__ src, uint32_t* __restrict__ dst, uint8_t* __restrict__ dep) {
+                             uint64_t n, uint32_t* __restrict__ src, uint32_t* __restrict__ dst, uint8_t* __restrict__ dep,
+                             const unsigned* __restrict__ overflow, uint64_t capacity) {
+    if (*overflow != 0 || offs[n] > capacity) return;
     const int lane = lane_id();
     for (uint64_t i = global_warp_id(); i < n; i += total_warps()) {
         const uint64_t o = offs[i], c = offs[i + 1] - o;
@@ -984,6 +989,13 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     CSAW_CUDA(cudaGetLastError());
     CSAW_TRY(hot_end(g, st));
     CSAW_TRY(device_scan(U64Val{a.cnt}, n, ScanToArray{d_offsets}, static_cast<uint64_t*>(pp), st));
+    if (out_on_device && capacity > 0) {   // no host round trip before the copy
+        k_fused_copy<<<grid, FUSED_WARPS * 32, 0, st>>>(a.s_src, a.s_dst, a.s_dep, ecap, d_offsets, n, src, dst, dep, ovf,
+                                                         static_cast<uint64_t>(capacity));
+        note_launch();
+        CSAW_CUDA(cudaGetLastError());
+    }
+    CSAW_TRY(stats_end(g, st));
     hbox[0] = 0;
     CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[0], ovf, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[1], d_offsets + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
@@ -999,32 +1011,26 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     g->stats.pools = hbox[3];
     g->stats.cache_probes = hbox[4];
     g->stats.draws = hbox[5];
-    if (static_cast<int64_t>(nedges) > capacity) {
-        CSAW_TRY(stats_end(g, st));
+    if (static_cast<int64_t>(nedges) > capacity)
         return fail(CSAW_ERR_CAPACITY, "output capacity " + std::to_string(capacity) + " < required " +
                                            std::to_string(nedges));
-    }
-    uint32_t *osrc = src, *odst = dst;
-    uint8_t* odep = dep;
-    if (!out_on_device && nedges > 0) {
+    if (!out_on_device && nedges > 0) {   // host output: compact into scratch, then copy down
         void *p0, *p1, *p2;
         CSAW_TRY(g->scratch.get(SL_SRC, sizeof(uint32_t) * nedges, &p0));
         CSAW_TRY(g->scratch.get(SL_DST, sizeof(uint32_t) * nedges, &p1));
         CSAW_TRY(g->scratch.get(SL_DEP, nedges, &p2));
-        osrc = static_cast<uint32_t*>(p0); odst = static_cast<uint32_t*>(p1); odep = static_cast<uint8_t*>(p2);
-    }
-    if (nedges > 0) {
-        k_fused_copy<<<grid, FUSED_WARPS * 32, 0, st>>>(a.s_src, a.s_dst, a.s_dep, ecap, d_offsets, n, osrc, odst, odep);
+        uint32_t* osrc = static_cast<uint32_t*>(p0);
+        uint32_t* odst = static_cast<uint32_t*>(p1);
+        uint8_t* odep = static_cast<uint8_t*>(p2);
+        k_fused_copy<<<grid, FUSED_WARPS * 32, 0, st>>>(a.s_src, a.s_dst, a.s_dep, ecap, d_offsets, n, osrc, odst, odep,
+                                                         ovf, static_cast<uint64_t>(nedges));
         note_launch();
         CSAW_CUDA(cudaGetLastError());
-    }
-    CSAW_TRY(stats_end(g, st));
-    if (!out_on_device && nedges > 0) {
         CSAW_CUDA(cudaMemcpyAsync(src, osrc, sizeof(uint32_t) * nedges, cudaMemcpyDeviceToHost, st));
         CSAW_CUDA(cudaMemcpyAsync(dst, odst, sizeof(uint32_t) * nedges, cudaMemcpyDeviceToHost, st));
         CSAW_CUDA(cudaMemcpyAsync(dep, odep, nedges, cudaMemcpyDeviceToHost, st));
+        CSAW_CUDA(cudaStreamSynchronize(st));
     }
-    CSAW_CUDA(cudaStreamSynchronize(st));
     return CSAW_OK;
 }
 

@@ -335,7 +335,9 @@ __device__ __forceinline__ bool n2v_find(const uint32_t* __restrict__ big, uint6
     return found;
 }
 
-__device__ bool n2v_implicit_step(Node2vecPool& P, uint32_t* spec, uint64_t U64, uint32_t& out) {
+constexpr uint32_t TILE_N = 512;   // N(prev) tile (u32) in shared memory (reuses the CTPS table)
+
+__device__ bool n2v_implicit_step(Node2vecPool& P, uint32_t* spec, uint32_t* tilebuf, uint64_t U64, uint32_t& out) {
     const int lane = lane_id();
     const uint32_t n = P.n;
     const uint32_t nrows = (n + 31) >> 5;
@@ -344,8 +346,21 @@ __device__ bool n2v_implicit_step(Node2vecPool& P, uint32_t* spec, uint64_t U64,
     bool has_prev = false;
     const uint64_t dv = n, dp = P.np;
     if (dp <= 8 * dv && dv <= 8 * dp) {
-        // balanced sizes: stream N(v) rows against a forward-moving window of N(prev)
-        P.seek(0);
+        // balanced sizes: merge 8-row chunks of N(v) (registers) against 512-entry
+        // tiles of N(prev) staged in shared memory -- coalesced loads, each list read
+        // once, membership by a branch-free binary search in the tile
+        uint32_t* tile = tilebuf;
+        uint64_t bpos = 0;
+        uint32_t tn = 0, tmax = 0;
+        auto load_tile = [&](uint64_t at) {
+            bpos = at;
+            tn = static_cast<uint32_t>(min(static_cast<uint64_t>(TILE_N), dp - at));
+            __syncwarp();
+            for (uint32_t j = lane; j < tn; j += 32) tile[j] = __ldg(P.nprev + at + j);
+            __syncwarp();
+            tmax = tile[tn - 1];
+        };
+        load_tile(0);
         for (uint32_t r0 = 0; r0 < nrows; r0 += U) {
             uint32_t key[U];
 #pragma unroll
@@ -353,12 +368,31 @@ __device__ bool n2v_implicit_step(Node2vecPool& P, uint32_t* spec, uint64_t U64,
                 const uint32_t i = (r0 + u) * 32 + lane;
                 key[u] = (i < n) ? __ldg(P.col + P.beg + i) : NONE;
             }
+            uint32_t open = 0, memmask = 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (key[u] != NONE && key[u] != P.prev) open |= 1u << u;
+            for (;;) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (((open >> u) & 1u) && key[u] <= tmax) {
+                        uint32_t pos = 0;
+#pragma unroll
+                        for (uint32_t st = TILE_N / 2; st > 0; st >>= 1)
+                            if (pos + st <= tn && tile[pos + st - 1] < key[u]) pos += st;
+                        if (pos < tn && tile[pos] == key[u]) memmask |= 1u << u;
+                        open &= ~(1u << u);
+                    }
+                }
+                if (!__any_sync(FULL, open != 0)) break;
+                if (bpos + tn >= dp) break;            // N(prev) exhausted: the rest are not members
+                load_tile(bpos + tn);
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (r0 + u < nrows) {
-                    const bool mem = P.member_row(key[u]);
                     const bool isp = key[u] == P.prev;
-                    const bool sp = key[u] != NONE && (isp || mem);
+                    const bool sp = key[u] != NONE && (isp || ((memmask >> u) & 1u));
                     const unsigned bal = __ballot_sync(FULL, sp);
                     if (sp) {
                         const uint32_t idx = cnt + __popc(bal & lanemask_lt());
@@ -497,7 +531,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 3) k_node2vec(N2vArgs na) {
                             nxt = n2v_float_step(P, na.wf, reinterpret_cast<double*>(tab), U64);
                         } else {
                             P.w[0] = na.wint[0]; P.w[1] = na.wint[1]; P.w[2] = na.wint[2];
-                            if (!n2v_implicit_step(P, spec, U64, nxt)) {
+                            if (!n2v_implicit_step(P, spec, reinterpret_cast<uint32_t*>(tab), U64, nxt)) {
                                 const Ctps C = build_ctps(P, tab);   // > SPEC_CAP common neighbours
                                 nxt = select_wr(P, C, tab, U64);
                             }
