@@ -63,13 +63,17 @@ typedef enum {
     CSAW_BIAS_NODE2VEC = 2,     /* EdgeBias = alpha(prev, u) (R16); walks only */
     CSAW_BIAS_FOREST_FIRE = 3,  /* uniform EdgeBias, per-vertex burn count with P_f (R15); sampling only */
     CSAW_BIAS_LAYER = 4,        /* EdgeBias = deg(u) over the union pool of the frontier (R14); sampling only */
-    CSAW_BIAS_MDRW = 5          /* VertexBias = deg(v), EdgeBias = 1, Update = replace (Fig. 4); walks only */
+    CSAW_BIAS_MDRW = 5,         /* VertexBias = deg(v), EdgeBias = 1, Update = replace (Fig. 4); walks only */
+    /* Table-1 walk variants, uniform proposal u = N(v)[below(U(EDGE), d)]: */
+    CSAW_BIAS_MH = 6,           /* Metropolis-Hastings walk: accept iff below(U(ACCEPT), deg u) < deg v, else stay */
+    CSAW_BIAS_RESTART = 7,      /* walk with restart: with probability pf return to the start vertex */
+    CSAW_BIAS_JUMP = 8          /* walk with jump: with probability pf jump to below(U(TARGET), V) */
 } csaw_bias_kind;
 
 typedef struct {
     int32_t kind;       /* csaw_bias_kind */
     double p, q;        /* node2vec return / in-out parameters, > 0 */
-    double pf;          /* forest-fire burning probability, in [0, 1) */
+    double pf;          /* forest-fire burning probability, or restart / jump probability; in [0, 1) */
     int32_t pool_size;  /* MDRW FrontierSize m (2,000), >= 1 */
     int32_t a_max;      /* BRS attempt cap before exact updated sampling (R2); 0 = default 64; even, 2..16382 */
     int32_t migration;  /* collision migration without replacement (§4.2): 0 = bipartite region search

@@ -55,6 +55,8 @@ def lib():
             "oracle_layer_sample": (i64, [P, P, i64, P, i32, u32, u32, u64, i32, P, P, P, i64, P]),
             "oracle_walk_step": (u32, [P, P, i64, i32, u32, u32, u32, u64]),
             "oracle_walk": (None, [P, P, i64, i32, i32, u32, u32, u64, P]),
+            "oracle_walk_variant_step": (u32, [P, P, i64, i32, f64, u32, u32, u32, u32, u64]),
+            "oracle_walk_variant": (None, [P, P, i64, i32, f64, i32, u32, u32, u64, P]),
             "oracle_n2v_scale": (u32, [f64, f64]),
             "oracle_node2vec_step": (u32, [P, P, i64, f64, f64, u32, u32, u32, u32, u64, P]),
             "oracle_node2vec": (None, [P, P, i64, f64, f64, i32, u32, u32, u64, P, P]),
@@ -191,6 +193,20 @@ def walk(g: Graph, kind, length, s0, inst, rng_seed) -> np.ndarray:
     path = np.zeros(length + 1, dtype=np.uint32)
     lib().oracle_walk(_p(g.row_ptr), _p(g.col), g.V, kind, length, s0, inst, rng_seed, _p(path))
     return path
+
+
+KIND_MH, KIND_RESTART, KIND_JUMP = 6, 7, 8
+
+
+def walk_variant(g: Graph, kind, length, s0, inst, rng_seed, pr=0.0) -> np.ndarray:
+    """Metropolis-Hastings (6), restart (7) or jump (8) walk (Table 1 variants)."""
+    path = np.zeros(length + 1, dtype=np.uint32)
+    lib().oracle_walk_variant(_p(g.row_ptr), _p(g.col), g.V, kind, pr, length, s0, inst, rng_seed, _p(path))
+    return path
+
+
+def walk_variant_step(g: Graph, kind, pr, s0, v, inst, t, rng_seed) -> int:
+    return int(lib().oracle_walk_variant_step(_p(g.row_ptr), _p(g.col), g.V, kind, pr, s0, v, inst, t, rng_seed))
 
 
 def node2vec_step(g: Graph, p, q, prev, v, inst, t, rng_seed):

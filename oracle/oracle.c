@@ -55,7 +55,7 @@ ORACLE_EXPORT void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t
 }
 
 /* Purposes of a draw (R7). */
-enum { P_EDGE = 0, P_VERTEX = 1, P_BURN = 2 };
+enum { P_EDGE = 0, P_VERTEX = 1, P_BURN = 2, P_ACCEPT = 3, P_JUMP = 4, P_TARGET = 5 };
 
 /* U(i, t, slot, word3) = o0 | o1 << 32 of philox((i, t, slot, word3); key(seed)). */
 static uint64_t draw_u64(uint64_t seed, uint32_t i, uint32_t t, uint32_t slot, uint32_t word3, uint32_t *o0_out)
@@ -451,6 +451,54 @@ ORACLE_EXPORT void oracle_walk(const int64_t *row_ptr, const uint32_t *col, int6
         uint32_t v = path[t];
         path[t + 1] = (v == 0xFFFFFFFFu) ? 0xFFFFFFFFu
                                          : oracle_walk_step(row_ptr, col, V, kind, v, inst, (uint32_t)t, rng_seed);
+    }
+}
+
+/*
+ * Table-1 walk variants, one step at v, uniform proposal
+ * u = N(v)[below(U(i,t,0,EDGE), d)] (the simple walk's draw):
+ *   kind 6 Metropolis-Hastings walk: accept u iff
+ *          below(U(i,t,0,ACCEPT), deg u) < deg v  (probability min(1, deg v / deg u)),
+ *          else stay at v;
+ *   kind 7 random walk with restart: with probability pr (o0 of
+ *          U(i,t,0,JUMP) < floor(pr 2^32)) return to the walk's start s0;
+ *   kind 8 random walk with jump: with the same test, jump to the
+ *          vertex below(U(i,t,0,TARGET), V).
+ * A vertex without neighbours ends the walk (R20) unless a restart / jump fires.
+ */
+ORACLE_EXPORT uint32_t oracle_walk_variant_step(const int64_t *row_ptr, const uint32_t *col, int64_t V,
+                                                int32_t kind, double pr, uint32_t s0, uint32_t v,
+                                                uint32_t inst, uint32_t t, uint64_t rng_seed)
+{
+    csr_t g = { row_ptr, col, V };
+    if (kind == 7 || kind == 8) {
+        uint32_t o0;
+        draw_u64(rng_seed, inst, t, 0, word3_of(P_JUMP, 0, 0), &o0);
+        if ((uint64_t)o0 < (uint64_t)floor(pr * 4294967296.0)) {
+            if (kind == 7) return s0;
+            return (uint32_t)oracle_below(draw_u64(rng_seed, inst, t, 0, word3_of(P_TARGET, 0, 0), 0), (uint64_t)V);
+        }
+    }
+    int64_t d = deg_of(&g, v);
+    if (d == 0) return 0xFFFFFFFFu;
+    uint32_t u = col[row_ptr[v] + (int64_t)oracle_below(draw_u64(rng_seed, inst, t, 0, word3_of(P_EDGE, 0, 0), 0), (uint64_t)d)];
+    if (kind == 6) {
+        uint64_t du = (uint64_t)deg_of(&g, u);
+        uint64_t a = oracle_below(draw_u64(rng_seed, inst, t, 0, word3_of(P_ACCEPT, 0, 0), 0), du);
+        if (!(a < (uint64_t)d)) return v;   /* rejected: stay */
+    }
+    return u;
+}
+
+ORACLE_EXPORT void oracle_walk_variant(const int64_t *row_ptr, const uint32_t *col, int64_t V, int32_t kind,
+                                       double pr, int32_t length, uint32_t s0, uint32_t inst, uint64_t rng_seed,
+                                       uint32_t *path)
+{
+    path[0] = s0;
+    for (int32_t t = 0; t < length; t++) {
+        uint32_t v = path[t];
+        path[t + 1] = (v == 0xFFFFFFFFu) ? 0xFFFFFFFFu
+            : oracle_walk_variant_step(row_ptr, col, V, kind, pr, s0, v, inst, (uint32_t)t, rng_seed);
     }
 }
 

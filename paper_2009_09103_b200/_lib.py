@@ -49,7 +49,8 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "OUT_OF_RANGE", 3: "BAD_GRAPH", 4:
 CSAW_OK, CSAW_ERR_CAPACITY = 0, 5
 
 # csaw_bias_kind
-BIAS = {"uniform": 0, "degree": 1, "node2vec": 2, "forest_fire": 3, "layer": 4, "mdrw": 5}
+BIAS = {"uniform": 0, "degree": 1, "node2vec": 2, "forest_fire": 3, "layer": 4, "mdrw": 5, "mh": 6, "restart": 7,
+        "jump": 8}
 
 
 class csaw_bias(C.Structure):

@@ -508,7 +508,7 @@ CSAW_API csaw_status csaw_sample_capacity(const csaw_bias* bias, const int32_t* 
 
 static csaw_status check_bias(const csaw_bias* b) {
     if (!b) return fail(CSAW_ERR_INVALID_ARG, "bias is NULL");
-    if (b->kind < CSAW_BIAS_UNIFORM || b->kind > CSAW_BIAS_MDRW) return fail(CSAW_ERR_INVALID_ARG, "unknown bias kind");
+    if (b->kind < CSAW_BIAS_UNIFORM || b->kind > CSAW_BIAS_JUMP) return fail(CSAW_ERR_INVALID_ARG, "unknown bias kind");
     if (b->migration < 0 || b->migration > 2) return fail(CSAW_ERR_INVALID_ARG, "migration must be 0, 1 or 2");
     if (b->a_max != 0 && (b->a_max < 2 || b->a_max > 16382 || (b->a_max & 1)))
         return fail(CSAW_ERR_INVALID_ARG, "a_max must be 0 (default 64) or even in [2, 16382]");
@@ -526,6 +526,8 @@ CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32
     if (b.kind == CSAW_BIAS_NODE2VEC && !(b.p > 0 && b.q > 0 && std::isfinite(b.p) && std::isfinite(b.q)))
         return fail(CSAW_ERR_INVALID_ARG, "node2vec needs finite p, q > 0");
     if (b.kind == CSAW_BIAS_MDRW && b.pool_size < 1) return fail(CSAW_ERR_INVALID_ARG, "MDRW needs pool_size >= 1");
+    if ((b.kind == CSAW_BIAS_RESTART || b.kind == CSAW_BIAS_JUMP) && !(b.pf >= 0.0 && b.pf < 1.0))
+        return fail(CSAW_ERR_INVALID_ARG, "restart / jump probability (pf) must be in [0, 1)");
     if (instance_base + static_cast<uint64_t>(n) > 0xFFFFFFFFull)
         return fail(CSAW_ERR_INVALID_ARG, "instance ids must fit in 32 bits");
     if (n == 0 || (b.kind != CSAW_BIAS_MDRW && length < 0)) return CSAW_OK;
@@ -576,8 +578,8 @@ CSAW_API csaw_status csaw_sample(const csaw_graph* g, const csaw_bias* bias, con
     CSAW_TRY(begin_call(g));
     CSAW_TRY(check_bias(bias));
     const csaw_bias b = *bias;
-    if (b.kind == CSAW_BIAS_NODE2VEC || b.kind == CSAW_BIAS_MDRW)
-        return fail(CSAW_ERR_INVALID_ARG, "node2vec / MDRW are walk selectors (use csaw_walk)");
+    if (b.kind == CSAW_BIAS_NODE2VEC || b.kind == CSAW_BIAS_MDRW || b.kind >= CSAW_BIAS_MH)
+        return fail(CSAW_ERR_INVALID_ARG, "node2vec / MDRW / MH / restart / jump are walk selectors (use csaw_walk)");
     if (!num_edges) return fail(CSAW_ERR_INVALID_ARG, "num_edges is NULL");
     *num_edges = 0;
     if (depth < 1 || depth > 255) return fail(CSAW_ERR_INVALID_ARG, "depth must be in [1, 255]");

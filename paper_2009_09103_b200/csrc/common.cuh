@@ -14,7 +14,8 @@ constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 
 // Purposes of a draw (counter word 3, bits 28..31).
-enum : uint32_t { PURPOSE_EDGE = 0, PURPOSE_VERTEX = 1, PURPOSE_BURN = 2 };
+enum : uint32_t { PURPOSE_EDGE = 0, PURPOSE_VERTEX = 1, PURPOSE_BURN = 2, PURPOSE_ACCEPT = 3, PURPOSE_JUMP = 4,
+                  PURPOSE_TARGET = 5 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ unsigned lanemask_lt() {

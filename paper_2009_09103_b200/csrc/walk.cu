@@ -128,6 +128,55 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- Table-1 walk variants (NEXT-3)
+// Metropolis-Hastings, restart and jump walks:
+// a uniform proposal u = N(v)[below(U(EDGE), d)] plus one extra keyed draw.
+template <int kKind>   // CSAW_BIAS_MH / RESTART / JUMP
+__global__ void __launch_bounds__(WALK_WARPS * 32) k_walk_variant(WalkArgs a, uint64_t theta, int64_t V) {
+    const int lane = lane_id();
+    unsigned long long steps = 0;
+    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+        const uint32_t s0 = a.seeds[w];
+        uint32_t cur = s0;
+        const uint32_t inst = a.base + static_cast<uint32_t>(w);
+        PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
+        pw.put(0, cur);
+        for (int32_t t = 0; t < a.L; ++t) {
+            uint32_t nxt = NONE;
+            const uint32_t tt = static_cast<uint32_t>(t);
+            if (cur != NONE) {
+                bool jumped = false;
+                if constexpr (kKind == CSAW_BIAS_RESTART || kKind == CSAW_BIAS_JUMP) {
+                    const uint4 o = philox4x32_10(make_uint4(inst, tt, 0u, word3(PURPOSE_JUMP, 0, 0)), a.key);
+                    if (static_cast<uint64_t>(o.x) < theta) {
+                        jumped = true;
+                        if constexpr (kKind == CSAW_BIAS_RESTART) nxt = s0;
+                        else nxt = static_cast<uint32_t>(below(draw_u64(a.key, inst, tt, 0u, word3(PURPOSE_TARGET, 0, 0)),
+                                                               static_cast<uint64_t>(V)));
+                    }
+                }
+                if (!jumped) {
+                    const int64_t b0 = __ldg(a.rp + cur);
+                    const uint32_t d = static_cast<uint32_t>(__ldg(a.rp + cur + 1) - b0);
+                    if (d > 0) {
+                        const uint32_t u = __ldg(a.col + b0 + below(draw_u64(a.key, inst, tt, 0u, word3(PURPOSE_EDGE, 0, 0)), d));
+                        nxt = u;
+                        if constexpr (kKind == CSAW_BIAS_MH) {
+                            const uint32_t du = __ldg(a.deg + u);
+                            const uint64_t acc = below(draw_u64(a.key, inst, tt, 0u, word3(PURPOSE_ACCEPT, 0, 0)), du);
+                            if (!(acc < d)) nxt = cur;   // rejected: stay
+                        }
+                    }
+                }
+                ++steps;
+            }
+            cur = nxt;
+            pw.put(t + 1, cur);
+        }
+    }
+    if (lane == 0 && steps) atomicAdd(a.counters + 1, steps);
+}
+
 // ---------------------------------------------------------------- node2vec
 // EdgeBias of u in N(v) with predecessor prev: class 0 (u == prev, alpha 1/p),
 // class 1 (u in N(prev), alpha 1), class 2 (otherwise, alpha 1/q) -- Grover &
@@ -337,13 +386,15 @@ __device__ __forceinline__ bool n2v_find(const uint32_t* __restrict__ big, uint6
 
 constexpr uint32_t TILE_N = 512;   // N(prev) tile (u32) in shared memory (reuses the CTPS table)
 
-__device__ bool n2v_implicit_step(Node2vecPool& P, uint32_t* spec, uint32_t* tilebuf, uint64_t U64, uint32_t& out) {
+// Enumerates the special positions of N(v) -- prev and the common neighbours with
+// N(prev) -- in ascending order; stores those of rank [skip, skip + SPEC_CAP) in
+// spec[rank - skip] (bit 31 = prev).  Returns the total count.
+__device__ uint32_t n2v_specials(Node2vecPool& P, uint32_t* spec, uint32_t* tilebuf, uint32_t skip, bool& has_prev) {
     const int lane = lane_id();
     const uint32_t n = P.n;
     const uint32_t nrows = (n + 31) >> 5;
-    const uint64_t wp = P.w[0], w1 = P.w[1], wq = P.w[2];
     uint32_t cnt = 0;
-    bool has_prev = false;
+    has_prev = false;
     const uint64_t dv = n, dp = P.np;
     if (dp <= 8 * dv && dv <= 8 * dp) {
         // balanced sizes: merge 8-row chunks of N(v) (registers) against 512-entry
@@ -396,7 +447,7 @@ __device__ bool n2v_implicit_step(Node2vecPool& P, uint32_t* spec, uint32_t* til
                     const unsigned bal = __ballot_sync(FULL, sp);
                     if (sp) {
                         const uint32_t idx = cnt + __popc(bal & lanemask_lt());
-                        if (idx < SPEC_CAP) spec[idx] = ((r0 + u) * 32 + lane) | (isp ? 0x80000000u : 0u);
+                        if (idx >= skip && idx - skip < SPEC_CAP) spec[idx - skip] = ((r0 + u) * 32 + lane) | (isp ? 0x80000000u : 0u);
                     }
                     has_prev |= __any_sync(FULL, isp);
                     cnt += __popc(bal);
@@ -432,16 +483,16 @@ __device__ bool n2v_implicit_step(Node2vecPool& P, uint32_t* spec, uint32_t* til
                     const unsigned bal0 = __ballot_sync(FULL, mem && posA < pp);
                     if (mem && posA < pp) {
                         const uint32_t idx = cnt + __popc(bal0 & lanemask_lt());
-                        if (idx < SPEC_CAP) spec[idx] = static_cast<uint32_t>(posA);
+                        if (idx >= skip && idx - skip < SPEC_CAP) spec[idx - skip] = static_cast<uint32_t>(posA);
                     }
                     cnt += __popc(bal0);
-                    if (lane == 0 && cnt < SPEC_CAP) spec[cnt] = static_cast<uint32_t>(pp) | 0x80000000u;
+                    if (lane == 0 && cnt >= skip && cnt - skip < SPEC_CAP) spec[cnt - skip] = static_cast<uint32_t>(pp) | 0x80000000u;
                     ++cnt;
                     prev_done = true;
                     const unsigned bal1 = __ballot_sync(FULL, mem && posA > pp);
                     if (mem && posA > pp) {
                         const uint32_t idx = cnt + __popc(bal1 & lanemask_lt());
-                        if (idx < SPEC_CAP) spec[idx] = static_cast<uint32_t>(posA);
+                        if (idx >= skip && idx - skip < SPEC_CAP) spec[idx - skip] = static_cast<uint32_t>(posA);
                     }
                     cnt += __popc(bal1);
                     continue;
@@ -450,49 +501,67 @@ __device__ bool n2v_implicit_step(Node2vecPool& P, uint32_t* spec, uint32_t* til
             const unsigned bal = __ballot_sync(FULL, mem);
             if (mem) {
                 const uint32_t idx = cnt + __popc(bal & lanemask_lt());
-                if (idx < SPEC_CAP) spec[idx] = static_cast<uint32_t>(posA);
+                if (idx >= skip && idx - skip < SPEC_CAP) spec[idx - skip] = static_cast<uint32_t>(posA);
             }
             cnt += __popc(bal);
         }
         if (!prev_done) {   // empty small list
-            if (lane == 0 && cnt < SPEC_CAP) spec[cnt] = static_cast<uint32_t>(pp) | 0x80000000u;
+            if (lane == 0 && cnt >= skip && cnt - skip < SPEC_CAP) spec[cnt - skip] = static_cast<uint32_t>(pp) | 0x80000000u;
             ++cnt;
         }
     }
     __syncwarp();
-    if (cnt > SPEC_CAP) return false;
+    return cnt;
+}
+
+// Integer node2vec step with an implicit CTPS (see above).  Specials beyond the
+// shared-memory window are handled by re-enumerating the next window.
+__device__ void n2v_implicit_step(Node2vecPool& P, uint32_t* spec, uint32_t* tilebuf, uint64_t U64, uint32_t& out) {
+    const int lane = lane_id();
+    const uint32_t n = P.n;
+    const uint64_t wp = P.w[0], w1 = P.w[1], wq = P.w[2];
+    bool has_prev = false;
+    const uint32_t cnt = n2v_specials(P, spec, tilebuf, 0, has_prev);
     const uint64_t np_ = has_prev ? 1 : 0;
     const uint64_t T = wq * (n - cnt) + w1 * (cnt - np_) + wp * np_;
     const uint64_t x = below(U64, T);
     // largest special j with S(p_j) = wq * (p_j - j) + sum_{j' < j} w_j' <= x
-    bool found = false;
+    bool found = false, stop = false;
     uint64_t Ssel = 0, wsel = 0, psel = 0, base = 0;
-    for (uint32_t j0 = 0; j0 < cnt; j0 += 32) {
-        const uint32_t j = j0 + lane;
-        const bool valid = j < cnt;
-        const uint32_t e = valid ? spec[j] : 0u;
-        const uint64_t pos = e & 0x7FFFFFFFu;
-        const uint64_t wj = valid ? ((e >> 31) ? wp : w1) : 0;
-        const uint64_t incl = warp_incl_scan(wj);
-        const uint64_t Sj = wq * (pos - j) + base + incl - wj;
-        const unsigned vm = __ballot_sync(FULL, valid);
-        const unsigned le = __ballot_sync(FULL, valid && Sj <= x);
-        if (le) {
-            const int f = 31 - __clz(le);
-            found = true;
-            Ssel = __shfl_sync(FULL, Sj, f);
-            wsel = __shfl_sync(FULL, wj, f);
-            psel = __shfl_sync(FULL, pos, f);
+    for (uint32_t win = 0; win < cnt && !stop; win += SPEC_CAP) {
+        if (win > 0) {
+            bool hp;
+            n2v_specials(P, spec, tilebuf, win, hp);
         }
-        if (le != vm) break;
-        base += __shfl_sync(FULL, incl, 31);
+        const uint32_t wn = min(SPEC_CAP, cnt - win);
+        for (uint32_t j0 = 0; j0 < wn; j0 += 32) {
+            const uint32_t jl = j0 + lane;
+            const uint64_t j = win + jl;
+            const bool valid = jl < wn;
+            const uint32_t e = valid ? spec[jl] : 0u;
+            const uint64_t pos = e & 0x7FFFFFFFu;
+            const uint64_t wj = valid ? ((e >> 31) ? wp : w1) : 0;
+            const uint64_t incl = warp_incl_scan(wj);
+            const uint64_t Sj = wq * (pos - j) + base + incl - wj;
+            const unsigned vm = __ballot_sync(FULL, valid);
+            const unsigned le = __ballot_sync(FULL, valid && Sj <= x);
+            if (le) {
+                const int f = 31 - __clz(le);
+                found = true;
+                Ssel = __shfl_sync(FULL, Sj, f);
+                wsel = __shfl_sync(FULL, wj, f);
+                psel = __shfl_sync(FULL, pos, f);
+            }
+            if (le != vm) { stop = true; break; }
+            base += __shfl_sync(FULL, incl, 31);
+        }
+        __syncwarp();
     }
     uint64_t i;
     if (!found) i = x / wq;
     else if (x < Ssel + wsel) i = psel;
     else i = psel + 1 + (x - Ssel - wsel) / wq;
     out = __ldg(P.col + P.beg + i);
-    return true;
 }
 
 template <bool kFloat>
@@ -531,10 +600,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 3) k_node2vec(N2vArgs na) {
                             nxt = n2v_float_step(P, na.wf, reinterpret_cast<double*>(tab), U64);
                         } else {
                             P.w[0] = na.wint[0]; P.w[1] = na.wint[1]; P.w[2] = na.wint[2];
-                            if (!n2v_implicit_step(P, spec, reinterpret_cast<uint32_t*>(tab), U64, nxt)) {
-                                const Ctps C = build_ctps(P, tab);   // > SPEC_CAP common neighbours
-                                nxt = select_wr(P, C, tab, U64);
-                            }
+                            n2v_implicit_step(P, spec, reinterpret_cast<uint32_t*>(tab), U64, nxt);
                         }
                         scanned += d;
                     }
@@ -705,6 +771,12 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         k_walk<false><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a);
     } else if (b.kind == CSAW_BIAS_UNIFORM) {
         k_walk<true><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a);
+    } else if (b.kind == CSAW_BIAS_MH) {
+        k_walk_variant<CSAW_BIAS_MH><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a, 0, g->V);
+    } else if (b.kind == CSAW_BIAS_RESTART || b.kind == CSAW_BIAS_JUMP) {
+        const uint64_t theta = static_cast<uint64_t>(std::floor(b.pf * 4294967296.0));
+        if (b.kind == CSAW_BIAS_RESTART) k_walk_variant<CSAW_BIAS_RESTART><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a, theta, g->V);
+        else k_walk_variant<CSAW_BIAS_JUMP><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a, theta, g->V);
     } else if (b.kind == CSAW_BIAS_NODE2VEC) {
         if (!g->rows_sorted) return fail(CSAW_ERR_BAD_GRAPH, "node2vec needs sorted CSR rows (N(prev) membership)");
         N2vArgs na;

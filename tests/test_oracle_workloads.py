@@ -349,3 +349,56 @@ def test_fig8_partition_facts():
     G = O.Graph(rp, col)
     for a, c in ex["edges_present"]:
         assert c in G.nbrs(a).tolist()
+
+
+# ------------------------------------------------------------- Table-1 walk variants (NEXT-3)
+def test_mh_walk_acceptance_law(G):
+    """MH walk: from v=0 (deg 1) the only proposal is 7 (deg 6): accept 1/6, else stay."""
+    N = 24000
+    counts = {}
+    for inst in range(N):
+        u = O.walk_variant_step(G, O.KIND_MH, 0.0, 0, 0, inst, 2, 31)
+        counts[u] = counts.get(u, 0) + 1
+    assert chi2(counts, {7: 1 / 6, 0: 5 / 6}, N) > 1e-4
+
+
+def test_mh_walk_stationary_uniform(G):
+    """MH with acceptance min(1, d(v)/d(u)) has the uniform stationary law."""
+    counts = np.zeros(G.V)
+    for inst in range(300):
+        p = O.walk_variant(G, O.KIND_MH, 600, 8, inst, 4)
+        np.add.at(counts, p[100:].astype(np.int64), 1)
+    freq = counts / counts.sum()
+    assert np.abs(freq - 1 / G.V).sum() / 2 < 0.03
+
+
+def test_restart_and_jump_with_zero_probability_are_the_simple_walk(R):
+    og, tg = R
+    seeds = instance_seeds(tg, 8).numpy().astype(np.uint32)
+    for i, s0 in enumerate(seeds):
+        w = O.walk(og, O.KIND_UNIFORM, 50, int(s0), i, 9)
+        assert O.walk_variant(og, O.KIND_RESTART, 50, int(s0), i, 9, 0.0).tolist() == w.tolist()
+        assert O.walk_variant(og, O.KIND_JUMP, 50, int(s0), i, 9, 0.0).tolist() == w.tolist()
+
+
+def test_restart_probability(G):
+    """Restart: from v=8 (0 not a neighbour) P(next = s0 = 0) = floor(pr 2^32) / 2^32."""
+    pr = 0.3
+    th = np.floor(pr * 2**32) / 2**32
+    N = 30000
+    back = sum(O.walk_variant_step(G, O.KIND_RESTART, pr, 0, 8, inst, 5, 77) == 0 for inst in range(N))
+    assert chi2({1: back, 0: N - back}, {1: th, 0: 1 - th}, N) > 1e-4
+
+
+def test_jump_law(G):
+    """Jump: from v=0 (N = {7}): 7 w.p. (1-th) + th/12, every other vertex th/12."""
+    pr = 0.25
+    th = np.floor(pr * 2**32) / 2**32
+    probs = {u: th / 12 for u in range(12)}
+    probs[7] += 1 - th
+    N = 40000
+    counts = {}
+    for inst in range(N):
+        u = O.walk_variant_step(G, O.KIND_JUMP, pr, 0, 0, inst, 1, 5)
+        counts[u] = counts.get(u, 0) + 1
+    assert chi2(counts, probs, N) > 1e-4
