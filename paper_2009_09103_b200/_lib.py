@@ -13,7 +13,7 @@ import subprocess
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG_DIR)
 CSRC = os.path.join(PKG_DIR, "csrc")
-LIB_PATH = os.path.join(PKG_DIR, "libcsaw.so")
+LIB_PATH = os.environ.get("CSAW_LIB") or os.path.join(PKG_DIR, "libcsaw.so")   # override: A/B experiments
 HEADER = os.path.join(ROOT, "include", "csaw.h")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

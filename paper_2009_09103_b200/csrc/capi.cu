@@ -211,10 +211,23 @@ __device__ __forceinline__ uint64_t bt_size_of(uint64_t d) {
     return s;
 }
 
-struct BtSize {
-    const int64_t* rp;
-    __device__ __forceinline__ uint64_t operator()(uint64_t v) const { return bt_size_of(rp[v + 1] - rp[v]); }
-};
+// bt_off[v] = row_ptr[v] / 16 + 8 v: a row's index needs <= d/31 + 7 entries <= the
+// gap d/16 + 8 to the next row's offset, so offsets are computable (no lookup).
+__global__ void k_bt_off(const int64_t* __restrict__ rp, int64_t V, uint64_t* __restrict__ bt_off) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= V; v += (int64_t)gridDim.x * blockDim.x)
+        bt_off[v] = static_cast<uint64_t>(rp[v]) / 16 + 8 * static_cast<uint64_t>(v);
+}
+
+// nmp[e] = row_ptr[u] << 24 | deg(u) for u = col[e]: a walk step that picks entry e
+// learns the next vertex's row and degree in the same round (no row_ptr lookup).
+__global__ void k_build_nmp(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col, int64_t E,
+                            uint64_t* __restrict__ nmp) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = col[e];
+        const int64_t a = rp[u];
+        nmp[e] = (static_cast<uint64_t>(a) << 24) | static_cast<uint64_t>(rp[u + 1] - a);
+    }
+}
 
 __global__ void k_build_bt(const int64_t* __restrict__ rp, const uint64_t* __restrict__ cps,
                            const uint64_t* __restrict__ bt_off, int64_t V, uint64_t* __restrict__ bt) {
@@ -386,16 +399,16 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         CREATE_CUDA(cudaEventCreate(&c1), "event");
         cudaEventRecord(c0);
         if (V > 0) k_build_cps<<<blocks, 256>>>(g->row_ptr, g->col, g->deg, V, g->cps, g->npos);
-        // B-tree index over the cached prefix
+        // B-tree index over the cached prefix (computable offsets)
         CREATE_CUDA(cudaMalloc(&g->bt_off, sizeof(uint64_t) * (V + 1)), "cudaMalloc(bt_off)");
-        uint64_t* part = nullptr;
-        CREATE_CUDA(cudaMalloc(&part, sizeof(uint64_t) * (SCAN_MAX_GRID + 8)), "cudaMalloc");
-        device_scan(BtSize{g->row_ptr}, static_cast<uint64_t>(V), ScanToArray{g->bt_off}, part, nullptr);
-        uint64_t btn = 0;
-        CREATE_CUDA(cudaMemcpy(&btn, g->bt_off + V, sizeof(uint64_t), cudaMemcpyDeviceToHost), "bt size");
-        cudaFree(part);
-        CREATE_CUDA(cudaMalloc(&g->bt, sizeof(uint64_t) * std::max<uint64_t>(btn, 1)), "cudaMalloc(bt)");
+        k_bt_off<<<blocks, 256>>>(g->row_ptr, V, g->bt_off);
+        const uint64_t btn = static_cast<uint64_t>(E) / 16 + 8 * static_cast<uint64_t>(V) + 64;
+        CREATE_CUDA(cudaMalloc(&g->bt, sizeof(uint64_t) * btn), "cudaMalloc(bt)");
         if (V > 0) k_build_bt<<<blocks, 256>>>(g->row_ptr, g->cps, g->bt_off, V, g->bt);
+        if (g->max_deg < (1 << 24) && E < (int64_t(1) << 40) && E > 0) {
+            CREATE_CUDA(cudaMalloc(&g->nmp, sizeof(uint64_t) * E), "cudaMalloc(nmp)");
+            k_build_nmp<<<blocks, 256>>>(g->row_ptr, g->col, E, g->nmp);
+        }
         cudaEventRecord(c1);
         CREATE_CUDA(cudaEventSynchronize(c1), "build cps");
         float ms = 0.f;
@@ -423,6 +436,7 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->npos) cudaFree(g->npos);
     if (g->bt) cudaFree(g->bt);
     if (g->bt_off) cudaFree(g->bt_off);
+    if (g->nmp) cudaFree(g->nmp);
     auto& st = g->oomst;
     if (st.h_col) cudaFreeHost(st.h_col);
     if (st.h_row) cudaFreeHost(st.h_row);

@@ -97,7 +97,8 @@ struct csaw_graph {
     uint64_t* cps = nullptr;      // static-bias CTPS cache [E] (CSAW_GRAPH_CTPS_CACHE), inclusive per row
     uint32_t* npos = nullptr;     // [V] positive-bias neighbours per row (cache builds only)
     uint64_t* bt = nullptr;       // fanout-32 B-tree index levels over cps (rows with d > 32)
-    uint64_t* bt_off = nullptr;   // [V] start of a row's index segment in bt
+    uint64_t* bt_off = nullptr;   // [V] start of a row's index segment in bt (= row_ptr/16 + 8 v)
+    uint64_t* nmp = nullptr;      // [E] next-vertex metadata row_ptr[u] << 24 | deg(u) (walks)
     double cache_build_ms = 0.0;
     int num_sms = 148;
     bool oom = false;

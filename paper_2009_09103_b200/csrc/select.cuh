@@ -511,9 +511,10 @@ struct CpsTree {
     }
     // Warp-collective.  kDraw: x = below(U, T) with T from the top level (returned);
     // else x is given.  Result: CSR index e of the pick, S_s = lo, S_{s+1} = hi, col[e].
-    template <bool kDraw>
+    template <bool kDraw, bool kMeta = false>
     __device__ __forceinline__ void search(uint64_t U, uint64_t& x, uint64_t& T, uint64_t& e, uint64_t& lo,
-                                           uint64_t& hi, uint32_t& item, uint32_t& probes) const {
+                                           uint64_t& hi, uint32_t& item, uint32_t& probes,
+                                           const uint64_t* __restrict__ nmp = nullptr, uint64_t* meta = nullptr) const {
         const int lane = lane_id();
         const int K = num_levels(d);
         uint32_t j = 0;          // block index at the current level
@@ -523,10 +524,14 @@ struct CpsTree {
             const uint32_t nk = k == 0 ? d : ((d - 1) >> (5 * k)) + 1;
             const uint32_t idx = j * 32 + lane;
             const bool valid = idx < nk;
-            uint64_t v = 0;
+            uint64_t v = 0, mt = 0;
             uint32_t it = NONE;
             if (valid) {
-                if (k == 0) { v = __ldg(cps + beg + idx); it = __ldg(col + beg + idx); }
+                if (k == 0) {
+                    v = __ldg(cps + beg + idx);
+                    it = __ldg(col + beg + idx);
+                    if constexpr (kMeta) mt = __ldg(nmp + beg + idx);   // next vertex's (row_ptr, degree)
+                }
                 else v = __ldg(bt + boff + off + idx);
             }
             probes += min(32u, nk - j * 32);
@@ -544,6 +549,7 @@ struct CpsTree {
                 hi = __shfl_sync(FULL, v, f);
                 lo = left;
                 item = __shfl_sync(FULL, it, f);
+                if constexpr (kMeta) *meta = __shfl_sync(FULL, mt, f);
             }
             off += nk;
             j = j * 32 + f;
