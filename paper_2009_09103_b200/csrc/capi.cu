@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -211,12 +212,10 @@ __device__ __forceinline__ uint64_t bt_size_of(uint64_t d) {
     return s;
 }
 
-// bt_off[v] = row_ptr[v] / 16 + 8 v: a row's index needs <= d/31 + 7 entries <= the
-// gap d/16 + 8 to the next row's offset, so offsets are computable (no lookup).
-__global__ void k_bt_off(const int64_t* __restrict__ rp, int64_t V, uint64_t* __restrict__ bt_off) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= V; v += (int64_t)gridDim.x * blockDim.x)
-        bt_off[v] = static_cast<uint64_t>(rp[v]) / 16 + 8 * static_cast<uint64_t>(v);
-}
+struct BtSize {
+    const int64_t* rp;
+    __device__ __forceinline__ uint64_t operator()(uint64_t v) const { return bt_size_of(rp[v + 1] - rp[v]); }
+};
 
 // nmp[e] = row_ptr[u] << 24 | deg(u) for u = col[e]: a walk step that picks entry e
 // learns the next vertex's row and degree in the same round (no row_ptr lookup).
@@ -399,13 +398,20 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         CREATE_CUDA(cudaEventCreate(&c1), "event");
         cudaEventRecord(c0);
         if (V > 0) k_build_cps<<<blocks, 256>>>(g->row_ptr, g->col, g->deg, V, g->cps, g->npos);
-        // B-tree index over the cached prefix (computable offsets)
+        // B-tree index over the cached prefix: dense segments (prefix sum of the sizes)
         CREATE_CUDA(cudaMalloc(&g->bt_off, sizeof(uint64_t) * (V + 1)), "cudaMalloc(bt_off)");
-        k_bt_off<<<blocks, 256>>>(g->row_ptr, V, g->bt_off);
-        const uint64_t btn = static_cast<uint64_t>(E) / 16 + 8 * static_cast<uint64_t>(V) + 64;
-        CREATE_CUDA(cudaMalloc(&g->bt, sizeof(uint64_t) * btn), "cudaMalloc(bt)");
+        uint64_t* part = nullptr;
+        CREATE_CUDA(cudaMalloc(&part, sizeof(uint64_t) * (SCAN_MAX_GRID + 8)), "cudaMalloc");
+        device_scan(BtSize{g->row_ptr}, static_cast<uint64_t>(V), ScanToArray{g->bt_off}, part, nullptr);
+        uint64_t btn = 0;
+        CREATE_CUDA(cudaMemcpy(&btn, g->bt_off + V, sizeof(uint64_t), cudaMemcpyDeviceToHost), "bt size");
+        cudaFree(part);
+        CREATE_CUDA(cudaMalloc(&g->bt, sizeof(uint64_t) * std::max<uint64_t>(btn, 1)), "cudaMalloc(bt)");
         if (V > 0) k_build_bt<<<blocks, 256>>>(g->row_ptr, g->cps, g->bt_off, V, g->bt);
-        if (g->max_deg < (1 << 24) && E < (int64_t(1) << 40) && E > 0) {
+        // next-vertex metadata for walks: off by default (measured 2.5 % slower on cfg2:
+        // the extra 256 B per step outweighs the saved row_ptr round); CSAW_WALK_META=1 enables
+        const char* meta = std::getenv("CSAW_WALK_META");
+        if (g->max_deg < (1 << 24) && E < (int64_t(1) << 40) && E > 0 && meta && meta[0] == '1') {
             CREATE_CUDA(cudaMalloc(&g->nmp, sizeof(uint64_t) * E), "cudaMalloc(nmp)");
             k_build_nmp<<<blocks, 256>>>(g->row_ptr, g->col, E, g->nmp);
         }

@@ -53,6 +53,7 @@ struct PathWriter {
 // load -- O(log32 d) round trips instead of an 8 d-byte rescan.  Bit-identical.
 __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_cached(WalkArgs a, const uint64_t* __restrict__ cps,
                                                                   const uint64_t* __restrict__ bt,
+                                                                  const uint64_t* __restrict__ bt_off,
                                                                   const uint64_t* __restrict__ nmp) {
     const int lane = lane_id();
     unsigned long long probes = 0, steps = 0;
@@ -64,24 +65,27 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_cached(WalkArgs a, 
         // current vertex's row: from row_ptr for the seed, then carried in nmp
         uint64_t rb = static_cast<uint64_t>(__ldg(a.rp + cur));
         uint32_t d = static_cast<uint32_t>(__ldg(a.rp + cur + 1) - static_cast<int64_t>(rb));
+        uint64_t boff = __ldg(bt_off + cur);
         for (int32_t t = 0; t < a.L; ++t) {
             uint32_t nxt = NONE;
             if (cur != NONE && d > 0) {
                 const uint64_t U = draw_u64(a.key, inst, static_cast<uint32_t>(t), 0u, word3(PURPOSE_EDGE, 0, 0));
                 // B-tree over the cached prefix: T from the top level, one coalesced block
                 // per level; col and the next vertex's (row, degree) read with the last block
-                CpsTree tr{cps, bt, a.col, rb, d, rb / 16 + 8 * static_cast<uint64_t>(cur)};
+                CpsTree tr{cps, bt, a.col, rb, d, boff};
                 uint64_t x = 0, T = 0, e = 0, lo = 0, hi = 0, meta = 0;
                 uint32_t pr = 0;
                 if (nmp) {
                     tr.template search<true, true>(U, x, T, e, lo, hi, nxt, pr, nmp, &meta);
                     rb = meta >> 24;
                     d = static_cast<uint32_t>(meta & 0xFFFFFFu);
+                    if (nxt != NONE) boff = __ldg(bt_off + nxt);
                 } else {
                     tr.template search<true>(U, x, T, e, lo, hi, nxt, pr);
                     if (nxt != NONE) {
                         rb = static_cast<uint64_t>(__ldg(a.rp + nxt));
                         d = static_cast<uint32_t>(__ldg(a.rp + nxt + 1) - static_cast<int64_t>(rb));
+                        boff = __ldg(bt_off + nxt);
                     }
                 }
                 probes += pr;
@@ -473,97 +477,45 @@ __device__ uint32_t n2v_specials(Node2vecPool& P, uint32_t* spec, uint32_t* tile
         const uint64_t ns = small_is_v ? dv : dp, nb = small_is_v ? dp : dv;
         uint64_t lo0 = 0;
         bool prev_done = !has_prev;
-        for (uint64_t c0 = 0; c0 < ns; c0 += 32 * U) {
-            // 8 rows of the small list; their value span's range [lo, hi) in the big list
-            uint32_t xv[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint64_t i = c0 + u * 32 + lane;
-                xv[u] = i < ns ? __ldg(small + i) : NONE;
-            }
-            const uint64_t last = min(ns, c0 + 32 * U) - 1;
-            const uint32_t cmin = __shfl_sync(FULL, xv[0], 0);
-            const uint32_t cmax = __ldg(small + last);
-            const uint64_t lo = warp_lower_bound(big, lo0, nb, cmin);
-            const uint64_t hi = warp_lower_bound(big, lo, nb, cmax + 1u);
-            lo0 = hi;
-            uint32_t fnd = 0;          // bit u: xv[u] found in the big list
-            uint32_t bidx[U];          // position relative to lo
-            const uint32_t R = static_cast<uint32_t>(hi - lo);
-            if (R <= TILE_N) {
-                // small range: stage it in shared memory, branch-free searches there
-                __syncwarp();
-                for (uint32_t j = lane; j < R; j += 32) tilebuf[j] = __ldg(big + lo + j);
-                __syncwarp();
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    uint32_t pos = 0;
-#pragma unroll
-                    for (uint32_t st = TILE_N / 2; st > 0; st >>= 1)
-                        if (pos + st <= R && tilebuf[pos + st - 1] < xv[u]) pos += st;
-                    if (xv[u] != NONE && pos < R && tilebuf[pos] == xv[u]) fnd |= 1u << u;
-                    bidx[u] = pos;
-                }
-            } else {
-                // large range: 8 independent binary searches per lane (latency overlapped)
-                const uint32_t* bb = big + lo;
-                uint32_t l[U], h[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) { l[u] = 0; h[u] = R; }
-                for (uint32_t len = R; len > 0; len >>= 1) {
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        if (l[u] < h[u]) {
-                            const uint32_t mid = (l[u] + h[u]) >> 1;
-                            if (__ldg(bb + mid) < xv[u]) l[u] = mid + 1; else h[u] = mid;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (xv[u] != NONE && l[u] < R && __ldg(bb + l[u]) == xv[u]) fnd |= 1u << u;
-                    bidx[u] = l[u];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint64_t r0 = c0 + u * 32;
-                if (r0 >= ns) break;   // warp-uniform
-                const uint64_t i = r0 + lane;
-                const bool mem = ((fnd >> u) & 1u) && xv[u] != P.prev;
-                const uint64_t posA = small_is_v ? i : lo + bidx[u];      // position in N(v)
-                bool handled = false;
-                // insert prev's own position in order (it is not in N(prev): no self-loops)
-                if (!prev_done) {
-                    const unsigned after = __ballot_sync(FULL, mem && posA > pp);
-                    if (after || r0 + 32 >= ns) {
-                        const unsigned bal0 = __ballot_sync(FULL, mem && posA < pp);
-                        if (mem && posA < pp) {
-                            const uint32_t idx = cnt + __popc(bal0 & lanemask_lt());
-                            if (idx >= skip && idx - skip < SPEC_CAP) spec[idx - skip] = static_cast<uint32_t>(posA);
-                        }
-                        cnt += __popc(bal0);
-                        if (lane == 0 && cnt >= skip && cnt - skip < SPEC_CAP) spec[cnt - skip] = static_cast<uint32_t>(pp) | 0x80000000u;
-                        ++cnt;
-                        prev_done = true;
-                        const unsigned bal1 = __ballot_sync(FULL, mem && posA > pp);
-                        if (mem && posA > pp) {
-                            const uint32_t idx = cnt + __popc(bal1 & lanemask_lt());
-                            if (idx >= skip && idx - skip < SPEC_CAP) spec[idx - skip] = static_cast<uint32_t>(posA);
-                        }
-                        cnt += __popc(bal1);
-                        handled = true;
-                    }
-                }
-                if (!handled) {
-                    const unsigned bal = __ballot_sync(FULL, mem);
-                    if (mem) {
-                        const uint32_t idx = cnt + __popc(bal & lanemask_lt());
+        for (uint64_t r0 = 0; r0 < ns; r0 += 32) {
+            const uint64_t i = r0 + lane;
+            const bool valid = i < ns;
+            const uint32_t xv = valid ? __ldg(small + i) : NONE;
+            uint64_t bi = 0;
+            const bool f = n2v_find(big, lo0, nb, xv, valid, bi);
+            const bool mem = f && xv != P.prev;
+            const uint64_t posA = small_is_v ? i : bi;      // position in N(v)
+            // insert prev's own position in order (it is not in N(prev): no self-loops)
+            if (!prev_done) {
+                const unsigned before = __ballot_sync(FULL, mem && posA < pp);
+                const unsigned after = __ballot_sync(FULL, mem && posA > pp);
+                (void)before;
+                if (after || r0 + 32 >= ns) {
+                    // emit members < pp first, then prev, then the rest of this row
+                    const unsigned bal0 = __ballot_sync(FULL, mem && posA < pp);
+                    if (mem && posA < pp) {
+                        const uint32_t idx = cnt + __popc(bal0 & lanemask_lt());
                         if (idx >= skip && idx - skip < SPEC_CAP) spec[idx - skip] = static_cast<uint32_t>(posA);
                     }
-                    cnt += __popc(bal);
+                    cnt += __popc(bal0);
+                    if (lane == 0 && cnt >= skip && cnt - skip < SPEC_CAP) spec[cnt - skip] = static_cast<uint32_t>(pp) | 0x80000000u;
+                    ++cnt;
+                    prev_done = true;
+                    const unsigned bal1 = __ballot_sync(FULL, mem && posA > pp);
+                    if (mem && posA > pp) {
+                        const uint32_t idx = cnt + __popc(bal1 & lanemask_lt());
+                        if (idx >= skip && idx - skip < SPEC_CAP) spec[idx - skip] = static_cast<uint32_t>(posA);
+                    }
+                    cnt += __popc(bal1);
+                    continue;
                 }
             }
+            const unsigned bal = __ballot_sync(FULL, mem);
+            if (mem) {
+                const uint32_t idx = cnt + __popc(bal & lanemask_lt());
+                if (idx >= skip && idx - skip < SPEC_CAP) spec[idx - skip] = static_cast<uint32_t>(posA);
+            }
+            cnt += __popc(bal);
         }
         if (!prev_done) {   // empty small list
             if (lane == 0 && cnt >= skip && cnt - skip < SPEC_CAP) spec[cnt - skip] = static_cast<uint32_t>(pp) | 0x80000000u;
@@ -833,7 +785,7 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
     WalkArgs a{g->row_ptr, colp, g->deg, d_seeds, static_cast<uint64_t>(n), length,
                static_cast<uint32_t>(base), key, d_path, static_cast<unsigned long long*>(cnt)};
     if (b.kind == CSAW_BIAS_DEGREE && g->cps) {
-        k_walk_cached<<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a, g->cps, g->bt, g->nmp);
+        k_walk_cached<<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a, g->cps, g->bt, g->bt_off, g->nmp);
     } else if (b.kind == CSAW_BIAS_DEGREE) {
         k_walk<false><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a);
     } else if (b.kind == CSAW_BIAS_UNIFORM) {
