@@ -427,26 +427,45 @@ def main():
 
     # ---------------- cfg5: the B200-native zero-copy OOM variant (NEXT-4), reported apart
     zc = None
-    if oom and cfg.workload == "mdrw" and not args.no_zerocopy:
+    if oom and not args.no_zerocopy:
         try:
             Gz = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, budget_bytes=cfg.oom_budget_bytes,
                                       num_partitions=cfg.oom_partitions, max_resident=1, zerocopy=True)
-            outz = torch.empty((n, cfg.length, 2), dtype=torch.int32, device=dev)
-            cs.csaw_walk(Gz, bias, seeds, cfg.length, instance_base=base, rng_seed=args.rng_seed, out=outz, stream=stream)
+            if kind == "walk":
+                outz = torch.empty((n, cfg.length, 2), dtype=torch.int32, device=dev)
+
+                def zstep():
+                    cs.csaw_walk(Gz, bias, seeds, cfg.length, instance_base=base, rng_seed=args.rng_seed, out=outz,
+                                 stream=stream)
+                    return n * cfg.length
+
+                def zsame():
+                    return bool(torch.equal(outz, out_dev))
+            else:
+                zr = []
+
+                def zstep():
+                    zr[:] = cs.csaw_sample(Gz, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth,
+                                           instance_base=base, rng_seed=args.rng_seed, stream=stream)
+                    return int(zr[1].numel())
+
+                def zsame():
+                    ref = r_last(cs, G, bias, seeds, cfg, base, args, stream)
+                    return all(bool(torch.equal(a, b)) for a, b in zip(ref, zr))
+            zstep()
             torch.cuda.synchronize(dev)
-            zt = []
+            zt, ze = [], 0
             for _ in range(max(1, args.steps)):
                 flush.fill_(1)
                 z0 = torch.cuda.Event(enable_timing=True)
                 z1 = torch.cuda.Event(enable_timing=True)
                 z0.record(stream)
-                cs.csaw_walk(Gz, bias, seeds, cfg.length, instance_base=base, rng_seed=args.rng_seed, out=outz,
-                             stream=stream)
+                ze += zstep()
                 z1.record(stream)
                 torch.cuda.synchronize(dev)
                 zt.append(z0.elapsed_time(z1))
-            zc = {"value": n * cfg.length / (sum(zt) / len(zt) / 1000.0), "unit": UNIT, "ms_per_step": sum(zt) / len(zt),
-                  "identical_to_partitioned": bool(torch.equal(outz, out_dev)),
+            zc = {"value": ze / (sum(zt) / 1000.0), "unit": UNIT, "ms_per_step": sum(zt) / len(zt),
+                  "identical_to_partitioned": zsame(),
                   "what": "OOM zero-copy: col_idx read in place from pinned host memory, same 8 GB budget (NEXT-4)"}
             Gz.close()
         except Exception as ex:
@@ -498,6 +517,8 @@ def main():
                            "partition_loads_per_step": st_last["partition_loads"] if st_last else None,
                            "h2d_bytes_per_step": st_last["h2d_bytes"] if st_last else None,
                            "transfer_ms_per_step": st_last["transfer_ms"] if st_last else None,
+                           "host_link_gbs": (st_last["h2d_bytes"] / st_last["transfer_ms"] / 1e6)
+                           if st_last and st_last["transfer_ms"] else None,
                            "cache_probes_per_step": st_last["cache_probes"] if st_last else None,
                            "oom_zerocopy": zc,
                            "neighbours_scanned_per_step": st_last["neighbours_scanned"] if st_last else None,
@@ -570,6 +591,9 @@ def hot_kernel_name(cfg, cached=False, oom=False):
         return "k_mdrw_oom_part" if oom else "k_mdrw"
     if cfg.workload == "node2vec":
         return "k_node2vec<int>"
+    if oom:
+        # OOM traversal sampling runs the batched level driver, one select launch per resident partition
+        return "k_ns_select<1>" if cfg.bias == "degree" else "k_ns_select<0>"
     # sampling: the fused one-warp-per-instance kernel (small per-instance frontiers)
     mode = {"neighbor": 2 if cached else 1, "forest_fire": 3, "layer": 5 if cached else 4}[cfg.workload]
     if cfg.workload == "neighbor" and cfg.bias == "uniform":

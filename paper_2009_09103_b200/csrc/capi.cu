@@ -613,7 +613,9 @@ CSAW_API csaw_status csaw_sample(const csaw_graph* g, const csaw_bias* bias, con
     }
     if (instance_base + static_cast<uint64_t>(n) > 0xFFFFFFFFull)
         return fail(CSAW_ERR_INVALID_ARG, "instance ids must fit in 32 bits");
-    if (g->oom) return fail(CSAW_ERR_UNSUPPORTED, "OOM-mode traversal sampling is not implemented yet");
+    if (g->oom && b.kind == CSAW_BIAS_LAYER && !g->oomst.zerocopy)
+        return fail(CSAW_ERR_UNSUPPORTED, "OOM partition scheduling implements neighbor sampling and forest fire "
+                                          "(layer pools span partitions; use CSAW_GRAPH_OOM_ZEROCOPY)");
     if (!offsets) return fail(CSAW_ERR_INVALID_ARG, "offsets is NULL");
     if (n > 0 && !seeds) return fail(CSAW_ERR_INVALID_ARG, "seeds is NULL");
     cudaStream_t st = static_cast<cudaStream_t>(stream);

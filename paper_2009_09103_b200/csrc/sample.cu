@@ -128,6 +128,8 @@ struct SelArgs {
     const uint64_t* __restrict__ bt;
     const uint64_t* __restrict__ bt_off;
     uint32_t mode;                   // collision migration (MIGRATE_*)
+    const uint32_t* __restrict__ qidx;   // OOM: queue entries of one partition (nullptr = all nq entries)
+    uint64_t nidx;
 };
 
 // Neighbor sampling / forest fire: one warp per queue entry.
@@ -142,7 +144,9 @@ __global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_ns_select(SelArgs a) {
     const int lane = lane_id();
     PickRec* gl = a.glist ? a.glist + global_warp_id() * a.kmax : nullptr;
     unsigned long long scanned = 0, pools = 0, probes = 0, draws = 0;
-    for (uint64_t q = global_warp_id(); q < a.nq; q += total_warps()) {
+    const uint64_t nwork = a.qidx ? a.nidx : a.nq;
+    for (uint64_t jq = global_warp_id(); jq < nwork; jq += total_warps()) {
+        const uint64_t q = a.qidx ? a.qidx[jq] : jq;
         const uint32_t v = a.qv[q];
         const uint32_t inst = a.qi[q];
         const int64_t b0 = __ldg(a.rp + v);
@@ -642,6 +646,34 @@ __global__ void k_write(LevelDesc L, int depth1, const uint32_t* __restrict__ s_
     }
 }
 
+// ---------------------------------------------------------------- OOM: partition-grouped levels
+// Batched multi-instance sampling in the out-of-memory mode (§5.2-5.3):
+// a level's queue (all instances mixed) is grouped by the partition owning each
+// frontier vertex; partitions are made resident busiest-first and one select
+// kernel per resident partition processes its entries (CTAs ~ its count).  Levels
+// run in order, so the visited filter sees complete earlier levels (R22).
+struct OwnerP {
+    uint64_t base, rem;
+    __device__ __forceinline__ uint32_t operator()(uint32_t v) const {
+        const uint64_t big = rem * (base + 1);
+        if (v < big) return static_cast<uint32_t>(v / (base + 1));
+        return static_cast<uint32_t>(rem + (v - big) / base);
+    }
+};
+
+__global__ void k_part_count(const uint32_t* __restrict__ qv, uint64_t nq, OwnerP own, uint32_t* __restrict__ cnt) {
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(cnt + own(qv[q]), 1u);
+}
+
+__global__ void k_part_scatter(const uint32_t* __restrict__ qv, uint64_t nq, OwnerP own, uint32_t* __restrict__ fill,
+                               uint32_t* __restrict__ idx) {
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t pos = atomicAdd(fill + own(qv[q]), 1u);   // fill[p] starts at partition p's offset
+        idx[pos] = static_cast<uint32_t>(q);
+    }
+}
+
 // ---------------------------------------------------------------- fused per-instance sampler
 // For small per-instance frontiers (the paper's NeighborSize = Depth = 2 setups,
 // P:972-974) the whole traversal of one instance runs in ONE warp: frontier,
@@ -915,6 +947,113 @@ static csaw_status lvl_buf(const csaw_graph* g, int l, int k, uint64_t count, T*
     return CSAW_OK;
 }
 
+// One level of batched sampling in OOM mode (see k_part_count above).
+static csaw_status oom_select_level(const csaw_graph* g, const csaw_bias& b, const uint32_t* qv, const uint32_t* qi,
+                                    uint64_t nq, const uint32_t* kq, const uint32_t* ub, const uint64_t* eoff,
+                                    uint32_t* s_inst, uint32_t* s_src, uint32_t* s_dst, uint32_t d, uint32_t base,
+                                    uint2 key, uint32_t a_max, PickRec* glist, uint32_t kmax,
+                                    unsigned long long* counters, bool degree_bias, cudaStream_t st) {
+    auto& os = const_cast<csaw_graph*>(g)->oomst;
+    const uint32_t P = static_cast<uint32_t>(os.P);
+    OwnerP own{static_cast<uint64_t>(g->V) / P, static_cast<uint64_t>(g->V) % P};
+    void *pc, *pi;
+    CSAW_TRY(g->scratch.get(SL_LEVEL_BASE + 253 * 16 + 0, sizeof(uint32_t) * 2 * (P + 1), &pc));
+    CSAW_TRY(g->scratch.get(SL_LEVEL_BASE + 253 * 16 + 1, sizeof(uint32_t) * std::max<uint64_t>(nq, 1), &pi));
+    uint32_t* cnt = static_cast<uint32_t*>(pc);
+    uint32_t* fill = cnt + (P + 1);
+    uint32_t* idx = static_cast<uint32_t*>(pi);
+    std::vector<uint32_t> hc(2 * (P + 1));   // P is unbounded: pageable staging, synchronised below
+    CSAW_CUDA(cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * P, st));
+    k_part_count<<<grid_for(g, nq), 256, 0, st>>>(qv, nq, own, cnt);
+    note_launch();
+    CSAW_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, st));
+    CSAW_CUDA(cudaStreamSynchronize(st));
+    std::vector<uint64_t> c(P), off(P + 1, 0);
+    for (uint32_t p = 0; p < P; ++p) { c[p] = hc[p]; off[p + 1] = off[p] + c[p]; }
+    for (uint32_t p = 0; p < P; ++p) hc[P + 1 + p] = static_cast<uint32_t>(off[p]);
+    CSAW_CUDA(cudaMemcpyAsync(fill, hc.data() + P + 1, sizeof(uint32_t) * P, cudaMemcpyHostToDevice, st));
+    k_part_scatter<<<grid_for(g, nq), 256, 0, st>>>(qv, nq, own, fill, idx);
+    note_launch();
+    CSAW_CUDA(cudaGetLastError());
+    // workload-aware waves: residents with work stay; free / idle slots take the busiest
+    std::vector<bool> done(P, false);
+    for (uint32_t p = 0; p < P; ++p) done[p] = c[p] == 0;
+    std::vector<int32_t>& res = os.resident;
+    cudaEvent_t evs;
+    CSAW_CUDA(cudaEventCreateWithFlags(&evs, cudaEventDisableTiming));
+    CSAW_CUDA(cudaEventRecord(evs, st));
+    for (;;) {
+        std::vector<int32_t> order;
+        for (uint32_t p = 0; p < P; ++p) if (!done[p]) order.push_back(static_cast<int32_t>(p));
+        if (order.empty()) break;
+        std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return c[x] > c[y]; });
+        std::vector<std::pair<int32_t, int>> wave;   // (partition, slot)
+        for (int s = 0; s < os.R; ++s)
+            if (res[s] >= 0 && !done[res[s]]) wave.push_back({res[s], s});
+        for (int32_t p : order) {
+            if (static_cast<int>(wave.size()) >= os.R) break;
+            bool inwave = false;
+            for (auto& w : wave) inwave |= w.first == p;
+            if (inwave) continue;
+            int slot = -1;
+            for (int s = 0; s < os.R && slot < 0; ++s) {
+                bool used = false;
+                for (auto& w : wave) used |= w.second == s;
+                if (!used) slot = s;
+            }
+            if (slot < 0) break;
+            res[slot] = p;
+            const int sidx = slot % os.S;
+            CSAW_CUDA(cudaStreamWaitEvent(os.streams[sidx], evs, 0));
+            cudaEvent_t t0, t1;
+            CSAW_CUDA(cudaEventCreate(&t0));
+            CSAW_CUDA(cudaEventCreate(&t1));
+            CSAW_CUDA(cudaEventRecord(t0, os.streams[sidx]));
+            const int64_t ne = os.ebeg[p + 1] - os.ebeg[p];
+            CSAW_CUDA(cudaMemcpyAsync(os.d_slots + static_cast<int64_t>(slot) * os.slot_edges, os.h_col + os.ebeg[p],
+                                      sizeof(uint32_t) * ne, cudaMemcpyHostToDevice, os.streams[sidx]));
+            CSAW_CUDA(cudaEventRecord(t1, os.streams[sidx]));
+            CSAW_CUDA(cudaEventSynchronize(t1));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, t0, t1);
+            cudaEventDestroy(t0);
+            cudaEventDestroy(t1);
+            g->stats.transfer_ms += ms;
+            g->stats.partition_loads += 1;
+            g->stats.h2d_bytes += sizeof(uint32_t) * ne;
+            wave.push_back({p, slot});
+        }
+        uint64_t wave_total = 0;
+        for (auto& w : wave) wave_total += c[w.first];
+        for (auto& w : wave) {
+            const int32_t p = w.first;
+            const int sidx = w.second % os.S;
+            CSAW_CUDA(cudaStreamWaitEvent(os.streams[sidx], evs, 0));
+            const int total_blocks = g->num_sms * 8;
+            int blocks = static_cast<int>(std::max<uint64_t>(1, total_blocks * c[p] / std::max<uint64_t>(wave_total, 1)));
+            blocks = std::min<int>(blocks, static_cast<int>((c[p] + SEL_WARPS - 1) / SEL_WARPS));   // P:850 balancing
+            const uint32_t* colp = os.d_slots + static_cast<int64_t>(w.second) * os.slot_edges - os.ebeg[p];
+            SelArgs sa{g->row_ptr, colp, g->deg, qv, qi, nq, kq, ub, eoff, s_inst, s_src, s_dst, d, base, key, a_max,
+                       glist, kmax, counters, nullptr, nullptr, nullptr, nullptr, static_cast<uint32_t>(b.migration),
+                       idx + off[p], c[p]};
+            CSAW_TRY(hot_begin(g, os.streams[sidx]));
+            if (degree_bias) k_ns_select<1><<<std::max(1, blocks), SEL_WARPS * 32, 0, os.streams[sidx]>>>(sa);
+            else k_ns_select<0><<<std::max(1, blocks), SEL_WARPS * 32, 0, os.streams[sidx]>>>(sa);
+            note_launch();
+            CSAW_CUDA(cudaGetLastError());
+            CSAW_TRY(hot_end(g, os.streams[sidx]));
+            done[p] = true;
+        }
+        for (int s = 0; s < os.S; ++s) {
+            CSAW_CUDA(cudaEventRecord(evs, os.streams[s]));
+            CSAW_CUDA(cudaStreamWaitEvent(st, evs, 0));
+        }
+        CSAW_CUDA(cudaEventRecord(evs, st));
+    }
+    cudaEventDestroy(evs);
+    return CSAW_OK;
+}
+
 // Fused path: returns CSAW_OK when done, CSAW_ERR_CAPACITY / OUT_OF_RANGE as usual, and
 // FUSED_FALLBACK when the batched level-synchronous driver must run instead.
 constexpr csaw_status FUSED_FALLBACK = static_cast<csaw_status>(-1);
@@ -958,7 +1097,7 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     CSAW_CUDA(cudaMemcpyAsync(pf, hfan, sizeof(int32_t) * depth, cudaMemcpyHostToDevice, st));
     CSAW_TRY(stats_begin(g, st));
     FusedArgs a;
-    a.rp = g->row_ptr; a.col = g->col; a.deg = g->deg; a.cps = g->cps; a.npos = g->npos; a.bt = g->bt;
+    a.rp = g->row_ptr; a.col = g->oom ? g->oomst.h_col : g->col; a.deg = g->deg; a.cps = g->cps; a.npos = g->npos; a.bt = g->bt;
     a.bt_off = g->bt_off; a.seeds = d_seeds; a.n = n; a.depth = depth; a.fanout = static_cast<int32_t*>(pf);
     a.theta = ff ? static_cast<uint64_t>(std::floor(b.pf * 4294967296.0)) : 0;
     a.base = static_cast<uint32_t>(base);
@@ -1038,7 +1177,7 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
                        const uint32_t* d_seeds, int64_t n_i64, uint64_t base, uint64_t seed, uint64_t* d_offsets,
                        uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
                        bool out_on_device, cudaStream_t st) {
-    if (!g->force_batched) {
+    if (!g->force_batched && (!g->oom || g->oomst.zerocopy)) {
         const csaw_status s = run_sample_fused(g, b, fanout, depth, d_seeds, static_cast<uint64_t>(n_i64), base, seed,
                                                d_offsets, src, dst, dep, capacity, num_edges, out_on_device, st);
         if (s != FUSED_FALLBACK) return s;
@@ -1056,6 +1195,8 @@ csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int
     const bool layer = b.kind == CSAW_BIAS_LAYER;
     const bool ff = b.kind == CSAW_BIAS_FOREST_FIRE;
     const bool degree_bias = b.kind == CSAW_BIAS_DEGREE;
+    // zero-copy OOM mode reads col_idx in place from pinned host memory (UVA)
+    const uint32_t* colz = g->oom ? g->oomst.h_col : g->col;
     const uint32_t a_max = b.a_max ? static_cast<uint32_t>(b.a_max) : 64u;
     const uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     const uint64_t theta = ff ? static_cast<uint64_t>(std::floor(b.pf * 4294967296.0)) : 0;
@@ -1161,19 +1302,22 @@ csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int
             CSAW_TRY(g->scratch.get(SL_GLIST, sizeof(PickRec) * kmax * static_cast<uint64_t>(sgrid) * SEL_WARPS, &p));
             glist = static_cast<PickRec*>(p);
         }
-        if (nwork > 0 && total > 0) {
+        if (nwork > 0 && total > 0 && g->oom && !g->oomst.zerocopy) {
+            CSAW_TRY(oom_select_level(g, b, qv, qi, nq, kq, ub, eoff, s_inst, s_src, s_dst, static_cast<uint32_t>(l),
+                                      static_cast<uint32_t>(base), key, a_max, glist, kmax, counters, degree_bias, st));
+        } else if (nwork > 0 && total > 0) {
             CSAW_TRY(hot_begin(g, st));
             note_launch();
             if (layer) {
-                LayerArgs la{g->row_ptr, g->col, g->deg, qv, inst_off, qpref, n, fan, ub, eoff, s_inst, s_src, s_dst,
+                LayerArgs la{g->row_ptr, colz, g->deg, qv, inst_off, qpref, n, fan, ub, eoff, s_inst, s_src, s_dst,
                              static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters,
                              g->cps, g->npos, g->bt, g->bt_off, static_cast<uint32_t>(b.migration)};
                 if (g->cps) k_layer_select<true><<<sgrid, SEL_WARPS * 32, 0, st>>>(la);
                 else k_layer_select<false><<<sgrid, SEL_WARPS * 32, 0, st>>>(la);
             } else {
-                SelArgs sa{g->row_ptr, g->col, g->deg, qv, qi, nq, kq, ub, eoff, s_inst, s_src, s_dst,
+                SelArgs sa{g->row_ptr, colz, g->deg, qv, qi, nq, kq, ub, eoff, s_inst, s_src, s_dst,
                            static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters,
-                           g->cps, g->npos, g->bt, g->bt_off, static_cast<uint32_t>(b.migration)};
+                           g->cps, g->npos, g->bt, g->bt_off, static_cast<uint32_t>(b.migration), nullptr, 0};
                 if (degree_bias && g->cps) k_ns_select<2><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
                 else if (degree_bias) k_ns_select<1><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
                 else k_ns_select<0><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
