@@ -67,7 +67,9 @@ typedef enum {
     /* Table-1 walk variants, uniform proposal u = N(v)[below(U(EDGE), d)]: */
     CSAW_BIAS_MH = 6,           /* Metropolis-Hastings walk: accept iff below(U(ACCEPT), deg u) < deg v, else stay */
     CSAW_BIAS_RESTART = 7,      /* walk with restart: with probability pf return to the start vertex */
-    CSAW_BIAS_JUMP = 8          /* walk with jump: with probability pf jump to below(U(TARGET), V) */
+    CSAW_BIAS_JUMP = 8,         /* walk with jump: with probability pf jump to below(U(TARGET), V) */
+    CSAW_BIAS_SNOWBALL = 9      /* snowball sampling: every neighbour of every expanded vertex to
+                                   `depth` (select-all, R8); fanout ignored (may be NULL); sampling only */
 } csaw_bias_kind;
 
 typedef struct {
@@ -115,13 +117,24 @@ typedef struct {
  * (§5.2 workload-aware scheduling, the default), kernels read col_idx in place
  * from pinned, mapped host memory (zero-copy).  Useful
  * when a step needs one neighbour entry (MDRW, uniform walks); the device then
- * holds only row_ptr + deg + run state.  Other selectors return UNSUPPORTED. */
+ * holds only row_ptr + deg + run state.  Every selector is supported.  Without
+ * this flag (partition scheduling) csaw_walk implements MDRW, degree and uniform
+ * walks and csaw_sample neighbor / forest fire / snowball; others return
+ * UNSUPPORTED. */
 #define CSAW_GRAPH_OOM_ZEROCOPY 0x2u
 /* csaw_graph_opts.flags: csaw_sample always uses the level-synchronous batched
  * driver (one frontier queue mixing all instances) instead of the
  * fused one-warp-per-instance path chosen for small per-instance frontiers.
  * Outputs are identical either way (R7); this flag exists for tests/ablation. */
 #define CSAW_GRAPH_SAMPLE_BATCHED 0x4u
+/* csaw_graph_opts.flags, OOM ablation (Fig. 13-15; results unchanged):
+ * NO_WS  -- partitions are taken in round-robin id order (skipping empty queues)
+ *           and evicted first-in-first-out, instead of workload-aware scheduling
+ *           (busiest first, residents with work kept);
+ * NO_BAL -- every partition kernel of a wave gets the same CTA count instead of
+ *           CTAs proportional to its active count. */
+#define CSAW_GRAPH_OOM_NO_WS 0x8u
+#define CSAW_GRAPH_OOM_NO_BAL 0x10u
 
 typedef struct {
     int64_t num_vertices, num_edges;

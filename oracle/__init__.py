@@ -156,7 +156,7 @@ def n2v_scale(p, q) -> int:
 
 
 # ---------------------------------------------------------------- workloads
-KIND_UNIFORM, KIND_DEGREE, KIND_FF = 0, 1, 2
+KIND_UNIFORM, KIND_DEGREE, KIND_FF, KIND_SNOWBALL = 0, 1, 2, 3
 
 
 def neighbor_sample(g: Graph, kind, fanout, depth, seed_vertex, inst, rng_seed, pf=0.0,
@@ -255,7 +255,8 @@ def sample_instances(g: Graph, workload: str, seeds, instance_base, rng_seed, fa
         if workload == "layer":
             out.append(layer_sample(g, fanout, depth, int(seeds[i]), gi, rng_seed, a_max))
         else:
-            kind = {"uniform": KIND_UNIFORM, "degree": KIND_DEGREE, "forest_fire": KIND_FF}[workload]
+            kind = {"uniform": KIND_UNIFORM, "degree": KIND_DEGREE, "forest_fire": KIND_FF,
+                    "snowball": KIND_SNOWBALL}[workload]
             out.append(neighbor_sample(g, kind, fanout, depth, int(seeds[i]), gi, rng_seed, pf, a_max))
     return out
 

@@ -316,8 +316,9 @@ ORACLE_EXPORT int64_t oracle_ff_burn(uint64_t seed, uint32_t inst, uint32_t dept
 
 /*
  * Traversal sampling for one instance: neighbor sampling (bias 0 = uniform,
- * 1 = degree of the neighbour, R12) and forest fire (kind 2, uniform bias, k
- * per vertex from oracle_ff_burn).  Fig. 2(b) main loop:
+ * 1 = degree of the neighbour, R12), forest fire (kind 2, uniform bias, k
+ * per vertex from oracle_ff_burn) and snowball (kind 3: every
+ * neighbour of every expanded vertex, i.e. k = deg(v) -> select-all, R8).  Fig. 2(b) main loop:
  * FrontierPool <- seeds; per depth: NeighborPool = N(v) in CSR order, EdgeBias,
  * Select (select_wor), Update = post-filter of visited vertices (R9),
  * Sampled <- picks.  Each v in sorted(F) is one pool.
@@ -343,7 +344,8 @@ ORACLE_EXPORT int64_t oracle_neighbor_sample(const int64_t *row_ptr, const uint3
             uint32_t *b = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)(n > 0 ? n : 1));
             for (int64_t i = 0; i < n; i++)
                 b[i] = (kind == 1) ? (uint32_t)deg_of(&g, pool[i]) : 1u;
-            int64_t k = (kind == 2) ? oracle_ff_burn(rng_seed, inst, (uint32_t)d, v, n, pf) : fanout[d];
+            int64_t k = (kind == 2) ? oracle_ff_burn(rng_seed, inst, (uint32_t)d, v, n, pf)
+                      : (kind == 3) ? n : fanout[d];
             int64_t *picks = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
             int64_t np = oracle_select_wor(b, n, k, rng_seed, inst, (uint32_t)d, v, a_max, picks, attempts_out);
             for (int64_t p = 0; p < np; p++) {

@@ -50,7 +50,7 @@ CSAW_OK, CSAW_ERR_CAPACITY = 0, 5
 
 # csaw_bias_kind
 BIAS = {"uniform": 0, "degree": 1, "node2vec": 2, "forest_fire": 3, "layer": 4, "mdrw": 5, "mh": 6, "restart": 7,
-        "jump": 8}
+        "jump": 8, "snowball": 9}
 
 
 class csaw_bias(C.Structure):

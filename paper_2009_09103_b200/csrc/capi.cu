@@ -339,6 +339,8 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         auto& st = g->oomst;
         st.budget = o.device_budget_bytes;
         st.zerocopy = (o.flags & CSAW_GRAPH_OOM_ZEROCOPY) != 0;
+        st.ws = (o.flags & CSAW_GRAPH_OOM_NO_WS) == 0;
+        st.bal = (o.flags & CSAW_GRAPH_OOM_NO_BAL) == 0;
         st.P = o.num_partitions > 0 ? o.num_partitions : 4;
         st.R = o.max_resident > 0 ? o.max_resident : 2;
         st.S = o.num_streams > 0 ? o.num_streams : 2;
@@ -506,7 +508,10 @@ CSAW_API csaw_status csaw_sample_capacity(const csaw_bias* bias, const int32_t* 
     clear_error();
     if (!bias || !cap || n < 0 || depth < 0) return fail(CSAW_ERR_INVALID_ARG, "bad argument");
     double total = 0;
-    if (bias->kind == CSAW_BIAS_FOREST_FIRE) {
+    if (bias->kind == CSAW_BIAS_SNOWBALL) {
+        // unbounded (a BFS ball): a first guess; csaw_sample reports the exact size on CAPACITY
+        total = 64.0 * n * depth + 1024;
+    } else if (bias->kind == CSAW_BIAS_FOREST_FIRE) {
         // mean burn count pf/(1-pf) per expanded vertex; 4x headroom + slack
         const double m = bias->pf / std::max(1e-9, 1.0 - bias->pf);
         double level = 1.0;
@@ -528,7 +533,7 @@ CSAW_API csaw_status csaw_sample_capacity(const csaw_bias* bias, const int32_t* 
 
 static csaw_status check_bias(const csaw_bias* b) {
     if (!b) return fail(CSAW_ERR_INVALID_ARG, "bias is NULL");
-    if (b->kind < CSAW_BIAS_UNIFORM || b->kind > CSAW_BIAS_JUMP) return fail(CSAW_ERR_INVALID_ARG, "unknown bias kind");
+    if (b->kind < CSAW_BIAS_UNIFORM || b->kind > CSAW_BIAS_SNOWBALL) return fail(CSAW_ERR_INVALID_ARG, "unknown bias kind");
     if (b->migration < 0 || b->migration > 2) return fail(CSAW_ERR_INVALID_ARG, "migration must be 0, 1 or 2");
     if (b->a_max != 0 && (b->a_max < 2 || b->a_max > 16382 || (b->a_max & 1)))
         return fail(CSAW_ERR_INVALID_ARG, "a_max must be 0 (default 64) or even in [2, 16382]");
@@ -540,8 +545,8 @@ CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32
     CSAW_TRY(begin_call(g));
     CSAW_TRY(check_bias(bias));
     const csaw_bias b = *bias;
-    if (b.kind == CSAW_BIAS_FOREST_FIRE || b.kind == CSAW_BIAS_LAYER)
-        return fail(CSAW_ERR_INVALID_ARG, "forest fire / layer are sampling selectors (use csaw_sample)");
+    if (b.kind == CSAW_BIAS_FOREST_FIRE || b.kind == CSAW_BIAS_LAYER || b.kind == CSAW_BIAS_SNOWBALL)
+        return fail(CSAW_ERR_INVALID_ARG, "forest fire / layer / snowball are sampling selectors (use csaw_sample)");
     if (length < 0 || n < 0) return fail(CSAW_ERR_INVALID_ARG, "negative length / n_walkers");
     if (b.kind == CSAW_BIAS_NODE2VEC && !(b.p > 0 && b.q > 0 && std::isfinite(b.p) && std::isfinite(b.q)))
         return fail(CSAW_ERR_INVALID_ARG, "node2vec needs finite p, q > 0");
@@ -573,13 +578,10 @@ CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32
     }
     csaw_status s;
     if (g->oom && g->oomst.zerocopy) {
-        if (b.kind != CSAW_BIAS_MDRW && b.kind != CSAW_BIAS_UNIFORM)
-            return fail(CSAW_ERR_UNSUPPORTED, "zero-copy OOM mode implements MDRW and uniform walks");
-        s = run_walk(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
+        s = run_walk(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);   // every kernel reads h_col
     } else if (g->oom) {
-        if (b.kind != CSAW_BIAS_MDRW)
-            return fail(CSAW_ERR_UNSUPPORTED, "OOM-mode walks implement MDRW (config 5)");
-        s = run_mdrw_oom(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
+        if (b.kind == CSAW_BIAS_MDRW) s = run_mdrw_oom(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
+        else s = run_walk_oom(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
     } else {
         s = run_walk(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
     }
@@ -598,7 +600,8 @@ CSAW_API csaw_status csaw_sample(const csaw_graph* g, const csaw_bias* bias, con
     CSAW_TRY(begin_call(g));
     CSAW_TRY(check_bias(bias));
     const csaw_bias b = *bias;
-    if (b.kind == CSAW_BIAS_NODE2VEC || b.kind == CSAW_BIAS_MDRW || b.kind >= CSAW_BIAS_MH)
+    if (b.kind == CSAW_BIAS_NODE2VEC || b.kind == CSAW_BIAS_MDRW || b.kind == CSAW_BIAS_MH ||
+        b.kind == CSAW_BIAS_RESTART || b.kind == CSAW_BIAS_JUMP)
         return fail(CSAW_ERR_INVALID_ARG, "node2vec / MDRW / MH / restart / jump are walk selectors (use csaw_walk)");
     if (!num_edges) return fail(CSAW_ERR_INVALID_ARG, "num_edges is NULL");
     *num_edges = 0;
@@ -606,7 +609,7 @@ CSAW_API csaw_status csaw_sample(const csaw_graph* g, const csaw_bias* bias, con
     if (n < 0 || capacity < 0) return fail(CSAW_ERR_INVALID_ARG, "negative n_instances / capacity");
     if (b.kind == CSAW_BIAS_FOREST_FIRE && !(b.pf >= 0.0 && b.pf < 1.0))
         return fail(CSAW_ERR_INVALID_ARG, "forest fire needs pf in [0, 1)");
-    if (b.kind != CSAW_BIAS_FOREST_FIRE) {
+    if (b.kind != CSAW_BIAS_FOREST_FIRE && b.kind != CSAW_BIAS_SNOWBALL) {
         if (!fanout) return fail(CSAW_ERR_INVALID_ARG, "fanout is NULL");
         for (int d = 0; d < depth; ++d)
             if (fanout[d] < 0 || fanout[d] >= (1 << 14)) return fail(CSAW_ERR_INVALID_ARG, "fanout must be in [0, 2^14)");

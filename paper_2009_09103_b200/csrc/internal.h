@@ -81,7 +81,29 @@ struct OomState {
     uint32_t* d_slots = nullptr;   // R arena slots of col entries
     std::vector<int32_t> resident; // partition id per slot (-1 = empty)
     std::vector<cudaStream_t> streams;
+    // ablation switches (Fig. 13-15): workload-aware scheduling, thread-block balancing
+    bool ws = true;
+    bool bal = true;
+    int32_t rr = 0;                // round-robin cursor (ws off)
+    int32_t fifo = 0;              // eviction cursor (ws off)
 };
+
+// One partition sampled in a wave: its arena slot and whether it is transferred now.
+struct WavePick {
+    int32_t p;
+    int32_t slot;
+    bool fresh;
+};
+// Choose this wave's partitions and slots from the per-partition active counts
+// (updates os.resident); see oom.cu.
+std::vector<WavePick> oom_plan_wave(OomState& os, const std::vector<uint64_t>& cnt);
+// Enqueue the col-slice transfer of partition p into `slot` on the slot's stream,
+// ordered after `after`; appends a timing event pair to tev and counts the load.
+csaw_status oom_load(const csaw_graph* g, int32_t p, int32_t slot, cudaEvent_t after, std::vector<cudaEvent_t>& tev);
+// Sum the transfer event pairs into stats.transfer_ms (after a sync) and destroy them.
+void oom_account_transfers(const csaw_graph* g, std::vector<cudaEvent_t>& tev);
+// CTAs for a partition kernel: proportional to its active count (BAL) or an even split.
+int oom_blocks(const OomState& os, int blocks_total, uint64_t c, uint64_t wave_total, size_t nchosen, int warps);
 
 }  // namespace csaw
 
@@ -150,5 +172,7 @@ csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int
                               uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
                               bool out_on_device, cudaStream_t st);
 csaw_status run_mdrw_oom(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds,
+                         int64_t n, uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st);
+csaw_status run_walk_oom(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds,
                          int64_t n, uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st);
 }  // namespace csaw

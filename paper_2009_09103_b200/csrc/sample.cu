@@ -77,7 +77,7 @@ __global__ void k_ns_bound(const int64_t* __restrict__ rp, const uint32_t* __res
         const uint32_t k = ff ? ff_burn(key, base + qi[q], d, v, deg, theta) : fanout;
         kq[q] = k;
         ub[q] = min(k, deg);
-        mk = max(mk, min(k, deg));
+        if (k < deg) mk = max(mk, k);   // select-all pools (k >= deg) need no pick list / draw index
     }
     mk = __reduce_max_sync(FULL, mk);
     if ((threadIdx.x & 31) == 0 && mk) atomicMax(kmax, mk);
@@ -975,81 +975,46 @@ static csaw_status oom_select_level(const csaw_graph* g, const csaw_bias& b, con
     k_part_scatter<<<grid_for(g, nq), 256, 0, st>>>(qv, nq, own, fill, idx);
     note_launch();
     CSAW_CUDA(cudaGetLastError());
-    // workload-aware waves: residents with work stay; free / idle slots take the busiest
-    std::vector<bool> done(P, false);
-    for (uint32_t p = 0; p < P; ++p) done[p] = c[p] == 0;
-    std::vector<int32_t>& res = os.resident;
+    // waves over the partitions with entries (oom_plan_wave: workload-aware, or the
+    // round-robin ablation); each partition of the level is sampled exactly once
+    std::vector<uint64_t> left(c);
+    std::vector<cudaEvent_t> tev;
     cudaEvent_t evs;
     CSAW_CUDA(cudaEventCreateWithFlags(&evs, cudaEventDisableTiming));
-    CSAW_CUDA(cudaEventRecord(evs, st));
+    const int blocks_total = g->num_sms * 8;
     for (;;) {
-        std::vector<int32_t> order;
-        for (uint32_t p = 0; p < P; ++p) if (!done[p]) order.push_back(static_cast<int32_t>(p));
-        if (order.empty()) break;
-        std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return c[x] > c[y]; });
-        std::vector<std::pair<int32_t, int>> wave;   // (partition, slot)
-        for (int s = 0; s < os.R; ++s)
-            if (res[s] >= 0 && !done[res[s]]) wave.push_back({res[s], s});
-        for (int32_t p : order) {
-            if (static_cast<int>(wave.size()) >= os.R) break;
-            bool inwave = false;
-            for (auto& w : wave) inwave |= w.first == p;
-            if (inwave) continue;
-            int slot = -1;
-            for (int s = 0; s < os.R && slot < 0; ++s) {
-                bool used = false;
-                for (auto& w : wave) used |= w.second == s;
-                if (!used) slot = s;
-            }
-            if (slot < 0) break;
-            res[slot] = p;
-            const int sidx = slot % os.S;
-            CSAW_CUDA(cudaStreamWaitEvent(os.streams[sidx], evs, 0));
-            cudaEvent_t t0, t1;
-            CSAW_CUDA(cudaEventCreate(&t0));
-            CSAW_CUDA(cudaEventCreate(&t1));
-            CSAW_CUDA(cudaEventRecord(t0, os.streams[sidx]));
-            const int64_t ne = os.ebeg[p + 1] - os.ebeg[p];
-            CSAW_CUDA(cudaMemcpyAsync(os.d_slots + static_cast<int64_t>(slot) * os.slot_edges, os.h_col + os.ebeg[p],
-                                      sizeof(uint32_t) * ne, cudaMemcpyHostToDevice, os.streams[sidx]));
-            CSAW_CUDA(cudaEventRecord(t1, os.streams[sidx]));
-            CSAW_CUDA(cudaEventSynchronize(t1));
-            float ms = 0;
-            cudaEventElapsedTime(&ms, t0, t1);
-            cudaEventDestroy(t0);
-            cudaEventDestroy(t1);
-            g->stats.transfer_ms += ms;
-            g->stats.partition_loads += 1;
-            g->stats.h2d_bytes += sizeof(uint32_t) * ne;
-            wave.push_back({p, slot});
-        }
+        bool any = false;
+        for (uint32_t p = 0; p < P; ++p) any |= left[p] > 0;
+        if (!any) break;
+        const std::vector<WavePick> wave = oom_plan_wave(os, left);
+        CSAW_CUDA(cudaEventRecord(evs, st));
+        for (const WavePick& w : wave)
+            if (w.fresh) CSAW_TRY(oom_load(g, w.p, w.slot, evs, tev));
         uint64_t wave_total = 0;
-        for (auto& w : wave) wave_total += c[w.first];
-        for (auto& w : wave) {
-            const int32_t p = w.first;
-            const int sidx = w.second % os.S;
-            CSAW_CUDA(cudaStreamWaitEvent(os.streams[sidx], evs, 0));
-            const int total_blocks = g->num_sms * 8;
-            int blocks = static_cast<int>(std::max<uint64_t>(1, total_blocks * c[p] / std::max<uint64_t>(wave_total, 1)));
-            blocks = std::min<int>(blocks, static_cast<int>((c[p] + SEL_WARPS - 1) / SEL_WARPS));   // P:850 balancing
-            const uint32_t* colp = os.d_slots + static_cast<int64_t>(w.second) * os.slot_edges - os.ebeg[p];
+        for (const WavePick& w : wave) wave_total += left[w.p];
+        for (const WavePick& w : wave) {
+            const int32_t p = w.p;
+            cudaStream_t ss = os.streams[w.slot % os.S];
+            CSAW_CUDA(cudaStreamWaitEvent(ss, evs, 0));
+            const int blocks = oom_blocks(os, blocks_total, left[p], wave_total, wave.size(), SEL_WARPS);
+            const uint32_t* colp = os.d_slots + static_cast<int64_t>(w.slot) * os.slot_edges - os.ebeg[p];
             SelArgs sa{g->row_ptr, colp, g->deg, qv, qi, nq, kq, ub, eoff, s_inst, s_src, s_dst, d, base, key, a_max,
                        glist, kmax, counters, nullptr, nullptr, nullptr, nullptr, static_cast<uint32_t>(b.migration),
                        idx + off[p], c[p]};
-            CSAW_TRY(hot_begin(g, os.streams[sidx]));
-            if (degree_bias) k_ns_select<1><<<std::max(1, blocks), SEL_WARPS * 32, 0, os.streams[sidx]>>>(sa);
-            else k_ns_select<0><<<std::max(1, blocks), SEL_WARPS * 32, 0, os.streams[sidx]>>>(sa);
+            CSAW_TRY(hot_begin(g, ss));
+            if (degree_bias) k_ns_select<1><<<blocks, SEL_WARPS * 32, 0, ss>>>(sa);
+            else k_ns_select<0><<<blocks, SEL_WARPS * 32, 0, ss>>>(sa);
             note_launch();
             CSAW_CUDA(cudaGetLastError());
-            CSAW_TRY(hot_end(g, os.streams[sidx]));
-            done[p] = true;
+            CSAW_TRY(hot_end(g, ss));
+            left[p] = 0;
         }
         for (int s = 0; s < os.S; ++s) {
             CSAW_CUDA(cudaEventRecord(evs, os.streams[s]));
             CSAW_CUDA(cudaStreamWaitEvent(st, evs, 0));
         }
-        CSAW_CUDA(cudaEventRecord(evs, st));
     }
+    oom_account_transfers(g, tev);
     cudaEventDestroy(evs);
     return CSAW_OK;
 }
@@ -1177,7 +1142,7 @@ csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* f
                        const uint32_t* d_seeds, int64_t n_i64, uint64_t base, uint64_t seed, uint64_t* d_offsets,
                        uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
                        bool out_on_device, cudaStream_t st) {
-    if (!g->force_batched && (!g->oom || g->oomst.zerocopy)) {
+    if (!g->force_batched && (!g->oom || g->oomst.zerocopy) && b.kind != CSAW_BIAS_SNOWBALL) {
         const csaw_status s = run_sample_fused(g, b, fanout, depth, d_seeds, static_cast<uint64_t>(n_i64), base, seed,
                                                d_offsets, src, dst, dep, capacity, num_edges, out_on_device, st);
         if (s != FUSED_FALLBACK) return s;
@@ -1194,6 +1159,7 @@ csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int
     const uint64_t n = static_cast<uint64_t>(n_i64);
     const bool layer = b.kind == CSAW_BIAS_LAYER;
     const bool ff = b.kind == CSAW_BIAS_FOREST_FIRE;
+    const bool snow = b.kind == CSAW_BIAS_SNOWBALL;   // uniform bias, k = all (select-all path, R8)
     const bool degree_bias = b.kind == CSAW_BIAS_DEGREE;
     // zero-copy OOM mode reads col_idx in place from pinned host memory (UVA)
     const uint32_t* colz = g->oom ? g->oomst.h_col : g->col;
@@ -1251,7 +1217,7 @@ csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int
         CSAW_TRY(lvl_buf(g, l, 3, nwork, &ub));
         CSAW_TRY(lvl_buf(g, l, 4, nwork + 1, &eoff));
         uint64_t* qpref = nullptr;
-        const uint32_t fan = ff ? 0u : static_cast<uint32_t>(fanout[l]);
+        const uint32_t fan = ff ? 0u : snow ? 0xFFFFFFFFu : static_cast<uint32_t>(fanout[l]);
         CSAW_CUDA(cudaMemsetAsync(kmaxd, 0, sizeof(unsigned), st));
         if (layer) {
             CSAW_TRY(lvl_buf(g, l, 5, nq + 1, &qpref));

@@ -27,7 +27,8 @@ def check_sample(G, og, workload, seeds, fanout=(), depth=None, rng_seed=1, inst
                  a_max=0, instances=None, migration="brs"):
     """Run csaw_sample and compare every instance (or `instances`) with the oracle, element by element."""
     depth = len(fanout) if depth is None else depth
-    kind = {"degree": "degree", "uniform": "uniform", "forest_fire": "forest_fire", "layer": "layer"}[workload]
+    kind = {"degree": "degree", "uniform": "uniform", "forest_fire": "forest_fire", "layer": "layer",
+            "snowball": "snowball"}[workload]
     seeds_t = torch.as_tensor(np.asarray(seeds).astype(np.uint32).view(np.int32)).to(DEV)
     b = cs.make_bias(kind, pf=pf, a_max=a_max, migration=migration)
     offs, src, dst, dep = cs.csaw_sample(G, b, seeds_t, fanout=fanout, depth=depth, rng_seed=rng_seed,
@@ -53,7 +54,8 @@ def _compare_instances(og, workload, seeds, fanout, depth, rng_seed, instance_ba
         if workload == "layer":
             es, ed, ee = O.layer_sample(og, fanout, depth, int(seeds[i]), gi, rng_seed, am)
         else:
-            k = {"degree": O.KIND_DEGREE, "uniform": O.KIND_UNIFORM, "forest_fire": O.KIND_FF}[workload]
+            k = {"degree": O.KIND_DEGREE, "uniform": O.KIND_UNIFORM, "forest_fire": O.KIND_FF,
+                 "snowball": O.KIND_SNOWBALL}[workload]
             es, ed, ee = O.neighbor_sample(og, k, fanout, depth, int(seeds[i]), gi, rng_seed, pf, am)
         a, bnd = int(offs[i]), int(offs[i + 1])
         assert bnd - a == es.size, f"instance {i}: {bnd - a} edges vs oracle {es.size}"

@@ -97,8 +97,48 @@ def test_oom_zerocopy_equals_in_memory(medium):
                        cs.csaw_walk(Gz, cs.make_bias("mdrw"), seeds, L, rng_seed=5))
     s1 = seeds[:, 0].contiguous()
     assert torch.equal(cs.csaw_walk(Gm, "uniform", s1, L, rng_seed=6), cs.csaw_walk(Gz, "uniform", s1, L, rng_seed=6))
-    with pytest.raises(cs.CsawError) as ei:
-        cs.csaw_walk(Gz, "degree", s1, 10)
-    assert ei.value.status == 8
+    assert torch.equal(cs.csaw_walk(Gm, "degree", s1, 60, rng_seed=7), cs.csaw_walk(Gz, "degree", s1, 60, rng_seed=7))
     Gm.close()
     Gz.close()
+
+
+@pytest.mark.parametrize("kind", ["degree", "uniform"])
+@pytest.mark.parametrize("P,R,S,ws,bal", [(4, 2, 2, True, True), (3, 1, 1, True, True), (5, 2, 2, False, True),
+                                          (4, 2, 2, True, False), (4, 2, 1, False, False)])
+def test_oom_walk_equals_in_memory(medium, kind, P, R, S, ws, bal):
+    """Fig. 13(b) workload: degree-biased / uniform walks under partition scheduling
+    (walkers migrate between per-partition queues); schedule switches never change results."""
+    g = medium
+    seeds = mdrw_seeds(g, 300, 1)[:, 0].contiguous().to(DEV)
+    L = 120
+    Gm = cs.csaw_graph_create(g.row_ptr.to(DEV), g.col_idx.to(DEV))
+    ref = cs.csaw_walk(Gm, kind, seeds, L, rng_seed=4, instance_base=9)
+    Go = cs.csaw_graph_create(g.row_ptr, g.col_idx, budget_bytes=budget_for(g, P, R, 1, 1) + (1 << 20),
+                              num_partitions=P, max_resident=R, num_streams=S, oom_ws=ws, oom_bal=bal)
+    got = cs.csaw_walk(Go, kind, seeds, L, rng_seed=4, instance_base=9)
+    assert torch.equal(ref, got)
+    st = cs.csaw_stats(Go)
+    assert st["sampled_edges"] == 300 * L and st["partition_loads"] >= 1
+    if kind == "degree":
+        assert st["neighbours_scanned"] > 0
+    Gm.close()
+    Go.close()
+
+
+@pytest.mark.parametrize("ws,bal", [(False, True), (True, False), (False, False)])
+def test_oom_schedule_switches_keep_results(medium, ws, bal):
+    g = medium
+    n, m, L = 32, 100, 150
+    seeds = mdrw_seeds(g, n, m).to(DEV)
+    Gm = cs.csaw_graph_create(g.row_ptr.to(DEV), g.col_idx.to(DEV))
+    Go = cs.csaw_graph_create(g.row_ptr, g.col_idx, budget_bytes=budget_for(g, 4, 2, n, m), num_partitions=4,
+                              max_resident=2, oom_ws=ws, oom_bal=bal)
+    assert torch.equal(cs.csaw_walk(Gm, cs.make_bias("mdrw"), seeds, L, rng_seed=5),
+                       cs.csaw_walk(Go, cs.make_bias("mdrw"), seeds, L, rng_seed=5))
+    s1 = seeds[:, 0].contiguous()
+    a = cs.csaw_sample(Gm, "degree", s1, fanout=[4, 3], rng_seed=2)
+    b = cs.csaw_sample(Go, "degree", s1, fanout=[4, 3], rng_seed=2)
+    for x, y in zip(a, b):
+        assert torch.equal(x.cpu(), y.cpu())
+    Gm.close()
+    Go.close()

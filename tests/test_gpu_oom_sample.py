@@ -113,3 +113,17 @@ def test_oom_zerocopy_sample_equals_in_memory(medium, kind):
     assert cs.csaw_stats(Gz)["partition_loads"] == 0
     Gm.close()
     Gz.close()
+
+
+def test_oom_snowball_equals_in_memory(medium):
+    g = medium
+    seeds = instance_seeds(g, 40, set_id=8).to(DEV)
+    Gm = cs.csaw_graph_create(g.row_ptr.to(DEV), g.col_idx.to(DEV))
+    ref = _run(Gm, "snowball", seeds, [], 2)
+    Go = cs.csaw_graph_create(g.row_ptr, g.col_idx, budget_bytes=oom_budget(g, 4, 2), num_partitions=4,
+                              max_resident=2)
+    got = _run(Go, "snowball", seeds, [], 2)
+    for a, b in zip(ref, got):
+        assert torch.equal(a.cpu(), b.cpu())
+    Gm.close()
+    Go.close()

@@ -402,3 +402,36 @@ def test_jump_law(G):
         u = O.walk_variant_step(G, O.KIND_JUMP, pr, 0, 0, inst, 1, 5)
         counts[u] = counts.get(u, 0) + 1
     assert chi2(counts, probs, N) > 1e-4
+
+
+def _bfs_ball_edges(og, seed, depth):
+    """Snowball sampling written out as a plain BFS: every edge out of
+    every vertex first reached at distance < depth, tagged with its distance + 1."""
+    dist = {seed: 0}
+    layer = [seed]
+    out = []
+    for d in range(depth):
+        nxt = []
+        for v in layer:
+            for u in og.nbrs(v).tolist():
+                out.append((d + 1, v, int(u)))
+                if u not in dist:
+                    dist[u] = d + 1
+                    nxt.append(int(u))
+        layer = nxt
+    return sorted(out)
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_snowball_is_the_bfs_ball(G, R, depth):
+    """NEXT-3 snowball = select-all neighbor sampling; pinned to a BFS written here."""
+    og, tg = R
+    cases = [(G, v) for v in range(G.V) if G.deg(v) > 0]
+    cases += [(og, int(s)) for s in instance_seeds(tg, 6).numpy()]
+    for i, (g, sd) in enumerate(cases):
+        s, d, e = O.neighbor_sample(g, O.KIND_SNOWBALL, [], depth, sd, i, 3)
+        got = sorted(zip(e.tolist(), s.tolist(), d.tolist()))
+        assert got == _bfs_ball_edges(g, sd, depth)
+        # no draws: independent of the RNG seed and instance id
+        s2, d2, e2 = O.neighbor_sample(g, O.KIND_SNOWBALL, [], depth, sd, i + 7, 11)
+        assert np.array_equal(s, s2) and np.array_equal(d, d2) and np.array_equal(e, e2)
