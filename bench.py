@@ -387,7 +387,9 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        torch.cuda.nvtx.range_push("csaw_step")   # lets ncu select the timed launches (--nvtx-include csaw_step/)
         edges += step()
+        torch.cuda.nvtx.range_pop()
         e1.record(stream)
         evs.append((e0, e1))
         st = cs.csaw_stats(G)
@@ -482,7 +484,12 @@ def main():
     bytes_per_launch = alg_bytes / max(hot_launches, 1)
     achieved = bytes_per_launch / (hot_avg_ms / 1000.0) / 1e9 if hot_avg_ms > 0 else None
     peak = peaks.get("hbm_gbs", 6650.0)
-    traffic = load_traffic(cfg.name)
+    variant = cfg.name
+    if cfg.oom_budget_bytes and args.in_memory:
+        variant += "_inmem"
+    elif not ginfo.get("ctps_cache") and cfg.bias in ("degree", "layer") and not ginfo.get("oom_mode"):
+        variant += "_scan"
+    traffic = load_traffic(variant)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "kernel": hot_kernel_name(cfg, bool(ginfo.get("ctps_cache")), bool(ginfo.get("oom_mode"))), "alg_bytes_per_launch": bytes_per_launch,

@@ -1,0 +1,107 @@
+"""Summarise ncu `--page raw --csv` exports (one full capture per config) into a
+markdown table and refresh profiles/ncu_traffic.json (DRAM bytes per launch of
+each config's hot kernel, which bench.py reports as roofline.traffic).
+
+    python scripts/ncu_summary.py gpurun_out/prof r01 > profiles/r01_ncu_summary.md
+"""
+import csv
+import glob
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+        "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
+
+METRICS = [
+    ("time", "gpu__time_duration.sum"),
+    ("dram_rd", "dram__bytes_read.sum"),
+    ("dram_wr", "dram__bytes_write.sum"),
+    ("dram_pct", "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+    ("l2_hit", "lts__t_sector_hit_rate.pct"),
+    ("l1_hit", "l1tex__t_sector_hit_rate.pct"),
+    ("l2_rd_sectors", "lts__t_sectors_srcunit_tex_op_read.sum"),
+    ("bytes_per_sector", "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio"),
+    ("warps_active", "sm__warps_active.avg.pct_of_peak_sustained_active"),
+    ("issue_active", "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+    ("sm_thr", "sm__throughput.avg.pct_of_peak_sustained_elapsed"),
+    ("mem_thr", "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed"),
+    ("regs", "launch__registers_per_thread"),
+    ("grid", "launch__grid_size"),
+    ("block", "launch__block_size"),
+]
+
+
+def load(path):
+    rows = list(csv.reader(open(path)))
+    if len(rows) < 3:
+        return None
+    h, u, v = rows[0], rows[1], rows[2]
+    d = {"kernel": v[h.index("Kernel Name")].split("(")[0]}
+    for key, m in METRICS:
+        if m in h:
+            i = h.index(m)
+            try:
+                x = float(v[i].replace(",", ""))
+            except ValueError:
+                continue
+            d[key] = x * UNIT.get(u[i], 1.0) if u[i] in UNIT else x
+    stalls = []
+    for i, name in enumerate(h):
+        if name.startswith("smsp__average_warps_issue_stalled_") and name.endswith("_per_issue_active.ratio"):
+            try:
+                stalls.append((float(v[i]), name[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+            except ValueError:
+                pass
+    stalls.sort(reverse=True)
+    d["stalls"] = stalls[:3]
+    return d
+
+
+def main():
+    src = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/prof"
+    rnd = sys.argv[2] if len(sys.argv) > 2 else "r01"
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)
+    out = [f"# {rnd} — ncu `--set full` summary, one hot-kernel launch per config", "",
+           "Each row: `ncu --set full --clock-control none --import-source on --nvtx --nvtx-include csaw_step/ "
+           "-k regex:<kernel> -c 1` around `bench.py --config <cfg> --steps 1 --warmup 1` "
+           "(cfg3: `scripts/prof_n2v.py 40`, a 1/40 walker subset), exported with `ncu -i --page raw --csv` "
+           "(`scripts/gpu_prof_all.sh`, `scripts/ncu_summary.py`).  ncu times are cold-cache and serialised: "
+           "the bench line's CUDA-event numbers are the measurement; these explain them.", "",
+           f"DRAM GB/s is ncu DRAM bytes / ncu duration; fraction of the measured {peak:.1f} GB/s copy peak.", "",
+           "| config | kernel | ncu ms | DRAM rd+wr | DRAM GB/s (frac) | L2 hit | L1 hit | B used/sector (ld) | warps active | issue active | regs | grid x block | top stalls (per issue) |",
+           "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+    traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        traffic = json.load(open(traffic_path))
+    except Exception:
+        traffic = {}
+    for path in sorted(glob.glob(os.path.join(src, "*_raw.csv"))):
+        cfg = os.path.basename(path)[:-len("_raw.csv")]
+        d = load(path)
+        if not d or "time" not in d:
+            continue
+        dram = d.get("dram_rd", 0) + d.get("dram_wr", 0)
+        gbs = dram / d["time"] / 1e9
+        st = ", ".join(f"{n} {x:.1f}" for x, n in d["stalls"])
+        out.append(f"| {cfg} | `{d['kernel']}` | {d['time'] * 1e3:.3f} | {dram / 1e9:.3f} GB | {gbs:.0f} ({gbs / peak:.3f}) | "
+                   f"{d.get('l2_hit', 0):.1f} % | {d.get('l1_hit', 0):.1f} % | {d.get('bytes_per_sector', 0):.1f} | "
+                   f"{d.get('warps_active', 0):.1f} % | {d.get('issue_active', 0):.1f} % | {d.get('regs', 0):.0f} | "
+                   f"{d.get('grid', 0):.0f} x {d.get('block', 0):.0f} | {st} |")
+        key = cfg.replace("@", "_")   # e.g. cfg5_inmem, cfg2_scan (bench.py picks the key of its variant)
+        if cfg == "cfg3_subset40":
+            note = "1/40 walker subset (scripts/prof_n2v.py); per launch of that subset"
+        else:
+            note = "per launch of the bench's hot kernel (1 bench step)"
+        traffic[key] = {"kernel": d["kernel"], "dram_bytes_per_launch": int(dram), "ncu_ms": d["time"] * 1e3,
+                        "round": rnd, "note": note}
+    traffic["_source"] = ("ncu --set full --clock-control none (profiles/%s_ncu_summary.md); "
+                          "dram__bytes_read.sum + dram__bytes_write.sum per launch of the hot kernel" % rnd)
+    json.dump(traffic, open(traffic_path, "w"), indent=1)
+    print("\n".join(out))
+
+
+if __name__ == "__main__":
+    main()
