@@ -98,6 +98,9 @@ def algorithmic_bytes(cfg, st, n, edges):
     sampling select kernel: 16 per pool + 8 per scanned candidate + 12 per staged edge."""
     scanned, pools = st["neighbours_scanned"], st["pools"]
     probes = st.get("cache_probes", 0)
+    if st.get("index_bytes") and cfg.workload == "walk":
+        # narrow walk index: record 16 + node / leaf (+ col) entries read, counted in the kernel, + path
+        return st["index_bytes"] + 4 * n * (cfg.length + 1) + 4 * n
     if probes and cfg.workload == "walk":
         # cached CTPS: row_ptr pair 16 + T 8 + col 4 per step, 8 per cache probe, + path
         return 28 * pools + 8 * probes + 4 * n * (cfg.length + 1) + 4 * n
@@ -489,10 +492,12 @@ def main():
         variant += "_inmem"
     elif not ginfo.get("ctps_cache") and cfg.bias in ("degree", "layer") and not ginfo.get("oom_mode"):
         variant += "_scan"
-    traffic = load_traffic(variant)
+    kname = hot_kernel_name(cfg, bool(ginfo.get("ctps_cache")), bool(ginfo.get("oom_mode")),
+                            int(ginfo.get("walk_index_leaf") or 0), int(ginfo.get("walk_index_group") or 0))
+    traffic = load_traffic(variant, kname)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": hot_kernel_name(cfg, bool(ginfo.get("ctps_cache")), bool(ginfo.get("oom_mode"))), "alg_bytes_per_launch": bytes_per_launch,
+            "kernel": kname, "alg_bytes_per_launch": bytes_per_launch,
             "hot_ms_per_launch": hot_avg_ms, "hot_share_of_step": (hot_ms / total_ms) if total_ms else None,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
 
@@ -591,8 +596,10 @@ def run_e2e(cs, G, bias, seeds, cfg, base, args, kind, n, dev, world):
             "steps": steps, "timing": "host wall clock around the synchronous C-ABI call (max over ranks)"}
 
 
-def hot_kernel_name(cfg, cached=False, oom=False):
+def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0):
     if cfg.workload == "walk":
+        if cfg.bias == "degree" and wix_leaf:
+            return f"k_walk_wix<{wix_leaf}>" if wix_group == 32 else f"k_walk_wixg<{wix_group}, {wix_leaf}>"
         return "k_walk_cached" if (cfg.bias == "degree" and cached) else f"k_walk<{cfg.bias}>"
     if cfg.workload == "mdrw":
         return "k_mdrw_oom_part" if oom else "k_mdrw"
@@ -616,14 +623,20 @@ def load_peaks() -> dict:
         return {}
 
 
-def load_traffic(cfg_name):
+def load_traffic(cfg_name, kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the hot kernel, from the
-    committed ncu --set full capture summary (profiles/ncu_traffic.json), else null."""
+    committed ncu --set full capture summary (profiles/ncu_traffic.json), else null.  Only
+    a capture of the same kernel counts (a stale entry for another variant is ignored)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
         v = d.get(cfg_name)
-        return v.get("dram_bytes_per_launch") if isinstance(v, dict) else v
+        if not isinstance(v, dict):
+            return None
+        norm = lambda k: k.replace("void ", "").replace("csaw::", "").replace(" ", "")
+        if norm(v.get("kernel", "")) != norm(kernel):
+            return None
+        return v.get("dram_bytes_per_launch")
     except Exception:
         return None
 

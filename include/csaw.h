@@ -135,6 +135,12 @@ typedef struct {
  *           CTAs proportional to its active count. */
 #define CSAW_GRAPH_OOM_NO_WS 0x8u
 #define CSAW_GRAPH_OOM_NO_BAL 0x10u
+/* csaw_graph_opts.flags, with CSAW_GRAPH_CTPS_CACHE: do not build the narrow walk
+ * index (paper_2009_09103_b200/csrc/wix.cuh; one 16 B record per vertex, S as u32,
+ * fanout-128 internal nodes, built only when every row total is < 2^32).  Degree
+ * walks then search the u64 fanout-32 index instead.  Results are identical
+ * either way; this flag exists for tests and A/B measurements. */
+#define CSAW_GRAPH_NO_WALK_INDEX 0x20u
 
 typedef struct {
     int64_t num_vertices, num_edges;
@@ -144,8 +150,10 @@ typedef struct {
     int32_t oom_mode;               /* 1 if created with a device budget */
     int64_t device_bytes;           /* device memory held by the graph (CSR + degree + scratch) */
     int32_t ctps_cache;             /* 1 if the static-bias CTPS cache was built */
-    int32_t reserved;
+    int32_t walk_index_leaf;        /* narrow walk index leaf fanout (32/64/128; 129 = col read after the leaf), 0 = not built */
     double cache_build_ms;          /* device time of the cache build */
+    int32_t walk_index_group;       /* lanes per walker of the degree-walk kernel (8 / 16; 32 = one warp per walker) */
+    int32_t reserved;
 } csaw_graph_info_t;
 
 typedef struct csaw_graph csaw_graph;  /* opaque */
@@ -164,6 +172,7 @@ typedef struct {
     double kernel_ms;               /* device time, first launch -> last completion (CUDA events) */
     double hot_kernel_ms;           /* summed device time of the hot-kernel launches (CUDA events) */
     double transfer_ms;             /* OOM: partition-transfer time */
+    uint64_t index_bytes;           /* bytes of walk-index records, nodes, leaves and col entries read (narrow walk index) */
 } csaw_run_stats;
 
 /* Create a graph on opt->device (opt may be NULL: device 0, in-memory).

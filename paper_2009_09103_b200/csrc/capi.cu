@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "wix.cuh"
 #include "util.cuh"
 
 namespace csaw {
@@ -253,6 +254,127 @@ __global__ void k_build_bt(const int64_t* __restrict__ rp, const uint64_t* __res
     }
 }
 
+
+// ---------------------------------------------------------------- narrow walk index (wix.cuh)
+// Every row total T = cps[row end - 1] must be < 2^32 for the u32 index.
+__global__ void k_wix_check(const int64_t* __restrict__ rp, const uint64_t* __restrict__ cps, int64_t V,
+                            unsigned int* __restrict__ wide) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = rp[v + 1];
+        if (b > rp[v] && cps[b - 1] >> 32) atomicOr(wide, 1u);
+    }
+}
+
+template <int FL>
+struct WixSize {
+    const int64_t* rp;
+    __device__ __forceinline__ uint64_t operator()(uint64_t v) const {
+        return WixShape<FL>::index_size(static_cast<uint32_t>(rp[v + 1] - rp[v]));
+    }
+};
+
+// Warp per row: padded leaf copies, the record, then the internal levels bottom-up
+// (level k reads k-1).
+template <int FL>
+__global__ void k_wix_build(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                            const uint64_t* __restrict__ cps, const uint64_t* __restrict__ woff, int64_t V,
+                            uint4* __restrict__ rec, uint32_t* __restrict__ c32p, uint32_t* __restrict__ colp,
+                            uint32_t* __restrict__ inn) {
+    using W = WixShape<FL>;
+    const int lane = lane_id();
+    for (uint64_t v = global_warp_id(); v < static_cast<uint64_t>(V); v += total_warps()) {
+        const int64_t rb = rp[v];
+        const uint32_t d = static_cast<uint32_t>(rp[v + 1] - rb);
+        const uint64_t p = W::leaf_pos(static_cast<uint64_t>(rb), v);
+        const uint64_t io = woff[v];
+        if (lane == 0)   // T = S_d (the caller checked T < 2^32, p < 2^32, io < 2^32)
+            rec[v] = make_uint4(static_cast<uint32_t>(p), d, static_cast<uint32_t>(io),
+                                d ? static_cast<uint32_t>(cps[rb + d - 1]) : 0u);
+        for (uint32_t i = lane; i < d; i += 32) {
+            c32p[p + i] = static_cast<uint32_t>(cps[rb + i]);
+            colp[p + i] = col[rb + i];
+        }
+        __syncwarp();
+        const int K = W::levels(d);
+        uint64_t offk[8];
+        uint64_t acc = 0;
+        for (int k = K; k >= 1; --k) { offk[k] = acc; acc += W::round4(W::count(d, k)); }
+        for (int k = 1; k <= K; ++k) {
+            const uint32_t nk = W::count(d, k);
+            const uint32_t nchild = k == 1 ? d : W::count(d, k - 1);
+            const uint32_t span = k == 1 ? FL : WIX_NODE;
+            for (uint32_t j = lane; j < nk; j += 32) {
+                const uint32_t last = min((j + 1) * span, nchild) - 1;
+                inn[io + offk[k] + j] = k == 1 ? c32p[p + last] : inn[io + offk[k - 1] + last];
+            }
+            __syncwarp();
+        }
+    }
+}
+
+template <int FL>
+static csaw_status build_wix_t(csaw_graph* g, int blocks) {
+    using W = WixShape<FL>;
+    const int64_t V = g->V, E = g->E;
+    uint64_t* woff = nullptr;
+    uint64_t* part = nullptr;
+    CSAW_CUDA(cudaMalloc(&woff, sizeof(uint64_t) * (V + 1)));
+    CSAW_CUDA(cudaMalloc(&part, sizeof(uint64_t) * (SCAN_MAX_GRID + 8)));
+    csaw_status s = device_scan(WixSize<FL>{g->row_ptr}, static_cast<uint64_t>(V), ScanToArray{woff}, part, nullptr);
+    uint64_t total = 0;
+    if (s == CSAW_OK && cudaMemcpy(&total, woff + V, sizeof(uint64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+        s = fail(CSAW_ERR_CUDA, "walk index size");
+    cudaFree(part);
+    const uint64_t nl = W::leaf_total(static_cast<uint64_t>(E), static_cast<uint64_t>(V));
+    // u32 record fields: else keep the u64 index
+    if (s == CSAW_OK && total + 16 < (uint64_t(1) << 32) && nl < (uint64_t(1) << 32)) {
+        if (cudaMalloc(&g->c32, sizeof(uint32_t) * nl) != cudaSuccess ||
+            cudaMalloc(&g->wcol, sizeof(uint32_t) * nl) != cudaSuccess ||
+            cudaMalloc(&g->wrec, sizeof(uint4) * std::max<int64_t>(V, 1)) != cudaSuccess ||
+            cudaMalloc(&g->winn, sizeof(uint32_t) * (total + 16)) != cudaSuccess) {
+            cudaGetLastError();
+            s = fail(CSAW_ERR_NO_MEMORY, "cudaMalloc(walk index)");
+        } else {
+            cudaMemset(g->c32, 0, sizeof(uint32_t) * nl);   // padding entries (read, then masked)
+            cudaMemset(g->wcol, 0, sizeof(uint32_t) * nl);
+            cudaMemset(g->winn, 0, sizeof(uint32_t) * (total + 16));
+            k_wix_build<FL><<<blocks, 256>>>(g->row_ptr, g->col, g->cps, woff, V, g->wrec, g->c32, g->wcol, g->winn);
+            g->winn_entries = total + 16;
+            g->wleaf_entries = nl;
+        }
+    }
+    cudaFree(woff);
+    return s;
+}
+
+// Builds the index unless disabled or some row total is >= 2^32 (then walks keep the u64
+// CpsTree path).  Leaf fanout: CSAW_WIX_LEAF = 32 | 64 | 128 (0 = not built, A/B).
+static csaw_status build_wix(csaw_graph* g, int blocks) {
+    const char* env = std::getenv("CSAW_WIX_LEAF");
+    int leaf = env ? std::atoi(env) : 64;
+    if (env && leaf == 0) return CSAW_OK;   // A/B: u64 index only
+    if (leaf != 32 && leaf != 64 && leaf != 128) leaf = 64;
+    unsigned int* wide = nullptr;
+    CSAW_CUDA(cudaMalloc(&wide, sizeof(unsigned int)));
+    CSAW_CUDA(cudaMemset(wide, 0, sizeof(unsigned int)));
+    if (g->V > 0) k_wix_check<<<blocks, 256>>>(g->row_ptr, g->cps, g->V, wide);
+    unsigned int hw = 0;
+    CSAW_CUDA(cudaMemcpy(&hw, wide, sizeof(hw), cudaMemcpyDeviceToHost));
+    cudaFree(wide);
+    if (hw || g->E <= 0) return CSAW_OK;
+    csaw_status s = leaf == 32 ? build_wix_t<32>(g, blocks) : leaf == 64 ? build_wix_t<64>(g, blocks)
+                                                               : build_wix_t<128>(g, blocks);
+    if (s == CSAW_OK && g->c32) {
+        g->wix_leaf = leaf;
+        // lanes per walker: 32 (one warp per walker, default) | 16 | 8 (A/B: the sub-warp
+        // kernels are slower at cfg2, 3.7 / 4.4 ms vs 2.8 ms: a warp's walkers then wait for
+        // the slowest of their dependent-load chains every step)
+        const char* ge = std::getenv("CSAW_WIX_GROUP");
+        const int grp = ge ? std::atoi(ge) : 32;
+        g->wix_group = (grp == 16 && leaf >= 64) ? 16 : grp == 8 ? 8 : 32;
+    }
+    return s;
+}
 }  // namespace csaw
 
 using namespace csaw;
@@ -417,6 +539,10 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
             CREATE_CUDA(cudaMalloc(&g->nmp, sizeof(uint64_t) * E), "cudaMalloc(nmp)");
             k_build_nmp<<<blocks, 256>>>(g->row_ptr, g->col, E, g->nmp);
         }
+        if (!(o.flags & CSAW_GRAPH_NO_WALK_INDEX)) {
+            const csaw_status ws = build_wix(g, blocks);
+            if (ws != CSAW_OK) return cleanup(ws);
+        }
         cudaEventRecord(c1);
         CREATE_CUDA(cudaEventSynchronize(c1), "build cps");
         float ms = 0.f;
@@ -445,6 +571,10 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->bt) cudaFree(g->bt);
     if (g->bt_off) cudaFree(g->bt_off);
     if (g->nmp) cudaFree(g->nmp);
+    if (g->c32) cudaFree(g->c32);
+    if (g->wcol) cudaFree(g->wcol);
+    if (g->winn) cudaFree(g->winn);
+    if (g->wrec) cudaFree(g->wrec);
     auto& st = g->oomst;
     if (st.h_col) cudaFreeHost(st.h_col);
     if (st.h_row) cudaFreeHost(st.h_row);
@@ -469,8 +599,11 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
     out->device_bytes = sizeof(int64_t) * (g->V + 1) + sizeof(uint32_t) * g->V +
                         (g->col ? sizeof(uint32_t) * g->E : 0) + static_cast<int64_t>(g->scratch.bytes_held()) +
                         (g->oom ? static_cast<int64_t>(g->oomst.R) * g->oomst.slot_edges * 4 : 0) +
-                        (g->cps ? static_cast<int64_t>(sizeof(uint64_t) * g->E + sizeof(uint32_t) * g->V) : 0);
+                        (g->cps ? static_cast<int64_t>(sizeof(uint64_t) * g->E + sizeof(uint32_t) * g->V) : 0) +
+                        (g->wix_leaf ? static_cast<int64_t>(sizeof(uint32_t) * (2 * g->wleaf_entries + g->winn_entries) + sizeof(uint4) * g->V) : 0);
     out->ctps_cache = g->cps ? 1 : 0;
+    out->walk_index_leaf = g->wix_leaf;
+    out->walk_index_group = g->wix_leaf ? g->wix_group : 0;
     out->reserved = 0;
     out->cache_build_ms = g->cache_build_ms;
     return CSAW_OK;
@@ -492,11 +625,12 @@ CSAW_API csaw_status csaw_stats(const csaw_graph* g, csaw_run_stats* out) {
     }
     g->stats.hot_kernel_ms = hot;
     if (g->pending_counters) {
-        unsigned long long c[3] = {0, 0, 0};
+        unsigned long long c[4] = {0, 0, 0, 0};
         CSAW_CUDA(cudaMemcpy(c, g->pending_counters, sizeof(c), cudaMemcpyDeviceToHost));
         g->stats.neighbours_scanned = c[0];
         g->stats.pools = c[1];
         g->stats.cache_probes = c[2];
+        g->stats.index_bytes = c[3];
         g->pending_counters = nullptr;
     }
     *out = g->stats;

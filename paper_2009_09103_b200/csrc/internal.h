@@ -121,6 +121,15 @@ struct csaw_graph {
     uint64_t* bt = nullptr;       // fanout-32 B-tree index levels over cps (rows with d > 32)
     uint64_t* bt_off = nullptr;   // [V] start of a row's index segment in bt (= row_ptr/16 + 8 v)
     uint64_t* nmp = nullptr;      // [E] next-vertex metadata row_ptr[u] << 24 | deg(u) (walks)
+    // narrow walk index (wix.cuh): built with the cache when every row total T < 2^32
+    uint32_t* c32 = nullptr;      // padded leaves: S_{i+1} as u32 (wix.cuh leaf_pos)
+    uint32_t* wcol = nullptr;     // padded leaves: col copy
+    uint4* wrec = nullptr;        // [V] {row start lo, hi, degree, index offset}
+    uint32_t* winn = nullptr;     // internal levels (fanout 128), top level first per row
+    uint64_t winn_entries = 0;    // size of winn
+    uint64_t wleaf_entries = 0;   // size of c32 / wcol
+    int wix_group = 8;            // lanes per walker in k_walk_wixg (32 = k_walk_wix, one warp per walker)
+    int wix_leaf = 0;             // leaf fanout 32 / 64 / 128 (0 = not built)
     double cache_build_ms = 0.0;
     int num_sms = 148;
     bool oom = false;

@@ -15,6 +15,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "select.cuh"
+#include "wix.cuh"
 
 namespace csaw {
 
@@ -97,6 +98,238 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_cached(WalkArgs a, 
     }
     if (lane == 0) {
         if (probes) atomicAdd(a.counters + 2, probes);
+        if (steps) atomicAdd(a.counters + 1, steps);
+    }
+}
+
+// ---------------------------------------------------------------- narrow walk index (wix.cuh)
+// Entries base[q * 32 + lane], q < N, of one node / leaf block; entries past cnt read as
+// 0xFFFFFFFF, which is above every draw (x < T <= 2^32 - 1).
+template <int N>
+__device__ __forceinline__ void wix_load(const uint32_t* __restrict__ p, uint32_t cnt, uint32_t (&v)[N]) {
+    const uint32_t lane = static_cast<uint32_t>(lane_id());
+#pragma unroll
+    for (int q = 0; q < N; ++q) v[q] = q * 32 + lane < cnt ? __ldg(p + q * 32 + lane) : 0xFFFFFFFFu;
+}
+template <int N>
+__device__ __forceinline__ uint32_t wix_pick(const uint32_t (&v)[N], uint32_t q) {
+    uint32_t r = v[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) if (q == static_cast<uint32_t>(i)) r = v[i];
+    return r;
+}
+// entry i of the block (all lanes)
+template <int N>
+__device__ __forceinline__ uint32_t wix_entry(const uint32_t (&v)[N], uint32_t i) {
+    return __shfl_sync(FULL, wix_pick(v, i >> 5), i & 31);
+}
+// number of entries <= x = position of the first entry > x (the block is sorted)
+template <int N>
+__device__ __forceinline__ uint32_t wix_rank(const uint32_t (&v)[N], uint32_t x) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < N; ++q) c += v[q] <= x ? 1u : 0u;
+    return __reduce_add_sync(FULL, c);
+}
+
+// Degree-biased walk over the narrow index, one warp per walker: per step one 16 B
+// vertex record (with T, so the draw x is ready before the first node arrives), K <= 4 internal 512 B nodes (K = 0 for d <= FL, 1 for d <= 128 FL) and
+// one leaf block with its col entries (4 strided u32 loads per lane and node).  The
+// step's Philox draws are computed 32 at a time (lane j: step t0 + j) and broadcast, so
+// the 10-round generator costs 1/32 per step.  Same S, same draws, same region as
+// k_walk<degree> and the oracle (bit-identical).
+template <int FL>
+__global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_wix(WalkArgs a, const uint4* __restrict__ rec,
+                                                               const uint32_t* __restrict__ c32p,
+                                                               const uint32_t* __restrict__ colp,
+                                                               const uint32_t* __restrict__ inn) {
+    using W = WixShape<FL>;
+    constexpr int NL = FL / 32;
+    const int lane = lane_id();
+    unsigned long long bytes = 0, steps = 0;
+    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+        uint32_t cur = a.seeds[w];
+        const uint32_t inst = a.base + static_cast<uint32_t>(w);
+        PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
+        pw.put(0, cur);
+        uint4 r = __ldg(rec + cur);   // {leaf position, degree, index offset, row total T}
+        bytes += 16;
+        uint64_t ubuf = 0;
+        for (int32_t t = 0; t < a.L; ++t) {
+            if ((t & 31) == 0)
+                ubuf = draw_u64(a.key, inst, static_cast<uint32_t>(t + lane), 0u, word3(PURPOSE_EDGE, 0, 0));
+            const uint64_t U = __shfl_sync(FULL, ubuf, t & 31);
+            uint32_t nxt = NONE;
+            const uint32_t d = r.y;
+            if (cur != NONE && d > 0 && r.w > 0) {   // T = 0: no positive-bias neighbour, the walk ends (R20)
+                const uint32_t x = static_cast<uint32_t>(below(U, r.w));
+                const int K = W::levels(d);
+                uint32_t j = 0;
+                uint64_t off = r.z;
+                for (int k = K; k >= 1; --k) {
+                    const uint32_t nk = W::count(d, k);
+                    const uint32_t cnt = min(static_cast<uint32_t>(WIX_NODE), nk - j * WIX_NODE);
+                    uint32_t v[WIX_NODE / 32];
+                    wix_load(inn + off + j * WIX_NODE, cnt, v);
+                    bytes += 4ull * cnt;
+                    j = j * WIX_NODE + wix_rank(v, x);
+                    off += W::round4(nk);
+                }
+                const uint64_t lb = static_cast<uint64_t>(r.x) + static_cast<uint64_t>(j) * FL;
+                const uint32_t cnt = min(static_cast<uint32_t>(FL), d - j * FL);
+                uint32_t v[NL], cv[NL];
+                wix_load(c32p + lb, cnt, v);
+                wix_load(colp + lb, cnt, cv);
+                bytes += 8ull * cnt;
+                nxt = wix_entry(cv, wix_rank(v, x));
+                ++steps;
+            }
+            cur = nxt;
+            pw.put(t + 1, cur);
+            if (cur != NONE) {
+                r = __ldg(rec + cur);
+                bytes += 16;
+            }
+        }
+    }
+    if (lane == 0) {
+        if (bytes) atomicAdd(a.counters + 3, bytes);
+        if (steps) atomicAdd(a.counters + 1, steps);
+    }
+}
+
+// One node / leaf block read by a group of G lanes: lane gl holds entries 4 gl + 4 G i .. +3
+// (i < N), 16 B aligned uint4 loads; entries past cnt read as 0xFFFFFFFF (above every draw).
+template <int G, int N>
+__device__ __forceinline__ void wixg_load(const uint32_t* __restrict__ p, uint32_t cnt, int gl, uint4 (&q)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const uint32_t e0 = 4 * gl + 4 * G * i;
+        q[i] = e0 < cnt ? __ldg(reinterpret_cast<const uint4*>(p + e0)) : make_uint4(~0u, ~0u, ~0u, ~0u);
+        if (e0 + 1 >= cnt) q[i].y = ~0u;
+        if (e0 + 2 >= cnt) q[i].z = ~0u;
+        if (e0 + 3 >= cnt) q[i].w = ~0u;
+    }
+}
+template <int N>
+__device__ __forceinline__ uint32_t wixg_count(const uint4 (&q)[N], uint32_t x) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) c += (q[i].x <= x) + (q[i].y <= x) + (q[i].z <= x) + (q[i].w <= x);
+    return c;
+}
+
+// Sub-warp variant: G lanes per walker, 32/G walkers per warp.  The chain of dependent
+// loads per step is the same (record -> K nodes -> leaf), but one warp instruction now
+// advances 32/G walkers, so the SM issue slots per walker step drop ~32/G-fold (the
+// warp-per-walker kernel was ~50 % issue-bound at cfg2), at the price of lockstep: each
+// step waits for the slowest of the warp's walkers.  Draws: lane gl computes step t0 + gl
+// every G steps.  Bit-identical to k_walk_wix.
+template <int G, int FL>
+__global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_wixg(WalkArgs a, const uint4* __restrict__ rec,
+                                                                const uint32_t* __restrict__ c32p,
+                                                                const uint32_t* __restrict__ colp,
+                                                                const uint32_t* __restrict__ inn) {
+    using W = WixShape<FL>;
+    constexpr int NI = WIX_NODE / (4 * G);   // uint4 chunks per lane: internal node
+    constexpr int NF = FL / (4 * G);         // uint4 chunks per lane: leaf block
+    static_assert(NF >= 1 && NI >= 1, "FL must be a multiple of 4 G");
+    const int lane = lane_id();
+    const int gl = lane % G;
+    const int gb = lane - gl;
+    const uint64_t ngroups = total_warps() * (32 / G);
+    const uint64_t gid0 = global_warp_id() * (32 / G) + static_cast<uint64_t>(lane / G);
+    const uint64_t rounds = (a.n + ngroups - 1) / ngroups;   // warp-uniform trip count (shuffles below)
+    unsigned long long bytes = 0, steps = 0;
+    for (uint64_t rd = 0; rd < rounds; ++rd) {
+        const uint64_t w = gid0 + rd * ngroups;
+        const bool live = w < a.n;
+        uint32_t cur = live ? a.seeds[w] : NONE;
+        const uint32_t inst = a.base + static_cast<uint32_t>(w);
+        uint32_t* prow = a.path + (live ? w : 0) * (static_cast<uint64_t>(a.L) + 1);
+        uint32_t pbuf = cur;                  // path[pi] buffered in lane pi % G
+        uint4 r = make_uint4(0, 0, 0, 0);
+        if (cur != NONE) {
+            r = __ldg(rec + cur);
+            if (gl == 0) bytes += 16;
+        }
+        if (live && a.L == 0 && gl == 0) prow[0] = pbuf;
+        uint64_t ubuf = 0;
+        for (int32_t t = 0; t < a.L; ++t) {
+            if (t % G == 0)
+                ubuf = draw_u64(a.key, inst, static_cast<uint32_t>(t + gl), 0u, word3(PURPOSE_EDGE, 0, 0));
+            const uint64_t U = __shfl_sync(FULL, ubuf, gb + t % G);
+            const uint32_t d = r.y;
+            const bool on = cur != NONE && d > 0 && r.w > 0;   // T = 0: the walk ends (R20)
+            const uint32_t x = static_cast<uint32_t>(below(U, r.w));
+            const int K = on ? W::levels(d) : 0;
+            const int Kmax = static_cast<int>(__reduce_max_sync(FULL, static_cast<uint32_t>(K)));
+            uint32_t j = 0;
+            uint64_t off = r.z;
+            for (int k = Kmax; k >= 1; --k) {
+                const bool act = on && k <= K;
+                uint32_t c = 0;
+                if (act) {
+                    const uint32_t nk = W::count(d, k);
+                    const uint32_t cnt = min(static_cast<uint32_t>(WIX_NODE), nk - j * WIX_NODE);
+                    uint4 q[NI];
+                    wixg_load<G>(inn + off + j * WIX_NODE, cnt, gl, q);
+                    if (gl == 0) bytes += 4ull * cnt;
+                    c = wixg_count(q, x);
+                    off += W::round4(nk);
+                }
+#pragma unroll
+                for (int o = G / 2; o >= 1; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+                if (act) j = j * WIX_NODE + c;
+            }
+            uint32_t c = 0;
+            uint4 cv[NF];
+            if (on) {
+                const uint64_t lb = static_cast<uint64_t>(r.x) + static_cast<uint64_t>(j) * FL;
+                const uint32_t cnt = min(static_cast<uint32_t>(FL), d - j * FL);
+                uint4 q[NF];
+                wixg_load<G>(c32p + lb, cnt, gl, q);
+#pragma unroll
+                for (int i = 0; i < NF; ++i) {
+                    const uint32_t e0 = 4 * gl + 4 * G * i;
+                    cv[i] = e0 < cnt ? __ldg(reinterpret_cast<const uint4*>(colp + lb + e0)) : make_uint4(0, 0, 0, 0);
+                }
+                if (gl == 0) bytes += 8ull * cnt;
+                c = wixg_count(q, x);
+            } else {
+#pragma unroll
+                for (int i = 0; i < NF; ++i) cv[i] = make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int o = G / 2; o >= 1; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+            // entry c of the leaf: chunk c / (4 G), lane (c / 4) % G of the group, component c % 4
+            uint32_t val = 0;
+            const uint32_t ci = c / (4 * G), cc = c & 3;
+#pragma unroll
+            for (int i = 0; i < NF; ++i)
+                if (ci == static_cast<uint32_t>(i)) val = cc == 0 ? cv[i].x : cc == 1 ? cv[i].y : cc == 2 ? cv[i].z : cv[i].w;
+            val = __shfl_sync(FULL, val, gb + static_cast<int>((c >> 2) % G));
+            uint32_t nxt = NONE;
+            if (on) {
+                nxt = val;
+                if (gl == 0) ++steps;
+            }
+            cur = nxt;
+            // path[t + 1]: buffered in lane (t + 1) % G, flushed as one G x 4 B segment
+            const int32_t pi = t + 1;
+            if (pi % G == gl) pbuf = cur;
+            if (live && (pi % G == G - 1 || pi == a.L)) {
+                const int32_t idx = pi - pi % G + gl;
+                if (idx <= pi) prow[idx] = pbuf;
+            }
+            if (cur != NONE) {
+                r = __ldg(rec + cur);
+                if (gl == 0) bytes += 16;
+            }
+        }
+    }
+    if (gl == 0) {
+        if (bytes) atomicAdd(a.counters + 3, bytes);
         if (steps) atomicAdd(a.counters + 1, steps);
     }
 }
@@ -784,7 +1017,28 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
     const uint32_t* colp = g->col ? g->col : g->oomst.h_col;
     WalkArgs a{g->row_ptr, colp, g->deg, d_seeds, static_cast<uint64_t>(n), length,
                static_cast<uint32_t>(base), key, d_path, static_cast<unsigned long long*>(cnt)};
-    if (b.kind == CSAW_BIAS_DEGREE && g->cps) {
+    if (b.kind == CSAW_BIAS_DEGREE && g->wix_leaf) {
+        // group kernels: 2-warp blocks, so few walkers (cfg2: 1,000 warps) still spread over all SMs
+        const int wpb = g->wix_group == 32 ? WALK_WARPS : 2;
+        const int blk = wpb * 32;
+        const int64_t walkers_per_warp = 32 / g->wix_group;
+        const int64_t warps = std::min<int64_t>((n + walkers_per_warp - 1) / walkers_per_warp,
+                                                static_cast<int64_t>(g->num_sms) * 64);
+        const int grid = static_cast<int>(std::max<int64_t>(1, (warps + wpb - 1) / wpb));
+        const uint4* rec = g->wrec;
+        if (g->wix_group == 32) {
+            if (g->wix_leaf == 32) k_walk_wix<32><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);
+            else if (g->wix_leaf == 64) k_walk_wix<64><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);
+            else k_walk_wix<128><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);
+        } else if (g->wix_group == 16) {
+            if (g->wix_leaf == 64) k_walk_wixg<16, 64><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);
+            else k_walk_wixg<16, 128><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);
+        } else {
+            if (g->wix_leaf == 32) k_walk_wixg<8, 32><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);
+            else if (g->wix_leaf == 64) k_walk_wixg<8, 64><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);
+            else k_walk_wixg<8, 128><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);
+        }
+    } else if (b.kind == CSAW_BIAS_DEGREE && g->cps) {
         k_walk_cached<<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a, g->cps, g->bt, g->bt_off, g->nmp);
     } else if (b.kind == CSAW_BIAS_DEGREE) {
         k_walk<false><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a);

@@ -1,0 +1,77 @@
+// wix.cuh — narrow walk index over the static-bias CTPS cache (NEXT-1).
+//
+// A degree-biased walk step is latency-bound: 4,000 walkers each run a serial
+// chain of dependent loads (row -> index levels -> leaf + col -> next row), so
+// the number of round trips per step and the instructions between them set the
+// speed, not bytes.  This index cuts both against the fanout-32 u64 B-tree of
+// select.cuh (CpsTree):
+//   * every row total T < 2^32 (checked at build), so S fits u32: a 128-entry
+//     internal node is one 512 B coalesced read (4 strided u32 loads per lane);
+//   * leaf blocks hold FL = 32 / 64 / 128 entries of S (u32) read together with
+//     the matching col entries, so the pick's vertex arrives with the leaf;
+//   * one 16 B record per vertex {leaf position, degree, index offset, T} is the
+//     only per-vertex lookup (built when all four fit u32);
+//   * leaves (S and a copy of col) are laid out 16 B aligned per row, and every
+//     node starts 16 B aligned, so a group of G lanes can read a node with
+//     uint4 loads: with G = 8 one warp walks 4 walkers at once.
+// The searched values are the same integer prefix S_{i+1} = sum of deg over the
+// first i+1 neighbours, so a pick is the same region s (Eq. 1) as
+// the scan path and the oracle: bit-identical.
+//
+// Layout of row v (d = deg, rb = row start):
+//   leaf     c32p[p + i] = S_{i+1} (u32), colp[p + i] = col[rb + i], i in [0, d),
+//            p = leaf_pos(rb, v)
+//   level k  (k >= 1) n_k = ceil(d / (FL * 128^(k-1))) entries; entry j = last S
+//            of its child block; rows with d <= FL have no internal level.
+//   K        = number of internal levels = first k with n_k <= 128 (top node);
+//            stored top level first (each level padded to 4 entries) at inn[ioff[v] ...],
+//            ioff = exclusive prefix of index_size over the vertices.
+#pragma once
+
+#include <cstdint>
+
+namespace csaw {
+
+constexpr int WIX_NODE = 128;   // internal fanout
+constexpr int WIX_NODE_LOG = 7;
+
+template <int FL>
+struct WixShape {
+    static constexpr int kLeafLog = FL == 32 ? 5 : FL == 64 ? 6 : 7;
+    // internal levels of a row of degree d
+    __host__ __device__ __forceinline__ static int levels(uint32_t d) {
+        if (d <= static_cast<uint32_t>(FL)) return 0;
+        const int bits = 32 - clz32(d - 1);
+        return (bits - kLeafLog + WIX_NODE_LOG - 1) / WIX_NODE_LOG;
+    }
+    // entries at level k >= 1
+    __host__ __device__ __forceinline__ static uint32_t count(uint32_t d, int k) {
+        return ((d - 1) >> (kLeafLog + WIX_NODE_LOG * (k - 1))) + 1;
+    }
+    __host__ __device__ __forceinline__ static uint32_t round4(uint32_t n) { return (n + 3) & ~3u; }
+    // a row's index segment: its levels top first, each padded to a multiple of 4 entries
+    // so every node starts 16 B aligned
+    __host__ __device__ __forceinline__ static uint64_t index_size(uint32_t d) {
+        uint64_t s = 0;
+        const int K = levels(d);
+        for (int k = 1; k <= K; ++k) s += round4(count(d, k));
+        return s;
+    }
+    // start of row v's leaf entries in the padded leaf arrays (16 B aligned):
+    // 4 ceil((rb + 3v) / 4); the gap to row v+1 is >= d.
+    __host__ __device__ __forceinline__ static uint64_t leaf_pos(uint64_t rb, uint64_t v) {
+        return (rb + 3 * v + 3) & ~uint64_t(3);
+    }
+    __host__ __device__ __forceinline__ static uint64_t leaf_total(uint64_t E, uint64_t V) {
+        return E + 3 * V + 16;
+    }
+    __host__ __device__ __forceinline__ static int clz32(uint32_t x) {
+#ifdef __CUDA_ARCH__
+        return __clz(x);
+#else
+        return x ? __builtin_clz(x) : 32;
+#endif
+    }
+};
+
+}  // namespace csaw
