@@ -998,6 +998,92 @@ __global__ void k_mdrw(MdrwArgs a) {
     }
 }
 
+// MDRW, pools of m <= 2048 slots (nblk <= 64 blocks of 32): the instruction diet of
+// k_mdrw.  Block totals live in registers (lane l: blocks 2l, 2l+1) so the block search
+// is one u64 warp scan; a slot's state is one 16 B record {v, bias, row start lo, hi}
+// (one load per lane per step); the step's two draws come from a per-lane buffer
+// refilled every 32 steps; the neighbour and its row are loaded by every lane (broadcast
+// loads) so no lane-0 section and no result shuffles remain.  Same x, same slot, same
+// neighbour as k_mdrw and the oracle (bit-identical).
+constexpr int MDRW_WARPS = 4;
+__global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, uint4* __restrict__ pool) {
+    const int lane = lane_id();
+    const uint32_t m = static_cast<uint32_t>(a.m);
+    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+        const uint32_t inst = a.base + static_cast<uint32_t>(w);
+        uint4* ps = pool + w * m;
+        // init pool (slot order = seeds order) and the two block totals of this lane
+        uint64_t bA = 0, bB = 0;
+        for (uint32_t b = 0; b * 32 < m; ++b) {   // block b is held by lane b >> 1
+            const uint32_t s = b * 32 + lane;
+            uint32_t dv = 0;
+            if (s < m) {
+                const uint32_t v = a.seeds[w * m + s];
+                const int64_t r0 = __ldg(a.rp + v);
+                dv = static_cast<uint32_t>(__ldg(a.rp + v + 1) - r0);
+                ps[s] = make_uint4(v, dv, static_cast<uint32_t>(r0), static_cast<uint32_t>(static_cast<uint64_t>(r0) >> 32));
+            }
+            const uint64_t tot = warp_sum(static_cast<uint64_t>(dv));
+            if (lane == static_cast<int>(b >> 1)) { if (b & 1) bB = tot; else bA = tot; }
+        }
+        uint64_t T = warp_sum(bA + bB);
+        __syncwarp();
+        uint32_t* orow = a.out + w * static_cast<uint64_t>(a.L) * 2;
+        uint32_t ebuf = NONE;
+        uint64_t uxb = 0, ueb = 0;
+        for (int32_t t = 0; t < a.L; ++t) {
+            if ((t & 31) == 0) {
+                uxb = draw_u64(a.key, inst, static_cast<uint32_t>(t + lane), 0u, word3(PURPOSE_VERTEX, 0, 0));
+                ueb = draw_u64(a.key, inst, static_cast<uint32_t>(t + lane), 0u, word3(PURPOSE_EDGE, 0, 0));
+            }
+            const uint64_t Ux = __shfl_sync(FULL, uxb, t & 31);
+            const uint64_t Ue = __shfl_sync(FULL, ueb, t & 31);
+            uint32_t v = NONE, u = NONE;
+            if (T > 0) {
+                const uint64_t x = below(Ux, T);
+                // block containing x: scan of the lanes' block pairs
+                const uint64_t pair = bA + bB;
+                const uint64_t incl = warp_incl_scan(pair);
+                const int f = __ffs(__ballot_sync(FULL, incl > x)) - 1;   // exists: x < T
+                const uint64_t ex = __shfl_sync(FULL, incl - pair, f);
+                const uint64_t fa = __shfl_sync(FULL, bA, f);
+                const bool second = x >= ex + fa;
+                const uint32_t bsel = 2 * f + (second ? 1 : 0);
+                const uint64_t blo = second ? ex + fa : ex;
+                // the block's slots: one 16 B record per lane
+                const uint32_t s0 = bsel * 32 + lane;
+                const uint4 e = s0 < m ? ps[s0] : make_uint4(NONE, 0, 0, 0);
+                const uint64_t incl2 = warp_incl_scan(static_cast<uint64_t>(e.y)) + blo;
+                const int fl = __ffs(__ballot_sync(FULL, incl2 > x)) - 1;
+                const uint32_t d = __shfl_sync(FULL, e.y, fl);
+                v = __shfl_sync(FULL, e.x, fl);
+                const uint64_t rb = static_cast<uint64_t>(__shfl_sync(FULL, e.w, fl)) << 32 | __shfl_sync(FULL, e.z, fl);
+                u = __ldg(a.col + rb + below(Ue, d));
+                const int64_t ru = __ldg(a.rp + u);
+                const uint32_t du = static_cast<uint32_t>(__ldg(a.rp + u + 1) - ru);
+                if (lane == fl)
+                    ps[s0] = make_uint4(u, du, static_cast<uint32_t>(ru), static_cast<uint32_t>(static_cast<uint64_t>(ru) >> 32));
+                if (lane == static_cast<int>(bsel >> 1)) {
+                    if (bsel & 1) bB = bB + du - d;
+                    else bA = bA + du - d;
+                }
+                T = T + du - d;
+                __syncwarp();
+            }
+            // buffer 16 steps (2 words each) per 32 lanes, flush coalesced
+            const int k = t & 15;
+            if (lane == 2 * k) ebuf = v;
+            if (lane == 2 * k + 1) ebuf = u;
+            if (k == 15 || t == a.L - 1) {
+                const int32_t t0 = t & ~15;
+                const int32_t idx = t0 * 2 + lane;
+                if (idx < (t + 1) * 2) orow[idx] = ebuf;
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // ---------------------------------------------------------------- host launchers
 static int walk_grid(const csaw_graph* g, int64_t n) {
     const int64_t warps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 64);
@@ -1066,6 +1152,21 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
     } else if (b.kind == CSAW_BIAS_MDRW) {
         const uint32_t m = static_cast<uint32_t>(b.pool_size);
         const uint32_t nblk = (m + 31) / 32;
+        if (nblk <= 64 && !std::getenv("CSAW_MDRW_SLOW")) {   // pools up to 2,048 slots (cfg5: 2,000)
+            void* pool;
+            CSAW_TRY(g->scratch.get(SL_TMP0, sizeof(uint4) * n * m, &pool));
+            MdrwArgs ma{g->row_ptr, colp, d_seeds, static_cast<uint64_t>(n), b.pool_size, length,
+                        static_cast<uint32_t>(base), key, d_path, nullptr, nullptr, nullptr, nullptr, 0, WALK_WARPS};
+            const int64_t warps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 7 * MDRW_WARPS);
+            k_mdrw_fast<<<static_cast<int>((warps + MDRW_WARPS - 1) / MDRW_WARPS), MDRW_WARPS * 32, 0, st>>>(
+                ma, static_cast<uint4*>(pool));
+            CSAW_CUDA(cudaGetLastError());
+            CSAW_TRY(hot_end(g, st));
+            CSAW_TRY(stats_end(g, st));
+            g->stats.sampled_edges = static_cast<uint64_t>(n) * length;
+            g->pending_counters = static_cast<const unsigned long long*>(cnt);
+            return CSAW_OK;
+        }
         const size_t per = static_cast<size_t>(nblk) * 8;
         int wpb = static_cast<int>(std::min<size_t>(8, (200 * 1024) / std::max<size_t>(per, 1)));
         const bool smem_ok = wpb >= 1;

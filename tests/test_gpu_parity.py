@@ -272,3 +272,21 @@ def test_repeatable(cfg1):
     b = cs.csaw_walk(G, "degree", seeds, 300, rng_seed=1)
     c = cs.csaw_walk(G, "degree", seeds, 300, rng_seed=2)
     assert torch.equal(a, b) and not torch.equal(a, c)
+
+
+@pytest.mark.parametrize("m,n,L", [(2048, 5, 200), (2049, 4, 150), (33, 40, 300), (64, 7, 100), (1, 5000, 37)])
+def test_mdrw_pool_sizes(medium, m, n, L):
+    """k_mdrw_fast (pools <= 2,048 slots: register block totals, 16 B slot records) and
+    k_mdrw (larger pools, or CSAW_MDRW_SLOW=1) against the oracle, incl. ragged last
+    blocks and more instances than resident warps."""
+    import os
+    G2, og2, g2 = medium
+    s = mdrw_seeds(g2, n, m).numpy()
+    e = check_mdrw(G2, og2, s, L, rng_seed=7, instances=range(0, n, max(1, n // 40)))
+    os.environ["CSAW_MDRW_SLOW"] = "1"
+    try:
+        e2 = u32(cs.csaw_walk(G2, cs.make_bias("mdrw", pool_size=m), torch.as_tensor(s.view(np.int32)).to(DEV), L,
+                              rng_seed=7))
+    finally:
+        del os.environ["CSAW_MDRW_SLOW"]
+    assert np.array_equal(e, e2)
