@@ -98,8 +98,9 @@ def algorithmic_bytes(cfg, st, n, edges):
     sampling select kernel: 16 per pool + 8 per scanned candidate + 12 per staged edge."""
     scanned, pools = st["neighbours_scanned"], st["pools"]
     probes = st.get("cache_probes", 0)
-    if st.get("index_bytes") and cfg.workload == "walk":
-        # narrow walk index: record 16 + node / leaf (+ col) entries read, counted in the kernel, + path
+    if st.get("index_bytes") and cfg.workload in ("walk", "node2vec"):
+        # bytes the kernel read, counted in the kernel (narrow walk index: record + nodes + leaf
+        # and col entries; node2vec with triangle counts: row_ptr pairs, tri, list entries), + path
         return st["index_bytes"] + 4 * n * (cfg.length + 1) + 4 * n
     if probes and cfg.workload == "walk":
         # cached CTPS: row_ptr pair 16 + T 8 + col 4 per step, 8 per cache probe, + path
@@ -332,7 +333,7 @@ def main():
                                  num_streams=cfg.oom_resident)
     else:
         # static-bias CTPS cache (§8(f) NEXT-1, bit-identical) for degree-biased selections
-        use_cache = (not args.no_cache) and cfg.bias in ("degree", "layer")
+        use_cache = (not args.no_cache) and (cfg.bias in ("degree", "layer") or cfg.workload == "node2vec")
         G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache)
     ginfo = G.info()
     bias = bias_of(cs, cfg)
@@ -492,7 +493,8 @@ def main():
         variant += "_inmem"
     elif not ginfo.get("ctps_cache") and cfg.bias in ("degree", "layer") and not ginfo.get("oom_mode"):
         variant += "_scan"
-    kname = hot_kernel_name(cfg, bool(ginfo.get("ctps_cache")), bool(ginfo.get("oom_mode")),
+    kname = hot_kernel_name(cfg, bool(ginfo.get("node2vec_tri") if cfg.workload == "node2vec" else ginfo.get("ctps_cache")),
+                            bool(ginfo.get("oom_mode")),
                             int(ginfo.get("walk_index_leaf") or 0), int(ginfo.get("walk_index_group") or 0))
     traffic = load_traffic(variant, kname)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -604,7 +606,7 @@ def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0):
     if cfg.workload == "mdrw":
         return "k_mdrw_oom_part" if oom else "k_mdrw"
     if cfg.workload == "node2vec":
-        return "k_node2vec<int>"
+        return "k_node2vec_tri" if cached else "k_node2vec<int>"
     if oom:
         # OOM traversal sampling runs the batched level driver, one select launch per resident partition
         return "k_ns_select<1>" if cfg.bias == "degree" else "k_ns_select<0>"

@@ -153,7 +153,7 @@ typedef struct {
     int32_t walk_index_leaf;        /* narrow walk index leaf fanout (32/64/128; 129 = col read after the leaf), 0 = not built */
     double cache_build_ms;          /* device time of the cache build */
     int32_t walk_index_group;       /* lanes per walker of the degree-walk kernel (8 / 16; 32 = one warp per walker) */
-    int32_t reserved;
+    int32_t node2vec_tri;           /* 1 if per-edge triangle counts were built (node2vec partial scans) */
 } csaw_graph_info_t;
 
 typedef struct csaw_graph csaw_graph;  /* opaque */

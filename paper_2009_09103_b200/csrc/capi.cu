@@ -375,6 +375,96 @@ static csaw_status build_wix(csaw_graph* g, int blocks) {
     }
     return s;
 }
+
+// ---------------------------------------------------------------- node2vec edge triangle counts
+// tri[e] = |N(v) ∩ N(u)| for the CSR entry e = (v -> u): the number of "common
+// neighbour" specials of a node2vec step that arrived at v from u (or at u from v), so
+// the row total T of the step's CTPS is closed-form (walk.cu k_node2vec_tri).  Built
+// once per undirected edge (u > v), written to both entries; any entry without its
+// reverse (or a self-loop) marks the graph asymmetric and the cache is not used.
+__global__ void k_src_of(const int64_t* __restrict__ rp, int64_t V, uint32_t* __restrict__ src) {
+    const int lane = lane_id();
+    for (uint64_t v = global_warp_id(); v < static_cast<uint64_t>(V); v += total_warps())
+        for (int64_t e = rp[v] + lane; e < rp[v + 1]; e += 32) src[e] = static_cast<uint32_t>(v);
+}
+
+// Count of the sorted list small[0, ns) in the sorted list big[0, nb) (warp-collective):
+// rows of 32 small entries, the big range of each row narrowed by two 32-ary searches,
+// then a per-lane binary search.
+__device__ uint32_t warp_intersect_count(const uint32_t* __restrict__ small, uint64_t ns,
+                                         const uint32_t* __restrict__ big, uint64_t nb) {
+    const int lane = lane_id();
+    uint32_t cnt = 0;
+    uint64_t lo0 = 0;
+    for (uint64_t r0 = 0; r0 < ns && lo0 < nb; r0 += 32) {
+        const uint64_t i = r0 + lane;
+        const bool valid = i < ns;
+        const uint32_t x = valid ? __ldg(small + i) : NONE;
+        const uint32_t xmin = __shfl_sync(FULL, x, 0);
+        const int last = static_cast<int>(ns - 1 - r0 < 31 ? ns - 1 - r0 : 31);
+        const uint32_t xmax = __shfl_sync(FULL, x, last);
+        const uint64_t lo = warp_lower_bound(big, lo0, nb, xmin);
+        const uint64_t hi = xmax == NONE ? nb : warp_lower_bound(big, lo, nb, xmax + 1u);
+        uint64_t l = lo, h = hi;
+        while (l < h) {   // same trip count on every lane
+            const uint64_t mid = (l + h) >> 1;
+            if (__ldg(big + mid) < x) l = mid + 1; else h = mid;
+        }
+        const bool f = valid && l < hi && __ldg(big + l) == x;
+        cnt += __popc(__ballot_sync(FULL, f));
+        lo0 = hi;
+    }
+    return cnt;
+}
+
+__global__ void k_tri(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                      const uint32_t* __restrict__ src, int64_t E, uint32_t* __restrict__ tri,
+                      unsigned int* __restrict__ asym) {
+    for (uint64_t e = global_warp_id(); e < static_cast<uint64_t>(E); e += total_warps()) {
+        const uint32_t v = src[e], u = col[e];
+        if (u == v) { if (lane_id() == 0) atomicOr(asym, 1u); continue; }
+        if (u < v) continue;
+        const int64_t bv = rp[v], bu = rp[u];
+        const uint64_t dv = static_cast<uint64_t>(rp[v + 1] - bv), du = static_cast<uint64_t>(rp[u + 1] - bu);
+        // reverse entry: v in N(u)
+        const uint64_t j = warp_lower_bound(col + bu, 0, du, v);
+        const bool has_rev = j < du && __ldg(col + bu + j) == v;
+        const uint32_t c = dv <= du ? warp_intersect_count(col + bv, dv, col + bu, du)
+                                    : warp_intersect_count(col + bu, du, col + bv, dv);
+        if (lane_id() == 0) {
+            tri[e] = c;
+            if (has_rev) tri[bu + j] = c;
+            else atomicOr(asym, 1u);
+        }
+    }
+}
+
+// Builds tri (CTPS-cache graphs with sorted rows); leaves g->tri null if the graph is not
+// symmetric.  CSAW_N2V_TRI=0 skips it (A/B).
+static csaw_status build_tri(csaw_graph* g, int blocks) {
+    const char* env = std::getenv("CSAW_N2V_TRI");
+    if ((env && env[0] == '0') || !g->rows_sorted || g->E <= 0) return CSAW_OK;
+    uint32_t* src = nullptr;
+    unsigned int* asym = nullptr;
+    if (cudaMalloc(&src, sizeof(uint32_t) * g->E) != cudaSuccess || cudaMalloc(&asym, sizeof(unsigned int)) != cudaSuccess ||
+        cudaMalloc(&g->tri, sizeof(uint32_t) * g->E) != cudaSuccess) {
+        cudaGetLastError();
+        if (src) cudaFree(src);
+        if (asym) cudaFree(asym);
+        if (g->tri) { cudaFree(g->tri); g->tri = nullptr; }
+        return fail(CSAW_ERR_NO_MEMORY, "cudaMalloc(node2vec triangle counts)");
+    }
+    cudaMemset(asym, 0, sizeof(unsigned int));
+    k_src_of<<<blocks, 256>>>(g->row_ptr, g->V, src);
+    k_tri<<<blocks * 4, 256>>>(g->row_ptr, g->col, src, g->E, g->tri, asym);
+    unsigned int h = 0;
+    const cudaError_t err = cudaMemcpy(&h, asym, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(src);
+    cudaFree(asym);
+    if (err != cudaSuccess) return fail(CSAW_ERR_CUDA, cudaGetErrorString(err));
+    if (h) { cudaFree(g->tri); g->tri = nullptr; }
+    return CSAW_OK;
+}
 }  // namespace csaw
 
 using namespace csaw;
@@ -543,6 +633,10 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
             const csaw_status ws = build_wix(g, blocks);
             if (ws != CSAW_OK) return cleanup(ws);
         }
+        {
+            const csaw_status ts = build_tri(g, blocks);
+            if (ts != CSAW_OK) return cleanup(ts);
+        }
         cudaEventRecord(c1);
         CREATE_CUDA(cudaEventSynchronize(c1), "build cps");
         float ms = 0.f;
@@ -572,6 +666,7 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->bt_off) cudaFree(g->bt_off);
     if (g->nmp) cudaFree(g->nmp);
     if (g->c32) cudaFree(g->c32);
+    if (g->tri) cudaFree(g->tri);
     if (g->wcol) cudaFree(g->wcol);
     if (g->winn) cudaFree(g->winn);
     if (g->wrec) cudaFree(g->wrec);
@@ -600,11 +695,12 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
                         (g->col ? sizeof(uint32_t) * g->E : 0) + static_cast<int64_t>(g->scratch.bytes_held()) +
                         (g->oom ? static_cast<int64_t>(g->oomst.R) * g->oomst.slot_edges * 4 : 0) +
                         (g->cps ? static_cast<int64_t>(sizeof(uint64_t) * g->E + sizeof(uint32_t) * g->V) : 0) +
-                        (g->wix_leaf ? static_cast<int64_t>(sizeof(uint32_t) * (2 * g->wleaf_entries + g->winn_entries) + sizeof(uint4) * g->V) : 0);
+                        (g->wix_leaf ? static_cast<int64_t>(sizeof(uint32_t) * (2 * g->wleaf_entries + g->winn_entries) + sizeof(uint4) * g->V) : 0) +
+                        (g->tri ? static_cast<int64_t>(sizeof(uint32_t) * g->E) : 0);
     out->ctps_cache = g->cps ? 1 : 0;
     out->walk_index_leaf = g->wix_leaf;
     out->walk_index_group = g->wix_leaf ? g->wix_group : 0;
-    out->reserved = 0;
+    out->node2vec_tri = g->tri ? 1 : 0;
     out->cache_build_ms = g->cache_build_ms;
     return CSAW_OK;
 }

@@ -128,6 +128,7 @@ struct csaw_graph {
     uint32_t* winn = nullptr;     // internal levels (fanout 128), top level first per row
     uint64_t winn_entries = 0;    // size of winn
     uint64_t wleaf_entries = 0;   // size of c32 / wcol
+    uint32_t* tri = nullptr;      // [E] node2vec: |N(v) ∩ N(u)| per entry (symmetric sorted graphs, cache builds)
     int wix_group = 8;            // lanes per walker in k_walk_wixg (32 = k_walk_wix, one warp per walker)
     int wix_leaf = 0;             // leaf fanout 32 / 64 / 128 (0 = not built)
     double cache_build_ms = 0.0;

@@ -809,6 +809,254 @@ __device__ void n2v_implicit_step(Node2vecPool& P, uint32_t* spec, uint32_t* til
     out = __ldg(P.col + P.beg + i);
 }
 
+// ---------------------------------------------------------------- node2vec with edge triangle counts
+// With tri[e] = |N(v) ∩ N(prev)| (capi.cu build_tri; symmetric graphs) the step's row total
+// is closed-form: T = wq (d - C - 1) + w1 C + wp (prev is in N(v), C common neighbours).
+// The draw x then fixes the region without a full merge: N(v) is scanned from the end
+// nearer to x (x < T/2: forward; else backward, as a forward scan of the mirrored lists
+// with x' = T - 1 - x -- bitwise NOT reverses u32 order, so both directions share one
+// code path) only until the running S passes x.  Expected scan length: a quarter of
+// N(v) instead of all of it plus all of N(prev).  Same S, same x, same region as the
+// scanned CTPS and the oracle (bit-identical).
+constexpr uint32_t N2T_TILE = 1024;   // N(prev) window in shared memory (u32), per warp
+constexpr int N2T_K = 8;              // keys per lane per chunk (contiguous positions)
+constexpr int N2T_WARPS = 8;
+#ifndef N2T_MINB
+#define N2T_MINB 3
+#endif
+
+template <bool kRev>
+struct MirList {
+    const uint32_t* __restrict__ p;
+    uint32_t n;
+    __device__ __forceinline__ uint32_t at(uint32_t i) const { return kRev ? ~__ldg(p + (n - 1 - i)) : __ldg(p + i); }
+};
+
+// First idx in [lo, hi) with L.at(idx) >= key (hi if none); 32-ary warp search.
+template <bool kRev>
+__device__ __forceinline__ uint32_t mir_lower_bound(const MirList<kRev>& L, uint32_t lo, uint32_t hi, uint32_t key) {
+    const uint32_t lane = static_cast<uint32_t>(lane_id());
+    while (hi - lo > 32) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t p = lo + lane * step;
+        const bool inr = p < hi;
+        const unsigned b = __ballot_sync(FULL, inr && L.at(p) >= key);
+        const unsigned inb = __ballot_sync(FULL, inr);
+        if (b == 0) {
+            lo = lo + static_cast<uint32_t>(31 - __clz(inb)) * step + 1;
+        } else {
+            const uint32_t f = static_cast<uint32_t>(__ffs(b) - 1);
+            if (f == 0) return lo;
+            const uint32_t nlo = lo + (f - 1) * step + 1;
+            hi = lo + f * step;
+            lo = nlo;
+        }
+    }
+    const uint32_t p = lo + lane;
+    const unsigned b = __ballot_sync(FULL, p < hi && L.at(p) >= key);
+    return b ? lo + static_cast<uint32_t>(__ffs(b) - 1) : hi;
+}
+
+struct N2tStats {
+    unsigned long long keys = 0;    // N(v) entries scanned
+    unsigned long long bkeys = 0;   // N(prev) entries read (tiles / searches)
+};
+
+// Position (in A's order) of the region containing xs: first i with S_{i+1} > xs, where
+// S sums w(A[j]) = wp (A[j] == pvk), w1 (A[j] in B), wq (otherwise).  Chunks of 256 keys,
+// lane l holding the 8 consecutive positions 8 l .. 8 l + 7; membership against a
+// shared-memory tile of B: per lane one binary search for its first key, then a linear
+// merge (B about as dense as A) or galloping searches (B denser); B much longer than A:
+// per-key binary searches of B in global memory.
+template <bool kRev>
+__device__ uint32_t n2t_scan(const MirList<kRev>& A, const MirList<kRev>& B, uint32_t pvk, uint64_t xs, uint32_t wp,
+                             uint32_t w1, uint32_t wq, uint32_t* tile, N2tStats& st) {
+    const uint32_t lane = static_cast<uint32_t>(lane_id());
+    const bool bsearch = B.n > 16u * A.n;
+    const bool linear = B.n <= 3u * A.n;
+    uint64_t acc = 0;
+    uint32_t bnext = 0;                     // B entries before bnext are below every key still to come
+    uint32_t tlo = 0, tn = 0, tmax = 0;     // tile = B[tlo, tlo + tn)
+    bool tile_ok = false;
+    for (uint32_t c0 = 0; c0 < A.n; c0 += 32 * N2T_K) {
+        const uint32_t base = c0 + N2T_K * lane;
+        const uint32_t nv = base < A.n ? min(static_cast<uint32_t>(N2T_K), A.n - base) : 0u;   // valid keys of the lane
+        uint32_t k[N2T_K];
+#pragma unroll
+        for (int u = 0; u < N2T_K; ++u) k[u] = static_cast<uint32_t>(u) < nv ? A.at(base + u) : 0u;
+        const uint32_t cn = min(static_cast<uint32_t>(32 * N2T_K), A.n - c0);
+        st.keys += cn;
+        uint32_t mem = 0;
+        if (bsearch) {
+            uint32_t l[N2T_K], h[N2T_K];
+#pragma unroll
+            for (int u = 0; u < N2T_K; ++u) { l[u] = bnext; h[u] = static_cast<uint32_t>(u) < nv ? B.n : bnext; }
+            for (uint32_t span = B.n - bnext; span > 0; span >>= 1) {   // same trip count on all lanes
+#pragma unroll
+                for (int u = 0; u < N2T_K; ++u) {
+                    if (l[u] < h[u]) {
+                        const uint32_t mid = (l[u] + h[u]) >> 1;
+                        if (B.at(mid) < k[u]) l[u] = mid + 1; else h[u] = mid;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < N2T_K; ++u)
+                if (static_cast<uint32_t>(u) < nv && l[u] < B.n && B.at(l[u]) == k[u]) mem |= 1u << u;
+            st.bkeys += static_cast<unsigned long long>(cn) * (32 - __clz(B.n - bnext + 1));
+        } else if (bnext < B.n) {
+            uint32_t open = 0;
+#pragma unroll
+            for (int u = 0; u < N2T_K; ++u)
+                if (static_cast<uint32_t>(u) < nv && k[u] != pvk) open |= 1u << u;
+            for (;;) {
+                if (!tile_ok) {
+                    tlo = bnext;
+                    tn = min(N2T_TILE, B.n - bnext);
+                    __syncwarp();
+                    for (uint32_t j = lane; j < tn; j += 32) tile[j] = B.at(tlo + j);
+                    __syncwarp();
+                    tmax = tile[tn - 1];
+                    tile_ok = true;
+                    st.bkeys += tn;
+                }
+                // the lane's open keys <= tmax: binary search for the first, then merge / gallop
+                uint32_t first = N2T_K;
+#pragma unroll
+                for (int u = N2T_K - 1; u >= 0; --u)
+                    if (((open >> u) & 1u) && k[u] <= tmax) first = u;
+                if (first < N2T_K) {
+                    uint32_t k0 = k[0];
+#pragma unroll
+                    for (int u = 1; u < N2T_K; ++u) if (first == static_cast<uint32_t>(u)) k0 = k[u];
+                    uint32_t p = 0;
+#pragma unroll
+                    for (uint32_t s = N2T_TILE / 2; s > 0; s >>= 1)
+                        if (p + s <= tn && tile[p + s - 1] < k0) p += s;
+#pragma unroll
+                    for (int u = 0; u < N2T_K; ++u) {
+                        if (((open >> u) & 1u) && k[u] <= tmax) {
+                            if (linear) {
+                                while (p < tn && tile[p] < k[u]) ++p;
+                            } else {
+                                uint32_t step = 1;
+                                while (p + step <= tn && tile[p + step - 1] < k[u]) { p += step; step <<= 1; }
+                                uint32_t hi = min(p + step - 1, tn);
+                                while (p < hi) {
+                                    const uint32_t mid = (p + hi) >> 1;
+                                    if (tile[mid] < k[u]) p = mid + 1; else hi = mid;
+                                }
+                            }
+                            if (p < tn && tile[p] == k[u]) mem |= 1u << u;
+                            open &= ~(1u << u);
+                        }
+                    }
+                }
+                if (!__any_sync(FULL, open != 0)) break;
+                // smallest key still open (positions ascend with u, then lane)
+                uint32_t kmin = 0xFFFFFFFFu;
+#pragma unroll
+                for (int u = N2T_K - 1; u >= 0; --u)
+                    if ((open >> u) & 1u) kmin = k[u];
+                kmin = __reduce_min_sync(FULL, kmin);
+                bnext = tlo + tn;
+                tile_ok = false;
+                if (bnext >= B.n) break;   // B exhausted: the open keys are not members
+                bnext = mir_lower_bound(B, bnext, B.n, kmin);
+                if (bnext >= B.n) break;
+            }
+        }
+        // running S: lane-local prefix of 8 weights, warp scan of the lane totals
+        uint32_t loc[N2T_K];
+        uint32_t tot = 0;
+#pragma unroll
+        for (int u = 0; u < N2T_K; ++u) {
+            const uint32_t w = static_cast<uint32_t>(u) < nv ? (k[u] == pvk ? wp : ((mem >> u) & 1u) ? w1 : wq) : 0u;
+            tot += w;
+            loc[u] = tot;
+        }
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        const uint64_t lbase = acc + (incl - tot);   // S before the lane's first key
+        const unsigned hit = __ballot_sync(FULL, nv > 0 && lbase + tot > xs);
+        if (hit) {
+            const int f = __ffs(hit) - 1;
+            uint32_t pos = 0;
+            if (lane == static_cast<uint32_t>(f)) {
+                pos = N2T_K - 1;
+#pragma unroll
+                for (int u = N2T_K - 1; u >= 0; --u)
+                    if (lbase + loc[u] > xs) pos = u;
+            }
+            return c0 + N2T_K * f + __shfl_sync(FULL, pos, f);
+        }
+        acc += __shfl_sync(FULL, incl, 31);
+    }
+    return A.n - 1;   // not reached for xs < T
+}
+
+__global__ void __launch_bounds__(N2T_WARPS * 32, N2T_MINB) k_node2vec_tri(N2vArgs na, const uint32_t* __restrict__ tri) {
+    __shared__ uint32_t tile_all[N2T_WARPS][N2T_TILE];
+    uint32_t* tile = tile_all[threadIdx.x >> 5];
+    const WalkArgs& a = na.wa;
+    const uint32_t wp = na.wint[0], w1 = na.wint[1], wq = na.wint[2];
+    const int lane = lane_id();
+    N2tStats st;
+    unsigned long long steps = 0;
+    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+        uint32_t cur = a.seeds[w], prev = NONE;
+        uint64_t e_in = 0;   // CSR entry prev -> cur
+        const uint32_t inst = a.base + static_cast<uint32_t>(w);
+        PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
+        pw.put(0, cur);
+        uint64_t ubuf = 0;
+        for (int32_t t = 0; t < a.L; ++t) {
+            if ((t & 31) == 0)
+                ubuf = draw_u64(a.key, inst, static_cast<uint32_t>(t + lane), 0u, word3(PURPOSE_EDGE, 0, 0));
+            const uint64_t U = __shfl_sync(FULL, ubuf, t & 31);
+            uint32_t nxt = NONE;
+            if (cur != NONE) {
+                const int64_t b0 = __ldg(a.rp + cur);
+                const uint32_t d = static_cast<uint32_t>(__ldg(a.rp + cur + 1) - b0);
+                if (d > 0) {
+                    uint32_t s;
+                    if (prev == NONE) {
+                        s = static_cast<uint32_t>(below(U, d));   // step 0: uniform (R16)
+                    } else {
+                        const uint32_t C = __ldg(tri + e_in);
+                        const uint64_t T = static_cast<uint64_t>(wq) * (d - C - 1) + static_cast<uint64_t>(w1) * C + wp;
+                        const uint64_t x = below(U, T);
+                        const int64_t p0 = __ldg(a.rp + prev);
+                        const uint32_t dp = static_cast<uint32_t>(__ldg(a.rp + prev + 1) - p0);
+                        if (2 * x < T) {
+                            const MirList<false> A{a.col + b0, d}, B{a.col + p0, dp};
+                            s = n2t_scan(A, B, prev, x, wp, w1, wq, tile, st);
+                        } else {   // mirrored: the same forward scan from the end
+                            const MirList<true> A{a.col + b0, d}, B{a.col + p0, dp};
+                            s = d - 1 - n2t_scan(A, B, ~prev, T - 1 - x, wp, w1, wq, tile, st);
+                        }
+                    }
+                    e_in = static_cast<uint64_t>(b0) + s;
+                    nxt = __ldg(a.col + e_in);
+                    ++steps;
+                }
+            }
+            prev = cur;
+            cur = nxt;
+            pw.put(t + 1, cur);
+        }
+    }
+    if (lane == 0) {   // bytes: row_ptr pairs of v and prev, tri, the pick's col, + 4 per list entry read
+        if (st.keys + st.bkeys) atomicAdd(a.counters + 0, st.keys + st.bkeys);
+        if (steps) atomicAdd(a.counters + 1, steps);
+        atomicAdd(a.counters + 3, 4ull * (st.keys + st.bkeys) + 40ull * steps);
+    }
+}
+
 template <bool kFloat>
 __global__ void __launch_bounds__(WALK_WARPS * 32, 3) k_node2vec(N2vArgs na) {
     __shared__ uint64_t tab_all[WALK_WARPS][TAB];
@@ -1147,7 +1395,8 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         na.wf[0] = static_cast<float>(1.0 / b.p);
         na.wf[1] = 1.0f;
         na.wf[2] = static_cast<float>(1.0 / b.q);
-        if (m) k_node2vec<false><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(na);
+        if (m && g->tri) k_node2vec_tri<<<walk_grid(g, n), N2T_WARPS * 32, 0, st>>>(na, g->tri);
+        else if (m) k_node2vec<false><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(na);
         else k_node2vec<true><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(na);
     } else if (b.kind == CSAW_BIAS_MDRW) {
         const uint32_t m = static_cast<uint32_t>(b.pool_size);

@@ -20,9 +20,9 @@ from tests._parity import DEV, u32
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
-def build(cfg):
+def build(cfg, ctps_cache=False):
     g = rmat_csr(cfg.graph_vertices, cfg.graph_entries, cfg.graph_seed, device=DEV)
-    G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0)
+    G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, ctps_cache=ctps_cache)
     og = O.Graph(g.row_ptr.cpu().numpy(), g.col_idx.cpu().numpy().view(np.uint32))
     return g, G, og
 
@@ -54,9 +54,12 @@ def check_edges_exist(og, src, dst):
         assert i < row.size and row[i] == d
 
 
-def test_cfg2_degree_walk_full():
+@pytest.mark.parametrize("cached", [False, True])
+def test_cfg2_degree_walk_full(cached):
+    """cached=True is the bench's launch: CTPS cache + narrow walk index (k_walk_wix)."""
     cfg = CONFIGS["cfg2"]
-    g, G, og = build(cfg)
+    g, G, og = build(cfg, ctps_cache=cached)
+    assert G.info()["walk_index_leaf"] == (64 if cached else 0)
     seeds = instance_seeds(g, cfg.n_instances).to(DEV)
     path = u32(cs.csaw_walk(G, "degree", seeds, cfg.length, rng_seed=1))
     assert path.shape == (cfg.n_instances, cfg.length + 1)
@@ -70,9 +73,12 @@ def test_cfg2_degree_walk_full():
     release(G)
 
 
-def test_cfg3_node2vec_full():
+@pytest.mark.parametrize("cached", [False, True])
+def test_cfg3_node2vec_full(cached):
+    """cached=True is the bench's launch: per-edge triangle counts + partial scans (k_node2vec_tri)."""
     cfg = CONFIGS["cfg3"]
-    g, G, og = build(cfg)
+    g, G, og = build(cfg, ctps_cache=cached)
+    assert G.info()["node2vec_tri"] == (1 if cached else 0)
     seeds = nonisolated_vertices(g).to(torch.int32).to(DEV)
     n = seeds.numel()
     path = u32(cs.csaw_walk(G, cs.make_bias("node2vec", p=cfg.p, q=cfg.q), seeds, cfg.length, rng_seed=1))
