@@ -604,7 +604,7 @@ def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0):
             return f"k_walk_wix<{wix_leaf}>" if wix_group == 32 else f"k_walk_wixg<{wix_group}, {wix_leaf}>"
         return "k_walk_cached" if (cfg.bias == "degree" and cached) else f"k_walk<{cfg.bias}>"
     if cfg.workload == "mdrw":
-        return "k_mdrw_oom_part" if oom else "k_mdrw"
+        return "k_mdrw_oom_part" if oom else ("k_mdrw_fast" if cfg.pool_size <= 2048 else "k_mdrw")
     if cfg.workload == "node2vec":
         return "k_node2vec_tri" if cached else "k_node2vec<int>"
     if oom:

@@ -330,14 +330,16 @@ static csaw_status build_wix_t(csaw_graph* g, int blocks) {
     if (s == CSAW_OK && total + 16 < (uint64_t(1) << 32) && nl < (uint64_t(1) << 32)) {
         if (cudaMalloc(&g->c32, sizeof(uint32_t) * nl) != cudaSuccess ||
             cudaMalloc(&g->wcol, sizeof(uint32_t) * nl) != cudaSuccess ||
-            cudaMalloc(&g->wrec, sizeof(uint4) * std::max<int64_t>(V, 1)) != cudaSuccess ||
-            cudaMalloc(&g->winn, sizeof(uint32_t) * (total + 16)) != cudaSuccess) {
+            cudaMalloc(&g->winn, sizeof(uint32_t) * (total + 16) + sizeof(uint4) * std::max<int64_t>(V, 1)) != cudaSuccess) {
             cudaGetLastError();
             s = fail(CSAW_ERR_NO_MEMORY, "cudaMalloc(walk index)");
         } else {
             cudaMemset(g->c32, 0, sizeof(uint32_t) * nl);   // padding entries (read, then masked)
             cudaMemset(g->wcol, 0, sizeof(uint32_t) * nl);
             cudaMemset(g->winn, 0, sizeof(uint32_t) * (total + 16));
+            // records right after the nodes (total + 16 is a multiple of 4: 16 B aligned), so one
+            // L2 access-policy window can cover both (the per-step upper levels of the chain)
+            g->wrec = reinterpret_cast<uint4*>(g->winn + total + 16);
             k_wix_build<FL><<<blocks, 256>>>(g->row_ptr, g->col, g->cps, woff, V, g->wrec, g->c32, g->wcol, g->winn);
             g->winn_entries = total + 16;
             g->wleaf_entries = nl;
@@ -366,6 +368,14 @@ static csaw_status build_wix(csaw_graph* g, int blocks) {
                                                                : build_wix_t<128>(g, blocks);
     if (s == CSAW_OK && g->c32) {
         g->wix_leaf = leaf;
+        const char* pe = std::getenv("CSAW_L2_PERSIST");   // A/B: pin nodes + records in L2
+        if (pe && pe[0] == '1') {
+            int maxp = 0;
+            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, g->device);
+            if (maxp > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(maxp)) == cudaSuccess)
+                g->l2_persist_bytes = static_cast<size_t>(maxp);
+            cudaGetLastError();
+        }
         // lanes per walker: 32 (one warp per walker, default) | 16 | 8 (A/B: the sub-warp
         // kernels are slower at cfg2, 3.7 / 4.4 ms vs 2.8 ms: a warp's walkers then wait for
         // the slowest of their dependent-load chains every step)
@@ -669,7 +679,6 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->tri) cudaFree(g->tri);
     if (g->wcol) cudaFree(g->wcol);
     if (g->winn) cudaFree(g->winn);
-    if (g->wrec) cudaFree(g->wrec);
     auto& st = g->oomst;
     if (st.h_col) cudaFreeHost(st.h_col);
     if (st.h_row) cudaFreeHost(st.h_row);

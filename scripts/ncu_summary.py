@@ -67,7 +67,8 @@ def main():
     out = [f"# {rnd} — ncu `--set full` summary, one hot-kernel launch per config", "",
            "Each row: `ncu --set full --clock-control none --import-source on --nvtx --nvtx-include csaw_step/ "
            "-k regex:<kernel> -c 1` around `bench.py --config <cfg> --steps 1 --warmup 1` "
-           "(cfg3: `scripts/prof_n2v.py 40`, a 1/40 walker subset), exported with `ncu -i --page raw --csv` "
+           "(cfg3: `scripts/prof_n2v.py 40 cache`, a 1/40 walker subset; its full bench launch is measured by a "
+           "metrics-only pass), exported with `ncu -i --page raw --csv` "
            "(`scripts/gpu_prof_all.sh`, `scripts/ncu_summary.py`).  ncu times are cold-cache and serialised: "
            "the bench line's CUDA-event numbers are the measurement; these explain them.", "",
            f"DRAM GB/s is ncu DRAM bytes / ncu duration; fraction of the measured {peak:.1f} GB/s copy peak.", "",
@@ -97,6 +98,31 @@ def main():
             note = "per launch of the bench's hot kernel (1 bench step)"
         traffic[key] = {"kernel": d["kernel"], "dram_bytes_per_launch": int(dram), "ncu_ms": d["time"] * 1e3,
                         "round": rnd, "note": note}
+    # metrics-only launch lists with DRAM counters (cfg3: the full bench launch, too long for --set full)
+    for path in sorted(glob.glob(os.path.join(src, "*_launches.csv"))):
+        cfg = os.path.basename(path)[:-len("_launches.csv")]
+        rows = [r for r in csv.reader(open(path)) if r]
+        hi = [j for j, r in enumerate(rows) if r[0] == "ID"]
+        if not hi:
+            continue
+        h = rows[hi[0]]
+        per = {}
+        for r in rows[hi[0] + 1:]:
+            d = dict(zip(h, r))
+            if d.get("Metric Name") in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"):
+                k = (d.get("ID"), d.get("Kernel Name", "").split("(")[0])
+                per.setdefault(k, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+        for (lid, kname), m in per.items():
+            if "dram__bytes_read.sum" not in m:
+                continue
+            dram = m["dram__bytes_read.sum"] + m.get("dram__bytes_write.sum", 0.0)
+            t = m.get("gpu__time_duration.sum", 0.0) * 1e-9
+            key = cfg.replace("@", "_")
+            traffic[key] = {"kernel": kname, "dram_bytes_per_launch": int(dram), "ncu_ms": t * 1e3, "round": rnd,
+                            "note": "metrics-only pass (dram__bytes_read/write.sum) over the bench's timed launch"}
+            if t > 0:
+                out.append(f"| {cfg} (metrics-only, full launch) | `{kname}` | {t * 1e3:.3f} | {dram / 1e9:.3f} GB | "
+                           f"{dram / t / 1e9:.0f} ({dram / t / 1e9 / peak:.3f}) | | | | | | | | |")
     traffic["_source"] = ("ncu --set full --clock-control none (profiles/%s_ncu_summary.md); "
                           "dram__bytes_read.sum + dram__bytes_write.sum per launch of the hot kernel" % rnd)
     json.dump(traffic, open(traffic_path, "w"), indent=1)
