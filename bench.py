@@ -52,7 +52,8 @@ def parse_args():
     ap.add_argument("--gather", action="store_true", help="NCCL-gather outputs after timing (reported apart)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--in-memory", action="store_true", help="cfg5: ignore the OOM budget (in-memory MDRW)")
-    ap.add_argument("--no-cache", action="store_true", help="disable the static-bias CTPS cache (scan every pool)")
+    ap.add_argument("--no-cache", action="store_true",
+                    help="disable the static-bias CTPS cache / node2vec triangle counts (scan every pool)")
     ap.add_argument("--no-zerocopy", action="store_true", help="cfg5: skip the zero-copy OOM variant")
     return ap.parse_args()
 
@@ -333,8 +334,9 @@ def main():
                                  num_streams=cfg.oom_resident)
     else:
         # static-bias CTPS cache (§8(f) NEXT-1, bit-identical) for degree-biased selections
-        use_cache = (not args.no_cache) and (cfg.bias in ("degree", "layer") or cfg.workload == "node2vec")
-        G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache)
+        use_cache = (not args.no_cache) and cfg.bias in ("degree", "layer")
+        use_tri = (not args.no_cache) and cfg.workload == "node2vec"   # node2vec edge triangle counts
+        G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache, node2vec_tri=use_tri)
     ginfo = G.info()
     bias = bias_of(cs, cfg)
     stream = torch.cuda.current_stream(dev)

@@ -141,6 +141,13 @@ typedef struct {
  * walks then search the u64 fanout-32 index instead.  Results are identical
  * either way; this flag exists for tests and A/B measurements. */
 #define CSAW_GRAPH_NO_WALK_INDEX 0x20u
+/* csaw_graph_opts.flags (in-memory graphs with sorted rows): build per-edge triangle
+ * counts tri[e] = |N(v) ∩ N(u)| for every CSR entry e = (v -> u) (one u32 per entry;
+ * ignored unless the graph is symmetric).  Integer node2vec walks (R16) then
+ * get the row total of each step's CTPS in closed form and scan N(v) only from the end
+ * nearer the draw up to its region, instead of merging all of N(v) with N(prev).  The
+ * picks are identical (same integer S, same draw).  Reported in csaw_graph_info_t. */
+#define CSAW_GRAPH_N2V_TRI 0x40u
 
 typedef struct {
     int64_t num_vertices, num_edges;
@@ -153,7 +160,7 @@ typedef struct {
     int32_t walk_index_leaf;        /* narrow walk index leaf fanout (32/64/128; 129 = col read after the leaf), 0 = not built */
     double cache_build_ms;          /* device time of the cache build */
     int32_t walk_index_group;       /* lanes per walker of the degree-walk kernel (8 / 16; 32 = one warp per walker) */
-    int32_t node2vec_tri;           /* 1 if per-edge triangle counts were built (node2vec partial scans) */
+    int32_t node2vec_tri;           /* 1 if per-edge triangle counts were built (CSAW_GRAPH_N2V_TRI on a symmetric graph) */
 } csaw_graph_info_t;
 
 typedef struct csaw_graph csaw_graph;  /* opaque */

@@ -337,8 +337,7 @@ static csaw_status build_wix_t(csaw_graph* g, int blocks) {
             cudaMemset(g->c32, 0, sizeof(uint32_t) * nl);   // padding entries (read, then masked)
             cudaMemset(g->wcol, 0, sizeof(uint32_t) * nl);
             cudaMemset(g->winn, 0, sizeof(uint32_t) * (total + 16));
-            // records right after the nodes (total + 16 is a multiple of 4: 16 B aligned), so one
-            // L2 access-policy window can cover both (the per-step upper levels of the chain)
+            // records right after the nodes (total + 16 is a multiple of 4: 16 B aligned)
             g->wrec = reinterpret_cast<uint4*>(g->winn + total + 16);
             k_wix_build<FL><<<blocks, 256>>>(g->row_ptr, g->col, g->cps, woff, V, g->wrec, g->c32, g->wcol, g->winn);
             g->winn_entries = total + 16;
@@ -368,14 +367,6 @@ static csaw_status build_wix(csaw_graph* g, int blocks) {
                                                                : build_wix_t<128>(g, blocks);
     if (s == CSAW_OK && g->c32) {
         g->wix_leaf = leaf;
-        const char* pe = std::getenv("CSAW_L2_PERSIST");   // A/B: pin nodes + records in L2
-        if (pe && pe[0] == '1') {
-            int maxp = 0;
-            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, g->device);
-            if (maxp > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(maxp)) == cudaSuccess)
-                g->l2_persist_bytes = static_cast<size_t>(maxp);
-            cudaGetLastError();
-        }
         // lanes per walker: 32 (one warp per walker, default) | 16 | 8 (A/B: the sub-warp
         // kernels are slower at cfg2, 3.7 / 4.4 ms vs 2.8 ms: a warp's walkers then wait for
         // the slowest of their dependent-load chains every step)
@@ -449,11 +440,10 @@ __global__ void k_tri(const int64_t* __restrict__ rp, const uint32_t* __restrict
     }
 }
 
-// Builds tri (CTPS-cache graphs with sorted rows); leaves g->tri null if the graph is not
-// symmetric.  CSAW_N2V_TRI=0 skips it (A/B).
+// Builds tri (CSAW_GRAPH_N2V_TRI, sorted rows); leaves g->tri null if the graph is not
+// symmetric (node2vec then keeps the full-merge kernel).
 static csaw_status build_tri(csaw_graph* g, int blocks) {
-    const char* env = std::getenv("CSAW_N2V_TRI");
-    if ((env && env[0] == '0') || !g->rows_sorted || g->E <= 0) return CSAW_OK;
+    if (!g->rows_sorted || g->E <= 0) return CSAW_OK;
     uint32_t* src = nullptr;
     unsigned int* asym = nullptr;
     if (cudaMalloc(&src, sizeof(uint32_t) * g->E) != cudaSuccess || cudaMalloc(&asym, sizeof(unsigned int)) != cudaSuccess ||
@@ -643,15 +633,27 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
             const csaw_status ws = build_wix(g, blocks);
             if (ws != CSAW_OK) return cleanup(ws);
         }
-        {
-            const csaw_status ts = build_tri(g, blocks);
-            if (ts != CSAW_OK) return cleanup(ts);
-        }
+
         cudaEventRecord(c1);
         CREATE_CUDA(cudaEventSynchronize(c1), "build cps");
         float ms = 0.f;
         cudaEventElapsedTime(&ms, c0, c1);
         g->cache_build_ms = ms;
+        cudaEventDestroy(c0);
+        cudaEventDestroy(c1);
+    }
+    if ((o.flags & CSAW_GRAPH_N2V_TRI) && !g->oom) {   // node2vec edge triangle counts (walk.cu k_node2vec_tri)
+        cudaEvent_t c0, c1;
+        CREATE_CUDA(cudaEventCreate(&c0), "event");
+        CREATE_CUDA(cudaEventCreate(&c1), "event");
+        cudaEventRecord(c0);
+        const csaw_status ts = build_tri(g, blocks);
+        if (ts != CSAW_OK) return cleanup(ts);
+        cudaEventRecord(c1);
+        CREATE_CUDA(cudaEventSynchronize(c1), "build tri");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c0, c1);
+        g->cache_build_ms += ms;
         cudaEventDestroy(c0);
         cudaEventDestroy(c1);
     }

@@ -127,7 +127,6 @@ struct csaw_graph {
     uint4* wrec = nullptr;        // [V] {row start lo, hi, degree, index offset}
     uint32_t* winn = nullptr;     // internal levels (fanout 128), top level first per row
     uint64_t winn_entries = 0;    // size of winn (the records wrec follow it in the same allocation)
-    size_t l2_persist_bytes = 0;  // CSAW_L2_PERSIST=1: L2 set-aside for the walk index's nodes + records (0 = off)
     uint64_t wleaf_entries = 0;   // size of c32 / wcol
     uint32_t* tri = nullptr;      // [E] node2vec: |N(v) ∩ N(u)| per entry (symmetric sorted graphs, cache builds)
     int wix_group = 8;            // lanes per walker in k_walk_wixg (32 = k_walk_wix, one warp per walker)

@@ -1360,32 +1360,7 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
                                                 static_cast<int64_t>(g->num_sms) * 64);
         const int grid = static_cast<int>(std::max<int64_t>(1, (warps + wpb - 1) / wpb));
         const uint4* rec = g->wrec;
-        if (g->wix_group == 32 && g->l2_persist_bytes) {
-            // nodes + records (one allocation) as a persisting L2 window for this launch
-            int maxw = 0;
-            cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, g->device);
-            const size_t want = sizeof(uint32_t) * g->winn_entries + sizeof(uint4) * static_cast<size_t>(g->V);
-            const size_t nb = std::min(want, static_cast<size_t>(maxw));
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-            at[0].val.accessPolicyWindow.base_ptr = g->winn;
-            at[0].val.accessPolicyWindow.num_bytes = nb;
-            at[0].val.accessPolicyWindow.hitRatio = nb ? std::min(1.0f, static_cast<float>(g->l2_persist_bytes) / nb) : 0.f;
-            at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-            at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-            cudaLaunchConfig_t lc{};
-            lc.gridDim = dim3(grid);
-            lc.blockDim = dim3(blk);
-            lc.stream = st;
-            lc.attrs = at;
-            lc.numAttrs = 1;
-            const uint32_t* c32 = g->c32;
-            const uint32_t* wcol = g->wcol;
-            const uint32_t* winn = g->winn;
-            if (g->wix_leaf == 32) CSAW_CUDA(cudaLaunchKernelEx(&lc, k_walk_wix<32>, a, rec, c32, wcol, winn));
-            else if (g->wix_leaf == 64) CSAW_CUDA(cudaLaunchKernelEx(&lc, k_walk_wix<64>, a, rec, c32, wcol, winn));
-            else CSAW_CUDA(cudaLaunchKernelEx(&lc, k_walk_wix<128>, a, rec, c32, wcol, winn));
-        } else if (g->wix_group == 32) {
+        if (g->wix_group == 32) {
             if (g->wix_leaf == 32) k_walk_wix<32><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);
             else if (g->wix_leaf == 64) k_walk_wix<64><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);
             else k_walk_wix<128><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);

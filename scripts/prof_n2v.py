@@ -8,7 +8,7 @@ import paper_2009_09103_b200 as cs
 from synth import CONFIGS, rmat_csr, nonisolated_vertices
 cfg = CONFIGS["cfg3"]
 g = rmat_csr(cfg.graph_vertices, cfg.graph_entries, cfg.graph_seed, device="cuda")
-G = cs.csaw_graph_create(g.row_ptr, g.col_idx, ctps_cache="cache" in sys.argv[2:])  # "cache": k_node2vec_tri
+G = cs.csaw_graph_create(g.row_ptr, g.col_idx, node2vec_tri="cache" in sys.argv[2:])  # "cache": k_node2vec_tri
 seeds = nonisolated_vertices(g)[:: max(1, int(sys.argv[1]) if len(sys.argv) > 1 else 40)].to(torch.int32).cuda()
 b = cs.make_bias("node2vec", p=cfg.p, q=cfg.q)
 for _ in range(2):

@@ -20,9 +20,9 @@ from tests._parity import DEV, u32
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
-def build(cfg, ctps_cache=False):
+def build(cfg, ctps_cache=False, node2vec_tri=False):
     g = rmat_csr(cfg.graph_vertices, cfg.graph_entries, cfg.graph_seed, device=DEV)
-    G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, ctps_cache=ctps_cache)
+    G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, ctps_cache=ctps_cache, node2vec_tri=node2vec_tri)
     og = O.Graph(g.row_ptr.cpu().numpy(), g.col_idx.cpu().numpy().view(np.uint32))
     return g, G, og
 
@@ -77,7 +77,7 @@ def test_cfg2_degree_walk_full(cached):
 def test_cfg3_node2vec_full(cached):
     """cached=True is the bench's launch: per-edge triangle counts + partial scans (k_node2vec_tri)."""
     cfg = CONFIGS["cfg3"]
-    g, G, og = build(cfg, ctps_cache=cached)
+    g, G, og = build(cfg, node2vec_tri=cached)
     assert G.info()["node2vec_tri"] == (1 if cached else 0)
     seeds = nonisolated_vertices(g).to(torch.int32).to(DEV)
     n = seeds.numel()

@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 def cached(rp, col):
     rpt = torch.as_tensor(np.asarray(rp, dtype=np.int64))
     ct = torch.as_tensor(np.asarray(col).astype(np.uint32).view(np.int32))
-    G = cs.csaw_graph_create(rpt.to(DEV), ct.to(DEV), ctps_cache=True)
+    G = cs.csaw_graph_create(rpt.to(DEV), ct.to(DEV), node2vec_tri=True)
     return G, O.Graph(rpt.numpy(), ct.numpy().view(np.uint32))
 
 
@@ -82,7 +82,7 @@ def test_tri_not_built_for_asymmetric():
 def test_tri_equals_uncached_large_batch():
     g = rmat_csr(1 << 16, 1 << 20, 5, device=DEV)
     seeds = instance_seeds(g, 20_000, set_id=2).to(DEV)
-    G1 = cs.csaw_graph_create(g.row_ptr, g.col_idx, ctps_cache=True)
+    G1 = cs.csaw_graph_create(g.row_ptr, g.col_idx, node2vec_tri=True)
     G2 = cs.csaw_graph_create(g.row_ptr, g.col_idx)
     b = cs.make_bias("node2vec", p=2.0, q=0.5)
     assert torch.equal(cs.csaw_walk(G1, b, seeds, 25, rng_seed=4), cs.csaw_walk(G2, b, seeds, 25, rng_seed=4))
