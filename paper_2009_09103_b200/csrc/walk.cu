@@ -819,22 +819,34 @@ __device__ void n2v_implicit_step(Node2vecPool& P, uint32_t* spec, uint32_t* til
 // N(v) instead of all of it plus all of N(prev).  Same S, same x, same region as the
 // scanned CTPS and the oracle (bit-identical).
 constexpr uint32_t N2T_TILE = 1024;   // N(prev) window in shared memory (u32), per warp
-constexpr int N2T_K = 8;              // keys per lane per chunk (contiguous positions)
+#ifndef N2T_KEYS
+#define N2T_KEYS 4
+#endif
+constexpr int N2T_K = N2T_KEYS;       // keys per lane per chunk (contiguous positions)
 constexpr int N2T_WARPS = 8;
 #ifndef N2T_MINB
 #define N2T_MINB 3
 #endif
 
-template <bool kRev>
+// A sorted list read forwards, or backwards with every value complemented (x -> ~x
+// reverses u32 order, so the mirrored list is ascending too): at(i) = p[b + s i] ^ m with
+// (b, s, m) = (0, 1, 0) or (n - 1, -1, ~0).  One code path for both scan directions (a
+// template per direction doubled the kernel and stalled on instruction fetch).
 struct MirList {
-    const uint32_t* __restrict__ p;
+    const uint32_t* __restrict__ p;   // p[0] = the first element in scan order
     uint32_t n;
-    __device__ __forceinline__ uint32_t at(uint32_t i) const { return kRev ? ~__ldg(p + (n - 1 - i)) : __ldg(p + i); }
+    int32_t s;                         // +1 / -1
+    uint32_t m;                        // 0 / 0xFFFFFFFF
+    __device__ __forceinline__ uint32_t at(uint32_t i) const {
+        return __ldg(p + static_cast<int64_t>(s) * static_cast<int64_t>(i)) ^ m;
+    }
 };
+__device__ __forceinline__ MirList mir_list(const uint32_t* p, uint32_t n, bool rev) {
+    return rev ? MirList{p + (n ? n - 1 : 0), n, -1, 0xFFFFFFFFu} : MirList{p, n, 1, 0u};
+}
 
 // First idx in [lo, hi) with L.at(idx) >= key (hi if none); 32-ary warp search.
-template <bool kRev>
-__device__ __forceinline__ uint32_t mir_lower_bound(const MirList<kRev>& L, uint32_t lo, uint32_t hi, uint32_t key) {
+__device__ __forceinline__ uint32_t mir_lower_bound(const MirList& L, uint32_t lo, uint32_t hi, uint32_t key) {
     const uint32_t lane = static_cast<uint32_t>(lane_id());
     while (hi - lo > 32) {
         const uint32_t step = (hi - lo + 31) / 32;
@@ -868,8 +880,7 @@ struct N2tStats {
 // shared-memory tile of B: per lane one binary search for its first key, then a linear
 // merge (B about as dense as A) or galloping searches (B denser); B much longer than A:
 // per-key binary searches of B in global memory.
-template <bool kRev>
-__device__ uint32_t n2t_scan(const MirList<kRev>& A, const MirList<kRev>& B, uint32_t pvk, uint64_t xs, uint32_t wp,
+__device__ uint32_t n2t_scan(const MirList& A, const MirList& B, uint32_t pvk, uint64_t xs, uint32_t wp,
                              uint32_t w1, uint32_t wq, uint32_t* tile, N2tStats& st) {
     const uint32_t lane = static_cast<uint32_t>(lane_id());
     const bool bsearch = B.n > 16u * A.n;
@@ -1032,13 +1043,10 @@ __global__ void __launch_bounds__(N2T_WARPS * 32, N2T_MINB) k_node2vec_tri(N2vAr
                         const uint64_t x = below(U, T);
                         const int64_t p0 = __ldg(a.rp + prev);
                         const uint32_t dp = static_cast<uint32_t>(__ldg(a.rp + prev + 1) - p0);
-                        if (2 * x < T) {
-                            const MirList<false> A{a.col + b0, d}, B{a.col + p0, dp};
-                            s = n2t_scan(A, B, prev, x, wp, w1, wq, tile, st);
-                        } else {   // mirrored: the same forward scan from the end
-                            const MirList<true> A{a.col + b0, d}, B{a.col + p0, dp};
-                            s = d - 1 - n2t_scan(A, B, ~prev, T - 1 - x, wp, w1, wq, tile, st);
-                        }
+                        const bool rev = 2 * x >= T;   // mirrored: the same forward scan from the end
+                        const MirList A = mir_list(a.col + b0, d, rev), B = mir_list(a.col + p0, dp, rev);
+                        const uint32_t sp = n2t_scan(A, B, rev ? ~prev : prev, rev ? T - 1 - x : x, wp, w1, wq, tile, st);
+                        s = rev ? d - 1 - sp : sp;
                     }
                     e_in = static_cast<uint64_t>(b0) + s;
                     nxt = __ldg(a.col + e_in);
