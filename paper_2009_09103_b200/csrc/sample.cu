@@ -686,6 +686,9 @@ __global__ void k_part_scatter(const uint32_t* __restrict__ qv, uint64_t nq, Own
 // pool needing > 32 picks) raises the overflow flag and the host reruns the call
 // with the batched driver.
 constexpr int FUSED_WARPS = 4;
+#ifndef FUSED_MINB
+#define FUSED_MINB 4
+#endif
 constexpr uint32_t F_CAP = 256;
 constexpr uint32_t VIS_CAP = 512;
 
@@ -700,7 +703,7 @@ struct FusedArgs {
     const uint32_t* __restrict__ seeds;
     uint64_t n;
     int32_t depth;
-    const int32_t* __restrict__ fanout;   // device [depth]
+    int32_t fanout[16];                   // per level (kernel parameter: no copy per call)
     uint64_t theta;                       // forest fire
     uint32_t base;
     uint2 key;
@@ -748,7 +751,7 @@ struct FusedLayerEmit {
 // kMode: 0 uniform NS, 1 degree NS (scan), 2 degree NS (cache), 3 forest fire,
 //        4 layer (scan), 5 layer (cache)
 template <int kMode>
-__global__ void __launch_bounds__(FUSED_WARPS * 32, 4) k_sample_fused(FusedArgs a) {
+__global__ void __launch_bounds__(FUSED_WARPS * 32, kMode >= 3 ? 6 : FUSED_MINB) k_sample_fused(FusedArgs a) {
     __shared__ uint64_t tab_all[FUSED_WARPS][TAB];
     __shared__ uint32_t bm_all[FUSED_WARPS][BM_WORDS];
     __shared__ uint32_t F_all[FUSED_WARPS][F_CAP];
@@ -1023,6 +1026,15 @@ static csaw_status oom_select_level(const csaw_graph* g, const csaw_bias& b, con
 // FUSED_FALLBACK when the batched level-synchronous driver must run instead.
 constexpr csaw_status FUSED_FALLBACK = static_cast<csaw_status>(-1);
 
+__global__ void k_fused_report(const unsigned* __restrict__ ovf, const uint64_t* __restrict__ total,
+                               const unsigned long long* __restrict__ counters, uint64_t* hbox) {
+    const int t = threadIdx.x;
+    if (t == 0) hbox[0] = *ovf;
+    if (t == 1) hbox[1] = *total;
+    if (t >= 2 && t < 6) hbox[t] = counters[t - 2];
+    __threadfence_system();
+}
+
 static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
                                     const uint32_t* d_seeds, uint64_t n, uint64_t base, uint64_t seed,
                                     uint64_t* d_offsets, uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity,
@@ -1041,9 +1053,9 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
             ecap_d += level;
         }
     }
-    if (ecap_d > 2048 || n == 0) return FUSED_FALLBACK;
+    if (ecap_d > 2048 || n == 0 || depth > 16) return FUSED_FALLBACK;
     const uint32_t ecap = std::max<uint32_t>(1, static_cast<uint32_t>(ecap_d));
-    void *pc, *ps, *pd, *pe, *pk, *pf, *pp;
+    void *pc, *ps, *pd, *pe, *pk, *pp;
     CSAW_TRY(g->scratch.get(SL_COUNTS, 256, &pc));
     unsigned long long* counters = static_cast<unsigned long long*>(pc);
     unsigned* ovf = reinterpret_cast<unsigned*>(counters + 12);
@@ -1051,19 +1063,16 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     CSAW_TRY(g->scratch.get(SL_SRC + 201, sizeof(uint32_t) * n * ecap, &pd));
     CSAW_TRY(g->scratch.get(SL_SRC + 202, static_cast<size_t>(n) * ecap, &pe));
     CSAW_TRY(g->scratch.get(SL_SRC + 203, sizeof(uint64_t) * n, &pk));
-    CSAW_TRY(g->scratch.get(SL_SRC + 204, sizeof(int32_t) * std::max(depth, 1), &pf));
     CSAW_TRY(g->scratch.get(SL_TMP2, sizeof(uint64_t) * (SCAN_MAX_GRID + 8), &pp));
     void* hmb;
     CSAW_TRY(g->pinned.get(4096, &hmb));
     volatile uint64_t* hbox = static_cast<volatile uint64_t*>(hmb);
-    int32_t* hfan = reinterpret_cast<int32_t*>(const_cast<uint64_t*>(hbox) + 64);
-    for (int d = 0; d < depth; ++d) hfan[d] = ff ? 0 : fanout[d];
     CSAW_CUDA(cudaMemsetAsync(counters, 0, 256, st));
-    CSAW_CUDA(cudaMemcpyAsync(pf, hfan, sizeof(int32_t) * depth, cudaMemcpyHostToDevice, st));
     CSAW_TRY(stats_begin(g, st));
     FusedArgs a;
     a.rp = g->row_ptr; a.col = g->oom ? g->oomst.h_col : g->col; a.deg = g->deg; a.cps = g->cps; a.npos = g->npos; a.bt = g->bt;
-    a.bt_off = g->bt_off; a.seeds = d_seeds; a.n = n; a.depth = depth; a.fanout = static_cast<int32_t*>(pf);
+    a.bt_off = g->bt_off; a.seeds = d_seeds; a.n = n; a.depth = depth;
+    for (int d = 0; d < 16; ++d) a.fanout[d] = (d < depth && !ff) ? fanout[d] : 0;
     a.theta = ff ? static_cast<uint64_t>(std::floor(b.pf * 4294967296.0)) : 0;
     a.base = static_cast<uint32_t>(base);
     a.key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
@@ -1100,10 +1109,10 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
         CSAW_CUDA(cudaGetLastError());
     }
     CSAW_TRY(stats_end(g, st));
-    hbox[0] = 0;
-    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[0], ovf, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[1], d_offsets + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    CSAW_CUDA(cudaMemcpyAsync((void*)&hbox[2], counters, sizeof(uint64_t) * 4, cudaMemcpyDeviceToHost, st));
+    // flags, edge total and counters straight into the pinned mailbox (one launch, no copies)
+    k_fused_report<<<1, 32, 0, st>>>(ovf, d_offsets + n, counters, const_cast<uint64_t*>(hbox));
+    note_launch();
+    CSAW_CUDA(cudaGetLastError());
     CSAW_CUDA(cudaStreamSynchronize(st));
     const unsigned flags = static_cast<unsigned>(hbox[0] & 0xFFFFFFFFu);
     if (flags & 2u) return fail(CSAW_ERR_OUT_OF_RANGE, "a seed vertex is >= num_vertices");

@@ -87,9 +87,35 @@ struct ScanToArray {
     __device__ __forceinline__ void total(uint64_t n, uint64_t t) const { dst[n] = t; }
 };
 
+// Small n (<= SCAN_BLOCK * SCAN_ONE_PER): one block, each thread a contiguous run of
+// ceil(n / SCAN_BLOCK) values -> one launch instead of three.
+constexpr uint64_t SCAN_ONE_PER = 32;
+template <class Val, class Out>
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_one(Val val, uint64_t n, Out out) {
+    __shared__ uint64_t wsum[SCAN_BLOCK / 32];
+    __shared__ uint64_t total;
+    const uint64_t per = (n + SCAN_BLOCK - 1) / SCAN_BLOCK;
+    const uint64_t b0 = min(n, threadIdx.x * per), b1 = min(n, b0 + per);
+    uint64_t s = 0;
+    for (uint64_t i = b0; i < b1; ++i) s += val(i);
+    uint64_t run = block_excl_scan<SCAN_BLOCK>(s, wsum, &total);
+    for (uint64_t i = b0; i < b1; ++i) {
+        const uint64_t v = val(i);
+        out(i, run, v);
+        run += v;
+    }
+    if (threadIdx.x == 0) out.total(n, total);
+}
+
 // Host driver: exclusive scan of val(0..n) -> out; part = device scratch >= SCAN_MAX_GRID+1 u64.
 template <class Val, class Out>
 csaw_status device_scan(Val val, uint64_t n, Out out, uint64_t* part, cudaStream_t st) {
+    if (n > 0 && n <= SCAN_BLOCK * SCAN_ONE_PER) {
+        k_scan_one<<<1, SCAN_BLOCK, 0, st>>>(val, n, out);
+        note_launch();
+        CSAW_CUDA(cudaGetLastError());
+        return CSAW_OK;
+    }
     int g = static_cast<int>(std::min<uint64_t>(SCAN_MAX_GRID, (n + 8 * SCAN_BLOCK - 1) / (8 * SCAN_BLOCK)));
     if (g < 1) g = 1;
     const uint64_t chunk = (n + g - 1) / g;
