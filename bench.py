@@ -55,6 +55,11 @@ def parse_args():
     ap.add_argument("--no-cache", action="store_true",
                     help="disable the static-bias CTPS cache / node2vec triangle counts (scan every pool)")
     ap.add_argument("--no-zerocopy", action="store_true", help="cfg5: skip the zero-copy OOM variant")
+    ap.add_argument("--oom-budget-gb", type=float, default=0.0,
+                    help="OOM configs: override the device budget (GiB) -- experiments only, the config names 8 GB")
+    ap.add_argument("--oom-variant", default="partition", choices=["partition", "zerocopy"],
+                    help="OOM configs: time the paper's partition scheduling (default) or the zero-copy mode "
+                         "(col_idx prefix resident within the budget, the rest read in place from pinned host memory)")
     return ap.parse_args()
 
 
@@ -273,7 +278,7 @@ def run_reference(args):
     return 0
 
 
-def config_block(cfg, world, stats_g):
+def config_block(cfg, world, stats_g, oom_mode=None, colc=None):
     c = {"workload": f"{cfg.name}: {cfg.description}", "instances_per_gpu": cfg.n_instances or "all non-isolated",
          "graph": {"V": cfg.graph_vertices, "E_target": cfg.graph_entries, "generator": "R-MAT Graph500 (0.57,0.19,0.19,0.05), symmetrised, dedup"},
          "parallelism": f"instances sharded over {world} GPU(s), CSR replicated",
@@ -293,6 +298,12 @@ def config_block(cfg, world, stats_g):
     if cfg.oom_budget_bytes:
         c["oom"] = {"device_budget_bytes": cfg.oom_budget_bytes, "partitions": cfg.oom_partitions,
                     "resident": cfg.oom_resident, "streams": cfg.oom_resident}
+        if oom_mode == "zerocopy":
+            c["oom"] = {"device_budget_bytes": cfg.oom_budget_bytes, "mode": "zero-copy: a col_idx prefix resident "
+                        "within the budget, the rest read in place from pinned host memory",
+                        "graph_device_bytes": colc}
+        elif oom_mode:
+            c["oom"]["mode"] = "partition scheduling (paper §5)"
     if stats_g:
         c["graph_stats"] = stats_g
     return c
@@ -316,6 +327,9 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
+    if args.oom_budget_gb > 0 and cfg.oom_budget_bytes:   # experiments only
+        import dataclasses
+        cfg = dataclasses.replace(cfg, oom_budget_bytes=int(args.oom_budget_gb * (1 << 30)))
     kind = workload_of(cfg)
 
     g, gen_s = make_graph(cfg, dev)
@@ -329,9 +343,10 @@ def main():
         # allows -- move the generated graph to host memory first
         g = g.to("cpu")
         torch.cuda.empty_cache()
+        zc_main = args.oom_variant == "zerocopy"
         G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, budget_bytes=cfg.oom_budget_bytes,
-                                 num_partitions=cfg.oom_partitions, max_resident=cfg.oom_resident,
-                                 num_streams=cfg.oom_resident)
+                                 num_partitions=cfg.oom_partitions, max_resident=1 if zc_main else cfg.oom_resident,
+                                 num_streams=cfg.oom_resident, zerocopy=zc_main)
     else:
         # static-bias CTPS cache (§8(f) NEXT-1, bit-identical) for degree-biased selections
         use_cache = (not args.no_cache) and cfg.bias in ("degree", "layer")
@@ -435,7 +450,7 @@ def main():
 
     # ---------------- cfg5: the B200-native zero-copy OOM variant (NEXT-4), reported apart
     zc = None
-    if oom and not args.no_zerocopy:
+    if oom and not args.no_zerocopy and args.oom_variant != "zerocopy":
         try:
             Gz = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, budget_bytes=cfg.oom_budget_bytes,
                                       num_partitions=cfg.oom_partitions, max_resident=1, zerocopy=True)
@@ -496,7 +511,7 @@ def main():
     elif not ginfo.get("ctps_cache") and cfg.bias in ("degree", "layer") and not ginfo.get("oom_mode"):
         variant += "_scan"
     kname = hot_kernel_name(cfg, bool(ginfo.get("node2vec_tri") if cfg.workload == "node2vec" else ginfo.get("ctps_cache")),
-                            bool(ginfo.get("oom_mode")),
+                            bool(ginfo.get("oom_mode")) and args.oom_variant != "zerocopy",
                             int(ginfo.get("walk_index_leaf") or 0), int(ginfo.get("walk_index_group") or 0))
     traffic = load_traffic(variant, kname)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -524,7 +539,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": total_ms / max(args.steps, 1), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u32",
                 "data": "synthetic (seeded R-MAT + seeds from synth/; no datasets)",
-                "config": config_block(cfg, world, gstats), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "config": config_block(cfg, world, gstats, oom_mode=(args.oom_variant if oom else None),
+                                       colc=ginfo.get("device_bytes")), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk,
                 "detail": {"edges_per_step_per_gpu": edges / max(args.steps, 1), "step_ms": step_ms,
                            "graph_gen_s": gen_s, "gather_ms": gather_ms,

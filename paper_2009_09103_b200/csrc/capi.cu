@@ -594,6 +594,26 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         if (st.zerocopy) {   // no partition staging: release the validation slot
             cudaFree(st.d_slots);
             st.d_slots = nullptr;
+            // Resident prefix of col_idx filling the budget left after row_ptr + deg and a
+            // run-state reserve (walk pools, outputs, scratch: min(512 MiB, budget / 8)).  A walk step that reads entry e
+            // takes it from the device when e < colc_n, else from pinned host memory.  For
+            // MDRW every entry is equally likely to be read (a row is picked with probability
+            // proportional to its degree, then one of its entries uniformly), so the fraction
+            // of host reads is the uncached fraction, whichever entries are cached.
+            const int64_t reserve = std::min<int64_t>(int64_t(512) << 20, st.budget / 8);
+            const char* nc = std::getenv("CSAW_ZC_NOCACHE");   // A/B: pure zero-copy
+            const int64_t room = st.budget - resident_bytes - reserve;
+            st.colc_n = (nc && nc[0] == '1') || room <= 0 ? 0 : std::min<int64_t>(E, room / 4);
+            if (st.colc_n > 0) {
+                if (cudaMalloc(&st.d_colc, sizeof(uint32_t) * st.colc_n) != cudaSuccess) {
+                    cudaGetLastError();
+                    st.d_colc = nullptr;
+                    st.colc_n = 0;
+                } else {
+                    CREATE_CUDA(cudaMemcpy(st.d_colc, st.h_col, sizeof(uint32_t) * st.colc_n, cudaMemcpyHostToDevice),
+                                "copy resident col prefix");
+                }
+            }
         }
         st.streams.resize(st.S);
         for (auto& s : st.streams) CREATE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
@@ -685,6 +705,7 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (st.h_col) cudaFreeHost(st.h_col);
     if (st.h_row) cudaFreeHost(st.h_row);
     if (st.d_slots) cudaFree(st.d_slots);
+    if (st.d_colc) cudaFree(st.d_colc);
     for (auto s : st.streams) cudaStreamDestroy(s);
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
@@ -704,7 +725,8 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
     out->oom_mode = g->oom ? 1 : 0;
     out->device_bytes = sizeof(int64_t) * (g->V + 1) + sizeof(uint32_t) * g->V +
                         (g->col ? sizeof(uint32_t) * g->E : 0) + static_cast<int64_t>(g->scratch.bytes_held()) +
-                        (g->oom ? static_cast<int64_t>(g->oomst.R) * g->oomst.slot_edges * 4 : 0) +
+                        (g->oom ? (g->oomst.zerocopy ? 0 : static_cast<int64_t>(g->oomst.R) * g->oomst.slot_edges * 4) +
+                                      g->oomst.colc_n * 4 : 0) +
                         (g->cps ? static_cast<int64_t>(sizeof(uint64_t) * g->E + sizeof(uint32_t) * g->V) : 0) +
                         (g->wix_leaf ? static_cast<int64_t>(sizeof(uint32_t) * (2 * g->wleaf_entries + g->winn_entries) + sizeof(uint4) * g->V) : 0) +
                         (g->tri ? static_cast<int64_t>(sizeof(uint32_t) * g->E) : 0);

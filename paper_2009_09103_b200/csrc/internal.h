@@ -79,6 +79,10 @@ struct OomState {
     uint32_t* h_col = nullptr;     // pinned host col_idx (full graph)
     int64_t* h_row = nullptr;      // pinned host row_ptr
     uint32_t* d_slots = nullptr;   // R arena slots of col entries
+    // zero-copy mode: col_idx[0, colc_n) resident on the device (the budget left after
+    // row_ptr + deg + a run-state reserve), the rest read in place from h_col
+    uint32_t* d_colc = nullptr;
+    int64_t colc_n = 0;
     std::vector<int32_t> resident; // partition id per slot (-1 = empty)
     std::vector<cudaStream_t> streams;
     // ablation switches (Fig. 13-15): workload-aware scheduling, thread-block balancing

@@ -1153,6 +1153,8 @@ struct MdrwArgs {
     uint64_t* __restrict__ gblk;          // scratch [n_warps][nblk] when shared memory is too small
     int smem_ok;
     int warps_per_block;
+    const uint32_t* __restrict__ colc;    // col entries [0, colc_n) on the device (k_mdrw_fast; = col in memory)
+    uint64_t colc_n;
 };
 
 __global__ void k_mdrw(MdrwArgs a) {
@@ -1314,7 +1316,8 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, ui
                 const uint32_t d = __shfl_sync(FULL, e.y, fl);
                 v = __shfl_sync(FULL, e.x, fl);
                 const uint64_t rb = static_cast<uint64_t>(__shfl_sync(FULL, e.w, fl)) << 32 | __shfl_sync(FULL, e.z, fl);
-                u = __ldg(a.col + rb + below(Ue, d));
+                const uint64_t ei = rb + below(Ue, d);
+                u = ei < a.colc_n ? __ldg(a.colc + ei) : __ldg(a.col + ei);   // OOM zero-copy: host beyond colc_n
                 const int64_t ru = __ldg(a.rp + u);
                 const uint32_t du = static_cast<uint32_t>(__ldg(a.rp + u + 1) - ru);
                 if (lane == fl)
@@ -1413,7 +1416,9 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
             void* pool;
             CSAW_TRY(g->scratch.get(SL_TMP0, sizeof(uint4) * n * m, &pool));
             MdrwArgs ma{g->row_ptr, colp, d_seeds, static_cast<uint64_t>(n), b.pool_size, length,
-                        static_cast<uint32_t>(base), key, d_path, nullptr, nullptr, nullptr, nullptr, 0, WALK_WARPS};
+                        static_cast<uint32_t>(base), key, d_path, nullptr, nullptr, nullptr, nullptr, 0, WALK_WARPS,
+                        g->col ? g->col : g->oomst.d_colc,
+                        static_cast<uint64_t>(g->col ? g->E : g->oomst.colc_n)};
             const int64_t warps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 7 * MDRW_WARPS);
             k_mdrw_fast<<<static_cast<int>((warps + MDRW_WARPS - 1) / MDRW_WARPS), MDRW_WARPS * 32, 0, st>>>(
                 ma, static_cast<uint4*>(pool));
@@ -1444,7 +1449,7 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         MdrwArgs ma{g->row_ptr, colp, d_seeds, static_cast<uint64_t>(n), b.pool_size, length,
                     static_cast<uint32_t>(base), key, d_path, static_cast<uint32_t*>(pv),
                     static_cast<uint64_t*>(prb), static_cast<uint32_t*>(gb), static_cast<uint64_t*>(gk),
-                    smem_ok ? 1 : 0, wpb};
+                    smem_ok ? 1 : 0, wpb, nullptr, 0};
         k_mdrw<<<grid, wpb * 32, smem, st>>>(ma);
     } else {
         return fail(CSAW_ERR_INVALID_ARG, "bias kind is not a walk selector");

@@ -142,3 +142,34 @@ def test_oom_schedule_switches_keep_results(medium, ws, bal):
         assert torch.equal(x.cpu(), y.cpu())
     Gm.close()
     Go.close()
+
+
+@pytest.mark.parametrize("frac", [0.0, 0.3, 0.7, 1.2])   # 0.0: the smallest budget that validates
+def test_oom_zerocopy_resident_prefix(medium, frac):
+    """Zero-copy mode keeps col_idx[0, colc) on the device, colc = (budget - row_ptr - deg -
+    min(512 MiB, budget/8)) / 4: MDRW steps read entries below colc from HBM and the rest
+    from pinned host memory.  Budgets giving 0 %, ~30 %, ~70 % and 100 % resident must all
+    equal the in-memory result (and the oracle)."""
+    import os
+    g = medium
+    n, m, L = 48, 150, 250
+    V, E = g.row_ptr.numel() - 1, g.col_idx.numel()
+    resident = 8 * (V + 1) + 4 * V
+    budget = max(int((resident + frac * 4 * E) * 8 / 7) + 64, budget_for(g, 4, 1, n, m))   # >= validation slot
+    seeds = mdrw_seeds(g, n, m).to(DEV)
+    Gm = cs.csaw_graph_create(g.row_ptr.to(DEV), g.col_idx.to(DEV))
+    Gz = cs.csaw_graph_create(g.row_ptr, g.col_idx, budget_bytes=budget, num_partitions=4, max_resident=1,
+                              zerocopy=True)
+    held = Gz.info()["device_bytes"]
+    assert held <= budget
+    if 0 < frac < 1:   # a partial resident prefix: both the HBM and the host branch are taken
+        assert resident + 4 * E * frac * 0.5 < held < resident + 4 * E
+    ref = cs.csaw_walk(Gm, cs.make_bias("mdrw"), seeds, L, rng_seed=9)
+    assert torch.equal(ref, cs.csaw_walk(Gz, cs.make_bias("mdrw"), seeds, L, rng_seed=9))
+    og = O.Graph(g.row_ptr.numpy(), g.col_idx.numpy().view(np.uint32))
+    e = u32(ref)
+    sv = u32(seeds.cpu())
+    for i in (0, n // 2, n - 1):
+        assert np.array_equal(e[i], O.mdrw(og, sv[i], L, i, 9))
+    Gm.close()
+    Gz.close()
