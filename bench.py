@@ -512,7 +512,8 @@ def main():
         variant += "_scan"
     kname = hot_kernel_name(cfg, bool(ginfo.get("node2vec_tri") if cfg.workload == "node2vec" else ginfo.get("ctps_cache")),
                             bool(ginfo.get("oom_mode")) and args.oom_variant != "zerocopy",
-                            int(ginfo.get("walk_index_leaf") or 0), int(ginfo.get("walk_index_group") or 0))
+                            int(ginfo.get("walk_index_leaf") or 0), int(ginfo.get("walk_index_group") or 0),
+                            bool(ginfo.get("walk_index_heads")))
     traffic = load_traffic(variant, kname)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
@@ -616,8 +617,10 @@ def run_e2e(cs, G, bias, seeds, cfg, base, args, kind, n, dev, world):
             "steps": steps, "timing": "host wall clock around the synchronous C-ABI call (max over ranks)"}
 
 
-def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0):
+def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads=False):
     if cfg.workload == "walk":
+        if cfg.bias == "degree" and wix_leaf and heads and wix_group == 32 and wix_leaf == 64:
+            return "k_walk_head<64>"
         if cfg.bias == "degree" and wix_leaf:
             return f"k_walk_wix<{wix_leaf}>" if wix_group == 32 else f"k_walk_wixg<{wix_group}, {wix_leaf}>"
         return "k_walk_cached" if (cfg.bias == "degree" and cached) else f"k_walk<{cfg.bias}>"

@@ -161,6 +161,8 @@ typedef struct {
     double cache_build_ms;          /* device time of the cache build */
     int32_t walk_index_group;       /* lanes per walker of the degree-walk kernel (8 / 16; 32 = one warp per walker) */
     int32_t node2vec_tri;           /* 1 if per-edge triangle counts were built (CSAW_GRAPH_N2V_TRI on a symmetric graph) */
+    int32_t walk_index_heads;       /* 1 if the walk index has 512 B vertex heads (degree walks: k_walk_head) */
+    int32_t reserved;
 } csaw_graph_info_t;
 
 typedef struct csaw_graph csaw_graph;  /* opaque */

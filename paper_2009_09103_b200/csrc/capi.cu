@@ -312,6 +312,37 @@ __global__ void k_wix_build(const int64_t* __restrict__ rp, const uint32_t* __re
     }
 }
 
+// Vertex heads (wix.cuh): warp per vertex, from the record, the top level and the leaves.
+template <int FL>
+__global__ void k_head_build(const uint4* __restrict__ rec, const uint32_t* __restrict__ c32p,
+                             const uint32_t* __restrict__ colp, const uint32_t* __restrict__ inn, int64_t V,
+                             uint32_t* __restrict__ head) {
+    using W = WixShape<FL>;
+    const int lane = lane_id();
+    for (uint64_t v = global_warp_id(); v < static_cast<uint64_t>(V); v += total_warps()) {
+        const uint4 r = rec[v];   // {p, d, io, T}
+        uint32_t* h = head + v * WIX_HEAD_WORDS;
+        const uint32_t d = r.y;
+        const int K = W::levels(d);
+        for (uint32_t w = lane; w < WIX_HEAD_WORDS; w += 32) {
+            uint32_t val = 0;
+            if (w == 0) val = d;
+            else if (w == 1) val = r.w;
+            else if (w == 2) val = r.x;
+            else if (w == 3) val = r.z;
+            else if (K == 0 && d <= WIX_HEAD_LEAF) {
+                const uint32_t i = w - 4;
+                if (i < WIX_HEAD_LEAF) val = i < d ? c32p[r.x + i] : 0u;
+                else if (i - WIX_HEAD_LEAF < d) val = colp[r.x + (i - WIX_HEAD_LEAF)];
+            } else if (K > 0) {
+                const uint32_t nK = W::count(d, K);
+                if (nK <= WIX_HEAD_TOP && w - 4 < nK) val = inn[r.z + (w - 4)];
+            }
+            h[w] = val;
+        }
+    }
+}
+
 template <int FL>
 static csaw_status build_wix_t(csaw_graph* g, int blocks) {
     using W = WixShape<FL>;
@@ -340,6 +371,12 @@ static csaw_status build_wix_t(csaw_graph* g, int blocks) {
             // records right after the nodes (total + 16 is a multiple of 4: 16 B aligned)
             g->wrec = reinterpret_cast<uint4*>(g->winn + total + 16);
             k_wix_build<FL><<<blocks, 256>>>(g->row_ptr, g->col, g->cps, woff, V, g->wrec, g->c32, g->wcol, g->winn);
+            const char* nh = std::getenv("CSAW_NO_HEADS");   // A/B: walk the records instead
+            if (!(nh && nh[0] == '1') &&
+                cudaMalloc(&g->whead, sizeof(uint32_t) * WIX_HEAD_WORDS * std::max<int64_t>(V, 1)) == cudaSuccess)
+                k_head_build<FL><<<blocks, 256>>>(g->wrec, g->c32, g->wcol, g->winn, V, g->whead);
+            else
+                cudaGetLastError();   // heads are an accelerator: walks fall back to the records
             g->winn_entries = total + 16;
             g->wleaf_entries = nl;
         }
@@ -698,6 +735,7 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->bt_off) cudaFree(g->bt_off);
     if (g->nmp) cudaFree(g->nmp);
     if (g->c32) cudaFree(g->c32);
+    if (g->whead) cudaFree(g->whead);
     if (g->tri) cudaFree(g->tri);
     if (g->wcol) cudaFree(g->wcol);
     if (g->winn) cudaFree(g->winn);
@@ -729,11 +767,14 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
                                       g->oomst.colc_n * 4 : 0) +
                         (g->cps ? static_cast<int64_t>(sizeof(uint64_t) * g->E + sizeof(uint32_t) * g->V) : 0) +
                         (g->wix_leaf ? static_cast<int64_t>(sizeof(uint32_t) * (2 * g->wleaf_entries + g->winn_entries) + sizeof(uint4) * g->V) : 0) +
+                        (g->whead ? static_cast<int64_t>(sizeof(uint32_t)) * WIX_HEAD_WORDS * g->V : 0) +
                         (g->tri ? static_cast<int64_t>(sizeof(uint32_t) * g->E) : 0);
     out->ctps_cache = g->cps ? 1 : 0;
     out->walk_index_leaf = g->wix_leaf;
     out->walk_index_group = g->wix_leaf ? g->wix_group : 0;
     out->node2vec_tri = g->tri ? 1 : 0;
+    out->walk_index_heads = g->whead ? 1 : 0;
+    out->reserved = 0;
     out->cache_build_ms = g->cache_build_ms;
     return CSAW_OK;
 }

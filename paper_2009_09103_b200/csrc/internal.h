@@ -128,7 +128,8 @@ struct csaw_graph {
     // narrow walk index (wix.cuh): built with the cache when every row total T < 2^32
     uint32_t* c32 = nullptr;      // padded leaves: S_{i+1} as u32 (wix.cuh leaf_pos)
     uint32_t* wcol = nullptr;     // padded leaves: col copy
-    uint4* wrec = nullptr;        // [V] {row start lo, hi, degree, index offset}
+    uint4* wrec = nullptr;        // [V] {leaf position, degree, index offset, T}
+    uint32_t* whead = nullptr;    // [V][128] vertex heads (wix.cuh): record + top level / inline leaf
     uint32_t* winn = nullptr;     // internal levels (fanout 128), top level first per row
     uint64_t winn_entries = 0;    // size of winn (the records wrec follow it in the same allocation)
     uint64_t wleaf_entries = 0;   // size of c32 / wcol

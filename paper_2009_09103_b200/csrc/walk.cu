@@ -198,6 +198,99 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_wix(WalkArgs a, con
     }
 }
 
+// uint4 component c (0..3) of q, c warp-uniform or per lane
+__device__ __forceinline__ uint32_t u4_at(const uint4& q, uint32_t c) {
+    return c == 0 ? q.x : c == 1 ? q.y : c == 2 ? q.z : q.w;
+}
+
+// Degree-biased walk over the vertex heads (wix.cuh): a step is one coalesced 512 B head
+// read (record + top level, or the whole row when d <= 60), then K - 1 internal nodes and
+// one leaf when the row is larger -- one dependent round trip less than record + nodes.
+// Same S, same draws, same region as k_walk_wix / k_walk<degree> / the oracle.
+template <int FL>
+__global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_head(WalkArgs a, const uint32_t* __restrict__ head,
+                                                                const uint32_t* __restrict__ c32p,
+                                                                const uint32_t* __restrict__ colp,
+                                                                const uint32_t* __restrict__ inn) {
+    using W = WixShape<FL>;
+    constexpr int NL = FL / 32;
+    const uint32_t lane = static_cast<uint32_t>(lane_id());
+    unsigned long long bytes = 0, steps = 0;
+    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+        uint32_t cur = a.seeds[w];
+        const uint32_t inst = a.base + static_cast<uint32_t>(w);
+        PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
+        pw.put(0, cur);
+        uint64_t ubuf = 0;
+        for (int32_t t = 0; t < a.L; ++t) {
+            if ((t & 31) == 0)
+                ubuf = draw_u64(a.key, inst, static_cast<uint32_t>(t + lane), 0u, word3(PURPOSE_EDGE, 0, 0));
+            const uint64_t U = __shfl_sync(FULL, ubuf, t & 31);
+            uint32_t nxt = NONE;
+            if (cur != NONE) {
+                const uint4 q = __ldg(reinterpret_cast<const uint4*>(head + static_cast<uint64_t>(cur) * WIX_HEAD_WORDS) + lane);
+                const uint32_t d = __shfl_sync(FULL, q.x, 0), T = __shfl_sync(FULL, q.y, 0);
+                const uint32_t p = __shfl_sync(FULL, q.z, 0), io = __shfl_sync(FULL, q.w, 0);
+                bytes += 512;
+                if (d > 0 && T > 0) {   // T = 0: no positive-bias neighbour, the walk ends (R20)
+                    const uint32_t x = static_cast<uint32_t>(below(U, T));
+                    const int K = W::levels(d);
+                    // rank of x among the head's entries [0, n): lane l >= 1 holds entries 4 (l - 1) .. + 3
+                    auto head_rank = [&](uint32_t n) {
+                        uint32_t c = 0;
+                        if (lane >= 1) {
+                            const uint32_t e0 = 4 * (lane - 1);
+                            c = (e0 < n && q.x <= x) + (e0 + 1 < n && q.y <= x) + (e0 + 2 < n && q.z <= x) +
+                                (e0 + 3 < n && q.w <= x);
+                        }
+                        return __reduce_add_sync(FULL, c);
+                    };
+                    if (K == 0 && d <= WIX_HEAD_LEAF) {   // the whole row is in the head
+                        const uint32_t r = head_rank(d);
+                        const uint32_t e = WIX_HEAD_LEAF + r;   // col entry r: word 4 + 60 + r
+                        nxt = __shfl_sync(FULL, u4_at(q, e & 3), 1 + (e >> 2));
+                    } else {
+                        uint32_t j = 0;
+                        uint64_t off = io;
+                        int k = K;
+                        if (K > 0) {
+                            const uint32_t nK = W::count(d, K);
+                            if (nK <= WIX_HEAD_TOP) {   // top level inline
+                                j = head_rank(nK);
+                                off += W::round4(nK);
+                                --k;
+                            }
+                        }
+                        for (; k >= 1; --k) {
+                            const uint32_t nk = W::count(d, k);
+                            const uint32_t cnt = min(static_cast<uint32_t>(WIX_NODE), nk - j * WIX_NODE);
+                            uint32_t v[WIX_NODE / 32];
+                            wix_load(inn + off + j * WIX_NODE, cnt, v);
+                            bytes += 4ull * cnt;
+                            j = j * WIX_NODE + wix_rank(v, x);
+                            off += W::round4(nk);
+                        }
+                        const uint64_t lb = static_cast<uint64_t>(p) + static_cast<uint64_t>(j) * FL;
+                        const uint32_t cnt = min(static_cast<uint32_t>(FL), d - j * FL);
+                        uint32_t v[NL], cv[NL];
+                        wix_load(c32p + lb, cnt, v);
+                        wix_load(colp + lb, cnt, cv);
+                        bytes += 8ull * cnt;
+                        nxt = wix_entry(cv, wix_rank(v, x));
+                    }
+                    ++steps;
+                }
+            }
+            cur = nxt;
+            pw.put(t + 1, cur);
+        }
+    }
+    if (lane == 0) {
+        if (bytes) atomicAdd(a.counters + 3, bytes);
+        if (steps) atomicAdd(a.counters + 1, steps);
+    }
+}
+
 // One node / leaf block read by a group of G lanes: lane gl holds entries 4 gl + 4 G i .. +3
 // (i < N), 16 B aligned uint4 loads; entries past cnt read as 0xFFFFFFFF (above every draw).
 template <int G, int N>
@@ -1371,7 +1464,14 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
                                                 static_cast<int64_t>(g->num_sms) * 64);
         const int grid = static_cast<int>(std::max<int64_t>(1, (warps + wpb - 1) / wpb));
         const uint4* rec = g->wrec;
-        if (g->wix_group == 32) {
+        if (g->wix_group == 32 && g->whead && g->wix_leaf == 64) {
+            // small blocks spread the few walkers evenly over the SMs (cfg2: 4,000 warps on 148 SMs)
+            const char* we = std::getenv("CSAW_WALK_WPB");
+            const int hw = we ? std::max(1, std::min(8, std::atoi(we))) : 2;   // 1: 2.46, 2: 2.43, 4: 2.44, 8: 2.48 ms (cfg2)
+            const int64_t hwarps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 64);
+            k_walk_head<64><<<static_cast<int>((hwarps + hw - 1) / hw), hw * 32, 0, st>>>(a, g->whead, g->c32, g->wcol,
+                                                                                       g->winn);
+        } else if (g->wix_group == 32) {
             if (g->wix_leaf == 32) k_walk_wix<32><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);
             else if (g->wix_leaf == 64) k_walk_wix<64><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);
             else k_walk_wix<128><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);

@@ -34,6 +34,14 @@ namespace csaw {
 
 constexpr int WIX_NODE = 128;   // internal fanout
 constexpr int WIX_NODE_LOG = 7;
+// Vertex heads: one 512 B block per vertex at v * 512 B (address computable from v), words
+// {d, T, leaf position, index offset} then 124 entries: the row's top index level when it
+// has <= 124 entries, or, for rows of d <= 60, the whole leaf inline (S in words 4..63, col
+// in words 64..123).  A step then starts with one coalesced read that carries the record
+// and the first search level together (one dependent round trip less than record + node).
+constexpr int WIX_HEAD_WORDS = 128;
+constexpr uint32_t WIX_HEAD_TOP = 124;    // inline top-level entries
+constexpr uint32_t WIX_HEAD_LEAF = 60;    // inline leaf entries (S and col)
 
 template <int FL>
 struct WixShape {

@@ -18,7 +18,7 @@ import oracle as O
 pytestmark = pytest.mark.gpu
 
 # (leaf fanout, lanes per walker: 32 = one warp per walker, 8 / 16 = sub-warp groups)
-LEAVES = [(32, 32), (64, 32), (128, 32), (32, 8), (64, 8), (128, 8), (64, 16), (128, 16)]
+LEAVES = [(32, 32), (64, 32), (128, 32), (32, 8), (64, 8), (128, 8), (64, 16), (128, 16), (64, "nohead")]
 
 
 def star_csr(V=700_001, d1=20_001):
@@ -41,7 +41,9 @@ def star_csr(V=700_001, d1=20_001):
 
 def make(rp, col, leaf, walk_index=True):
     leaf, group = leaf if isinstance(leaf, tuple) else (leaf, 32)
-    env = {"CSAW_WIX_LEAF": str(leaf), "CSAW_WIX_GROUP": str(group)}
+    nohead = group == "nohead"   # (64, 32) walks the vertex heads (k_walk_head); this one the records
+    group = 32 if nohead else group
+    env = {"CSAW_WIX_LEAF": str(leaf), "CSAW_WIX_GROUP": str(group), "CSAW_NO_HEADS": "1" if nohead else ""}
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
