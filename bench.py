@@ -351,7 +351,9 @@ def main():
         # static-bias CTPS cache (§8(f) NEXT-1, bit-identical) for degree-biased selections
         use_cache = (not args.no_cache) and cfg.bias in ("degree", "layer")
         use_tri = (not args.no_cache) and cfg.workload == "node2vec"   # node2vec edge triangle counts
-        G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache, node2vec_tri=use_tri)
+        use_meta = (not args.no_cache) and cfg.workload == "mdrw"   # next-vertex metadata per entry
+        G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache, node2vec_tri=use_tri,
+                                 next_meta=use_meta)
     ginfo = G.info()
     bias = bias_of(cs, cfg)
     stream = torch.cuda.current_stream(dev)

@@ -148,6 +148,11 @@ typedef struct {
  * nearer the draw up to its region, instead of merging all of N(v) with N(prev).  The
  * picks are identical (same integer S, same draw).  Reported in csaw_graph_info_t. */
 #define CSAW_GRAPH_N2V_TRI 0x40u
+/* csaw_graph_opts.flags (in-memory graphs, max degree < 2^24): build next-vertex
+ * metadata nmp[e] = row_ptr[u] << 24 | deg(u) for u = col[e] (8 B per CSR entry), so an
+ * MDRW step reads the new pool vertex's row and VertexBias together with the
+ * picked entry instead of one dependent row_ptr lookup later.  Results are identical. */
+#define CSAW_GRAPH_NEXT_META 0x80u
 
 typedef struct {
     int64_t num_vertices, num_edges;

@@ -679,10 +679,11 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         cudaFree(part);
         CREATE_CUDA(cudaMalloc(&g->bt, sizeof(uint64_t) * std::max<uint64_t>(btn, 1)), "cudaMalloc(bt)");
         if (V > 0) k_build_bt<<<blocks, 256>>>(g->row_ptr, g->cps, g->bt_off, V, g->bt);
-        // next-vertex metadata for walks: off by default (measured 2.5 % slower on cfg2:
-        // the extra 256 B per step outweighs the saved row_ptr round); CSAW_WALK_META=1 enables
+        // next-vertex metadata for the u64-index walk (k_walk_cached): off by default (measured
+        // 2.5 % slower on cfg2: the extra 256 B per step outweighs the saved row_ptr round);
+        // CSAW_WALK_META=1 enables
         const char* meta = std::getenv("CSAW_WALK_META");
-        if (g->max_deg < (1 << 24) && E < (int64_t(1) << 40) && E > 0 && meta && meta[0] == '1') {
+        if (!g->nmp && g->max_deg < (1 << 24) && E < (int64_t(1) << 40) && E > 0 && meta && meta[0] == '1') {
             CREATE_CUDA(cudaMalloc(&g->nmp, sizeof(uint64_t) * E), "cudaMalloc(nmp)");
             k_build_nmp<<<blocks, 256>>>(g->row_ptr, g->col, E, g->nmp);
         }
@@ -698,6 +699,11 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         g->cache_build_ms = ms;
         cudaEventDestroy(c0);
         cudaEventDestroy(c1);
+    }
+    if ((o.flags & CSAW_GRAPH_NEXT_META) && !g->oom && !g->nmp && g->max_deg < (1 << 24) && E < (int64_t(1) << 40) &&
+        E > 0) {   // nmp[e] = row_ptr[col[e]] << 24 | deg(col[e]) (MDRW: k_mdrw_fast)
+        CREATE_CUDA(cudaMalloc(&g->nmp, sizeof(uint64_t) * E), "cudaMalloc(nmp)");
+        k_build_nmp<<<blocks, 256>>>(g->row_ptr, g->col, E, g->nmp);
     }
     if ((o.flags & CSAW_GRAPH_N2V_TRI) && !g->oom) {   // node2vec edge triangle counts (walk.cu k_node2vec_tri)
         cudaEvent_t c0, c1;
@@ -768,7 +774,8 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
                         (g->cps ? static_cast<int64_t>(sizeof(uint64_t) * g->E + sizeof(uint32_t) * g->V) : 0) +
                         (g->wix_leaf ? static_cast<int64_t>(sizeof(uint32_t) * (2 * g->wleaf_entries + g->winn_entries) + sizeof(uint4) * g->V) : 0) +
                         (g->whead ? static_cast<int64_t>(sizeof(uint32_t)) * WIX_HEAD_WORDS * g->V : 0) +
-                        (g->tri ? static_cast<int64_t>(sizeof(uint32_t) * g->E) : 0);
+                        (g->tri ? static_cast<int64_t>(sizeof(uint32_t) * g->E) : 0) +
+                        (g->nmp ? static_cast<int64_t>(sizeof(uint64_t) * g->E) : 0);
     out->ctps_cache = g->cps ? 1 : 0;
     out->walk_index_leaf = g->wix_leaf;
     out->walk_index_group = g->wix_leaf ? g->wix_group : 0;

@@ -1248,6 +1248,7 @@ struct MdrwArgs {
     int warps_per_block;
     const uint32_t* __restrict__ colc;    // col entries [0, colc_n) on the device (k_mdrw_fast; = col in memory)
     uint64_t colc_n;
+    const uint64_t* __restrict__ nmp;     // optional next-vertex metadata per entry (row << 24 | deg)
 };
 
 __global__ void k_mdrw(MdrwArgs a) {
@@ -1410,9 +1411,18 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, ui
                 v = __shfl_sync(FULL, e.x, fl);
                 const uint64_t rb = static_cast<uint64_t>(__shfl_sync(FULL, e.w, fl)) << 32 | __shfl_sync(FULL, e.z, fl);
                 const uint64_t ei = rb + below(Ue, d);
-                u = ei < a.colc_n ? __ldg(a.colc + ei) : __ldg(a.col + ei);   // OOM zero-copy: host beyond colc_n
-                const int64_t ru = __ldg(a.rp + u);
-                const uint32_t du = static_cast<uint32_t>(__ldg(a.rp + u + 1) - ru);
+                int64_t ru;
+                uint32_t du;
+                if (a.nmp) {   // the new vertex's row and degree come with the entry (no dependent lookup)
+                    const uint64_t mt = __ldg(a.nmp + ei);
+                    u = __ldg(a.col + ei);
+                    ru = static_cast<int64_t>(mt >> 24);
+                    du = static_cast<uint32_t>(mt & 0xFFFFFFu);
+                } else {
+                    u = ei < a.colc_n ? __ldg(a.colc + ei) : __ldg(a.col + ei);   // OOM zero-copy: host beyond colc_n
+                    ru = __ldg(a.rp + u);
+                    du = static_cast<uint32_t>(__ldg(a.rp + u + 1) - ru);
+                }
                 if (lane == fl)
                     ps[s0] = make_uint4(u, du, static_cast<uint32_t>(ru), static_cast<uint32_t>(static_cast<uint64_t>(ru) >> 32));
                 if (lane == static_cast<int>(bsel >> 1)) {
@@ -1518,7 +1528,7 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
             MdrwArgs ma{g->row_ptr, colp, d_seeds, static_cast<uint64_t>(n), b.pool_size, length,
                         static_cast<uint32_t>(base), key, d_path, nullptr, nullptr, nullptr, nullptr, 0, WALK_WARPS,
                         g->col ? g->col : g->oomst.d_colc,
-                        static_cast<uint64_t>(g->col ? g->E : g->oomst.colc_n)};
+                        static_cast<uint64_t>(g->col ? g->E : g->oomst.colc_n), g->col ? g->nmp : nullptr};
             const int64_t warps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 7 * MDRW_WARPS);
             k_mdrw_fast<<<static_cast<int>((warps + MDRW_WARPS - 1) / MDRW_WARPS), MDRW_WARPS * 32, 0, st>>>(
                 ma, static_cast<uint4*>(pool));
@@ -1549,7 +1559,7 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         MdrwArgs ma{g->row_ptr, colp, d_seeds, static_cast<uint64_t>(n), b.pool_size, length,
                     static_cast<uint32_t>(base), key, d_path, static_cast<uint32_t*>(pv),
                     static_cast<uint64_t*>(prb), static_cast<uint32_t*>(gb), static_cast<uint64_t*>(gk),
-                    smem_ok ? 1 : 0, wpb, nullptr, 0};
+                    smem_ok ? 1 : 0, wpb, nullptr, 0, nullptr};
         k_mdrw<<<grid, wpb * 32, smem, st>>>(ma);
     } else {
         return fail(CSAW_ERR_INVALID_ARG, "bias kind is not a walk selector");

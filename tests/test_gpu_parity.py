@@ -290,3 +290,18 @@ def test_mdrw_pool_sizes(medium, m, n, L):
     finally:
         del os.environ["CSAW_MDRW_SLOW"]
     assert np.array_equal(e, e2)
+
+
+def test_mdrw_next_meta(medium):
+    """CSAW_GRAPH_NEXT_META: the new pool vertex's row and degree come with the picked CSR
+    entry (nmp) -- same edges as without it and as the oracle."""
+    _, og2, g2 = medium
+    Gm = cs.csaw_graph_create(g2.row_ptr.to(DEV), g2.col_idx.to(DEV), next_meta=True)
+    assert Gm.info()["device_bytes"] >= 8 * g2.col_idx.numel()
+    for m, n, L in [(2000, 6, 300), (37, 50, 200)]:
+        s = mdrw_seeds(g2, n, m, set_id=3).numpy()
+        e = check_mdrw(Gm, og2, s, L, rng_seed=17, instances=range(0, n, max(1, n // 10)))
+        G0, _, _ = medium
+        e0 = u32(cs.csaw_walk(G0, cs.make_bias("mdrw"), torch.as_tensor(s.view(np.int32)).to(DEV), L, rng_seed=17))
+        assert np.array_equal(e, e0)
+    Gm.close()
