@@ -387,8 +387,21 @@ def main():
             return int(r[1].numel())
 
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    # the clock sampler starts before the warm-up, and warm-up steps are the timed steps'
+    # exact sequence (flush + step), so the first timed step is not a cold-host outlier
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
     for _ in range(max(args.warmup, 0)):
+        flush.fill_(1)
+        w0 = torch.cuda.Event(enable_timing=True)
+        w1 = torch.cuda.Event(enable_timing=True)
+        w0.record(stream)
+        torch.cuda.nvtx.range_push("csaw_warmup")   # NVTX initialises on first use: not inside a timed step
         step()
+        torch.cuda.nvtx.range_pop()
+        w1.record(stream)
+        cs.csaw_stats(G)
     torch.cuda.synchronize(dev)
 
     # ---------------- timed region (device-resident inputs)
@@ -396,9 +409,7 @@ def main():
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize(dev)
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.15)
+    clocks.lines.clear()   # keep only samples taken during the timed region
     evs = []
     edges = 0
     launches = 0

@@ -717,7 +717,59 @@ struct FusedArgs {
     unsigned long long* counters;
     int64_t V;
     uint32_t mode;
+    // epilogue (last block to finish): offsets scan + the host report
+    uint64_t* offs;                       // [n + 1] exclusive prefix of cnt (caller's offsets)
+    unsigned* done;                       // block ticket (zeroed with the counters each call)
+    uint64_t* report;                     // pinned host mailbox: flags, total, counters[0..3]
 };
+
+// Run by the last block of k_sample_fused to finish (ticket): the per-instance edge
+// offsets (exclusive prefix of cnt, one block) and the call's report written straight
+// into pinned host memory -- two launches less per call than a separate scan + report.
+template <int NT>
+__device__ void fused_epilogue(const FusedArgs& a) {
+    __shared__ unsigned last;
+    __shared__ uint64_t wsum[NT / 32];
+    __shared__ uint64_t total;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(a.done, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const uint64_t n = a.n;
+    const uint64_t per = (n + NT - 1) / NT;
+    const uint64_t b0 = min(n, threadIdx.x * per), b1 = min(n, b0 + per);
+    // 8 independent loads in flight per thread (the counts sit in L2)
+    uint64_t s = 0;
+    for (uint64_t i0 = b0; i0 < b1; i0 += 8) {
+        uint64_t c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] = i0 + u < b1 ? __ldcg(a.cnt + i0 + u) : 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += c[u];
+    }
+    uint64_t run = block_excl_scan<NT>(s, wsum, &total);
+    for (uint64_t i0 = b0; i0 < b1; i0 += 8) {
+        uint64_t c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] = i0 + u < b1 ? __ldcg(a.cnt + i0 + u) : 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (i0 + u < b1) a.offs[i0 + u] = run;
+            run += c[u];
+        }
+    }
+    if (threadIdx.x == 0) {
+        a.offs[n] = total;
+        a.report[0] = *reinterpret_cast<volatile unsigned*>(a.overflow);
+        a.report[1] = total;
+        for (int k = 0; k < 4; ++k) a.report[2 + k] = reinterpret_cast<volatile unsigned long long*>(a.counters)[k];
+        __threadfence_system();
+    }
+}
 
 struct FusedEmit {
     uint32_t* s_src;
@@ -910,6 +962,7 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, kMode >= 3 ? 6 : FUSED_MINB)
         if (probes) atomicAdd(a.counters + 2, probes);
         if (draws) atomicAdd(a.counters + 3, draws);
     }
+    fused_epilogue<FUSED_WARPS * 32>(a);
 }
 
 // Compacts the staging rows into the caller's arrays.  Guarded on the device so the
@@ -1026,15 +1079,6 @@ static csaw_status oom_select_level(const csaw_graph* g, const csaw_bias& b, con
 // FUSED_FALLBACK when the batched level-synchronous driver must run instead.
 constexpr csaw_status FUSED_FALLBACK = static_cast<csaw_status>(-1);
 
-__global__ void k_fused_report(const unsigned* __restrict__ ovf, const uint64_t* __restrict__ total,
-                               const unsigned long long* __restrict__ counters, uint64_t* hbox) {
-    const int t = threadIdx.x;
-    if (t == 0) hbox[0] = *ovf;
-    if (t == 1) hbox[1] = *total;
-    if (t >= 2 && t < 6) hbox[t] = counters[t - 2];
-    __threadfence_system();
-}
-
 static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
                                     const uint32_t* d_seeds, uint64_t n, uint64_t base, uint64_t seed,
                                     uint64_t* d_offsets, uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity,
@@ -1082,6 +1126,9 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     a.cnt = static_cast<uint64_t*>(pk);
     a.overflow = ovf;
     a.counters = counters;
+    a.offs = d_offsets;
+    a.done = reinterpret_cast<unsigned*>(counters + 13);   // zeroed by the memset above
+    a.report = const_cast<uint64_t*>(hbox);
     a.V = g->V;
     a.mode = static_cast<uint32_t>(b.migration);
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((n + FUSED_WARPS - 1) / FUSED_WARPS,
@@ -1101,7 +1148,6 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     note_launch();
     CSAW_CUDA(cudaGetLastError());
     CSAW_TRY(hot_end(g, st));
-    CSAW_TRY(device_scan(U64Val{a.cnt}, n, ScanToArray{d_offsets}, static_cast<uint64_t*>(pp), st));
     if (out_on_device && capacity > 0) {   // no host round trip before the copy
         k_fused_copy<<<grid, FUSED_WARPS * 32, 0, st>>>(a.s_src, a.s_dst, a.s_dep, ecap, d_offsets, n, src, dst, dep, ovf,
                                                          static_cast<uint64_t>(capacity));
@@ -1109,11 +1155,7 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
         CSAW_CUDA(cudaGetLastError());
     }
     CSAW_TRY(stats_end(g, st));
-    // flags, edge total and counters straight into the pinned mailbox (one launch, no copies)
-    k_fused_report<<<1, 32, 0, st>>>(ovf, d_offsets + n, counters, const_cast<uint64_t*>(hbox));
-    note_launch();
-    CSAW_CUDA(cudaGetLastError());
-    CSAW_CUDA(cudaStreamSynchronize(st));
+    CSAW_CUDA(cudaStreamSynchronize(st));   // the fused kernel's last block wrote the report
     const unsigned flags = static_cast<unsigned>(hbox[0] & 0xFFFFFFFFu);
     if (flags & 2u) return fail(CSAW_ERR_OUT_OF_RANGE, "a seed vertex is >= num_vertices");
     if (flags & 1u) return FUSED_FALLBACK;

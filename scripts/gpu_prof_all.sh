@@ -14,7 +14,7 @@ run() {  # cfg kernel-regex extra-bench-args
   ncu -i gpurun_out/prof/${cfg}.ncu-rep --page details --csv > gpurun_out/prof/${cfg}_details.csv 2>/dev/null
   ls -la gpurun_out/prof/${cfg}*
 }
-run cfg2 k_walk_wix
+run cfg2 k_walk_head
 run cfg2@scan "^k_walk$" --no-cache
 run cfg1 k_sample_fused
 run cfg4_layer k_sample_fused
