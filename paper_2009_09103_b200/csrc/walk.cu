@@ -1358,6 +1358,18 @@ __global__ void k_mdrw(MdrwArgs a) {
 // loads) so no lane-0 section and no result shuffles remain.  Same x, same slot, same
 // neighbour as k_mdrw and the oracle (bit-identical).
 constexpr int MDRW_WARPS = 4;
+__device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, v, o);
+        if (lane >= o) v += y;
+    }
+    return v;
+}
+
+// kNarrow: a block of 32 slot biases sums below 2^32 (max degree < 2^27): u32 block scan.
+template <bool kNarrow>
 __global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, uint4* __restrict__ pool) {
     const int lane = lane_id();
     const uint32_t m = static_cast<uint32_t>(a.m);
@@ -1378,7 +1390,10 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, ui
             const uint64_t tot = warp_sum(static_cast<uint64_t>(dv));
             if (lane == static_cast<int>(b >> 1)) { if (b & 1) bB = tot; else bA = tot; }
         }
-        uint64_t T = warp_sum(bA + bB);
+        // inclusive prefix of the block-pair totals over the lanes, kept up to date by deltas
+        // (a step changes one block): the block search is one ballot, no scan
+        uint64_t incl = warp_incl_scan(bA + bB);
+        uint64_t T = __shfl_sync(FULL, incl, 31);
         __syncwarp();
         uint32_t* orow = a.out + w * static_cast<uint64_t>(a.L) * 2;
         uint32_t ebuf = NONE;
@@ -1393,11 +1408,9 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, ui
             uint32_t v = NONE, u = NONE;
             if (T > 0) {
                 const uint64_t x = below(Ux, T);
-                // block containing x: scan of the lanes' block pairs
-                const uint64_t pair = bA + bB;
-                const uint64_t incl = warp_incl_scan(pair);
+                // block containing x
                 const int f = __ffs(__ballot_sync(FULL, incl > x)) - 1;   // exists: x < T
-                const uint64_t ex = __shfl_sync(FULL, incl - pair, f);
+                const uint64_t ex = __shfl_sync(FULL, incl - bA - bB, f);
                 const uint64_t fa = __shfl_sync(FULL, bA, f);
                 const bool second = x >= ex + fa;
                 const uint32_t bsel = 2 * f + (second ? 1 : 0);
@@ -1405,7 +1418,9 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, ui
                 // the block's slots: one 16 B record per lane
                 const uint32_t s0 = bsel * 32 + lane;
                 const uint4 e = s0 < m ? ps[s0] : make_uint4(NONE, 0, 0, 0);
-                const uint64_t incl2 = warp_incl_scan(static_cast<uint64_t>(e.y)) + blo;
+                uint64_t incl2;
+                if constexpr (kNarrow) incl2 = static_cast<uint64_t>(warp_incl_scan_u32(e.y)) + blo;
+                else incl2 = warp_incl_scan(static_cast<uint64_t>(e.y)) + blo;
                 const int fl = __ffs(__ballot_sync(FULL, incl2 > x)) - 1;
                 const uint32_t d = __shfl_sync(FULL, e.y, fl);
                 v = __shfl_sync(FULL, e.x, fl);
@@ -1425,11 +1440,14 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, ui
                 }
                 if (lane == fl)
                     ps[s0] = make_uint4(u, du, static_cast<uint32_t>(ru), static_cast<uint32_t>(static_cast<uint64_t>(ru) >> 32));
-                if (lane == static_cast<int>(bsel >> 1)) {
-                    if (bsel & 1) bB = bB + du - d;
-                    else bA = bA + du - d;
+                const uint64_t delta = static_cast<uint64_t>(du) - d;   // mod 2^64
+                const int owner = static_cast<int>(bsel >> 1);
+                if (lane == owner) {
+                    if (bsel & 1) bB += delta;
+                    else bA += delta;
                 }
-                T = T + du - d;
+                if (lane >= owner) incl += delta;
+                T += delta;
                 __syncwarp();
             }
             // buffer 16 steps (2 words each) per 32 lanes, flush coalesced
@@ -1530,8 +1548,11 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
                         g->col ? g->col : g->oomst.d_colc,
                         static_cast<uint64_t>(g->col ? g->E : g->oomst.colc_n), g->col ? g->nmp : nullptr};
             const int64_t warps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 7 * MDRW_WARPS);
-            k_mdrw_fast<<<static_cast<int>((warps + MDRW_WARPS - 1) / MDRW_WARPS), MDRW_WARPS * 32, 0, st>>>(
-                ma, static_cast<uint4*>(pool));
+            const int mg = static_cast<int>((warps + MDRW_WARPS - 1) / MDRW_WARPS);
+            if (g->max_deg < (int64_t(1) << 27))
+                k_mdrw_fast<true><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, static_cast<uint4*>(pool));
+            else
+                k_mdrw_fast<false><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, static_cast<uint4*>(pool));
             CSAW_CUDA(cudaGetLastError());
             CSAW_TRY(hot_end(g, st));
             CSAW_TRY(stats_end(g, st));
