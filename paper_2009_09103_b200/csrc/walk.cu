@@ -915,7 +915,10 @@ constexpr uint32_t N2T_TILE = 1024;   // N(prev) window in shared memory (u32), 
 #ifndef N2T_KEYS
 #define N2T_KEYS 4
 #endif
-constexpr int N2T_K = N2T_KEYS;       // keys per lane per chunk (contiguous positions)
+constexpr int N2T_K = N2T_KEYS;
+#ifndef N2T_SPEC_RATIO
+#define N2T_SPEC_RATIO 8u   // N(prev) this much shorter than N(v): specials by search, no scan of N(v) (cfg3: 2x 777, 4x 727, 8x 727, 16x 750 ms)
+#endif       // keys per lane per chunk (contiguous positions)
 constexpr int N2T_WARPS = 8;
 #ifndef N2T_MINB
 #define N2T_MINB 3
@@ -973,9 +976,67 @@ struct N2tStats {
 // shared-memory tile of B: per lane one binary search for its first key, then a linear
 // merge (B about as dense as A) or galloping searches (B denser); B much longer than A:
 // per-key binary searches of B in global memory.
+// B much shorter than A (N(prev) << N(v)): instead of scanning A, locate the specials --
+// B's members of A (weight w1) and prev (weight wp) -- by searching each B entry in A;
+// between specials S grows by wq per position, so the region follows in closed form.
+// S(p) at a member at position p with j members before it: wq p - (wq - w1) j -
+// (wq - wp) [p > ppos].  Members come in ascending position (B is sorted), so the walk
+// over B stops at the first member whose S passes xs.
+__device__ uint32_t n2t_specials(const MirList& A, const MirList& B, uint32_t pvk, uint64_t xs, uint32_t wp,
+                                 uint32_t w1, uint32_t wq, N2tStats& st) {
+    const uint32_t lane = static_cast<uint32_t>(lane_id());
+    const uint32_t ppos = mir_lower_bound(A, 0, A.n, pvk);   // prev is in N(v) (symmetric graph)
+    // deficits per special (mod 2^64: negative when 1/q < 1 or 1/q < 1/p; S itself is exact)
+    const uint64_t dq1 = static_cast<uint64_t>(wq) - w1, dqp = static_cast<uint64_t>(wq) - wp;
+    uint32_t j = 0;                 // members seen so far
+    uint32_t before_prev = 0;       // members at positions < ppos
+    bool have = false;              // a member with S <= xs seen
+    uint32_t pm = 0;                // its position (the last such)
+    uint64_t Sm = 0;
+    bool stop = false;
+    for (uint32_t r0 = 0; r0 < B.n && !stop; r0 += 32) {
+        const uint32_t i = r0 + lane;
+        const bool valid = i < B.n;
+        const uint32_t b = valid ? B.at(i) : 0u;
+        uint32_t l = 0, h = valid ? A.n : 0u;
+        for (uint32_t span = A.n; span > 0; span >>= 1) {   // same trip count on every lane
+            if (l < h) {
+                const uint32_t mid = (l + h) >> 1;
+                if (A.at(mid) < b) l = mid + 1; else h = mid;
+            }
+        }
+        const bool mem = valid && l < A.n && A.at(l) == b;
+        st.bkeys += min(32u, B.n - r0) * (32 - __clz(A.n + 1));
+        const unsigned mb = __ballot_sync(FULL, mem);
+        const uint32_t jj = j + __popc(mb & lanemask_lt());   // members before this one
+        const uint64_t S = static_cast<uint64_t>(wq) * l - dq1 * jj - (l > ppos ? dqp : 0);
+        const unsigned le = __ballot_sync(FULL, mem && S <= xs);
+        if (le) {
+            const int f = 31 - __clz(le);
+            have = true;
+            pm = __shfl_sync(FULL, l, f);
+            Sm = __shfl_sync(FULL, S, f);
+        }
+        before_prev += __popc(__ballot_sync(FULL, mem && l < ppos));
+        if (__ballot_sync(FULL, mem && S > xs)) stop = true;   // later members only grow S
+        j += __popc(mb);
+    }
+    // prev as a special: S(ppos) = wq ppos - (wq - w1) (members before it); complete if
+    // the walk stopped after ppos (else S(ppos) > xs anyway, see above)
+    const uint64_t Sp = static_cast<uint64_t>(wq) * ppos - dq1 * before_prev;
+    uint32_t q;
+    uint64_t Sq, wqq;
+    if (Sp <= xs && (!have || ppos > pm)) { q = ppos; Sq = Sp; wqq = wp; }
+    else if (have) { q = pm; Sq = Sm; wqq = w1; }
+    else return static_cast<uint32_t>(xs / wq);   // before every special
+    if (xs < Sq + wqq) return q;
+    return q + 1 + static_cast<uint32_t>((xs - Sq - wqq) / wq);
+}
+
 __device__ uint32_t n2t_scan(const MirList& A, const MirList& B, uint32_t pvk, uint64_t xs, uint32_t wp,
                              uint32_t w1, uint32_t wq, uint32_t* tile, N2tStats& st) {
     const uint32_t lane = static_cast<uint32_t>(lane_id());
+    if (N2T_SPEC_RATIO * B.n < A.n) return n2t_specials(A, B, pvk, xs, wp, w1, wq, st);
     const bool bsearch = B.n > 16u * A.n;
     const bool linear = B.n <= 3u * A.n;
     uint64_t acc = 0;
