@@ -916,6 +916,9 @@ constexpr uint32_t N2T_TILE = 1024;   // N(prev) window in shared memory (u32), 
 #define N2T_KEYS 4
 #endif
 constexpr int N2T_K = N2T_KEYS;
+#ifndef N2T_BS_RATIO
+#define N2T_BS_RATIO 4u      // N(prev) this much longer than N(v): per-key binary searches of N(prev) (cfg3: 4x 714, 8x 715, 16x 727, 64x 774 ms)
+#endif
 #ifndef N2T_SPEC_RATIO
 #define N2T_SPEC_RATIO 8u   // N(prev) this much shorter than N(v): specials by search, no scan of N(v) (cfg3: 2x 777, 4x 727, 8x 727, 16x 750 ms)
 #endif       // keys per lane per chunk (contiguous positions)
@@ -1037,7 +1040,7 @@ __device__ uint32_t n2t_scan(const MirList& A, const MirList& B, uint32_t pvk, u
                              uint32_t w1, uint32_t wq, uint32_t* tile, N2tStats& st) {
     const uint32_t lane = static_cast<uint32_t>(lane_id());
     if (N2T_SPEC_RATIO * B.n < A.n) return n2t_specials(A, B, pvk, xs, wp, w1, wq, st);
-    const bool bsearch = B.n > 16u * A.n;
+    const bool bsearch = B.n > N2T_BS_RATIO * A.n;
     const bool linear = B.n <= 3u * A.n;
     uint64_t acc = 0;
     uint32_t bnext = 0;                     // B entries before bnext are below every key still to come
