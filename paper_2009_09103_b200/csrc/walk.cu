@@ -911,7 +911,10 @@ __device__ void n2v_implicit_step(Node2vecPool& P, uint32_t* spec, uint32_t* til
 // code path) only until the running S passes x.  Expected scan length: a quarter of
 // N(v) instead of all of it plus all of N(prev).  Same S, same x, same region as the
 // scanned CTPS and the oracle (bit-identical).
-constexpr uint32_t N2T_TILE = 1024;   // N(prev) window in shared memory (u32), per warp
+#ifndef N2T_TILE_N
+#define N2T_TILE_N 1024
+#endif
+constexpr uint32_t N2T_TILE = N2T_TILE_N;   // N(prev) window in shared memory (u32), per warp
 #ifndef N2T_KEYS
 #define N2T_KEYS 4
 #endif
@@ -924,7 +927,7 @@ constexpr int N2T_K = N2T_KEYS;
 #endif       // keys per lane per chunk (contiguous positions)
 constexpr int N2T_WARPS = 8;
 #ifndef N2T_MINB
-#define N2T_MINB 3
+#define N2T_MINB 4   // 64 registers, 32 warps / SM: the step is latency-bound (cfg3: 3: 714, 4: 543, 5: 699 (spills), 6: 972 ms)
 #endif
 
 // A sorted list read forwards, or backwards with every value complemented (x -> ~x
