@@ -670,7 +670,9 @@ def load_traffic(cfg_name, kernel):
         if not isinstance(v, dict):
             return None
         norm = lambda k: k.replace("void ", "").replace("csaw::", "").replace(" ", "")
-        if norm(v.get("kernel", "")) != norm(kernel):
+        a, b = norm(v.get("kernel", "")), norm(kernel)
+        # same kernel; template arguments must agree when both names carry them
+        if a.split("<")[0] != b.split("<")[0] or ("<" in a and "<" in b and a != b):
             return None
         return v.get("dram_bytes_per_launch")
     except Exception:
