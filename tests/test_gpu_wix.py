@@ -120,3 +120,40 @@ def test_wix_isolated_seed():
         G, og = make(rp, col, leaf)
         check_walk(G, og, "degree", np.array([0, 1, 2, 3], np.uint32), 5, rng_seed=1)
         G.close()
+
+
+def boundary_csr():
+    """Rows at the vertex-head boundaries: d = 7,936 (top level of 124 entries, inline),
+    7,937 / 8,100 / 8,192 (125 / 127 / 128 top entries: read from the node array), d = 60
+    (inline leaf) and 61..64 (leaf read from the leaf arrays), plus a ring."""
+    V = 9_000
+    adj = {v: set() for v in range(V)}
+
+    def link(a, b):
+        if a != b:
+            adj[a].add(b)
+            adj[b].add(a)
+
+    for hub, d in [(0, 7936), (1, 7937), (2, 8100), (3, 8192)]:
+        for u in range(10, 10 + d):
+            link(hub, u % V if u < V else 10 + (u % (V - 10)))
+    for v, d in [(4, 60), (5, 61), (6, 62), (7, 63), (8, 64)]:
+        for u in range(100 + 97 * v, 100 + 97 * v + d):
+            link(v, u)
+    for v in range(9, V):
+        link(v, v + 1 if v + 1 < V else 9)
+    rp = np.zeros(V + 1, np.int64)
+    rp[1:] = np.cumsum([len(adj[v]) for v in range(V)])
+    col = np.concatenate([np.array(sorted(adj[v]), np.uint32) for v in range(V)])
+    return rp, col
+
+
+@pytest.mark.parametrize("leaf", [(64, 32), (64, "nohead"), (32, 32)])
+def test_wix_head_boundaries(leaf):
+    rp, col = boundary_csr()
+    deg = np.diff(rp)
+    assert {7936, 7937, 8192, 60, 61, 64} <= set(deg[:9].tolist())
+    G, og = make(rp, col, leaf)
+    seeds = np.array([0, 1, 2, 3, 4, 5, 6, 7, 8] * 8 + [100, 500, 4000], dtype=np.uint32)
+    check_walk(G, og, "degree", seeds, 120, rng_seed=31)
+    G.close()
