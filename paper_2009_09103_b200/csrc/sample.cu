@@ -689,6 +689,9 @@ constexpr int FUSED_WARPS = 4;
 #ifndef FUSED_MINB
 #define FUSED_MINB 4
 #endif
+#ifndef FUSED_FF_MINB
+#define FUSED_FF_MINB 8
+#endif
 constexpr uint32_t F_CAP = 256;
 constexpr uint32_t VIS_CAP = 512;
 
@@ -803,13 +806,15 @@ struct FusedLayerEmit {
 // kMode: 0 uniform NS, 1 degree NS (scan), 2 degree NS (cache), 3 forest fire,
 //        4 layer (scan), 5 layer (cache)
 template <int kMode>
-__global__ void __launch_bounds__(FUSED_WARPS * 32, kMode >= 3 ? 6 : FUSED_MINB) k_sample_fused(FusedArgs a) {
+// blocks / SM: forest fire (no layer prefix table, 7 KB smem per warp) 8, layer 6 (smem-bound), NS 4
+__global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB : kMode >= 4 ? 6 : FUSED_MINB)
+    k_sample_fused(FusedArgs a) {
     __shared__ uint64_t tab_all[FUSED_WARPS][TAB];
     __shared__ uint32_t bm_all[FUSED_WARPS][BM_WORDS];
     __shared__ uint32_t F_all[FUSED_WARPS][F_CAP];
     __shared__ uint32_t NX_all[FUSED_WARPS][F_CAP];
     __shared__ uint32_t VIS_all[FUSED_WARPS][VIS_CAP];
-    __shared__ uint64_t PF_all[FUSED_WARPS][F_CAP];
+    __shared__ uint64_t PF_all[FUSED_WARPS][kMode >= 4 ? F_CAP : 1];   // layer pools only
     const int wib = threadIdx.x >> 5;
     uint64_t* tab = tab_all[wib];
     uint32_t* bm = bm_all[wib];
