@@ -14,7 +14,9 @@
  *  - Pointers are plain host or device pointers; the library detects which with
  *    cudaPointerGetAttributes.  Device pointers must live on the graph's device.
  *    Host pointers are staged through library-owned device scratch inside the
- *    call (copies on `stream`), and the call then synchronises `stream`.
+ *    call (copies on `stream`), and the call then synchronises `stream`.  One
+ *    exception: a page-locked (pinned) host `path` of csaw_walk is written by the
+ *    kernels directly over the host link, overlapped with the walk.
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  With device
  *    buffers, csaw_walk is stream-ordered and returns after enqueue;
  *    csaw_sample synchronises `stream` once (it must return *num_edges).

@@ -102,6 +102,17 @@ bool is_device_ptr(const void* p, int device) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Device-side address of pinned (page-locked) host memory, or nullptr for pageable memory.
+void* pinned_device_ptr(void* p) {
+    if (!p) return nullptr;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 csaw_status begin_call(const csaw_graph* g) {
     clear_error();
     if (!g) return fail(CSAW_ERR_INVALID_ARG, "graph is NULL");
@@ -882,7 +893,12 @@ CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32
         CSAW_CUDA(cudaMemcpyAsync(p, seeds, sizeof(uint32_t) * nseeds, cudaMemcpyHostToDevice, st));
         d_seeds = static_cast<const uint32_t*>(p);
     }
-    if (!path_dev) {
+    // pinned host output: the kernels write the paths straight into it over the host link,
+    // overlapped with the walk (no device staging, no copy after the kernel)
+    void* const path_pinned = path_dev ? nullptr : pinned_device_ptr(path);
+    if (path_pinned) {
+        d_path = static_cast<uint32_t*>(path_pinned);
+    } else if (!path_dev) {
         void* p;
         CSAW_TRY(g->scratch.get(SL_OUT, sizeof(uint32_t) * std::max<int64_t>(nout, 1), &p));
         d_path = static_cast<uint32_t*>(p);
@@ -897,7 +913,7 @@ CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32
         s = run_walk(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
     }
     if (s != CSAW_OK) return s;
-    if (!path_dev) {
+    if (!path_dev && !path_pinned) {
         CSAW_CUDA(cudaMemcpyAsync(path, d_path, sizeof(uint32_t) * nout, cudaMemcpyDeviceToHost, st));
     }
     if (!seeds_dev || !path_dev) CSAW_CUDA(cudaStreamSynchronize(st));

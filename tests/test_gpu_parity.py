@@ -305,3 +305,23 @@ def test_mdrw_next_meta(medium):
         e0 = u32(cs.csaw_walk(G0, cs.make_bias("mdrw"), torch.as_tensor(s.view(np.int32)).to(DEV), L, rng_seed=17))
         assert np.array_equal(e, e0)
     Gm.close()
+
+
+@pytest.mark.parametrize("kind", ["degree", "uniform", "node2vec", "mdrw"])
+def test_walk_into_pinned_host_output(medium, kind):
+    """A pinned host `path` is written by the kernels directly (zero-copy); a pageable one is
+    staged and copied.  Both must equal the device-buffer result."""
+    G, og, g = medium
+    if kind == "mdrw":
+        seeds = mdrw_seeds(g, 40, 64)
+        shape, L = (40, 90, 2), 90
+    else:
+        seeds = instance_seeds(g, 300, set_id=7)
+        shape, L = (300, 91), 90
+    b = cs.make_bias(kind, p=2.0, q=0.5)
+    ref = cs.csaw_walk(G, b, seeds.to(DEV), L, rng_seed=3)
+    pinned = torch.empty(shape, dtype=torch.int32).pin_memory()
+    pageable = torch.empty(shape, dtype=torch.int32)
+    cs.csaw_walk(G, b, seeds.pin_memory(), L, rng_seed=3, out=pinned)
+    cs.csaw_walk(G, b, seeds, L, rng_seed=3, out=pageable)
+    assert torch.equal(ref.cpu(), pinned) and torch.equal(ref.cpu(), pageable)
