@@ -132,3 +132,11 @@ def test_cfg5_mdrw_in_memory_full():
         assert np.array_equal(edges[i], ref), f"instance {i}"
     check_edges_exist(og, edges[:, :, 0].ravel(), edges[:, :, 1].ravel())
     release(G)
+    # the config's out-of-memory launch (8 GB budget), zero-copy mode with the resident
+    # col_idx prefix: identical to the in-memory edges on 100 % of the output
+    Gz = cs.csaw_graph_create(g.row_ptr.cpu(), g.col_idx.cpu(), device=0, budget_bytes=cfg.oom_budget_bytes,
+                              num_partitions=cfg.oom_partitions, max_resident=1, zerocopy=True)
+    assert Gz.info()["device_bytes"] <= cfg.oom_budget_bytes
+    ez = u32(cs.csaw_walk(Gz, cs.make_bias("mdrw"), seeds, cfg.length, rng_seed=1))
+    assert np.array_equal(ez, edges)
+    release(Gz)
