@@ -17,9 +17,10 @@
  *    call (copies on `stream`), and the call then synchronises `stream`.  One
  *    exception: a page-locked (pinned) host `path` of csaw_walk is written by the
  *    kernels directly over the host link, overlapped with the walk.
- *  - `stream` is a cudaStream_t (NULL = legacy default stream).  With device
- *    buffers, csaw_walk is stream-ordered and returns after enqueue;
- *    csaw_sample synchronises `stream` once (it must return *num_edges).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  csaw_walk
+ *    synchronises `stream` once after its seed check and returns after enqueuing
+ *    the walk (device buffers); csaw_sample synchronises `stream` once (it must
+ *    return *num_edges).
  *  - Ownership: callers own every buffer they pass.  csaw_graph_create copies
  *    the CSR; the graph owns its device copy and its internal scratch (reused
  *    across calls, freed by csaw_graph_destroy).  A graph may be used by one
@@ -240,6 +241,8 @@ CSAW_API csaw_status csaw_sample(const csaw_graph *g, const csaw_bias *bias, con
  *     neighbour stops and the rest of its row is CSAW_NONE (R20).
  *   MDRW: seeds uint32[n_walkers][pool_size] (the instance's initial pool, slot
  *     order); path uint32[n_walkers][length][2] = the (v, u) edge sampled at each step.
+ * Returns OUT_OF_RANGE if a seed >= V (checked on the device before any walk kernel;
+ * the call then synchronises `stream` once, nothing is written to path).
  */
 CSAW_API csaw_status csaw_walk(const csaw_graph *g, const csaw_bias *bias, int32_t length,
                                const uint32_t *seeds, int64_t n_walkers, uint64_t instance_base,

@@ -862,6 +862,12 @@ static csaw_status check_bias(const csaw_bias* b) {
     return CSAW_OK;
 }
 
+// Any seed >= V sets *bad (a plain store into pinned, host-mapped memory).
+__global__ void k_check_seeds(const uint32_t* __restrict__ seeds, int64_t n, int64_t V, volatile unsigned* bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (static_cast<int64_t>(seeds[i]) >= V) *bad = 1u;
+}
+
 CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32_t length, const uint32_t* seeds,
                                int64_t n, uint64_t instance_base, uint64_t rng_seed, uint32_t* path, void* stream) {
     CSAW_TRY(begin_call(g));
@@ -892,6 +898,19 @@ CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32
         CSAW_TRY(g->scratch.get(SL_SEEDS, sizeof(uint32_t) * nseeds, &p));
         CSAW_CUDA(cudaMemcpyAsync(p, seeds, sizeof(uint32_t) * nseeds, cudaMemcpyHostToDevice, st));
         d_seeds = static_cast<const uint32_t*>(p);
+    }
+    // seeds must be vertices: checked on the device before any walk kernel reads a row
+    {
+        void* hm;
+        CSAW_TRY(g->pinned.get(4096, &hm));
+        volatile unsigned* bad = static_cast<volatile unsigned*>(hm) + 1000;
+        *bad = 0u;
+        const int cb = static_cast<int>(std::min<int64_t>((nseeds + 255) / 256, int64_t(g->num_sms) * 8));
+        k_check_seeds<<<std::max(cb, 1), 256, 0, st>>>(d_seeds, nseeds, g->V, bad);
+        note_launch();
+        CSAW_CUDA(cudaGetLastError());
+        CSAW_CUDA(cudaStreamSynchronize(st));
+        if (*bad) return fail(CSAW_ERR_OUT_OF_RANGE, "a seed vertex is >= num_vertices");
     }
     // pinned host output: the kernels write the paths straight into it over the host link,
     // overlapped with the walk (no device staging, no copy after the kernel)

@@ -222,15 +222,18 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_head(WalkArgs a, co
         PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
         pw.put(0, cur);
         uint64_t ubuf = 0;
+        // the head of the vertex a step starts from is requested as soon as that vertex is
+        // known (end of the previous step); every lane also loads the 16 B header itself
+        // (same line, one transaction), so no shuffles sit between the head and the draw
+        const uint4* hp = reinterpret_cast<const uint4*>(head + static_cast<uint64_t>(cur) * WIX_HEAD_WORDS);
+        uint4 q = __ldg(hp + lane), hd = __ldg(hp);
         for (int32_t t = 0; t < a.L; ++t) {
             if ((t & 31) == 0)
                 ubuf = draw_u64(a.key, inst, static_cast<uint32_t>(t + lane), 0u, word3(PURPOSE_EDGE, 0, 0));
             const uint64_t U = __shfl_sync(FULL, ubuf, t & 31);
             uint32_t nxt = NONE;
             if (cur != NONE) {
-                const uint4 q = __ldg(reinterpret_cast<const uint4*>(head + static_cast<uint64_t>(cur) * WIX_HEAD_WORDS) + lane);
-                const uint32_t d = __shfl_sync(FULL, q.x, 0), T = __shfl_sync(FULL, q.y, 0);
-                const uint32_t p = __shfl_sync(FULL, q.z, 0), io = __shfl_sync(FULL, q.w, 0);
+                const uint32_t d = hd.x, T = hd.y, p = hd.z, io = hd.w;
                 bytes += 512;
                 if (d > 0 && T > 0) {   // T = 0: no positive-bias neighbour, the walk ends (R20)
                     const uint32_t x = static_cast<uint32_t>(below(U, T));
@@ -282,6 +285,11 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_head(WalkArgs a, co
                 }
             }
             cur = nxt;
+            if (cur != NONE && t + 1 < a.L) {
+                const uint4* np = reinterpret_cast<const uint4*>(head + static_cast<uint64_t>(cur) * WIX_HEAD_WORDS);
+                q = __ldg(np + lane);
+                hd = __ldg(np);
+            }
             pw.put(t + 1, cur);
         }
     }

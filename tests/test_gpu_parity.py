@@ -325,3 +325,20 @@ def test_walk_into_pinned_host_output(medium, kind):
     cs.csaw_walk(G, b, seeds.pin_memory(), L, rng_seed=3, out=pinned)
     cs.csaw_walk(G, b, seeds, L, rng_seed=3, out=pageable)
     assert torch.equal(ref.cpu(), pinned) and torch.equal(ref.cpu(), pageable)
+
+
+@pytest.mark.parametrize("kind", ["degree", "uniform", "node2vec", "mdrw"])
+def test_walk_seed_out_of_range(medium, kind):
+    """A seed >= V is rejected before any walk kernel reads a row (OUT_OF_RANGE)."""
+    G, og, g = medium
+    V = g.row_ptr.numel() - 1
+    if kind == "mdrw":
+        seeds = mdrw_seeds(g, 4, 8).clone()
+        seeds[2, 5] = V
+    else:
+        seeds = instance_seeds(g, 40).clone()
+        seeds[17] = V + 3
+    for dev in (DEV, "cpu"):
+        with pytest.raises(cs.CsawError) as ei:
+            cs.csaw_walk(G, cs.make_bias(kind, p=2.0, q=0.5), seeds.to(dev), 20, rng_seed=1)
+        assert ei.value.status == 2
