@@ -1444,13 +1444,20 @@ __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v) {
 }
 
 // kNarrow: a block of 32 slot biases sums below 2^32 (max degree < 2^27): u32 block scan.
-template <bool kNarrow>
-__global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, uint4* __restrict__ pool) {
+// kPacked (max degree < 2^24, E < 2^40): a slot is one u64 {row start << 24 | degree} --
+// the same word as the next-vertex metadata -- and the slot's vertex id sits in a separate
+// array read only for the output, off the step's dependent chain; the per-step block read
+// is 256 B instead of 512 B and the pool state (n x m x 8 B) is more L2-resident.
+template <bool kNarrow, bool kPacked>
+__global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, uint4* __restrict__ pool,
+                                                                 uint64_t* __restrict__ prec, uint32_t* __restrict__ pvid) {
     const int lane = lane_id();
     const uint32_t m = static_cast<uint32_t>(a.m);
     for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
         uint4* ps = pool + w * m;
+        uint64_t* pr = prec + w * m;
+        uint32_t* pvv = pvid + w * m;
         // init pool (slot order = seeds order) and the two block totals of this lane
         uint64_t bA = 0, bB = 0;
         for (uint32_t b = 0; b * 32 < m; ++b) {   // block b is held by lane b >> 1
@@ -1460,7 +1467,12 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, ui
                 const uint32_t v = a.seeds[w * m + s];
                 const int64_t r0 = __ldg(a.rp + v);
                 dv = static_cast<uint32_t>(__ldg(a.rp + v + 1) - r0);
-                ps[s] = make_uint4(v, dv, static_cast<uint32_t>(r0), static_cast<uint32_t>(static_cast<uint64_t>(r0) >> 32));
+                if constexpr (kPacked) {
+                    pr[s] = static_cast<uint64_t>(r0) << 24 | dv;
+                    pvv[s] = v;
+                } else {
+                    ps[s] = make_uint4(v, dv, static_cast<uint32_t>(r0), static_cast<uint32_t>(static_cast<uint64_t>(r0) >> 32));
+                }
             }
             const uint64_t tot = warp_sum(static_cast<uint64_t>(dv));
             if (lane == static_cast<int>(b >> 1)) { if (b & 1) bB = tot; else bA = tot; }
@@ -1490,21 +1502,37 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, ui
                 const bool second = x >= ex + fa;
                 const uint32_t bsel = 2 * f + (second ? 1 : 0);
                 const uint64_t blo = second ? ex + fa : ex;
-                // the block's slots: one 16 B record per lane
+                // the block's slots
                 const uint32_t s0 = bsel * 32 + lane;
-                const uint4 e = s0 < m ? ps[s0] : make_uint4(NONE, 0, 0, 0);
+                uint32_t bias;
+                uint64_t rec = 0;
+                uint4 e = make_uint4(NONE, 0, 0, 0);
+                if constexpr (kPacked) {
+                    rec = s0 < m ? pr[s0] : 0;
+                    bias = static_cast<uint32_t>(rec & 0xFFFFFFu);
+                } else {
+                    e = s0 < m ? ps[s0] : make_uint4(NONE, 0, 0, 0);
+                    bias = e.y;
+                }
                 uint64_t incl2;
-                if constexpr (kNarrow) incl2 = static_cast<uint64_t>(warp_incl_scan_u32(e.y)) + blo;
-                else incl2 = warp_incl_scan(static_cast<uint64_t>(e.y)) + blo;
+                if constexpr (kNarrow) incl2 = static_cast<uint64_t>(warp_incl_scan_u32(bias)) + blo;
+                else incl2 = warp_incl_scan(static_cast<uint64_t>(bias)) + blo;
                 const int fl = __ffs(__ballot_sync(FULL, incl2 > x)) - 1;
-                const uint32_t d = __shfl_sync(FULL, e.y, fl);
-                v = __shfl_sync(FULL, e.x, fl);
-                const uint64_t rb = static_cast<uint64_t>(__shfl_sync(FULL, e.w, fl)) << 32 | __shfl_sync(FULL, e.z, fl);
+                const uint32_t d = __shfl_sync(FULL, bias, fl);
+                uint64_t rb;
+                if constexpr (kPacked) {
+                    rb = __shfl_sync(FULL, rec, fl) >> 24;
+                    v = pvv[bsel * 32 + fl];   // for the output only (not on the next step's chain)
+                } else {
+                    v = __shfl_sync(FULL, e.x, fl);
+                    rb = static_cast<uint64_t>(__shfl_sync(FULL, e.w, fl)) << 32 | __shfl_sync(FULL, e.z, fl);
+                }
                 const uint64_t ei = rb + below(Ue, d);
                 int64_t ru;
                 uint32_t du;
+                uint64_t mt = 0;
                 if (a.nmp) {   // the new vertex's row and degree come with the entry (no dependent lookup)
-                    const uint64_t mt = __ldg(a.nmp + ei);
+                    mt = __ldg(a.nmp + ei);
                     u = __ldg(a.col + ei);
                     ru = static_cast<int64_t>(mt >> 24);
                     du = static_cast<uint32_t>(mt & 0xFFFFFFu);
@@ -1512,9 +1540,16 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, ui
                     u = ei < a.colc_n ? __ldg(a.colc + ei) : __ldg(a.col + ei);   // OOM zero-copy: host beyond colc_n
                     ru = __ldg(a.rp + u);
                     du = static_cast<uint32_t>(__ldg(a.rp + u + 1) - ru);
+                    mt = static_cast<uint64_t>(ru) << 24 | du;
                 }
-                if (lane == fl)
-                    ps[s0] = make_uint4(u, du, static_cast<uint32_t>(ru), static_cast<uint32_t>(static_cast<uint64_t>(ru) >> 32));
+                if (lane == fl) {
+                    if constexpr (kPacked) {
+                        pr[s0] = mt;
+                        pvv[s0] = u;
+                    } else {
+                        ps[s0] = make_uint4(u, du, static_cast<uint32_t>(ru), static_cast<uint32_t>(static_cast<uint64_t>(ru) >> 32));
+                    }
+                }
                 const uint64_t delta = static_cast<uint64_t>(du) - d;   // mod 2^64
                 const int owner = static_cast<int>(bsel >> 1);
                 if (lane == owner) {
@@ -1616,18 +1651,29 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         const uint32_t m = static_cast<uint32_t>(b.pool_size);
         const uint32_t nblk = (m + 31) / 32;
         if (nblk <= 64 && !std::getenv("CSAW_MDRW_SLOW")) {   // pools up to 2,048 slots (cfg5: 2,000)
-            void* pool;
-            CSAW_TRY(g->scratch.get(SL_TMP0, sizeof(uint4) * n * m, &pool));
+            const bool packed = g->max_deg < (int64_t(1) << 24) && g->E < (int64_t(1) << 40) &&
+                                !std::getenv("CSAW_MDRW_WIDE");
+            void *pool = nullptr, *pvid = nullptr;
+            if (packed) {
+                CSAW_TRY(g->scratch.get(SL_TMP0, sizeof(uint64_t) * n * m, &pool));
+                CSAW_TRY(g->scratch.get(SL_TMP1, sizeof(uint32_t) * n * m, &pvid));
+            } else {
+                CSAW_TRY(g->scratch.get(SL_TMP0, sizeof(uint4) * n * m, &pool));
+            }
             MdrwArgs ma{g->row_ptr, colp, d_seeds, static_cast<uint64_t>(n), b.pool_size, length,
                         static_cast<uint32_t>(base), key, d_path, nullptr, nullptr, nullptr, nullptr, 0, WALK_WARPS,
                         g->col ? g->col : g->oomst.d_colc,
                         static_cast<uint64_t>(g->col ? g->E : g->oomst.colc_n), g->col ? g->nmp : nullptr};
             const int64_t warps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 7 * MDRW_WARPS);
             const int mg = static_cast<int>((warps + MDRW_WARPS - 1) / MDRW_WARPS);
-            if (g->max_deg < (int64_t(1) << 27))
-                k_mdrw_fast<true><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, static_cast<uint4*>(pool));
-            else
-                k_mdrw_fast<false><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, static_cast<uint4*>(pool));
+            uint4* p4 = static_cast<uint4*>(pool);
+            uint64_t* p8 = static_cast<uint64_t*>(pool);
+            uint32_t* pv = static_cast<uint32_t*>(pvid);
+            const bool narrow = g->max_deg < (int64_t(1) << 27);
+            if (packed && narrow) k_mdrw_fast<true, true><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, p4, p8, pv);
+            else if (packed) k_mdrw_fast<false, true><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, p4, p8, pv);
+            else if (narrow) k_mdrw_fast<true, false><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, p4, p8, pv);
+            else k_mdrw_fast<false, false><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, p4, p8, pv);
             CSAW_CUDA(cudaGetLastError());
             CSAW_TRY(hot_end(g, st));
             CSAW_TRY(stats_end(g, st));

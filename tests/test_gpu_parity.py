@@ -283,13 +283,14 @@ def test_mdrw_pool_sizes(medium, m, n, L):
     G2, og2, g2 = medium
     s = mdrw_seeds(g2, n, m).numpy()
     e = check_mdrw(G2, og2, s, L, rng_seed=7, instances=range(0, n, max(1, n // 40)))
-    os.environ["CSAW_MDRW_SLOW"] = "1"
-    try:
-        e2 = u32(cs.csaw_walk(G2, cs.make_bias("mdrw", pool_size=m), torch.as_tensor(s.view(np.int32)).to(DEV), L,
-                              rng_seed=7))
-    finally:
-        del os.environ["CSAW_MDRW_SLOW"]
-    assert np.array_equal(e, e2)
+    for env in ("CSAW_MDRW_SLOW", "CSAW_MDRW_WIDE"):   # large-pool kernel; 16 B slot records
+        os.environ[env] = "1"
+        try:
+            e2 = u32(cs.csaw_walk(G2, cs.make_bias("mdrw", pool_size=m), torch.as_tensor(s.view(np.int32)).to(DEV), L,
+                                  rng_seed=7))
+        finally:
+            del os.environ[env]
+        assert np.array_equal(e, e2), env
 
 
 def test_mdrw_next_meta(medium):
