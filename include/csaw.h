@@ -15,8 +15,9 @@
  *    cudaPointerGetAttributes.  Device pointers must live on the graph's device.
  *    Host pointers are staged through library-owned device scratch inside the
  *    call (copies on `stream`), and the call then synchronises `stream`.  One
- *    exception: a page-locked (pinned) host `path` of csaw_walk is written by the
- *    kernels directly over the host link, overlapped with the walk.
+ *    exception: page-locked (pinned) host outputs -- csaw_walk's `path`, and
+ *    csaw_sample's src / dst / edge_depth on its fused path -- are written by the
+ *    kernels directly over the host link, overlapped with the computation.
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  csaw_walk
  *    synchronises `stream` once after its seed check and returns after enqueuing
  *    the walk (device buffers); csaw_sample synchronises `stream` once (it must

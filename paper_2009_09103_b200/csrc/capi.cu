@@ -985,8 +985,15 @@ CSAW_API csaw_status csaw_sample(const csaw_graph* g, const csaw_bias* bias, con
         CSAW_TRY(g->scratch.get(SL_OFFS, sizeof(uint64_t) * (n + 1), &p));
         d_offs = static_cast<uint64_t*>(p);
     }
+    PinnedOut po{nullptr, nullptr, nullptr};
+    if (!out_dev) {
+        po.src = static_cast<uint32_t*>(pinned_device_ptr(src));
+        po.dst = static_cast<uint32_t*>(pinned_device_ptr(dst));
+        po.dep = static_cast<uint8_t*>(pinned_device_ptr(edge_depth));
+    }
+    const bool all_pinned = po.src && po.dst && po.dep;
     csaw_status s = run_sample(g, b, fanout, depth, d_seeds, n, instance_base, rng_seed, d_offs, src, dst,
-                               edge_depth, capacity, num_edges, out_dev, st);
+                               edge_depth, capacity, num_edges, out_dev, st, all_pinned ? &po : nullptr);
     if (s != CSAW_OK && s != CSAW_ERR_CAPACITY) return s;
     if (!offs_dev) {
         CSAW_CUDA(cudaMemcpyAsync(offsets, d_offs, sizeof(uint64_t) * (n + 1), cudaMemcpyDeviceToHost, st));

@@ -178,10 +178,17 @@ csaw_status stats_end(const csaw_graph* g, cudaStream_t st);
 // walk.cu / sample.cu entry points
 csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds,
                      int64_t n, uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st);
+// pinned host outputs, device-mapped (the fused sampler writes them directly; the batched
+// driver's scattered writes stage through device scratch instead)
+struct PinnedOut {
+    uint32_t* src;
+    uint32_t* dst;
+    uint8_t* dep;
+};
 csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
                        const uint32_t* d_seeds, int64_t n, uint64_t base, uint64_t seed, uint64_t* d_offsets,
                        uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
-                       bool out_on_device, cudaStream_t st);
+                       bool out_on_device, cudaStream_t st, const PinnedOut* pinned = nullptr);
 csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
                               const uint32_t* d_seeds, int64_t n, uint64_t base, uint64_t seed, uint64_t* d_offsets,
                               uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,

@@ -1197,10 +1197,15 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
 csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
                        const uint32_t* d_seeds, int64_t n_i64, uint64_t base, uint64_t seed, uint64_t* d_offsets,
                        uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
-                       bool out_on_device, cudaStream_t st) {
+                       bool out_on_device, cudaStream_t st, const PinnedOut* pinned) {
     if (!g->force_batched && (!g->oom || g->oomst.zerocopy) && b.kind != CSAW_BIAS_SNOWBALL) {
+        // pinned host outputs: the fused copy writes each instance's contiguous segment over the
+        // host link (coalesced), so no staging and no copy after the kernels
+        const bool direct = !out_on_device && pinned != nullptr;
         const csaw_status s = run_sample_fused(g, b, fanout, depth, d_seeds, static_cast<uint64_t>(n_i64), base, seed,
-                                               d_offsets, src, dst, dep, capacity, num_edges, out_on_device, st);
+                                               d_offsets, direct ? pinned->src : src, direct ? pinned->dst : dst,
+                                               direct ? pinned->dep : dep, capacity, num_edges,
+                                               out_on_device || direct, st);
         if (s != FUSED_FALLBACK) return s;
     }
     return run_sample_levels(g, b, fanout, depth, d_seeds, n_i64, base, seed, d_offsets, src, dst, dep, capacity,

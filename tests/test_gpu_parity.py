@@ -343,3 +343,22 @@ def test_walk_seed_out_of_range(medium, kind):
         with pytest.raises(cs.CsawError) as ei:
             cs.csaw_walk(G, cs.make_bias(kind, p=2.0, q=0.5), seeds.to(dev), 20, rng_seed=1)
         assert ei.value.status == 2
+
+
+@pytest.mark.parametrize("workload,fanout", [("degree", [2, 2]), ("layer", [2, 3]), ("forest_fire", []),
+                                             ("degree", [40])])
+def test_sample_into_pinned_host_output(cfg1, workload, fanout):
+    """Pinned host outputs: the fused sampler's copy writes them directly (zero-copy); a
+    fused-path fallback (fanout 40 > 32) stages through device scratch.  Both equal the
+    device-buffer result."""
+    G, og, g = cfg1
+    seeds = instance_seeds(g, 200, set_id=9)
+    kw = dict(fanout=fanout, depth=2, rng_seed=5, pf=0.7)
+    ref = cs.csaw_sample(G, workload, seeds.to(DEV), **kw)
+    cap = int(ref[1].numel()) + 16
+    out = [torch.empty(seeds.numel() + 1, dtype=torch.int64).pin_memory(),
+           torch.empty(cap, dtype=torch.int32).pin_memory(), torch.empty(cap, dtype=torch.int32).pin_memory(),
+           torch.empty(cap, dtype=torch.uint8).pin_memory()]
+    got = cs.csaw_sample(G, workload, seeds.pin_memory(), out=out, **kw)
+    for a, b in zip(ref, got):
+        assert torch.equal(a.cpu(), b.cpu())
