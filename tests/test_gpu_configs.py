@@ -7,6 +7,7 @@ oracle element by element (integer biases: bit-exact).  Invariants that hold
 at any size are checked on 100 % of the output.
 """
 import gc
+import os
 
 import numpy as np
 import pytest
@@ -18,6 +19,9 @@ from synth import CONFIGS, instance_seeds, mdrw_seeds, nonisolated_vertices, rma
 from tests._parity import DEV, u32
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+# Philox seed of the runs (CSAW_TEST_SEED overrides: the same checks under other random streams)
+SEED = int(os.environ.get("CSAW_TEST_SEED", "1"))
 
 
 def build(cfg, ctps_cache=False, node2vec_tri=False):
@@ -61,12 +65,12 @@ def test_cfg2_degree_walk_full(cached):
     g, G, og = build(cfg, ctps_cache=cached)
     assert G.info()["walk_index_leaf"] == (64 if cached else 0)
     seeds = instance_seeds(g, cfg.n_instances).to(DEV)
-    path = u32(cs.csaw_walk(G, "degree", seeds, cfg.length, rng_seed=1))
+    path = u32(cs.csaw_walk(G, "degree", seeds, cfg.length, rng_seed=SEED))
     assert path.shape == (cfg.n_instances, cfg.length + 1)
     assert (path != cs.NONE).all()                       # symmetric graph, non-isolated seeds: exact length
     sv = u32(seeds)
     for w in sample_ids(cfg.n_instances, 24):
-        ref = O.walk(og, O.KIND_DEGREE, cfg.length, int(sv[w]), w, 1)
+        ref = O.walk(og, O.KIND_DEGREE, cfg.length, int(sv[w]), w, SEED)
         assert np.array_equal(path[w], ref), f"walker {w}"
     # 100 % invariant: consecutive path vertices are adjacent
     check_edges_exist(og, path[:, :-1].ravel(), path[:, 1:].ravel())
@@ -81,11 +85,11 @@ def test_cfg3_node2vec_full(cached):
     assert G.info()["node2vec_tri"] == (1 if cached else 0)
     seeds = nonisolated_vertices(g).to(torch.int32).to(DEV)
     n = seeds.numel()
-    path = u32(cs.csaw_walk(G, cs.make_bias("node2vec", p=cfg.p, q=cfg.q), seeds, cfg.length, rng_seed=1))
+    path = u32(cs.csaw_walk(G, cs.make_bias("node2vec", p=cfg.p, q=cfg.q), seeds, cfg.length, rng_seed=SEED))
     assert path.shape == (n, cfg.length + 1) and (path != cs.NONE).all()
     sv = u32(seeds)
     for w in sample_ids(n, 40):
-        ref = O.node2vec(og, cfg.p, cfg.q, cfg.length, int(sv[w]), w, 1)
+        ref = O.node2vec(og, cfg.p, cfg.q, cfg.length, int(sv[w]), w, SEED)
         assert np.array_equal(path[w], ref), f"walker {w}"
     check_edges_exist(og, path[:, :-1].ravel(), path[:, 1:].ravel())
     release(G)
@@ -94,15 +98,15 @@ def test_cfg3_node2vec_full(cached):
 def _check_sampling(cfg, g, G, og, workload, k_sample=160):
     seeds = instance_seeds(g, cfg.n_instances).to(DEV)
     bias = cs.make_bias(cfg.bias, pf=cfg.pf)
-    offs, src, dst, dep = cs.csaw_sample(G, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth, rng_seed=1)
+    offs, src, dst, dep = cs.csaw_sample(G, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth, rng_seed=SEED)
     offs = offs.cpu().numpy().astype(np.int64)
     src, dst, dep = u32(src), u32(dst), dep.cpu().numpy()
     sv = u32(seeds)
     for i in sample_ids(cfg.n_instances, k_sample):
         if workload == "layer":
-            es, ed, ee = O.layer_sample(og, list(cfg.fanout), cfg.depth, int(sv[i]), i, 1)
+            es, ed, ee = O.layer_sample(og, list(cfg.fanout), cfg.depth, int(sv[i]), i, SEED)
         else:
-            es, ed, ee = O.neighbor_sample(og, O.KIND_FF, [], cfg.depth, int(sv[i]), i, 1, cfg.pf)
+            es, ed, ee = O.neighbor_sample(og, O.KIND_FF, [], cfg.depth, int(sv[i]), i, SEED, cfg.pf)
         a, b = offs[i], offs[i + 1]
         assert np.array_equal(src[a:b], es) and np.array_equal(dst[a:b], ed) and np.array_equal(dep[a:b], ee), i
     check_edges_exist(og, src, dst)
@@ -124,11 +128,11 @@ def test_cfg5_mdrw_in_memory_full():
     cfg = CONFIGS["cfg5"]
     g, G, og = build(cfg)
     seeds = mdrw_seeds(g, cfg.n_instances, cfg.pool_size).to(DEV)
-    edges = u32(cs.csaw_walk(G, cs.make_bias("mdrw"), seeds, cfg.length, rng_seed=1))
+    edges = u32(cs.csaw_walk(G, cs.make_bias("mdrw"), seeds, cfg.length, rng_seed=SEED))
     assert edges.shape == (cfg.n_instances, cfg.length, 2) and (edges != cs.NONE).all()
     sv = u32(seeds)
     for i in sample_ids(cfg.n_instances, 16):
-        ref = O.mdrw(og, sv[i], cfg.length, i, 1)
+        ref = O.mdrw(og, sv[i], cfg.length, i, SEED)
         assert np.array_equal(edges[i], ref), f"instance {i}"
     check_edges_exist(og, edges[:, :, 0].ravel(), edges[:, :, 1].ravel())
     release(G)
@@ -137,6 +141,6 @@ def test_cfg5_mdrw_in_memory_full():
     Gz = cs.csaw_graph_create(g.row_ptr.cpu(), g.col_idx.cpu(), device=0, budget_bytes=cfg.oom_budget_bytes,
                               num_partitions=cfg.oom_partitions, max_resident=1, zerocopy=True)
     assert Gz.info()["device_bytes"] <= cfg.oom_budget_bytes
-    ez = u32(cs.csaw_walk(Gz, cs.make_bias("mdrw"), seeds, cfg.length, rng_seed=1))
+    ez = u32(cs.csaw_walk(Gz, cs.make_bias("mdrw"), seeds, cfg.length, rng_seed=SEED))
     assert np.array_equal(ez, edges)
     release(Gz)
