@@ -632,8 +632,8 @@ def run_e2e(cs, G, bias, seeds, cfg, base, args, kind, n, dev, world):
 
 def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads=False):
     if cfg.workload == "walk":
-        if cfg.bias == "degree" and wix_leaf and heads and wix_group == 32 and wix_leaf == 64:
-            return "k_walk_head<64>"
+        if cfg.bias == "degree" and wix_leaf and heads and wix_group == 32:
+            return f"k_walk_head<{wix_leaf}>"
         if cfg.bias == "degree" and wix_leaf:
             return f"k_walk_wix<{wix_leaf}>" if wix_group == 32 else f"k_walk_wixg<{wix_group}, {wix_leaf}>"
         return "k_walk_cached" if (cfg.bias == "degree" and cached) else f"k_walk<{cfg.bias}>"

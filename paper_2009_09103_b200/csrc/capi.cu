@@ -400,9 +400,9 @@ static csaw_status build_wix_t(csaw_graph* g, int blocks) {
 // CpsTree path).  Leaf fanout: CSAW_WIX_LEAF = 32 | 64 | 128 (0 = not built, A/B).
 static csaw_status build_wix(csaw_graph* g, int blocks) {
     const char* env = std::getenv("CSAW_WIX_LEAF");
-    int leaf = env ? std::atoi(env) : 64;
+    int leaf = env ? std::atoi(env) : 128;   // cfg2 with vertex heads: 128: 2.374, 64: 2.397, 32: 2.522 ms
     if (env && leaf == 0) return CSAW_OK;   // A/B: u64 index only
-    if (leaf != 32 && leaf != 64 && leaf != 128) leaf = 64;
+    if (leaf != 32 && leaf != 64 && leaf != 128) leaf = 128;
     unsigned int* wide = nullptr;
     CSAW_CUDA(cudaMalloc(&wide, sizeof(unsigned int)));
     CSAW_CUDA(cudaMemset(wide, 0, sizeof(unsigned int)));

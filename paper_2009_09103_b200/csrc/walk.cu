@@ -1602,13 +1602,15 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
                                                 static_cast<int64_t>(g->num_sms) * 64);
         const int grid = static_cast<int>(std::max<int64_t>(1, (warps + wpb - 1) / wpb));
         const uint4* rec = g->wrec;
-        if (g->wix_group == 32 && g->whead && g->wix_leaf == 64) {
+        if (g->wix_group == 32 && g->whead) {
             // small blocks spread the few walkers evenly over the SMs (cfg2: 4,000 warps on 148 SMs)
             const char* we = std::getenv("CSAW_WALK_WPB");
             const int hw = we ? std::max(1, std::min(8, std::atoi(we))) : 2;   // 1: 2.46, 2: 2.43, 4: 2.44, 8: 2.48 ms (cfg2)
             const int64_t hwarps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 64);
-            k_walk_head<64><<<static_cast<int>((hwarps + hw - 1) / hw), hw * 32, 0, st>>>(a, g->whead, g->c32, g->wcol,
-                                                                                       g->winn);
+            const int hg = static_cast<int>((hwarps + hw - 1) / hw);
+            if (g->wix_leaf == 32) k_walk_head<32><<<hg, hw * 32, 0, st>>>(a, g->whead, g->c32, g->wcol, g->winn);
+            else if (g->wix_leaf == 128) k_walk_head<128><<<hg, hw * 32, 0, st>>>(a, g->whead, g->c32, g->wcol, g->winn);
+            else k_walk_head<64><<<hg, hw * 32, 0, st>>>(a, g->whead, g->c32, g->wcol, g->winn);
         } else if (g->wix_group == 32) {
             if (g->wix_leaf == 32) k_walk_wix<32><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);
             else if (g->wix_leaf == 64) k_walk_wix<64><<<grid, blk, 0, st>>>(a, rec, g->c32, g->wcol, g->winn);

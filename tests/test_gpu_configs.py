@@ -63,7 +63,7 @@ def test_cfg2_degree_walk_full(cached):
     """cached=True is the bench's launch: CTPS cache + narrow walk index (k_walk_wix)."""
     cfg = CONFIGS["cfg2"]
     g, G, og = build(cfg, ctps_cache=cached)
-    assert G.info()["walk_index_leaf"] == (64 if cached else 0)
+    assert G.info()["walk_index_leaf"] == (128 if cached else 0)
     seeds = instance_seeds(g, cfg.n_instances).to(DEV)
     path = u32(cs.csaw_walk(G, "degree", seeds, cfg.length, rng_seed=SEED))
     assert path.shape == (cfg.n_instances, cfg.length + 1)

@@ -148,7 +148,7 @@ def boundary_csr():
     return rp, col
 
 
-@pytest.mark.parametrize("leaf", [(64, 32), (64, "nohead"), (32, 32)])
+@pytest.mark.parametrize("leaf", [(128, 32), (64, 32), (64, "nohead"), (32, 32)])
 def test_wix_head_boundaries(leaf):
     rp, col = boundary_csr()
     deg = np.diff(rp)
