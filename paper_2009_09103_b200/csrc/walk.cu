@@ -225,8 +225,12 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_head(WalkArgs a, co
         // the head of the vertex a step starts from is requested as soon as that vertex is
         // known (end of the previous step); every lane also loads the 16 B header itself
         // (same line, one transaction), so no shuffles sit between the head and the draw
+        constexpr int NQ = WIX_HEAD_NQ;   // lane l holds head words 4 NQ l .. 4 NQ l + 4 NQ - 1
         const uint4* hp = reinterpret_cast<const uint4*>(head + static_cast<uint64_t>(cur) * WIX_HEAD_WORDS);
-        uint4 q = __ldg(hp + lane), hd = __ldg(hp);
+        uint4 q[NQ];
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) q[i] = __ldg(hp + NQ * lane + i);
+        uint4 hd = __ldg(hp);
         for (int32_t t = 0; t < a.L; ++t) {
             if ((t & 31) == 0)
                 ubuf = draw_u64(a.key, inst, static_cast<uint32_t>(t + lane), 0u, word3(PURPOSE_EDGE, 0, 0));
@@ -234,24 +238,32 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_head(WalkArgs a, co
             uint32_t nxt = NONE;
             if (cur != NONE) {
                 const uint32_t d = hd.x, T = hd.y, p = hd.z, io = hd.w;
-                bytes += 512;
+                bytes += 4 * WIX_HEAD_WORDS;
                 if (d > 0 && T > 0) {   // T = 0: no positive-bias neighbour, the walk ends (R20)
                     const uint32_t x = static_cast<uint32_t>(below(U, T));
                     const int K = W::levels(d);
-                    // rank of x among the head's entries [0, n): lane l >= 1 holds entries 4 (l - 1) .. + 3
+                    // rank of x among the head's entries [0, n): entry e is word 4 + e
                     auto head_rank = [&](uint32_t n) {
                         uint32_t c = 0;
-                        if (lane >= 1) {
-                            const uint32_t e0 = 4 * (lane - 1);
-                            c = (e0 < n && q.x <= x) + (e0 + 1 < n && q.y <= x) + (e0 + 2 < n && q.z <= x) +
-                                (e0 + 3 < n && q.w <= x);
+#pragma unroll
+                        for (int i = 0; i < NQ; ++i) {
+                            const uint32_t w0 = 4 * (NQ * lane + i);   // first word of q[i]
+                            if (w0 >= 4) {
+                                const uint32_t e0 = w0 - 4;
+                                c += (e0 < n && q[i].x <= x) + (e0 + 1 < n && q[i].y <= x) +
+                                     (e0 + 2 < n && q[i].z <= x) + (e0 + 3 < n && q[i].w <= x);
+                            }
                         }
                         return __reduce_add_sync(FULL, c);
                     };
                     if (K == 0 && d <= WIX_HEAD_LEAF) {   // the whole row is in the head
                         const uint32_t r = head_rank(d);
-                        const uint32_t e = WIX_HEAD_LEAF + r;   // col entry r: word 4 + 60 + r
-                        nxt = __shfl_sync(FULL, u4_at(q, e & 3), 1 + (e >> 2));
+                        const uint32_t wc = 4 + WIX_HEAD_LEAF + r;   // col entry r
+                        const uint32_t qi = (wc >> 2) % NQ;
+                        uint4 qq = q[0];
+#pragma unroll
+                        for (int i = 1; i < NQ; ++i) if (qi == static_cast<uint32_t>(i)) qq = q[i];
+                        nxt = __shfl_sync(FULL, u4_at(qq, wc & 3), wc / (4 * NQ));
                     } else {
                         uint32_t j = 0;
                         uint64_t off = io;
@@ -287,7 +299,8 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_head(WalkArgs a, co
             cur = nxt;
             if (cur != NONE && t + 1 < a.L) {
                 const uint4* np = reinterpret_cast<const uint4*>(head + static_cast<uint64_t>(cur) * WIX_HEAD_WORDS);
-                q = __ldg(np + lane);
+#pragma unroll
+                for (int i = 0; i < NQ; ++i) q[i] = __ldg(np + NQ * lane + i);
                 hd = __ldg(np);
             }
             pw.put(t + 1, cur);

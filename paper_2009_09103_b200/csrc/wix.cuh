@@ -39,9 +39,13 @@ constexpr int WIX_NODE_LOG = 7;
 // has <= 124 entries, or, for rows of d <= 60, the whole leaf inline (S in words 4..63, col
 // in words 64..123).  A step then starts with one coalesced read that carries the record
 // and the first search level together (one dependent round trip less than record + node).
-constexpr int WIX_HEAD_WORDS = 128;
-constexpr uint32_t WIX_HEAD_TOP = 124;    // inline top-level entries
-constexpr uint32_t WIX_HEAD_LEAF = 60;    // inline leaf entries (S and col)
+#ifndef WIX_HEAD_WORDS_N
+#define WIX_HEAD_WORDS_N 128
+#endif
+constexpr int WIX_HEAD_WORDS = WIX_HEAD_WORDS_N;                 // 128 (512 B) or 256 (1 KB)
+constexpr uint32_t WIX_HEAD_TOP = WIX_HEAD_WORDS - 4;             // inline top-level entries
+constexpr uint32_t WIX_HEAD_LEAF = (WIX_HEAD_WORDS - 8) / 2;      // inline leaf entries (S and col)
+constexpr int WIX_HEAD_NQ = WIX_HEAD_WORDS / 128;                 // uint4 per lane
 
 template <int FL>
 struct WixShape {
