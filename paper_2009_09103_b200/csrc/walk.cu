@@ -1666,8 +1666,10 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         const uint32_t m = static_cast<uint32_t>(b.pool_size);
         const uint32_t nblk = (m + 31) / 32;
         if (nblk <= 64 && !std::getenv("CSAW_MDRW_SLOW")) {   // pools up to 2,048 slots (cfg5: 2,000)
-            const bool packed = g->max_deg < (int64_t(1) << 24) && g->E < (int64_t(1) << 40) &&
-                                !std::getenv("CSAW_MDRW_WIDE");
+            // packed 8 B slot records: opt-in (A/B: same speed in memory, 14 % slower in the OOM
+            // zero-copy mode, where the separate vertex-id load lands on the step's chain)
+            const char* pk = std::getenv("CSAW_MDRW_PACKED");
+            const bool packed = g->max_deg < (int64_t(1) << 24) && g->E < (int64_t(1) << 40) && pk && pk[0] == '1';
             void *pool = nullptr, *pvid = nullptr;
             if (packed) {
                 CSAW_TRY(g->scratch.get(SL_TMP0, sizeof(uint64_t) * n * m, &pool));

@@ -283,7 +283,7 @@ def test_mdrw_pool_sizes(medium, m, n, L):
     G2, og2, g2 = medium
     s = mdrw_seeds(g2, n, m).numpy()
     e = check_mdrw(G2, og2, s, L, rng_seed=7, instances=range(0, n, max(1, n // 40)))
-    for env in ("CSAW_MDRW_SLOW", "CSAW_MDRW_WIDE"):   # large-pool kernel; 16 B slot records
+    for env in ("CSAW_MDRW_SLOW", "CSAW_MDRW_PACKED"):   # large-pool kernel; packed 8 B slot records
         os.environ[env] = "1"
         try:
             e2 = u32(cs.csaw_walk(G2, cs.make_bias("mdrw", pool_size=m), torch.as_tensor(s.view(np.int32)).to(DEV), L,
