@@ -1104,7 +1104,7 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     }
     if (ecap_d > 2048 || n == 0 || depth > 16) return FUSED_FALLBACK;
     const uint32_t ecap = std::max<uint32_t>(1, static_cast<uint32_t>(ecap_d));
-    void *pc, *ps, *pd, *pe, *pk, *pp;
+    void *pc, *ps, *pd, *pe, *pk;
     CSAW_TRY(g->scratch.get(SL_COUNTS, 256, &pc));
     unsigned long long* counters = static_cast<unsigned long long*>(pc);
     unsigned* ovf = reinterpret_cast<unsigned*>(counters + 12);
@@ -1112,7 +1112,6 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     CSAW_TRY(g->scratch.get(SL_SRC + 201, sizeof(uint32_t) * n * ecap, &pd));
     CSAW_TRY(g->scratch.get(SL_SRC + 202, static_cast<size_t>(n) * ecap, &pe));
     CSAW_TRY(g->scratch.get(SL_SRC + 203, sizeof(uint64_t) * n, &pk));
-    CSAW_TRY(g->scratch.get(SL_TMP2, sizeof(uint64_t) * (SCAN_MAX_GRID + 8), &pp));
     void* hmb;
     CSAW_TRY(g->pinned.get(4096, &hmb));
     volatile uint64_t* hbox = static_cast<volatile uint64_t*>(hmb);
