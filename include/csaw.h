@@ -157,6 +157,13 @@ typedef struct {
  * MDRW step reads the new pool vertex's row and VertexBias together with the
  * picked entry instead of one dependent row_ptr lookup later.  Results are identical. */
 #define CSAW_GRAPH_NEXT_META 0x80u
+/* csaw_graph_opts.flags (in-memory graphs; built automatically in out-of-memory mode
+ * when it fits the budget): chunk-total cache of the degree bias -- for every row of more
+ * than 256 candidates, the chunk prefix sums of its CTPS (<= 256 chunks) and its count of
+ * positive-bias candidates, E / 64 + 512 u64 in all.  Degree-biased selections read the
+ * chunk table instead of scanning the whole pool and rescan one chunk per draw.  Results
+ * are identical. */
+#define CSAW_GRAPH_CHUNK_CACHE 0x100u
 
 typedef struct {
     int64_t num_vertices, num_edges;

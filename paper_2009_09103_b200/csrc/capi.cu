@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "select.cuh"
 #include "wix.cuh"
 #include "util.cuh"
 
@@ -513,6 +514,53 @@ static csaw_status build_tri(csaw_graph* g, int blocks) {
     if (h) { cudaFree(g->tri); g->tri = nullptr; }
     return CSAW_OK;
 }
+
+// ---------------------------------------------------------------- chunk-total cache (select.cuh)
+// For every row of d > TAB candidates: the degree-bias chunk prefix sums build_ctps would
+// compute (same chunk size m), then npos, at cc[row start / 64 ...].  Static bias, so
+// degree-biased selections read the chunk table instead of scanning the whole pool and
+// rescan one chunk per draw (bit-identical).  col may be pinned host memory (OOM modes).
+__global__ void k_build_ccache(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                               const uint32_t* __restrict__ deg, int64_t V, uint64_t* __restrict__ cc) {
+    const int lane = lane_id();
+    for (uint64_t v = global_warp_id(); v < static_cast<uint64_t>(V); v += total_warps()) {
+        const int64_t rb = rp[v];
+        const uint32_t d = static_cast<uint32_t>(rp[v + 1] - rb);
+        if (d <= static_cast<uint32_t>(TAB)) continue;
+        const uint32_t nrows = (d + 31) / 32;
+        const uint32_t m = ctps_chunk_rows(nrows);
+        const uint32_t nch = (nrows + m - 1) / m;
+        uint64_t carry = 0;
+        uint32_t npos = 0;
+        uint64_t* out = cc + static_cast<uint64_t>(rb) / 64;
+        for (uint32_t c = 0; c < nch; ++c) {
+            const uint32_t e0 = c * m * 32, e1 = min(d, (c + 1) * m * 32);
+            uint64_t acc = 0;
+            for (uint32_t e = e0 + lane; e < e1; e += 32) {
+                const uint32_t b = deg[col[rb + e]];
+                acc += b;
+                npos += b > 0 ? 1u : 0u;
+            }
+            carry += warp_sum(acc);
+            if (lane == 0) out[c] = carry;
+        }
+        npos = __reduce_add_sync(FULL, npos);
+        if (lane == 0) out[nch] = npos;
+    }
+}
+
+static csaw_status build_ccache(csaw_graph* g, const uint32_t* col, int blocks) {
+    const uint64_t n = static_cast<uint64_t>(g->E) / 64 + 512;
+    if (cudaMalloc(&g->ccache, sizeof(uint64_t) * n) != cudaSuccess) {
+        cudaGetLastError();
+        g->ccache = nullptr;
+        return fail(CSAW_ERR_NO_MEMORY, "cudaMalloc(chunk-total cache)");
+    }
+    cudaMemset(g->ccache, 0, sizeof(uint64_t) * n);
+    if (g->V > 0) k_build_ccache<<<blocks, 256>>>(g->row_ptr, col, g->deg, g->V, g->ccache);
+    g->ccache_entries = n;
+    return CSAW_OK;
+}
 }  // namespace csaw
 
 using namespace csaw;
@@ -618,7 +666,13 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         for (int p = 0; p <= st.P; ++p) st.ebeg[p] = st.h_row[st.bounds[p]];
         for (int p = 0; p < st.P; ++p) maxpe = std::max(maxpe, st.ebeg[p + 1] - st.ebeg[p]);
         st.slot_edges = std::max<int64_t>(maxpe, 1);
-        const int64_t resident_bytes = sizeof(int64_t) * (V + 1) + sizeof(uint32_t) * V;
+        // + the chunk-total cache of the degree bias when it fits (E / 64 + 512 u64)
+        const int64_t cc_bytes = static_cast<int64_t>(sizeof(uint64_t)) * (E / 64 + 512);
+        const int64_t base_resident = sizeof(int64_t) * (V + 1) + sizeof(uint32_t) * V;
+        const int64_t arena0 = static_cast<int64_t>(st.zerocopy ? 1 : st.R) * st.slot_edges *
+                               static_cast<int64_t>(sizeof(uint32_t));
+        st.want_ccache = !std::getenv("CSAW_NO_CCACHE") && base_resident + cc_bytes + arena0 <= st.budget;
+        const int64_t resident_bytes = base_resident + (st.want_ccache ? cc_bytes : 0);
         // the arena holds R partitions; zero-copy mode validates through a 1-partition slot only
         const int64_t arena = static_cast<int64_t>(st.zerocopy ? 1 : st.R) * st.slot_edges *
                               static_cast<int64_t>(sizeof(uint32_t));
@@ -672,6 +726,12 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
     if (hv.bad_col != ~0ull)
         return cleanup(fail(CSAW_ERR_BAD_GRAPH, "col_idx[" + std::to_string(hv.bad_col - 1) + "] >= num_vertices"));
     g->rows_sorted = hv.unsorted == 0;
+    // chunk-total cache of the degree bias: always in OOM mode when it fits the budget (no
+    // per-entry cache does), on request in memory
+    if ((g->oom && g->oomst.want_ccache) || (!g->oom && (o.flags & CSAW_GRAPH_CHUNK_CACHE))) {
+        const csaw_status cs_ = build_ccache(g, g->oom ? g->oomst.h_col : g->col, blocks);
+        if (cs_ != CSAW_OK) return cleanup(cs_);
+    }
     if ((o.flags & CSAW_GRAPH_CTPS_CACHE) && !g->oom) {
         CREATE_CUDA(cudaMalloc(&g->cps, sizeof(uint64_t) * std::max<int64_t>(E, 1)), "cudaMalloc(cps)");
         CREATE_CUDA(cudaMalloc(&g->npos, sizeof(uint32_t) * std::max<int64_t>(V, 1)), "cudaMalloc(npos)");
@@ -752,6 +812,7 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->bt_off) cudaFree(g->bt_off);
     if (g->nmp) cudaFree(g->nmp);
     if (g->c32) cudaFree(g->c32);
+    if (g->ccache) cudaFree(g->ccache);
     if (g->whead) cudaFree(g->whead);
     if (g->tri) cudaFree(g->tri);
     if (g->wcol) cudaFree(g->wcol);
@@ -786,7 +847,8 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
                         (g->wix_leaf ? static_cast<int64_t>(sizeof(uint32_t) * (2 * g->wleaf_entries + g->winn_entries) + sizeof(uint4) * g->V) : 0) +
                         (g->whead ? static_cast<int64_t>(sizeof(uint32_t)) * WIX_HEAD_WORDS * g->V : 0) +
                         (g->tri ? static_cast<int64_t>(sizeof(uint32_t) * g->E) : 0) +
-                        (g->nmp ? static_cast<int64_t>(sizeof(uint64_t) * g->E) : 0);
+                        (g->nmp ? static_cast<int64_t>(sizeof(uint64_t) * g->E) : 0) +
+                        static_cast<int64_t>(sizeof(uint64_t) * g->ccache_entries);
     out->ctps_cache = g->cps ? 1 : 0;
     out->walk_index_leaf = g->wix_leaf;
     out->walk_index_group = g->wix_leaf ? g->wix_group : 0;

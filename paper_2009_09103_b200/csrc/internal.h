@@ -73,6 +73,7 @@ struct OomState {
     int32_t S = 0;                 // streams
     int64_t budget = 0;
     bool zerocopy = false;         // CSAW_GRAPH_OOM_ZEROCOPY: kernels read h_col in place
+    bool want_ccache = false;      // the chunk-total cache fits the budget (built after validation)
     std::vector<int64_t> bounds;   // vertex bounds [P+1]
     std::vector<int64_t> ebeg;     // first edge of partition p
     int64_t slot_edges = 0;        // capacity of an arena slot in col entries
@@ -133,6 +134,8 @@ struct csaw_graph {
     uint32_t* winn = nullptr;     // internal levels (fanout 128), top level first per row
     uint64_t winn_entries = 0;    // size of winn (the records wrec follow it in the same allocation)
     uint64_t wleaf_entries = 0;   // size of c32 / wcol
+    uint64_t* ccache = nullptr;   // chunk-total cache of the degree bias (select.cuh; rows of d > TAB)
+    uint64_t ccache_entries = 0;
     uint32_t* tri = nullptr;      // [E] node2vec: |N(v) ∩ N(u)| per entry (symmetric sorted graphs, cache builds)
     int wix_group = 8;            // lanes per walker in k_walk_wixg (32 = k_walk_wix, one warp per walker)
     int wix_leaf = 0;             // leaf fanout 32 / 64 / 128 (0 = not built)

@@ -460,6 +460,7 @@ struct WalkOomArgs {
     uint32_t* cnt_out;
     unsigned long long* counters;    // [0] scanned, [1] steps
     Owner own;
+    const uint64_t* ccache;          // chunk-total cache (degree pools), optional
 };
 
 __global__ void __launch_bounds__(OOM_WARPS * 32) k_walk_oom_init(WalkOomArgs a, const uint32_t* __restrict__ seeds) {
@@ -502,10 +503,10 @@ __global__ void __launch_bounds__(OOM_WARPS * 32) k_walk_oom_part(WalkOomArgs a,
             if constexpr (kUniform) {
                 nxt = __ldg(colq + b0 + below(U, d));
             } else {
-                DegreePool P{colq, a.deg, static_cast<uint64_t>(b0), d};
+                DegreePool P{colq, a.deg, static_cast<uint64_t>(b0), d, a.ccache};
                 const Ctps C = build_ctps(P, tab);
                 nxt = select_wr(P, C, tab, U);
-                scanned += d;
+                scanned += (a.ccache && C.m) ? 32u * C.m : d;
             }
             ++steps;
             ++t;
@@ -555,6 +556,7 @@ csaw_status run_walk_oom(const csaw_graph* g, const csaw_bias& b, int32_t length
     char* curp = static_cast<char*>(p0);
     auto take = [&](size_t bytes) { char* r = curp; curp += (bytes + 15) / 16 * 16; return static_cast<void*>(r); };
     WalkOomArgs a;
+    a.ccache = g->ccache;
     a.rp = g->row_ptr; a.deg = g->deg; a.n = n; a.L = length; a.ibase = static_cast<uint32_t>(base);
     a.key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     a.path = d_path;

@@ -130,6 +130,7 @@ struct SelArgs {
     uint32_t mode;                   // collision migration (MIGRATE_*)
     const uint32_t* __restrict__ qidx;   // OOM: queue entries of one partition (nullptr = all nq entries)
     uint64_t nidx;
+    const uint64_t* __restrict__ ccache;  // chunk-total cache (degree pools), optional
 };
 
 // Neighbor sampling / forest fire: one warp per queue entry.
@@ -165,10 +166,10 @@ __global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_ns_select(SelArgs a) {
                 cnt = select_wor(P, C, tab, bm, k, dk, a.a_max, gl, emit);
                 probes += P.probes;
             } else if constexpr (kMode == 1) {
-                DegreePool P{a.col, a.deg, static_cast<uint64_t>(b0), n};
+                DegreePool P{a.col, a.deg, static_cast<uint64_t>(b0), n, a.ccache};
                 const Ctps C = build_ctps(P, tab);
                 cnt = select_wor(P, C, tab, bm, k, dk, a.a_max, gl, emit);
-                scanned += n;
+                scanned += (a.ccache && C.m) ? 32u * C.m : n;   // chunk cache: ~one chunk rescanned per pick
             } else {
                 UniformPool P{a.col, static_cast<uint64_t>(b0), n};
                 const Ctps C = build_ctps(P, tab);
@@ -724,6 +725,7 @@ struct FusedArgs {
     uint64_t* offs;                       // [n + 1] exclusive prefix of cnt (caller's offsets)
     unsigned* done;                       // block ticket (zeroed with the counters each call)
     uint64_t* report;                     // pinned host mailbox: flags, total, counters[0..3]
+    const uint64_t* __restrict__ ccache;  // chunk-total cache (degree pools), optional
 };
 
 // Run by the last block of k_sample_fused to finish (ticket): the per-instance edge
@@ -891,10 +893,10 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB :
                         c = select_wor(P, C, tab, bm, k, dk, a.a_max, nullptr, emit);
                         probes += P.probes;
                     } else if constexpr (kMode == 1) {
-                        DegreePool P{a.col, a.deg, static_cast<uint64_t>(b0), nd};
+                        DegreePool P{a.col, a.deg, static_cast<uint64_t>(b0), nd, a.ccache};
                         const Ctps C = build_ctps(P, tab);
                         c = select_wor(P, C, tab, bm, k, dk, a.a_max, nullptr, emit);
-                        scanned += nd;
+                        scanned += (a.ccache && C.m) ? 32u * C.m : nd;
                     } else {
                         UniformPool P{a.col, static_cast<uint64_t>(b0), nd};
                         const Ctps C = build_ctps(P, tab);
@@ -1061,7 +1063,7 @@ static csaw_status oom_select_level(const csaw_graph* g, const csaw_bias& b, con
             const uint32_t* colp = os.d_slots + static_cast<int64_t>(w.slot) * os.slot_edges - os.ebeg[p];
             SelArgs sa{g->row_ptr, colp, g->deg, qv, qi, nq, kq, ub, eoff, s_inst, s_src, s_dst, d, base, key, a_max,
                        glist, kmax, counters, nullptr, nullptr, nullptr, nullptr, static_cast<uint32_t>(b.migration),
-                       idx + off[p], c[p]};
+                       idx + off[p], c[p], g->ccache};
             CSAW_TRY(hot_begin(g, ss));
             if (degree_bias) k_ns_select<1><<<blocks, SEL_WARPS * 32, 0, ss>>>(sa);
             else k_ns_select<0><<<blocks, SEL_WARPS * 32, 0, ss>>>(sa);
@@ -1131,6 +1133,7 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     a.overflow = ovf;
     a.counters = counters;
     a.offs = d_offsets;
+    a.ccache = g->ccache;
     a.done = reinterpret_cast<unsigned*>(counters + 13);   // zeroed by the memset above
     a.report = const_cast<uint64_t*>(hbox);
     a.V = g->V;
@@ -1343,7 +1346,8 @@ csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int
             } else {
                 SelArgs sa{g->row_ptr, colz, g->deg, qv, qi, nq, kq, ub, eoff, s_inst, s_src, s_dst,
                            static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters,
-                           g->cps, g->npos, g->bt, g->bt_off, static_cast<uint32_t>(b.migration), nullptr, 0};
+                           g->cps, g->npos, g->bt, g->bt_off, static_cast<uint32_t>(b.migration), nullptr, 0,
+                           g->ccache};
                 if (degree_bias && g->cps) k_ns_select<2><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
                 else if (degree_bias) k_ns_select<1><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
                 else k_ns_select<0><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);

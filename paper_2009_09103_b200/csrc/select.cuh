@@ -19,6 +19,8 @@
 // locate a draw inside it -- two-level ITS, bit-identical to a flat search.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace csaw {
@@ -58,6 +60,17 @@ struct PickRec {
 //   void seek(uint32_t row0);              // start a sequential run of rows at row0
 //   void load_rows<NR>(row0, key[NR], b[NR]);  // rows row0..row0+NR-1, in increasing order
 //   uint32_t item(uint32_t i) const;       // lane-local random access
+struct DegreePool;
+
+// Chunk-total cache (capi.cu build_ccache): for a row of d > TAB candidates, the chunk
+// prefix sums this scan would produce (same m, same chunks) followed by npos, at
+// ccache[row start / 64 ...].  Rows are disjoint there: the gap to the next row,
+// floor(d / 64), exceeds nch + 1 <= d / 256 + 3 for d > 256.
+__device__ __forceinline__ uint32_t ctps_chunk_rows(uint32_t nrows) {
+    uint32_t m = (nrows + TAB - 1) / TAB;
+    return ((m + U - 1) / U) * U;
+}
+
 template <class Pool>
 __device__ __forceinline__ Ctps build_ctps(Pool& P, uint64_t* __restrict__ tab) {
     const int lane = lane_id();
@@ -94,10 +107,19 @@ __device__ __forceinline__ Ctps build_ctps(Pool& P, uint64_t* __restrict__ tab) 
             }
         }
     } else {
-        uint32_t m = (nrows + TAB - 1) / TAB;
-        m = ((m + U - 1) / U) * U;
+        const uint32_t m = ctps_chunk_rows(nrows);
         c.m = m;
         c.nch = (nrows + m - 1) / m;
+        if constexpr (std::is_same<Pool, DegreePool>::value) {
+            if (P.ccache) {   // static degree bias: the chunk table is read, not scanned
+                const uint64_t* cc = P.ccache + P.beg / 64;
+                for (uint32_t i = lane; i < c.nch; i += 32) tab[i] = __ldg(cc + i);
+                c.T = __ldg(cc + c.nch - 1);
+                c.npos = static_cast<uint32_t>(__ldg(cc + c.nch));
+                __syncwarp();
+                return c;
+            }
+        }
         const uint32_t groups_per_chunk = m / U;
         uint32_t g = 0, chunk = 0;
         uint64_t acc = 0;
@@ -453,6 +475,7 @@ struct DegreePool {
     const uint32_t* __restrict__ deg;
     uint64_t beg;
     uint32_t n;
+    const uint64_t* __restrict__ ccache = nullptr;   // chunk-total cache (rows of d > TAB), optional
     __device__ __forceinline__ void seek(uint32_t) {}
     template <int NR>
     __device__ __forceinline__ void load_rows(uint32_t row0, uint32_t (&key)[NR], uint32_t (&b)[NR]) {

@@ -32,6 +32,7 @@ struct WalkArgs {
     uint2 key;
     uint32_t* __restrict__ path;
     unsigned long long* __restrict__ counters;   // [0] = neighbours scanned, [1] = steps
+    const uint64_t* __restrict__ ccache;          // chunk-total cache (degree pools), optional
 };
 
 // path[w][pi] buffered in lane (pi & 31); flushed when a 32-block completes.
@@ -469,10 +470,10 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkArgs a) {
                     if constexpr (kUniform) {
                         nxt = __ldg(a.col + b0 + below(U, d));
                     } else {
-                        DegreePool P{a.col, a.deg, static_cast<uint64_t>(b0), d};
+                        DegreePool P{a.col, a.deg, static_cast<uint64_t>(b0), d, a.ccache};
                         const Ctps C = build_ctps(P, tab);
                         nxt = select_wr(P, C, tab, U);
-                        scanned += d;
+                        scanned += (a.ccache && C.m) ? 32u * C.m : d;   // chunk cache: one chunk rescanned
                     }
                     ++steps;
                 }
@@ -1605,7 +1606,7 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
     // zero-copy OOM mode: col_idx is read in place from pinned host memory (UVA)
     const uint32_t* colp = g->col ? g->col : g->oomst.h_col;
     WalkArgs a{g->row_ptr, colp, g->deg, d_seeds, static_cast<uint64_t>(n), length,
-               static_cast<uint32_t>(base), key, d_path, static_cast<unsigned long long*>(cnt)};
+               static_cast<uint32_t>(base), key, d_path, static_cast<unsigned long long*>(cnt), g->ccache};
     if (b.kind == CSAW_BIAS_DEGREE && g->wix_leaf) {
         // group kernels: 2-warp blocks, so few walkers (cfg2: 1,000 warps) still spread over all SMs
         const int wpb = g->wix_group == 32 ? WALK_WARPS : 2;
