@@ -1107,7 +1107,17 @@ __device__ uint32_t n2t_scan(const MirList& A, const MirList& B, uint32_t pvk, u
                     tlo = bnext;
                     tn = min(N2T_TILE, B.n - bnext);
                     __syncwarp();
-                    for (uint32_t j = lane; j < tn; j += 32) tile[j] = B.at(tlo + j);
+                    // global -> shared without a register round trip per element: all of the
+                    // lane's copies are in flight at once (cp.async), then mirrored lists are
+                    // complemented in place
+                    for (uint32_t j = lane; j < tn; j += 32) {
+                        const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(tile + j));
+                        const uint32_t* src = B.p + static_cast<int64_t>(B.s) * static_cast<int64_t>(tlo + j);
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src) : "memory");
+                    }
+                    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+                    if (B.m)
+                        for (uint32_t j = lane; j < tn; j += 32) tile[j] ^= B.m;
                     __syncwarp();
                     tmax = tile[tn - 1];
                     tile_ok = true;
