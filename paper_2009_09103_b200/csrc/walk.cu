@@ -1004,6 +1004,42 @@ struct N2tStats {
 // shared-memory tile of B: per lane one binary search for its first key, then a linear
 // merge (B about as dense as A) or galloping searches (B denser); B much longer than A:
 // per-key binary searches of B in global memory.
+// Splitters: every step-th entry of a (mirrored) list staged in shared memory with
+// cp.async (one round trip), so a key's lower bound is narrowed to a window of `step`
+// entries by a shared-memory search before the global binary search (log2(step) round
+// trips instead of log2(n)).
+struct Splitters {
+    uint32_t ns, step;
+};
+__device__ __forceinline__ Splitters stage_splitters(const MirList& L, uint32_t* tile) {
+    const uint32_t lane = static_cast<uint32_t>(lane_id());
+    Splitters sp;
+    sp.step = max(1u, (L.n + N2T_TILE - 1) / N2T_TILE);
+    sp.ns = (L.n + sp.step - 1) / sp.step;
+    __syncwarp();
+    for (uint32_t i = lane; i < sp.ns; i += 32) {
+        const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(tile + i));
+        const uint32_t* src = L.p + static_cast<int64_t>(L.s) * static_cast<int64_t>(i * sp.step);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    if (L.m)
+        for (uint32_t i = lane; i < sp.ns; i += 32) tile[i] ^= L.m;
+    __syncwarp();
+    return sp;
+}
+// [l, h): the lower bound of k in L lies in [l, h] (h when every entry of [l, h) is < k)
+__device__ __forceinline__ void split_window(const uint32_t* tile, const Splitters& sp, uint32_t n, uint32_t k,
+                                             uint32_t& l, uint32_t& h) {
+    uint32_t c = 0;   // splitters < k, in [0, ns] (ns <= N2T_TILE: the first step may take all of them)
+#pragma unroll
+    for (uint32_t s = N2T_TILE; s > 0; s >>= 1)
+        if (c + s <= sp.ns && tile[c + s - 1] < k) c += s;
+    if (c == 0) { l = 0; h = 0; return; }   // L[0] >= k
+    l = (c - 1) * sp.step + 1;
+    h = c < sp.ns ? c * sp.step : n;
+}
+
 // B much shorter than A (N(prev) << N(v)): instead of scanning A, locate the specials --
 // B's members of A (weight w1) and prev (weight wp) -- by searching each B entry in A;
 // between specials S grows by wq per position, so the region follows in closed form.
@@ -1011,9 +1047,10 @@ struct N2tStats {
 // (wq - wp) [p > ppos].  Members come in ascending position (B is sorted), so the walk
 // over B stops at the first member whose S passes xs.
 __device__ uint32_t n2t_specials(const MirList& A, const MirList& B, uint32_t pvk, uint64_t xs, uint32_t wp,
-                                 uint32_t w1, uint32_t wq, N2tStats& st) {
+                                 uint32_t w1, uint32_t wq, uint32_t* tile, N2tStats& st) {
     const uint32_t lane = static_cast<uint32_t>(lane_id());
     const uint32_t ppos = mir_lower_bound(A, 0, A.n, pvk);   // prev is in N(v) (symmetric graph)
+    const Splitters sp = stage_splitters(A, tile);
     // deficits per special (mod 2^64: negative when 1/q < 1 or 1/q < 1/p; S itself is exact)
     const uint64_t dq1 = static_cast<uint64_t>(wq) - w1, dqp = static_cast<uint64_t>(wq) - wp;
     uint32_t j = 0;                 // members seen so far
@@ -1026,15 +1063,16 @@ __device__ uint32_t n2t_specials(const MirList& A, const MirList& B, uint32_t pv
         const uint32_t i = r0 + lane;
         const bool valid = i < B.n;
         const uint32_t b = valid ? B.at(i) : 0u;
-        uint32_t l = 0, h = valid ? A.n : 0u;
-        for (uint32_t span = A.n; span > 0; span >>= 1) {   // same trip count on every lane
+        uint32_t l = 0, h = 0;
+        if (valid) split_window(tile, sp, A.n, b, l, h);
+        for (uint32_t span = sp.step; span > 0; span >>= 1) {   // same trip count on every lane
             if (l < h) {
                 const uint32_t mid = (l + h) >> 1;
                 if (A.at(mid) < b) l = mid + 1; else h = mid;
             }
         }
         const bool mem = valid && l < A.n && A.at(l) == b;
-        st.bkeys += min(32u, B.n - r0) * (32 - __clz(A.n + 1));
+        st.bkeys += min(32u, B.n - r0) * (32 - __clz(sp.step + 1));
         const unsigned mb = __ballot_sync(FULL, mem);
         const uint32_t jj = j + __popc(mb & lanemask_lt());   // members before this one
         const uint64_t S = static_cast<uint64_t>(wq) * l - dq1 * jj - (l > ppos ? dqp : 0);
@@ -1064,13 +1102,14 @@ __device__ uint32_t n2t_specials(const MirList& A, const MirList& B, uint32_t pv
 __device__ uint32_t n2t_scan(const MirList& A, const MirList& B, uint32_t pvk, uint64_t xs, uint32_t wp,
                              uint32_t w1, uint32_t wq, uint32_t* tile, N2tStats& st) {
     const uint32_t lane = static_cast<uint32_t>(lane_id());
-    if (N2T_SPEC_RATIO * B.n < A.n) return n2t_specials(A, B, pvk, xs, wp, w1, wq, st);
+    if (N2T_SPEC_RATIO * B.n < A.n) return n2t_specials(A, B, pvk, xs, wp, w1, wq, tile, st);
     const bool bsearch = B.n > N2T_BS_RATIO * A.n;
     const bool linear = B.n <= 3u * A.n;
     uint64_t acc = 0;
     uint32_t bnext = 0;                     // B entries before bnext are below every key still to come
     uint32_t tlo = 0, tn = 0, tmax = 0;     // tile = B[tlo, tlo + tn)
     bool tile_ok = false;
+    Splitters bsp{0, 1};                    // bsearch mode: splitters of B in the tile
     for (uint32_t c0 = 0; c0 < A.n; c0 += 32 * N2T_K) {
         const uint32_t base = c0 + N2T_K * lane;
         const uint32_t nv = base < A.n ? min(static_cast<uint32_t>(N2T_K), A.n - base) : 0u;   // valid keys of the lane
@@ -1081,10 +1120,14 @@ __device__ uint32_t n2t_scan(const MirList& A, const MirList& B, uint32_t pvk, u
         st.keys += cn;
         uint32_t mem = 0;
         if (bsearch) {
+            if (c0 == 0) bsp = stage_splitters(B, tile);   // once per step (bnext stays 0 in this mode)
             uint32_t l[N2T_K], h[N2T_K];
 #pragma unroll
-            for (int u = 0; u < N2T_K; ++u) { l[u] = bnext; h[u] = static_cast<uint32_t>(u) < nv ? B.n : bnext; }
-            for (uint32_t span = B.n - bnext; span > 0; span >>= 1) {   // same trip count on all lanes
+            for (int u = 0; u < N2T_K; ++u) {
+                l[u] = 0; h[u] = 0;
+                if (static_cast<uint32_t>(u) < nv) split_window(tile, bsp, B.n, k[u], l[u], h[u]);
+            }
+            for (uint32_t span = bsp.step; span > 0; span >>= 1) {   // same trip count on all lanes
 #pragma unroll
                 for (int u = 0; u < N2T_K; ++u) {
                     if (l[u] < h[u]) {
@@ -1096,7 +1139,7 @@ __device__ uint32_t n2t_scan(const MirList& A, const MirList& B, uint32_t pvk, u
 #pragma unroll
             for (int u = 0; u < N2T_K; ++u)
                 if (static_cast<uint32_t>(u) < nv && l[u] < B.n && B.at(l[u]) == k[u]) mem |= 1u << u;
-            st.bkeys += static_cast<unsigned long long>(cn) * (32 - __clz(B.n - bnext + 1));
+            st.bkeys += static_cast<unsigned long long>(cn) * (32 - __clz(bsp.step + 1));
         } else if (bnext < B.n) {
             uint32_t open = 0;
 #pragma unroll
