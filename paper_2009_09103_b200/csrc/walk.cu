@@ -1008,13 +1008,16 @@ struct N2tStats {
 // cp.async (one round trip), so a key's lower bound is narrowed to a window of `step`
 // entries by a shared-memory search before the global binary search (log2(step) round
 // trips instead of log2(n)).
+#ifndef N2T_SPLIT
+#define N2T_SPLIT 256u    // splitters staged per list (<= N2T_TILE; cfg3: 1024: 480, 256: 476, 128: 482 ms)
+#endif
 struct Splitters {
     uint32_t ns, step;
 };
 __device__ __forceinline__ Splitters stage_splitters(const MirList& L, uint32_t* tile) {
     const uint32_t lane = static_cast<uint32_t>(lane_id());
     Splitters sp;
-    sp.step = max(1u, (L.n + N2T_TILE - 1) / N2T_TILE);
+    sp.step = max(1u, (L.n + N2T_SPLIT - 1) / N2T_SPLIT);
     sp.ns = (L.n + sp.step - 1) / sp.step;
     __syncwarp();
     for (uint32_t i = lane; i < sp.ns; i += 32) {
