@@ -140,10 +140,13 @@ typedef struct {
 #define CSAW_GRAPH_OOM_NO_WS 0x8u
 #define CSAW_GRAPH_OOM_NO_BAL 0x10u
 /* csaw_graph_opts.flags, with CSAW_GRAPH_CTPS_CACHE: do not build the narrow walk
- * index (paper_2009_09103_b200/csrc/wix.cuh; one 16 B record per vertex, S as u32,
- * fanout-128 internal nodes, built only when every row total is < 2^32).  Degree
- * walks then search the u64 fanout-32 index instead.  Results are identical
- * either way; this flag exists for tests and A/B measurements. */
+ * index (paper_2009_09103_b200/csrc/wix.cuh; built by default with the cache when
+ * every row total is < 2^32: S as u32 in 128-entry leaves with a col copy, fanout-128
+ * internal nodes, a 16 B record and a 512 B head per vertex -- the head holds the
+ * record and the row's top index level, or the whole row when d <= 60, at v x 512 B).
+ * Degree walks then search the u64 fanout-32 index instead.  Results are identical
+ * either way; this flag exists for tests, A/B measurements and memory savings
+ * (the index costs 8 (E + 3V) + 528 V bytes). */
 #define CSAW_GRAPH_NO_WALK_INDEX 0x20u
 /* csaw_graph_opts.flags (in-memory graphs with sorted rows): build per-edge triangle
  * counts tri[e] = |N(v) ∩ N(u)| for every CSR entry e = (v -> u) (one u32 per entry;
