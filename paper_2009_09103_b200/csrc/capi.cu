@@ -374,8 +374,12 @@ static csaw_status build_wix_t(csaw_graph* g, int blocks) {
         if (cudaMalloc(&g->c32, sizeof(uint32_t) * nl) != cudaSuccess ||
             cudaMalloc(&g->wcol, sizeof(uint32_t) * nl) != cudaSuccess ||
             cudaMalloc(&g->winn, sizeof(uint32_t) * (total + 16) + sizeof(uint4) * std::max<int64_t>(V, 1)) != cudaSuccess) {
+            // the walk index is an accelerator: without memory for it, walks use the u64 index
             cudaGetLastError();
-            s = fail(CSAW_ERR_NO_MEMORY, "cudaMalloc(walk index)");
+            if (g->c32) cudaFree(g->c32);
+            if (g->wcol) cudaFree(g->wcol);
+            if (g->winn) cudaFree(g->winn);
+            g->c32 = g->wcol = g->winn = nullptr;
         } else {
             cudaMemset(g->c32, 0, sizeof(uint32_t) * nl);   // padding entries (read, then masked)
             cudaMemset(g->wcol, 0, sizeof(uint32_t) * nl);
