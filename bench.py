@@ -353,7 +353,7 @@ def main():
         use_tri = (not args.no_cache) and cfg.workload == "node2vec"   # node2vec edge triangle counts
         use_meta = (not args.no_cache) and cfg.workload == "mdrw"   # next-vertex metadata per entry
         G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache, node2vec_tri=use_tri,
-                                 next_meta=use_meta, walk_index=(cfg.workload == "walk"))   # walk index: walks only
+                                 next_meta=use_meta, walk_index=use_cache)   # walk index + vertex heads
     ginfo = G.info()
     bias = bias_of(cs, cfg)
     stream = torch.cuda.current_stream(dev)

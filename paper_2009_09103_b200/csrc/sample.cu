@@ -131,6 +131,7 @@ struct SelArgs {
     const uint32_t* __restrict__ qidx;   // OOM: queue entries of one partition (nullptr = all nq entries)
     uint64_t nidx;
     const uint64_t* __restrict__ ccache;  // chunk-total cache (degree pools), optional
+    WixPtrs wx;                           // vertex heads (cached degree pools), optional
 };
 
 // Neighbor sampling / forest fire: one warp per queue entry.
@@ -161,7 +162,9 @@ __global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_ns_select(SelArgs a) {
         if (n > 0 && k > 0) {
             if constexpr (kMode == 2) {
                 CachedDegreePool P{a.col, a.cps, static_cast<uint64_t>(b0), n, __ldg(a.npos + v), 0, a.bt,
-                                   __ldg(a.bt_off + v)};
+                                   a.wx.head ? 0 : __ldg(a.bt_off + v)};
+                P.wx = a.wx;
+                P.vid = v;
                 const Ctps C = build_ctps(P, tab);
                 cnt = select_wor(P, C, tab, bm, k, dk, a.a_max, gl, emit);
                 probes += P.probes;
@@ -207,6 +210,7 @@ struct LayerPoolT {
     const uint32_t* __restrict__ npos;   // positive-bias neighbours per row (kCache)
     const uint64_t* __restrict__ bt;     // B-tree index over cps (kCache)
     const uint64_t* __restrict__ bt_off;
+    WixPtrs wx{};                        // vertex heads (optional; kCache)
     const uint32_t* fv;                  // frontier vertices of the instance (global or shared)
     const uint64_t* pref;                // exclusive prefix of frontier degrees (global or shared)
     uint64_t pbase;                      // pref at the instance's first segment
@@ -313,6 +317,17 @@ struct LayerPoolT {
             base = __shfl_sync(FULL, incl, 31);
         }
         const uint32_t v = fv[js];
+        if (wx.head) {   // vertex head -> (node) -> leaf; S < 2^32 for every row
+            uint32_t s, lo, b, it, nb;
+            wix_head_search<128>(wx.head, wx.c32, wx.col, wx.inn, v, static_cast<uint32_t>(x - O), s, lo, b, it, nb);
+            probes += nb / 8;   // in 8 B cache-entry units (statistics)
+            Region r;
+            r.s = static_cast<uint32_t>((pref[js] - pbase) + s);
+            r.lo = O + lo;
+            r.b = b;
+            r.item = it;
+            return r;
+        }
         const int64_t ra = __ldg(rp + v), rb = __ldg(rp + v + 1);
         CpsTree t{cps, bt, col, static_cast<uint64_t>(ra), static_cast<uint32_t>(rb - ra), __ldg(bt_off + v)};
         uint64_t xl = x - O, T = 0, e = 0, lo = 0, hi = 0;
@@ -391,6 +406,7 @@ struct LayerArgs {
     const uint64_t* __restrict__ bt;
     const uint64_t* __restrict__ bt_off;
     uint32_t mode;
+    WixPtrs wx;                          // vertex heads, optional
 };
 
 // one warp per instance (its layer pool); kCache: union CTPS from the static-bias cache
@@ -411,7 +427,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_layer_select(LayerArgs a)
         uint32_t cnt = 0;
         if (qe > qb && ub > 0) {
             LayerPoolT<kCache> P;
-            P.rp = a.rp; P.col = a.col; P.deg = a.deg; P.cps = a.cps; P.npos = a.npos; P.probes = 0;
+            P.rp = a.rp; P.col = a.col; P.deg = a.deg; P.cps = a.cps; P.npos = a.npos; P.probes = 0; P.wx = a.wx;
             P.bt = a.bt; P.bt_off = a.bt_off;
             P.fv = a.qv + qb;
             P.pref = a.qpref + qb;
@@ -726,6 +742,7 @@ struct FusedArgs {
     unsigned* done;                       // block ticket (zeroed with the counters each call)
     uint64_t* report;                     // pinned host mailbox: flags, total, counters[0..3]
     const uint64_t* __restrict__ ccache;  // chunk-total cache (degree pools), optional
+    WixPtrs wx;                           // vertex heads (cached degree / layer pools), optional
 };
 
 // Run by the last block of k_sample_fused to finish (ticket): the per-instance edge
@@ -860,7 +877,7 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB :
                 if (pn > 0 && k > 0) {
                     if (ec + min(k, pn) > a.ecap) { ovf = true; break; }
                     LayerPoolT<kMode == 5> P;
-                    P.rp = a.rp; P.col = a.col; P.deg = a.deg; P.cps = a.cps; P.npos = a.npos; P.probes = 0;
+                    P.rp = a.rp; P.col = a.col; P.deg = a.deg; P.cps = a.cps; P.npos = a.npos; P.probes = 0; P.wx = a.wx;
                     P.bt = a.bt; P.bt_off = a.bt_off;
                     P.fv = F; P.pref = PF; P.pbase = 0; P.nf = nf; P.n = pn;
                     DrawKey dk{a.key, inst, static_cast<uint32_t>(d), NONE, a.mode, 0};
@@ -888,7 +905,9 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB :
                     uint32_t c;
                     if constexpr (kMode == 2) {
                         CachedDegreePool P{a.col, a.cps, static_cast<uint64_t>(b0), nd, __ldg(a.npos + v), 0, a.bt,
-                                           __ldg(a.bt_off + v)};
+                                           a.wx.head ? 0 : __ldg(a.bt_off + v)};
+                        P.wx = a.wx;
+                        P.vid = v;
                         const Ctps C = build_ctps(P, tab);
                         c = select_wor(P, C, tab, bm, k, dk, a.a_max, nullptr, emit);
                         probes += P.probes;
@@ -1063,7 +1082,7 @@ static csaw_status oom_select_level(const csaw_graph* g, const csaw_bias& b, con
             const uint32_t* colp = os.d_slots + static_cast<int64_t>(w.slot) * os.slot_edges - os.ebeg[p];
             SelArgs sa{g->row_ptr, colp, g->deg, qv, qi, nq, kq, ub, eoff, s_inst, s_src, s_dst, d, base, key, a_max,
                        glist, kmax, counters, nullptr, nullptr, nullptr, nullptr, static_cast<uint32_t>(b.migration),
-                       idx + off[p], c[p], g->ccache};
+                       idx + off[p], c[p], g->ccache, WixPtrs{}};
             CSAW_TRY(hot_begin(g, ss));
             if (degree_bias) k_ns_select<1><<<blocks, SEL_WARPS * 32, 0, ss>>>(sa);
             else k_ns_select<0><<<blocks, SEL_WARPS * 32, 0, ss>>>(sa);
@@ -1085,6 +1104,15 @@ static csaw_status oom_select_level(const csaw_graph* g, const csaw_bias& b, con
 // Fused path: returns CSAW_OK when done, CSAW_ERR_CAPACITY / OUT_OF_RANGE as usual, and
 // FUSED_FALLBACK when the batched level-synchronous driver must run instead.
 constexpr csaw_status FUSED_FALLBACK = static_cast<csaw_status>(-1);
+
+// vertex heads usable by the cached sampling pools (leaf fanout 128 only)
+static WixPtrs wix_ptrs(const csaw_graph* g) {
+    WixPtrs w;
+    if (g->whead && g->wix_leaf == 128 && !std::getenv("CSAW_SAMPLE_NO_HEADS")) {
+        w.head = g->whead; w.c32 = g->c32; w.col = g->wcol; w.inn = g->winn;
+    }
+    return w;
+}
 
 static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
                                     const uint32_t* d_seeds, uint64_t n, uint64_t base, uint64_t seed,
@@ -1134,6 +1162,7 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     a.counters = counters;
     a.offs = d_offsets;
     a.ccache = g->ccache;
+    a.wx = wix_ptrs(g);
     a.done = reinterpret_cast<unsigned*>(counters + 13);   // zeroed by the memset above
     a.report = const_cast<uint64_t*>(hbox);
     a.V = g->V;
@@ -1340,14 +1369,14 @@ csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int
             if (layer) {
                 LayerArgs la{g->row_ptr, colz, g->deg, qv, inst_off, qpref, n, fan, ub, eoff, s_inst, s_src, s_dst,
                              static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters,
-                             g->cps, g->npos, g->bt, g->bt_off, static_cast<uint32_t>(b.migration)};
+                             g->cps, g->npos, g->bt, g->bt_off, static_cast<uint32_t>(b.migration), wix_ptrs(g)};
                 if (g->cps) k_layer_select<true><<<sgrid, SEL_WARPS * 32, 0, st>>>(la);
                 else k_layer_select<false><<<sgrid, SEL_WARPS * 32, 0, st>>>(la);
             } else {
                 SelArgs sa{g->row_ptr, colz, g->deg, qv, qi, nq, kq, ub, eoff, s_inst, s_src, s_dst,
                            static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters,
                            g->cps, g->npos, g->bt, g->bt_off, static_cast<uint32_t>(b.migration), nullptr, 0,
-                           g->ccache};
+                           g->ccache, wix_ptrs(g)};
                 if (degree_bias && g->cps) k_ns_select<2><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
                 else if (degree_bias) k_ns_select<1><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
                 else k_ns_select<0><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);

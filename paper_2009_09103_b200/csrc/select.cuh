@@ -22,6 +22,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "wix.cuh"
 
 namespace csaw {
 
@@ -584,6 +585,15 @@ struct CpsTree {
 // reading R25): cps[beg + i] = S_{i+1}.  T is one load; a draw is located by a
 // 32-ary warp search of the cached prefix (O(log32 d) round trips) -- the same
 // integer S as DegreePool's scan, hence the same picks.
+// The narrow walk index's vertex heads (wix.cuh), when built with leaf fanout 128: cached
+// degree selections search them (head -> (node) -> leaf) instead of the u64 B-tree.
+struct WixPtrs {
+    const uint32_t* head = nullptr;
+    const uint32_t* c32 = nullptr;
+    const uint32_t* col = nullptr;
+    const uint32_t* inn = nullptr;
+};
+
 struct CachedDegreePool {
     static constexpr bool kClosedForm = false;
     static constexpr bool kCached = true;
@@ -595,9 +605,19 @@ struct CachedDegreePool {
     uint32_t probes;      // cache loads issued (statistics)
     const uint64_t* __restrict__ bt;   // B-tree index (CpsTree)
     uint64_t boff;
+    WixPtrs wx{};                      // vertex heads (optional)
+    uint32_t vid = 0;                  // the pool's vertex (head address)
     __device__ __forceinline__ uint64_t total() const { return n ? __ldg(cps + beg + n - 1) : 0; }
     __device__ __forceinline__ uint32_t npos_count() const { return np; }
     __device__ __forceinline__ Region search(uint64_t x) {
+        if (wx.head) {   // T < 2^32 for every row when the heads exist
+            uint32_t s, lo, b, it, nb;
+            wix_head_search<128>(wx.head, wx.c32, wx.col, wx.inn, vid, static_cast<uint32_t>(x), s, lo, b, it, nb);
+            probes += nb / 8;   // in 8 B cache-entry units (statistics)
+            Region r;
+            r.s = s; r.lo = lo; r.b = b; r.item = it;
+            return r;
+        }
         CpsTree t{cps, bt, col, beg, n, boff};
         uint64_t T = 0, e = 0, lo = 0, hi = 0;
         uint32_t item = NONE;

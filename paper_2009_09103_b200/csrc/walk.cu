@@ -104,35 +104,6 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_cached(WalkArgs a, 
 }
 
 // ---------------------------------------------------------------- narrow walk index (wix.cuh)
-// Entries base[q * 32 + lane], q < N, of one node / leaf block; entries past cnt read as
-// 0xFFFFFFFF, which is above every draw (x < T <= 2^32 - 1).
-template <int N>
-__device__ __forceinline__ void wix_load(const uint32_t* __restrict__ p, uint32_t cnt, uint32_t (&v)[N]) {
-    const uint32_t lane = static_cast<uint32_t>(lane_id());
-#pragma unroll
-    for (int q = 0; q < N; ++q) v[q] = q * 32 + lane < cnt ? __ldg(p + q * 32 + lane) : 0xFFFFFFFFu;
-}
-template <int N>
-__device__ __forceinline__ uint32_t wix_pick(const uint32_t (&v)[N], uint32_t q) {
-    uint32_t r = v[0];
-#pragma unroll
-    for (int i = 1; i < N; ++i) if (q == static_cast<uint32_t>(i)) r = v[i];
-    return r;
-}
-// entry i of the block (all lanes)
-template <int N>
-__device__ __forceinline__ uint32_t wix_entry(const uint32_t (&v)[N], uint32_t i) {
-    return __shfl_sync(FULL, wix_pick(v, i >> 5), i & 31);
-}
-// number of entries <= x = position of the first entry > x (the block is sorted)
-template <int N>
-__device__ __forceinline__ uint32_t wix_rank(const uint32_t (&v)[N], uint32_t x) {
-    uint32_t c = 0;
-#pragma unroll
-    for (int q = 0; q < N; ++q) c += v[q] <= x ? 1u : 0u;
-    return __reduce_add_sync(FULL, c);
-}
-
 // Degree-biased walk over the narrow index, one warp per walker: per step one 16 B
 // vertex record (with T, so the draw x is ready before the first node arrives), K <= 4 internal 512 B nodes (K = 0 for d <= FL, 1 for d <= 128 FL) and
 // one leaf block with its col entries (4 strided u32 loads per lane and node).  The
@@ -197,11 +168,6 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_wix(WalkArgs a, con
         if (bytes) atomicAdd(a.counters + 3, bytes);
         if (steps) atomicAdd(a.counters + 1, steps);
     }
-}
-
-// uint4 component c (0..3) of q, c warp-uniform or per lane
-__device__ __forceinline__ uint32_t u4_at(const uint4& q, uint32_t c) {
-    return c == 0 ? q.x : c == 1 ? q.y : c == 2 ? q.z : q.w;
 }
 
 // Degree-biased walk over the vertex heads (wix.cuh): a step is one coalesced 512 B head

@@ -30,6 +30,8 @@
 
 #include <cstdint>
 
+#include "common.cuh"
+
 namespace csaw {
 
 constexpr int WIX_NODE = 128;   // internal fanout
@@ -85,5 +87,119 @@ struct WixShape {
 #endif
     }
 };
+
+// Entries base[q * 32 + lane], q < N, of one node / leaf block; entries past cnt read as
+// 0xFFFFFFFF, which is above every draw (x < T <= 2^32 - 1).
+template <int N>
+__device__ __forceinline__ void wix_load(const uint32_t* __restrict__ p, uint32_t cnt, uint32_t (&v)[N]) {
+    const uint32_t lane = static_cast<uint32_t>(lane_id());
+#pragma unroll
+    for (int q = 0; q < N; ++q) v[q] = q * 32 + lane < cnt ? __ldg(p + q * 32 + lane) : 0xFFFFFFFFu;
+}
+template <int N>
+__device__ __forceinline__ uint32_t wix_pick(const uint32_t (&v)[N], uint32_t q) {
+    uint32_t r = v[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) if (q == static_cast<uint32_t>(i)) r = v[i];
+    return r;
+}
+// entry i of the block (all lanes)
+template <int N>
+__device__ __forceinline__ uint32_t wix_entry(const uint32_t (&v)[N], uint32_t i) {
+    return __shfl_sync(FULL, wix_pick(v, i >> 5), i & 31);
+}
+// number of entries <= x = position of the first entry > x (the block is sorted)
+template <int N>
+__device__ __forceinline__ uint32_t wix_rank(const uint32_t (&v)[N], uint32_t x) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < N; ++q) c += v[q] <= x ? 1u : 0u;
+    return __reduce_add_sync(FULL, c);
+}
+
+// uint4 component c (0..3) of q, c warp-uniform or per lane
+__device__ __forceinline__ uint32_t u4_at(const uint4& q, uint32_t c) {
+    return c == 0 ? q.x : c == 1 ? q.y : c == 2 ? q.z : q.w;
+}
+
+
+// Warp-collective search of row v for the draw x (< T): the region s with S_s <= x <
+// S_{s+1}, through the vertex head (record + top level, or the inline row), the
+// remaining internal nodes and one leaf.  Returns s, S_s (lo), b_s = S_{s+1} - S_s and
+// col[s] -- what a without-replacement selection needs (BRS works on lo and b) -- and the
+// bytes the search read.
+template <int FL>
+__device__ __forceinline__ void wix_head_search(const uint32_t* __restrict__ head, const uint32_t* __restrict__ c32p,
+                                                const uint32_t* __restrict__ colp, const uint32_t* __restrict__ inn,
+                                                uint32_t v, uint32_t x, uint32_t& s, uint32_t& lo, uint32_t& b,
+                                                uint32_t& item, uint32_t& nbytes) {
+    static_assert(WIX_HEAD_NQ == 1, "512 B heads");
+    using W = WixShape<FL>;
+    constexpr int NL = FL / 32;
+    const uint32_t lane = static_cast<uint32_t>(lane_id());
+    const uint4* hp = reinterpret_cast<const uint4*>(head + static_cast<uint64_t>(v) * WIX_HEAD_WORDS);
+    const uint4 q = __ldg(hp + lane), hd = __ldg(hp);
+    const uint32_t d = hd.x, p = hd.z, io = hd.w;
+    auto head_entry = [&](uint32_t e) { return __shfl_sync(FULL, u4_at(q, e & 3), 1 + (e >> 2)); };
+    auto head_rank = [&](uint32_t n) {
+        uint32_t c = 0;
+        if (lane >= 1) {
+            const uint32_t e0 = 4 * (lane - 1);
+            c = (e0 < n && q.x <= x) + (e0 + 1 < n && q.y <= x) + (e0 + 2 < n && q.z <= x) + (e0 + 3 < n && q.w <= x);
+        }
+        return __reduce_add_sync(FULL, c);
+    };
+    const int K = W::levels(d);
+    nbytes = 4 * WIX_HEAD_WORDS;
+    if (K == 0 && d <= WIX_HEAD_LEAF) {
+        const uint32_t r = head_rank(d);
+        const uint32_t hi = head_entry(r);
+        lo = head_entry(r > 0 ? r - 1 : 0);
+        if (r == 0) lo = 0;
+        b = hi - lo;
+        item = head_entry(WIX_HEAD_LEAF + r);
+        s = r;
+        return;
+    }
+    uint32_t j = 0, left = 0;
+    uint64_t off = io;
+    int k = K;
+    if (K > 0) {
+        const uint32_t nK = W::count(d, K);
+        if (nK <= WIX_HEAD_TOP) {
+            const uint32_t r = head_rank(nK);
+            const uint32_t lv = head_entry(r > 0 ? r - 1 : 0);
+            if (r > 0) left = lv;
+            j = r;
+            off += W::round4(nK);
+            --k;
+        }
+    }
+    for (; k >= 1; --k) {
+        const uint32_t nk = W::count(d, k);
+        const uint32_t cnt = min(static_cast<uint32_t>(WIX_NODE), nk - j * WIX_NODE);
+        uint32_t vv[WIX_NODE / 32];
+        wix_load(inn + off + static_cast<uint64_t>(j) * WIX_NODE, cnt, vv);
+        nbytes += 4 * cnt;
+        const uint32_t r = wix_rank(vv, x);
+        const uint32_t lv = wix_entry(vv, r > 0 ? r - 1 : 0);
+        if (r > 0) left = lv;
+        j = j * WIX_NODE + r;
+        off += W::round4(nk);
+    }
+    const uint64_t lb = static_cast<uint64_t>(p) + static_cast<uint64_t>(j) * FL;
+    const uint32_t cnt = min(static_cast<uint32_t>(FL), d - j * FL);
+    uint32_t sv[NL], cv[NL];
+    wix_load(c32p + lb, cnt, sv);
+    wix_load(colp + lb, cnt, cv);
+    nbytes += 8 * cnt;
+    const uint32_t r = wix_rank(sv, x);
+    const uint32_t hi = wix_entry(sv, r);
+    const uint32_t lv = wix_entry(sv, r > 0 ? r - 1 : 0);
+    lo = r > 0 ? lv : left;
+    b = hi - lo;
+    item = wix_entry(cv, r);
+    s = j * FL + r;
+}
 
 }  // namespace csaw

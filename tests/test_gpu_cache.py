@@ -104,3 +104,21 @@ def test_cfg2_cached_full():
     for w in (0, 1, 1000, 2047, 3999):
         assert np.array_equal(path[w], O.walk(og, O.KIND_DEGREE, cfg.length, int(sv[w]), w, 1)), w
     G.close()
+
+
+@pytest.mark.parametrize("heads", [True, False])
+def test_cached_sampling_heads_vs_btree(hubc, heads):
+    """Cached degree / layer pools search the vertex heads (wix.cuh) when the walk index
+    exists; CSAW_SAMPLE_NO_HEADS=1 forces the u64 B-tree.  Both bit-exact."""
+    import os
+    G, og = hubc
+    assert G.info()["walk_index_heads"] == 1
+    seeds = np.array([0, 1, 0, 1, 5, 0, 1, 17, 299_999, 20_000], dtype=np.uint32)
+    if not heads:
+        os.environ["CSAW_SAMPLE_NO_HEADS"] = "1"
+    try:
+        check_sample(G, og, "degree", seeds, fanout=[30, 3], rng_seed=41)
+        check_sample(G, og, "degree", seeds, fanout=[3, 2], rng_seed=42, a_max=2)
+        check_sample(G, og, "layer", seeds, fanout=[3, 4], rng_seed=43)
+    finally:
+        os.environ.pop("CSAW_SAMPLE_NO_HEADS", None)
