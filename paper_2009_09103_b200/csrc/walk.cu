@@ -1468,7 +1468,10 @@ __global__ void k_mdrw(MdrwArgs a) {
 // refilled every 32 steps; the neighbour and its row are loaded by every lane (broadcast
 // loads) so no lane-0 section and no result shuffles remain.  Same x, same slot, same
 // neighbour as k_mdrw and the oracle (bit-identical).
-constexpr int MDRW_WARPS = 4;
+#ifndef MDRW_WARPS_N
+#define MDRW_WARPS_N 4
+#endif
+constexpr int MDRW_WARPS = MDRW_WARPS_N;   // warps per block; 28 warps / SM at 72 registers
 __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v) {
     const int lane = lane_id();
 #pragma unroll
@@ -1485,7 +1488,7 @@ __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v) {
 // array read only for the output, off the step's dependent chain; the per-step block read
 // is 256 B instead of 512 B and the pool state (n x m x 8 B) is more L2-resident.
 template <bool kNarrow, bool kPacked>
-__global__ void __launch_bounds__(MDRW_WARPS * 32, 7) k_mdrw_fast(MdrwArgs a, uint4* __restrict__ pool,
+__global__ void __launch_bounds__(MDRW_WARPS * 32, 28 / MDRW_WARPS) k_mdrw_fast(MdrwArgs a, uint4* __restrict__ pool,
                                                                  uint64_t* __restrict__ prec, uint32_t* __restrict__ pvid) {
     const int lane = lane_id();
     const uint32_t m = static_cast<uint32_t>(a.m);
@@ -1704,7 +1707,7 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
                         static_cast<uint32_t>(base), key, d_path, nullptr, nullptr, nullptr, nullptr, 0, WALK_WARPS,
                         g->col ? g->col : g->oomst.d_colc,
                         static_cast<uint64_t>(g->col ? g->E : g->oomst.colc_n), g->col ? g->nmp : nullptr};
-            const int64_t warps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 7 * MDRW_WARPS);
+            const int64_t warps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 28);
             const int mg = static_cast<int>((warps + MDRW_WARPS - 1) / MDRW_WARPS);
             uint4* p4 = static_cast<uint4*>(pool);
             uint64_t* p8 = static_cast<uint64_t*>(pool);
