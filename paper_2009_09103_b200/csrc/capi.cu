@@ -1057,11 +1057,12 @@ CSAW_API csaw_status csaw_sample(const csaw_graph* g, const csaw_bias* bias, con
         po.dst = static_cast<uint32_t*>(pinned_device_ptr(dst));
         po.dep = static_cast<uint8_t*>(pinned_device_ptr(edge_depth));
     }
-    const bool all_pinned = po.src && po.dst && po.dep;
+    if (!offs_dev) po.offs = static_cast<uint64_t*>(pinned_device_ptr(offsets));
+    const bool any_pinned = (po.src && po.dst && po.dep) || po.offs;
     csaw_status s = run_sample(g, b, fanout, depth, d_seeds, n, instance_base, rng_seed, d_offs, src, dst,
-                               edge_depth, capacity, num_edges, out_dev, st, all_pinned ? &po : nullptr);
+                               edge_depth, capacity, num_edges, out_dev, st, any_pinned ? &po : nullptr);
     if (s != CSAW_OK && s != CSAW_ERR_CAPACITY) return s;
-    if (!offs_dev) {
+    if (!offs_dev && !po.offs_done) {
         CSAW_CUDA(cudaMemcpyAsync(offsets, d_offs, sizeof(uint64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
         CSAW_CUDA(cudaStreamSynchronize(st));
     }

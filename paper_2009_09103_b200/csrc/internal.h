@@ -187,11 +187,13 @@ struct PinnedOut {
     uint32_t* src;
     uint32_t* dst;
     uint8_t* dep;
+    uint64_t* offs = nullptr;     // pinned host offsets (device-mapped), or nullptr
+    bool offs_done = false;       // set when the fused sampler wrote them directly
 };
 csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
                        const uint32_t* d_seeds, int64_t n, uint64_t base, uint64_t seed, uint64_t* d_offsets,
                        uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
-                       bool out_on_device, cudaStream_t st, const PinnedOut* pinned = nullptr);
+                       bool out_on_device, cudaStream_t st, PinnedOut* pinned = nullptr);
 csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
                               const uint32_t* d_seeds, int64_t n, uint64_t base, uint64_t seed, uint64_t* d_offsets,
                               uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,

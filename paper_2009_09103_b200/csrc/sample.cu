@@ -739,6 +739,7 @@ struct FusedArgs {
     uint32_t mode;
     // epilogue (last block to finish): offsets scan + the host report
     uint64_t* offs;                       // [n + 1] exclusive prefix of cnt (caller's offsets)
+    uint64_t* offs_host;                  // optional pinned host copy (device-mapped), written alongside
     unsigned* done;                       // block ticket (zeroed with the counters each call)
     uint64_t* report;                     // pinned host mailbox: flags, total, counters[0..3]
     const uint64_t* __restrict__ ccache;  // chunk-total cache (degree pools), optional
@@ -780,12 +781,16 @@ __device__ void fused_epilogue(const FusedArgs& a) {
         for (int u = 0; u < 8; ++u) c[u] = i0 + u < b1 ? __ldcg(a.cnt + i0 + u) : 0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            if (i0 + u < b1) a.offs[i0 + u] = run;
+            if (i0 + u < b1) {
+                a.offs[i0 + u] = run;
+                if (a.offs_host) a.offs_host[i0 + u] = run;
+            }
             run += c[u];
         }
     }
     if (threadIdx.x == 0) {
         a.offs[n] = total;
+        if (a.offs_host) a.offs_host[n] = total;
         a.report[0] = *reinterpret_cast<volatile unsigned*>(a.overflow);
         a.report[1] = total;
         for (int k = 0; k < 4; ++k) a.report[2 + k] = reinterpret_cast<volatile unsigned long long*>(a.counters)[k];
@@ -1117,7 +1122,8 @@ static WixPtrs wix_ptrs(const csaw_graph* g) {
 static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
                                     const uint32_t* d_seeds, uint64_t n, uint64_t base, uint64_t seed,
                                     uint64_t* d_offsets, uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity,
-                                    int64_t* num_edges, bool out_on_device, cudaStream_t st) {
+                                    int64_t* num_edges, bool out_on_device, cudaStream_t st,
+                                    uint64_t* offs_host = nullptr) {
     const bool layer = b.kind == CSAW_BIAS_LAYER;
     const bool ff = b.kind == CSAW_BIAS_FOREST_FIRE;
     // per-instance staging capacity from the fanouts (forest fire: a fixed budget)
@@ -1161,6 +1167,7 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     a.overflow = ovf;
     a.counters = counters;
     a.offs = d_offsets;
+    a.offs_host = offs_host;
     a.ccache = g->ccache;
     a.wx = wix_ptrs(g);
     a.done = reinterpret_cast<unsigned*>(counters + 13);   // zeroed by the memset above
@@ -1228,16 +1235,20 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
 csaw_status run_sample(const csaw_graph* g, const csaw_bias& b, const int32_t* fanout, int32_t depth,
                        const uint32_t* d_seeds, int64_t n_i64, uint64_t base, uint64_t seed, uint64_t* d_offsets,
                        uint32_t* src, uint32_t* dst, uint8_t* dep, int64_t capacity, int64_t* num_edges,
-                       bool out_on_device, cudaStream_t st, const PinnedOut* pinned) {
+                       bool out_on_device, cudaStream_t st, PinnedOut* pinned) {
     if (!g->force_batched && (!g->oom || g->oomst.zerocopy) && b.kind != CSAW_BIAS_SNOWBALL) {
         // pinned host outputs: the fused copy writes each instance's contiguous segment over the
         // host link (coalesced), so no staging and no copy after the kernels
-        const bool direct = !out_on_device && pinned != nullptr;
+        const bool direct = !out_on_device && pinned != nullptr && pinned->src && pinned->dst && pinned->dep;
+        uint64_t* offs_host = pinned ? pinned->offs : nullptr;
         const csaw_status s = run_sample_fused(g, b, fanout, depth, d_seeds, static_cast<uint64_t>(n_i64), base, seed,
                                                d_offsets, direct ? pinned->src : src, direct ? pinned->dst : dst,
                                                direct ? pinned->dep : dep, capacity, num_edges,
-                                               out_on_device || direct, st);
-        if (s != FUSED_FALLBACK) return s;
+                                               out_on_device || direct, st, offs_host);
+        if (s != FUSED_FALLBACK) {
+            if (offs_host) pinned->offs_done = true;
+            return s;
+        }
     }
     return run_sample_levels(g, b, fanout, depth, d_seeds, n_i64, base, seed, d_offsets, src, dst, dep, capacity,
                              num_edges, out_on_device, st);
