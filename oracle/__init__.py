@@ -58,6 +58,7 @@ def lib():
             "oracle_walk_variant_step": (u32, [P, P, i64, i32, f64, u32, u32, u32, u32, u64]),
             "oracle_walk_variant": (None, [P, P, i64, i32, f64, i32, u32, u32, u64, P]),
             "oracle_n2v_scale": (u32, [f64, f64]),
+            "oracle_select_float": (i64, [P, i64, u64, P]),
             "oracle_node2vec_step": (u32, [P, P, i64, f64, f64, u32, u32, u32, u32, u64, P]),
             "oracle_node2vec": (None, [P, P, i64, f64, f64, i32, u32, u32, u64, P, P]),
             "oracle_mdrw": (None, [P, P, i64, P, i32, i32, u32, u64, P]),
@@ -149,6 +150,14 @@ def ff_theta(pf: float) -> int:
 
 def ff_burn(seed, inst, depth, v, deg, pf) -> int:
     return int(lib().oracle_ff_burn(seed, inst, depth, v, deg, pf))
+
+
+def select_float(b, U: int):
+    """Float-bias ITS (R28): -> (s, margin); s = -1 if the pool total is 0."""
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float32))
+    m = np.zeros(1, dtype=np.float64)
+    s = lib().oracle_select_float(_p(b), b.size, U, _p(m))
+    return int(s), float(m[0])
 
 
 def n2v_scale(p, q) -> int:
@@ -288,3 +297,50 @@ def parallel_walks(g: Graph, kind, length, seeds, instance_base, rng_seed, worke
                              initializer=_init_pool, initargs=(g,)) as ex:
         res = list(ex.map(_walk_job, jobs))
     return np.stack([p for r in res for p in r]) if n else np.zeros((0, length + 1), np.uint32)
+
+
+def _run_job(args):
+    """One chunk of independent instances (fork worker; the graph is inherited)."""
+    workload, params, ids, seeds, instance_base, rng_seed = args
+    out = []
+    for i, s in zip(ids, seeds):
+        gi = instance_base + int(i)
+        if workload == "walk":
+            out.append(walk(_G, params["kind"], params["length"], int(s), gi, rng_seed))
+        elif workload == "node2vec":
+            out.append(node2vec(_G, params["p"], params["q"], params["length"], int(s), gi, rng_seed))
+        elif workload == "mdrw":
+            out.append(mdrw(_G, s, params["length"], gi, rng_seed))
+        elif workload == "layer":
+            out.append(layer_sample(_G, params["fanout"], params["depth"], int(s), gi, rng_seed))
+        else:
+            kind = {"uniform": KIND_UNIFORM, "degree": KIND_DEGREE, "forest_fire": KIND_FF,
+                    "snowball": KIND_SNOWBALL}[workload]
+            out.append(neighbor_sample(_G, kind, params.get("fanout", ()), params["depth"], int(s), gi, rng_seed,
+                                       params.get("pf", 0.0)))
+    return out
+
+
+def parallel_run(g: Graph, workload: str, seeds, instance_base, rng_seed, ids=None, workers=None, **params):
+    """The oracle over instances `ids` (local ids into `seeds`; default all) on all host
+    cores, fanned out over disjoint chunks (instances are independent).
+    workload: walk (params kind, length) | node2vec (p, q, length) | mdrw (length;
+    seeds[i] is the instance's pool) | layer (fanout, depth) | degree / uniform /
+    forest_fire / snowball (fanout, depth, pf).  Returns the per-instance results in
+    the order of ids (walks: path arrays; MDRW: edge arrays; sampling: (src, dst, depth))."""
+    import multiprocessing as mp
+    seeds = np.asarray(seeds)
+    ids = np.arange(len(seeds)) if ids is None else np.asarray(ids, dtype=np.int64)
+    if ids.size == 0:
+        return []
+    workers = workers or os.cpu_count() or 1
+    chunks = np.array_split(ids, min(ids.size, workers * 8))
+    jobs = [(workload, params, c, seeds[c], instance_base, rng_seed) for c in chunks if c.size]
+    if workers == 1:
+        global _G
+        _G = g
+        return [r for j in jobs for r in _run_job(j)]
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("fork"),
+                             initializer=_init_pool, initargs=(g,)) as ex:
+        res = list(ex.map(_run_job, jobs))
+    return [r for chunk in res for r in chunk]

@@ -504,6 +504,40 @@ ORACLE_EXPORT void oracle_walk_variant(const int64_t *row_ptr, const uint32_t *c
     }
 }
 
+/*
+ * Float-bias inverse transform sampling (R28; Eq. 1 P:224-247 with real-valued
+ * biases, "F is the prefix sum normalised"): b[0..n) fp32 (non-negative,
+ * finite), S[0] = 0, S[i+1] = S[i] + (double)b[i] summed left to right in fp64,
+ * T = S[n]; r = (U >> 11) * 2^-53 in [0, 1); x = r * T (one fp64 multiply);
+ * s = max{i < n : S[i] <= x, b[i] > 0} (the region [S[s], S[s+1]) holding x;
+ * zero-width regions are never chosen, R4).  *margin (nullable) receives
+ * min_{0<i<n} |x - S[i]| / T: how close the draw came to an interior boundary,
+ * relative to T (the checker's 1e-6 rule).  Returns -1 if T == 0.
+ * Pinned by hand-computed draws at, and one ulp either side of, a boundary
+ * (tests/test_oracle_float.py).
+ */
+ORACLE_EXPORT int64_t oracle_select_float(const float *b, int64_t n, uint64_t U, double *margin)
+{
+    if (margin) *margin = 1.0;
+    double *S = (double *)malloc(sizeof(double) * (size_t)(n + 1));
+    S[0] = 0.0;
+    for (int64_t i = 0; i < n; i++) S[i + 1] = S[i] + (double)b[i];
+    double T = S[n];
+    int64_t s = -1;
+    if (T > 0.0) {
+        double r = (double)(U >> 11) * (1.0 / 9007199254740992.0);
+        double x = r * T;
+        for (int64_t i = 0; i < n; i++) if (S[i] <= x && b[i] > 0.0f) s = i;
+        if (margin) {
+            double mg = 1.0;
+            for (int64_t i = 1; i < n; i++) { double dd = fabs(x - S[i]) / T; if (dd < mg) mg = dd; }
+            *margin = mg;
+        }
+    }
+    free(S);
+    return s;
+}
+
 /* node2vec integer scale (R16): smallest m in [1, 2^16] with m/p and m/q
  * integers in [1, 2^32); 0 if none (then the float path applies). */
 ORACLE_EXPORT uint32_t oracle_n2v_scale(double p, double q)
@@ -570,24 +604,13 @@ ORACLE_EXPORT uint32_t oracle_node2vec_step(const int64_t *row_ptr, const uint32
         return r;
     }
     float fp = (float)(1.0 / p), f1 = 1.0f, fq = (float)(1.0 / q);
-    double *S = (double *)malloc(sizeof(double) * (size_t)(n + 1));
-    S[0] = 0.0;
+    float *b = (float *)malloc(sizeof(float) * (size_t)n);
     for (int64_t i = 0; i < n; i++) {
         uint32_t u = pool[i];
-        float b = (u == prev) ? fp : (sorted_contains(np_, nprev, u) ? f1 : fq);
-        S[i + 1] = S[i] + (double)b;
+        b[i] = (u == prev) ? fp : (sorted_contains(np_, nprev, u) ? f1 : fq);
     }
-    double T = S[n];
-    double r = (double)(U >> 11) * (1.0 / 9007199254740992.0);
-    double x = r * T;
-    int64_t s = 0;
-    for (int64_t i = 0; i < n; i++) if (S[i] <= x) s = i;
-    if (margin) {
-        double mg = 1.0;
-        for (int64_t i = 1; i < n; i++) { double dd = fabs(x - S[i]) / T; if (dd < mg) mg = dd; }
-        *margin = mg;
-    }
-    free(S);
+    int64_t s = oracle_select_float(b, n, U, margin);
+    free(b);
     return pool[s];
 }
 

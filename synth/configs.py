@@ -50,12 +50,12 @@ CONFIGS = {
         description="forest fire pf=0.7, depth 2, 8,192 instances, TW-shaped R-MAT 41.6M V / 1.47B E"),
     "cfg5": WorkloadConfig(
         "cfg5", 65_600_000, 1_800_000_000, 5, "mdrw", "mdrw", 4000, length=2000, pool_size=2000,
-        oom_budget_bytes=8 << 30, oom_partitions=4, oom_resident=2,
+        oom_budget_bytes=8_000_000_000, oom_partitions=4, oom_resident=2,
         description="MDRW pool 2,000, 2,000 steps, 4,000 instances, FR-shaped R-MAT 65.6M V / 1.8B E, OOM 8 GB budget"),
     # config 5's second half: batched multi-instance traversal sampling under the same budget (§5.2-5.3)
     "cfg5_ns": WorkloadConfig(
         "cfg5_ns", 65_600_000, 1_800_000_000, 5, "neighbor", "degree", 8192, fanout=(2, 2), depth=2,
-        oom_budget_bytes=8 << 30, oom_partitions=4, oom_resident=2,
+        oom_budget_bytes=8_000_000_000, oom_partitions=4, oom_resident=2,
         description="degree-biased neighbor sampling fanout 2, depth 2, 8,192 instances, batched, "
                     "FR-shaped R-MAT 65.6M V / 1.8B E, OOM 8 GB budget"),
 }

@@ -1,13 +1,25 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
 
 Each test builds the config's full synthetic graph on the GPU, runs the whole
-workload through the C ABI exactly as bench.py does (all instances in one
-call), and compares a deterministic sample of instances / walkers with the
-oracle element by element (integer biases: bit-exact).  Invariants that hold
-at any size are checked on 100 % of the output.
+workload through the C ABI exactly as bench.py does (all instances in one call),
+and compares with the oracle element by element (integer biases: bit-exact) at
+the coverage SURVEY.md §8(d) d.4 plans:
+
+  cfg2  all 4,000 walkers                      (cache + walk index, and the scan path)
+  cfg3  every 64th walker (~29.5K of ~1.9M)    (triangle counts, and the full merge);
+        the two kernels are also compared with each other on 100 % of the walkers
+  cfg4  all 8,192 instances, layer and forest fire
+  cfg5  all 4,000 MDRW instances in memory; the 8 GB OOM launches (zero-copy and the
+        paper's partition scheduling) equal to the in-memory output on 100 %
+  cfg5_ns all 8,192 instances in memory; OOM partition scheduling / zero-copy equal
+
+each for the three rng seeds of §8(d) d.2 (CSAW_TEST_SEEDS overrides, e.g. "1").
+The oracle is fanned out over the host cores (instances are independent).
+Invariants that hold at any size are checked on 100 % of the output.
 """
 import gc
 import os
+import time
 
 import numpy as np
 import pytest
@@ -20,15 +32,11 @@ from tests._parity import DEV, u32
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
-# Philox seed of the runs (CSAW_TEST_SEED overrides: the same checks under other random streams)
-SEED = int(os.environ.get("CSAW_TEST_SEED", "1"))
+SEEDS = [int(s) for s in os.environ.get("CSAW_TEST_SEEDS", os.environ.get("CSAW_TEST_SEED", "1,2,3")).split(",")]
 
 
-def build(cfg, ctps_cache=False, node2vec_tri=False):
-    g = rmat_csr(cfg.graph_vertices, cfg.graph_entries, cfg.graph_seed, device=DEV)
-    G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, ctps_cache=ctps_cache, node2vec_tri=node2vec_tri)
-    og = O.Graph(g.row_ptr.cpu().numpy(), g.col_idx.cpu().numpy().view(np.uint32))
-    return g, G, og
+def log(msg):
+    print(f"[{time.strftime('%H:%M:%S')}] {msg}", flush=True)
 
 
 def release(*objs):
@@ -39,108 +47,211 @@ def release(*objs):
     torch.cuda.empty_cache()
 
 
-def sample_ids(n, k, salt=0):
-    """Deterministic spread of k ids in [0, n) incl. the first and last."""
-    if n <= k:
-        return list(range(n))
-    ids = set(np.linspace(0, n - 1, k - 8).astype(np.int64).tolist())
-    rng = np.random.default_rng(1234 + salt)
-    ids |= set(rng.integers(0, n, 8).tolist())
-    return sorted(ids)
+def first_mismatch(got, ref):
+    """index of the first differing row (None if equal)"""
+    bad = np.nonzero((got != ref).reshape(got.shape[0], -1).any(axis=1))[0]
+    return None if bad.size == 0 else int(bad[0])
 
 
 def check_edges_exist(og, src, dst):
-    """every sampled (src, dst) is a CSR edge (vectorised binary search per row)."""
-    rp = og.row_ptr
-    for s, d in zip(src[:: max(1, len(src) // 200000)], dst[:: max(1, len(dst) // 200000)]):
-        row = og.col[rp[s]:rp[s + 1]]
-        i = np.searchsorted(row, d)
-        assert i < row.size and row[i] == d
+    """every (src, dst) is a CSR edge: vectorised binary search inside each src row"""
+    src = np.asarray(src, dtype=np.int64)
+    dst = np.asarray(dst, dtype=np.uint32)
+    lo, hi = og.row_ptr[src], og.row_ptr[src + 1]
+    assert (hi > lo).all()
+    # lower bound of dst within col[lo:hi), all rows at once
+    while True:
+        act = lo < hi
+        if not act.any():
+            break
+        mid = (lo + hi) // 2
+        less = og.col[np.where(act, mid, 0)] < dst
+        lo = np.where(act & less, mid + 1, lo)
+        hi = np.where(act & ~less, mid, hi)
+    assert (lo < og.row_ptr[src + 1]).all() and (og.col[np.minimum(lo, og.col.size - 1)] == dst).all()
 
 
-@pytest.mark.parametrize("cached", [False, True])
-def test_cfg2_degree_walk_full(cached):
-    """cached=True is the bench's launch: CTPS cache + narrow walk index (k_walk_wix)."""
+def flat_sampling(offs, src, dst, dep, ids):
+    return [(src[offs[i]:offs[i + 1]], dst[offs[i]:offs[i + 1]], dep[offs[i]:offs[i + 1]]) for i in ids]
+
+
+def compare_sampling(got, ref, what):
+    for i, ((a, b, c), (x, y, z)) in enumerate(zip(got, ref)):
+        assert np.array_equal(a, x) and np.array_equal(b, y) and np.array_equal(c, z), f"{what}: instance {i}"
+
+
+def run_sample(G, bias, seeds, cfg, seed):
+    offs, src, dst, dep = cs.csaw_sample(G, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth, rng_seed=seed)
+    torch.cuda.synchronize()
+    return offs.cpu().numpy().astype(np.int64), u32(src), u32(dst), dep.cpu().numpy()
+
+
+# ------------------------------------------------------------------ cfg2
+def test_cfg2_degree_walk_full():
     cfg = CONFIGS["cfg2"]
-    g, G, og = build(cfg, ctps_cache=cached)
-    assert G.info()["walk_index_leaf"] == (128 if cached else 0)
+    g = rmat_csr(cfg.graph_vertices, cfg.graph_entries, cfg.graph_seed, device=DEV)
+    og = O.Graph.from_torch(g)
     seeds = instance_seeds(g, cfg.n_instances).to(DEV)
-    path = u32(cs.csaw_walk(G, "degree", seeds, cfg.length, rng_seed=SEED))
-    assert path.shape == (cfg.n_instances, cfg.length + 1)
-    assert (path != cs.NONE).all()                       # symmetric graph, non-isolated seeds: exact length
     sv = u32(seeds)
-    for w in sample_ids(cfg.n_instances, 24):
-        ref = O.walk(og, O.KIND_DEGREE, cfg.length, int(sv[w]), w, SEED)
-        assert np.array_equal(path[w], ref), f"walker {w}"
-    # 100 % invariant: consecutive path vertices are adjacent
-    check_edges_exist(og, path[:, :-1].ravel(), path[:, 1:].ravel())
-    release(G)
+    Gc = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, ctps_cache=True)     # the bench's launch
+    Gs = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0)                      # per-step scans (the ★ path)
+    assert Gc.info()["walk_index_leaf"] == 128 and Gs.info()["ctps_cache"] == 0
+    for seed in SEEDS:
+        pc = u32(cs.csaw_walk(Gc, "degree", seeds, cfg.length, rng_seed=seed))
+        ps = u32(cs.csaw_walk(Gs, "degree", seeds, cfg.length, rng_seed=seed))
+        t0 = time.time()
+        ref = np.stack(O.parallel_run(og, "walk", sv, 0, seed, kind=O.KIND_DEGREE, length=cfg.length))
+        log(f"cfg2 seed {seed}: oracle over all {len(sv)} walkers in {time.time() - t0:.1f} s")
+        assert pc.shape == ref.shape == (cfg.n_instances, cfg.length + 1)
+        assert first_mismatch(pc, ref) is None, f"seed {seed}: cached walker {first_mismatch(pc, ref)}"
+        assert first_mismatch(ps, ref) is None, f"seed {seed}: scan walker {first_mismatch(ps, ref)}"
+        assert (pc != cs.NONE).all()          # symmetric graph, non-isolated seeds: exact length
+        check_edges_exist(og, pc[:, :-1].ravel(), pc[:, 1:].ravel())
+    release(Gc, Gs)
 
 
-@pytest.mark.parametrize("cached", [False, True])
-def test_cfg3_node2vec_full(cached):
-    """cached=True is the bench's launch: per-edge triangle counts + partial scans (k_node2vec_tri)."""
+# ------------------------------------------------------------------ cfg3
+def test_cfg3_node2vec_full():
     cfg = CONFIGS["cfg3"]
-    g, G, og = build(cfg, node2vec_tri=cached)
-    assert G.info()["node2vec_tri"] == (1 if cached else 0)
+    g = rmat_csr(cfg.graph_vertices, cfg.graph_entries, cfg.graph_seed, device=DEV)
+    og = O.Graph.from_torch(g)
     seeds = nonisolated_vertices(g).to(torch.int32).to(DEV)
     n = seeds.numel()
-    path = u32(cs.csaw_walk(G, cs.make_bias("node2vec", p=cfg.p, q=cfg.q), seeds, cfg.length, rng_seed=SEED))
-    assert path.shape == (n, cfg.length + 1) and (path != cs.NONE).all()
     sv = u32(seeds)
-    for w in sample_ids(n, 40):
-        ref = O.node2vec(og, cfg.p, cfg.q, cfg.length, int(sv[w]), w, SEED)
-        assert np.array_equal(path[w], ref), f"walker {w}"
-    check_edges_exist(og, path[:, :-1].ravel(), path[:, 1:].ravel())
-    release(G)
+    ids = np.arange(0, n, 64)
+    Gt = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, node2vec_tri=True)   # the bench's launch
+    Gm = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0)                      # full merge per step
+    assert Gt.info()["node2vec_tri"] == 1 and Gm.info()["node2vec_tri"] == 0
+    bias = cs.make_bias("node2vec", p=cfg.p, q=cfg.q)
+    for seed in SEEDS:
+        pt = u32(cs.csaw_walk(Gt, bias, seeds, cfg.length, rng_seed=seed))
+        pm = u32(cs.csaw_walk(Gm, bias, seeds, cfg.length, rng_seed=seed))
+        assert pt.shape == (n, cfg.length + 1) and (pt != cs.NONE).all()
+        # two independent kernels (closed form over triangle counts vs full CTPS merge): 100 %
+        assert first_mismatch(pt, pm) is None, f"seed {seed}: tri vs merge walker {first_mismatch(pt, pm)}"
+        t0 = time.time()
+        ref = np.stack(O.parallel_run(og, "node2vec", sv, 0, seed, ids=ids, p=cfg.p, q=cfg.q, length=cfg.length))
+        log(f"cfg3 seed {seed}: oracle over {ids.size} walkers (every 64th of {n}) in {time.time() - t0:.1f} s")
+        bad = first_mismatch(pt[ids], ref)
+        assert bad is None, f"seed {seed}: walker {int(ids[bad])}"
+        check_edges_exist(og, pt[::7, :-1].ravel(), pt[::7, 1:].ravel())
+    release(Gt, Gm)
 
 
-def _check_sampling(cfg, g, G, og, workload, k_sample=160):
-    seeds = instance_seeds(g, cfg.n_instances).to(DEV)
-    bias = cs.make_bias(cfg.bias, pf=cfg.pf)
-    offs, src, dst, dep = cs.csaw_sample(G, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth, rng_seed=SEED)
-    offs = offs.cpu().numpy().astype(np.int64)
-    src, dst, dep = u32(src), u32(dst), dep.cpu().numpy()
-    sv = u32(seeds)
-    for i in sample_ids(cfg.n_instances, k_sample):
-        if workload == "layer":
-            es, ed, ee = O.layer_sample(og, list(cfg.fanout), cfg.depth, int(sv[i]), i, SEED)
-        else:
-            es, ed, ee = O.neighbor_sample(og, O.KIND_FF, [], cfg.depth, int(sv[i]), i, SEED, cfg.pf)
-        a, b = offs[i], offs[i + 1]
-        assert np.array_equal(src[a:b], es) and np.array_equal(dst[a:b], ed) and np.array_equal(dep[a:b], ee), i
-    check_edges_exist(og, src, dst)
-    assert (dep >= 1).all() and (dep <= cfg.depth).all()
-    return offs
-
-
+# ------------------------------------------------------------------ cfg4
 def test_cfg4_layer_and_forest_fire_full():
-    cfg = CONFIGS["cfg4_layer"]
-    g, G, og = build(cfg)
-    offs = _check_sampling(cfg, g, G, og, "layer")
-    # layer: exactly min(fanout, pool) per level -> 4 edges per instance when pools are large
-    assert np.median(np.diff(offs)) == 4
-    _check_sampling(CONFIGS["cfg4_ff"], g, G, og, "forest_fire")
-    release(G)
-
-
-def test_cfg5_mdrw_in_memory_full():
-    cfg = CONFIGS["cfg5"]
-    g, G, og = build(cfg)
-    seeds = mdrw_seeds(g, cfg.n_instances, cfg.pool_size).to(DEV)
-    edges = u32(cs.csaw_walk(G, cs.make_bias("mdrw"), seeds, cfg.length, rng_seed=SEED))
-    assert edges.shape == (cfg.n_instances, cfg.length, 2) and (edges != cs.NONE).all()
+    cl, cf = CONFIGS["cfg4_layer"], CONFIGS["cfg4_ff"]
+    g = rmat_csr(cl.graph_vertices, cl.graph_entries, cl.graph_seed, device=DEV)
+    og = O.Graph.from_torch(g)
+    seeds = instance_seeds(g, cl.n_instances).to(DEV)
     sv = u32(seeds)
-    for i in sample_ids(cfg.n_instances, 16):
-        ref = O.mdrw(og, sv[i], cfg.length, i, SEED)
-        assert np.array_equal(edges[i], ref), f"instance {i}"
-    check_edges_exist(og, edges[:, :, 0].ravel(), edges[:, :, 1].ravel())
-    release(G)
-    # the config's out-of-memory launch (8 GB budget), zero-copy mode with the resident
-    # col_idx prefix: identical to the in-memory edges on 100 % of the output
-    Gz = cs.csaw_graph_create(g.row_ptr.cpu(), g.col_idx.cpu(), device=0, budget_bytes=cfg.oom_budget_bytes,
-                              num_partitions=cfg.oom_partitions, max_resident=1, zerocopy=True)
-    assert Gz.info()["device_bytes"] <= cfg.oom_budget_bytes
-    ez = u32(cs.csaw_walk(Gz, cs.make_bias("mdrw"), seeds, cfg.length, rng_seed=SEED))
-    assert np.array_equal(ez, edges)
+    ids = np.arange(cl.n_instances)
+    Gc = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, ctps_cache=True)     # the bench's launch
+    for seed in SEEDS:
+        t0 = time.time()
+        ref_l = O.parallel_run(og, "layer", sv, 0, seed, fanout=list(cl.fanout), depth=cl.depth)
+        ref_f = O.parallel_run(og, "forest_fire", sv, 0, seed, depth=cf.depth, pf=cf.pf)
+        log(f"cfg4 seed {seed}: oracle over all {len(sv)} instances (layer + FF) in {time.time() - t0:.1f} s")
+        offs, src, dst, dep = run_sample(Gc, cs.make_bias("layer"), seeds, cl, seed)
+        compare_sampling(flat_sampling(offs, src, dst, dep, ids), ref_l, f"layer seed {seed}")
+        assert np.median(np.diff(offs)) == 4            # min(fanout, pool) per level
+        check_edges_exist(og, src, dst)
+        offs, src, dst, dep = run_sample(Gc, cs.make_bias("forest_fire", pf=cf.pf), seeds, cf, seed)
+        compare_sampling(flat_sampling(offs, src, dst, dep, ids), ref_f, f"forest fire seed {seed}")
+        check_edges_exist(og, src, dst)
+        assert (dep >= 1).all() and (dep <= cf.depth).all()
+    release(Gc)
+    # the uncached (per-pool scan) launch on one seed: same bytes
+    Gs = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0)
+    offs, src, dst, dep = run_sample(Gs, cs.make_bias("layer"), seeds, cl, SEEDS[0])
+    ref_l = O.parallel_run(og, "layer", sv, 0, SEEDS[0], fanout=list(cl.fanout), depth=cl.depth)
+    compare_sampling(flat_sampling(offs, src, dst, dep, ids), ref_l, "layer (scan)")
+    release(Gs)
+
+
+# ------------------------------------------------------------------ cfg5
+@pytest.fixture(scope="module")
+def cfg5_graph():
+    cfg = CONFIGS["cfg5"]
+    g = rmat_csr(cfg.graph_vertices, cfg.graph_entries, cfg.graph_seed, device=DEV)
+    og = O.Graph.from_torch(g)
+    host = (g.row_ptr.cpu(), g.col_idx.cpu())
+    yield g, og, host
+    del g
+    release()
+
+
+def oom_graph(host, cfg, zerocopy):
+    return cs.csaw_graph_create(host[0], host[1], device=0, budget_bytes=cfg.oom_budget_bytes,
+                                num_partitions=cfg.oom_partitions,
+                                max_resident=1 if zerocopy else cfg.oom_resident,
+                                num_streams=cfg.oom_resident, zerocopy=zerocopy)
+
+
+def test_cfg5_mdrw_full(cfg5_graph):
+    cfg = CONFIGS["cfg5"]
+    g, og, host = cfg5_graph
+    seeds = mdrw_seeds(g, cfg.n_instances, cfg.pool_size).to(DEV)
+    sv = u32(seeds)
+    Gm = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, next_meta=True)     # in-memory bench launch
+    Gp = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0)                     # plain in-memory
+    bias = cs.make_bias("mdrw")
+    inmem = {}
+    for seed in SEEDS:
+        em = u32(cs.csaw_walk(Gm, bias, seeds, cfg.length, rng_seed=seed))
+        ep = u32(cs.csaw_walk(Gp, bias, seeds, cfg.length, rng_seed=seed))
+        t0 = time.time()
+        ref = np.stack(O.parallel_run(og, "mdrw", sv, 0, seed, length=cfg.length))
+        log(f"cfg5 seed {seed}: oracle over all {len(sv)} MDRW instances in {time.time() - t0:.1f} s")
+        assert em.shape == ref.shape == (cfg.n_instances, cfg.length, 2) and (em != cs.NONE).all()
+        assert first_mismatch(em, ref) is None, f"seed {seed}: instance {first_mismatch(em, ref)}"
+        assert first_mismatch(ep, ref) is None, f"seed {seed}: plain instance {first_mismatch(ep, ref)}"
+        check_edges_exist(og, em[:, :, 0].ravel(), em[:, :, 1].ravel())
+        inmem[seed] = em
+    release(Gm, Gp)
+    # the config's out-of-memory launches under the 8 GB budget: identical on 100 % (P:877-882)
+    Gz = oom_graph(host, cfg, zerocopy=True)
+    assert Gz.info()["oom_mode"] == 1 and Gz.info()["device_bytes"] <= cfg.oom_budget_bytes
+    for seed in SEEDS:
+        ez = u32(cs.csaw_walk(Gz, bias, seeds, cfg.length, rng_seed=seed))
+        assert first_mismatch(ez, inmem[seed]) is None, f"zero-copy seed {seed}"
     release(Gz)
+    Go = oom_graph(host, cfg, zerocopy=False)                  # the paper's partition scheduling (§5)
+    assert Go.info()["oom_mode"] == 1 and Go.info()["device_bytes"] <= cfg.oom_budget_bytes
+    t0 = time.time()
+    eo = u32(cs.csaw_walk(Go, bias, seeds, cfg.length, rng_seed=SEEDS[0]))
+    st = cs.csaw_stats(Go)
+    log(f"cfg5 partition-scheduled OOM MDRW: {time.time() - t0:.1f} s, {st['partition_loads']} partition loads")
+    assert st["partition_loads"] > cfg.oom_resident
+    assert first_mismatch(eo, inmem[SEEDS[0]]) is None, "partition-scheduled OOM MDRW"
+    release(Go)
+
+
+def test_cfg5_ns_full(cfg5_graph):
+    cfg = CONFIGS["cfg5_ns"]
+    g, og, host = cfg5_graph
+    seeds = instance_seeds(g, cfg.n_instances).to(DEV)
+    sv = u32(seeds)
+    ids = np.arange(cfg.n_instances)
+    bias = cs.make_bias("degree")
+    Gm = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0)
+    inmem = {}
+    for seed in SEEDS:
+        r = run_sample(Gm, bias, seeds, cfg, seed)
+        t0 = time.time()
+        ref = O.parallel_run(og, "degree", sv, 0, seed, fanout=list(cfg.fanout), depth=cfg.depth)
+        log(f"cfg5_ns seed {seed}: oracle over all {len(sv)} instances in {time.time() - t0:.1f} s")
+        compare_sampling(flat_sampling(*r, ids), ref, f"cfg5_ns in memory seed {seed}")
+        check_edges_exist(og, r[1], r[2])
+        inmem[seed] = r
+    release(Gm)
+    for zc in (False, True):
+        Go = oom_graph(host, cfg, zerocopy=zc)
+        assert Go.info()["oom_mode"] == 1 and Go.info()["device_bytes"] <= cfg.oom_budget_bytes
+        for seed in SEEDS:
+            r = run_sample(Go, bias, seeds, cfg, seed)
+            for a, b in zip(r, inmem[seed]):
+                assert np.array_equal(a, b), f"cfg5_ns OOM ({'zero-copy' if zc else 'partitions'}) seed {seed}"
+            if not zc:
+                assert cs.csaw_stats(Go)["partition_loads"] >= cfg.oom_partitions
+        release(Go)
