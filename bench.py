@@ -1,25 +1,35 @@
 #!/usr/bin/env python
 """bench.py — C-SAW hot path on B200: sampled edges per second (SEPS) + roofline.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--scaling strong|weak]
+                    [--impl ours|reference]
 
-A "step" is one pass of the whole hot path over one batch: for the default
-config (cfg2, BASELINE.json configs[1]) every walker of the 4,000-walker,
-2,000-step degree-biased random walk on the LJ-shaped R-MAT graph.  Inputs are
-synthetic (synth/, seeded), resident in HBM when the timed region starts; L2 is
-flushed (256 MB write) before every timed step, and each step is timed with
-CUDA events on the launching stream.  Multi-GPU: one process per GPU
-(torchrun), weak scaling (each rank runs the config's workload on its own
-disjoint instance-id range), max-over-ranks time, NCCL used only for the
-optional output gather after timing.  The oracle (oracle/) is executed only by
-the cpu_baseline leg and by --impl reference.
+A "step" is one pass of the whole hot path over one batch of synthetic input.
+The default workload is cfg3 (BASELINE.json configs[2]): the node2vec walk
+(p = 2, q = 0.5, length 80) of one walker per non-isolated vertex (~1.89M) on
+the Orkut-shaped R-MAT graph -- the largest config that BASELINE.json does not
+tag as multi-GPU (DESIGN.md §6 "Which config is the bench line").  Inputs are
+synthetic (synth/, seeded) and resident in HBM when the timed region starts; L2
+is flushed (256 MB write) before every timed step; each step is timed with CUDA
+events on the launching stream.  Timed steps cycle through the rng seeds 1, 2, 3
+(the mean over three seed sets).
+
+Multi-GPU (§8(e)): one process per GPU.  `--gpus N` without a torchrun
+environment re-launches itself under torch.distributed.run.  Default is STRONG
+scaling: the config's fixed instance set is split into contiguous ranges, one
+per rank (Fig. 17), instance ids stay global (Philox
+counter), so the union of the ranks' outputs is bit-identical to N = 1.
+`--scaling weak` gives every rank the full workload on its own id range.  No
+collective on the data path; max-over-ranks device time; NCCL only for the
+optional output gather after timing.  The oracle (oracle/) runs only in the
+cpu_baseline leg and in --impl reference.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,16 +47,20 @@ from synth import CONFIGS, degree_stats, instance_seeds, mdrw_seeds, nonisolated
 METRIC = "sampled edges/sec (SEPS) at 1/2/4/8 B200; % of HBM roofline"
 UNIT = "sampled_edges/s"
 L2_FLUSH_BYTES = 256 << 20
+DEFAULT_CONFIG = "cfg3"
 
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--rng-seed", type=int, default=1)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong (default): the config's instance set split across ranks; weak: every rank runs "
+                         "the whole config on its own instance-id range")
+    ap.add_argument("--rng-seeds", default="1,2,3", help="timed steps cycle through these Philox seeds (P:968)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle CPU-baseline budget (wall s)")
     ap.add_argument("--gather", action="store_true", help="NCCL-gather outputs after timing (reported apart)")
@@ -54,18 +68,33 @@ def parse_args():
     ap.add_argument("--in-memory", action="store_true", help="cfg5: ignore the OOM budget (in-memory MDRW)")
     ap.add_argument("--no-cache", action="store_true",
                     help="disable the static-bias CTPS cache / node2vec triangle counts (scan every pool)")
-    ap.add_argument("--no-zerocopy", action="store_true", help="cfg5: skip the zero-copy OOM variant")
+    ap.add_argument("--no-zerocopy", action="store_true", help="OOM configs: skip the zero-copy OOM variant")
     ap.add_argument("--oom-budget-gb", type=float, default=0.0,
-                    help="OOM configs: override the device budget (GiB) -- experiments only, the config names 8 GB")
+                    help="OOM configs: override the device budget (1e9 B) -- experiments only, the config names 8 GB")
     ap.add_argument("--oom-variant", default="partition", choices=["partition", "zerocopy"],
-                    help="OOM configs: time the paper's partition scheduling (default) or the zero-copy mode "
-                         "(col_idx prefix resident within the budget, the rest read in place from pinned host memory)")
-    return ap.parse_args()
+                    help="OOM configs: time the paper's partition scheduling (default) or the zero-copy mode")
+    return ap.parse_args(argv)
+
+
+# ------------------------------------------------------------------ self-launch (--gpus N)
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args) -> int | None:
+    """`--gpus N` (N > 1) outside torchrun: re-launch this script as N ranks under
+    torch.distributed.run on 127.0.0.1 and return its exit code (None = run here)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 # ------------------------------------------------------------------ workload description
 def workload_of(cfg):
-    """(kind, bias name, csaw entry) for a config."""
     return {"walk": "walk", "node2vec": "walk", "mdrw": "walk",
             "neighbor": "sample", "layer": "sample", "forest_fire": "sample"}[cfg.workload]
 
@@ -73,22 +102,35 @@ def workload_of(cfg):
 def make_graph(cfg, device):
     t0 = time.perf_counter()
     g = rmat_csr(cfg.graph_vertices, cfg.graph_entries, cfg.graph_seed, device=device)
-    torch.cuda.synchronize(device) if device.type == "cuda" else None
+    if device.type == "cuda":
+        torch.cuda.synchronize(device)
     return g, time.perf_counter() - t0
 
 
-def make_seeds(cfg, g, rank, world):
-    """This rank's instance ids [base, base+n) and seeds (weak scaling: n per rank)."""
+def total_instances(cfg, g):
+    if cfg.workload == "node2vec" and cfg.n_instances == 0:
+        return int(nonisolated_vertices(g).numel())
+    return cfg.n_instances
+
+
+def make_seeds(cfg, g, rank, world, scaling):
+    """(instance_base, seeds, n_total) of this rank.  strong: the config's instances split
+    into contiguous ranges [floor(rN/W), floor((r+1)N/W)); weak: N instances per rank
+    with global ids [rN, (r+1)N)."""
+    N = total_instances(cfg, g)
+    if scaling == "strong":
+        lo, hi, total = rank * N // world, (rank + 1) * N // world, N
+    else:
+        lo, hi, total = rank * N, (rank + 1) * N, N * world
     if cfg.workload == "node2vec":
         verts = nonisolated_vertices(g)
-        n = verts.numel() if cfg.n_instances == 0 else cfg.n_instances
-        return rank * n, verts[:n].to(torch.int32)
-    n = cfg.n_instances
+        idx = torch.arange(lo, hi, device=verts.device) % verts.numel()   # one walker per non-isolated vertex
+        return lo, verts[idx].to(torch.int32), total
     if cfg.workload == "mdrw":
-        s = mdrw_seeds(g, n * world, cfg.pool_size)
-        return rank * n, s[rank * n:(rank + 1) * n].contiguous()
-    s = instance_seeds(g, n * world)
-    return rank * n, s[rank * n:(rank + 1) * n].contiguous()
+        s = mdrw_seeds(g, hi, cfg.pool_size)
+        return lo, s[lo:hi].contiguous(), total
+    s = instance_seeds(g, hi)
+    return lo, s[lo:hi].contiguous(), total
 
 
 def bias_of(cs, cfg):
@@ -97,34 +139,84 @@ def bias_of(cs, cfg):
             "layer": cs.make_bias("layer"), "forest_fire": cs.make_bias("forest_fire", pf=cfg.pf)}[cfg.workload]
 
 
-def algorithmic_bytes(cfg, st, n, edges):
-    """Bytes the method must move (element granularity), DESIGN.md §6:
-    degree pool: 16 (row_ptr pair) + 8 d (col + deg) per pool, + output;
-    uniform: 16 + 4 per step; node2vec: 16 + 4 d(v) + 4 d(prev); MDRW: 32 per step;
-    sampling select kernel: 16 per pool + 8 per scanned candidate + 12 per staged edge."""
-    scanned, pools = st["neighbours_scanned"], st["pools"]
-    probes = st.get("cache_probes", 0)
-    if st.get("index_bytes") and cfg.workload in ("walk", "node2vec"):
-        # bytes the kernel read, counted in the kernel (narrow walk index: record + nodes + leaf
-        # and col entries; node2vec with triangle counts: row_ptr pairs, tri, list entries), + path
-        return st["index_bytes"] + 4 * n * (cfg.length + 1) + 4 * n
-    if probes and cfg.workload == "walk":
-        # cached CTPS: row_ptr pair 16 + T 8 + col 4 per step, 8 per cache probe, + path
-        return 28 * pools + 8 * probes + 4 * n * (cfg.length + 1) + 4 * n
-    if probes:
-        return 24 * pools + 8 * probes + 12 * edges
-    if cfg.workload == "walk":
-        out = 4 * n * (cfg.length + 1) + 4 * n
-        if cfg.bias == "degree":
-            return 16 * pools + 8 * scanned + out
-        return 20 * pools + out
-    if cfg.workload == "node2vec":
-        return 16 * pools + 8 * scanned + 4 * n * (cfg.length + 1) + 4 * n
+# ------------------------------------------------------------------ §8(d) algorithmic bytes
+def _bit_length(x: torch.Tensor) -> torch.Tensor:
+    """bit length of non-negative int64 x (exact: frexp of the float64 value), so
+    ceil(log2 d) = bit_length(d - 1)."""
+    _, e = torch.frexp(x.to(torch.float64))
+    return torch.where(x > 0, e.to(torch.int64), torch.zeros_like(x))
+
+
+BYTES_MODEL = {
+    "walk_degree_scan": "SURVEY §8(d) degree-biased pool: 16 (row_ptr pair) + 8 d(v) (col + deg) per step + 4 (path)",
+    "walk_degree_cached": "SURVEY §8(f) NEXT-1 cached CTPS: 32 B sectors x (row_ptr pair + ceil(log2 d(v)) probes "
+                          "+ col) per step + 4 (path)",
+    "walk_uniform": "16 (row_ptr pair) + 4 (one col entry) + 4 (path) per step",
+    "node2vec": "SURVEY §8(d) node2vec step: 16 + 4 d(v) + 4 (N(prev) carried from the previous step); "
+                "step 0 uniform: 16 + 4 + 4",
+    "mdrw": "SURVEY §8(d) MDRW step: 16 (row_ptr v) + 4 (col) + 4 (deg u) + 8 (edge out) = 32",
+    "sample_degree": "SURVEY §8(d) degree-biased pool: 16 + 8 d(v) per expanded vertex + 9 per emitted edge",
+    "sample_layer": "SURVEY §8(d) layer: sum over levels and frontier vertices of 16 + 8 d(v) + 9 per edge",
+    "sample_ff": "SURVEY §8(d) uniform / FF expanded vertex: 16 + 4 x + 9 x (x = its emitted edges)",
+    "oom_host": "host link: partition / zero-copy bytes moved H2D per step (library counters)",
+}
+
+
+def walk_alg_bytes(cfg, deg, out, cached):
+    """§8(d) bytes of one walk launch, from its output (device tensors)."""
     if cfg.workload == "mdrw":
-        return 32 * n * cfg.length + 16 * n * cfg.pool_size
+        return 32 * out.shape[0] * out.shape[1], "mdrw"
+    p = out.to(torch.int64) & 0xFFFFFFFF
+    v = p[:, :-1]
+    valid = v != 0xFFFFFFFF
+    d = torch.where(valid, deg[torch.where(valid, v, torch.zeros_like(v))], torch.zeros_like(v))
+    nsteps = int(valid.sum())
+    if cfg.workload == "node2vec":
+        first = int(valid[:, 0].sum())
+        return int(16 * nsteps + 4 * d[:, 1:].sum() + 4 * first + 4 * nsteps), "node2vec"
+    if cfg.bias == "uniform":
+        return 24 * nsteps, "walk_uniform"
+    if cached:
+        probes = _bit_length(torch.clamp(d - 1, min=0))
+        return int(32 * (2 * nsteps + probes[valid].sum()) + 4 * nsteps), "walk_degree_cached"
+    return int(16 * nsteps + 8 * d.sum() + 4 * nsteps), "walk_degree_scan"
+
+
+def sample_alg_bytes(cfg, deg, seeds, offs, src, dst, dep):
+    """§8(d) bytes of one sampling launch: the expanded vertices of every level are the
+    seed (level 0) and the new vertices of the previous level (UPDATE's post-filter)."""
+    n = seeds.numel()
+    V = deg.numel()
+    m = src.numel()
+    inst = torch.repeat_interleave(torch.arange(n, device=offs.device), (offs[1:] - offs[:-1]).to(torch.int64))
+    s64 = src.to(torch.int64) & 0xFFFFFFFF
+    d64 = dst.to(torch.int64) & 0xFFFFFFFF
+    dp = dep.to(torch.int64)
+    seeds64 = seeds.to(torch.int64) & 0xFFFFFFFF
     if cfg.workload == "forest_fire":
-        return 16 * pools + 16 * edges
-    return 16 * pools + 8 * scanned + 12 * edges
+        # every expanded vertex: 16 + 4 x + 9 x; vertices that burned nothing still cost 16
+        exp = [torch.ones(n, dtype=torch.int64, device=offs.device)]
+        visited = inst * V + seeds64[inst]
+        for lvl in range(1, cfg.depth):
+            key = torch.unique((inst * V + d64)[dp == lvl])
+            key = key[~torch.isin(key, torch.unique(visited))]
+            exp.append(torch.ones(key.numel(), dtype=torch.int64, device=offs.device))
+            visited = torch.cat([visited, key])
+        npools = sum(int(e.numel()) for e in exp)
+        return 16 * npools + 13 * m, "sample_ff"
+    # degree / layer: every expanded vertex's whole neighbour list (16 + 8 d)
+    level_keys = [torch.arange(n, device=offs.device) * V + seeds64]
+    visited = level_keys[0]
+    for lvl in range(1, cfg.depth):
+        key = torch.unique((inst * V + d64)[dp == lvl])
+        key = key[~torch.isin(key, visited)]
+        level_keys.append(key)
+        visited = torch.cat([visited, key])
+    tot = 0
+    for key in level_keys:
+        dv = deg[key % V]
+        tot += int(16 * key.numel() + 8 * dv.sum())
+    return tot + 9 * m, ("sample_layer" if cfg.workload == "layer" else "sample_degree")
 
 
 # ------------------------------------------------------------------ clocks
@@ -220,14 +312,12 @@ def oracle_timed_sample(cfg, og, seeds_np, base, rng_seed, budget_s, workers=Non
     workers = workers or os.cpu_count() or 1
     n = len(seeds_np)
     O._G = og
-    # calibrate single-instance cost
     t0 = time.perf_counter()
     _oracle_job((cfg.name, 0, 1, base, seeds_np[:1], rng_seed))
     t1 = max(time.perf_counter() - t0, 1e-4)
     per_worker = max(1, int(budget_s / t1))
     m = int(min(n, per_worker * workers))
     m = max(m, min(n, workers))
-    # tiny workloads (e.g. cfg1): repeat whole passes so the sample is ~budget_s of CPU work
     passes = max(1, min(1000, int(budget_s * workers / max(t1 * n, 1e-9)))) if m == n else 1
     chunks = np.array_split(np.arange(m), workers * 2)
     jobs = [(cfg.name, int(c[0]), int(c[-1]) + 1, base, seeds_np[int(c[0]):int(c[-1]) + 1], rng_seed)
@@ -243,6 +333,7 @@ def oracle_timed_sample(cfg, og, seeds_np, base, rng_seed, budget_s, workers=Non
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
+    """The oracle, as it stands, on the box's host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -251,37 +342,46 @@ def run_reference(args):
     O.build()
     dev = torch.device("cuda:0") if torch.cuda.is_available() else torch.device("cpu")
     g, _ = make_graph(cfg, dev)
-    base, seeds = make_seeds(cfg, g, 0, 1)
+    base, seeds, _ = make_seeds(cfg, g, 0, 1, "strong")
     og = O.Graph.from_torch(g)
     seeds_np = seeds.cpu().numpy().view(np.uint32)
     del g
     if dev.type == "cuda":
         torch.cuda.empty_cache()
+    rng = [int(s) for s in args.rng_seeds.split(",")]
     per_step = max(2.0, 120.0 / max(1, args.steps + args.warmup))
-    for _ in range(args.warmup):
-        oracle_timed_sample(cfg, og, seeds_np, base, args.rng_seed, min(per_step, 3.0))
+    for i in range(args.warmup):
+        oracle_timed_sample(cfg, og, seeds_np, base, rng[i % len(rng)], min(per_step, 3.0))
     vals, walls, samples = [], [], []
-    for _ in range(args.steps):
-        v, cores, sample, edges, wall = oracle_timed_sample(cfg, og, seeds_np, base, args.rng_seed, per_step)
+    for i in range(args.steps):
+        v, cores, sample, edges, wall = oracle_timed_sample(cfg, og, seeds_np, base, rng[i % len(rng)], per_step)
         vals.append(v)
         walls.append(wall)
         samples.append(sample)
     value = statistics.mean(vals)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(walls),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (seeded R-MAT, synth/)",
-            "config": config_block(cfg, 1, None),
+            "config": config_block(cfg, args.gpus, None, args.scaling, total_instances_cfg(cfg)),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": samples[-1]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def config_block(cfg, world, stats_g, oom_mode=None, colc=None):
-    c = {"workload": f"{cfg.name}: {cfg.description}", "instances_per_gpu": cfg.n_instances or "all non-isolated",
-         "graph": {"V": cfg.graph_vertices, "E_target": cfg.graph_entries, "generator": "R-MAT Graph500 (0.57,0.19,0.19,0.05), symmetrised, dedup"},
-         "parallelism": f"instances sharded over {world} GPU(s), CSR replicated",
+def total_instances_cfg(cfg):
+    return cfg.n_instances or "one walker per non-isolated vertex"
+
+
+def config_block(cfg, world, stats_g, scaling, n_total, oom_mode=None, colc=None):
+    c = {"workload": f"{cfg.name}: {cfg.description}", "instances_total": n_total,
+         "graph": {"V": cfg.graph_vertices, "E_target": cfg.graph_entries,
+                   "generator": "R-MAT Graph500 (0.57,0.19,0.19,0.05), symmetrised, dedup"},
+         "parallelism": (f"strong scaling: the {n_total} instances split into {world} contiguous ranges, one per GPU; "
+                         "CSR replicated" if scaling == "strong" else
+                         f"weak scaling: every one of {world} GPU(s) runs the whole config on its own instance-id "
+                         "range; CSR replicated"),
          "l2": "flushed (256 MB write) before every timed step; CSR also larger than L2"}
     if cfg.workload in ("walk", "node2vec", "mdrw"):
         c["length"] = cfg.length
@@ -309,9 +409,29 @@ def config_block(cfg, world, stats_g, oom_mode=None, colc=None):
     return c
 
 
+def measure_h2d_peak(dev, nbytes=1 << 30, reps=5) -> float:
+    """Pinned host -> device cudaMemcpyAsync bandwidth (GB/s, best of reps): the
+    roofline of the OOM configs."""
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    best = 0.0
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d.copy_(h, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, nbytes / (e0.elapsed_time(e1) / 1000.0) / 1e9)
+    del h, d
+    return best
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse_args()
+    rc = maybe_spawn(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     import paper_2009_09103_b200 as cs
@@ -329,18 +449,20 @@ def main():
     cfg = CONFIGS[args.config]
     if args.oom_budget_gb > 0 and cfg.oom_budget_bytes:   # experiments only
         import dataclasses
-        cfg = dataclasses.replace(cfg, oom_budget_bytes=int(args.oom_budget_gb * (1 << 30)))
+        cfg = dataclasses.replace(cfg, oom_budget_bytes=int(args.oom_budget_gb * 1e9))
     kind = workload_of(cfg)
+    rng_seeds = [int(s) for s in args.rng_seeds.split(",")]
 
     g, gen_s = make_graph(cfg, dev)
     gstats = degree_stats(g)
-    base, seeds = make_seeds(cfg, g, rank, world)
+    deg = (g.row_ptr[1:] - g.row_ptr[:-1]).to(torch.int64)
+    base, seeds, n_total = make_seeds(cfg, g, rank, world, args.scaling)
     seeds = seeds.to(dev).contiguous()
     n = seeds.shape[0]
     oom = cfg.oom_budget_bytes > 0 and not args.in_memory
     if oom:
-        # out-of-memory mode (§5): the device holds only what the imposed budget
-        # allows -- move the generated graph to host memory first
+        # out-of-memory mode (§5): the device holds only what the imposed budget allows
+        del deg
         g = g.to("cpu")
         torch.cuda.empty_cache()
         zc_main = args.oom_variant == "zerocopy"
@@ -348,57 +470,54 @@ def main():
                                  num_partitions=cfg.oom_partitions, max_resident=1 if zc_main else cfg.oom_resident,
                                  num_streams=cfg.oom_resident, zerocopy=zc_main)
     else:
-        # static-bias CTPS cache (§8(f) NEXT-1, bit-identical) for degree-biased selections
         use_cache = (not args.no_cache) and cfg.bias in ("degree", "layer")
-        use_tri = (not args.no_cache) and cfg.workload == "node2vec"   # node2vec edge triangle counts
-        use_meta = (not args.no_cache) and cfg.workload == "mdrw"   # next-vertex metadata per entry
+        use_tri = (not args.no_cache) and cfg.workload == "node2vec"
+        use_meta = (not args.no_cache) and cfg.workload == "mdrw"
         G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache, node2vec_tri=use_tri,
-                                 next_meta=use_meta, walk_index=use_cache)   # walk index + vertex heads
+                                 next_meta=use_meta, walk_index=use_cache)
     ginfo = G.info()
     bias = bias_of(cs, cfg)
     stream = torch.cuda.current_stream(dev)
 
-    # output buffers (device) for the device-resident timed region
     if kind == "walk":
         shape = (n, cfg.length, 2) if cfg.workload == "mdrw" else (n, cfg.length + 1)
         out_dev = torch.empty(shape, dtype=torch.int32, device=dev)
 
-        def step():
-            cs.csaw_walk(G, bias, seeds, cfg.length, instance_base=base, rng_seed=args.rng_seed, out=out_dev,
-                         stream=stream)
+        def step(seed):
+            cs.csaw_walk(G, bias, seeds, cfg.length, instance_base=base, rng_seed=seed, out=out_dev, stream=stream)
             return n * cfg.length
     else:
         cap = cs.csaw_sample_capacity(bias, list(cfg.fanout), cfg.depth, n)
         bufs = [torch.empty(n + 1, dtype=torch.int64, device=dev), torch.empty(cap, dtype=torch.int32, device=dev),
                 torch.empty(cap, dtype=torch.int32, device=dev), torch.empty(cap, dtype=torch.uint8, device=dev)]
+        last = {}
 
-        def step():
+        def step(seed):
             nonlocal bufs, cap
             try:
                 r = cs.csaw_sample(G, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth, instance_base=base,
-                                   rng_seed=args.rng_seed, out=bufs, stream=stream)
+                                   rng_seed=seed, out=bufs, stream=stream)
             except cs.CsawError as e:
                 if e.status != 5:
                     raise
                 cap = int(cap * 2)
                 bufs = [bufs[0]] + [torch.empty(cap, dtype=t.dtype, device=dev) for t in bufs[1:]]
                 r = cs.csaw_sample(G, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth, instance_base=base,
-                                   rng_seed=args.rng_seed, out=bufs, stream=stream)
+                                   rng_seed=seed, out=bufs, stream=stream)
+            last["r"] = r
             return int(r[1].numel())
 
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
-    # the clock sampler starts before the warm-up, and warm-up steps are the timed steps'
-    # exact sequence (flush + step), so the first timed step is not a cold-host outlier
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.15)
-    for _ in range(max(args.warmup, 0)):
+    for i in range(max(args.warmup, 0)):       # the timed sequence exactly (flush, step, stats read)
         flush.fill_(1)
         w0 = torch.cuda.Event(enable_timing=True)
         w1 = torch.cuda.Event(enable_timing=True)
         w0.record(stream)
-        torch.cuda.nvtx.range_push("csaw_warmup")   # NVTX initialises on first use: not inside a timed step
-        step()
+        torch.cuda.nvtx.range_push("csaw_warmup")
+        step(rng_seeds[i % len(rng_seeds)])
         torch.cuda.nvtx.range_pop()
         w1.record(stream)
         cs.csaw_stats(G)
@@ -409,20 +528,21 @@ def main():
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize(dev)
-    clocks.lines.clear()   # keep only samples taken during the timed region
+    clocks.lines.clear()
     evs = []
     edges = 0
     launches = 0
     hot_ms, hot_launches = 0.0, 0
-    alg_bytes = 0
+    kbytes = 0
+    h2d_bytes, transfer_ms = 0, 0.0
     st_last = None
-    for _ in range(args.steps):
+    for i in range(args.steps):
         flush.fill_(1)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        torch.cuda.nvtx.range_push("csaw_step")   # lets ncu select the timed launches (--nvtx-include csaw_step/)
-        edges += step()
+        torch.cuda.nvtx.range_push("csaw_step")   # ncu: --nvtx --nvtx-include csaw_step/
+        edges += step(rng_seeds[i % len(rng_seeds)])
         torch.cuda.nvtx.range_pop()
         e1.record(stream)
         evs.append((e0, e1))
@@ -431,7 +551,9 @@ def main():
         launches += st["kernel_launches"]
         hot_ms += st["hot_kernel_ms"]
         hot_launches += st["hot_launches"]
-        alg_bytes += algorithmic_bytes(cfg, st, n, st["sampled_edges"])
+        kbytes += st["index_bytes"]
+        h2d_bytes += st["h2d_bytes"]
+        transfer_ms += st["transfer_ms"]
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in evs]
@@ -448,6 +570,22 @@ def main():
     else:
         edges_all = edges
     value = edges_all / (total_ms / 1000.0)
+    steps_per_seed = {s: sum(1 for i in range(args.steps) if rng_seeds[i % len(rng_seeds)] == s) for s in rng_seeds}
+
+    # ---------------- §8(d) algorithmic bytes of the timed launches (from the outputs, untimed re-runs)
+    alg_bytes, model = 0, "oom_host"
+    if not oom:
+        cached = bool(ginfo.get("ctps_cache"))
+        for s, k in steps_per_seed.items():
+            if k == 0:
+                continue
+            step(s)
+            torch.cuda.synchronize(dev)
+            if kind == "walk":
+                b, model = walk_alg_bytes(cfg, deg, out_dev, cached)
+            else:
+                b, model = sample_alg_bytes(cfg, deg, seeds, *last["r"])
+            alg_bytes += b * k
 
     # ---------------- optional NCCL gather of the sampled outputs (not on the SEPS clock, G31)
     gather_ms = None
@@ -457,82 +595,57 @@ def main():
         if kind == "walk":
             cdist.gather_walks(out_dev)
         else:
-            cdist.gather_samples(*r_last(cs, G, bias, seeds, cfg, base, args, stream))
+            cdist.gather_samples(*last["r"])
         torch.cuda.synchronize(dev)
         gather_ms = 1000 * (time.perf_counter() - t0)
 
-    # ---------------- cfg5: the B200-native zero-copy OOM variant (NEXT-4), reported apart
+    # ---------------- OOM configs: measured host-link peak + the zero-copy variant (NEXT-4)
+    h2d_peak = measure_h2d_peak(dev) if oom else None
     zc = None
     if oom and not args.no_zerocopy and args.oom_variant != "zerocopy":
-        try:
-            Gz = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, budget_bytes=cfg.oom_budget_bytes,
-                                      num_partitions=cfg.oom_partitions, max_resident=1, zerocopy=True)
-            if kind == "walk":
-                outz = torch.empty((n, cfg.length, 2), dtype=torch.int32, device=dev)
-
-                def zstep():
-                    cs.csaw_walk(Gz, bias, seeds, cfg.length, instance_base=base, rng_seed=args.rng_seed, out=outz,
-                                 stream=stream)
-                    return n * cfg.length
-
-                def zsame():
-                    return bool(torch.equal(outz, out_dev))
-            else:
-                zr = []
-
-                def zstep():
-                    zr[:] = cs.csaw_sample(Gz, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth,
-                                           instance_base=base, rng_seed=args.rng_seed, stream=stream)
-                    return int(zr[1].numel())
-
-                def zsame():
-                    ref = r_last(cs, G, bias, seeds, cfg, base, args, stream)
-                    return all(bool(torch.equal(a, b)) for a, b in zip(ref, zr))
-            zstep()
-            torch.cuda.synchronize(dev)
-            zt, ze = [], 0
-            for _ in range(max(1, args.steps)):
-                flush.fill_(1)
-                z0 = torch.cuda.Event(enable_timing=True)
-                z1 = torch.cuda.Event(enable_timing=True)
-                z0.record(stream)
-                ze += zstep()
-                z1.record(stream)
-                torch.cuda.synchronize(dev)
-                zt.append(z0.elapsed_time(z1))
-            zc = {"value": ze / (sum(zt) / 1000.0), "unit": UNIT, "ms_per_step": sum(zt) / len(zt),
-                  "identical_to_partitioned": zsame(),
-                  "what": "OOM zero-copy: col_idx read in place from pinned host memory, same 8 GB budget (NEXT-4)"}
-            Gz.close()
-        except Exception as ex:
-            zc = {"error": str(ex)}
+        zc = run_zerocopy(cs, g, cfg, bias, seeds, base, rng_seeds[0], kind, n, dev, local, stream, flush,
+                          out_dev if kind == "walk" else None, last.get("r"), G, args)
 
     # ---------------- end-to-end through the C ABI with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(cs, G, bias, seeds, cfg, base, args, kind, n, dev, world)
+        e2e = run_e2e(cs, G, bias, seeds, cfg, base, rng_seeds, args, kind, n, dev, world, flush, oom)
 
     # ---------------- roofline of the hot kernel
     peaks = load_peaks()
     hot_avg_ms = hot_ms / max(hot_launches, 1)
-    bytes_per_launch = alg_bytes / max(hot_launches, 1)
-    achieved = bytes_per_launch / (hot_avg_ms / 1000.0) / 1e9 if hot_avg_ms > 0 else None
-    peak = peaks.get("hbm_gbs", 6650.0)
-    variant = cfg.name
-    if cfg.oom_budget_bytes and args.in_memory:
-        variant += "_inmem"
-    elif not ginfo.get("ctps_cache") and cfg.bias in ("degree", "layer") and not ginfo.get("oom_mode"):
+    variant = cfg.name + ("_inmem" if cfg.oom_budget_bytes and args.in_memory else "")
+    if not oom and not ginfo.get("ctps_cache") and cfg.bias in ("degree", "layer"):
         variant += "_scan"
+    if cfg.workload == "node2vec" and not ginfo.get("node2vec_tri"):
+        variant += "_merge"
     kname = hot_kernel_name(cfg, bool(ginfo.get("node2vec_tri") if cfg.workload == "node2vec" else ginfo.get("ctps_cache")),
-                            bool(ginfo.get("oom_mode")) and args.oom_variant != "zerocopy",
-                            int(ginfo.get("walk_index_leaf") or 0), int(ginfo.get("walk_index_group") or 0),
-                            bool(ginfo.get("walk_index_heads")))
-    traffic = load_traffic(variant, kname)
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": kname, "alg_bytes_per_launch": bytes_per_launch,
-            "hot_ms_per_launch": hot_avg_ms, "hot_share_of_step": (hot_ms / total_ms) if total_ms else None,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
+                            oom and args.oom_variant != "zerocopy", int(ginfo.get("walk_index_leaf") or 0),
+                            int(ginfo.get("walk_index_group") or 0), bool(ginfo.get("walk_index_heads")))
+    ncu = load_ncu(variant, kname)
+    if oom:
+        ach = (h2d_bytes / (total_ms / 1000.0) / 1e9) if h2d_bytes else None
+        roof = {"bound": "host-link", "achieved": ach, "peak": h2d_peak, "unit": "GB/s",
+                "frac": (ach / h2d_peak) if ach and h2d_peak else None, "traffic": None,
+                "kernel": kname, "bytes_model": BYTES_MODEL["oom_host"],
+                "h2d_bytes_per_step": h2d_bytes / max(args.steps, 1),
+                "transfer_ms_per_step": transfer_ms / max(args.steps, 1),
+                "peak_source": "pinned cudaMemcpyAsync H2D, 1 GiB, best of 5, measured in this run",
+                "host_link_peak_gbs": h2d_peak}
+    else:
+        bytes_per_launch = alg_bytes / max(hot_launches, 1)
+        achieved = bytes_per_launch / (hot_avg_ms / 1000.0) / 1e9 if hot_avg_ms > 0 else None
+        peak = peaks.get("hbm_gbs", 7672.0)
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": ncu.get("dram_bytes_per_launch"),
+                "f_dram": ncu.get("f_dram"), "l2_sector_eff": ncu.get("l2_sector_eff"),
+                "ncu_round": ncu.get("round"),
+                "kernel": kname, "bytes_model": BYTES_MODEL[model], "alg_bytes_per_launch": bytes_per_launch,
+                "kernel_requested_bytes_per_launch": (kbytes / max(hot_launches, 1)) if kbytes else None,
+                "hot_ms_per_launch": hot_avg_ms, "hot_share_of_step": (hot_ms / total_ms) if total_ms else None,
+                "peak_source": ("MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)" if "hbm_gbs" in peaks
+                                else "fallback: B200_PROFILING.md")}
 
     # ---------------- oracle CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -543,29 +656,33 @@ def main():
             og = O.Graph.from_torch(g)
             sv = seeds.cpu().numpy()
             sv = sv.view(np.uint32) if sv.dtype == np.int32 else sv.astype(np.uint32)
-            v, cores, sample, _, _ = oracle_timed_sample(cfg, og, sv, base, args.rng_seed, args.cpu_seconds)
+            v, cores, sample, _, _ = oracle_timed_sample(cfg, og, sv, base, rng_seeds[0], args.cpu_seconds)
             cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
         except Exception as ex:  # report, never hide
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": f"failed: {ex}"}
 
     if rank == 0:
+        ms_step = total_ms / max(args.steps, 1)
+        build_ms = float(ginfo.get("cache_build_ms") or 0.0)
+        eps = edges_all / max(args.steps, 1)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": total_ms / max(args.steps, 1), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "u32",
                 "data": "synthetic (seeded R-MAT + seeds from synth/; no datasets)",
-                "config": config_block(cfg, world, gstats, oom_mode=(args.oom_variant if oom else None),
-                                       colc=ginfo.get("device_bytes")), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk,
-                "detail": {"edges_per_step_per_gpu": edges / max(args.steps, 1), "step_ms": step_ms,
-                           "graph_gen_s": gen_s, "gather_ms": gather_ms,
-                           "ctps_cache": bool(ginfo.get("ctps_cache")), "cache_build_ms": ginfo.get("cache_build_ms"),
+                "config": config_block(cfg, world, gstats, args.scaling, n_total,
+                                       oom_mode=(args.oom_variant if oom else None), colc=ginfo.get("device_bytes")),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+                "detail": {"edges_per_step": eps, "edges_per_step_rank0": edges / max(args.steps, 1),
+                           "step_ms": step_ms, "rng_seeds": rng_seeds, "graph_gen_s": gen_s, "gather_ms": gather_ms,
+                           "cache": {"ctps_cache": bool(ginfo.get("ctps_cache")),
+                                     "node2vec_tri": bool(ginfo.get("node2vec_tri")),
+                                     "build_ms": build_ms,
+                                     "one_call_seps": eps / ((ms_step + build_ms) / 1000.0),
+                                     "calls_to_amortise_build": (build_ms / ms_step) if ms_step else None,
+                                     "note": "one_call_seps = edges of one step / (step time + the graph's cache "
+                                             "build, P:784-786 computes its cache during sampling)"},
                            "oom": bool(ginfo.get("oom_mode")),
                            "partition_loads_per_step": st_last["partition_loads"] if st_last else None,
-                           "h2d_bytes_per_step": st_last["h2d_bytes"] if st_last else None,
-                           "transfer_ms_per_step": st_last["transfer_ms"] if st_last else None,
-                           "host_link_gbs": (st_last["h2d_bytes"] / st_last["transfer_ms"] / 1e6)
-                           if st_last and st_last["transfer_ms"] else None,
-                           "cache_probes_per_step": st_last["cache_probes"] if st_last else None,
                            "oom_zerocopy": zc,
                            "neighbours_scanned_per_step": st_last["neighbours_scanned"] if st_last else None,
                            "pools_per_step": st_last["pools"] if st_last else None}}
@@ -578,26 +695,76 @@ def main():
     return 0
 
 
-def r_last(cs, G, bias, seeds, cfg, base, args, stream):
-    return cs.csaw_sample(G, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth, instance_base=base,
-                          rng_seed=args.rng_seed, stream=stream)
+def run_zerocopy(cs, g, cfg, bias, seeds, base, seed, kind, n, dev, local, stream, flush, out_ref, r_ref, G, args):
+    """cfg5: the zero-copy OOM variant under the same budget, reported apart (NEXT-4)."""
+    try:
+        Gz = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, budget_bytes=cfg.oom_budget_bytes,
+                                  num_partitions=cfg.oom_partitions, max_resident=1, zerocopy=True)
+        if kind == "walk":
+            outz = torch.empty(out_ref.shape, dtype=torch.int32, device=dev)
+
+            def zstep():
+                cs.csaw_walk(Gz, bias, seeds, cfg.length, instance_base=base, rng_seed=seed, out=outz, stream=stream)
+                return n * cfg.length
+
+            def zsame():
+                cs.csaw_walk(G, bias, seeds, cfg.length, instance_base=base, rng_seed=seed, out=out_ref, stream=stream)
+                return bool(torch.equal(outz, out_ref))
+        else:
+            zr = []
+
+            def zstep():
+                zr[:] = cs.csaw_sample(Gz, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth,
+                                       instance_base=base, rng_seed=seed, stream=stream)
+                return int(zr[1].numel())
+
+            def zsame():
+                ref = cs.csaw_sample(G, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth, instance_base=base,
+                                     rng_seed=seed, stream=stream)
+                return all(bool(torch.equal(a, b)) for a, b in zip(ref, zr))
+        zstep()
+        torch.cuda.synchronize(dev)
+        zt, ze, zh = [], 0, 0
+        for _ in range(max(1, args.steps)):
+            flush.fill_(1)
+            z0 = torch.cuda.Event(enable_timing=True)
+            z1 = torch.cuda.Event(enable_timing=True)
+            z0.record(stream)
+            ze += zstep()
+            z1.record(stream)
+            torch.cuda.synchronize(dev)
+            zt.append(z0.elapsed_time(z1))
+            zh += cs.csaw_stats(Gz)["h2d_bytes"]
+        res = {"value": ze / (sum(zt) / 1000.0), "unit": UNIT, "ms_per_step": sum(zt) / len(zt),
+               "device_bytes": Gz.info()["device_bytes"], "h2d_bytes_per_step": zh / len(zt),
+               "identical_to_partitioned": zsame(),
+               "what": "OOM zero-copy: col_idx prefix resident, the rest read in place from pinned host memory, "
+                       "same 8 GB budget (NEXT-4)"}
+        Gz.close()
+        return res
+    except Exception as ex:
+        return {"error": str(ex)}
 
 
-def run_e2e(cs, G, bias, seeds, cfg, base, args, kind, n, dev, world):
+def run_e2e(cs, G, bias, seeds, cfg, base, rng_seeds, args, kind, n, dev, world, flush, oom):
     """Same metric through the C ABI with pinned HOST buffers: the library copies the
-    step's seeds host->device and the step's result device->host inside the call."""
+    step's seeds host->device and writes the step's result into host memory inside the
+    call.  Timed like `value`: L2 flushed before every step, same step count (OOM
+    partition mode: at most 2 steps), host wall clock around the synchronous call."""
     seeds_h = seeds.cpu().pin_memory()
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 2) if oom else args.steps)
     times = []
     edges = 0
     if kind == "walk":
         shape = (n, cfg.length, 2) if cfg.workload == "mdrw" else (n, cfg.length + 1)
         out_h = torch.empty(shape, dtype=torch.int32).pin_memory()
-        cs.csaw_walk(G, bias, seeds_h, cfg.length, instance_base=base, rng_seed=args.rng_seed, out=out_h)
-        for _ in range(steps):
+        cs.csaw_walk(G, bias, seeds_h, cfg.length, instance_base=base, rng_seed=rng_seeds[0], out=out_h)
+        for i in range(steps):
+            flush.fill_(1)
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
-            cs.csaw_walk(G, bias, seeds_h, cfg.length, instance_base=base, rng_seed=args.rng_seed, out=out_h)
+            cs.csaw_walk(G, bias, seeds_h, cfg.length, instance_base=base, rng_seed=rng_seeds[i % len(rng_seeds)],
+                         out=out_h)
             times.append(time.perf_counter() - t0)
             edges += n * cfg.length
         h2d = seeds_h.numel() * 4
@@ -607,17 +774,19 @@ def run_e2e(cs, G, bias, seeds, cfg, base, args, kind, n, dev, world):
         out_h = [torch.empty(n + 1, dtype=torch.int64).pin_memory(), torch.empty(cap, dtype=torch.int32).pin_memory(),
                  torch.empty(cap, dtype=torch.int32).pin_memory(), torch.empty(cap, dtype=torch.uint8).pin_memory()]
         r = cs.csaw_sample(G, bias, seeds_h, fanout=list(cfg.fanout), depth=cfg.depth, instance_base=base,
-                           rng_seed=args.rng_seed, out=out_h)
-        m = r[1].numel()
-        for _ in range(steps):
+                           rng_seed=rng_seeds[0], out=out_h)
+        m = 0
+        for i in range(steps):
+            flush.fill_(1)
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
             r = cs.csaw_sample(G, bias, seeds_h, fanout=list(cfg.fanout), depth=cfg.depth, instance_base=base,
-                               rng_seed=args.rng_seed, out=out_h)
+                               rng_seed=rng_seeds[i % len(rng_seeds)], out=out_h)
             times.append(time.perf_counter() - t0)
             edges += r[1].numel()
+            m += r[1].numel()
         h2d = seeds_h.numel() * 4
-        d2h = (n + 1) * 8 + m * 9
+        d2h = (n + 1) * 8 + (m / steps) * 9
     t = sum(times)
     if world > 1:
         import torch.distributed as dist
@@ -627,7 +796,8 @@ def run_e2e(cs, G, bias, seeds, cfg, base, args, kind, n, dev, world):
         dist.all_reduce(ee, op=dist.ReduceOp.SUM)
         t, edges = float(tt.item()), int(ee.item())
     return {"value": edges / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "steps": steps, "timing": "host wall clock around the synchronous C-ABI call (max over ranks)"}
+            "steps": steps, "timing": "host wall clock around the synchronous C-ABI call, L2 flushed before each "
+                                      "step (max over ranks)"}
 
 
 def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads=False):
@@ -642,9 +812,7 @@ def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads
     if cfg.workload == "node2vec":
         return "k_node2vec_tri" if cached else "k_node2vec<int>"
     if oom:
-        # OOM traversal sampling runs the batched level driver, one select launch per resident partition
         return "k_ns_select<1>" if cfg.bias == "degree" else "k_ns_select<0>"
-    # sampling: the fused one-warp-per-instance kernel (small per-instance frontiers)
     mode = {"neighbor": 2 if cached else 1, "forest_fire": 3, "layer": 5 if cached else 4}[cfg.workload]
     if cfg.workload == "neighbor" and cfg.bias == "uniform":
         mode = 0
@@ -659,24 +827,23 @@ def load_peaks() -> dict:
         return {}
 
 
-def load_traffic(cfg_name, kernel):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the hot kernel, from the
-    committed ncu --set full capture summary (profiles/ncu_traffic.json), else null.  Only
-    a capture of the same kernel counts (a stale entry for another variant is ignored)."""
+def load_ncu(cfg_name, kernel) -> dict:
+    """DRAM bytes per launch, f_dram and L2 sector efficiency of the hot kernel from the
+    committed ncu --set full capture summary (profiles/ncu_traffic.json, written by
+    scripts/ncu_summary.py); {} unless the capture is of the same kernel."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
         v = d.get(cfg_name)
         if not isinstance(v, dict):
-            return None
+            return {}
         norm = lambda k: k.replace("void ", "").replace("csaw::", "").replace(" ", "")
         a, b = norm(v.get("kernel", "")), norm(kernel)
-        # same kernel; template arguments must agree when both names carry them
         if a.split("<")[0] != b.split("<")[0] or ("<" in a and "<" in b and a != b):
-            return None
-        return v.get("dram_bytes_per_launch")
+            return {}
+        return v
     except Exception:
-        return None
+        return {}
 
 
 if __name__ == "__main__":

@@ -40,9 +40,10 @@ def _ptr(t) -> int:
     raise TypeError(f"unsupported buffer type {type(t)}")
 
 
-def _stream_ptr(stream) -> int:
+def _stream_ptr(stream, device: int = 0) -> int:
+    """None -> the current torch stream of the graph's device."""
     if stream is None:
-        return torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else 0
+        return torch.cuda.current_stream(device).cuda_stream if torch.cuda.is_available() else 0
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
@@ -164,7 +165,7 @@ def csaw_sample(g: Graph, bias, seeds, fanout=(), depth=None, instance_base=0, r
     ne = C.c_int64()
     st = check(lib().csaw_sample(g.handle, C.byref(b), fan, depth, _ptr(seeds), n, instance_base, rng_seed,
                                  _ptr(offs), _ptr(src), _ptr(dst), _ptr(dep), capacity, C.byref(ne),
-                                 C.c_void_p(_stream_ptr(stream))), allow=(CSAW_OK, CSAW_ERR_CAPACITY))
+                                 C.c_void_p(_stream_ptr(stream, g.device))), allow=(CSAW_OK, CSAW_ERR_CAPACITY))
     if st == CSAW_ERR_CAPACITY:
         if out is not None:
             raise CsawError(st, lib().csaw_last_error().decode())
@@ -188,7 +189,7 @@ def csaw_walk(g: Graph, bias, seeds, length: int, instance_base=0, rng_seed=1, o
         dev = seeds.device if isinstance(seeds, torch.Tensor) else torch.device("cpu")
         out = torch.empty(shape, dtype=torch.int32, device=dev)
     check(lib().csaw_walk(g.handle, C.byref(b), length, _ptr(seeds), n, instance_base, rng_seed, _ptr(out),
-                          C.c_void_p(_stream_ptr(stream))))
+                          C.c_void_p(_stream_ptr(stream, g.device))))
     return out
 
 

@@ -92,15 +92,27 @@ csaw_status PinnedBuf::get(size_t bytes, void** out) {
     return CSAW_OK;
 }
 
-bool is_device_ptr(const void* p, int device) {
-    if (!p) return false;
+PtrKind ptr_kind(const void* p, int device) {
+    if (!p) return PtrKind::Pageable;
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
-        return false;
+        return PtrKind::Pageable;
     }
-    (void)device;
-    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+    if (a.type == cudaMemoryTypeDevice) return a.device == device ? PtrKind::Device : PtrKind::OtherDevice;
+    if (a.type == cudaMemoryTypeManaged) return PtrKind::Device;
+    if (a.type == cudaMemoryTypeHost) return PtrKind::Pinned;
+    return PtrKind::Pageable;
+}
+
+bool is_device_ptr(const void* p, int device) { return ptr_kind(p, device) == PtrKind::Device; }
+
+CallOrder::CallOrder(const csaw_graph* g_, cudaStream_t st_) : g(g_), st(st_) {
+    if (g && g->ev_done) cudaStreamWaitEvent(st, g->ev_done, 0);
+}
+
+CallOrder::~CallOrder() {
+    if (g && g->ev_done) cudaEventRecord(g->ev_done, st);
 }
 
 // Device-side address of pinned (page-locked) host memory, or nullptr for pageable memory.
@@ -797,6 +809,7 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
     }
     CREATE_CUDA(cudaEventCreate(&g->ev0), "event");
     CREATE_CUDA(cudaEventCreate(&g->ev1), "event");
+    CREATE_CUDA(cudaEventCreateWithFlags(&g->ev_done, cudaEventDisableTiming), "event");
     CREATE_CUDA(cudaDeviceSynchronize(), "graph_create");
 #undef CREATE_CUDA
     *out = g;
@@ -829,6 +842,7 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     for (auto s : st.streams) cudaStreamDestroy(s);
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
+    if (g->ev_done) cudaEventDestroy(g->ev_done);
     g->scratch.release_all();
     delete g;
     return CSAW_OK;
@@ -955,8 +969,12 @@ CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32
     const int64_t nseeds = b.kind == CSAW_BIAS_MDRW ? n * static_cast<int64_t>(b.pool_size) : n;
     const int64_t nout = b.kind == CSAW_BIAS_MDRW ? n * static_cast<int64_t>(length) * 2
                                                   : n * (static_cast<int64_t>(length) + 1);
-    const bool seeds_dev = is_device_ptr(seeds, g->device);
-    const bool path_dev = is_device_ptr(path, g->device);
+    const PtrKind ks = ptr_kind(seeds, g->device), kp = ptr_kind(path, g->device);
+    if (ks == PtrKind::OtherDevice || kp == PtrKind::OtherDevice)
+        return fail(CSAW_ERR_INVALID_ARG, "seeds/path live on another GPU than the graph");
+    const bool seeds_dev = ks == PtrKind::Device;
+    const bool path_dev = kp == PtrKind::Device;
+    CallOrder order(g, st);
     const uint32_t* d_seeds = seeds;
     uint32_t* d_path = path;
     if (!seeds_dev) {
@@ -1034,10 +1052,20 @@ CSAW_API csaw_status csaw_sample(const csaw_graph* g, const csaw_bias* bias, con
     if (!offsets) return fail(CSAW_ERR_INVALID_ARG, "offsets is NULL");
     if (n > 0 && !seeds) return fail(CSAW_ERR_INVALID_ARG, "seeds is NULL");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const bool seeds_dev = n == 0 || is_device_ptr(seeds, g->device);
-    const bool offs_dev = is_device_ptr(offsets, g->device);
-    const bool out_dev = capacity == 0 || is_device_ptr(dst, g->device);
     if (capacity > 0 && (!src || !dst || !edge_depth)) return fail(CSAW_ERR_INVALID_ARG, "src/dst/edge_depth is NULL");
+    const PtrKind ks = n == 0 ? PtrKind::Device : ptr_kind(seeds, g->device);
+    const PtrKind ko = ptr_kind(offsets, g->device);
+    const PtrKind kd = capacity == 0 ? PtrKind::Device : ptr_kind(dst, g->device);
+    if (ks == PtrKind::OtherDevice || ko == PtrKind::OtherDevice || kd == PtrKind::OtherDevice)
+        return fail(CSAW_ERR_INVALID_ARG, "seeds/offsets/outputs live on another GPU than the graph");
+    // src, dst and edge_depth are written by the same kernels: they must share one location class
+    if (capacity > 0 && (ptr_kind(src, g->device) != kd || ptr_kind(edge_depth, g->device) != kd))
+        return fail(CSAW_ERR_INVALID_ARG, "src, dst and edge_depth must all be device, all pinned or all pageable host "
+                                          "buffers");
+    const bool seeds_dev = ks == PtrKind::Device;
+    const bool offs_dev = ko == PtrKind::Device;
+    const bool out_dev = kd == PtrKind::Device;
+    CallOrder order(g, st);
     const uint32_t* d_seeds = seeds;
     if (!seeds_dev) {
         void* p;

@@ -147,6 +147,9 @@ struct csaw_graph {
     mutable csaw::PinnedBuf pinned;
     mutable csaw_run_stats stats{};
     mutable cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // completion of the previous call's work on its stream: every call's stream waits on
+    // it first, so calls on different streams never overlap on the shared scratch
+    mutable cudaEvent_t ev_done = nullptr;
     // hot-kernel timing: event pairs recorded around each selection-kernel launch
     mutable std::vector<cudaEvent_t> hot_ev;
     mutable int hot_used = 0;
@@ -164,8 +167,21 @@ enum Slot : int {
     SL_MAX = 16 + 256 * 16
 };
 
+// Where a caller buffer lives: device memory of the graph's GPU, of another GPU (an
+// error: kernels on g->device cannot dereference it without peer access), pinned
+// (page-locked, device-mapped) host memory, or pageable host memory.
+enum class PtrKind { Device, OtherDevice, Pinned, Pageable };
+PtrKind ptr_kind(const void* p, int device);
 bool is_device_ptr(const void* p, int device);
 csaw_status begin_call(const csaw_graph* g);
+// Orders a call after the previous one on the same graph (any stream) and records the
+// call's completion on its stream when the guard goes out of scope.
+struct CallOrder {
+    const csaw_graph* g;
+    cudaStream_t st;
+    CallOrder(const csaw_graph* g_, cudaStream_t st_);
+    ~CallOrder();
+};
 
 // kernels launched by the current call (per host thread)
 extern thread_local uint64_t tl_launches;

@@ -97,7 +97,9 @@ def main():
         else:
             note = "per launch of the bench's hot kernel (1 bench step)"
         traffic[key] = {"kernel": d["kernel"], "dram_bytes_per_launch": int(dram), "ncu_ms": d["time"] * 1e3,
-                        "round": rnd, "note": note}
+                        "f_dram": gbs / peak,
+                        "l2_sector_eff": (d["bytes_per_sector"] / 32.0) if "bytes_per_sector" in d else None,
+                        "l2_hit_pct": d.get("l2_hit"), "round": rnd, "note": note}
     # metrics-only launch lists with DRAM counters (cfg3: the full bench launch, too long for --set full)
     for path in sorted(glob.glob(os.path.join(src, "*_launches.csv"))):
         cfg = os.path.basename(path)[:-len("_launches.csv")]
@@ -118,8 +120,12 @@ def main():
             dram = m["dram__bytes_read.sum"] + m.get("dram__bytes_write.sum", 0.0)
             t = m.get("gpu__time_duration.sum", 0.0) * 1e-9
             key = cfg.replace("@", "_")
+            prev = traffic.get(key, {}) if traffic.get(key, {}).get("round") == rnd else {}
             traffic[key] = {"kernel": kname, "dram_bytes_per_launch": int(dram), "ncu_ms": t * 1e3, "round": rnd,
-                            "note": "metrics-only pass (dram__bytes_read/write.sum) over the bench's timed launch"}
+                            "f_dram": (dram / t / 1e9 / peak) if t > 0 else None,
+                            "l2_sector_eff": prev.get("l2_sector_eff"), "l2_hit_pct": prev.get("l2_hit_pct"),
+                            "note": "metrics-only pass (dram__bytes_read/write.sum) over the bench's timed launch; "
+                                    "sector efficiency from the --set full capture of the same round"}
             if t > 0:
                 out.append(f"| {cfg} (metrics-only, full launch) | `{kname}` | {t * 1e3:.3f} | {dram / 1e9:.3f} GB | "
                            f"{dram / t / 1e9:.0f} ({dram / t / 1e9 / peak:.3f}) | | | | | | | | |")
