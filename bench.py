@@ -154,6 +154,9 @@ BYTES_MODEL = {
     "walk_uniform": "16 (row_ptr pair) + 4 (one col entry) + 4 (path) per step",
     "node2vec": "SURVEY §8(d) node2vec step: 16 + 4 d(v) + 4 (N(prev) carried from the previous step); "
                 "step 0 uniform: 16 + 4 + 4",
+    "node2vec_index": "NEXT-1-style sector model of the node2vec intersection index: 32 B sectors x (the 64 B "
+                      "record of the entry the walker arrived by (2 sectors) + the binary-search probes between its "
+                      "splitters) per step + 4 (path); probes counted in the kernel",
     "mdrw": "SURVEY §8(d) MDRW step: 16 (row_ptr v) + 4 (col) + 4 (deg u) + 8 (edge out) = 32",
     "sample_degree": "SURVEY §8(d) degree-biased pool: 16 + 8 d(v) per expanded vertex + 9 per emitted edge",
     "sample_layer": "SURVEY §8(d) layer: sum over levels and frontier vertices of 16 + 8 d(v) + 9 per edge",
@@ -474,7 +477,7 @@ def main():
         use_tri = (not args.no_cache) and cfg.workload == "node2vec"
         use_meta = (not args.no_cache) and cfg.workload == "mdrw"
         G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache, node2vec_tri=use_tri,
-                                 next_meta=use_meta, walk_index=use_cache)
+                                 next_meta=use_meta, walk_index=use_cache, node2vec_index=use_tri)
     ginfo = G.info()
     bias = bias_of(cs, cfg)
     stream = torch.cuda.current_stream(dev)
@@ -581,7 +584,9 @@ def main():
                 continue
             step(s)
             torch.cuda.synchronize(dev)
-            if kind == "walk":
+            if kind == "walk" and ginfo.get("node2vec_index") and cfg.workload == "node2vec":
+                b, model = cs.csaw_stats(G)["index_bytes"], "node2vec_index"
+            elif kind == "walk":
                 b, model = walk_alg_bytes(cfg, deg, out_dev, cached)
             else:
                 b, model = sample_alg_bytes(cfg, deg, seeds, *last["r"])
@@ -617,11 +622,12 @@ def main():
     variant = cfg.name + ("_inmem" if cfg.oom_budget_bytes and args.in_memory else "")
     if not oom and not ginfo.get("ctps_cache") and cfg.bias in ("degree", "layer"):
         variant += "_scan"
-    if cfg.workload == "node2vec" and not ginfo.get("node2vec_tri"):
+    if cfg.workload == "node2vec" and not ginfo.get("node2vec_tri") and not ginfo.get("node2vec_index"):
         variant += "_merge"
     kname = hot_kernel_name(cfg, bool(ginfo.get("node2vec_tri") if cfg.workload == "node2vec" else ginfo.get("ctps_cache")),
                             oom and args.oom_variant != "zerocopy", int(ginfo.get("walk_index_leaf") or 0),
-                            int(ginfo.get("walk_index_group") or 0), bool(ginfo.get("walk_index_heads")))
+                            int(ginfo.get("walk_index_group") or 0), bool(ginfo.get("walk_index_heads")),
+                            bool(ginfo.get("node2vec_index")))
     ncu = load_ncu(variant, kname)
     if oom:
         ach = (h2d_bytes / (total_ms / 1000.0) / 1e9) if h2d_bytes else None
@@ -676,6 +682,8 @@ def main():
                            "step_ms": step_ms, "rng_seeds": rng_seeds, "graph_gen_s": gen_s, "gather_ms": gather_ms,
                            "cache": {"ctps_cache": bool(ginfo.get("ctps_cache")),
                                      "node2vec_tri": bool(ginfo.get("node2vec_tri")),
+                                     "node2vec_index": bool(ginfo.get("node2vec_index")),
+                                     "graph_device_bytes": ginfo.get("device_bytes"),
                                      "build_ms": build_ms,
                                      "one_call_seps": eps / ((ms_step + build_ms) / 1000.0),
                                      "calls_to_amortise_build": (build_ms / ms_step) if ms_step else None,
@@ -800,7 +808,7 @@ def run_e2e(cs, G, bias, seeds, cfg, base, rng_seeds, args, kind, n, dev, world,
                                       "step (max over ranks)"}
 
 
-def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads=False):
+def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads=False, n2x=False):
     if cfg.workload == "walk":
         if cfg.bias == "degree" and wix_leaf and heads and wix_group == 32:
             return f"k_walk_head<{wix_leaf}>"
@@ -810,6 +818,8 @@ def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads
     if cfg.workload == "mdrw":
         return "k_mdrw_oom_part" if oom else ("k_mdrw_fast" if cfg.pool_size <= 2048 else "k_mdrw")
     if cfg.workload == "node2vec":
+        if n2x:
+            return "k_node2vec_idx"
         return "k_node2vec_tri" if cached else "k_node2vec<int>"
     if oom:
         return "k_ns_select<1>" if cfg.bias == "degree" else "k_ns_select<0>"

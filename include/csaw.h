@@ -167,6 +167,16 @@ typedef struct {
  * chunk table instead of scanning the whole pool and rescan one chunk per draw.  Results
  * are identical. */
 #define CSAW_GRAPH_CHUNK_CACHE 0x100u
+/* csaw_graph_opts.flags (in-memory graphs with sorted rows, max degree < 2^24; used only
+ * if the graph is symmetric): node2vec per-edge intersection index.  For every CSR entry
+ * e = (prev -> v): the count C of common neighbours N(v) ∩ N(prev), the position of prev in
+ * N(v), and the ascending positions in N(v) of the common neighbours (16 B per entry + 4 B
+ * per common neighbour pair; ~53 GB for the cfg3 graph).  Integer node2vec walks
+ * (R16) then binary-search those positions for the region of the draw (the CTPS
+ * is piecewise linear between them) instead of merging N(v) with N(prev): O(log C) reads
+ * per step.  Picks are identical.  Best-effort: if the index does not fit, the graph is
+ * created without it (csaw_graph_info_t.node2vec_index = 0). */
+#define CSAW_GRAPH_N2V_INDEX 0x200u
 
 typedef struct {
     int64_t num_vertices, num_edges;
@@ -181,7 +191,7 @@ typedef struct {
     int32_t walk_index_group;       /* lanes per walker of the degree-walk kernel (8 / 16; 32 = one warp per walker) */
     int32_t node2vec_tri;           /* 1 if per-edge triangle counts were built (CSAW_GRAPH_N2V_TRI on a symmetric graph) */
     int32_t walk_index_heads;       /* 1 if the walk index has 512 B vertex heads (degree walks: k_walk_head) */
-    int32_t reserved;
+    int32_t node2vec_index;         /* 1 if the node2vec intersection index was built (CSAW_GRAPH_N2V_INDEX) */
 } csaw_graph_info_t;
 
 typedef struct csaw_graph csaw_graph;  /* opaque */

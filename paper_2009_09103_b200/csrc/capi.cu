@@ -792,7 +792,22 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         CREATE_CUDA(cudaMalloc(&g->nmp, sizeof(uint64_t) * E), "cudaMalloc(nmp)");
         k_build_nmp<<<blocks, 256>>>(g->row_ptr, g->col, E, g->nmp);
     }
-    if ((o.flags & CSAW_GRAPH_N2V_TRI) && !g->oom) {   // node2vec edge triangle counts (walk.cu k_node2vec_tri)
+    if ((o.flags & CSAW_GRAPH_N2V_INDEX) && !g->oom) {   // node2vec per-edge intersection index (n2v_index.cu)
+        cudaEvent_t c0, c1;
+        CREATE_CUDA(cudaEventCreate(&c0), "event");
+        CREATE_CUDA(cudaEventCreate(&c1), "event");
+        cudaEventRecord(c0);
+        const csaw_status xs = build_n2v_index(g, blocks);
+        cudaEventRecord(c1);
+        cudaEventSynchronize(c1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c0, c1);
+        cudaEventDestroy(c0);
+        cudaEventDestroy(c1);
+        if (xs != CSAW_OK) return cleanup(xs);
+        g->cache_build_ms += ms;
+    }
+    if ((o.flags & CSAW_GRAPH_N2V_TRI) && !g->oom && !g->n2x_rec) {   // node2vec edge triangle counts (k_node2vec_tri; not needed with the index)
         cudaEvent_t c0, c1;
         CREATE_CUDA(cudaEventCreate(&c0), "event");
         CREATE_CUDA(cudaEventCreate(&c1), "event");
@@ -832,6 +847,8 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->ccache) cudaFree(g->ccache);
     if (g->whead) cudaFree(g->whead);
     if (g->tri) cudaFree(g->tri);
+    if (g->n2x_rec) cudaFree(g->n2x_rec);
+    if (g->n2x_idx) cudaFree(g->n2x_idx);
     if (g->wcol) cudaFree(g->wcol);
     if (g->winn) cudaFree(g->winn);
     auto& st = g->oomst;
@@ -865,6 +882,7 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
                         (g->wix_leaf ? static_cast<int64_t>(sizeof(uint32_t) * (2 * g->wleaf_entries + g->winn_entries) + sizeof(uint4) * g->V) : 0) +
                         (g->whead ? static_cast<int64_t>(sizeof(uint32_t)) * WIX_HEAD_WORDS * g->V : 0) +
                         (g->tri ? static_cast<int64_t>(sizeof(uint32_t) * g->E) : 0) +
+                        (g->n2x_rec ? static_cast<int64_t>(4 * sizeof(uint4) * g->E + sizeof(uint32_t) * g->n2x_total) : 0) +
                         (g->nmp ? static_cast<int64_t>(sizeof(uint64_t) * g->E) : 0) +
                         static_cast<int64_t>(sizeof(uint64_t) * g->ccache_entries);
     out->ctps_cache = g->cps ? 1 : 0;
@@ -872,7 +890,7 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
     out->walk_index_group = g->wix_leaf ? g->wix_group : 0;
     out->node2vec_tri = g->tri ? 1 : 0;
     out->walk_index_heads = g->whead ? 1 : 0;
-    out->reserved = 0;
+    out->node2vec_index = g->n2x_rec ? 1 : 0;
     out->cache_build_ms = g->cache_build_ms;
     return CSAW_OK;
 }

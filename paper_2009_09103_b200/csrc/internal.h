@@ -137,6 +137,10 @@ struct csaw_graph {
     uint64_t* ccache = nullptr;   // chunk-total cache of the degree bias (select.cuh; rows of d > TAB)
     uint64_t ccache_entries = 0;
     uint32_t* tri = nullptr;      // [E] node2vec: |N(v) ∩ N(u)| per entry (symmetric sorted graphs, cache builds)
+    // node2vec per-edge intersection index (n2v_index.cu, CSAW_GRAPH_N2V_INDEX)
+    uint4* n2x_rec = nullptr;     // [4 E] {offset lo, offset hi 8 | C << 8, ppos, mb}, {v, row lo, row hi 8 | deg << 8, 0}, P[8]
+    uint32_t* n2x_idx = nullptr;  // member positions, n2x_total entries
+    uint64_t n2x_total = 0;
     int wix_group = 8;            // lanes per walker in k_walk_wixg (32 = k_walk_wix, one warp per walker)
     int wix_leaf = 0;             // leaf fanout 32 / 64 / 128 (0 = not built)
     double cache_build_ms = 0.0;
@@ -193,6 +197,12 @@ csaw_status hot_begin(const csaw_graph* g, cudaStream_t st);
 csaw_status hot_end(const csaw_graph* g, cudaStream_t st);
 // end a call: records ev1, stores the launch count
 csaw_status stats_end(const csaw_graph* g, cudaStream_t st);
+
+// n2v_index.cu
+csaw_status build_n2v_index(csaw_graph* g, int blocks);
+csaw_status launch_node2vec_index(const csaw_graph* g, const uint32_t* seeds, uint64_t n, int32_t L, uint32_t base,
+                                  uint2 key, uint32_t* path, unsigned long long* counters, uint32_t wp, uint32_t w1,
+                                  uint32_t wq, cudaStream_t st);
 
 // walk.cu / sample.cu entry points
 csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds,

@@ -1,0 +1,358 @@
+// n2v_index.cu — node2vec per-edge intersection index (CSAW_GRAPH_N2V_INDEX) and the
+// thread-per-walker node2vec kernel that searches it.
+//
+// A node2vec step at v arriving from prev (R16) selects from N(v) with the
+// integer biases wp (u == prev), w1 (u in N(prev)), wq (otherwise).  Its CTPS is
+// piecewise linear: S grows by wq per position except at the "specials" -- prev
+// itself and the common neighbours N(v) ∩ N(prev).  For a member at position p of
+// N(v) with j members before it,
+//     S(p) = wq p - (wq - w1) j - (wq - wp) [p > ppos]          (ppos = position of prev),
+// so the region of a draw x follows from the LAST special with S <= x and a closed
+// form between specials (the same algebra as k_node2vec_tri's n2t_specials).
+//
+// The specials depend only on the directed edge e = (prev -> v) -- a static property
+// of the graph, for any p and q -- so they are listed once per edge at graph creation
+// (the paper's deleted "caching transition probability", R25, applied to
+// the dynamic node2vec bias keyed by the edge the walker arrived by):
+//     rec[e] (64 B) = {index offset (40 bits) | C = |N(v) ∩ N(prev)| (24 bits), ppos, mb,
+//                      v = col[e], row start of v (40 bits) | deg(v) (24 bits), 0,
+//                      P[0..8)}
+//         mb = members before ppos (members with value < prev: rows are sorted)
+//         P  = the member positions themselves when C <= 8, else 8 splitters
+//              P[k] = I[j_k], j_k = floor((k + 1) C / 9)
+//     idx[off .. off + C) = ascending positions I in N(v) of the members (C > 8 only).
+// The record of the entry a walker arrived by carries everything the next step needs
+// (its vertex, row and degree, and the step's specials or their splitters), so a step
+// is one 64 B record and, for C > 8, a binary search of about log2(C / 9) probes
+// between two splitters: O(log C) dependent sectors instead of a merge of N(v) with
+// N(prev).  The pick is bit-identical to the full CTPS (same integer S, same draw) and
+// to the oracle.  Memory: 64 B per CSR entry + 4 B per (edge, common neighbour) pair of
+// the edges with C > 8; built only if it fits (best-effort).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+#include "util.cuh"
+
+namespace csaw {
+
+// ---------------------------------------------------------------- build
+// One warp per undirected edge {v, u} (entry e = (v -> u) with u > v, its reverse r =
+// (u -> v)).  The shorter list is walked in rows of 32; each entry's lower bound in the
+// longer list gives its position there.  Pass 1 (kList = false) writes the records'
+// C, ppos and mb; pass 2 lists the member positions into both edges' index ranges.
+template <bool kList>
+__global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                      const uint32_t* __restrict__ src, int64_t E, uint4* __restrict__ rec,
+                      uint32_t* __restrict__ idx, unsigned int* __restrict__ asym) {
+    const int lane = lane_id();
+    for (uint64_t e = global_warp_id(); e < static_cast<uint64_t>(E); e += total_warps()) {
+        const uint32_t v = src[e], u = col[e];
+        if (u == v) { if (lane == 0) atomicOr(asym, 1u); continue; }
+        if (u < v) continue;
+        const int64_t bv = rp[v], bu = rp[u];
+        const uint64_t dv = static_cast<uint64_t>(rp[v + 1] - bv), du = static_cast<uint64_t>(rp[u + 1] - bu);
+        const uint64_t j = warp_lower_bound(col + bu, 0, du, v);   // position of v in N(u)
+        if (!(j < du && __ldg(col + bu + j) == v)) { if (lane == 0) atomicOr(asym, 1u); continue; }
+        const uint64_t r = static_cast<uint64_t>(bu) + j;
+        const bool sv = dv <= du;                                   // N(v) is the shorter list
+        const uint32_t* small = col + (sv ? bv : bu);
+        const uint32_t* big = col + (sv ? bu : bv);
+        const uint64_t ns = sv ? dv : du, nb = sv ? du : dv;
+        uint64_t off_e = 0, off_r = 0;
+        uint32_t C_all = 0;
+        if (kList) {
+            const uint4 re = rec[4 * e], rr = rec[4 * r];
+            off_e = re.x | (static_cast<uint64_t>(re.y & 0xFFu) << 32);
+            off_r = rr.x | (static_cast<uint64_t>(rr.y & 0xFFu) << 32);
+            C_all = re.y >> 8;
+        }
+        uint32_t cnt = 0, below_v = 0, below_u = 0;
+        uint64_t lo0 = 0;
+        for (uint64_t r0 = 0; r0 < ns && lo0 < nb; r0 += 32) {
+            const uint64_t i = r0 + lane;
+            const bool valid = i < ns;
+            const uint32_t x = valid ? __ldg(small + i) : NONE;
+            const uint32_t xmin = __shfl_sync(FULL, x, 0);
+            const int last = static_cast<int>(ns - 1 - r0 < 31 ? ns - 1 - r0 : 31);
+            const uint32_t xmax = __shfl_sync(FULL, x, last);
+            const uint64_t lo = warp_lower_bound(big, lo0, nb, xmin);
+            const uint64_t hi = xmax == NONE ? nb : warp_lower_bound(big, lo, nb, xmax + 1u);
+            uint64_t l = lo, h = hi;
+            while (l < h) {   // same trip count on every lane
+                const uint64_t mid = (l + h) >> 1;
+                if (__ldg(big + mid) < x) l = mid + 1; else h = mid;
+            }
+            const bool f = valid && l < hi && __ldg(big + l) == x;
+            const unsigned m = __ballot_sync(FULL, f);
+            if (kList) {
+                if (f) {
+                    const uint32_t rank = cnt + __popc(m & lanemask_lt());
+                    const uint32_t pu = static_cast<uint32_t>(sv ? l : i), pv = static_cast<uint32_t>(sv ? i : l);
+                    if (C_all > 8) {   // entry e: positions in N(u); entry r: positions in N(v)
+                        idx[off_e + rank] = pu;
+                        idx[off_r + rank] = pv;
+                    } else {           // inline in the records
+                        reinterpret_cast<uint32_t*>(rec + 4 * e + 2)[rank] = pu;
+                        reinterpret_cast<uint32_t*>(rec + 4 * r + 2)[rank] = pv;
+                    }
+                }
+            } else {
+                below_v += __popc(__ballot_sync(FULL, f && x < v));
+                below_u += __popc(__ballot_sync(FULL, f && x < u));
+            }
+            cnt += __popc(m);
+            lo0 = hi;
+        }
+        if (!kList && lane == 0) {
+            // e = (v -> u): a walker at u that came from v; prev = v sits at position j of N(u)
+            rec[4 * e] = make_uint4(0u, cnt << 8, static_cast<uint32_t>(j), below_v);
+            // r = (u -> v): a walker at v that came from u; prev = u sits at position e - bv of N(v)
+            rec[4 * r] = make_uint4(0u, cnt << 8, static_cast<uint32_t>(e - static_cast<uint64_t>(bv)), below_u);
+        }
+    }
+}
+
+// exclusive scan of the listed member counts (C > 8) into the records' 40-bit offsets
+struct N2xCount {
+    const uint4* rec;
+    __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+        const uint32_t c = rec[4 * i].y >> 8;
+        return c > 8 ? c : 0;
+    }
+};
+struct N2xOffset {
+    uint4* rec;
+    unsigned long long* sum;
+    __device__ __forceinline__ void operator()(uint64_t i, uint64_t e, uint64_t) const {
+        rec[4 * i].x = static_cast<uint32_t>(e);
+        rec[4 * i].y = static_cast<uint32_t>(e >> 32) | (rec[4 * i].y & 0xFFFFFF00u);
+    }
+    __device__ __forceinline__ void total(uint64_t, uint64_t t) const { *sum = t; }
+};
+
+// rest of each record: the entry's vertex v = col[e], its row start and degree, and for
+// C > 8 the 8 splitters P[k] = I[floor((k + 1) C / 9)] (C <= 8: the list pass wrote P)
+__global__ void k_n2x_dst(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col, int64_t E,
+                          const uint32_t* __restrict__ idx, uint4* __restrict__ rec) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = col[e];
+        const uint64_t rs = static_cast<uint64_t>(rp[v]);
+        const uint32_t d = static_cast<uint32_t>(rp[v + 1] - rp[v]);
+        rec[4 * e + 1] = make_uint4(v, static_cast<uint32_t>(rs), static_cast<uint32_t>(rs >> 32) | (d << 8), 0u);
+        const uint4 q = rec[4 * e];
+        const uint32_t C = q.y >> 8;
+        if (C > 8) {
+            const uint32_t* I = idx + (q.x | (static_cast<uint64_t>(q.y & 0xFFu) << 32));
+            uint32_t P[8];
+#pragma unroll
+            for (uint32_t k = 0; k < 8; ++k) P[k] = I[((k + 1) * static_cast<uint64_t>(C)) / 9];
+            rec[4 * e + 2] = make_uint4(P[0], P[1], P[2], P[3]);
+            rec[4 * e + 3] = make_uint4(P[4], P[5], P[6], P[7]);
+        }
+    }
+}
+
+__global__ void k_n2x_src(const int64_t* __restrict__ rp, int64_t V, uint32_t* __restrict__ src) {
+    const int lane = lane_id();
+    for (uint64_t v = global_warp_id(); v < static_cast<uint64_t>(V); v += total_warps())
+        for (int64_t e = rp[v] + lane; e < rp[v + 1]; e += 32) src[e] = static_cast<uint32_t>(v);
+}
+
+csaw_status build_n2v_index(csaw_graph* g, int blocks) {
+    if (!g->rows_sorted || g->E <= 0 || g->max_deg >= (int64_t(1) << 24)) return CSAW_OK;
+    const int64_t E = g->E;
+    uint32_t* src = nullptr;
+    unsigned int* asym = nullptr;
+    unsigned long long* tot = nullptr;
+    uint64_t* part = nullptr;
+    auto release = [&]() {
+        if (src) cudaFree(src);
+        if (asym) cudaFree(asym);
+        if (tot) cudaFree(tot);
+        if (part) cudaFree(part);
+        cudaGetLastError();
+    };
+    auto drop = [&]() {   // best-effort: without the index node2vec uses k_node2vec_tri / the merge kernel
+        release();
+        if (g->n2x_rec) cudaFree(g->n2x_rec);
+        if (g->n2x_idx) cudaFree(g->n2x_idx);
+        g->n2x_rec = nullptr;
+        g->n2x_idx = nullptr;
+        g->n2x_total = 0;
+        cudaGetLastError();
+        return CSAW_OK;
+    };
+    if (cudaMalloc(&src, sizeof(uint32_t) * E) != cudaSuccess || cudaMalloc(&asym, sizeof(unsigned int)) != cudaSuccess ||
+        cudaMalloc(&tot, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&part, sizeof(uint64_t) * (SCAN_MAX_GRID + 8)) != cudaSuccess ||
+        cudaMalloc(&g->n2x_rec, 4 * sizeof(uint4) * E) != cudaSuccess)
+        return drop();
+    if (g->E >= (int64_t(1) << 40)) return drop();
+    cudaMemset(asym, 0, sizeof(unsigned int));
+    cudaMemset(g->n2x_rec, 0xFF, 4 * sizeof(uint4) * E);   // unused inline slots
+    k_n2x_src<<<blocks, 256>>>(g->row_ptr, g->V, src);
+    k_n2x<false><<<blocks * 4, 256>>>(g->row_ptr, g->col, src, E, g->n2x_rec, nullptr, asym);
+    unsigned int h = 0;
+    if (cudaMemcpy(&h, asym, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess || h) return drop();   // not symmetric
+    if (device_scan(N2xCount{g->n2x_rec}, static_cast<uint64_t>(E), N2xOffset{g->n2x_rec, tot}, part, nullptr) != CSAW_OK)
+        return drop();
+    unsigned long long total = 0;
+    if (cudaMemcpy(&total, tot, sizeof(total), cudaMemcpyDeviceToHost) != cudaSuccess) return drop();
+    if (total >= (1ull << 40)) return drop();
+    if (cudaMalloc(&g->n2x_idx, sizeof(uint32_t) * std::max<unsigned long long>(total, 1)) != cudaSuccess) return drop();
+    g->n2x_total = total;
+    k_n2x<true><<<blocks * 4, 256>>>(g->row_ptr, g->col, src, E, g->n2x_rec, g->n2x_idx, asym);
+    k_n2x_dst<<<blocks * 4, 256>>>(g->row_ptr, g->col, E, g->n2x_idx, g->n2x_rec);
+    if (cudaDeviceSynchronize() != cudaSuccess) return drop();
+    release();
+    return CSAW_OK;
+}
+
+// ---------------------------------------------------------------- walk
+struct N2xArgs {
+    const int64_t* __restrict__ rp;
+    const uint4* __restrict__ rec;            // [4 E]: 64 B per entry
+    const uint32_t* __restrict__ idx;
+    const uint32_t* __restrict__ seeds;
+    uint64_t n;
+    int32_t L;
+    uint32_t base;
+    uint2 key;
+    uint32_t* __restrict__ path;
+    unsigned long long* __restrict__ counters;   // [1] steps, [2] index probes, [3] sector bytes
+    uint32_t wp, w1, wq;
+};
+
+// S(j, p) = wq p - dq1 j - sub, exact in int64 (wq < 2^32, p, j < 2^24; dq1 may be negative):
+// the CTPS at the member of rank j and position p (sub = wq - wp after prev, else 0)
+__device__ __forceinline__ int64_t n2x_S(uint32_t wq, int64_t dq1, uint32_t p, uint32_t j, int64_t sub) {
+    return static_cast<int64_t>(static_cast<uint64_t>(wq) * p) - dq1 * static_cast<int64_t>(j) - sub;
+}
+
+// Last member rank j in [lo, hi) with S(j, I[j]) <= x (S increases with j: the predicate
+// holds on a prefix); found = false if none, else pos = I[j].  The record's 8 inline
+// values resolve it outright for C <= 8 and otherwise narrow [lo, hi) to the gap between
+// two splitters, searched by a plain binary search over idx (about log2(C / 9) probes).
+__device__ __forceinline__ uint32_t n2x_last_le(const uint32_t* __restrict__ I, const uint32_t (&P)[8], uint32_t C,
+                                                uint32_t lo, uint32_t hi, int64_t x, uint32_t wq, int64_t dq1,
+                                                int64_t sub, uint32_t& probes, bool& found, uint32_t& pos) {
+    uint32_t l = lo, h = hi;
+    if (C <= 8) {
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k)
+            if (k >= lo && k < hi && n2x_S(wq, dq1, P[k], k, sub) <= x) { l = k + 1; pos = P[k]; }
+        h = l;
+    } else {
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k) {
+            const uint32_t j = static_cast<uint32_t>(((k + 1) * static_cast<uint64_t>(C)) / 9);
+            if (j >= lo && j < hi) {
+                if (n2x_S(wq, dq1, P[k], j, sub) <= x) { l = j + 1; pos = P[k]; }
+                else h = min(h, j);
+            }
+        }
+    }
+    while (l < h) {
+        const uint32_t mid = (l + h) >> 1;
+        const uint32_t p = __ldg(I + mid);
+        ++probes;
+        if (n2x_S(wq, dq1, p, mid, sub) <= x) { l = mid + 1; pos = p; } else h = mid;
+    }
+    found = l > lo;   // l - 1 is the last true rank, pos = I[l - 1]
+    return l - 1;
+}
+
+// One thread per walker: the walkers are independent and a step is a short chain of
+// dependent sector loads, so thread-level parallelism (up to 2,048 walkers per SM in
+// flight) hides the latency that a warp-per-walker kernel exposes.  Per step: the
+// record of the entry the walker arrived by (its vertex, row, degree and the step's
+// specials), the binary search, and the path store.
+#ifndef N2X_MINB
+#define N2X_MINB 3   // <= 80 registers, 768 walkers per SM (A/B r02 cfg3: 80 regs 10.1 ms; 64 regs + spills 11.6 ms; 128 regs 11.9 ms)
+#endif
+__global__ void __launch_bounds__(256, N2X_MINB) k_node2vec_idx(N2xArgs a) {
+    const uint32_t wq = a.wq, w1 = a.w1, wp = a.wp;
+    const int64_t dq1 = static_cast<int64_t>(wq) - w1, dqp = static_cast<int64_t>(wq) - wp;   // may be negative
+    unsigned long long steps = 0, probes_all = 0;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < a.n; w += nthreads) {
+        uint32_t* row = a.path + w * (static_cast<uint64_t>(a.L) + 1);
+        const uint32_t seed = a.seeds[w];
+        const uint32_t inst = a.base + static_cast<uint32_t>(w);
+        row[0] = seed;
+        if (a.L == 0) continue;
+        // step 0: uniform over N(seed) (R16)
+        const int64_t b0 = __ldg(a.rp + seed);
+        const uint32_t d0 = static_cast<uint32_t>(__ldg(a.rp + seed + 1) - b0);
+        if (d0 == 0) {   // isolated seed: the walk ends (R20)
+            for (int32_t t = 1; t <= a.L; ++t) row[t] = NONE;
+            continue;
+        }
+        uint64_t e = static_cast<uint64_t>(b0) +
+                     below(draw_u64(a.key, inst, 0u, 0u, word3(PURPOSE_EDGE, 0, 0)), d0);
+        ++steps;
+        for (int32_t t = 1;; ++t) {
+            const uint4 ra = __ldg(a.rec + 4 * e), rb = __ldg(a.rec + 4 * e + 1);
+            const uint4 rc = __ldg(a.rec + 4 * e + 2), rd = __ldg(a.rec + 4 * e + 3);
+            row[t] = rb.x;                          // the vertex this entry leads to
+            if (t == a.L) break;
+            // step t at v = rb.x, arrived from prev by entry e (d >= 1: prev is in N(v))
+            const uint64_t U = draw_u64(a.key, inst, static_cast<uint32_t>(t), 0u, word3(PURPOSE_EDGE, 0, 0));
+            const uint64_t rs = rb.y | (static_cast<uint64_t>(rb.z & 0xFFu) << 32);
+            const uint32_t d = rb.z >> 8;
+            const uint32_t C = ra.y >> 8, ppos = ra.z, mb = ra.w;
+            const uint32_t* I = a.idx + (ra.x | (static_cast<uint64_t>(ra.y & 0xFFu) << 32));
+            const uint64_t T = static_cast<uint64_t>(wq) * (d - C - 1) + static_cast<uint64_t>(w1) * C + wp;
+            const int64_t x = static_cast<int64_t>(below(U, T));   // < 2^56
+            const int64_t Sp = n2x_S(wq, dq1, ppos, mb, 0);          // S at prev's position
+            uint32_t probes = 0, pos = 0, s;
+            if (x >= Sp && x < Sp + wp) {
+                s = ppos;                                   // prev's own region
+            } else {
+                // before prev: members [0, mb); after prev: members [mb, C), S one (wq - wp) lower
+                const bool after = x >= Sp;
+                const int64_t sub = after ? dqp : 0;
+                bool found = false;
+                const uint32_t P[8] = {rc.x, rc.y, rc.z, rc.w, rd.x, rd.y, rd.z, rd.w};
+                const uint32_t j = n2x_last_le(I, P, C, after ? mb : 0, after ? C : mb, x, wq, dq1, sub, probes, found,
+                                               pos);
+                if (found) {
+                    const int64_t Sm = n2x_S(wq, dq1, pos, j, sub);
+                    s = x < Sm + w1 ? pos : pos + 1 + static_cast<uint32_t>((x - Sm - w1) / wq);
+                } else {
+                    s = after ? ppos + 1 + static_cast<uint32_t>((x - Sp - wp) / wq) : static_cast<uint32_t>(x / wq);
+                }
+            }
+            probes_all += probes;
+            ++steps;
+            e = rs + s;
+        }
+    }
+    // sector model (32 B sectors): the 64 B edge record (2 sectors) + the probes per step,
+    // + 4 B path (step 0: the seed's row_ptr pair instead of a record)
+    steps = warp_sum(steps);
+    probes_all = warp_sum(probes_all);
+    if (lane_id() == 0 && steps) {
+        atomicAdd(a.counters + 1, steps);
+        atomicAdd(a.counters + 2, probes_all);
+        atomicAdd(a.counters + 3, 32ull * (2 * steps + probes_all) + 4ull * steps);
+    }
+}
+
+csaw_status launch_node2vec_index(const csaw_graph* g, const uint32_t* seeds, uint64_t n, int32_t L, uint32_t base,
+                                  uint2 key, uint32_t* path, unsigned long long* counters, uint32_t wp, uint32_t w1,
+                                  uint32_t wq, cudaStream_t st) {
+    N2xArgs a{g->row_ptr, g->n2x_rec, g->n2x_idx, seeds, n, L, base, key, path, counters, wp, w1, wq};
+    const uint64_t resident = static_cast<uint64_t>(g->num_sms) * 2048;
+    const uint64_t threads = std::min<uint64_t>(n, resident);
+    const int grid = static_cast<int>(std::max<uint64_t>(1, (threads + 255) / 256));
+    k_node2vec_idx<<<grid, 256, 0, st>>>(a);
+    note_launch();
+    CSAW_CUDA(cudaGetLastError());
+    return CSAW_OK;
+}
+
+}  // namespace csaw

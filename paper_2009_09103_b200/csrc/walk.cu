@@ -1685,7 +1685,11 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         na.wf[0] = static_cast<float>(1.0 / b.p);
         na.wf[1] = 1.0f;
         na.wf[2] = static_cast<float>(1.0 / b.q);
-        if (m && g->tri) k_node2vec_tri<<<walk_grid(g, n), N2T_WARPS * 32, 0, st>>>(na, g->tri);
+        if (m && g->n2x_rec)
+            CSAW_TRY(launch_node2vec_index(g, d_seeds, static_cast<uint64_t>(n), length, static_cast<uint32_t>(base), key,
+                                           d_path, static_cast<unsigned long long*>(cnt), na.wint[0], na.wint[1],
+                                           na.wint[2], st));
+        else if (m && g->tri) k_node2vec_tri<<<walk_grid(g, n), N2T_WARPS * 32, 0, st>>>(na, g->tri);
         else if (m) k_node2vec<false><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(na);
         else k_node2vec<true><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(na);
     } else if (b.kind == CSAW_BIAS_MDRW) {

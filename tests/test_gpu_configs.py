@@ -6,8 +6,9 @@ and compares with the oracle element by element (integer biases: bit-exact) at
 the coverage SURVEY.md §8(d) d.4 plans:
 
   cfg2  all 4,000 walkers                      (cache + walk index, and the scan path)
-  cfg3  every 64th walker (~29.5K of ~1.9M)    (triangle counts, and the full merge);
-        the two kernels are also compared with each other on 100 % of the walkers
+  cfg3  every 64th walker (~29.5K of ~1.9M)    (intersection index = the bench's launch);
+        the index, triangle-count and full-merge kernels are also compared with each
+        other on 100 % of the walkers
   cfg4  all 8,192 instances, layer and forest fire
   cfg5  all 4,000 MDRW instances in memory; the 8 GB OOM launches (zero-copy and the
         paper's partition scheduling) equal to the in-memory output on 100 %
@@ -119,23 +120,28 @@ def test_cfg3_node2vec_full():
     n = seeds.numel()
     sv = u32(seeds)
     ids = np.arange(0, n, 64)
-    Gt = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, node2vec_tri=True)   # the bench's launch
-    Gm = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0)                      # full merge per step
-    assert Gt.info()["node2vec_tri"] == 1 and Gm.info()["node2vec_tri"] == 0
+    Gx = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, node2vec_index=True)  # the bench's launch
+    Gt = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, node2vec_tri=True)    # triangle counts + scans
+    Gm = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0)                       # full merge per step
+    assert Gx.info()["node2vec_index"] == 1 and Gt.info()["node2vec_tri"] == 1 and Gm.info()["node2vec_tri"] == 0
     bias = cs.make_bias("node2vec", p=cfg.p, q=cfg.q)
     for seed in SEEDS:
+        px = u32(cs.csaw_walk(Gx, bias, seeds, cfg.length, rng_seed=seed))
         pt = u32(cs.csaw_walk(Gt, bias, seeds, cfg.length, rng_seed=seed))
         pm = u32(cs.csaw_walk(Gm, bias, seeds, cfg.length, rng_seed=seed))
-        assert pt.shape == (n, cfg.length + 1) and (pt != cs.NONE).all()
-        # two independent kernels (closed form over triangle counts vs full CTPS merge): 100 %
+        assert px.shape == (n, cfg.length + 1) and (px != cs.NONE).all()
+        # three independent kernels (intersection index, triangle counts + partial scans,
+        # full CTPS merge) on 100 % of the walkers
+        assert first_mismatch(px, pm) is None, f"seed {seed}: index vs merge walker {first_mismatch(px, pm)}"
         assert first_mismatch(pt, pm) is None, f"seed {seed}: tri vs merge walker {first_mismatch(pt, pm)}"
+        pt = px
         t0 = time.time()
         ref = np.stack(O.parallel_run(og, "node2vec", sv, 0, seed, ids=ids, p=cfg.p, q=cfg.q, length=cfg.length))
         log(f"cfg3 seed {seed}: oracle over {ids.size} walkers (every 64th of {n}) in {time.time() - t0:.1f} s")
         bad = first_mismatch(pt[ids], ref)
         assert bad is None, f"seed {seed}: walker {int(ids[bad])}"
         check_edges_exist(og, pt[::7, :-1].ravel(), pt[::7, 1:].ravel())
-    release(Gt, Gm)
+    release(Gx, Gt, Gm)
 
 
 # ------------------------------------------------------------------ cfg4
