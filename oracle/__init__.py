@@ -62,6 +62,10 @@ def lib():
             "oracle_node2vec_step": (u32, [P, P, i64, f64, f64, u32, u32, u32, u32, u64, P]),
             "oracle_node2vec": (None, [P, P, i64, f64, f64, i32, u32, u32, u64, P, P]),
             "oracle_mdrw": (None, [P, P, i64, P, i32, i32, u32, u64, P]),
+            "oracle_select_wor_float": (i64, [P, i64, i64, u64, u32, u32, u32, i32, P, P]),
+            "oracle_weight_walk_step": (u32, [P, P, P, i64, u32, u32, u32, u64, P]),
+            "oracle_weight_walk": (None, [P, P, P, i64, i32, u32, u32, u64, P, P]),
+            "oracle_weight_sample": (i64, [P, P, P, i64, P, i32, u32, u32, u64, i32, P, P, P, i64, P]),
             "oracle_partition_bounds": (None, [i64, i32, P]),
             "oracle_active_counts": (None, [P, i32, P, i64, P]),
         }
@@ -78,16 +82,19 @@ def _p(a: np.ndarray):
 
 
 class Graph:
-    """Host CSR handed to the oracle: row_ptr int64[V+1], col uint32[E] (sorted rows)."""
+    """Host CSR handed to the oracle: row_ptr int64[V+1], col uint32[E] (sorted rows),
+    optional edge weights w float32[E] (EdgeBias = w(e))."""
 
-    def __init__(self, row_ptr, col_idx):
+    def __init__(self, row_ptr, col_idx, weights=None):
         self.row_ptr = np.ascontiguousarray(np.asarray(row_ptr, dtype=np.int64))
         self.col = np.ascontiguousarray(np.asarray(col_idx).astype(np.uint32, copy=False))
         self.V = self.row_ptr.size - 1
+        self.w = None if weights is None else np.ascontiguousarray(np.asarray(weights, dtype=np.float32))
 
     @classmethod
-    def from_torch(cls, g):
-        return cls(g.row_ptr.cpu().numpy(), g.col_idx.cpu().numpy().view(np.uint32))
+    def from_torch(cls, g, weights=None):
+        w = None if weights is None else weights.cpu().numpy().astype(np.float32, copy=False)
+        return cls(g.row_ptr.cpu().numpy(), g.col_idx.cpu().numpy().view(np.uint32), w)
 
     def deg(self, v):
         return int(self.row_ptr[v + 1] - self.row_ptr[v])
@@ -158,6 +165,44 @@ def select_float(b, U: int):
     m = np.zeros(1, dtype=np.float64)
     s = lib().oracle_select_float(_p(b), b.size, U, _p(m))
     return int(s), float(m[0])
+
+
+def select_wor_float(b, k, seed, inst, t, slot, a_max=A_MAX_DEFAULT):
+    """Without-replacement selection over fp32 biases (float BRS, R28) -> (picks in
+    pick order, minimum boundary margin over the draws)."""
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float32))
+    picks = np.zeros(max(b.size, 1), dtype=np.int64)
+    m = np.ones(1, dtype=np.float64)
+    n = lib().oracle_select_wor_float(_p(b), b.size, k, seed, inst, t, slot, a_max, _p(picks), _p(m))
+    return [int(x) for x in picks[:n]], float(m[0])
+
+
+def weight_walk_step(g: Graph, v, inst, t, rng_seed):
+    """One edge-weight walk step at v -> (next vertex, margin)."""
+    m = np.ones(1, dtype=np.float64)
+    u = lib().oracle_weight_walk_step(_p(g.row_ptr), _p(g.col), _p(g.w), g.V, v, inst, t, rng_seed, _p(m))
+    return int(u), float(m[0])
+
+
+def weight_walk(g: Graph, length, s0, inst, rng_seed, with_margins=False):
+    path = np.zeros(length + 1, dtype=np.uint32)
+    mg = np.ones(max(length, 1), dtype=np.float64)
+    lib().oracle_weight_walk(_p(g.row_ptr), _p(g.col), _p(g.w), g.V, length, s0, inst, rng_seed, _p(path), _p(mg))
+    return (path, mg[:length]) if with_margins else path
+
+
+def weight_sample(g: Graph, fanout, depth, seed_vertex, inst, rng_seed, a_max=A_MAX_DEFAULT):
+    """Edge-weight neighbor sampling of one instance -> (src, dst, depth, min margin)."""
+    fan = np.ascontiguousarray(np.asarray(list(fanout) + [0] * max(0, depth - len(fanout)), dtype=np.int32))
+    cap = 1024
+    m = np.ones(1, dtype=np.float64)
+    while True:
+        s = np.zeros(cap, np.uint32); d = np.zeros(cap, np.uint32); e = np.zeros(cap, np.uint8)
+        n = lib().oracle_weight_sample(_p(g.row_ptr), _p(g.col), _p(g.w), g.V, _p(fan), depth, seed_vertex, inst,
+                                       rng_seed, a_max, _p(s), _p(d), _p(e), cap, _p(m))
+        if n >= 0:
+            return s[:n], d[:n], e[:n], float(m[0])
+        cap = -n
 
 
 def n2v_scale(p, q) -> int:
@@ -313,6 +358,10 @@ def _run_job(args):
             out.append(mdrw(_G, s, params["length"], gi, rng_seed))
         elif workload == "layer":
             out.append(layer_sample(_G, params["fanout"], params["depth"], int(s), gi, rng_seed))
+        elif workload == "weight_walk":
+            out.append(weight_walk(_G, params["length"], int(s), gi, rng_seed, with_margins=True))
+        elif workload == "weight":
+            out.append(weight_sample(_G, params["fanout"], params["depth"], int(s), gi, rng_seed))
         else:
             kind = {"uniform": KIND_UNIFORM, "degree": KIND_DEGREE, "forest_fire": KIND_FF,
                     "snowball": KIND_SNOWBALL}[workload]
@@ -326,7 +375,8 @@ def parallel_run(g: Graph, workload: str, seeds, instance_base, rng_seed, ids=No
     cores, fanned out over disjoint chunks (instances are independent).
     workload: walk (params kind, length) | node2vec (p, q, length) | mdrw (length;
     seeds[i] is the instance's pool) | layer (fanout, depth) | degree / uniform /
-    forest_fire / snowball (fanout, depth, pf).  Returns the per-instance results in
+    forest_fire / snowball (fanout, depth, pf) | weight_walk (length; -> (path, margins)) |
+    weight (fanout, depth; -> (src, dst, depth, margin)).  Returns the per-instance results in
     the order of ids (walks: path arrays; MDRW: edge arrays; sampling: (src, dst, depth))."""
     import multiprocessing as mp
     seeds = np.asarray(seeds)

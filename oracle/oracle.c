@@ -324,13 +324,18 @@ ORACLE_EXPORT int64_t oracle_ff_burn(uint64_t seed, uint32_t inst, uint32_t dept
  * Sampled <- picks.  Each v in sorted(F) is one pool.
  * Returns #edges (canonical order), or -(#edges) if cap is too small.
  */
-ORACLE_EXPORT int64_t oracle_neighbor_sample(const int64_t *row_ptr, const uint32_t *col, int64_t V,
-                                             int32_t kind, const int32_t *fanout, int32_t depth, double pf,
-                                             uint32_t seed_vertex, uint32_t inst, uint64_t rng_seed, int32_t a_max,
-                                             uint32_t *src, uint32_t *dst, uint8_t *edepth, int64_t cap,
-                                             int64_t *attempts_out)
+ORACLE_EXPORT int64_t oracle_select_wor_float(const float *b, int64_t n, int64_t k, uint64_t seed, uint32_t inst,
+                                              uint32_t t, uint32_t slot, int32_t a_max, int64_t *picks,
+                                              double *margin);   /* defined with the float path below */
+
+static int64_t neighbor_sample_core(const int64_t *row_ptr, const uint32_t *col, const float *w, int64_t V,
+                                    int32_t kind, const int32_t *fanout, int32_t depth, double pf,
+                                    uint32_t seed_vertex, uint32_t inst, uint64_t rng_seed, int32_t a_max,
+                                    uint32_t *src, uint32_t *dst, uint8_t *edepth, int64_t cap,
+                                    int64_t *attempts_out, double *margin_out)
 {
     csr_t g = { row_ptr, col, V };
+    if (margin_out) *margin_out = 1.0;
     vec_t visited = {0}, F = {0}, nxt = {0};
     evec_t out = {0};
     vpush(&visited, seed_vertex);
@@ -347,7 +352,14 @@ ORACLE_EXPORT int64_t oracle_neighbor_sample(const int64_t *row_ptr, const uint3
             int64_t k = (kind == 2) ? oracle_ff_burn(rng_seed, inst, (uint32_t)d, v, n, pf)
                       : (kind == 3) ? n : fanout[d];
             int64_t *picks = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
-            int64_t np = oracle_select_wor(b, n, k, rng_seed, inst, (uint32_t)d, v, a_max, picks, attempts_out);
+            int64_t np;
+            if (w) {   /* EdgeBias = w(e) (Eq. 3): float path (R28) */
+                double mg = 1.0;
+                np = oracle_select_wor_float(w + row_ptr[v], n, k, rng_seed, inst, (uint32_t)d, v, a_max, picks, &mg);
+                if (margin_out && mg < *margin_out) *margin_out = mg;
+            } else {
+                np = oracle_select_wor(b, n, k, rng_seed, inst, (uint32_t)d, v, a_max, picks, attempts_out);
+            }
             for (int64_t p = 0; p < np; p++) {
                 uint32_t u = pool[picks[p]];
                 epush(&out, v, u, (uint8_t)(d + 1));
@@ -364,6 +376,29 @@ ORACLE_EXPORT int64_t oracle_neighbor_sample(const int64_t *row_ptr, const uint3
     int64_t r = emit_edges(&out, src, dst, edepth, cap);
     free(visited.v); free(F.v); free(nxt.v); free(out.e);
     return r;
+}
+
+ORACLE_EXPORT int64_t oracle_neighbor_sample(const int64_t *row_ptr, const uint32_t *col, int64_t V,
+                                             int32_t kind, const int32_t *fanout, int32_t depth, double pf,
+                                             uint32_t seed_vertex, uint32_t inst, uint64_t rng_seed, int32_t a_max,
+                                             uint32_t *src, uint32_t *dst, uint8_t *edepth, int64_t cap,
+                                             int64_t *attempts_out)
+{
+    return neighbor_sample_core(row_ptr, col, NULL, V, kind, fanout, depth, pf, seed_vertex, inst, rng_seed, a_max,
+                                src, dst, edepth, cap, attempts_out, NULL);
+}
+
+/* Edge-weight neighbor sampling (EdgeBias = w(e), Eq. 3): the traversal
+ * of oracle_neighbor_sample with fanout[d] picks per pool from
+ * oracle_select_wor_float over the row's weights.  *margin_out (nullable) = the
+ * minimum boundary margin over every draw of the instance (R28). */
+ORACLE_EXPORT int64_t oracle_weight_sample(const int64_t *row_ptr, const uint32_t *col, const float *w, int64_t V,
+                                           const int32_t *fanout, int32_t depth, uint32_t seed_vertex, uint32_t inst,
+                                           uint64_t rng_seed, int32_t a_max, uint32_t *src, uint32_t *dst,
+                                           uint8_t *edepth, int64_t cap, double *margin_out)
+{
+    return neighbor_sample_core(row_ptr, col, w, V, 0, fanout, depth, 0.0, seed_vertex, inst, rng_seed, a_max,
+                                src, dst, edepth, cap, NULL, margin_out);
 }
 
 /*
@@ -536,6 +571,150 @@ ORACLE_EXPORT int64_t oracle_select_float(const float *b, int64_t n, uint64_t U,
     }
     free(S);
     return s;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Edge-weight bias (EdgeBias = f(e), Eq. 3; "F is real-valued",   */
+/* P:228): the float path of reading R28 for walks and without-replacement  */
+/* sampling.                                                                 */
+/* ------------------------------------------------------------------------- */
+
+/* r = (U >> 11) * 2^-53 in [0, 1) (R28). */
+static double unit_r(uint64_t U) { return (double)(U >> 11) * (1.0 / 9007199254740992.0); }
+
+/* its over an fp64 prefix: max{i < n : S[i] <= x, b[i] > 0}, -1 if none (R4, R28). */
+static int64_t its_float(const double *S, const float *b, int64_t n, double x)
+{
+    int64_t s = -1;
+    for (int64_t i = 0; i < n; i++) if (S[i] <= x && b[i] > 0.0f) s = i;
+    return s;
+}
+
+/* min_{0<i<n} |x - S[i]| / T, the checker's boundary margin (R28). */
+static double margin_float(const double *S, int64_t n, double x, double T)
+{
+    double mg = 1.0;
+    for (int64_t i = 1; i < n; i++) { double dd = fabs(x - S[i]) / T; if (dd < mg) mg = dd; }
+    return mg;
+}
+
+/* Exact updated sampling over float biases (Fig. 6(b)): the CTPS of
+ * the positive-bias, untaken candidates (ascending), summed left to right in
+ * fp64, searched at x = r(U) * T'.  *mg = min(*mg, margin of that draw). */
+static int64_t updated_pick_float(const float *b, int64_t n, const int64_t *picks, int64_t taken, uint64_t U,
+                                  double *mg)
+{
+    int64_t nsv = 0;
+    int64_t *sv = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    float *b2 = (float *)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; i++)
+        if (b[i] > 0.0f && !in_list(picks, taken, i)) { sv[nsv] = i; b2[nsv] = b[i]; nsv++; }
+    double *S2 = (double *)malloc(sizeof(double) * (size_t)(nsv + 1));
+    S2[0] = 0.0;
+    for (int64_t i = 0; i < nsv; i++) S2[i + 1] = S2[i] + (double)b2[i];
+    double x = unit_r(U) * S2[nsv];
+    int64_t q = its_float(S2, b2, nsv, x);
+    double m = margin_float(S2, nsv, x, S2[nsv]);
+    if (m < *mg) *mg = m;
+    int64_t s = sv[q];
+    free(S2); free(b2); free(sv);
+    return s;
+}
+
+/*
+ * select_wor over fp32 biases (R28 float path of the box steps):
+ * S[0] = 0, S[i+1] = S[i] + (double)b[i] left to right, T = S[n]; every draw is
+ * x = r(U) * M for the space size M it draws over.
+ *   (1)(2) s = its(S, r(U(j,a)) * T); accept if not taken
+ *   (3)    fresh x' = r(U(j,a+1)) * (T - b[s]) over the space without the taken
+ *          region [S[s], S[s] + b[s]) (R1; b[s] the region's bias, in fp64)
+ *   (4)(5) y = x' if x' < S[s] else x' + b[s]; s = its(S, y); accept if not
+ *          taken, else back to (1)
+ *   after a_max attempts: exact updated sampling with U(j, a_max) (R2).
+ * If k >= #positive-bias candidates: all of them, ascending (R8).
+ * *margin (nullable) = the minimum boundary margin over every draw searched
+ * (R28: a GPU pick may differ from this one only if it is <= 1e-6).
+ */
+ORACLE_EXPORT int64_t oracle_select_wor_float(const float *b, int64_t n, int64_t k,
+                                              uint64_t seed, uint32_t inst, uint32_t t, uint32_t slot,
+                                              int32_t a_max, int64_t *picks, double *margin)
+{
+    double mg = 1.0;
+    int64_t npos = 0;
+    for (int64_t i = 0; i < n; i++) if (b[i] > 0.0f) npos++;
+    if (margin) *margin = 1.0;
+    if (k <= 0 || npos == 0) return 0;
+    if (k >= npos) {
+        int64_t c = 0;
+        for (int64_t i = 0; i < n; i++) if (b[i] > 0.0f) picks[c++] = i;
+        return c;
+    }
+    double *S = (double *)malloc(sizeof(double) * (size_t)(n + 1));
+    S[0] = 0.0;
+    for (int64_t i = 0; i < n; i++) S[i + 1] = S[i] + (double)b[i];
+    double T = S[n];
+    int64_t taken = 0;
+    for (int64_t j = 0; j < k; j++) {
+        uint32_t a = 0;
+        int64_t s;
+        for (;;) {
+            double x = unit_r(draw_u64(seed, inst, t, slot, word3_of(P_EDGE, (uint32_t)j, a), 0)) * T;
+            a += 1;
+            s = its_float(S, b, n, x);
+            double m = margin_float(S, n, x, T);
+            if (m < mg) mg = m;
+            if (!in_list(picks, taken, s)) break;
+            double L = S[s], d = (double)b[s];
+            double x2 = unit_r(draw_u64(seed, inst, t, slot, word3_of(P_EDGE, (uint32_t)j, a), 0)) * (T - d);
+            a += 1;
+            double y = (x2 < L) ? x2 : x2 + d;
+            s = its_float(S, b, n, y);
+            m = margin_float(S, n, y, T);
+            if (m < mg) mg = m;
+            if (!in_list(picks, taken, s)) break;
+            if ((int32_t)a >= a_max) {
+                s = updated_pick_float(b, n, picks, taken,
+                                       draw_u64(seed, inst, t, slot, word3_of(P_EDGE, (uint32_t)j, (uint32_t)a_max), 0),
+                                       &mg);
+                break;
+            }
+        }
+        picks[taken++] = s;
+    }
+    free(S);
+    if (margin) *margin = mg;
+    return taken;
+}
+
+/* One step of the edge-weight walk at v (biased DeepWalk with EdgeBias = w(e),
+ * P:172 with Eq. 3's f(e)): b[i] = w[row_ptr[v] + i], oracle_select_float with
+ * U(i, t, 0, EDGE).  Returns the next vertex, or 0xFFFFFFFF if the row's weights
+ * sum to 0 (R20).  *margin (nullable) = that draw's boundary margin (R28). */
+ORACLE_EXPORT uint32_t oracle_weight_walk_step(const int64_t *row_ptr, const uint32_t *col, const float *w,
+                                               int64_t V, uint32_t v, uint32_t inst, uint32_t t, uint64_t rng_seed,
+                                               double *margin)
+{
+    (void)V;
+    int64_t n = row_ptr[v + 1] - row_ptr[v];
+    if (margin) *margin = 1.0;
+    if (n == 0) return 0xFFFFFFFFu;
+    uint64_t U = draw_u64(rng_seed, inst, t, 0, word3_of(P_EDGE, 0, 0), 0);
+    int64_t s = oracle_select_float(w + row_ptr[v], n, U, margin);
+    return s < 0 ? 0xFFFFFFFFu : col[row_ptr[v] + s];
+}
+
+ORACLE_EXPORT void oracle_weight_walk(const int64_t *row_ptr, const uint32_t *col, const float *w, int64_t V,
+                                      int32_t length, uint32_t s0, uint32_t inst, uint64_t rng_seed,
+                                      uint32_t *path, double *margins)
+{
+    path[0] = s0;
+    for (int32_t t = 0; t < length; t++) {
+        uint32_t v = path[t];
+        double mg = 1.0;
+        path[t + 1] = (v == 0xFFFFFFFFu) ? 0xFFFFFFFFu
+            : oracle_weight_walk_step(row_ptr, col, w, V, v, inst, (uint32_t)t, rng_seed, &mg);
+        if (margins) margins[t] = mg;
+    }
 }
 
 /* node2vec integer scale (R16): smallest m in [1, 2^16] with m/p and m/q

@@ -13,9 +13,10 @@ are implemented separately in `oracle/` and in the CUDA library.
 from .rmat import RmatGraph, rmat_csr, gtoy_csr, degree_stats
 from .seeds import instance_seeds, nonisolated_vertices, mdrw_seeds
 from .configs import CONFIGS, WorkloadConfig, small_config
+from .weights import edge_weights
 
 __all__ = [
     "RmatGraph", "rmat_csr", "gtoy_csr", "degree_stats",
     "instance_seeds", "nonisolated_vertices", "mdrw_seeds",
-    "CONFIGS", "WorkloadConfig", "small_config",
+    "CONFIGS", "WorkloadConfig", "small_config", "edge_weights",
 ]
