@@ -68,6 +68,12 @@ def parse_args(argv=None):
     ap.add_argument("--in-memory", action="store_true", help="cfg5: ignore the OOM budget (in-memory MDRW)")
     ap.add_argument("--no-cache", action="store_true",
                     help="disable the static-bias CTPS cache / node2vec triangle counts (scan every pool)")
+    ap.add_argument("--gather-bias", action="store_true",
+                    help="with --no-cache: degree walks gather deg[u] per neighbour instead of streaming the "
+                         "materialised per-edge bias (CSAW_GRAPH_EDGE_BIAS)")
+    ap.add_argument("--scan-path-steps", type=int, default=1,
+                    help="detail.scan_path: time this many steps of the config's per-step scan path (no caches; "
+                         "0 = skip)")
     ap.add_argument("--no-zerocopy", action="store_true", help="OOM configs: skip the zero-copy OOM variant")
     ap.add_argument("--oom-budget-gb", type=float, default=0.0,
                     help="OOM configs: override the device budget (1e9 B) -- experiments only, the config names 8 GB")
@@ -149,6 +155,8 @@ def _bit_length(x: torch.Tensor) -> torch.Tensor:
 
 BYTES_MODEL = {
     "walk_degree_scan": "SURVEY §8(d) degree-biased pool: 16 (row_ptr pair) + 8 d(v) (col + deg) per step + 4 (path)",
+    "walk_degree_stream": "per-step scan of the materialised degree bias (CSAW_GRAPH_EDGE_BIAS): 16 (row_ptr "
+                          "pair) + 4 d(v) (the pool's biases, streamed) + 4 (the pick's col) + 4 (path)",
     "walk_degree_cached": "SURVEY §8(f) NEXT-1 cached CTPS: 32 B sectors x (row_ptr pair + ceil(log2 d(v)) probes "
                           "+ col) per step + 4 (path)",
     "walk_uniform": "16 (row_ptr pair) + 4 (one col entry) + 4 (path) per step",
@@ -165,7 +173,7 @@ BYTES_MODEL = {
 }
 
 
-def walk_alg_bytes(cfg, deg, out, cached):
+def walk_alg_bytes(cfg, deg, out, cached, stream=False):
     """§8(d) bytes of one walk launch, from its output (device tensors)."""
     if cfg.workload == "mdrw":
         return 32 * out.shape[0] * out.shape[1], "mdrw"
@@ -182,6 +190,8 @@ def walk_alg_bytes(cfg, deg, out, cached):
     if cached:
         probes = _bit_length(torch.clamp(d - 1, min=0))
         return int(32 * (2 * nsteps + probes[valid].sum()) + 4 * nsteps), "walk_degree_cached"
+    if stream:
+        return int(16 * nsteps + 4 * d.sum() + 8 * nsteps), "walk_degree_stream"
     return int(16 * nsteps + 8 * d.sum() + 4 * nsteps), "walk_degree_scan"
 
 
@@ -476,8 +486,9 @@ def main():
         use_cache = (not args.no_cache) and cfg.bias in ("degree", "layer")
         use_tri = (not args.no_cache) and cfg.workload == "node2vec"
         use_meta = (not args.no_cache) and cfg.workload == "mdrw"
+        use_eb = args.no_cache and not args.gather_bias and cfg.workload == "walk" and cfg.bias == "degree"
         G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache, node2vec_tri=use_tri,
-                                 next_meta=use_meta, walk_index=use_cache, node2vec_index=use_tri)
+                                 next_meta=use_meta, walk_index=use_cache, node2vec_index=use_tri, edge_bias=use_eb)
     ginfo = G.info()
     bias = bias_of(cs, cfg)
     stream = torch.cuda.current_stream(dev)
@@ -587,7 +598,7 @@ def main():
             if kind == "walk" and ginfo.get("node2vec_index") and cfg.workload == "node2vec":
                 b, model = cs.csaw_stats(G)["index_bytes"], "node2vec_index"
             elif kind == "walk":
-                b, model = walk_alg_bytes(cfg, deg, out_dev, cached)
+                b, model = walk_alg_bytes(cfg, deg, out_dev, cached, bool(ginfo.get("edge_bias")))
             else:
                 b, model = sample_alg_bytes(cfg, deg, seeds, *last["r"])
             alg_bytes += b * k
@@ -611,6 +622,11 @@ def main():
         zc = run_zerocopy(cs, g, cfg, bias, seeds, base, rng_seeds[0], kind, n, dev, local, stream, flush,
                           out_dev if kind == "walk" else None, last.get("r"), G, args)
 
+    # ---------------- the config's per-step scan path (no caches), reported apart
+    scan_path = None
+    if args.scan_path_steps > 0 and not oom and not args.no_cache and rank == 0:
+        scan_path = run_scan_path(cs, g, cfg, deg, seeds, base, rng_seeds, n, dev, local, stream, flush, args)
+
     # ---------------- end-to-end through the C ABI with host buffers
     e2e = None
     if not args.no_e2e:
@@ -621,13 +637,13 @@ def main():
     hot_avg_ms = hot_ms / max(hot_launches, 1)
     variant = cfg.name + ("_inmem" if cfg.oom_budget_bytes and args.in_memory else "")
     if not oom and not ginfo.get("ctps_cache") and cfg.bias in ("degree", "layer"):
-        variant += "_scan"
+        variant += "_stream" if ginfo.get("edge_bias") else "_scan"
     if cfg.workload == "node2vec" and not ginfo.get("node2vec_tri") and not ginfo.get("node2vec_index"):
         variant += "_merge"
     kname = hot_kernel_name(cfg, bool(ginfo.get("node2vec_tri") if cfg.workload == "node2vec" else ginfo.get("ctps_cache")),
                             oom and args.oom_variant != "zerocopy", int(ginfo.get("walk_index_leaf") or 0),
                             int(ginfo.get("walk_index_group") or 0), bool(ginfo.get("walk_index_heads")),
-                            bool(ginfo.get("node2vec_index")))
+                            bool(ginfo.get("node2vec_index")), bool(ginfo.get("edge_bias")))
     ncu = load_ncu(variant, kname)
     if oom:
         ach = (h2d_bytes / (total_ms / 1000.0) / 1e9) if h2d_bytes else None
@@ -689,6 +705,7 @@ def main():
                                      "calls_to_amortise_build": (build_ms / ms_step) if ms_step else None,
                                      "note": "one_call_seps = edges of one step / (step time + the graph's cache "
                                              "build, P:784-786 computes its cache during sampling)"},
+                           "scan_path": scan_path,
                            "oom": bool(ginfo.get("oom_mode")),
                            "partition_loads_per_step": st_last["partition_loads"] if st_last else None,
                            "oom_zerocopy": zc,
@@ -701,6 +718,65 @@ def main():
         dist.destroy_process_group()
     G.close()
     return 0
+
+
+def run_scan_path(cs, g, cfg, deg, seeds, base, rng_seeds, n, dev, local, stream, flush, args):
+    """detail.scan_path: the same workload through the per-step scan path -- no CTPS cache, no
+    walk index, no node2vec index: every step evaluates its pool's biases and scans them
+    (the north star's literal hot path, §4.1).  Degree walks stream the materialised per-edge
+    bias (CSAW_GRAPH_EDGE_BIAS) unless --gather-bias.  Timed like `value` (L2 flushed before
+    each step, CUDA events on the launching stream)."""
+    try:
+        eb = cfg.workload == "walk" and cfg.bias == "degree" and not args.gather_bias
+        Gs = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, edge_bias=eb)
+        info = Gs.info()
+        bias = bias_of(cs, cfg)
+        kind = workload_of(cfg)
+        if kind == "walk":
+            shape = (n, cfg.length, 2) if cfg.workload == "mdrw" else (n, cfg.length + 1)
+            out = torch.empty(shape, dtype=torch.int32, device=dev)
+            res = {}
+
+            def sstep(seed):
+                cs.csaw_walk(Gs, bias, seeds, cfg.length, instance_base=base, rng_seed=seed, out=out, stream=stream)
+                return n * cfg.length
+        else:
+            res = {}
+
+            def sstep(seed):
+                res["r"] = cs.csaw_sample(Gs, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth,
+                                          instance_base=base, rng_seed=seed, stream=stream)
+                return int(res["r"][1].numel())
+        sstep(rng_seeds[0])            # warm-up
+        torch.cuda.synchronize(dev)
+        ts, edges, hot, hl = [], 0, 0.0, 0
+        for i in range(args.scan_path_steps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            edges += sstep(rng_seeds[i % len(rng_seeds)])
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ts.append(e0.elapsed_time(e1))
+            st = cs.csaw_stats(Gs)
+            hot += st["hot_kernel_ms"]
+            hl += st["hot_launches"]
+        if kind == "walk":
+            b, model = walk_alg_bytes(cfg, deg, out, False, eb)
+        else:
+            b, model = sample_alg_bytes(cfg, deg, seeds, *res["r"])
+        peak = load_peaks().get("hbm_gbs", 7672.0)
+        hot_avg = hot / max(hl, 1)
+        ach = b / (hot_avg / 1000.0) / 1e9 if hot_avg > 0 else None
+        kname = hot_kernel_name(cfg, False, False, 0, 0, False, False, eb)
+        Gs.close()
+        return {"kernel": kname, "ms_per_step": sum(ts) / len(ts), "value": edges / (sum(ts) / 1000.0), "unit": UNIT,
+                "steps": len(ts), "alg_bytes_per_launch": b, "bytes_model": BYTES_MODEL[model],
+                "achieved_gbs": ach, "frac": (ach / peak) if ach else None, "hot_ms_per_launch": hot_avg,
+                "edge_bias": bool(info.get("edge_bias")),
+                "what": "per-step bias evaluation + warp-scan CTPS + ITS (no static-bias cache / index)"}
+    except Exception as ex:  # report, never hide
+        return {"error": str(ex)}
 
 
 def run_zerocopy(cs, g, cfg, bias, seeds, base, seed, kind, n, dev, local, stream, flush, out_ref, r_ref, G, args):
@@ -808,8 +884,10 @@ def run_e2e(cs, G, bias, seeds, cfg, base, rng_seeds, args, kind, n, dev, world,
                                       "step (max over ranks)"}
 
 
-def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads=False, n2x=False):
+def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads=False, n2x=False, eb=False):
     if cfg.workload == "walk":
+        if cfg.bias == "degree" and not cached and eb:
+            return "k_walk_vscan<uint32>"
         if cfg.bias == "degree" and wix_leaf and heads and wix_group == 32:
             return f"k_walk_head<{wix_leaf}>"
         if cfg.bias == "degree" and wix_leaf:

@@ -72,8 +72,15 @@ typedef enum {
     CSAW_BIAS_MH = 6,           /* Metropolis-Hastings walk: accept iff below(U(ACCEPT), deg u) < deg v, else stay */
     CSAW_BIAS_RESTART = 7,      /* walk with restart: with probability pf return to the start vertex */
     CSAW_BIAS_JUMP = 8,         /* walk with jump: with probability pf jump to below(U(TARGET), V) */
-    CSAW_BIAS_SNOWBALL = 9      /* snowball sampling: every neighbour of every expanded vertex to
+    CSAW_BIAS_SNOWBALL = 9,     /* snowball sampling: every neighbour of every expanded vertex to
                                    `depth` (select-all, R8); fanout ignored (may be NULL); sampling only */
+    CSAW_BIAS_WEIGHT = 10       /* EdgeBias = w(e), the graph's fp32 edge weights (Eq. 3, f(e); F real-valued
+                                   P:228): walks (biased DeepWalk over weights) and neighbor sampling without
+                                   replacement.  Float path (R28): fp32 weights summed in fp64, draw x = r * T with
+                                   r = (U >> 11) * 2^-53, region [S_s, S_{s+1}) holding x, zero weights never chosen;
+                                   the picks equal the exact fp64 left-to-right definition except for draws within a
+                                   few ulps of a region boundary (the summation order differs).  Needs a graph
+                                   created with csaw_csr.weights (else INVALID_ARG); in-memory graphs only. */
 } csaw_bias_kind;
 
 typedef struct {
@@ -91,7 +98,10 @@ typedef struct {
  * col_idx uint32[E] with values < V.  Rows should be sorted ascending without
  * duplicates (node2vec's N(prev) membership test relies on sorted rows; the
  * library checks and reports csaw_graph_info.rows_sorted).  Host or device
- * pointers; copied, never retained.  weights: reserved, must be NULL. */
+ * pointers; copied, never retained.
+ * weights: nullable fp32[E], finite and >= 0 (else BAD_GRAPH), aligned with col_idx: the
+ * EdgeBias w(e) of CSAW_BIAS_WEIGHT (Eq. 3).  Copied to the device (+ 512 B of
+ * zero padding); not supported together with an out-of-memory budget (UNSUPPORTED). */
 typedef struct {
     int64_t num_vertices;
     int64_t num_edges;
@@ -177,6 +187,12 @@ typedef struct {
  * per step.  Picks are identical.  Best-effort: if the index does not fit, the graph is
  * created without it (csaw_graph_info_t.node2vec_index = 0). */
 #define CSAW_GRAPH_N2V_INDEX 0x200u
+/* csaw_graph_opts.flags (in-memory graphs): materialised degree bias ebias[e] = deg(col[e]),
+ * one u32 per CSR entry (+ padding).  Degree-biased walks without the CTPS cache then stream
+ * each pool's biases as 16 B vectors (vscan.cuh) instead of gathering deg[u] per neighbour
+ * (one 32 B sector per 4 B): the per-step bias evaluation + warp scan of the CTPS (§4.1,
+ * P:477-480) stays, only the gather becomes a coalesced read.  Results are identical. */
+#define CSAW_GRAPH_EDGE_BIAS 0x400u
 
 typedef struct {
     int64_t num_vertices, num_edges;
@@ -192,6 +208,8 @@ typedef struct {
     int32_t node2vec_tri;           /* 1 if per-edge triangle counts were built (CSAW_GRAPH_N2V_TRI on a symmetric graph) */
     int32_t walk_index_heads;       /* 1 if the walk index has 512 B vertex heads (degree walks: k_walk_head) */
     int32_t node2vec_index;         /* 1 if the node2vec intersection index was built (CSAW_GRAPH_N2V_INDEX) */
+    int32_t has_weights;            /* 1 if the graph carries edge weights (csaw_csr.weights) */
+    int32_t edge_bias;              /* 1 if the materialised degree bias was built (CSAW_GRAPH_EDGE_BIAS) */
 } csaw_graph_info_t;
 
 typedef struct csaw_graph csaw_graph;  /* opaque */
@@ -216,7 +234,8 @@ typedef struct {
 /* Create a graph on opt->device (opt may be NULL: device 0, in-memory).
  * Validates the CSR (row_ptr monotone, row_ptr[V] = E, col < V) on the device,
  * builds deg[v] = row_ptr[v+1]-row_ptr[v] (u32).  Errors: INVALID_ARG (null /
- * negative sizes / V >= 2^32-1 / weights != NULL), BAD_GRAPH, NO_MEMORY, CUDA. */
+ * negative sizes / V >= 2^32-1), BAD_GRAPH (incl. a negative or non-finite weight),
+ * UNSUPPORTED (weights with a device budget), NO_MEMORY, CUDA. */
 CSAW_API csaw_status csaw_graph_create(const csaw_csr *csr, const csaw_graph_opts *opt, csaw_graph **out);
 CSAW_API csaw_status csaw_graph_destroy(csaw_graph *g);
 CSAW_API csaw_status csaw_graph_info(const csaw_graph *g, csaw_graph_info_t *out);

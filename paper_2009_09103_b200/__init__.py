@@ -88,13 +88,15 @@ CSAW_GRAPH_N2V_TRI = 0x40
 CSAW_GRAPH_NEXT_META = 0x80
 CSAW_GRAPH_CHUNK_CACHE = 0x100
 CSAW_GRAPH_N2V_INDEX = 0x200
+CSAW_GRAPH_EDGE_BIAS = 0x400
 
 
 def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, num_partitions: int = 0,
                       max_resident: int = 0, num_streams: int = 0, ctps_cache: bool = False,
                       zerocopy: bool = False, batched_only: bool = False, oom_ws: bool = True,
                       oom_bal: bool = True, walk_index: bool = True, node2vec_tri: bool = False,
-                      next_meta: bool = False, chunk_cache: bool = False, node2vec_index: bool = False) -> Graph:
+                      next_meta: bool = False, chunk_cache: bool = False, node2vec_index: bool = False,
+                      weights=None, edge_bias: bool = False) -> Graph:
     """row_ptr int64[V+1], col_idx int32/uint32[E] (torch tensors, host or device).
     ctps_cache=True builds the static-bias CTPS cache (CSAW_GRAPH_CTPS_CACHE);
     zerocopy=True (with budget_bytes > 0) reads col_idx from pinned host memory;
@@ -104,9 +106,13 @@ def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, 
     node2vec_tri=True builds per-edge triangle counts (CSAW_GRAPH_N2V_TRI); next_meta=True
     the per-entry next-vertex metadata used by MDRW (CSAW_GRAPH_NEXT_META); chunk_cache=True
     the degree-bias chunk-total cache (CSAW_GRAPH_CHUNK_CACHE; automatic in OOM mode); node2vec_index=True
-    the node2vec per-edge intersection index (CSAW_GRAPH_N2V_INDEX, best-effort)."""
+    the node2vec per-edge intersection index (CSAW_GRAPH_N2V_INDEX, best-effort); weights = float32[E]
+    edge weights (csaw_csr.weights, EdgeBias of the "weight" selector); edge_bias=True the materialised
+    degree bias deg(col[e]) (CSAW_GRAPH_EDGE_BIAS: degree walks without the cache stream it)."""
     V = row_ptr.numel() - 1
-    csr = csaw_csr(V, col_idx.numel(), _ptr(row_ptr), _ptr(col_idx), None)
+    if weights is not None and weights.dtype != torch.float32:
+        raise TypeError("weights must be float32")
+    csr = csaw_csr(V, col_idx.numel(), _ptr(row_ptr), _ptr(col_idx), _ptr(weights) or None)
     opt = csaw_graph_opts(device, budget_bytes, num_partitions, max_resident, num_streams,
                           (CSAW_GRAPH_CTPS_CACHE if ctps_cache else 0) | (CSAW_GRAPH_OOM_ZEROCOPY if zerocopy else 0)
                           | (CSAW_GRAPH_SAMPLE_BATCHED if batched_only else 0)
@@ -115,7 +121,8 @@ def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, 
                           | (CSAW_GRAPH_N2V_TRI if node2vec_tri else 0)
                           | (CSAW_GRAPH_NEXT_META if next_meta else 0)
                           | (CSAW_GRAPH_CHUNK_CACHE if chunk_cache else 0)
-                          | (CSAW_GRAPH_N2V_INDEX if node2vec_index else 0))
+                          | (CSAW_GRAPH_N2V_INDEX if node2vec_index else 0)
+                          | (CSAW_GRAPH_EDGE_BIAS if edge_bias else 0))
     out = C.c_void_p()
     check(lib().csaw_graph_create(C.byref(csr), C.byref(opt), C.byref(out)))
     return Graph(out.value, device)

@@ -50,7 +50,7 @@ CSAW_OK, CSAW_ERR_CAPACITY = 0, 5
 
 # csaw_bias_kind
 BIAS = {"uniform": 0, "degree": 1, "node2vec": 2, "forest_fire": 3, "layer": 4, "mdrw": 5, "mh": 6, "restart": 7,
-        "jump": 8, "snowball": 9}
+        "jump": 8, "snowball": 9, "weight": 10}
 
 
 class csaw_bias(C.Structure):
@@ -72,7 +72,8 @@ class csaw_graph_info_t(C.Structure):
     _fields_ = [("num_vertices", C.c_int64), ("num_edges", C.c_int64), ("max_degree", C.c_int64),
                 ("nonisolated", C.c_int64), ("rows_sorted", C.c_int32), ("oom_mode", C.c_int32),
                 ("device_bytes", C.c_int64), ("ctps_cache", C.c_int32), ("walk_index_leaf", C.c_int32),
-                ("cache_build_ms", C.c_double), ("walk_index_group", C.c_int32), ("node2vec_tri", C.c_int32), ("walk_index_heads", C.c_int32), ("node2vec_index", C.c_int32)]
+                ("cache_build_ms", C.c_double), ("walk_index_group", C.c_int32), ("node2vec_tri", C.c_int32), ("walk_index_heads", C.c_int32), ("node2vec_index", C.c_int32),
+                ("has_weights", C.c_int32), ("edge_bias", C.c_int32)]
 
 
 class csaw_run_stats(C.Structure):

@@ -175,7 +175,20 @@ struct ValidateOut {
     unsigned long long unsorted;       // count of rows not strictly ascending
     unsigned long long max_deg;
     unsigned long long nonisolated;
+    unsigned long long bad_weight;     // first e with weights[e] < 0 or not finite (+1)
 };
+
+__global__ void k_validate_weights(const float* __restrict__ w, int64_t E, ValidateOut* out) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+        if (!(w[e] >= 0.0f && isfinite(w[e]))) atomicMin(&out->bad_weight, static_cast<unsigned long long>(e + 1));
+}
+
+// materialised degree bias per CSR entry (vscan.cuh): ebias[e] = deg(col[e])
+__global__ void k_build_ebias(const uint32_t* __restrict__ col, const uint32_t* __restrict__ deg, int64_t E,
+                              uint32_t* __restrict__ ebias) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+        ebias[e] = __ldg(deg + __ldg(col + e));
+}
 
 __global__ void k_validate_rows(const int64_t* __restrict__ rp, int64_t V, uint32_t* __restrict__ deg,
                                 ValidateOut* out) {
@@ -390,6 +403,8 @@ static csaw_status build_wix_t(csaw_graph* g, int blocks) {
             cudaGetLastError();
             if (g->c32) cudaFree(g->c32);
             if (g->wcol) cudaFree(g->wcol);
+    if (g->w) cudaFree(g->w);
+    if (g->ebias) cudaFree(g->ebias);
             if (g->winn) cudaFree(g->winn);
             g->c32 = g->wcol = g->winn = nullptr;
         } else {
@@ -594,9 +609,10 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
     if (csr->num_vertices < 0 || csr->num_edges < 0) return fail(CSAW_ERR_INVALID_ARG, "negative size");
     if (csr->num_vertices >= static_cast<int64_t>(NONE)) return fail(CSAW_ERR_INVALID_ARG, "num_vertices must be < 2^32-1");
     if (!csr->row_ptr || (csr->num_edges > 0 && !csr->col_idx)) return fail(CSAW_ERR_INVALID_ARG, "row_ptr/col_idx is NULL");
-    if (csr->weights) return fail(CSAW_ERR_UNSUPPORTED, "edge weights are reserved (must be NULL)");
     csaw_graph_opts o{};
     if (opt) o = *opt;
+    if (csr->weights && o.device_budget_bytes > 0)
+        return fail(CSAW_ERR_UNSUPPORTED, "edge weights are not supported in out-of-memory mode");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
         cudaGetLastError();
@@ -637,7 +653,7 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
     if (rp_first != 0 || rp_last != E)
         return cleanup(fail(CSAW_ERR_BAD_GRAPH, "row_ptr[0] must be 0 and row_ptr[V] must equal num_edges"));
     CREATE_CUDA(cudaMalloc(&dv, sizeof(ValidateOut)), "cudaMalloc");
-    ValidateOut hv{~0ull, ~0ull, 0, 0, 0};
+    ValidateOut hv{~0ull, ~0ull, 0, 0, 0, ~0ull};
     cudaMemcpy(dv, &hv, sizeof(hv), cudaMemcpyHostToDevice);
     const int blocks = g->num_sms * 8;
     if (V > 0) k_validate_rows<<<blocks, 256>>>(g->row_ptr, V, g->deg, dv);
@@ -655,6 +671,12 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         if (E > 0) CREATE_CUDA(cudaMemcpy(dcol, csr->col_idx, sizeof(uint32_t) * E, cudaMemcpyDefault), "copy col_idx");
         if (E > 0) k_validate_cols<<<blocks, 256>>>(dcol, E, 0, V, dv);
         if (V > 0) k_validate_sorted<<<blocks, 256>>>(g->row_ptr, dcol, 0, V, dv);
+        if (csr->weights) {   // EdgeBias = w(e): fp32, finite, >= 0; VROW entries of zero padding (vscan.cuh)
+            CREATE_CUDA(cudaMalloc(&g->w, sizeof(float) * (E + VSCAN_PAD)), "cudaMalloc(weights)");
+            CREATE_CUDA(cudaMemset(g->w, 0, sizeof(float) * (E + VSCAN_PAD)), "memset(weights)");
+            if (E > 0) CREATE_CUDA(cudaMemcpy(g->w, csr->weights, sizeof(float) * E, cudaMemcpyDefault), "copy weights");
+            if (E > 0) k_validate_weights<<<blocks, 256>>>(g->w, E, dv);
+        }
     } else {
         // Out-of-memory mode (§5): the full col_idx lives in pinned host memory; the
         // device holds row_ptr + deg and R arena slots of one partition each.  The
@@ -741,6 +763,9 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
     dv = nullptr;
     if (hv.bad_col != ~0ull)
         return cleanup(fail(CSAW_ERR_BAD_GRAPH, "col_idx[" + std::to_string(hv.bad_col - 1) + "] >= num_vertices"));
+    if (hv.bad_weight != ~0ull)
+        return cleanup(fail(CSAW_ERR_BAD_GRAPH, "weights[" + std::to_string(hv.bad_weight - 1) +
+                                                    "] is negative or not finite"));
     g->rows_sorted = hv.unsorted == 0;
     // chunk-total cache of the degree bias: always in OOM mode when it fits the budget (no
     // per-entry cache does), on request in memory
@@ -822,6 +847,26 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         cudaEventDestroy(c0);
         cudaEventDestroy(c1);
     }
+    if ((o.flags & CSAW_GRAPH_EDGE_BIAS) && !g->oom) {   // ebias[e] = deg(col[e]) (vscan.cuh degree pools)
+        cudaEvent_t c0, c1;
+        CREATE_CUDA(cudaEventCreate(&c0), "event");
+        CREATE_CUDA(cudaEventCreate(&c1), "event");
+        cudaEventRecord(c0);
+        if (cudaMalloc(&g->ebias, sizeof(uint32_t) * (E + VSCAN_PAD)) != cudaSuccess) {   // an accelerator: skip it
+            cudaGetLastError();
+            g->ebias = nullptr;
+        } else {
+            cudaMemsetAsync(g->ebias, 0, sizeof(uint32_t) * (E + VSCAN_PAD));
+            if (E > 0) k_build_ebias<<<blocks, 256>>>(g->col, g->deg, E, g->ebias);
+        }
+        cudaEventRecord(c1);
+        cudaEventSynchronize(c1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c0, c1);
+        cudaEventDestroy(c0);
+        cudaEventDestroy(c1);
+        if (g->ebias) g->cache_build_ms += ms;
+    }
     CREATE_CUDA(cudaEventCreate(&g->ev0), "event");
     CREATE_CUDA(cudaEventCreate(&g->ev1), "event");
     CREATE_CUDA(cudaEventCreateWithFlags(&g->ev_done, cudaEventDisableTiming), "event");
@@ -850,6 +895,8 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->n2x_rec) cudaFree(g->n2x_rec);
     if (g->n2x_idx) cudaFree(g->n2x_idx);
     if (g->wcol) cudaFree(g->wcol);
+    if (g->w) cudaFree(g->w);
+    if (g->ebias) cudaFree(g->ebias);
     if (g->winn) cudaFree(g->winn);
     auto& st = g->oomst;
     if (st.h_col) cudaFreeHost(st.h_col);
@@ -884,6 +931,8 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
                         (g->tri ? static_cast<int64_t>(sizeof(uint32_t) * g->E) : 0) +
                         (g->n2x_rec ? static_cast<int64_t>(4 * sizeof(uint4) * g->E + sizeof(uint32_t) * g->n2x_total) : 0) +
                         (g->nmp ? static_cast<int64_t>(sizeof(uint64_t) * g->E) : 0) +
+                        (g->w ? static_cast<int64_t>(sizeof(float) * (g->E + VSCAN_PAD)) : 0) +
+                        (g->ebias ? static_cast<int64_t>(sizeof(uint32_t) * (g->E + VSCAN_PAD)) : 0) +
                         static_cast<int64_t>(sizeof(uint64_t) * g->ccache_entries);
     out->ctps_cache = g->cps ? 1 : 0;
     out->walk_index_leaf = g->wix_leaf;
@@ -892,6 +941,8 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
     out->walk_index_heads = g->whead ? 1 : 0;
     out->node2vec_index = g->n2x_rec ? 1 : 0;
     out->cache_build_ms = g->cache_build_ms;
+    out->has_weights = g->w ? 1 : 0;
+    out->edge_bias = g->ebias ? 1 : 0;
     return CSAW_OK;
 }
 
@@ -953,7 +1004,7 @@ CSAW_API csaw_status csaw_sample_capacity(const csaw_bias* bias, const int32_t* 
 
 static csaw_status check_bias(const csaw_bias* b) {
     if (!b) return fail(CSAW_ERR_INVALID_ARG, "bias is NULL");
-    if (b->kind < CSAW_BIAS_UNIFORM || b->kind > CSAW_BIAS_SNOWBALL) return fail(CSAW_ERR_INVALID_ARG, "unknown bias kind");
+    if (b->kind < CSAW_BIAS_UNIFORM || b->kind > CSAW_BIAS_WEIGHT) return fail(CSAW_ERR_INVALID_ARG, "unknown bias kind");
     if (b->migration < 0 || b->migration > 2) return fail(CSAW_ERR_INVALID_ARG, "migration must be 0, 1 or 2");
     if (b->a_max != 0 && (b->a_max < 2 || b->a_max > 16382 || (b->a_max & 1)))
         return fail(CSAW_ERR_INVALID_ARG, "a_max must be 0 (default 64) or even in [2, 16382]");
@@ -1016,7 +1067,9 @@ CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32
     }
     // pinned host output: the kernels write the paths straight into it over the host link,
     // overlapped with the walk (no device staging, no copy after the kernel)
-    void* const path_pinned = path_dev ? nullptr : pinned_device_ptr(path);
+    // (kernels that store one scattered 4 B entry per thread and step -- the node2vec index
+    // kernel -- would turn that into uncoalesced host-link writes: they stage and copy)
+    void* const path_pinned = (path_dev || !walk_path_direct_ok(g, b)) ? nullptr : pinned_device_ptr(path);
     if (path_pinned) {
         d_path = static_cast<uint32_t*>(path_pinned);
     } else if (!path_dev) {
@@ -1051,6 +1104,8 @@ CSAW_API csaw_status csaw_sample(const csaw_graph* g, const csaw_bias* bias, con
     if (b.kind == CSAW_BIAS_NODE2VEC || b.kind == CSAW_BIAS_MDRW || b.kind == CSAW_BIAS_MH ||
         b.kind == CSAW_BIAS_RESTART || b.kind == CSAW_BIAS_JUMP)
         return fail(CSAW_ERR_INVALID_ARG, "node2vec / MDRW / MH / restart / jump are walk selectors (use csaw_walk)");
+    if (b.kind == CSAW_BIAS_WEIGHT && !g->w)
+        return fail(CSAW_ERR_INVALID_ARG, "CSAW_BIAS_WEIGHT needs a graph created with edge weights");
     if (!num_edges) return fail(CSAW_ERR_INVALID_ARG, "num_edges is NULL");
     *num_edges = 0;
     if (depth < 1 || depth > 255) return fail(CSAW_ERR_INVALID_ARG, "depth must be in [1, 255]");

@@ -23,6 +23,9 @@ struct Status {
 
 csaw_status cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 
+// zero padding after per-edge arrays read as 16 B vectors (vscan.cuh: one warp row = 128 entries)
+#define VSCAN_PAD 128
+
 #define CSAW_CUDA(call)                                                         \
     do {                                                                        \
         cudaError_t e_ = (call);                                                \
@@ -141,6 +144,8 @@ struct csaw_graph {
     uint4* n2x_rec = nullptr;     // [4 E] {offset lo, offset hi 8 | C << 8, ppos, mb}, {v, row lo, row hi 8 | deg << 8, 0}, P[8]
     uint32_t* n2x_idx = nullptr;  // member positions, n2x_total entries
     uint64_t n2x_total = 0;
+    float* w = nullptr;           // [E + VSCAN_PAD] caller edge weights (EdgeBias = w(e), vscan.cuh), zero-padded
+    uint32_t* ebias = nullptr;    // [E + VSCAN_PAD] materialised degree bias deg(col[e]) (CSAW_GRAPH_EDGE_BIAS)
     int wix_group = 8;            // lanes per walker in k_walk_wixg (32 = k_walk_wix, one warp per walker)
     int wix_leaf = 0;             // leaf fanout 32 / 64 / 128 (0 = not built)
     double cache_build_ms = 0.0;
@@ -204,7 +209,16 @@ csaw_status launch_node2vec_index(const csaw_graph* g, const uint32_t* seeds, ui
                                   uint2 key, uint32_t* path, unsigned long long* counters, uint32_t wp, uint32_t w1,
                                   uint32_t wq, cudaStream_t st);
 
+// vwalk.cu: walks over a per-edge bias stream (weights = true: g->w, else g->ebias); group =
+// warps per walker (0 = automatic; results do not depend on it)
+csaw_status launch_walk_vscan(const csaw_graph* g, bool weights, const uint32_t* seeds, uint64_t n, int32_t L,
+                              uint32_t base, uint2 key, uint32_t* path, unsigned long long* counters, int group,
+                              cudaStream_t st);
+
 // walk.cu / sample.cu entry points
+// false if run_walk's kernel for b writes the path with scattered per-thread stores (the
+// node2vec index kernel): a pinned host path is then staged in device memory and copied
+bool walk_path_direct_ok(const csaw_graph* g, const csaw_bias& b);
 csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds,
                      int64_t n, uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st);
 // pinned host outputs, device-mapped (the fused sampler writes them directly; the batched

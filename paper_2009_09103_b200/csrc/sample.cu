@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "select.cuh"
+#include "vscan.cuh"
 #include "util.cuh"
 
 namespace csaw {
@@ -132,10 +133,12 @@ struct SelArgs {
     uint64_t nidx;
     const uint64_t* __restrict__ ccache;  // chunk-total cache (degree pools), optional
     WixPtrs wx;                           // vertex heads (cached degree pools), optional
+    const float* __restrict__ w = nullptr;   // edge weights (kMode 3)
 };
 
 // Neighbor sampling / forest fire: one warp per queue entry.
-// kMode: 0 = uniform (closed form), 1 = degree (scanned CTPS), 2 = degree (cached CTPS)
+// kMode: 0 = uniform (closed form), 1 = degree (scanned CTPS), 2 = degree (cached CTPS),
+//        3 = edge weights (float CTPS over the weight stream, vscan.cuh; R28)
 template <int kMode>
 __global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_ns_select(SelArgs a) {
     __shared__ uint64_t tab_all[SEL_WARPS][TAB];
@@ -173,6 +176,13 @@ __global__ void __launch_bounds__(SEL_WARPS * 32, 3) k_ns_select(SelArgs a) {
                 const Ctps C = build_ctps(P, tab);
                 cnt = select_wor(P, C, tab, bm, k, dk, a.a_max, gl, emit);
                 scanned += (a.ccache && C.m) ? 32u * C.m : n;   // chunk cache: ~one chunk rescanned per pick
+            } else if constexpr (kMode == 3) {
+                VPool<float> P;
+                P.init(a.w, a.col, static_cast<uint64_t>(b0), n);
+                double* ftab = reinterpret_cast<double*>(tab);
+                const VCtps<float> C = vscan_build<float, 1>(P, ftab, nullptr, 0, [] {});
+                cnt = vscan_select_wor(P, C, ftab, k, dk, a.a_max, gl, emit);
+                scanned += n;
             } else {
                 UniformPool P{a.col, static_cast<uint64_t>(b0), n};
                 const Ctps C = build_ctps(P, tab);
@@ -744,6 +754,7 @@ struct FusedArgs {
     uint64_t* report;                     // pinned host mailbox: flags, total, counters[0..3]
     const uint64_t* __restrict__ ccache;  // chunk-total cache (degree pools), optional
     WixPtrs wx;                           // vertex heads (cached degree / layer pools), optional
+    const float* __restrict__ w = nullptr;   // edge weights (kMode 6)
 };
 
 // Run by the last block of k_sample_fused to finish (ticket): the per-instance edge
@@ -828,7 +839,7 @@ struct FusedLayerEmit {
 };
 
 // kMode: 0 uniform NS, 1 degree NS (scan), 2 degree NS (cache), 3 forest fire,
-//        4 layer (scan), 5 layer (cache)
+//        4 layer (scan), 5 layer (cache), 6 edge-weight NS (float CTPS, vscan.cuh; R28)
 template <int kMode>
 // blocks / SM: forest fire (no layer prefix table, 7 KB smem per warp) 8, layer 6 (smem-bound), NS 4
 __global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB : kMode >= 4 ? 6 : FUSED_MINB)
@@ -921,6 +932,13 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB :
                         const Ctps C = build_ctps(P, tab);
                         c = select_wor(P, C, tab, bm, k, dk, a.a_max, nullptr, emit);
                         scanned += (a.ccache && C.m) ? 32u * C.m : nd;
+                    } else if constexpr (kMode == 6) {
+                        VPool<float> P;
+                        P.init(a.w, a.col, static_cast<uint64_t>(b0), nd);
+                        double* ftab = reinterpret_cast<double*>(tab);
+                        const VCtps<float> C = vscan_build<float, 1>(P, ftab, nullptr, 0, [] {});
+                        c = vscan_select_wor(P, C, ftab, k, dk, a.a_max, nullptr, emit);
+                        scanned += nd;
                     } else {
                         UniformPool P{a.col, static_cast<uint64_t>(b0), nd};
                         const Ctps C = build_ctps(P, tab);
@@ -1170,6 +1188,7 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     a.offs_host = offs_host;
     a.ccache = g->ccache;
     a.wx = wix_ptrs(g);
+    a.w = g->w;
     a.done = reinterpret_cast<unsigned*>(counters + 13);   // zeroed by the memset above
     a.report = const_cast<uint64_t*>(hbox);
     a.V = g->V;
@@ -1185,6 +1204,8 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     } else if (b.kind == CSAW_BIAS_DEGREE) {
         if (g->cps) k_sample_fused<2><<<grid, FUSED_WARPS * 32, 0, st>>>(a);
         else k_sample_fused<1><<<grid, FUSED_WARPS * 32, 0, st>>>(a);
+    } else if (b.kind == CSAW_BIAS_WEIGHT) {
+        k_sample_fused<6><<<grid, FUSED_WARPS * 32, 0, st>>>(a);
     } else {
         k_sample_fused<0><<<grid, FUSED_WARPS * 32, 0, st>>>(a);
     }
@@ -1388,7 +1409,9 @@ csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int
                            static_cast<uint32_t>(l), static_cast<uint32_t>(base), key, a_max, glist, kmax, counters,
                            g->cps, g->npos, g->bt, g->bt_off, static_cast<uint32_t>(b.migration), nullptr, 0,
                            g->ccache, wix_ptrs(g)};
-                if (degree_bias && g->cps) k_ns_select<2><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
+                sa.w = g->w;
+                if (b.kind == CSAW_BIAS_WEIGHT) k_ns_select<3><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
+                else if (degree_bias && g->cps) k_ns_select<2><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
                 else if (degree_bias) k_ns_select<1><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
                 else k_ns_select<0><<<sgrid, SEL_WARPS * 32, 0, st>>>(sa);
             }

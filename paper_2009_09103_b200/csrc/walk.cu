@@ -1619,6 +1619,10 @@ static int walk_grid(const csaw_graph* g, int64_t n) {
     return static_cast<int>(std::max<int64_t>(1, (warps + WALK_WARPS - 1) / WALK_WARPS));
 }
 
+bool walk_path_direct_ok(const csaw_graph* g, const csaw_bias& b) {
+    return !(b.kind == CSAW_BIAS_NODE2VEC && g->n2x_rec && !g->oom && n2v_integer_scale(b.p, b.q) != 0);
+}
+
 csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds, int64_t n,
                      uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st) {
     void* cnt;
@@ -1664,6 +1668,13 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         }
     } else if (b.kind == CSAW_BIAS_DEGREE && g->cps) {
         k_walk_cached<<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a, g->cps, g->bt, g->bt_off, g->nmp);
+    } else if ((b.kind == CSAW_BIAS_DEGREE && g->ebias) || b.kind == CSAW_BIAS_WEIGHT) {
+        // per-edge bias streams (vscan.cuh): the materialised degree bias or the edge weights
+        if (b.kind == CSAW_BIAS_WEIGHT && !g->w)
+            return fail(CSAW_ERR_INVALID_ARG, "CSAW_BIAS_WEIGHT needs a graph created with edge weights");
+        CSAW_TRY(launch_walk_vscan(g, b.kind == CSAW_BIAS_WEIGHT, d_seeds, static_cast<uint64_t>(n), length,
+                                   static_cast<uint32_t>(base), key, d_path, static_cast<unsigned long long*>(cnt), 0,
+                                   st));
     } else if (b.kind == CSAW_BIAS_DEGREE) {
         k_walk<false><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a);
     } else if (b.kind == CSAW_BIAS_UNIFORM) {
