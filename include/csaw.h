@@ -168,7 +168,8 @@ typedef struct {
 /* csaw_graph_opts.flags (in-memory graphs, max degree < 2^24): build next-vertex
  * metadata nmp[e] = row_ptr[u] << 24 | deg(u) for u = col[e] (8 B per CSR entry), so an
  * MDRW step reads the new pool vertex's row and VertexBias together with the
- * picked entry instead of one dependent row_ptr lookup later.  Results are identical. */
+ * picked entry instead of one dependent row_ptr lookup later (degree walks on the u64
+ * index, k_walk_cached, use it too).  Results are identical. */
 #define CSAW_GRAPH_NEXT_META 0x80u
 /* csaw_graph_opts.flags (in-memory graphs; built automatically in out-of-memory mode
  * when it fits the budget): chunk-total cache of the degree bias -- for every row of more
@@ -193,6 +194,27 @@ typedef struct {
  * (one 32 B sector per 4 B): the per-step bias evaluation + warp scan of the CTPS (§4.1,
  * P:477-480) stays, only the gather becomes a coalesced read.  Results are identical. */
 #define CSAW_GRAPH_EDGE_BIAS 0x400u
+/* csaw_graph_opts.flags -- variant selectors.  Every one leaves the results unchanged (R7);
+ * they pick between equivalent data layouts / kernels for tests and A/B measurements:
+ *   WALK_NO_HEADS       the walk index without its 512 B vertex heads (walks search records)
+ *   WALK_LEAF_64 / _32  walk-index leaf fanout 64 / 32 instead of 128
+ *   WALK_GROUP_16 / _8  degree walks on the index with 16 / 8 lanes per walker (leaf >= 64
+ *                       for 16) instead of one warp per walker
+ *   SAMPLE_NO_HEADS     cached degree / layer sampling pools search the u64 B-tree, not the heads
+ *   OOM_NO_CHUNK_CACHE  out-of-memory mode without the automatic chunk-total cache
+ *   OOM_ZC_NO_PREFIX    zero-copy OOM mode keeps no col_idx prefix resident (all host reads)
+ *   MDRW_GENERIC        MDRW uses the general kernel (shared-memory block totals) for every pool
+ *   MDRW_PACKED         MDRW pools <= 2,048 slots keep 8 B packed slot records (row << 24 | degree) */
+#define CSAW_GRAPH_WALK_NO_HEADS 0x800u
+#define CSAW_GRAPH_WALK_LEAF_64 0x1000u
+#define CSAW_GRAPH_WALK_LEAF_32 0x2000u
+#define CSAW_GRAPH_WALK_GROUP_16 0x4000u
+#define CSAW_GRAPH_WALK_GROUP_8 0x8000u
+#define CSAW_GRAPH_SAMPLE_NO_HEADS 0x10000u
+#define CSAW_GRAPH_OOM_NO_CHUNK_CACHE 0x20000u
+#define CSAW_GRAPH_OOM_ZC_NO_PREFIX 0x40000u
+#define CSAW_GRAPH_MDRW_GENERIC 0x80000u
+#define CSAW_GRAPH_MDRW_PACKED 0x100000u
 
 typedef struct {
     int64_t num_vertices, num_edges;

@@ -89,6 +89,17 @@ CSAW_GRAPH_NEXT_META = 0x80
 CSAW_GRAPH_CHUNK_CACHE = 0x100
 CSAW_GRAPH_N2V_INDEX = 0x200
 CSAW_GRAPH_EDGE_BIAS = 0x400
+# variant selectors (results identical; tests / A/B), csaw.h
+CSAW_GRAPH_WALK_NO_HEADS = 0x800
+CSAW_GRAPH_WALK_LEAF_64 = 0x1000
+CSAW_GRAPH_WALK_LEAF_32 = 0x2000
+CSAW_GRAPH_WALK_GROUP_16 = 0x4000
+CSAW_GRAPH_WALK_GROUP_8 = 0x8000
+CSAW_GRAPH_SAMPLE_NO_HEADS = 0x10000
+CSAW_GRAPH_OOM_NO_CHUNK_CACHE = 0x20000
+CSAW_GRAPH_OOM_ZC_NO_PREFIX = 0x40000
+CSAW_GRAPH_MDRW_GENERIC = 0x80000
+CSAW_GRAPH_MDRW_PACKED = 0x100000
 
 
 def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, num_partitions: int = 0,
@@ -96,7 +107,7 @@ def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, 
                       zerocopy: bool = False, batched_only: bool = False, oom_ws: bool = True,
                       oom_bal: bool = True, walk_index: bool = True, node2vec_tri: bool = False,
                       next_meta: bool = False, chunk_cache: bool = False, node2vec_index: bool = False,
-                      weights=None, edge_bias: bool = False) -> Graph:
+                      weights=None, edge_bias: bool = False, flags: int = 0) -> Graph:
     """row_ptr int64[V+1], col_idx int32/uint32[E] (torch tensors, host or device).
     ctps_cache=True builds the static-bias CTPS cache (CSAW_GRAPH_CTPS_CACHE);
     zerocopy=True (with budget_bytes > 0) reads col_idx from pinned host memory;
@@ -108,7 +119,8 @@ def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, 
     the degree-bias chunk-total cache (CSAW_GRAPH_CHUNK_CACHE; automatic in OOM mode); node2vec_index=True
     the node2vec per-edge intersection index (CSAW_GRAPH_N2V_INDEX, best-effort); weights = float32[E]
     edge weights (csaw_csr.weights, EdgeBias of the "weight" selector); edge_bias=True the materialised
-    degree bias deg(col[e]) (CSAW_GRAPH_EDGE_BIAS: degree walks without the cache stream it)."""
+    degree bias deg(col[e]) (CSAW_GRAPH_EDGE_BIAS: degree walks without the cache stream it); flags = extra
+    CSAW_GRAPH_* bits (the variant selectors)."""
     V = row_ptr.numel() - 1
     if weights is not None and weights.dtype != torch.float32:
         raise TypeError("weights must be float32")
@@ -122,7 +134,7 @@ def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, 
                           | (CSAW_GRAPH_NEXT_META if next_meta else 0)
                           | (CSAW_GRAPH_CHUNK_CACHE if chunk_cache else 0)
                           | (CSAW_GRAPH_N2V_INDEX if node2vec_index else 0)
-                          | (CSAW_GRAPH_EDGE_BIAS if edge_bias else 0))
+                          | (CSAW_GRAPH_EDGE_BIAS if edge_bias else 0) | int(flags))
     out = C.c_void_p()
     check(lib().csaw_graph_create(C.byref(csr), C.byref(opt), C.byref(out)))
     return Graph(out.value, device)

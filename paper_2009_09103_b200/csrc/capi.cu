@@ -403,8 +403,6 @@ static csaw_status build_wix_t(csaw_graph* g, int blocks) {
             cudaGetLastError();
             if (g->c32) cudaFree(g->c32);
             if (g->wcol) cudaFree(g->wcol);
-    if (g->w) cudaFree(g->w);
-    if (g->ebias) cudaFree(g->ebias);
             if (g->winn) cudaFree(g->winn);
             g->c32 = g->wcol = g->winn = nullptr;
         } else {
@@ -414,8 +412,7 @@ static csaw_status build_wix_t(csaw_graph* g, int blocks) {
             // records right after the nodes (total + 16 is a multiple of 4: 16 B aligned)
             g->wrec = reinterpret_cast<uint4*>(g->winn + total + 16);
             k_wix_build<FL><<<blocks, 256>>>(g->row_ptr, g->col, g->cps, woff, V, g->wrec, g->c32, g->wcol, g->winn);
-            const char* nh = std::getenv("CSAW_NO_HEADS");   // A/B: walk the records instead
-            if (!(nh && nh[0] == '1') &&
+            if (!(g->flags & CSAW_GRAPH_WALK_NO_HEADS) &&
                 cudaMalloc(&g->whead, sizeof(uint32_t) * WIX_HEAD_WORDS * std::max<int64_t>(V, 1)) == cudaSuccess)
                 k_head_build<FL><<<blocks, 256>>>(g->wrec, g->c32, g->wcol, g->winn, V, g->whead);
             else
@@ -428,13 +425,11 @@ static csaw_status build_wix_t(csaw_graph* g, int blocks) {
     return s;
 }
 
-// Builds the index unless disabled or some row total is >= 2^32 (then walks keep the u64
-// CpsTree path).  Leaf fanout: CSAW_WIX_LEAF = 32 | 64 | 128 (0 = not built, A/B).
+// Builds the index unless some row total is >= 2^32 (then walks keep the u64 CpsTree path).
+// Leaf fanout 128, or 64 / 32 with CSAW_GRAPH_WALK_LEAF_64 / _32 (cfg2 with vertex heads:
+// 128: 2.374, 64: 2.397, 32: 2.522 ms).
 static csaw_status build_wix(csaw_graph* g, int blocks) {
-    const char* env = std::getenv("CSAW_WIX_LEAF");
-    int leaf = env ? std::atoi(env) : 128;   // cfg2 with vertex heads: 128: 2.374, 64: 2.397, 32: 2.522 ms
-    if (env && leaf == 0) return CSAW_OK;   // A/B: u64 index only
-    if (leaf != 32 && leaf != 64 && leaf != 128) leaf = 128;
+    const int leaf = (g->flags & CSAW_GRAPH_WALK_LEAF_32) ? 32 : (g->flags & CSAW_GRAPH_WALK_LEAF_64) ? 64 : 128;
     unsigned int* wide = nullptr;
     CSAW_CUDA(cudaMalloc(&wide, sizeof(unsigned int)));
     CSAW_CUDA(cudaMemset(wide, 0, sizeof(unsigned int)));
@@ -447,11 +442,10 @@ static csaw_status build_wix(csaw_graph* g, int blocks) {
                                                                : build_wix_t<128>(g, blocks);
     if (s == CSAW_OK && g->c32) {
         g->wix_leaf = leaf;
-        // lanes per walker: 32 (one warp per walker, default) | 16 | 8 (A/B: the sub-warp
-        // kernels are slower at cfg2, 3.7 / 4.4 ms vs 2.8 ms: a warp's walkers then wait for
-        // the slowest of their dependent-load chains every step)
-        const char* ge = std::getenv("CSAW_WIX_GROUP");
-        const int grp = ge ? std::atoi(ge) : 32;
+        // lanes per walker: 32 (one warp per walker, default) | 16 | 8 (CSAW_GRAPH_WALK_GROUP_*;
+        // the sub-warp kernels are slower at cfg2, 3.7 / 4.4 ms vs 2.8 ms: a warp's walkers
+        // then wait for the slowest of their dependent-load chains every step)
+        const int grp = (g->flags & CSAW_GRAPH_WALK_GROUP_8) ? 8 : (g->flags & CSAW_GRAPH_WALK_GROUP_16) ? 16 : 32;
         g->wix_group = (grp == 16 && leaf >= 64) ? 16 : grp == 8 ? 8 : 32;
     }
     return s;
@@ -630,6 +624,7 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
     g->num_sms = prop.multiProcessorCount;
     g->oom = o.device_budget_bytes > 0;
     g->force_batched = (o.flags & CSAW_GRAPH_SAMPLE_BATCHED) != 0;
+    g->flags = o.flags;
     const int64_t V = g->V, E = g->E;
     ValidateOut* dv = nullptr;
     uint32_t* dcol = nullptr;
@@ -709,7 +704,7 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         const int64_t base_resident = sizeof(int64_t) * (V + 1) + sizeof(uint32_t) * V;
         const int64_t arena0 = static_cast<int64_t>(st.zerocopy ? 1 : st.R) * st.slot_edges *
                                static_cast<int64_t>(sizeof(uint32_t));
-        st.want_ccache = !std::getenv("CSAW_NO_CCACHE") && base_resident + cc_bytes + arena0 <= st.budget;
+        st.want_ccache = !(o.flags & CSAW_GRAPH_OOM_NO_CHUNK_CACHE) && base_resident + cc_bytes + arena0 <= st.budget;
         const int64_t resident_bytes = base_resident + (st.want_ccache ? cc_bytes : 0);
         // the arena holds R partitions; zero-copy mode validates through a 1-partition slot only
         const int64_t arena = static_cast<int64_t>(st.zerocopy ? 1 : st.R) * st.slot_edges *
@@ -741,9 +736,8 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
             // proportional to its degree, then one of its entries uniformly), so the fraction
             // of host reads is the uncached fraction, whichever entries are cached.
             const int64_t reserve = std::min<int64_t>(int64_t(512) << 20, st.budget / 8);
-            const char* nc = std::getenv("CSAW_ZC_NOCACHE");   // A/B: pure zero-copy
             const int64_t room = st.budget - resident_bytes - reserve;
-            st.colc_n = (nc && nc[0] == '1') || room <= 0 ? 0 : std::min<int64_t>(E, room / 4);
+            st.colc_n = (o.flags & CSAW_GRAPH_OOM_ZC_NO_PREFIX) || room <= 0 ? 0 : std::min<int64_t>(E, room / 4);
             if (st.colc_n > 0) {
                 if (cudaMalloc(&st.d_colc, sizeof(uint32_t) * st.colc_n) != cudaSuccess) {
                     cudaGetLastError();
@@ -791,14 +785,8 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         cudaFree(part);
         CREATE_CUDA(cudaMalloc(&g->bt, sizeof(uint64_t) * std::max<uint64_t>(btn, 1)), "cudaMalloc(bt)");
         if (V > 0) k_build_bt<<<blocks, 256>>>(g->row_ptr, g->cps, g->bt_off, V, g->bt);
-        // next-vertex metadata for the u64-index walk (k_walk_cached): off by default (measured
-        // 2.5 % slower on cfg2: the extra 256 B per step outweighs the saved row_ptr round);
-        // CSAW_WALK_META=1 enables
-        const char* meta = std::getenv("CSAW_WALK_META");
-        if (!g->nmp && g->max_deg < (1 << 24) && E < (int64_t(1) << 40) && E > 0 && meta && meta[0] == '1') {
-            CREATE_CUDA(cudaMalloc(&g->nmp, sizeof(uint64_t) * E), "cudaMalloc(nmp)");
-            k_build_nmp<<<blocks, 256>>>(g->row_ptr, g->col, E, g->nmp);
-        }
+        // (next-vertex metadata for k_walk_cached: CSAW_GRAPH_NEXT_META, below; measured 2.5 %
+        // slower on cfg2 -- the extra 256 B per step outweighs the saved row_ptr round)
         if (!(o.flags & CSAW_GRAPH_NO_WALK_INDEX)) {
             const csaw_status ws = build_wix(g, blocks);
             if (ws != CSAW_OK) return cleanup(ws);

@@ -144,6 +144,7 @@ struct csaw_graph {
     uint4* n2x_rec = nullptr;     // [4 E] {offset lo, offset hi 8 | C << 8, ppos, mb}, {v, row lo, row hi 8 | deg << 8, 0}, P[8]
     uint32_t* n2x_idx = nullptr;  // member positions, n2x_total entries
     uint64_t n2x_total = 0;
+    uint32_t flags = 0;           // csaw_graph_opts.flags (variant selectors are read from here)
     float* w = nullptr;           // [E + VSCAN_PAD] caller edge weights (EdgeBias = w(e), vscan.cuh), zero-padded
     uint32_t* ebias = nullptr;    // [E + VSCAN_PAD] materialised degree bias deg(col[e]) (CSAW_GRAPH_EDGE_BIAS)
     int wix_group = 8;            // lanes per walker in k_walk_wixg (32 = k_walk_wix, one warp per walker)

@@ -842,14 +842,14 @@ struct FusedLayerEmit {
 //        4 layer (scan), 5 layer (cache), 6 edge-weight NS (float CTPS, vscan.cuh; R28)
 template <int kMode>
 // blocks / SM: forest fire (no layer prefix table, 7 KB smem per warp) 8, layer 6 (smem-bound), NS 4
-__global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB : kMode >= 4 ? 6 : FUSED_MINB)
+__global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB : (kMode == 4 || kMode == 5) ? 6 : FUSED_MINB)
     k_sample_fused(FusedArgs a) {
     __shared__ uint64_t tab_all[FUSED_WARPS][TAB];
     __shared__ uint32_t bm_all[FUSED_WARPS][BM_WORDS];
     __shared__ uint32_t F_all[FUSED_WARPS][F_CAP];
     __shared__ uint32_t NX_all[FUSED_WARPS][F_CAP];
     __shared__ uint32_t VIS_all[FUSED_WARPS][VIS_CAP];
-    __shared__ uint64_t PF_all[FUSED_WARPS][kMode >= 4 ? F_CAP : 1];   // layer pools only
+    __shared__ uint64_t PF_all[FUSED_WARPS][(kMode == 4 || kMode == 5) ? F_CAP : 1];   // layer pools only
     const int wib = threadIdx.x >> 5;
     uint64_t* tab = tab_all[wib];
     uint32_t* bm = bm_all[wib];
@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB :
     uint32_t* VIS = VIS_all[wib];
     uint64_t* PF = PF_all[wib];
     const int lane = lane_id();
-    constexpr bool kLayer = kMode >= 4;
+    constexpr bool kLayer = kMode == 4 || kMode == 5;
     unsigned long long scanned = 0, pools = 0, probes = 0, draws = 0;
     for (uint64_t i = global_warp_id(); i < a.n; i += total_warps()) {
         const uint32_t inst = a.base + static_cast<uint32_t>(i);
@@ -1131,7 +1131,7 @@ constexpr csaw_status FUSED_FALLBACK = static_cast<csaw_status>(-1);
 // vertex heads usable by the cached sampling pools (leaf fanout 128 only)
 static WixPtrs wix_ptrs(const csaw_graph* g) {
     WixPtrs w;
-    if (g->whead && g->wix_leaf == 128 && !std::getenv("CSAW_SAMPLE_NO_HEADS")) {
+    if (g->whead && g->wix_leaf == 128 && !(g->flags & CSAW_GRAPH_SAMPLE_NO_HEADS)) {
         w.head = g->whead; w.c32 = g->c32; w.col = g->wcol; w.inn = g->winn;
     }
     return w;

@@ -12,15 +12,17 @@
 // outside the pool read as 0.  The arrays carry >= 128 entries of zero padding.
 //
 // CTPS layout (shared memory, Acc[TAB] per pool): rows are grouped in chunks of
-// m = ceil(nrows / TAB) rows; tab[c] = the cumulative total at the end of chunk c.  The
-// chunking depends only on the pool (its first entry and length), never on how many warps
-// build it, so every launch shape gives the same sums (R7).  A search finds the chunk
-// holding x in the table and rescans it (two-level ITS).
+// m = max(VMIN, ceil(nrows / TAB)) rows (rounded up to whole batches of VU); tab[c] = the cumulative total at the end of chunk
+// c (lane accumulators over the chunk's rows, one warp reduction per chunk, then a prefix
+// over the chunks).  The chunking depends only on the pool (its first entry and length),
+// never on how many warps build it, so every launch shape gives the same sums (R7).  A
+// search finds the chunk holding x in the table and rescans it row by row (lane prefix of
+// 4 entries + Kogge-Stone across lanes): two-level ITS.
 //
-// Float rounding (R28): within a row a lane sums its 4 entries left to right and the lanes
-// are combined by a Kogge-Stone scan, so S differs from the oracle's left-to-right fp64 sum
-// by a few ulps -- picks may differ only for draws within that distance of a boundary, far
-// inside the checker's 1e-6 rule.  Zero-weight regions are never chosen (R4): the search
+// Float rounding (R28): those association orders differ from the oracle's left-to-right
+// fp64 sum by a few ulps -- picks may differ only for draws within that distance of a
+// boundary, far inside the checker's 1e-6 rule (a rescan that finds no boundary above x in
+// its chunk, possible only through rounding, continues into the next).  Zero-weight regions are never chosen (R4): the search
 // takes the first entry with b > 0 and S_{i+1} > x; a draw at or beyond every boundary
 // (possible only through rounding) takes the last positive entry.
 #pragma once
@@ -32,9 +34,16 @@ namespace csaw {
 
 constexpr int VROW = 128;   // pool entries per row (one 16 B vector per lane)
 #ifndef VSCAN_VU
-#define VSCAN_VU 8
+#define VSCAN_VU 4   // A/B r02 cfg2: VU 8 59.4 ms (register spills) vs 4: 44.4 ms
+#endif
+#ifndef VSCAN_PREFETCH
+#define VSCAN_PREFETCH 0   // A/B r02 cfg2: bulk L2 prefetch of the pool 48.4 ms, without 47.3 ms (hub pools sit in L2)
 #endif
 constexpr int VU = VSCAN_VU;   // rows in flight per warp (VU x 512 B)
+#ifndef VSCAN_VMIN
+#define VSCAN_VMIN 8   // A/B r02 cfg2: 1 row 114, 4 rows 48.4, 8 rows 44.4 ms
+#endif
+constexpr int VMIN = VSCAN_VMIN;   // rows per chunk at least (a search rescans one chunk)
 
 template <class E>
 struct VTraits;
@@ -47,6 +56,11 @@ struct VTraits<float> {
         return r * M;
     }
     __device__ static __forceinline__ double val(float e) { return static_cast<double>(e); }
+    __device__ static __forceinline__ double sum(double v) {   // butterfly warp reduction (fixed order)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        return v;
+    }
     __device__ static __forceinline__ double scan(double v) {   // inclusive Kogge-Stone
         const int lane = lane_id();
 #pragma unroll
@@ -63,6 +77,7 @@ struct VTraits<uint32_t> {
     using Vec = uint4;
     __device__ static __forceinline__ uint64_t draw(uint64_t U, uint64_t M) { return below(U, M); }
     __device__ static __forceinline__ uint64_t val(uint32_t e) { return e; }
+    __device__ static __forceinline__ uint64_t sum(uint64_t v) { return warp_sum(v); }
     __device__ static __forceinline__ uint64_t scan(uint64_t v) { return warp_incl_scan(v); }
 };
 
@@ -84,9 +99,13 @@ struct VPool {
     }
     // the lane's 4 entries of row r (pool indices r*128 + 4 lane + j - head); 0 outside the pool
     __device__ __forceinline__ void load(uint32_t r, E (&e)[4]) const {
-        const int lane = lane_id();
-        const int64_t i0 = static_cast<int64_t>(r) * VROW + 4 * lane - head;
-        const auto* vp = reinterpret_cast<const typename Tr::Vec*>(b + (beg - head)) + static_cast<uint64_t>(r) * 32 + lane;
+        const auto* vp = reinterpret_cast<const typename Tr::Vec*>(b + (beg - head)) + static_cast<uint64_t>(r) * 32 + lane_id();
+        if (r * VROW >= head && (r + 1) * VROW <= head + n) {   // interior row (warp-uniform): no masks
+            const typename Tr::Vec q = __ldg(vp);
+            e[0] = q.x; e[1] = q.y; e[2] = q.z; e[3] = q.w;
+            return;
+        }
+        const int64_t i0 = static_cast<int64_t>(r) * VROW + 4 * lane_id() - head;
         typename Tr::Vec q;
         if (i0 + 3 >= 0 && i0 < static_cast<int64_t>(n)) q = __ldg(vp);
         else q = typename Tr::Vec{};
@@ -97,6 +116,25 @@ struct VPool {
     }
     __device__ __forceinline__ uint32_t item(uint32_t s) const { return __ldg(col + beg + s); }
     __device__ __forceinline__ E bias(uint32_t s) const { return __ldg(b + beg + s); }
+    // Rows [r0, r1) requested into L2 at once by one bulk (TMA) prefetch per 64 KB
+    // (cp.async.bulk.prefetch.L2): the whole stretch is in flight while the warp's
+    // vector loads walk through it, instead of VU rows at a time.
+    __device__ __forceinline__ void prefetch_l2(uint32_t r0, uint32_t r1) const {
+#if VSCAN_PREFETCH
+        if (lane_id() == 0 && r1 > r0) {
+            const char* p = reinterpret_cast<const char*>(b + (beg - head)) + static_cast<uint64_t>(r0) * VROW * sizeof(E);
+            uint64_t bytes = static_cast<uint64_t>(r1 - r0) * VROW * sizeof(E);
+            while (bytes > 0) {
+                const uint32_t sz = static_cast<uint32_t>(bytes < 65536 ? bytes : 65536);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(sz) : "memory");
+                p += sz;
+                bytes -= sz;
+            }
+        }
+#else
+        (void)r0; (void)r1;
+#endif
+    }
 };
 
 template <class E>
@@ -144,49 +182,57 @@ struct VRow {
 };
 
 // Build the chunk table (warp gw of a G-warp group; bar() synchronises the group).
-template <class E, int G, class Bar>
+// kCount: also count the positive entries (npos, lastpos) -- needed without replacement;
+// a walk needs only T (npos = T > 0, lastpos found on demand).
+template <class E, int G, bool kCount = true, class Bar>
 __device__ __forceinline__ VCtps<E> vscan_build(const VPool<E>& P, typename VTraits<E>::Acc* __restrict__ tab,
                                                 VGroupShared<E>* sh, int gw, Bar&& bar) {
     using Acc = typename VTraits<E>::Acc;
     const int lane = lane_id();
     VCtps<E> C;
-    C.m = (P.nrows + TAB - 1) / TAB;
-    if (C.m == 0) C.m = 1;
+    C.m = max(static_cast<uint32_t>(VMIN), (P.nrows + TAB - 1) / TAB);
+    C.m = (C.m + VU - 1) / VU * VU;   // whole batches per chunk
     C.nch = (P.nrows + C.m - 1) / C.m;
     uint32_t npos = 0, last1 = 0;   // last1 = last positive index + 1 (0: none)
-    // phase 1: chunk-local totals (sum of the chunk's row totals, in row order); warp gw
-    // takes the contiguous chunks [c0, c1), rows in batches of VU across chunk ends
+    // phase 1: chunk totals; warp gw takes the contiguous chunks [c0, c1), rows in batches
+    // of VU (m is a multiple of VU).  Each lane accumulates its entries (left to right within its
+    // 4, then row after row); one warp reduction per chunk -- a row costs a vector load and
+    // four adds, no shuffles
     const uint32_t c0 = (C.nch * gw) / G, c1 = (C.nch * (gw + 1)) / G;
     const uint32_t rb = c0 * C.m, re = min(P.nrows, c1 * C.m);
-    Acc acc = 0;
-    for (uint32_t r0 = rb; r0 < re; r0 += VU) {
-        E e[VU][4];
+    if (re - rb > VU) P.prefetch_l2(rb + VU, re);   // the first VU rows are loaded right away
+    uint32_t pl = 0, ll = 0;
+    for (uint32_t c = c0; c < c1; ++c) {
+        const uint32_t r1 = min(P.nrows, (c + 1) * C.m);
+        Acc lacc = 0;
+        for (uint32_t r0 = c * C.m; r0 < r1; r0 += VU) {
+            E e[VU][4];
 #pragma unroll
-        for (int u = 0; u < VU; ++u)
-            if (r0 + u < re) P.load(r0 + u, e[u]);
+            for (int u = 0; u < VU; ++u)
+                if (r0 + u < r1) P.load(r0 + u, e[u]);
 #pragma unroll
-        for (int u = 0; u < VU; ++u) {
-            const uint32_t r = r0 + u;
-            if (r < re) {
-                VRow<E> row;
-                row.compute(e[u]);
-                acc += row.tot;
-                uint32_t pl = 0, ll = 0;
+            for (int u = 0; u < VU; ++u) {
+                if (r0 + u < r1) {
+                    using Tr = VTraits<E>;
+                    lacc += ((Tr::val(e[u][0]) + Tr::val(e[u][1])) + Tr::val(e[u][2])) + Tr::val(e[u][3]);
+                    if constexpr (kCount) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if (e[u][j] > E(0)) {
-                        ++pl;
-                        ll = r * VROW + 4 * lane + j - P.head + 1;
+                        for (int j = 0; j < 4; ++j) {
+                            if (e[u][j] > E(0)) {
+                                ++pl;
+                                ll = (r0 + u) * VROW + 4 * lane + j - P.head + 1;
+                            }
+                        }
                     }
-                }
-                npos += __reduce_add_sync(FULL, pl);
-                last1 = max(last1, __reduce_max_sync(FULL, ll));
-                if ((r + 1) % C.m == 0 || r + 1 == P.nrows) {
-                    if (lane == 0) tab[r / C.m] = acc;
-                    acc = 0;
                 }
             }
         }
+        const Acc tot = VTraits<E>::sum(lacc);
+        if (lane == 0) tab[c] = tot;
+    }
+    if constexpr (kCount) {
+        npos = __reduce_add_sync(FULL, pl);
+        last1 = __reduce_max_sync(FULL, ll);
     }
     if constexpr (G > 1) {
         if (lane == 0) { sh->npos[gw] = npos; sh->last[gw] = last1; }
@@ -230,8 +276,13 @@ __device__ __forceinline__ VCtps<E> vscan_build(const VPool<E>& P, typename VTra
         __syncwarp();
     }
     C.T = tab[C.nch - 1];
-    C.npos = npos;
-    C.lastpos = last1 ? last1 - 1 : NONE;
+    if constexpr (kCount) {
+        C.npos = npos;
+        C.lastpos = last1 ? last1 - 1 : NONE;
+    } else {
+        C.npos = C.T > 0 ? 1u : 0u;   // "some positive entry" (biases are >= 0)
+        C.lastpos = NONE;              // vscan_find locates it if ever needed
+    }
     return C;
 }
 
@@ -322,7 +373,23 @@ __device__ __forceinline__ VRegion<E> vscan_find(const VPool<E>& P, const VCtps<
             if (r0 == rend) rend = P.nrows;
         }
     }
-    return vscan_region_at(P, C, tab, C.lastpos);
+    uint32_t last = C.lastpos;
+    if (last == NONE) {   // walks: the last positive entry, by a backwards row scan (rounding only)
+        for (int32_t r = static_cast<int32_t>(P.nrows) - 1; r >= 0 && last == NONE; --r) {
+            E e[4];
+            P.load(static_cast<uint32_t>(r), e);
+            int jl = -1;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (e[j] > E(0)) jl = j;
+            const unsigned hp = __ballot_sync(FULL, jl >= 0);
+            if (hp) {
+                const int f = 31 - __clz(hp);
+                last = static_cast<uint32_t>(r) * VROW + 4 * f + __shfl_sync(FULL, jl, f) - P.head;
+            }
+        }
+    }
+    return vscan_region_at(P, C, tab, last);
 }
 
 // With replacement (walks): one draw, x = draw(U, T).

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(VW_WARPS * 32, 4) k_walk_vscan(VWalkArgs a, co
                 if (d > 0) {
                     VPool<E> P;
                     P.init(eb, a.col, static_cast<uint64_t>(b0), d);
-                    const VCtps<E> C = vscan_build<E, G>(P, tab, sh, gw, bar);
+                    const VCtps<E> C = vscan_build<E, G, false>(P, tab, sh, gw, bar);
                     if (gw == 0) {
                         const uint64_t U = draw_u64(a.key, inst, static_cast<uint32_t>(t), 0u, word3(PURPOSE_EDGE, 0, 0));
                         nxt = vscan_select_wr(P, C, tab, U);
@@ -97,14 +97,14 @@ __global__ void __launch_bounds__(VW_WARPS * 32, 4) k_walk_vscan(VWalkArgs a, co
     }
 }
 
-// G: warps per walker.  Walkers alone fill the GPU from ~32 per SM; with fewer, groups of
-// 2 / 4 / 8 warps share each pool's scan (results identical, R7).
+// G: warps per walker -- the widest group with every walker resident at once (32 warps per
+// SM at 64 registers); few walkers with large pools then still fill the GPU (results
+// identical, R7).
 static int vwalk_group(const csaw_graph* g, int64_t n) {
-    const int64_t full = static_cast<int64_t>(g->num_sms) * 32;
-    if (n >= full) return 1;
-    if (n * 2 >= full) return 2;
-    if (n * 4 >= full) return 4;
-    return 8;
+    const int64_t resident = static_cast<int64_t>(g->num_sms) * 32;
+    int G = 1;
+    while (G < 8 && n * (2 * G) <= resident) G *= 2;
+    return G;
 }
 
 template <class E>

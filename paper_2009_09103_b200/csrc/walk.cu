@@ -1647,8 +1647,7 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         const uint4* rec = g->wrec;
         if (g->wix_group == 32 && g->whead) {
             // small blocks spread the few walkers evenly over the SMs (cfg2: 4,000 warps on 148 SMs)
-            const char* we = std::getenv("CSAW_WALK_WPB");
-            const int hw = we ? std::max(1, std::min(8, std::atoi(we))) : 2;   // 1: 2.46, 2: 2.43, 4: 2.44, 8: 2.48 ms (cfg2)
+            constexpr int hw = 2;   // warps per block (A/B cfg2: 1: 2.46, 2: 2.43, 4: 2.44, 8: 2.48 ms)
             const int64_t hwarps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 64);
             const int hg = static_cast<int>((hwarps + hw - 1) / hw);
             if (g->wix_leaf == 32) k_walk_head<32><<<hg, hw * 32, 0, st>>>(a, g->whead, g->c32, g->wcol, g->winn);
@@ -1706,11 +1705,12 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
     } else if (b.kind == CSAW_BIAS_MDRW) {
         const uint32_t m = static_cast<uint32_t>(b.pool_size);
         const uint32_t nblk = (m + 31) / 32;
-        if (nblk <= 64 && !std::getenv("CSAW_MDRW_SLOW")) {   // pools up to 2,048 slots (cfg5: 2,000)
-            // packed 8 B slot records: opt-in (A/B: same speed in memory, 14 % slower in the OOM
-            // zero-copy mode, where the separate vertex-id load lands on the step's chain)
-            const char* pk = std::getenv("CSAW_MDRW_PACKED");
-            const bool packed = g->max_deg < (int64_t(1) << 24) && g->E < (int64_t(1) << 40) && pk && pk[0] == '1';
+        if (nblk <= 64 && !(g->flags & CSAW_GRAPH_MDRW_GENERIC)) {   // pools up to 2,048 slots (cfg5: 2,000)
+            // packed 8 B slot records: opt-in, CSAW_GRAPH_MDRW_PACKED (A/B: same speed in memory,
+            // 14 % slower in the OOM zero-copy mode, where the separate vertex-id load lands on
+            // the step's chain)
+            const bool packed = g->max_deg < (int64_t(1) << 24) && g->E < (int64_t(1) << 40) &&
+                                (g->flags & CSAW_GRAPH_MDRW_PACKED);
             void *pool = nullptr, *pvid = nullptr;
             if (packed) {
                 CSAW_TRY(g->scratch.get(SL_TMP0, sizeof(uint64_t) * n * m, &pool));

@@ -109,16 +109,14 @@ def test_cfg2_cached_full():
 @pytest.mark.parametrize("heads", [True, False])
 def test_cached_sampling_heads_vs_btree(hubc, heads):
     """Cached degree / layer pools search the vertex heads (wix.cuh) when the walk index
-    exists; CSAW_SAMPLE_NO_HEADS=1 forces the u64 B-tree.  Both bit-exact."""
-    import os
+    exists; CSAW_GRAPH_SAMPLE_NO_HEADS forces the u64 B-tree.  Both bit-exact."""
     G, og = hubc
     assert G.info()["walk_index_heads"] == 1
-    seeds = np.array([0, 1, 0, 1, 5, 0, 1, 17, 299_999, 20_000], dtype=np.uint32)
     if not heads:
-        os.environ["CSAW_SAMPLE_NO_HEADS"] = "1"
-    try:
-        check_sample(G, og, "degree", seeds, fanout=[30, 3], rng_seed=41)
-        check_sample(G, og, "degree", seeds, fanout=[3, 2], rng_seed=42, a_max=2)
-        check_sample(G, og, "layer", seeds, fanout=[3, 4], rng_seed=43)
-    finally:
-        os.environ.pop("CSAW_SAMPLE_NO_HEADS", None)
+        G = cs.csaw_graph_create(torch.as_tensor(og.row_ptr).to(DEV),
+                                 torch.as_tensor(og.col.view(np.int32)).to(DEV), ctps_cache=True,
+                                 flags=cs.CSAW_GRAPH_SAMPLE_NO_HEADS)
+    seeds = np.array([0, 1, 0, 1, 5, 0, 1, 17, 299_999, 20_000], dtype=np.uint32)
+    check_sample(G, og, "degree", seeds, fanout=[30, 3], rng_seed=41)
+    check_sample(G, og, "degree", seeds, fanout=[3, 2], rng_seed=42, a_max=2)
+    check_sample(G, og, "layer", seeds, fanout=[3, 4], rng_seed=43)

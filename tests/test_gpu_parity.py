@@ -277,20 +277,17 @@ def test_repeatable(cfg1):
 @pytest.mark.parametrize("m,n,L", [(2048, 5, 200), (2049, 4, 150), (33, 40, 300), (64, 7, 100), (1, 5000, 37)])
 def test_mdrw_pool_sizes(medium, m, n, L):
     """k_mdrw_fast (pools <= 2,048 slots: register block totals, 16 B slot records) and
-    k_mdrw (larger pools, or CSAW_MDRW_SLOW=1) against the oracle, incl. ragged last
+    k_mdrw (larger pools, or CSAW_GRAPH_MDRW_GENERIC) against the oracle, incl. ragged last
     blocks and more instances than resident warps."""
-    import os
     G2, og2, g2 = medium
     s = mdrw_seeds(g2, n, m).numpy()
     e = check_mdrw(G2, og2, s, L, rng_seed=7, instances=range(0, n, max(1, n // 40)))
-    for env in ("CSAW_MDRW_SLOW", "CSAW_MDRW_PACKED"):   # large-pool kernel; packed 8 B slot records
-        os.environ[env] = "1"
-        try:
-            e2 = u32(cs.csaw_walk(G2, cs.make_bias("mdrw", pool_size=m), torch.as_tensor(s.view(np.int32)).to(DEV), L,
-                                  rng_seed=7))
-        finally:
-            del os.environ[env]
-        assert np.array_equal(e, e2), env
+    for fl in (cs.CSAW_GRAPH_MDRW_GENERIC, cs.CSAW_GRAPH_MDRW_PACKED):   # large-pool kernel; packed 8 B slot records
+        Gv = cs.csaw_graph_create(g2.row_ptr.to(DEV), g2.col_idx.to(DEV), device=0, flags=fl)
+        e2 = u32(cs.csaw_walk(Gv, cs.make_bias("mdrw", pool_size=m), torch.as_tensor(s.view(np.int32)).to(DEV), L,
+                              rng_seed=7))
+        Gv.close()
+        assert np.array_equal(e, e2), hex(fl)
 
 
 def test_mdrw_next_meta(medium):

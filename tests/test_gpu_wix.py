@@ -2,7 +2,6 @@
 walks searched through u32 fanout-128 nodes and FL-entry leaf blocks must be
 bit-identical to the oracle for every leaf fanout, including rows deep enough for
 three internal levels, and to the u64 index path (walk_index=False)."""
-import os
 
 import numpy as np
 import pytest
@@ -43,19 +42,12 @@ def make(rp, col, leaf, walk_index=True):
     leaf, group = leaf if isinstance(leaf, tuple) else (leaf, 32)
     nohead = group == "nohead"   # (64, 32) walks the vertex heads (k_walk_head); this one the records
     group = 32 if nohead else group
-    env = {"CSAW_WIX_LEAF": str(leaf), "CSAW_WIX_GROUP": str(group), "CSAW_NO_HEADS": "1" if nohead else ""}
-    old = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
-    try:
-        rpt = torch.as_tensor(np.asarray(rp, dtype=np.int64))
-        ct = torch.as_tensor(np.asarray(col).astype(np.uint32).view(np.int32))
-        G = cs.csaw_graph_create(rpt.to(DEV), ct.to(DEV), ctps_cache=True, walk_index=walk_index)
-    finally:
-        for k, v in old.items():
-            if v is None:
-                del os.environ[k]
-            else:
-                os.environ[k] = v
+    flags = ({128: 0, 64: cs.CSAW_GRAPH_WALK_LEAF_64, 32: cs.CSAW_GRAPH_WALK_LEAF_32}[leaf]
+             | {32: 0, 16: cs.CSAW_GRAPH_WALK_GROUP_16, 8: cs.CSAW_GRAPH_WALK_GROUP_8}[group]
+             | (cs.CSAW_GRAPH_WALK_NO_HEADS if nohead else 0))
+    rpt = torch.as_tensor(np.asarray(rp, dtype=np.int64))
+    ct = torch.as_tensor(np.asarray(col).astype(np.uint32).view(np.int32))
+    G = cs.csaw_graph_create(rpt.to(DEV), ct.to(DEV), ctps_cache=True, walk_index=walk_index, flags=flags)
     assert G.info()["walk_index_leaf"] == (leaf if walk_index else 0)
     return G, O.Graph(rpt.numpy(), ct.numpy().view(np.uint32))
 
