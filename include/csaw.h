@@ -204,7 +204,8 @@ typedef struct {
  *   OOM_NO_CHUNK_CACHE  out-of-memory mode without the automatic chunk-total cache
  *   OOM_ZC_NO_PREFIX    zero-copy OOM mode keeps no col_idx prefix resident (all host reads)
  *   MDRW_GENERIC        MDRW uses the general kernel (shared-memory block totals) for every pool
- *   MDRW_PACKED         MDRW pools <= 2,048 slots keep 8 B packed slot records (row << 24 | degree) */
+ *   MDRW_ALT_RECORDS    MDRW pools <= 2,048 slots: the other slot-record layout (16 B records in
+ *                       memory, 8 B packed row << 24 | degree in out-of-memory mode) */
 #define CSAW_GRAPH_WALK_NO_HEADS 0x800u
 #define CSAW_GRAPH_WALK_LEAF_64 0x1000u
 #define CSAW_GRAPH_WALK_LEAF_32 0x2000u
@@ -214,7 +215,7 @@ typedef struct {
 #define CSAW_GRAPH_OOM_NO_CHUNK_CACHE 0x20000u
 #define CSAW_GRAPH_OOM_ZC_NO_PREFIX 0x40000u
 #define CSAW_GRAPH_MDRW_GENERIC 0x80000u
-#define CSAW_GRAPH_MDRW_PACKED 0x100000u
+#define CSAW_GRAPH_MDRW_ALT_RECORDS 0x100000u
 
 typedef struct {
     int64_t num_vertices, num_edges;

@@ -99,7 +99,7 @@ CSAW_GRAPH_SAMPLE_NO_HEADS = 0x10000
 CSAW_GRAPH_OOM_NO_CHUNK_CACHE = 0x20000
 CSAW_GRAPH_OOM_ZC_NO_PREFIX = 0x40000
 CSAW_GRAPH_MDRW_GENERIC = 0x80000
-CSAW_GRAPH_MDRW_PACKED = 0x100000
+CSAW_GRAPH_MDRW_ALT_RECORDS = 0x100000
 
 
 def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, num_partitions: int = 0,

@@ -1471,7 +1471,44 @@ __global__ void k_mdrw(MdrwArgs a) {
 #ifndef MDRW_WARPS_N
 #define MDRW_WARPS_N 4
 #endif
-constexpr int MDRW_WARPS = MDRW_WARPS_N;   // warps per block; 28 warps / SM at 72 registers
+constexpr int MDRW_WARPS = MDRW_WARPS_N;
+#ifndef MDRW_SPEC
+#define MDRW_SPEC 0          // guess step t+1's block during step t's metadata load (A/B r02 cfg5: 3.19 vs 2.93 ms off)
+#endif
+#ifndef MDRW_KEEP_POOL
+#define MDRW_KEEP_POOL 0     // pool-state loads / stores with an L2 evict-last policy (A/B r02 cfg5: 2.97 vs 2.91 ms off, same DRAM bytes)
+#endif
+
+// L2 evict-last accesses for the per-instance pool state (kept resident against the random
+// per-step entry reads, which are evict-first)
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+    uint64_t pol = 0;
+#if MDRW_KEEP_POOL
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
+    return pol;
+}
+__device__ __forceinline__ uint64_t ld_keep(const uint64_t* p, uint64_t pol) {
+#if MDRW_KEEP_POOL
+    uint64_t v;
+    asm volatile("ld.global.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+    return v;
+#else
+    (void)pol;
+    return *p;
+#endif
+}
+__device__ __forceinline__ void st_keep(uint64_t* p, uint64_t v, uint64_t pol) {
+#if MDRW_KEEP_POOL
+    asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+#else
+    (void)pol;
+    *p = v;
+#endif
+}
+#ifndef MDRW_STREAM_HINT
+#define MDRW_STREAM_HINT 1   // evict-first loads for the per-step random entry + metadata
+#endif   // warps per block; 28 warps / SM at 72 registers
 __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v) {
     const int lane = lane_id();
 #pragma unroll
@@ -1518,41 +1555,56 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 28 / MDRW_WARPS) k_mdrw_fast(
         }
         // inclusive prefix of the block-pair totals over the lanes, kept up to date by deltas
         // (a step changes one block): the block search is one ballot, no scan
+        const uint64_t pol = l2_keep_policy();
+        uint64_t pol_ef = 0;
+#if MDRW_STREAM_HINT == 2
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_ef));
+#endif
+        (void)pol_ef;
         uint64_t incl = warp_incl_scan(bA + bB);
         uint64_t T = __shfl_sync(FULL, incl, 31);
         __syncwarp();
         uint32_t* orow = a.out + w * static_cast<uint64_t>(a.L) * 2;
         uint32_t ebuf = NONE;
         uint64_t uxb = 0, ueb = 0;
-        for (int32_t t = 0; t < a.L; ++t) {
-            if ((t & 31) == 0) {
-                uxb = draw_u64(a.key, inst, static_cast<uint32_t>(t + lane), 0u, word3(PURPOSE_VERTEX, 0, 0));
-                ueb = draw_u64(a.key, inst, static_cast<uint32_t>(t + lane), 0u, word3(PURPOSE_EDGE, 0, 0));
+        // block of x: the pair owner f (ballot over the inclusive pair prefix), then which half
+        auto locate = [&](uint64_t x, uint32_t& bsel, uint64_t& blo) {
+            const int f = __ffs(__ballot_sync(FULL, incl > x)) - 1;   // exists: x < T
+            const uint64_t ex = __shfl_sync(FULL, incl - bA - bB, f);
+            const uint64_t fa = __shfl_sync(FULL, bA, f);
+            const bool second = x >= ex + fa;
+            bsel = 2 * f + (second ? 1 : 0);
+            blo = second ? ex + fa : ex;
+        };
+        // the block's slot records (lane = slot within the block)
+        auto load_block = [&](uint32_t bsel, uint64_t& rec, uint4& e) {
+            const uint32_t s0 = bsel * 32 + lane;
+            if constexpr (kPacked) rec = s0 < m ? ld_keep(pr + s0, pol) : 0;
+            else e = s0 < m ? ps[s0] : make_uint4(NONE, 0, 0, 0);
+        };
+        // step t's block, loaded ahead: at the end of step t-1 the block of step t is
+        // requested with the totals before t-1's update (a guess, usually right), so that
+        // load overlaps t-1's dependent metadata load; a wrong guess is reloaded
+        uint32_t bsel = 0;
+        uint64_t blo = 0, rec = 0;
+        uint4 e = make_uint4(NONE, 0, 0, 0);
+        if (a.L > 0) {
+            uxb = draw_u64(a.key, inst, static_cast<uint32_t>(lane), 0u, word3(PURPOSE_VERTEX, 0, 0));
+            ueb = draw_u64(a.key, inst, static_cast<uint32_t>(lane), 0u, word3(PURPOSE_EDGE, 0, 0));
+            if (T > 0) {
+                locate(below(__shfl_sync(FULL, uxb, 0), T), bsel, blo);
+                load_block(bsel, rec, e);
             }
-            const uint64_t Ux = __shfl_sync(FULL, uxb, t & 31);
+        }
+        for (int32_t t = 0; t < a.L; ++t) {
             const uint64_t Ue = __shfl_sync(FULL, ueb, t & 31);
             uint32_t v = NONE, u = NONE;
             if (T > 0) {
-                const uint64_t x = below(Ux, T);
-                // block containing x
-                const int f = __ffs(__ballot_sync(FULL, incl > x)) - 1;   // exists: x < T
-                const uint64_t ex = __shfl_sync(FULL, incl - bA - bB, f);
-                const uint64_t fa = __shfl_sync(FULL, bA, f);
-                const bool second = x >= ex + fa;
-                const uint32_t bsel = 2 * f + (second ? 1 : 0);
-                const uint64_t blo = second ? ex + fa : ex;
-                // the block's slots
+                const uint64_t x = below(__shfl_sync(FULL, uxb, t & 31), T);
                 const uint32_t s0 = bsel * 32 + lane;
                 uint32_t bias;
-                uint64_t rec = 0;
-                uint4 e = make_uint4(NONE, 0, 0, 0);
-                if constexpr (kPacked) {
-                    rec = s0 < m ? pr[s0] : 0;
-                    bias = static_cast<uint32_t>(rec & 0xFFFFFFu);
-                } else {
-                    e = s0 < m ? ps[s0] : make_uint4(NONE, 0, 0, 0);
-                    bias = e.y;
-                }
+                if constexpr (kPacked) bias = static_cast<uint32_t>(rec & 0xFFFFFFu);
+                else bias = e.y;
                 uint64_t incl2;
                 if constexpr (kNarrow) incl2 = static_cast<uint64_t>(warp_incl_scan_u32(bias)) + blo;
                 else incl2 = warp_incl_scan(static_cast<uint64_t>(bias)) + blo;
@@ -1570,23 +1622,50 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 28 / MDRW_WARPS) k_mdrw_fast(
                 int64_t ru;
                 uint32_t du;
                 uint64_t mt = 0;
+                // the next step's draws (refilled every 32 steps) and its guessed block
+                if (((t + 1) & 31) == 0 && t + 1 < a.L) {
+                    uxb = draw_u64(a.key, inst, static_cast<uint32_t>(t + 1 + lane), 0u, word3(PURPOSE_VERTEX, 0, 0));
+                    ueb = draw_u64(a.key, inst, static_cast<uint32_t>(t + 1 + lane), 0u, word3(PURPOSE_EDGE, 0, 0));
+                }
                 if (a.nmp) {   // the new vertex's row and degree come with the entry (no dependent lookup)
+#if MDRW_STREAM_HINT == 2
+                    asm volatile("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(mt) : "l"(a.nmp + ei), "l"(pol_ef));
+                    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(u) : "l"(a.col + ei), "l"(pol_ef));
+#elif MDRW_STREAM_HINT
+                    mt = __ldcs(a.nmp + ei);   // read once: evict first, keep the pool state in L2
+                    u = __ldcs(a.col + ei);
+#else
                     mt = __ldg(a.nmp + ei);
                     u = __ldg(a.col + ei);
+#endif
+                } else {
+                    u = ei < a.colc_n ? __ldg(a.colc + ei) : __ldg(a.col + ei);   // OOM zero-copy: host beyond colc_n
+                }
+                const uint64_t Uxn = __shfl_sync(FULL, uxb, (t + 1) & 31);
+                uint32_t gsel = 0;
+                uint64_t glo = 0, grec = 0;
+                uint4 ge = make_uint4(NONE, 0, 0, 0);
+                if (MDRW_SPEC && t + 1 < a.L) {   // guess with the totals before this step's update
+                    locate(below(Uxn, T), gsel, glo);
+                    load_block(gsel, grec, ge);
+                } else {
+                    gsel = NONE;
+                }
+                if (a.nmp) {
                     ru = static_cast<int64_t>(mt >> 24);
                     du = static_cast<uint32_t>(mt & 0xFFFFFFu);
                 } else {
-                    u = ei < a.colc_n ? __ldg(a.colc + ei) : __ldg(a.col + ei);   // OOM zero-copy: host beyond colc_n
                     ru = __ldg(a.rp + u);
                     du = static_cast<uint32_t>(__ldg(a.rp + u + 1) - ru);
                     mt = static_cast<uint64_t>(ru) << 24 | du;
                 }
+                const uint4 ne = make_uint4(u, du, static_cast<uint32_t>(ru), static_cast<uint32_t>(static_cast<uint64_t>(ru) >> 32));
                 if (lane == fl) {
                     if constexpr (kPacked) {
-                        pr[s0] = mt;
+                        st_keep(pr + s0, mt, pol);
                         pvv[s0] = u;
                     } else {
-                        ps[s0] = make_uint4(u, du, static_cast<uint32_t>(ru), static_cast<uint32_t>(static_cast<uint64_t>(ru) >> 32));
+                        ps[s0] = ne;
                     }
                 }
                 const uint64_t delta = static_cast<uint64_t>(du) - d;   // mod 2^64
@@ -1598,6 +1677,17 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 28 / MDRW_WARPS) k_mdrw_fast(
                 if (lane >= owner) incl += delta;
                 T += delta;
                 __syncwarp();
+                if (t + 1 < a.L && T > 0) {   // the real block of step t + 1
+                    const uint32_t osel = bsel;
+                    locate(below(Uxn, T), bsel, blo);
+                    if (bsel == gsel) {
+                        rec = grec;
+                        e = ge;
+                        if (bsel == osel && lane == fl) { rec = mt; e = ne; }   // the guess predates this write
+                    } else {
+                        load_block(bsel, rec, e);
+                    }
+                }
             }
             // buffer 16 steps (2 words each) per 32 lanes, flush coalesced
             const int k = t & 15;
@@ -1706,11 +1796,12 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         const uint32_t m = static_cast<uint32_t>(b.pool_size);
         const uint32_t nblk = (m + 31) / 32;
         if (nblk <= 64 && !(g->flags & CSAW_GRAPH_MDRW_GENERIC)) {   // pools up to 2,048 slots (cfg5: 2,000)
-            // packed 8 B slot records: opt-in, CSAW_GRAPH_MDRW_PACKED (A/B: same speed in memory,
-            // 14 % slower in the OOM zero-copy mode, where the separate vertex-id load lands on
-            // the step's chain)
-            const bool packed = g->max_deg < (int64_t(1) << 24) && g->E < (int64_t(1) << 40) &&
-                                (g->flags & CSAW_GRAPH_MDRW_PACKED);
+            // slot records: 8 B packed in memory (the n x m pool state stays L2-resident: cfg5
+            // 96 MB instead of 128 MB of 16 B records), 16 B in the OOM zero-copy mode (there the
+            // separate vertex-id load lands on the step's chain: 14 % slower packed);
+            // CSAW_GRAPH_MDRW_ALT_RECORDS picks the other layout (A/B)
+            const bool alt = (g->flags & CSAW_GRAPH_MDRW_ALT_RECORDS) != 0;
+            const bool packed = g->max_deg < (int64_t(1) << 24) && g->E < (int64_t(1) << 40) && (!g->oom != alt);
             void *pool = nullptr, *pvid = nullptr;
             if (packed) {
                 CSAW_TRY(g->scratch.get(SL_TMP0, sizeof(uint64_t) * n * m, &pool));
