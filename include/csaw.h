@@ -304,8 +304,15 @@ CSAW_API csaw_status csaw_sample(const csaw_graph *g, const csaw_bias *bias, con
  *     neighbour stops and the rest of its row is CSAW_NONE (R20).
  *   MDRW: seeds uint32[n_walkers][pool_size] (the instance's initial pool, slot
  *     order); path uint32[n_walkers][length][2] = the (v, u) edge sampled at each step.
+ *   WEIGHT: as DEGREE with EdgeBias = w(e) (graphs created with weights); MH / RESTART /
+ *     JUMP: the path is the sequence of positions -- a rejected Metropolis-Hastings proposal
+ *     repeats the current vertex, a restart / jump is the next entry like an edge step (the
+ *     path is not an edge list for these three).
  * Returns OUT_OF_RANGE if a seed >= V (checked on the device before any walk kernel;
  * the call then synchronises `stream` once, nothing is written to path).
+ * csaw_run_stats.sampled_edges counts length per walker (R30) even for a walk that ended
+ * early (R20, padded with CSAW_NONE); for degree / uniform / node2vec / weight walks .pools
+ * counts the transitions actually taken.
  */
 CSAW_API csaw_status csaw_walk(const csaw_graph *g, const csaw_bias *bias, int32_t length,
                                const uint32_t *seeds, int64_t n_walkers, uint64_t instance_base,

@@ -386,8 +386,12 @@ static csaw_status build_wix_t(csaw_graph* g, int blocks) {
     const int64_t V = g->V, E = g->E;
     uint64_t* woff = nullptr;
     uint64_t* part = nullptr;
-    CSAW_CUDA(cudaMalloc(&woff, sizeof(uint64_t) * (V + 1)));
-    CSAW_CUDA(cudaMalloc(&part, sizeof(uint64_t) * (SCAN_MAX_GRID + 8)));
+    if (cudaMalloc(&woff, sizeof(uint64_t) * (V + 1)) != cudaSuccess ||
+        cudaMalloc(&part, sizeof(uint64_t) * (SCAN_MAX_GRID + 8)) != cudaSuccess) {   // accelerator: skip it
+        cudaGetLastError();
+        if (woff) cudaFree(woff);
+        return CSAW_OK;
+    }
     csaw_status s = device_scan(WixSize<FL>{g->row_ptr}, static_cast<uint64_t>(V), ScanToArray{woff}, part, nullptr);
     uint64_t total = 0;
     if (s == CSAW_OK && cudaMemcpy(&total, woff + V, sizeof(uint64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
@@ -526,7 +530,7 @@ static csaw_status build_tri(csaw_graph* g, int blocks) {
         if (src) cudaFree(src);
         if (asym) cudaFree(asym);
         if (g->tri) { cudaFree(g->tri); g->tri = nullptr; }
-        return fail(CSAW_ERR_NO_MEMORY, "cudaMalloc(node2vec triangle counts)");
+        return CSAW_OK;   // an accelerator: node2vec keeps the merge kernel (csaw_graph_info_t.node2vec_tri = 0)
     }
     cudaMemset(asym, 0, sizeof(unsigned int));
     k_src_of<<<blocks, 256>>>(g->row_ptr, g->V, src);
@@ -573,6 +577,27 @@ __global__ void k_build_ccache(const int64_t* __restrict__ rp, const uint32_t* _
         if (lane == 0) out[nch] = npos;
     }
 }
+
+// Device time of one accelerator build at graph creation (events destroyed on every path).
+struct BuildTimer {
+    cudaEvent_t c0 = nullptr, c1 = nullptr;
+    BuildTimer() {
+        if (cudaEventCreate(&c0) != cudaSuccess || cudaEventCreate(&c1) != cudaSuccess) cudaGetLastError();
+        if (c0) cudaEventRecord(c0);
+    }
+    double ms() {
+        float t = 0.f;
+        if (c1 && cudaEventRecord(c1) == cudaSuccess && cudaEventSynchronize(c1) == cudaSuccess &&
+            cudaEventElapsedTime(&t, c0, c1) == cudaSuccess)
+            return t;
+        cudaGetLastError();
+        return 0.0;
+    }
+    ~BuildTimer() {
+        if (c0) cudaEventDestroy(c0);
+        if (c1) cudaEventDestroy(c1);
+    }
+};
 
 static csaw_status build_ccache(csaw_graph* g, const uint32_t* col, int blocks) {
     const uint64_t n = static_cast<uint64_t>(g->E) / 64 + 512;
@@ -767,13 +792,15 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         const csaw_status cs_ = build_ccache(g, g->oom ? g->oomst.h_col : g->col, blocks);
         if (cs_ != CSAW_OK) return cleanup(cs_);
     }
+    // Accelerators.  The CTPS cache is the one structure a caller asks for by name and is
+    // mandatory (NO_MEMORY if it does not fit); everything else -- walk index and heads,
+    // next-vertex metadata, node2vec index / triangle counts, materialised edge bias, chunk
+    // totals -- is best-effort: without memory for it the graph is created without it
+    // (csaw_graph_info_t says what was built) and the selections use the general kernels.
     if ((o.flags & CSAW_GRAPH_CTPS_CACHE) && !g->oom) {
+        BuildTimer tm;
         CREATE_CUDA(cudaMalloc(&g->cps, sizeof(uint64_t) * std::max<int64_t>(E, 1)), "cudaMalloc(cps)");
         CREATE_CUDA(cudaMalloc(&g->npos, sizeof(uint32_t) * std::max<int64_t>(V, 1)), "cudaMalloc(npos)");
-        cudaEvent_t c0, c1;
-        CREATE_CUDA(cudaEventCreate(&c0), "event");
-        CREATE_CUDA(cudaEventCreate(&c1), "event");
-        cudaEventRecord(c0);
         if (V > 0) k_build_cps<<<blocks, 256>>>(g->row_ptr, g->col, g->deg, V, g->cps, g->npos);
         // B-tree index over the cached prefix: dense segments (prefix sum of the sizes)
         CREATE_CUDA(cudaMalloc(&g->bt_off, sizeof(uint64_t) * (V + 1)), "cudaMalloc(bt_off)");
@@ -781,8 +808,9 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         CREATE_CUDA(cudaMalloc(&part, sizeof(uint64_t) * (SCAN_MAX_GRID + 8)), "cudaMalloc");
         device_scan(BtSize{g->row_ptr}, static_cast<uint64_t>(V), ScanToArray{g->bt_off}, part, nullptr);
         uint64_t btn = 0;
-        CREATE_CUDA(cudaMemcpy(&btn, g->bt_off + V, sizeof(uint64_t), cudaMemcpyDeviceToHost), "bt size");
+        const cudaError_t be = cudaMemcpy(&btn, g->bt_off + V, sizeof(uint64_t), cudaMemcpyDeviceToHost);
         cudaFree(part);
+        CREATE_CUDA(be, "bt size");
         CREATE_CUDA(cudaMalloc(&g->bt, sizeof(uint64_t) * std::max<uint64_t>(btn, 1)), "cudaMalloc(bt)");
         if (V > 0) k_build_bt<<<blocks, 256>>>(g->row_ptr, g->cps, g->bt_off, V, g->bt);
         // (next-vertex metadata for k_walk_cached: CSAW_GRAPH_NEXT_META, below; measured 2.5 %
@@ -791,68 +819,37 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
             const csaw_status ws = build_wix(g, blocks);
             if (ws != CSAW_OK) return cleanup(ws);
         }
-
-        cudaEventRecord(c1);
-        CREATE_CUDA(cudaEventSynchronize(c1), "build cps");
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, c0, c1);
-        g->cache_build_ms = ms;
-        cudaEventDestroy(c0);
-        cudaEventDestroy(c1);
+        g->cache_build_ms = tm.ms();
     }
     if ((o.flags & CSAW_GRAPH_NEXT_META) && !g->oom && !g->nmp && g->max_deg < (1 << 24) && E < (int64_t(1) << 40) &&
         E > 0) {   // nmp[e] = row_ptr[col[e]] << 24 | deg(col[e]) (MDRW: k_mdrw_fast)
-        CREATE_CUDA(cudaMalloc(&g->nmp, sizeof(uint64_t) * E), "cudaMalloc(nmp)");
-        k_build_nmp<<<blocks, 256>>>(g->row_ptr, g->col, E, g->nmp);
+        if (cudaMalloc(&g->nmp, sizeof(uint64_t) * E) == cudaSuccess) k_build_nmp<<<blocks, 256>>>(g->row_ptr, g->col, E, g->nmp);
+        else { cudaGetLastError(); g->nmp = nullptr; }
     }
     if ((o.flags & CSAW_GRAPH_N2V_INDEX) && !g->oom) {   // node2vec per-edge intersection index (n2v_index.cu)
-        cudaEvent_t c0, c1;
-        CREATE_CUDA(cudaEventCreate(&c0), "event");
-        CREATE_CUDA(cudaEventCreate(&c1), "event");
-        cudaEventRecord(c0);
+        BuildTimer tm;
         const csaw_status xs = build_n2v_index(g, blocks);
-        cudaEventRecord(c1);
-        cudaEventSynchronize(c1);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, c0, c1);
-        cudaEventDestroy(c0);
-        cudaEventDestroy(c1);
+        const double ms = tm.ms();
         if (xs != CSAW_OK) return cleanup(xs);
         g->cache_build_ms += ms;
     }
     if ((o.flags & CSAW_GRAPH_N2V_TRI) && !g->oom && !g->n2x_rec) {   // node2vec edge triangle counts (k_node2vec_tri; not needed with the index)
-        cudaEvent_t c0, c1;
-        CREATE_CUDA(cudaEventCreate(&c0), "event");
-        CREATE_CUDA(cudaEventCreate(&c1), "event");
-        cudaEventRecord(c0);
+        BuildTimer tm;
         const csaw_status ts = build_tri(g, blocks);
+        const double ms = tm.ms();
         if (ts != CSAW_OK) return cleanup(ts);
-        cudaEventRecord(c1);
-        CREATE_CUDA(cudaEventSynchronize(c1), "build tri");
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, c0, c1);
         g->cache_build_ms += ms;
-        cudaEventDestroy(c0);
-        cudaEventDestroy(c1);
     }
     if ((o.flags & CSAW_GRAPH_EDGE_BIAS) && !g->oom) {   // ebias[e] = deg(col[e]) (vscan.cuh degree pools)
-        cudaEvent_t c0, c1;
-        CREATE_CUDA(cudaEventCreate(&c0), "event");
-        CREATE_CUDA(cudaEventCreate(&c1), "event");
-        cudaEventRecord(c0);
-        if (cudaMalloc(&g->ebias, sizeof(uint32_t) * (E + VSCAN_PAD)) != cudaSuccess) {   // an accelerator: skip it
+        BuildTimer tm;
+        if (cudaMalloc(&g->ebias, sizeof(uint32_t) * (E + VSCAN_PAD)) != cudaSuccess) {
             cudaGetLastError();
             g->ebias = nullptr;
         } else {
             cudaMemsetAsync(g->ebias, 0, sizeof(uint32_t) * (E + VSCAN_PAD));
             if (E > 0) k_build_ebias<<<blocks, 256>>>(g->col, g->deg, E, g->ebias);
         }
-        cudaEventRecord(c1);
-        cudaEventSynchronize(c1);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, c0, c1);
-        cudaEventDestroy(c0);
-        cudaEventDestroy(c1);
+        const double ms = tm.ms();
         if (g->ebias) g->cache_build_ms += ms;
     }
     CREATE_CUDA(cudaEventCreate(&g->ev0), "event");

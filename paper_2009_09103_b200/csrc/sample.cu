@@ -786,6 +786,9 @@ __device__ void fused_epilogue(const FusedArgs& a) {
         for (int u = 0; u < 8; ++u) s += c[u];
     }
     uint64_t run = block_excl_scan<NT>(s, wsum, &total);
+    // pinned host offsets only for a call that succeeds here: a bad seed (bit 1) or a fallback
+    // to the batched driver (bit 0) leaves the caller's host buffer untouched
+    uint64_t* const offs_host = *reinterpret_cast<volatile unsigned*>(a.overflow) ? nullptr : a.offs_host;
     for (uint64_t i0 = b0; i0 < b1; i0 += 8) {
         uint64_t c[8];
 #pragma unroll
@@ -794,14 +797,14 @@ __device__ void fused_epilogue(const FusedArgs& a) {
         for (int u = 0; u < 8; ++u) {
             if (i0 + u < b1) {
                 a.offs[i0 + u] = run;
-                if (a.offs_host) a.offs_host[i0 + u] = run;
+                if (offs_host) offs_host[i0 + u] = run;
             }
             run += c[u];
         }
     }
     if (threadIdx.x == 0) {
         a.offs[n] = total;
-        if (a.offs_host) a.offs_host[n] = total;
+        if (offs_host) offs_host[n] = total;
         a.report[0] = *reinterpret_cast<volatile unsigned*>(a.overflow);
         a.report[1] = total;
         for (int k = 0; k < 4; ++k) a.report[2 + k] = reinterpret_cast<volatile unsigned long long*>(a.counters)[k];

@@ -1715,6 +1715,11 @@ bool walk_path_direct_ok(const csaw_graph* g, const csaw_bias& b) {
 
 csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds, int64_t n,
                      uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st) {
+    // argument checks before any statistics / timing state is recorded
+    if (b.kind == CSAW_BIAS_NODE2VEC && !g->rows_sorted)
+        return fail(CSAW_ERR_BAD_GRAPH, "node2vec needs sorted CSR rows (N(prev) membership)");
+    if (b.kind == CSAW_BIAS_WEIGHT && !g->w)
+        return fail(CSAW_ERR_INVALID_ARG, "CSAW_BIAS_WEIGHT needs a graph created with edge weights");
     void* cnt;
     CSAW_TRY(g->scratch.get(SL_COUNTS, 64, &cnt));
     CSAW_CUDA(cudaMemsetAsync(cnt, 0, 64, st));
@@ -1759,8 +1764,6 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         k_walk_cached<<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a, g->cps, g->bt, g->bt_off, g->nmp);
     } else if ((b.kind == CSAW_BIAS_DEGREE && g->ebias) || b.kind == CSAW_BIAS_WEIGHT) {
         // per-edge bias streams (vscan.cuh): the materialised degree bias or the edge weights
-        if (b.kind == CSAW_BIAS_WEIGHT && !g->w)
-            return fail(CSAW_ERR_INVALID_ARG, "CSAW_BIAS_WEIGHT needs a graph created with edge weights");
         CSAW_TRY(launch_walk_vscan(g, b.kind == CSAW_BIAS_WEIGHT, d_seeds, static_cast<uint64_t>(n), length,
                                    static_cast<uint32_t>(base), key, d_path, static_cast<unsigned long long*>(cnt), 0,
                                    st));
@@ -1775,7 +1778,6 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         if (b.kind == CSAW_BIAS_RESTART) k_walk_variant<CSAW_BIAS_RESTART><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a, theta, g->V);
         else k_walk_variant<CSAW_BIAS_JUMP><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(a, theta, g->V);
     } else if (b.kind == CSAW_BIAS_NODE2VEC) {
-        if (!g->rows_sorted) return fail(CSAW_ERR_BAD_GRAPH, "node2vec needs sorted CSR rows (N(prev) membership)");
         N2vArgs na;
         na.wa = a;
         const uint32_t m = n2v_integer_scale(b.p, b.q);
