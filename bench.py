@@ -77,6 +77,9 @@ def parse_args(argv=None):
     ap.add_argument("--no-zerocopy", action="store_true", help="OOM configs: skip the zero-copy OOM variant")
     ap.add_argument("--oom-budget-gb", type=float, default=0.0,
                     help="OOM configs: override the device budget (1e9 B) -- experiments only, the config names 8 GB")
+    ap.add_argument("--oom-store", default="host", choices=["host", "peer"],
+                    help="OOM configs: partition store in pinned host memory (the paper) or in a peer GPU's HBM "
+                         "(NEXT-4(i), CSAW_GRAPH_OOM_PEER_STORE; with one GPU a same-device stand-in)")
     ap.add_argument("--oom-variant", default="partition", choices=["partition", "zerocopy"],
                     help="OOM configs: time the paper's partition scheduling (default) or the zero-copy mode")
     return ap.parse_args(argv)
@@ -422,10 +425,12 @@ def config_block(cfg, world, stats_g, scaling, n_total, oom_mode=None, colc=None
     return c
 
 
-def measure_h2d_peak(dev, nbytes=1 << 30, reps=5) -> float:
+def measure_h2d_peak(dev, nbytes=1 << 30, reps=5, store=None) -> float:
     """Pinned host -> device cudaMemcpyAsync bandwidth (GB/s, best of reps): the
-    roofline of the OOM configs."""
-    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    roofline of the OOM configs.  store = a GPU index: the
+    store -> device copy of the peer partition store instead (NEXT-4(i))."""
+    h = (torch.empty(nbytes, dtype=torch.uint8).pin_memory() if store is None
+         else torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", store)))
     d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     best = 0.0
     for _ in range(reps):
@@ -479,9 +484,13 @@ def main():
         g = g.to("cpu")
         torch.cuda.empty_cache()
         zc_main = args.oom_variant == "zerocopy"
+        store = None
+        if args.oom_store == "peer":
+            ndev = torch.cuda.device_count()
+            store = (local + 1) % ndev if ndev > 1 else local
         G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, budget_bytes=cfg.oom_budget_bytes,
                                  num_partitions=cfg.oom_partitions, max_resident=1 if zc_main else cfg.oom_resident,
-                                 num_streams=cfg.oom_resident, zerocopy=zc_main)
+                                 num_streams=cfg.oom_resident, zerocopy=zc_main, store_device=store)
     else:
         use_cache = (not args.no_cache) and cfg.bias in ("degree", "layer")
         use_tri = (not args.no_cache) and cfg.workload == "node2vec"
@@ -616,7 +625,11 @@ def main():
         gather_ms = 1000 * (time.perf_counter() - t0)
 
     # ---------------- OOM configs: measured host-link peak + the zero-copy variant (NEXT-4)
-    h2d_peak = measure_h2d_peak(dev) if oom else None
+    store_dev = None
+    if oom and args.oom_store == "peer":
+        ndev = torch.cuda.device_count()
+        store_dev = (local + 1) % ndev if ndev > 1 else local
+    h2d_peak = measure_h2d_peak(dev, store=store_dev) if oom else None
     zc = None
     if oom and not args.no_zerocopy and args.oom_variant != "zerocopy":
         zc = run_zerocopy(cs, g, cfg, bias, seeds, base, rng_seeds[0], kind, n, dev, local, stream, flush,
@@ -647,13 +660,18 @@ def main():
     ncu = load_ncu(variant, kname)
     if oom:
         ach = (h2d_bytes / (total_ms / 1000.0) / 1e9) if h2d_bytes else None
-        roof = {"bound": "host-link", "achieved": ach, "peak": h2d_peak, "unit": "GB/s",
+        roof = {"bound": "host-link" if store_dev is None else ("nvlink" if store_dev != local else "d2d-standin"),
+                "achieved": ach, "peak": h2d_peak, "unit": "GB/s",
                 "frac": (ach / h2d_peak) if ach and h2d_peak else None, "traffic": None,
                 "kernel": kname, "bytes_model": BYTES_MODEL["oom_host"],
                 "h2d_bytes_per_step": h2d_bytes / max(args.steps, 1),
                 "transfer_ms_per_step": transfer_ms / max(args.steps, 1),
-                "peak_source": "pinned cudaMemcpyAsync H2D, 1 GiB, best of 5, measured in this run",
-                "host_link_peak_gbs": h2d_peak}
+                "peak_source": ("pinned cudaMemcpyAsync H2D, 1 GiB, best of 5, measured in this run"
+                                if store_dev is None else
+                                f"cudaMemcpyAsync cuda:{store_dev} -> cuda:{local}, 1 GiB, best of 5, measured in this run"
+                                + (" (same-device stand-in: one GPU)" if store_dev == local else " (NVLink)")),
+                "host_link_peak_gbs": h2d_peak if store_dev is None else None,
+                "store": "host" if store_dev is None else f"cuda:{store_dev}" + (" (stand-in)" if store_dev == local else "")}
     else:
         bytes_per_launch = alg_bytes / max(hot_launches, 1)
         achieved = bytes_per_launch / (hot_avg_ms / 1000.0) / 1e9 if hot_avg_ms > 0 else None

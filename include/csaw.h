@@ -117,6 +117,9 @@ typedef struct {
     int32_t max_resident;           /* OOM: partitions resident at once; 0 = default 2 */
     int32_t num_streams;            /* OOM: streams (one kernel per active partition); 0 = default 2 */
     uint32_t flags;                 /* CSAW_GRAPH_* bits */
+    int32_t store_device;           /* OOM with CSAW_GRAPH_OOM_PEER_STORE: the GPU whose HBM holds the partition
+                                       store (peer access over NVLink is enabled); == device: a same-device
+                                       stand-in (tests on one GPU).  Ignored otherwise. */
 } csaw_graph_opts;
 
 /* csaw_graph_opts.flags: build the static-bias CTPS cache at creation (in-memory
@@ -206,6 +209,14 @@ typedef struct {
  *   MDRW_GENERIC        MDRW uses the general kernel (shared-memory block totals) for every pool
  *   MDRW_ALT_RECORDS    MDRW pools <= 2,048 slots: the other slot-record layout (16 B records in
  *                       memory, 8 B packed row << 24 | degree in out-of-memory mode) */
+/* csaw_graph_opts.flags, out-of-memory mode: the partition store
+ * -- the full col_idx the §5 scheduler copies partitions from -- lives in the
+ * HBM of opts.store_device instead of pinned host memory.  Partition loads become
+ * device-to-device copies over NVLink (cudaMemcpyAsync, ~900 GB/s per direction on
+ * NVSwitch vs a PCIe / C2C host link), and with CSAW_GRAPH_OOM_ZEROCOPY the kernels read
+ * the peer's memory in place.  The planner, budget and results are unchanged (only the
+ * local arena counts against device_budget_bytes).  In-memory graphs ignore it. */
+#define CSAW_GRAPH_OOM_PEER_STORE 0x200000u
 #define CSAW_GRAPH_WALK_NO_HEADS 0x800u
 #define CSAW_GRAPH_WALK_LEAF_64 0x1000u
 #define CSAW_GRAPH_WALK_LEAF_32 0x2000u
@@ -243,7 +254,7 @@ typedef struct {
     uint64_t pools;                 /* selection pools processed (frontier entries / walk steps) */
     uint64_t neighbours_scanned;    /* candidates whose bias was evaluated (pass 1 of the CTPS build) */
     uint64_t partition_loads;       /* OOM: partition transfers (Fig. 15) */
-    uint64_t h2d_bytes;             /* OOM: bytes copied host -> device for partitions */
+    uint64_t h2d_bytes;             /* OOM: bytes copied from the partition store (host, or the peer GPU) */
     uint64_t cache_probes;          /* CTPS-cache entries read by the searches (CSAW_GRAPH_CTPS_CACHE) */
     uint64_t draws;                 /* random draws consumed by without-replacement selections (Fig. 11) */
     uint64_t kernel_launches;       /* kernels this library launched for the call */

@@ -65,7 +65,8 @@ class csaw_csr(C.Structure):
 
 class csaw_graph_opts(C.Structure):
     _fields_ = [("device", C.c_int32), ("device_budget_bytes", C.c_int64), ("num_partitions", C.c_int32),
-                ("max_resident", C.c_int32), ("num_streams", C.c_int32), ("flags", C.c_uint32)]
+                ("max_resident", C.c_int32), ("num_streams", C.c_int32), ("flags", C.c_uint32),
+                ("store_device", C.c_int32)]
 
 
 class csaw_graph_info_t(C.Structure):

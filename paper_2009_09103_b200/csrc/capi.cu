@@ -740,12 +740,35 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
                                     std::to_string(st.R) + " partition slots (" + std::to_string(arena) +
                                     " B) exceed the device budget " + std::to_string(st.budget) + " B"));
         CREATE_CUDA(cudaMalloc(&st.d_slots, arena), "cudaMalloc(arena)");
-        CREATE_CUDA(cudaMallocHost(&st.h_col, sizeof(uint32_t) * std::max<int64_t>(E, 1)), "cudaMallocHost(col)");
-        if (E > 0) CREATE_CUDA(cudaMemcpy(st.h_col, csr->col_idx, sizeof(uint32_t) * E, cudaMemcpyDefault), "copy col_idx");
+        if (o.flags & CSAW_GRAPH_OOM_PEER_STORE) {   // partition store in a peer GPU's HBM (NEXT-4(i))
+            if (o.store_device < 0 || o.store_device >= ndev)
+                return cleanup(fail(CSAW_ERR_INVALID_ARG, "OOM peer store: bad store_device"));
+            st.store_device = o.store_device;
+            if (o.store_device != o.device) {
+                int can = 0;
+                CREATE_CUDA(cudaDeviceCanAccessPeer(&can, o.device, o.store_device), "peer query");
+                if (!can) return cleanup(fail(CSAW_ERR_UNSUPPORTED, "OOM peer store: no peer access to store_device"));
+                const cudaError_t pe = cudaDeviceEnablePeerAccess(o.store_device, 0);
+                if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) CREATE_CUDA(pe, "enable peer access");
+                cudaGetLastError();
+            }
+            CREATE_CUDA(cudaSetDevice(o.store_device), "cudaSetDevice(store)");
+            const cudaError_t me = cudaMalloc(&st.d_store, sizeof(uint32_t) * std::max<int64_t>(E, 1));
+            cudaError_t ce = cudaSuccess;
+            if (me == cudaSuccess && E > 0) ce = cudaMemcpy(st.d_store, csr->col_idx, sizeof(uint32_t) * E, cudaMemcpyDefault);
+            CREATE_CUDA(cudaSetDevice(o.device), "cudaSetDevice");
+            CREATE_CUDA(me, "cudaMalloc(peer store)");
+            CREATE_CUDA(ce, "copy col_idx to the peer store");
+            st.src_col = st.d_store;
+        } else {
+            CREATE_CUDA(cudaMallocHost(&st.h_col, sizeof(uint32_t) * std::max<int64_t>(E, 1)), "cudaMallocHost(col)");
+            if (E > 0) CREATE_CUDA(cudaMemcpy(st.h_col, csr->col_idx, sizeof(uint32_t) * E, cudaMemcpyDefault), "copy col_idx");
+            st.src_col = st.h_col;
+        }
         for (int p = 0; p < st.P; ++p) {
             const int64_t e0 = st.ebeg[p], ne = st.ebeg[p + 1] - e0;
             if (ne == 0) continue;
-            CREATE_CUDA(cudaMemcpy(st.d_slots, st.h_col + e0, sizeof(uint32_t) * ne, cudaMemcpyHostToDevice), "slice");
+            CREATE_CUDA(cudaMemcpy(st.d_slots, st.src_col + e0, sizeof(uint32_t) * ne, cudaMemcpyDefault), "slice");
             k_validate_cols<<<blocks, 256>>>(st.d_slots, ne, e0, V, dv);
             k_validate_sorted<<<blocks, 256>>>(g->row_ptr, st.d_slots - e0, st.bounds[p], st.bounds[p + 1], dv);
             CREATE_CUDA(cudaDeviceSynchronize(), "validate slice");
@@ -769,7 +792,7 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
                     st.d_colc = nullptr;
                     st.colc_n = 0;
                 } else {
-                    CREATE_CUDA(cudaMemcpy(st.d_colc, st.h_col, sizeof(uint32_t) * st.colc_n, cudaMemcpyHostToDevice),
+                    CREATE_CUDA(cudaMemcpy(st.d_colc, st.src_col, sizeof(uint32_t) * st.colc_n, cudaMemcpyDefault),
                                 "copy resident col prefix");
                 }
             }
@@ -789,7 +812,7 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
     // chunk-total cache of the degree bias: always in OOM mode when it fits the budget (no
     // per-entry cache does), on request in memory
     if ((g->oom && g->oomst.want_ccache) || (!g->oom && (o.flags & CSAW_GRAPH_CHUNK_CACHE))) {
-        const csaw_status cs_ = build_ccache(g, g->oom ? g->oomst.h_col : g->col, blocks);
+        const csaw_status cs_ = build_ccache(g, g->oom ? g->oomst.src_col : g->col, blocks);
         if (cs_ != CSAW_OK) return cleanup(cs_);
     }
     // Accelerators.  The CTPS cache is the one structure a caller asks for by name and is
@@ -885,6 +908,11 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->winn) cudaFree(g->winn);
     auto& st = g->oomst;
     if (st.h_col) cudaFreeHost(st.h_col);
+    if (st.d_store) {
+        cudaSetDevice(st.store_device);
+        cudaFree(st.d_store);
+        cudaSetDevice(g->device);
+    }
     if (st.h_row) cudaFreeHost(st.h_row);
     if (st.d_slots) cudaFree(st.d_slots);
     if (st.d_colc) cudaFree(st.d_colc);
@@ -1064,7 +1092,7 @@ CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32
     }
     csaw_status s;
     if (g->oom && g->oomst.zerocopy) {
-        s = run_walk(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);   // every kernel reads h_col
+        s = run_walk(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);   // every kernel reads src_col
     } else if (g->oom) {
         if (b.kind == CSAW_BIAS_MDRW) s = run_mdrw_oom(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
         else s = run_walk_oom(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);

@@ -80,7 +80,10 @@ struct OomState {
     std::vector<int64_t> bounds;   // vertex bounds [P+1]
     std::vector<int64_t> ebeg;     // first edge of partition p
     int64_t slot_edges = 0;        // capacity of an arena slot in col entries
-    uint32_t* h_col = nullptr;     // pinned host col_idx (full graph)
+    uint32_t* h_col = nullptr;     // pinned host col_idx (full graph), unless the store is a peer GPU's
+    uint32_t* d_store = nullptr;   // CSAW_GRAPH_OOM_PEER_STORE: col_idx in store_device's HBM
+    int store_device = -1;
+    const uint32_t* src_col = nullptr;   // the partition store: h_col or d_store (UVA pointer)
     int64_t* h_row = nullptr;      // pinned host row_ptr
     uint32_t* d_slots = nullptr;   // R arena slots of col entries
     // zero-copy mode: col_idx[0, colc_n) resident on the device (the budget left after

@@ -268,8 +268,9 @@ csaw_status oom_load(const csaw_graph* g, int32_t p, int32_t slot, cudaEvent_t a
     CSAW_CUDA(cudaStreamWaitEvent(ss, after, 0));
     CSAW_CUDA(cudaEventRecord(t0, ss));
     const int64_t ne = os.ebeg[p + 1] - os.ebeg[p];
-    CSAW_CUDA(cudaMemcpyAsync(os.d_slots + static_cast<int64_t>(slot) * os.slot_edges, os.h_col + os.ebeg[p],
-                              sizeof(uint32_t) * ne, cudaMemcpyHostToDevice, ss));
+    // host -> device (the paper's §5 store) or peer HBM -> local HBM over NVLink (NEXT-4(i))
+    CSAW_CUDA(cudaMemcpyAsync(os.d_slots + static_cast<int64_t>(slot) * os.slot_edges, os.src_col + os.ebeg[p],
+                              sizeof(uint32_t) * ne, cudaMemcpyDefault, ss));
     CSAW_CUDA(cudaEventRecord(t1, ss));
     tev.push_back(t0);
     tev.push_back(t1);

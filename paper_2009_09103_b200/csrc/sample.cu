@@ -1175,7 +1175,7 @@ static csaw_status run_sample_fused(const csaw_graph* g, const csaw_bias& b, con
     CSAW_CUDA(cudaMemsetAsync(counters, 0, 256, st));
     CSAW_TRY(stats_begin(g, st));
     FusedArgs a;
-    a.rp = g->row_ptr; a.col = g->oom ? g->oomst.h_col : g->col; a.deg = g->deg; a.cps = g->cps; a.npos = g->npos; a.bt = g->bt;
+    a.rp = g->row_ptr; a.col = g->oom ? g->oomst.src_col : g->col; a.deg = g->deg; a.cps = g->cps; a.npos = g->npos; a.bt = g->bt;
     a.bt_off = g->bt_off; a.seeds = d_seeds; a.n = n; a.depth = depth;
     for (int d = 0; d < 16; ++d) a.fanout[d] = (d < depth && !ff) ? fanout[d] : 0;
     a.theta = ff ? static_cast<uint64_t>(std::floor(b.pf * 4294967296.0)) : 0;
@@ -1289,7 +1289,7 @@ csaw_status run_sample_levels(const csaw_graph* g, const csaw_bias& b, const int
     const bool snow = b.kind == CSAW_BIAS_SNOWBALL;   // uniform bias, k = all (select-all path, R8)
     const bool degree_bias = b.kind == CSAW_BIAS_DEGREE;
     // zero-copy OOM mode reads col_idx in place from pinned host memory (UVA)
-    const uint32_t* colz = g->oom ? g->oomst.h_col : g->col;
+    const uint32_t* colz = g->oom ? g->oomst.src_col : g->col;
     const uint32_t a_max = b.a_max ? static_cast<uint32_t>(b.a_max) : 64u;
     const uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     const uint64_t theta = ff ? static_cast<uint64_t>(std::floor(b.pf * 4294967296.0)) : 0;

@@ -1728,7 +1728,7 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
     note_launch();
     const uint2 key = make_uint2(static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
     // zero-copy OOM mode: col_idx is read in place from pinned host memory (UVA)
-    const uint32_t* colp = g->col ? g->col : g->oomst.h_col;
+    const uint32_t* colp = g->col ? g->col : g->oomst.src_col;
     WalkArgs a{g->row_ptr, colp, g->deg, d_seeds, static_cast<uint64_t>(n), length,
                static_cast<uint32_t>(base), key, d_path, static_cast<unsigned long long*>(cnt), g->ccache};
     if (b.kind == CSAW_BIAS_DEGREE && g->wix_leaf) {
