@@ -36,6 +36,10 @@
 #include "internal.h"
 #include "util.cuh"
 
+#ifndef N2X_SECTOR_PROBES
+#define N2X_SECTOR_PROBES 0   // search member positions 32 B sector by sector (A/B r02 cfg3: 11.1 ms, 14.2 GB requested; per-member binary search 10.1 ms, 18.4 GB)
+#endif
+
 namespace csaw {
 
 // ---------------------------------------------------------------- build
@@ -202,7 +206,9 @@ csaw_status build_n2v_index(csaw_graph* g, int blocks) {
     unsigned long long total = 0;
     if (cudaMemcpy(&total, tot, sizeof(total), cudaMemcpyDeviceToHost) != cudaSuccess) return drop();
     if (total >= (1ull << 40)) return drop();
-    if (cudaMalloc(&g->n2x_idx, sizeof(uint32_t) * std::max<unsigned long long>(total, 1)) != cudaSuccess) return drop();
+    // + 8 entries: a search reads whole 32 B groups of member positions (N2X_SECTOR_PROBES)
+    if (cudaMalloc(&g->n2x_idx, sizeof(uint32_t) * (total + 8)) != cudaSuccess) return drop();
+    cudaMemset(g->n2x_idx + total, 0, sizeof(uint32_t) * 8);
     g->n2x_total = total;
     k_n2x<true><<<blocks * 4, 256>>>(g->row_ptr, g->col, src, E, g->n2x_rec, g->n2x_idx, asym);
     k_n2x_dst<<<blocks * 4, 256>>>(g->row_ptr, g->col, E, g->n2x_idx, g->n2x_rec);
@@ -255,12 +261,45 @@ __device__ __forceinline__ uint32_t n2x_last_le(const uint32_t* __restrict__ I, 
             }
         }
     }
+#if N2X_SECTOR_PROBES
+    // Probe whole 32 B sectors (8 members, one sector per DRAM access anyway): the predicate
+    // holds on a prefix, so one sector either holds the boundary (done) or halves the range.
+    const uintptr_t ia = reinterpret_cast<uintptr_t>(I);
+    while (l < h) {
+        const uint32_t mid = (l + h) >> 1;
+        // the aligned 8-member group holding I[mid]
+        const uint4* g = reinterpret_cast<const uint4*>((ia + 4ull * mid) & ~static_cast<uintptr_t>(31));
+        const uint4 q0 = __ldg(g), q1 = __ldg(g + 1);
+        ++probes;
+        // rank of the group's first member (negative if the group starts before I[0])
+        const int64_t gb = (static_cast<int64_t>(reinterpret_cast<uintptr_t>(g)) - static_cast<int64_t>(ia)) / 4;
+        const uint32_t pv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        const int64_t f0 = max(static_cast<int64_t>(l), gb), f1 = min(static_cast<int64_t>(h), gb + 8);   // inside [l, h)
+        uint32_t nt = 0, lastp = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int64_t jj = gb + k;
+            if (jj >= f0 && jj < f1 && n2x_S(wq, dq1, pv[k], static_cast<uint32_t>(jj), sub) <= x) { ++nt; lastp = pv[k]; }
+        }
+        if (nt == static_cast<uint32_t>(f1 - f0)) {   // all true: the boundary is to the right
+            l = static_cast<uint32_t>(f1);
+            pos = lastp;
+        } else if (nt == 0) {                         // all false: to the left
+            h = static_cast<uint32_t>(f0);
+        } else {                                      // inside the group
+            l = static_cast<uint32_t>(f0) + nt;
+            pos = lastp;
+            h = l;
+        }
+    }
+#else
     while (l < h) {
         const uint32_t mid = (l + h) >> 1;
         const uint32_t p = __ldg(I + mid);
         ++probes;
         if (n2x_S(wq, dq1, p, mid, sub) <= x) { l = mid + 1; pos = p; } else h = mid;
     }
+#endif
     found = l > lo;   // l - 1 is the last true rank, pos = I[l - 1]
     return l - 1;
 }
