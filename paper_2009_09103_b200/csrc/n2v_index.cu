@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -43,6 +44,72 @@
 namespace csaw {
 
 // ---------------------------------------------------------------- build
+// Hub rank bitmaps: for the vertices of highest degree (d >= N2X_HUB_DEG, up to a memory
+// cap) a bitmap of N(h) over [0, V) plus the count of set bits before every 512-bit block.
+// Intersecting a list with a hub's list then costs one bit test per element (membership)
+// and a popcount over one 64 B line (its position in N(h)) instead of a binary search of
+// the hub's row -- the hub-hub pairs dominate the build.
+#ifndef N2X_HUB_DEG
+#define N2X_HUB_DEG 1024
+#endif
+#ifndef N2X_HUB_MAX_BYTES
+#define N2X_HUB_MAX_BYTES (4ull << 30)   // bitmap scratch during the build
+#endif
+struct HubRank {
+    const int32_t* __restrict__ hid;       // [V] hub slot or -1 (nullptr: no hubs)
+    const uint64_t* __restrict__ bits;     // [nhub][W]
+    const uint32_t* __restrict__ bcnt;     // [nhub][W / 8 + 1]
+    uint64_t W;                            // words per bitmap (multiple of 8)
+    // position of x in N(h) if x is a member
+    __device__ __forceinline__ bool find(int32_t h, uint32_t x, uint64_t& pos) const {
+        const uint64_t* b = bits + static_cast<uint64_t>(h) * W;
+        const uint64_t wi = x >> 6;
+        const uint64_t w = __ldg(b + wi);
+        if (!((w >> (x & 63)) & 1ull)) return false;
+        const uint64_t blk = wi >> 3;
+        uint64_t c = __ldg(bcnt + static_cast<uint64_t>(h) * (W / 8 + 1) + blk);
+        for (uint64_t k = blk * 8; k < wi; ++k) c += __popcll(__ldg(b + k));
+        pos = c + __popcll(w & ((1ull << (x & 63)) - 1ull));
+        return true;
+    }
+};
+
+__global__ void k_hub_bits(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                           const uint32_t* __restrict__ hubs, uint32_t nhub, uint64_t W, uint64_t* __restrict__ bits) {
+    for (uint32_t h = blockIdx.x; h < nhub; h += gridDim.x) {
+        const uint32_t v = hubs[h];
+        uint64_t* b = bits + static_cast<uint64_t>(h) * W;
+        for (int64_t e = rp[v] + threadIdx.x; e < rp[v + 1]; e += blockDim.x) {
+            const uint32_t x = col[e];
+            atomicOr(reinterpret_cast<unsigned long long*>(b + (x >> 6)), 1ull << (x & 63));
+        }
+    }
+}
+
+// bcnt[h][k] = set bits of words [0, 8 k): one block per hub, a block scan of block counts
+template <int NT>
+__global__ void k_hub_cnt(const uint64_t* __restrict__ bits, uint32_t nhub, uint64_t W, uint32_t* __restrict__ bcnt) {
+    __shared__ uint64_t wsum[NT / 32];
+    __shared__ uint64_t total;
+    const uint64_t nb = W / 8;
+    for (uint32_t h = blockIdx.x; h < nhub; h += gridDim.x) {
+        const uint64_t* b = bits + static_cast<uint64_t>(h) * W;
+        uint32_t* c = bcnt + static_cast<uint64_t>(h) * (nb + 1);
+        const uint64_t per = (nb + NT - 1) / NT;
+        const uint64_t k0 = min(nb, threadIdx.x * per), k1 = min(nb, k0 + per);
+        uint64_t s = 0;
+        for (uint64_t k = k0; k < k1; ++k)
+            for (int j = 0; j < 8; ++j) s += __popcll(b[8 * k + j]);
+        uint64_t run = block_excl_scan<NT>(s, wsum, &total);
+        for (uint64_t k = k0; k < k1; ++k) {
+            c[k] = static_cast<uint32_t>(run);
+            for (int j = 0; j < 8; ++j) run += __popcll(b[8 * k + j]);
+        }
+        if (threadIdx.x == 0) c[nb] = static_cast<uint32_t>(total);
+        __syncthreads();
+    }
+}
+
 // One warp per undirected edge {v, u} (entry e = (v -> u) with u > v, its reverse r =
 // (u -> v)).  The shorter list is walked in rows of 32; each entry's lower bound in the
 // longer list gives its position there.  Pass 1 (kList = false) writes the records'
@@ -50,7 +117,7 @@ namespace csaw {
 template <bool kList>
 __global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col,
                       const uint32_t* __restrict__ src, int64_t E, uint4* __restrict__ rec,
-                      uint32_t* __restrict__ idx, unsigned int* __restrict__ asym) {
+                      uint32_t* __restrict__ idx, unsigned int* __restrict__ asym, HubRank hr) {
     const int lane = lane_id();
     for (uint64_t e = global_warp_id(); e < static_cast<uint64_t>(E); e += total_warps()) {
         const uint32_t v = src[e], u = col[e];
@@ -75,21 +142,29 @@ __global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict
         }
         uint32_t cnt = 0, below_v = 0, below_u = 0;
         uint64_t lo0 = 0;
+        const int32_t hb = hr.hid ? __ldg(hr.hid + (sv ? u : v)) : -1;   // the longer list's owner a hub?
         for (uint64_t r0 = 0; r0 < ns && lo0 < nb; r0 += 32) {
             const uint64_t i = r0 + lane;
             const bool valid = i < ns;
             const uint32_t x = valid ? __ldg(small + i) : NONE;
-            const uint32_t xmin = __shfl_sync(FULL, x, 0);
-            const int last = static_cast<int>(ns - 1 - r0 < 31 ? ns - 1 - r0 : 31);
-            const uint32_t xmax = __shfl_sync(FULL, x, last);
-            const uint64_t lo = warp_lower_bound(big, lo0, nb, xmin);
-            const uint64_t hi = xmax == NONE ? nb : warp_lower_bound(big, lo, nb, xmax + 1u);
-            uint64_t l = lo, h = hi;
-            while (l < h) {   // same trip count on every lane
-                const uint64_t mid = (l + h) >> 1;
-                if (__ldg(big + mid) < x) l = mid + 1; else h = mid;
+            uint64_t l = 0, hi = 0;
+            bool f;
+            if (hb >= 0) {   // bit test + rank in the hub's bitmap
+                f = valid && hr.find(hb, x, l);
+            } else {
+                const uint32_t xmin = __shfl_sync(FULL, x, 0);
+                const int last = static_cast<int>(ns - 1 - r0 < 31 ? ns - 1 - r0 : 31);
+                const uint32_t xmax = __shfl_sync(FULL, x, last);
+                const uint64_t lo = warp_lower_bound(big, lo0, nb, xmin);
+                hi = xmax == NONE ? nb : warp_lower_bound(big, lo, nb, xmax + 1u);
+                l = lo;
+                uint64_t h = hi;
+                while (l < h) {   // same trip count on every lane
+                    const uint64_t mid = (l + h) >> 1;
+                    if (__ldg(big + mid) < x) l = mid + 1; else h = mid;
+                }
+                f = valid && l < hi && __ldg(big + l) == x;
             }
-            const bool f = valid && l < hi && __ldg(big + l) == x;
             const unsigned m = __ballot_sync(FULL, f);
             if (kList) {
                 if (f) {
@@ -108,7 +183,7 @@ __global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict
                 below_u += __popc(__ballot_sync(FULL, f && x < u));
             }
             cnt += __popc(m);
-            lo0 = hi;
+            if (hb < 0) lo0 = hi;
         }
         if (!kList && lane == 0) {
             // e = (v -> u): a walker at u that came from v; prev = v sits at position j of N(u)
@@ -198,21 +273,70 @@ csaw_status build_n2v_index(csaw_graph* g, int blocks) {
     cudaMemset(asym, 0, sizeof(unsigned int));
     cudaMemset(g->n2x_rec, 0xFF, 4 * sizeof(uint4) * E);   // unused inline slots
     k_n2x_src<<<blocks, 256>>>(g->row_ptr, g->V, src);
-    k_n2x<false><<<blocks * 4, 256>>>(g->row_ptr, g->col, src, E, g->n2x_rec, nullptr, asym);
+    // hub rank bitmaps for the highest-degree rows (build scratch, freed below): at most
+    // N2X_HUB_MAX_BYTES, the largest degrees first
+    HubRank hr{nullptr, nullptr, nullptr, 0};
+    int32_t* hid = nullptr;
+    uint32_t* hubs = nullptr;
+    uint64_t* hbits = nullptr;
+    uint32_t* hcnt = nullptr;
+    auto free_hubs = [&]() {
+        if (hid) cudaFree(hid);
+        if (hubs) cudaFree(hubs);
+        if (hbits) cudaFree(hbits);
+        if (hcnt) cudaFree(hcnt);
+        hid = nullptr; hubs = nullptr; hbits = nullptr; hcnt = nullptr;
+        cudaGetLastError();
+    };
+    {
+        std::vector<int64_t> hrp(static_cast<size_t>(g->V) + 1);
+        std::vector<uint32_t> hv;
+        if (cudaMemcpy(hrp.data(), g->row_ptr, sizeof(int64_t) * (g->V + 1), cudaMemcpyDeviceToHost) == cudaSuccess) {
+            for (int64_t v = 0; v < g->V; ++v)
+                if (hrp[v + 1] - hrp[v] >= N2X_HUB_DEG) hv.push_back(static_cast<uint32_t>(v));
+            std::sort(hv.begin(), hv.end(), [&](uint32_t a, uint32_t b) {
+                return hrp[a + 1] - hrp[a] > hrp[b + 1] - hrp[b];
+            });
+            const uint64_t W = ((static_cast<uint64_t>(g->V) + 63) / 64 + 7) / 8 * 8;
+            const uint64_t per = W * 8 + (W / 8 + 1) * 4;
+            const uint64_t cap = static_cast<uint64_t>(N2X_HUB_MAX_BYTES) / per;
+            if (hv.size() > cap) hv.resize(cap);
+            const uint32_t nhub = static_cast<uint32_t>(hv.size());
+            std::vector<int32_t> hh(static_cast<size_t>(g->V), -1);
+            for (uint32_t k = 0; k < nhub; ++k) hh[hv[k]] = static_cast<int32_t>(k);
+            if (nhub > 0 && cudaMalloc(&hid, sizeof(int32_t) * g->V) == cudaSuccess &&
+                cudaMalloc(&hubs, sizeof(uint32_t) * nhub) == cudaSuccess &&
+                cudaMalloc(&hbits, sizeof(uint64_t) * W * nhub) == cudaSuccess &&
+                cudaMalloc(&hcnt, sizeof(uint32_t) * (W / 8 + 1) * nhub) == cudaSuccess) {
+                cudaMemcpy(hid, hh.data(), sizeof(int32_t) * g->V, cudaMemcpyHostToDevice);
+                cudaMemcpy(hubs, hv.data(), sizeof(uint32_t) * nhub, cudaMemcpyHostToDevice);
+                cudaMemset(hbits, 0, sizeof(uint64_t) * W * nhub);
+                k_hub_bits<<<std::min<uint32_t>(nhub, 65535), 256>>>(g->row_ptr, g->col, hubs, nhub, W, hbits);
+                k_hub_cnt<256><<<std::min<uint32_t>(nhub, 65535), 256>>>(hbits, nhub, W, hcnt);
+                hr = HubRank{hid, hbits, hcnt, W};
+            } else {
+                free_hubs();   // an accelerator of the build: without it, binary searches
+            }
+        }
+    }
+    k_n2x<false><<<blocks * 4, 256>>>(g->row_ptr, g->col, src, E, g->n2x_rec, nullptr, asym, hr);
     unsigned int h = 0;
-    if (cudaMemcpy(&h, asym, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess || h) return drop();   // not symmetric
+    if (cudaMemcpy(&h, asym, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess || h)   // not symmetric
+        return (free_hubs(), drop());
     if (device_scan(N2xCount{g->n2x_rec}, static_cast<uint64_t>(E), N2xOffset{g->n2x_rec, tot}, part, nullptr) != CSAW_OK)
-        return drop();
+        return (free_hubs(), drop());
     unsigned long long total = 0;
-    if (cudaMemcpy(&total, tot, sizeof(total), cudaMemcpyDeviceToHost) != cudaSuccess) return drop();
-    if (total >= (1ull << 40)) return drop();
+    if (cudaMemcpy(&total, tot, sizeof(total), cudaMemcpyDeviceToHost) != cudaSuccess) return (free_hubs(), drop());
+    if (total >= (1ull << 40)) return (free_hubs(), drop());
     // + 8 entries: a search reads whole 32 B groups of member positions (N2X_SECTOR_PROBES)
-    if (cudaMalloc(&g->n2x_idx, sizeof(uint32_t) * (total + 8)) != cudaSuccess) return drop();
+    if (cudaMalloc(&g->n2x_idx, sizeof(uint32_t) * (total + 8)) != cudaSuccess) return (free_hubs(), drop());
     cudaMemset(g->n2x_idx + total, 0, sizeof(uint32_t) * 8);
     g->n2x_total = total;
-    k_n2x<true><<<blocks * 4, 256>>>(g->row_ptr, g->col, src, E, g->n2x_rec, g->n2x_idx, asym);
+    k_n2x<true><<<blocks * 4, 256>>>(g->row_ptr, g->col, src, E, g->n2x_rec, g->n2x_idx, asym, hr);
     k_n2x_dst<<<blocks * 4, 256>>>(g->row_ptr, g->col, E, g->n2x_idx, g->n2x_rec);
-    if (cudaDeviceSynchronize() != cudaSuccess) return drop();
+    const cudaError_t se = cudaDeviceSynchronize();
+    free_hubs();
+    if (se != cudaSuccess) return drop();
     release();
     return CSAW_OK;
 }
