@@ -684,6 +684,7 @@ def main():
                 "kernel": kname, "bytes_model": BYTES_MODEL[model], "alg_bytes_per_launch": bytes_per_launch,
                 "kernel_requested_bytes_per_launch": (kbytes / max(hot_launches, 1)) if kbytes else None,
                 "hot_ms_per_launch": hot_avg_ms, "hot_share_of_step": (hot_ms / total_ms) if total_ms else None,
+                **random_gather_context(achieved),
                 "peak_source": ("MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)" if "hbm_gbs" in peaks
                                 else "fallback: B200_PROFILING.md")}
 
@@ -923,6 +924,21 @@ def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads
     if cfg.workload == "neighbor" and cfg.bias == "uniform":
         mode = 0
     return f"k_sample_fused<{mode}>"
+
+
+def random_gather_context(achieved) -> dict:
+    """The measured random-access ceiling (profiles/random_gather_peaks.json, scripts/random_roofline.cu):
+    64 B records at uniformly random offsets of a 64 GiB buffer -- the access pattern of the pointer-chasing
+    walk kernels -- reach ~0.95 TB/s of requested bytes, far below the streaming copy peak.  Context for
+    `frac` (which stays against the copy peak): a dependent-gather kernel near this figure is at its
+    practical roofline."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "random_gather_peaks.json")) as f:
+            rg = json.load(f)["by_footprint_gib"]["64"]["64B"]
+    except Exception:
+        return {}
+    return {"random_gather_peak_gbs": rg,
+            "frac_of_random_gather_peak": (achieved / rg) if achieved else None}
 
 
 def load_peaks() -> dict:

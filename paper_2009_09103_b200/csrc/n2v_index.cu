@@ -505,14 +505,173 @@ __global__ void __launch_bounds__(256, N2X_MINB) k_node2vec_idx(N2xArgs a) {
     }
 }
 
+// ---- K = 2 walkers per thread, advanced in lock step: both walkers' record loads, and the
+// probes of both binary searches, are issued back to back -- twice the independent loads
+// in flight per thread (the kernel is bound by dependent DRAM latency).
+struct N2xSearch {          // one walker's step in flight
+    uint64_t rs;            // row start of v
+    const uint32_t* I;      // member positions of the entry
+    int64_t x, Sp, sub;
+    uint32_t C, ppos, mb, lo, l, h, pos, s;
+    bool after, done;
+};
+
+// record -> the step's search state (prev's own region resolves at once)
+__device__ __forceinline__ void n2x_setup(const N2xArgs& a, uint4 ra, uint4 rb, uint4 rc, uint4 rd, uint64_t U,
+                                          int64_t dq1, int64_t dqp, N2xSearch& q) {
+    const uint32_t wq = a.wq, w1 = a.w1, wp = a.wp;
+    q.rs = rb.y | (static_cast<uint64_t>(rb.z & 0xFFu) << 32);
+    const uint32_t d = rb.z >> 8;
+    q.C = ra.y >> 8; q.ppos = ra.z; q.mb = ra.w;
+    q.I = a.idx + (ra.x | (static_cast<uint64_t>(ra.y & 0xFFu) << 32));
+    const uint64_t T = static_cast<uint64_t>(wq) * (d - q.C - 1) + static_cast<uint64_t>(w1) * q.C + wp;
+    q.x = static_cast<int64_t>(below(U, T));
+    q.Sp = n2x_S(wq, dq1, q.ppos, q.mb, 0);
+    q.done = false;
+    q.pos = 0;
+    if (q.x >= q.Sp && q.x < q.Sp + wp) { q.s = q.ppos; q.done = true; q.l = q.h = 0; return; }
+    q.after = q.x >= q.Sp;
+    q.sub = q.after ? dqp : 0;
+    q.lo = q.after ? q.mb : 0;
+    const uint32_t hi = q.after ? q.C : q.mb;
+    const uint32_t P[8] = {rc.x, rc.y, rc.z, rc.w, rd.x, rd.y, rd.z, rd.w};
+    uint32_t l = q.lo, h = hi;
+    if (q.C <= 8) {
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k)
+            if (k >= q.lo && k < hi && n2x_S(wq, dq1, P[k], k, q.sub) <= q.x) { l = k + 1; q.pos = P[k]; }
+        h = l;
+    } else {
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k) {
+            const uint32_t j = static_cast<uint32_t>(((k + 1) * static_cast<uint64_t>(q.C)) / 9);
+            if (j >= q.lo && j < hi) {
+                if (n2x_S(wq, dq1, P[k], j, q.sub) <= q.x) { l = j + 1; q.pos = P[k]; }
+                else h = min(h, j);
+            }
+        }
+    }
+    q.l = l; q.h = h;
+}
+
+// search finished: the pick's position in N(v)
+__device__ __forceinline__ uint32_t n2x_finish(const N2xArgs& a, int64_t dq1, const N2xSearch& q) {
+    if (q.done) return q.s;
+    const uint32_t wq = a.wq, w1 = a.w1, wp = a.wp;
+    if (q.l > q.lo) {
+        const int64_t Sm = n2x_S(wq, dq1, q.pos, q.l - 1, q.sub);
+        return q.x < Sm + w1 ? q.pos : q.pos + 1 + static_cast<uint32_t>((q.x - Sm - w1) / wq);
+    }
+    return q.after ? q.ppos + 1 + static_cast<uint32_t>((q.x - q.Sp - wp) / wq) : static_cast<uint32_t>(q.x / wq);
+}
+
+#ifndef N2X_K2_MINB
+#define N2X_K2_MINB 2
+#endif
+__global__ void __launch_bounds__(256, N2X_K2_MINB) k_node2vec_idx2(N2xArgs a) {
+    const uint32_t wq = a.wq, w1 = a.w1, wp = a.wp;
+    const int64_t dq1 = static_cast<int64_t>(wq) - w1, dqp = static_cast<int64_t>(wq) - wp;
+    unsigned long long steps = 0, probes_all = 0;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (uint64_t w0 = tid; w0 < a.n; w0 += 2 * nthreads) {
+        uint64_t e[2];
+        uint32_t* row[2];
+        uint32_t inst[2];
+        bool live[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const uint64_t w = w0 + k * nthreads;
+            live[k] = w < a.n;
+            e[k] = 0;
+            row[k] = a.path + w * (static_cast<uint64_t>(a.L) + 1);
+            inst[k] = a.base + static_cast<uint32_t>(w);
+            if (!live[k]) continue;
+            const uint32_t seed = a.seeds[w];
+            row[k][0] = seed;
+            if (a.L == 0) { live[k] = false; continue; }
+            const int64_t b0 = __ldg(a.rp + seed);
+            const uint32_t d0 = static_cast<uint32_t>(__ldg(a.rp + seed + 1) - b0);
+            if (d0 == 0) {   // isolated seed: the walk ends (R20)
+                for (int32_t t = 1; t <= a.L; ++t) row[k][t] = NONE;
+                live[k] = false;
+                continue;
+            }
+            e[k] = static_cast<uint64_t>(b0) + below(draw_u64(a.key, inst[k], 0u, 0u, word3(PURPOSE_EDGE, 0, 0)), d0);
+            ++steps;
+        }
+        for (int32_t t = 1; t <= a.L && (live[0] || live[1]); ++t) {
+            uint4 ra[2], rb[2], rc[2], rd[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (live[k]) {
+                    ra[k] = __ldg(a.rec + 4 * e[k]); rb[k] = __ldg(a.rec + 4 * e[k] + 1);
+                    rc[k] = __ldg(a.rec + 4 * e[k] + 2); rd[k] = __ldg(a.rec + 4 * e[k] + 3);
+                }
+            }
+            N2xSearch q[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                q[k].done = true; q[k].l = q[k].h = 0;
+                if (!live[k]) continue;
+                row[k][t] = rb[k].x;
+                if (t == a.L) continue;
+                const uint64_t U = draw_u64(a.key, inst[k], static_cast<uint32_t>(t), 0u, word3(PURPOSE_EDGE, 0, 0));
+                n2x_setup(a, ra[k], rb[k], rc[k], rd[k], U, dq1, dqp, q[k]);
+            }
+            if (t == a.L) break;
+            // both binary searches, one probe of each per round
+            while (q[0].l < q[0].h || q[1].l < q[1].h) {
+                uint32_t mid[2], p[2];
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    mid[k] = (q[k].l + q[k].h) >> 1;
+                    p[k] = q[k].l < q[k].h ? __ldg(q[k].I + mid[k]) : 0u;
+                }
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    if (q[k].l < q[k].h) {
+                        ++probes_all;
+                        if (n2x_S(wq, dq1, p[k], mid[k], q[k].sub) <= q[k].x) { q[k].l = mid[k] + 1; q[k].pos = p[k]; }
+                        else q[k].h = mid[k];
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (!live[k]) continue;
+                e[k] = q[k].rs + n2x_finish(a, dq1, q[k]);
+                ++steps;
+            }
+        }
+    }
+    steps = warp_sum(steps);
+    probes_all = warp_sum(probes_all);
+    if (lane_id() == 0 && steps) {
+        atomicAdd(a.counters + 1, steps);
+        atomicAdd(a.counters + 2, probes_all);
+        atomicAdd(a.counters + 3, 32ull * (2 * steps + probes_all) + 4ull * steps);
+    }
+}
+
+#ifndef N2X_K
+#define N2X_K 1   // walkers per thread (A/B r02 cfg3: K = 1 10.12 ms; K = 2 11.40 ms at 128 regs, 10.96 ms at 80 regs)
+#endif
+
 csaw_status launch_node2vec_index(const csaw_graph* g, const uint32_t* seeds, uint64_t n, int32_t L, uint32_t base,
                                   uint2 key, uint32_t* path, unsigned long long* counters, uint32_t wp, uint32_t w1,
                                   uint32_t wq, cudaStream_t st) {
     N2xArgs a{g->row_ptr, g->n2x_rec, g->n2x_idx, seeds, n, L, base, key, path, counters, wp, w1, wq};
     const uint64_t resident = static_cast<uint64_t>(g->num_sms) * 2048;
-    const uint64_t threads = std::min<uint64_t>(n, resident);
-    const int grid = static_cast<int>(std::max<uint64_t>(1, (threads + 255) / 256));
-    k_node2vec_idx<<<grid, 256, 0, st>>>(a);
+    if (N2X_K == 2) {
+        const uint64_t threads = std::min<uint64_t>((n + 1) / 2, resident);
+        const int grid = static_cast<int>(std::max<uint64_t>(1, (threads + 255) / 256));
+        k_node2vec_idx2<<<grid, 256, 0, st>>>(a);
+    } else {
+        const uint64_t threads = std::min<uint64_t>(n, resident);
+        const int grid = static_cast<int>(std::max<uint64_t>(1, (threads + 255) / 256));
+        k_node2vec_idx<<<grid, 256, 0, st>>>(a);
+    }
     note_launch();
     CSAW_CUDA(cudaGetLastError());
     return CSAW_OK;
