@@ -42,7 +42,8 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from synth import CONFIGS, degree_stats, instance_seeds, mdrw_seeds, nonisolated_vertices, rmat_csr  # noqa: E402
+from synth import (CONFIGS, degree_stats, edge_weights, instance_seeds, mdrw_seeds, nonisolated_vertices,  # noqa: E402
+                   rmat_csr)
 
 METRIC = "sampled edges/sec (SEPS) at 1/2/4/8 B200; % of HBM roofline"
 UNIT = "sampled_edges/s"
@@ -163,6 +164,8 @@ BYTES_MODEL = {
     "walk_degree_cached": "SURVEY §8(f) NEXT-1 cached CTPS: 32 B sectors x (row_ptr pair + ceil(log2 d(v)) probes "
                           "+ col) per step + 4 (path)",
     "walk_uniform": "16 (row_ptr pair) + 4 (one col entry) + 4 (path) per step",
+    "walk_weight_stream": "per-step scan of the fp32 edge weights (float path): 16 (row_ptr pair) + 4 d(v) (the pool's "
+                          "weights, streamed) + 4 (the pick's col) + 4 (path)",
     "node2vec": "SURVEY §8(d) node2vec step: 16 + 4 d(v) + 4 (N(prev) carried from the previous step); "
                 "step 0 uniform: 16 + 4 + 4",
     "node2vec_index": "NEXT-1-style sector model of the node2vec intersection index: 32 B sectors x (the 64 B "
@@ -190,6 +193,8 @@ def walk_alg_bytes(cfg, deg, out, cached, stream=False):
         return int(16 * nsteps + 4 * d[:, 1:].sum() + 4 * first + 4 * nsteps), "node2vec"
     if cfg.bias == "uniform":
         return 24 * nsteps, "walk_uniform"
+    if cfg.bias == "weight":
+        return int(16 * nsteps + 4 * d.sum() + 8 * nsteps), "walk_weight_stream"
     if cached:
         probes = _bit_length(torch.clamp(d - 1, min=0))
         return int(32 * (2 * nsteps + probes[valid].sum()) + 4 * nsteps), "walk_degree_cached"
@@ -299,7 +304,10 @@ def _oracle_job(args):
     for j, i in enumerate(range(lo, hi)):
         gi = base + i
         s = seeds[j]
-        if cfg.workload == "walk":
+        if cfg.workload == "walk" and cfg.bias == "weight":
+            O.weight_walk(g, cfg.length, int(s), gi, rng_seed)
+            edges += cfg.length
+        elif cfg.workload == "walk":
             O.walk(g, O.KIND_DEGREE if cfg.bias == "degree" else O.KIND_UNIFORM, cfg.length, int(s), gi, rng_seed)
             edges += cfg.length
         elif cfg.workload == "node2vec":
@@ -359,7 +367,7 @@ def run_reference(args):
     dev = torch.device("cuda:0") if torch.cuda.is_available() else torch.device("cpu")
     g, _ = make_graph(cfg, dev)
     base, seeds, _ = make_seeds(cfg, g, 0, 1, "strong")
-    og = O.Graph.from_torch(g)
+    og = O.Graph.from_torch(g, edge_weights(g, cfg.graph_seed) if cfg.bias == "weight" else None)
     seeds_np = seeds.cpu().numpy().view(np.uint32)
     del g
     if dev.type == "cuda":
@@ -496,8 +504,10 @@ def main():
         use_tri = (not args.no_cache) and cfg.workload == "node2vec"
         use_meta = (not args.no_cache) and cfg.workload == "mdrw"
         use_eb = args.no_cache and not args.gather_bias and cfg.workload == "walk" and cfg.bias == "degree"
+        wts = edge_weights(g, cfg.graph_seed) if cfg.bias == "weight" else None
         G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache, node2vec_tri=use_tri,
-                                 next_meta=use_meta, walk_index=use_cache, node2vec_index=use_tri, edge_bias=use_eb)
+                                 next_meta=use_meta, walk_index=use_cache, node2vec_index=use_tri, edge_bias=use_eb,
+                                 weights=wts)
     ginfo = G.info()
     bias = bias_of(cs, cfg)
     stream = torch.cuda.current_stream(dev)
@@ -637,7 +647,7 @@ def main():
 
     # ---------------- the config's per-step scan path (no caches), reported apart
     scan_path = None
-    if args.scan_path_steps > 0 and not oom and not args.no_cache and rank == 0:
+    if args.scan_path_steps > 0 and not oom and not args.no_cache and rank == 0 and cfg.bias != "weight":
         scan_path = run_scan_path(cs, g, cfg, deg, seeds, base, rng_seeds, n, dev, local, stream, flush, args)
 
     # ---------------- end-to-end through the C ABI with host buffers
@@ -694,7 +704,7 @@ def main():
         try:
             import oracle as O
             O.build()
-            og = O.Graph.from_torch(g)
+            og = O.Graph.from_torch(g, edge_weights(g, cfg.graph_seed) if cfg.bias == "weight" else None)
             sv = seeds.cpu().numpy()
             sv = sv.view(np.uint32) if sv.dtype == np.int32 else sv.astype(np.uint32)
             v, cores, sample, _, _ = oracle_timed_sample(cfg, og, sv, base, rng_seeds[0], args.cpu_seconds)
@@ -905,6 +915,8 @@ def run_e2e(cs, G, bias, seeds, cfg, base, rng_seeds, args, kind, n, dev, world,
 
 def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads=False, n2x=False, eb=False):
     if cfg.workload == "walk":
+        if cfg.bias == "weight":
+            return "k_walk_vscan<float>"
         if cfg.bias == "degree" and not cached and eb:
             return "k_walk_vscan<uint32>"
         if cfg.bias == "degree" and wix_leaf and heads and wix_group == 32:

@@ -52,6 +52,13 @@ CONFIGS = {
         "cfg5", 65_600_000, 1_800_000_000, 5, "mdrw", "mdrw", 4000, length=2000, pool_size=2000,
         oom_budget_bytes=8_000_000_000, oom_partitions=4, oom_resident=2,
         description="MDRW pool 2,000, 2,000 steps, 4,000 instances, FR-shaped R-MAT 65.6M V / 1.8B E, OOM 8 GB budget"),
+    # the float path (R28/R32) at config-2 scale: the same LJ-shaped graph with seeded fp32 edge
+    # weights (synth/weights.py) and EdgeBias = w(e) -- not a BASELINE config, a measurement of
+    # the per-step weight scan
+    "cfg2_weight": WorkloadConfig(
+        "cfg2_weight", 4_800_000, 69_000_000, 2, "walk", "weight", 4000, length=2000,
+        description="edge-weight walk (EdgeBias = w(e), fp32 weights summed in fp64), length 2,000, 4,000 walkers, "
+                    "LJ-shaped R-MAT 4.8M V / 69M E with seeded weights"),
     # config 5's second half: batched multi-instance traversal sampling under the same budget (§5.2-5.3)
     "cfg5_ns": WorkloadConfig(
         "cfg5_ns", 65_600_000, 1_800_000_000, 5, "neighbor", "degree", 8192, fanout=(2, 2), depth=2,

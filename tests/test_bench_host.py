@@ -92,3 +92,20 @@ def test_self_launch_only_outside_torchrun(monkeypatch):
     monkeypatch.setenv("WORLD_SIZE", "2")
     assert bench.maybe_spawn(bench.parse_args(["--gpus", "2"])) is None
     assert bench.parse_args([]).config == "cfg3" and bench.parse_args([]).scaling == "strong"
+
+
+def test_walk_bytes_stream_model_and_scan_path_names():
+    # materialised degree-bias stream: 16 + 4 d(v) + 4 (the pick's col) + 4 (path) per step
+    deg = torch.tensor([3, 1, 2, 5], dtype=torch.int64)
+    path = torch.tensor([[0, 1, 0, 3], [2, 0, 2, 0]], dtype=torch.int32)
+    b, m = bench.walk_alg_bytes(CONFIGS["cfg2"], deg, path, cached=False, stream=True)
+    assert m == "walk_degree_stream" and b == 6 * 16 + 4 * 14 + 6 * 8
+    assert bench.hot_kernel_name(CONFIGS["cfg2"], cached=False, eb=True) == "k_walk_vscan<uint32>"
+    assert bench.hot_kernel_name(CONFIGS["cfg2"], cached=False) == "k_walk<degree>"
+    assert bench.hot_kernel_name(CONFIGS["cfg3"], n2x=True) == "k_node2vec_idx"
+
+
+def test_random_gather_context_reads_the_committed_measurement():
+    c = bench.random_gather_context(500.0)
+    assert c["random_gather_peak_gbs"] > 0
+    assert abs(c["frac_of_random_gather_peak"] - 500.0 / c["random_gather_peak_gbs"]) < 1e-12

@@ -5,7 +5,9 @@ workload through the C ABI exactly as bench.py does (all instances in one call),
 and compares with the oracle element by element (integer biases: bit-exact) at
 the coverage SURVEY.md §8(d) d.4 plans:
 
-  cfg2  all 4,000 walkers                      (cache + walk index, and the scan path)
+  cfg2  all 4,000 walkers                      (cache + walk index, and the scan paths: deg
+                                               gathers and the streamed materialised bias);
+        cfg2_weight: all 4,000 edge-weight walkers (float path, 1e-6 boundary rule)
   cfg3  every 64th walker (~29.5K of ~1.9M)    (intersection index = the bench's launch);
         the index, triangle-count and full-merge kernels are also compared with each
         other on 100 % of the walkers
@@ -96,10 +98,13 @@ def test_cfg2_degree_walk_full():
     sv = u32(seeds)
     Gc = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, ctps_cache=True)     # the bench's launch
     Gs = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0)                      # per-step scans (the ★ path)
-    assert Gc.info()["walk_index_leaf"] == 128 and Gs.info()["ctps_cache"] == 0
+    Ge = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, edge_bias=True)      # per-step scans of the streamed bias
+    assert Gc.info()["walk_index_leaf"] == 128 and Gs.info()["ctps_cache"] == 0 and Ge.info()["edge_bias"] == 1
     for seed in SEEDS:
         pc = u32(cs.csaw_walk(Gc, "degree", seeds, cfg.length, rng_seed=seed))
         ps = u32(cs.csaw_walk(Gs, "degree", seeds, cfg.length, rng_seed=seed))
+        pe = u32(cs.csaw_walk(Ge, "degree", seeds, cfg.length, rng_seed=seed))
+        assert first_mismatch(pe, ps) is None, f"seed {seed}: stream vs gather walker {first_mismatch(pe, ps)}"
         t0 = time.time()
         ref = np.stack(O.parallel_run(og, "walk", sv, 0, seed, kind=O.KIND_DEGREE, length=cfg.length))
         log(f"cfg2 seed {seed}: oracle over all {len(sv)} walkers in {time.time() - t0:.1f} s")
@@ -108,7 +113,35 @@ def test_cfg2_degree_walk_full():
         assert first_mismatch(ps, ref) is None, f"seed {seed}: scan walker {first_mismatch(ps, ref)}"
         assert (pc != cs.NONE).all()          # symmetric graph, non-isolated seeds: exact length
         check_edges_exist(og, pc[:, :-1].ravel(), pc[:, 1:].ravel())
-    release(Gc, Gs)
+    release(Gc, Gs, Ge)
+
+
+def test_cfg2_weight_walk_full():
+    """The float path (R28/R32) at config-2 scale: all 4,000 walkers of the edge-weight walk vs the
+    oracle; a walk may leave the oracle's only at a step whose draw lies within 1e-6 of a CTPS
+    boundary (the oracle reports the margin of every step)."""
+    from synth import edge_weights
+    cfg = CONFIGS["cfg2_weight"]
+    g = rmat_csr(cfg.graph_vertices, cfg.graph_entries, cfg.graph_seed, device=DEV)
+    w = edge_weights(g, cfg.graph_seed)
+    og = O.Graph.from_torch(g, w)
+    seeds = instance_seeds(g, cfg.n_instances).to(DEV)
+    sv = u32(seeds)
+    G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, weights=w)
+    for seed in SEEDS:
+        pw = u32(cs.csaw_walk(G, "weight", seeds, cfg.length, rng_seed=seed))
+        t0 = time.time()
+        ref = O.parallel_run(og, "weight_walk", sv, 0, seed, length=cfg.length)
+        log(f"cfg2_weight seed {seed}: oracle over all {len(sv)} walkers in {time.time() - t0:.1f} s")
+        excused = 0
+        for i, (rp, mg) in enumerate(ref):
+            if not np.array_equal(pw[i], rp):
+                t = int(np.argmax(pw[i] != rp)) - 1     # the step whose pick differs
+                assert mg[t] <= 1e-6, f"seed {seed}: walker {i} step {t} margin {mg[t]}"
+                excused += 1
+        assert excused <= 4, excused
+        check_edges_exist(og, pw[:, :-1].ravel(), pw[:, 1:].ravel())
+    release(G)
 
 
 # ------------------------------------------------------------------ cfg3
