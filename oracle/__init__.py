@@ -66,6 +66,8 @@ def lib():
             "oracle_weight_walk_step": (u32, [P, P, P, i64, u32, u32, u32, u64, P]),
             "oracle_weight_walk": (None, [P, P, P, i64, i32, u32, u32, u64, P, P]),
             "oracle_weight_sample": (i64, [P, P, P, i64, P, i32, u32, u32, u64, i32, P, P, P, i64, P]),
+            "oracle_node2vec_w_step": (u32, [P, P, P, i64, f64, f64, u32, u32, u32, u32, u64, P]),
+            "oracle_node2vec_w": (None, [P, P, P, i64, f64, f64, i32, u32, u32, u64, P, P]),
             "oracle_partition_bounds": (None, [i64, i32, P]),
             "oracle_active_counts": (None, [P, i32, P, i64, P]),
         }
@@ -276,6 +278,20 @@ def node2vec(g: Graph, p, q, length, s0, inst, rng_seed, with_margins=False):
     return (path, mg[:length]) if with_margins else path
 
 
+def node2vec_w_step(g: Graph, p, q, prev, v, inst, t, rng_seed):
+    """Weighted node2vec step (alpha * w, R33) -> (next vertex, margin)."""
+    m = np.ones(1, dtype=np.float64)
+    u = lib().oracle_node2vec_w_step(_p(g.row_ptr), _p(g.col), _p(g.w), g.V, p, q, prev, v, inst, t, rng_seed, _p(m))
+    return int(u), float(m[0])
+
+
+def node2vec_w(g: Graph, p, q, length, s0, inst, rng_seed, with_margins=False):
+    path = np.zeros(length + 1, dtype=np.uint32)
+    mg = np.ones(max(length, 1), dtype=np.float64)
+    lib().oracle_node2vec_w(_p(g.row_ptr), _p(g.col), _p(g.w), g.V, p, q, length, s0, inst, rng_seed, _p(path), _p(mg))
+    return (path, mg[:length]) if with_margins else path
+
+
 def mdrw(g: Graph, seeds, steps, inst, rng_seed) -> np.ndarray:
     seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint32))
     edges = np.zeros((steps, 2), dtype=np.uint32)
@@ -362,6 +378,9 @@ def _run_job(args):
             out.append(weight_walk(_G, params["length"], int(s), gi, rng_seed, with_margins=True))
         elif workload == "weight":
             out.append(weight_sample(_G, params["fanout"], params["depth"], int(s), gi, rng_seed))
+        elif workload == "node2vec_w":
+            out.append(node2vec_w(_G, params["p"], params["q"], params["length"], int(s), gi, rng_seed,
+                                  with_margins=True))
         else:
             kind = {"uniform": KIND_UNIFORM, "degree": KIND_DEGREE, "forest_fire": KIND_FF,
                     "snowball": KIND_SNOWBALL}[workload]

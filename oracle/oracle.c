@@ -811,6 +811,54 @@ ORACLE_EXPORT void oracle_node2vec(const int64_t *row_ptr, const uint32_t *col, 
 }
 
 /*
+ * Weighted node2vec step (the bias "depends upon the edge weight and its distance
+ * from the vertex explored at preceding step"; Grover & Leskovec: alpha(prev, u) * w(v, u);
+ * reading R33): b_i = fp32(alpha_i) * w[row_ptr[v] + i] as one fp32 multiply, alpha as in
+ * R16 ((float)(1/p) if u == prev, 1 if u in N(prev), (float)(1/q) otherwise), then the float
+ * path oracle_select_float (R28).  prev == 0xFFFFFFFF (step 0): b_i = w_i (the weighted
+ * walk's step).  *margin (nullable) = the draw's boundary margin.
+ */
+ORACLE_EXPORT uint32_t oracle_node2vec_w_step(const int64_t *row_ptr, const uint32_t *col, const float *w,
+                                              int64_t V, double p, double q, uint32_t prev, uint32_t v,
+                                              uint32_t inst, uint32_t t, uint64_t rng_seed, double *margin)
+{
+    csr_t g = { row_ptr, col, V };
+    int64_t n = deg_of(&g, v);
+    const uint32_t *pool = col + row_ptr[v];
+    const float *wv = w + row_ptr[v];
+    if (margin) *margin = 1.0;
+    if (n == 0) return 0xFFFFFFFFu;
+    uint64_t U = draw_u64(rng_seed, inst, t, 0, word3_of(P_EDGE, 0, 0), 0);
+    float fp = (float)(1.0 / p), f1 = 1.0f, fq = (float)(1.0 / q);
+    float *b = (float *)malloc(sizeof(float) * (size_t)n);
+    const uint32_t *np_ = (prev == 0xFFFFFFFFu) ? NULL : col + row_ptr[prev];
+    int64_t nprev = (prev == 0xFFFFFFFFu) ? 0 : deg_of(&g, prev);
+    for (int64_t i = 0; i < n; i++) {
+        uint32_t u = pool[i];
+        float a = (prev == 0xFFFFFFFFu) ? 1.0f : (u == prev ? fp : (sorted_contains(np_, nprev, u) ? f1 : fq));
+        b[i] = a * wv[i];
+    }
+    int64_t s = oracle_select_float(b, n, U, margin);
+    free(b);
+    return s < 0 ? 0xFFFFFFFFu : pool[s];
+}
+
+ORACLE_EXPORT void oracle_node2vec_w(const int64_t *row_ptr, const uint32_t *col, const float *w, int64_t V,
+                                     double p, double q, int32_t length, uint32_t s0, uint32_t inst,
+                                     uint64_t rng_seed, uint32_t *path, double *margins)
+{
+    path[0] = s0;
+    for (int32_t t = 0; t < length; t++) {
+        uint32_t v = path[t];
+        uint32_t prev = (t == 0) ? 0xFFFFFFFFu : path[t - 1];
+        double mg = 1.0;
+        path[t + 1] = (v == 0xFFFFFFFFu) ? 0xFFFFFFFFu
+            : oracle_node2vec_w_step(row_ptr, col, w, V, p, q, prev, v, inst, (uint32_t)t, rng_seed, &mg);
+        if (margins) margins[t] = mg;
+    }
+}
+
+/*
  * Multi-dimensional random walk (frontier sampling; Fig. 4):
  * pool = seeds[0..m) in slot order (R18); per step t: VertexBias = degree,
  * slot = its(S(pool), below(U(i,t,0,VERTEX), T)); v = pool[slot];

@@ -161,3 +161,50 @@ def test_weights_generator_is_symmetric_and_exact():
     d = dict(zip(zip(src.tolist(), col.tolist()), w.tolist()))
     assert all(d[(b, a)] == x for (a, b), x in d.items())
     assert 0.05 < (w == 0).mean() < 0.15 and np.isfinite(w).all() and (w >= 0).all()
+
+
+# ---------------------------------------------------------------- weighted node2vec (R33)
+def test_node2vec_w_with_p_q_1_is_the_weight_walk(R):
+    """alpha = 1 everywhere (p = q = 1): b = 1.0f * w = w exactly, and step 0 is the weighted
+    step -- the weighted node2vec walk is the edge-weight walk, pick for pick and margin for margin."""
+    g, og, _ = R
+    w = edge_weights(g, 5, zero_frac=0.05).numpy()
+    ow = O.Graph(og.row_ptr, og.col, w)
+    for i, s in enumerate(instance_seeds(g, 40).numpy()):
+        a, ma = O.node2vec_w(ow, 1.0, 1.0, 40, int(s), i, 9, with_margins=True)
+        b, mb = O.weight_walk(ow, 40, int(s), i, 9, with_margins=True)
+        assert np.array_equal(a, b) and np.array_equal(ma, mb)
+
+
+def test_node2vec_w_with_unit_weights_is_the_float_node2vec(R):
+    """w = 1: b = alpha exactly, so every step after the first equals the (unweighted) float
+    node2vec step at the same (prev, v) -- the pinned alpha law."""
+    g, og, _ = R
+    ow = O.Graph(og.row_ptr, og.col, np.ones(og.col.size, np.float32))
+    p, q = np.pi, np.e
+    for i, s in enumerate(instance_seeds(g, 30).numpy()):
+        path = O.node2vec_w(ow, p, q, 30, int(s), i, 4)
+        for t in range(1, 30):
+            if path[t + 1] == O.NONE32:
+                break
+            u, _ = O.node2vec_step(og, p, q, int(path[t - 1]), int(path[t]), i, t, 4)
+            assert u == path[t + 1]
+
+
+def test_node2vec_w_transition_law():
+    """v = 0 with prev = 1; N(0) = {1, 2, 3, 4}, N(1) = {0, 2}: alpha = (1/p, 1, 1/q, 1/q) for
+    u = 1, 2, 3, 4; weights (2, 1, 0.5, 0) -> P proportional to (2/p, 1, 0.5/q, 0)."""
+    rp = np.array([0, 4, 6, 7, 8, 9], np.int64)
+    col = np.array([1, 2, 3, 4, 0, 2, 0, 0, 0], np.uint32)
+    w = np.array([2.0, 1.0, 0.5, 0.0, 1.0, 1.0, 1.0, 1.0, 1.0], np.float32)
+    og = O.Graph(rp, col, w)
+    p, q = 2.0, 0.5
+    N = 16000
+    cnt = np.zeros(5)
+    for i in range(N):
+        u, _ = O.node2vec_w_step(og, p, q, 1, 0, i, 1, 33)
+        cnt[u] += 1
+    assert cnt[4] == 0 and cnt[0] == 0
+    pr = np.array([2 / p, 1.0, 0.5 / q])
+    from scipy import stats
+    assert stats.chisquare(cnt[[1, 2, 3]], pr / pr.sum() * N).pvalue > 1e-4
