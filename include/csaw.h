@@ -64,7 +64,9 @@ typedef enum {
 typedef enum {
     CSAW_BIAS_UNIFORM = 0,      /* EdgeBias = 1: unbiased neighbor sampling / simple walk */
     CSAW_BIAS_DEGREE = 1,       /* EdgeBias = deg(u): biased neighbor sampling (Fig. 1) / biased DeepWalk */
-    CSAW_BIAS_NODE2VEC = 2,     /* EdgeBias = alpha(prev, u) (R16); walks only */
+    CSAW_BIAS_NODE2VEC = 2,     /* EdgeBias = alpha(prev, u) (R16); walks only.  On a graph with
+                                   weights: alpha(prev, u) * w(e) as one fp32 multiply ("depends upon the edge
+                                   weight"; R33), float path (R28), step 0 weighted (b = w) */
     CSAW_BIAS_FOREST_FIRE = 3,  /* uniform EdgeBias, per-vertex burn count with P_f (R15); sampling only */
     CSAW_BIAS_LAYER = 4,        /* EdgeBias = deg(u) over the union pool of the frontier (R14); sampling only */
     CSAW_BIAS_MDRW = 5,         /* VertexBias = deg(v), EdgeBias = 1, Update = replace (Fig. 4); walks only */

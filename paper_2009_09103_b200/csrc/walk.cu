@@ -598,6 +598,7 @@ struct N2vArgs {
     WalkArgs wa;
     uint32_t wint[3];    // integer biases {m/p, m, m/q} (R16); unused on the float path
     float wf[3];         // float biases {(float)(1/p), 1, (float)(1/q)}
+    const float* __restrict__ ew = nullptr;   // edge weights: b = alpha * w(e) (R33), float path
 };
 
 // Float CTPS (general p, q): fp32 biases summed in fp64 (north star; R28).
@@ -611,9 +612,21 @@ __device__ __forceinline__ double warp_incl_scan_f64(double v) {
     return v;
 }
 
-// One float-path step: x = r*T with r = (U >> 11) 2^-53; s = first i with S_{i+1} > x
-// (clamped to n-1).  Two passes: totals per chunk of U rows, then a rescan.
-__device__ uint32_t n2v_float_step(Node2vecPool& P, const float (&wf)[3], double* ftab, uint64_t U64) {
+// The float bias of pool entry i: alpha (class code c) times the edge weight when weighted.
+__device__ __forceinline__ double n2v_fbias(const Node2vecPool& P, const float (&wf)[3], const float* __restrict__ ew,
+                                            bool first, uint32_t key, uint32_t c, uint32_t i) {
+    if (key == NONE) return 0.0;
+    const float a = first ? 1.0f : wf[c];
+    if (!ew) return static_cast<double>(a);
+    return static_cast<double>(__fmul_rn(a, __ldg(ew + P.beg + i)));   // one fp32 multiply (R33)
+}
+
+// One float-path step: x = r*T with r = (U >> 11) 2^-53; s = first i with b_i > 0 and
+// S_{i+1} > x (past every boundary through rounding: the last positive entry).  Two passes:
+// totals per chunk of U rows, then a rescan.  ew (nullable): b_i = fp32(alpha_i * w_i) (R33);
+// first: the weighted step 0 (b_i = w_i).
+__device__ uint32_t n2v_float_step(Node2vecPool& P, const float (&wf)[3], double* ftab, uint64_t U64,
+                                   const float* __restrict__ ew = nullptr, bool first = false) {
     const int lane = lane_id();
     const uint32_t n = P.n;
     const uint32_t nrows = (n + 31) >> 5;
@@ -628,7 +641,7 @@ __device__ uint32_t n2v_float_step(Node2vecPool& P, const float (&wf)[3], double
             P.template load_rows<U>(r0, key, b);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const double bv = key[u] == NONE ? 0.0 : static_cast<double>(wf[b[u]]);
+                const double bv = n2v_fbias(P, wf, ew, first, key[u], b[u], (r0 + u) * 32 + lane);
                 carry += __shfl_sync(FULL, warp_incl_scan_f64(bv), 31);
             }
         }
@@ -642,24 +655,24 @@ __device__ uint32_t n2v_float_step(Node2vecPool& P, const float (&wf)[3], double
     uint32_t c = 0;
     while (c + 1 < chunk && ftab[c] <= x) ++c;   // chunk containing x (clamped to the last)
     double base = c ? ftab[c - 1] : 0.0;
-    const uint32_t rbeg = c * m, rend = min(rbeg + m, nrows);
+    const uint32_t rbeg = c * m;
     P.seek(rbeg);
     uint32_t last_item = NONE;
-    for (uint32_t r0 = rbeg; r0 < rend; r0 += U) {
+    for (uint32_t r0 = rbeg; r0 < nrows; r0 += U) {   // past the chunk only through rounding
         uint32_t key[U], b[U];
         P.template load_rows<U>(r0, key, b);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const double bv = key[u] == NONE ? 0.0 : static_cast<double>(wf[b[u]]);
+            const double bv = n2v_fbias(P, wf, ew, first, key[u], b[u], (r0 + u) * 32 + lane);
             const double incl = warp_incl_scan_f64(bv) + base;
-            const unsigned hit = __ballot_sync(FULL, key[u] != NONE && incl > x);
-            const unsigned vm = __ballot_sync(FULL, key[u] != NONE);
+            const unsigned hit = __ballot_sync(FULL, bv > 0.0 && incl > x);
+            const unsigned vm = __ballot_sync(FULL, bv > 0.0);
             if (vm) last_item = __shfl_sync(FULL, key[u], 31 - __clz(vm));
             if (hit) return __shfl_sync(FULL, key[u], __ffs(hit) - 1);
             base = __shfl_sync(FULL, incl, 31);
         }
     }
-    return last_item;   // x >= T after rounding: the last candidate
+    return last_item;   // x >= T after rounding: the last positive candidate
 }
 
 // Integer node2vec step with an implicit CTPS.  The bias of u in N(v) takes only
@@ -1290,8 +1303,16 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 3) k_node2vec(N2vArgs na) {
                 const uint32_t d = static_cast<uint32_t>(__ldg(a.rp + cur + 1) - b0);
                 if (d > 0) {
                     const uint64_t U64 = draw_u64(a.key, inst, static_cast<uint32_t>(t), 0u, word3(PURPOSE_EDGE, 0, 0));
-                    if (prev == NONE) {
+                    if (prev == NONE && !(kFloat && na.ew)) {
                         nxt = __ldg(a.col + b0 + below(U64, d));     // step 0: uniform (R16)
+                    } else if (prev == NONE) {                       // weighted step 0: b = w (R33)
+                        Node2vecPool P;
+                        P.col = a.col; P.beg = static_cast<uint64_t>(b0); P.n = d;
+                        P.nprev = a.col; P.np = 0; P.prev = NONE;
+                        P.wp = 0; P.W = NONE; P.wvalid = false;
+                        P.w[0] = 0; P.w[1] = 1; P.w[2] = 2;
+                        nxt = n2v_float_step(P, na.wf, reinterpret_cast<double*>(tab), U64, na.ew, true);
+                        scanned += d;
                     } else {
                         const int64_t p0 = __ldg(a.rp + prev);
                         Node2vecPool P;
@@ -1302,7 +1323,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 3) k_node2vec(N2vArgs na) {
                         P.wp = 0; P.W = NONE; P.wvalid = false;
                         if constexpr (kFloat) {
                             P.w[0] = 0; P.w[1] = 1; P.w[2] = 2;
-                            nxt = n2v_float_step(P, na.wf, reinterpret_cast<double*>(tab), U64);
+                            nxt = n2v_float_step(P, na.wf, reinterpret_cast<double*>(tab), U64, na.ew);
                         } else {
                             P.w[0] = na.wint[0]; P.w[1] = na.wint[1]; P.w[2] = na.wint[2];
                             n2v_implicit_step(P, spec, reinterpret_cast<uint32_t*>(tab), U64, nxt);
@@ -1710,7 +1731,7 @@ static int walk_grid(const csaw_graph* g, int64_t n) {
 }
 
 bool walk_path_direct_ok(const csaw_graph* g, const csaw_bias& b) {
-    return !(b.kind == CSAW_BIAS_NODE2VEC && g->n2x_rec && !g->oom && n2v_integer_scale(b.p, b.q) != 0);
+    return !(b.kind == CSAW_BIAS_NODE2VEC && g->n2x_rec && !g->w && !g->oom && n2v_integer_scale(b.p, b.q) != 0);
 }
 
 csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds, int64_t n,
@@ -1787,7 +1808,9 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         na.wf[0] = static_cast<float>(1.0 / b.p);
         na.wf[1] = 1.0f;
         na.wf[2] = static_cast<float>(1.0 / b.q);
-        if (m && g->n2x_rec)
+        na.ew = g->w;   // weighted graph: b = alpha * w(e) (R33), always the float path
+        if (g->w) k_node2vec<true><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(na);
+        else if (m && g->n2x_rec)
             CSAW_TRY(launch_node2vec_index(g, d_seeds, static_cast<uint64_t>(n), length, static_cast<uint32_t>(base), key,
                                            d_path, static_cast<unsigned long long*>(cnt), na.wint[0], na.wint[1],
                                            na.wint[2], st));

@@ -200,3 +200,38 @@ def test_weight_errors(cfg1w):
     with pytest.raises(cs.CsawError) as e:
         cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, weights=torch.as_tensor(og.w), budget_bytes=1 << 20)
     assert e.value.status == 8
+
+
+# ---------------------------------------------------------------- weighted node2vec (R33)
+def test_weighted_node2vec_teacher_forced(mediumw):
+    """node2vec on a weighted graph: b = alpha * w(e), float path; every GPU transition
+    equals the oracle's step at the GPU's own (prev, v) unless the draw is within 1e-6 of a
+    boundary.  Integer-scale p, q (2, 0.5) take the float path too once the graph has weights."""
+    G, og, g = mediumw
+    seeds = instance_seeds(g, 600).numpy().view(np.uint32)
+    s = torch.as_tensor(seeds.view(np.int32)).to(DEV)
+    for p, q in ((2.0, 0.5), (np.pi, np.e)):
+        path = u32(cs.csaw_walk(G, cs.make_bias("node2vec", p=p, q=q), s, 30, rng_seed=12))
+        excused = 0
+        for w in range(0, 600, 3):
+            for t in range(30):
+                v = int(path[w][t])
+                if v == O.NONE32:
+                    assert path[w][t + 1] == O.NONE32
+                    continue
+                prev = O.NONE32 if t == 0 else int(path[w][t - 1])
+                ref, mg = O.node2vec_w_step(og, p, q, prev, v, w, t, 12)
+                if int(path[w][t + 1]) != ref:
+                    assert mg <= TOL, (p, q, w, t, mg)
+                    excused += 1
+        assert excused <= 2
+
+
+def test_weighted_node2vec_p1q1_equals_weight_walk(mediumw):
+    G, og, g = mediumw
+    s = instance_seeds(g, 256).to(DEV)
+    a = cs.csaw_walk(G, cs.make_bias("node2vec", p=1.0, q=1.0), s, 40, rng_seed=2)
+    b = cs.csaw_walk(G, cs.make_bias("weight"), s, 40, rng_seed=2)
+    # both are the edge-weight walk (b = 1.0f * w); the kernels sum in different orders, so
+    # they may differ only at boundary draws
+    assert (a != b).any(dim=1).sum().item() <= 2
