@@ -486,6 +486,7 @@ def main():
     seeds = seeds.to(dev).contiguous()
     n = seeds.shape[0]
     oom = cfg.oom_budget_bytes > 0 and not args.in_memory
+    torch.cuda.empty_cache()   # return the generator's transient buffers: the library allocates with cudaMalloc
     if oom:
         # out-of-memory mode (§5): the device holds only what the imposed budget allows
         del deg
@@ -771,6 +772,7 @@ def run_scan_path(cs, g, cfg, deg, seeds, base, rng_seeds, n, dev, local, stream
                 return n * cfg.length
         else:
             res = {}
+            out = None
 
             def sstep(seed):
                 res["r"] = cs.csaw_sample(Gs, bias, seeds, fanout=list(cfg.fanout), depth=cfg.depth,
@@ -799,6 +801,8 @@ def run_scan_path(cs, g, cfg, deg, seeds, base, rng_seeds, n, dev, local, stream
         ach = b / (hot_avg / 1000.0) / 1e9 if hot_avg > 0 else None
         kname = hot_kernel_name(cfg, False, False, 0, 0, False, False, eb)
         Gs.close()
+        del out, res
+        torch.cuda.empty_cache()
         return {"kernel": kname, "ms_per_step": sum(ts) / len(ts), "value": edges / (sum(ts) / 1000.0), "unit": UNIT,
                 "steps": len(ts), "alg_bytes_per_launch": b, "bytes_model": BYTES_MODEL[model],
                 "achieved_gbs": ach, "frac": (ach / peak) if ach else None, "hot_ms_per_launch": hot_avg,

@@ -62,14 +62,14 @@ def load(path):
 
 def main():
     src = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/prof"
-    rnd = sys.argv[2] if len(sys.argv) > 2 else "r01"
+    rnd = sys.argv[2] if len(sys.argv) > 2 else "r02"
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)
     out = [f"# {rnd} — ncu `--set full` summary, one hot-kernel launch per config", "",
            "Each row: `ncu --set full --clock-control none --import-source on --nvtx --nvtx-include csaw_step/ "
            "-k regex:<kernel> -c 1` around `bench.py --config <cfg> --steps 1 --warmup 1` "
-           "(cfg3: `scripts/prof_n2v.py 40 cache`, a 1/40 walker subset; its full bench launch is measured by a "
-           "metrics-only pass), exported with `ncu -i --page raw --csv` "
-           "(`scripts/gpu_prof_all.sh`, `scripts/ncu_summary.py`).  ncu times are cold-cache and serialised: "
+           "(`scripts/gpu_bench_all_r02.sh`; a @variant name adds the flags it names: cfg2@stream = --no-cache, "
+           "cfg5@inmem = --in-memory), exported with `ncu -i --page raw --csv` (`scripts/ncu_summary.py`); a "
+           "metrics-only pass (DRAM bytes + time) covers every launch of the timed step.  ncu times are cold-cache and serialised: "
            "the bench line's CUDA-event numbers are the measurement; these explain them.", "",
            f"DRAM GB/s is ncu DRAM bytes / ncu duration; fraction of the measured {peak:.1f} GB/s copy peak.", "",
            "| config | kernel | ncu ms | DRAM rd+wr | DRAM GB/s (frac) | L2 hit | L1 hit | B used/sector (ld) | warps active | issue active | regs | grid x block | top stalls (per issue) |",
@@ -92,10 +92,7 @@ def main():
                    f"{d.get('warps_active', 0):.1f} % | {d.get('issue_active', 0):.1f} % | {d.get('regs', 0):.0f} | "
                    f"{d.get('grid', 0):.0f} x {d.get('block', 0):.0f} | {st} |")
         key = cfg.replace("@", "_")   # e.g. cfg5_inmem, cfg2_scan (bench.py picks the key of its variant)
-        if cfg == "cfg3_subset40":
-            note = "1/40 walker subset (scripts/prof_n2v.py); per launch of that subset"
-        else:
-            note = "per launch of the bench's hot kernel (1 bench step)"
+        note = "per launch of the bench's hot kernel (1 bench step)"
         traffic[key] = {"kernel": d["kernel"], "dram_bytes_per_launch": int(dram), "ncu_ms": d["time"] * 1e3,
                         "f_dram": gbs / peak,
                         "l2_sector_eff": (d["bytes_per_sector"] / 32.0) if "bytes_per_sector" in d else None,
@@ -114,8 +111,18 @@ def main():
             if d.get("Metric Name") in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"):
                 k = (d.get("ID"), d.get("Kernel Name", "").split("(")[0])
                 per.setdefault(k, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+        # the hot kernel of the launch list = the longest launch (a list also holds the seed
+        # check, the fused copy, ...): only it updates the traffic record
+        hot = max(per.items(), key=lambda kv: kv[1].get("gpu__time_duration.sum", 0.0))[0] if per else None
         for (lid, kname), m in per.items():
             if "dram__bytes_read.sum" not in m:
+                continue
+            if (lid, kname) != hot:
+                t = m.get("gpu__time_duration.sum", 0.0) * 1e-9
+                dram = m["dram__bytes_read.sum"] + m.get("dram__bytes_write.sum", 0.0)
+                if t > 0:
+                    out.append(f"| {cfg} (metrics-only, full launch) | `{kname}` | {t * 1e3:.3f} | {dram / 1e9:.3f} GB | "
+                               f"{dram / t / 1e9:.0f} ({dram / t / 1e9 / peak:.3f}) | | | | | | | | |")
                 continue
             dram = m["dram__bytes_read.sum"] + m.get("dram__bytes_write.sum", 0.0)
             t = m.get("gpu__time_duration.sum", 0.0) * 1e-9
