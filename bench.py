@@ -175,6 +175,8 @@ BYTES_MODEL = {
     "sample_degree": "SURVEY §8(d) degree-biased pool: 16 + 8 d(v) per expanded vertex + 9 per emitted edge",
     "sample_layer": "SURVEY §8(d) layer: sum over levels and frontier vertices of 16 + 8 d(v) + 9 per edge",
     "sample_ff": "SURVEY §8(d) uniform / FF expanded vertex: 16 + 4 x + 9 x (x = its emitted edges)",
+    "sample_cached": "NEXT-1 sector model of the cached degree / layer pools: 16 (row_ptr pair) per expanded vertex + "
+                     "32 B x (2 + ceil(log2 d(src))) + 9 per emitted edge",
     "oom_host": "host link: partition / zero-copy bytes moved H2D per step (library counters)",
 }
 
@@ -203,7 +205,7 @@ def walk_alg_bytes(cfg, deg, out, cached, stream=False):
     return int(16 * nsteps + 8 * d.sum() + 4 * nsteps), "walk_degree_scan"
 
 
-def sample_alg_bytes(cfg, deg, seeds, offs, src, dst, dep):
+def sample_alg_bytes(cfg, deg, seeds, offs, src, dst, dep, cached=False):
     """§8(d) bytes of one sampling launch: the expanded vertices of every level are the
     seed (level 0) and the new vertices of the previous level (UPDATE's post-filter)."""
     n = seeds.numel()
@@ -234,6 +236,13 @@ def sample_alg_bytes(cfg, deg, seeds, offs, src, dst, dep):
         level_keys.append(key)
         visited = torch.cat([visited, key])
     tot = 0
+    if cached:   # NEXT-1 sector model: 16 B row_ptr pair per expanded vertex, 32 B x (2 + ceil(log2 d)) per pick
+        for key in level_keys:
+            tot += 16 * int(key.numel())
+        ds = deg[s64]
+        probes = _bit_length(torch.clamp(ds - 1, min=0))
+        tot += int(32 * (2 * m + probes.sum())) + 9 * m
+        return tot, "sample_cached"
     for key in level_keys:
         dv = deg[key % V]
         tot += int(16 * key.numel() + 8 * dv.sum())
@@ -620,7 +629,7 @@ def main():
             elif kind == "walk":
                 b, model = walk_alg_bytes(cfg, deg, out_dev, cached, bool(ginfo.get("edge_bias")))
             else:
-                b, model = sample_alg_bytes(cfg, deg, seeds, *last["r"])
+                b, model = sample_alg_bytes(cfg, deg, seeds, *last["r"], cached=cached)
             alg_bytes += b * k
 
     # ---------------- optional NCCL gather of the sampled outputs (not on the SEPS clock, G31)

@@ -109,3 +109,16 @@ def test_random_gather_context_reads_the_committed_measurement():
     c = bench.random_gather_context(500.0)
     assert c["random_gather_peak_gbs"] > 0
     assert abs(c["frac_of_random_gather_peak"] - 500.0 / c["random_gather_peak_gbs"]) < 1e-12
+
+
+def test_sample_bytes_cached_sector_model():
+    deg = torch.tensor([2, 4, 1, 3, 2], dtype=torch.int64)
+    seeds = torch.tensor([1, 3], dtype=torch.int32)
+    offs = torch.tensor([0, 4, 6], dtype=torch.int64)
+    src = torch.tensor([1, 1, 0, 2, 3, 4], dtype=torch.int32)
+    dst = torch.tensor([0, 2, 1, 4, 4, 3], dtype=torch.int32)
+    dep = torch.tensor([1, 1, 2, 2, 1, 2], dtype=torch.uint8)
+    # expanded vertices: 5 (as in the scan model); per pick ceil(log2 d(src)): src degrees
+    # 4, 4, 2, 1, 3, 2 -> 2, 2, 1, 0, 2, 1 = 8
+    b, m = bench.sample_alg_bytes(CONFIGS["cfg4_layer"], deg, seeds, offs, src, dst, dep, cached=True)
+    assert m == "sample_cached" and b == 16 * 5 + 32 * (2 * 6 + 8) + 9 * 6
