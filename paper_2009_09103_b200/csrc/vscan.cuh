@@ -194,6 +194,7 @@ __device__ __forceinline__ VCtps<E> vscan_build(const VPool<E>& P, typename VTra
     C.m = (C.m + VU - 1) / VU * VU;   // whole batches per chunk
     C.nch = (P.nrows + C.m - 1) / C.m;
     uint32_t npos = 0, last1 = 0;   // last1 = last positive index + 1 (0: none)
+    __syncwarp();   // the previous pool's readers of tab are done before it is rewritten
     // phase 1: chunk totals; warp gw takes the contiguous chunks [c0, c1), rows in batches
     // of VU (m is a multiple of VU).  Each lane accumulates its entries (left to right within its
     // 4, then row after row); one warp reduction per chunk -- a row costs a vector load and
