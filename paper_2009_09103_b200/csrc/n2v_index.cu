@@ -38,7 +38,7 @@
 #include "util.cuh"
 
 #ifndef N2X_SECTOR_PROBES
-#define N2X_SECTOR_PROBES 0   // search member positions 32 B sector by sector (A/B r02 cfg3: 11.1 ms, 14.2 GB requested; per-member binary search 10.1 ms, 18.4 GB)
+#define N2X_SECTOR_PROBES 0   // search member positions 32 B sector by sector (A/B r02 cfg3: 10.6-11.1 ms, 14.2 GB requested; per-member binary search 10.1 ms, 18.4 GB)
 #endif
 
 namespace csaw {
@@ -399,12 +399,14 @@ __device__ __forceinline__ uint32_t n2x_last_le(const uint32_t* __restrict__ I, 
         const int64_t gb = (static_cast<int64_t>(reinterpret_cast<uintptr_t>(g)) - static_cast<int64_t>(ia)) / 4;
         const uint32_t pv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
         const int64_t f0 = max(static_cast<int64_t>(l), gb), f1 = min(static_cast<int64_t>(h), gb + 8);   // inside [l, h)
-        uint32_t nt = 0, lastp = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int64_t jj = gb + k;
-            if (jj >= f0 && jj < f1 && n2x_S(wq, dq1, pv[k], static_cast<uint32_t>(jj), sub) <= x) { ++nt; lastp = pv[k]; }
+        // binary search of the true prefix inside the group (the predicate is monotone)
+        uint32_t a0 = static_cast<uint32_t>(f0 - gb), a1 = static_cast<uint32_t>(f1 - gb);
+        while (a0 < a1) {
+            const uint32_t k = (a0 + a1) >> 1;
+            if (n2x_S(wq, dq1, pv[k], static_cast<uint32_t>(gb + k), sub) <= x) a0 = k + 1; else a1 = k;
         }
+        const uint32_t nt = a0 - static_cast<uint32_t>(f0 - gb);
+        const uint32_t lastp = nt ? pv[a0 - 1] : 0;
         if (nt == static_cast<uint32_t>(f1 - f0)) {   // all true: the boundary is to the right
             l = static_cast<uint32_t>(f1);
             pos = lastp;
