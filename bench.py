@@ -941,7 +941,7 @@ def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads
         return "k_mdrw_oom_part" if oom else ("k_mdrw_fast" if cfg.pool_size <= 2048 else "k_mdrw")
     if cfg.workload == "node2vec":
         if n2x:
-            return "k_node2vec_idx"
+            return "k_node2vec_tma"
         return "k_node2vec_tri" if cached else "k_node2vec<int>"
     if oom:
         return "k_ns_select<1>" if cfg.bias == "degree" else "k_ns_select<0>"

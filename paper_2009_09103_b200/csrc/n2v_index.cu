@@ -656,6 +656,200 @@ __global__ void __launch_bounds__(256, N2X_K2_MINB) k_node2vec_idx2(N2xArgs a) {
     }
 }
 
+// ---- TMA variant: the records (and the probed member positions) are fetched by 1-D bulk
+// copies (cp.async.bulk, the Tensor Memory Accelerator) into shared memory and completed on an
+// mbarrier per group of 32 walkers.  Measured on this GPU, random 64 B records reach ~2.2 TB/s
+// through the TMA against ~0.95 TB/s through vector loads (profiles/r02_random_gather_tma.txt):
+// the bulk copies keep more bytes in flight per SM than the load unit's outstanding misses.
+// A warp runs N2X_TMA_K groups of 32 walkers round-robin (one group computes while the
+// others' copies are in flight; K = 1 measured best: the register budget of one group keeps
+// 32 warps per SM); the walkers of a group advance in lock step (same t).  The member-position
+// probes stay vector loads through L1 (hub lists are reused across walkers: 45 % L1 hits),
+// unless N2X_TMA_PROBES.
+#ifndef N2X_TMA
+#define N2X_TMA 1   // node2vec index walks through the TMA kernel (A/B r02 cfg3: 8.28 ms vs 10.14 ms with vector loads)
+#endif
+#ifndef N2X_TMA_K
+#define N2X_TMA_K 1   // A/B r02 cfg3: K = 1 8.28 ms; K = 2 9.54 ms (80 regs) / 13.6 ms (64 regs + stack)
+#endif
+#ifndef N2X_TMA_PROBES
+#define N2X_TMA_PROBES 0   // member positions by bulk copies too (else vector loads through L1)
+#endif
+#ifndef N2X_TMA_WARPS
+#define N2X_TMA_WARPS 8
+#endif
+__device__ __forceinline__ uint32_t n2x_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void n2x_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(n2x_smem(dst)), "l"(src), "r"(bytes), "r"(n2x_smem(bar)) : "memory");
+}
+__device__ __forceinline__ void n2x_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(n2x_smem(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void n2x_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(n2x_smem(bar)), "r"(parity) : "memory");
+}
+
+struct N2xGroup {           // one group of 32 walkers (per-lane fields)
+    uint64_t w;             // walker id (>= n: no walker on this lane)
+    uint64_t e;             // the entry the walker arrived by
+    N2xSearch q;            // the step in flight
+    int32_t t;              // step (group-uniform)
+    uint32_t parity;        // mbarrier phase
+    bool probing;           // waiting for member positions (else for records)
+    bool live;              // group-uniform: the group holds walkers
+};
+
+#ifndef N2X_TMA_MINB
+#define N2X_TMA_MINB 4   // <= 64 registers: 32 warps / SM (A/B r02 cfg3: 95 regs 11.45 ms, 64 regs 8.28, 48 regs + stack 9.14)
+#endif
+__global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_tma(N2xArgs a) {
+    constexpr int K = N2X_TMA_K;
+    __shared__ __align__(128) uint4 recs[N2X_TMA_WARPS][K][32][4];   // 64 B record per lane
+    __shared__ __align__(16) uint4 prb[N2X_TMA_WARPS][K][32];          // 16 B around the probed member
+    __shared__ __align__(8) uint64_t bars[N2X_TMA_WARPS][K];
+    const int lane = lane_id(), wib = threadIdx.x >> 5;
+    const uint32_t wq = a.wq, w1 = a.w1, wp = a.wp;
+    const int64_t dq1 = static_cast<int64_t>(wq) - w1, dqp = static_cast<int64_t>(wq) - wp;
+    unsigned long long steps = 0, probes_all = 0;
+    if (lane == 0)
+        for (int k = 0; k < K; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(n2x_smem(&bars[wib][k])));
+    __syncwarp();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * N2X_TMA_WARPS * K;   // groups in flight grid-wide
+    uint64_t next_group = (static_cast<uint64_t>(blockIdx.x) * N2X_TMA_WARPS + wib) * K;
+    N2xGroup G[K] = {};
+
+    auto issue_records = [&](int k) {
+        const bool me = G[k].w < a.n;
+        const uint32_t cnt = __popc(__ballot_sync(FULL, me));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // our reads of the slot before the copy
+        if (lane == 0) n2x_expect(&bars[wib][k], cnt * 64u);
+        __syncwarp();
+        if (me) n2x_bulk(&recs[wib][k][lane][0], a.rec + 4 * G[k].e, 64u, &bars[wib][k]);
+        G[k].probing = false;
+    };
+    // a new group: step 0 (uniform, R16) for each lane's walker, then its first record
+    auto start_group = [&](int k) {
+        for (;;) {
+            const uint64_t gi = next_group;
+            next_group += (gi % K == static_cast<uint64_t>(K - 1)) ? gstride - (K - 1) : 1;
+            const uint64_t w = gi * 32 + lane;
+            G[k].live = gi * 32 < a.n;
+            if (!G[k].live) return;
+            G[k].w = w < a.n ? w : ~0ull;
+            G[k].t = 1;
+            if (G[k].w != ~0ull) {
+                uint32_t* row = a.path + w * (static_cast<uint64_t>(a.L) + 1);
+                const uint32_t seed = a.seeds[w];
+                row[0] = seed;
+                const int64_t b0 = __ldg(a.rp + seed);
+                const uint32_t d0 = static_cast<uint32_t>(__ldg(a.rp + seed + 1) - b0);
+                if (a.L == 0) {
+                    G[k].w = ~0ull;
+                } else if (d0 == 0) {   // isolated seed: the walk ends (R20)
+                    for (int32_t t = 1; t <= a.L; ++t) row[t] = NONE;
+                    G[k].w = ~0ull;
+                } else {
+                    G[k].e = static_cast<uint64_t>(b0) +
+                             below(draw_u64(a.key, a.base + static_cast<uint32_t>(w), 0u, 0u, word3(PURPOSE_EDGE, 0, 0)), d0);
+                    ++steps;
+                }
+            }
+            if (__ballot_sync(FULL, G[k].w < a.n)) { issue_records(k); return; }
+            // nothing to fetch in this group (all isolated / L = 0): take the next one
+        }
+    };
+    // member-position probes of the lanes still searching; false if none
+    auto issue_probes = [&](int k) -> bool {
+        const bool me = G[k].w < a.n && G[k].q.l < G[k].q.h;
+        const unsigned m = __ballot_sync(FULL, me);
+        if (!m) return false;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (lane == 0) n2x_expect(&bars[wib][k], __popc(m) * 16u);
+        __syncwarp();
+        if (me) {
+            const uint32_t mid = (G[k].q.l + G[k].q.h) >> 1;
+            const uintptr_t ad = reinterpret_cast<uintptr_t>(G[k].q.I + mid) & ~static_cast<uintptr_t>(15);
+            n2x_bulk(&prb[wib][k][lane], reinterpret_cast<const void*>(ad), 16u, &bars[wib][k]);
+            ++probes_all;
+        }
+        G[k].probing = true;
+        return true;
+    };
+
+    for (int k = 0; k < K; ++k) { G[k].parity = 0; G[k].live = false; }
+    for (int k = 0; k < K; ++k) start_group(k);
+    for (;;) {
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (!G[k].live) continue;
+            any = true;
+            n2x_wait(&bars[wib][k], G[k].parity);
+            G[k].parity ^= 1u;
+            const bool me = G[k].w < a.n;
+            if (!G[k].probing) {   // records arrived: path entry, then the step's search
+                if (me) {
+                    const uint4 ra = recs[wib][k][lane][0], rb = recs[wib][k][lane][1];
+                    const uint4 rc = recs[wib][k][lane][2], rd = recs[wib][k][lane][3];
+                    uint32_t* row = a.path + G[k].w * (static_cast<uint64_t>(a.L) + 1);
+                    row[G[k].t] = rb.x;
+                    if (G[k].t < a.L) {
+                        const uint64_t U = draw_u64(a.key, a.base + static_cast<uint32_t>(G[k].w),
+                                                    static_cast<uint32_t>(G[k].t), 0u, word3(PURPOSE_EDGE, 0, 0));
+                        n2x_setup(a, ra, rb, rc, rd, U, dq1, dqp, G[k].q);
+                    }
+                }
+                if (G[k].t == a.L) {   // the group's walks are complete
+                    start_group(k);
+                    continue;
+                }
+            } else if (me && G[k].q.l < G[k].q.h) {   // a probe arrived
+                const uint32_t mid = (G[k].q.l + G[k].q.h) >> 1;
+                const uint4 pv = prb[wib][k][lane];
+                const uint32_t wsel = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(G[k].q.I + mid) >> 2) & 3u);
+                const uint32_t p = wsel == 0 ? pv.x : wsel == 1 ? pv.y : wsel == 2 ? pv.z : pv.w;
+                if (n2x_S(wq, dq1, p, mid, G[k].q.sub) <= G[k].q.x) { G[k].q.l = mid + 1; G[k].q.pos = p; }
+                else G[k].q.h = mid;
+            }
+            __syncwarp();
+#if N2X_TMA_PROBES
+            if (issue_probes(k)) continue;
+#else
+            if (me) {   // the member positions through L1 (hub lists are reused across walkers)
+                while (G[k].q.l < G[k].q.h) {
+                    const uint32_t mid = (G[k].q.l + G[k].q.h) >> 1;
+                    const uint32_t p = __ldg(G[k].q.I + mid);
+                    ++probes_all;
+                    if (n2x_S(wq, dq1, p, mid, G[k].q.sub) <= G[k].q.x) { G[k].q.l = mid + 1; G[k].q.pos = p; }
+                    else G[k].q.h = mid;
+                }
+            }
+#endif
+            // every lane's region is known: finish the step, fetch the next records
+            if (me) {
+                G[k].e = G[k].q.rs + n2x_finish(a, dq1, G[k].q);
+                ++steps;
+            }
+            ++G[k].t;
+            issue_records(k);
+        }
+        if (!any) break;
+    }
+    steps = warp_sum(steps);
+    probes_all = warp_sum(probes_all);
+    if (lane == 0 && steps) {
+        atomicAdd(a.counters + 1, steps);
+        atomicAdd(a.counters + 2, probes_all);
+        atomicAdd(a.counters + 3, 32ull * (2 * steps + probes_all) + 4ull * steps);
+    }
+}
+
 #ifndef N2X_K
 #define N2X_K 1   // walkers per thread (A/B r02 cfg3: K = 1 10.12 ms; K = 2 11.40 ms at 128 regs, 10.96 ms at 80 regs)
 #endif
@@ -665,7 +859,12 @@ csaw_status launch_node2vec_index(const csaw_graph* g, const uint32_t* seeds, ui
                                   uint32_t wq, cudaStream_t st) {
     N2xArgs a{g->row_ptr, g->n2x_rec, g->n2x_idx, seeds, n, L, base, key, path, counters, wp, w1, wq};
     const uint64_t resident = static_cast<uint64_t>(g->num_sms) * 2048;
-    if (N2X_K == 2) {
+    if (N2X_TMA) {
+        const uint64_t groups = (n + 31) / 32;
+        const uint64_t resident = static_cast<uint64_t>(g->num_sms) * (2048 / (N2X_TMA_WARPS * 32)) * N2X_TMA_WARPS * N2X_TMA_K;
+        const uint64_t blocks = (std::min<uint64_t>(groups, resident) + N2X_TMA_WARPS * N2X_TMA_K - 1) / (N2X_TMA_WARPS * N2X_TMA_K);
+        k_node2vec_tma<<<static_cast<int>(std::max<uint64_t>(1, blocks)), N2X_TMA_WARPS * 32, 0, st>>>(a);
+    } else if (N2X_K == 2) {
         const uint64_t threads = std::min<uint64_t>((n + 1) / 2, resident);
         const int grid = static_cast<int>(std::max<uint64_t>(1, (threads + 255) / 256));
         k_node2vec_idx2<<<grid, 256, 0, st>>>(a);

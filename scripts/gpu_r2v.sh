@@ -1,0 +1,13 @@
+#!/bin/bash
+# node2vec index walks through the TMA (bulk copies + mbarriers) vs vector loads
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 600 python -m pytest tests/test_gpu_n2v_index.py -x -q 2>&1 | tail -2
+for v in k1w4 k1w8 k1w16 k1w8m5 k1w8m6; do
+  if [ $v = default ]; then unset CSAW_LIB; else export CSAW_LIB=$PWD/exp/libcsaw_$v.so; fi
+  timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --scan-path-steps 0 > gpurun_out/r2v_$v.json 2>&1
+  python -c "
+import json
+for l in open('gpurun_out/r2v_$v.json'):
+    if l.startswith('{'): d=json.loads(l); r=d['roofline']; print('$v ms', round(d['ms_per_step'],3), 'frac', round(r['frac'],4))
+" || tail -3 gpurun_out/r2v_$v.json
+done

@@ -102,7 +102,7 @@ def test_walk_bytes_stream_model_and_scan_path_names():
     assert m == "walk_degree_stream" and b == 6 * 16 + 4 * 14 + 6 * 8
     assert bench.hot_kernel_name(CONFIGS["cfg2"], cached=False, eb=True) == "k_walk_vscan<uint32>"
     assert bench.hot_kernel_name(CONFIGS["cfg2"], cached=False) == "k_walk<degree>"
-    assert bench.hot_kernel_name(CONFIGS["cfg3"], n2x=True) == "k_node2vec_idx"
+    assert bench.hot_kernel_name(CONFIGS["cfg3"], n2x=True) == "k_node2vec_tma"
 
 
 def test_random_gather_context_reads_the_committed_measurement():
