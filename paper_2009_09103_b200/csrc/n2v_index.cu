@@ -507,9 +507,7 @@ __global__ void __launch_bounds__(256, N2X_MINB) k_node2vec_idx(N2xArgs a) {
     }
 }
 
-// ---- K = 2 walkers per thread, advanced in lock step: both walkers' record loads, and the
-// probes of both binary searches, are issued back to back -- twice the independent loads
-// in flight per thread (the kernel is bound by dependent DRAM latency).
+// ---- A step's search state (shared by the kernels below).
 struct N2xSearch {          // one walker's step in flight
     uint64_t rs;            // row start of v
     const uint32_t* I;      // member positions of the entry
@@ -565,95 +563,6 @@ __device__ __forceinline__ uint32_t n2x_finish(const N2xArgs& a, int64_t dq1, co
         return q.x < Sm + w1 ? q.pos : q.pos + 1 + static_cast<uint32_t>((q.x - Sm - w1) / wq);
     }
     return q.after ? q.ppos + 1 + static_cast<uint32_t>((q.x - q.Sp - wp) / wq) : static_cast<uint32_t>(q.x / wq);
-}
-
-#ifndef N2X_K2_MINB
-#define N2X_K2_MINB 2
-#endif
-__global__ void __launch_bounds__(256, N2X_K2_MINB) k_node2vec_idx2(N2xArgs a) {
-    const uint32_t wq = a.wq, w1 = a.w1, wp = a.wp;
-    const int64_t dq1 = static_cast<int64_t>(wq) - w1, dqp = static_cast<int64_t>(wq) - wp;
-    unsigned long long steps = 0, probes_all = 0;
-    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    for (uint64_t w0 = tid; w0 < a.n; w0 += 2 * nthreads) {
-        uint64_t e[2];
-        uint32_t* row[2];
-        uint32_t inst[2];
-        bool live[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const uint64_t w = w0 + k * nthreads;
-            live[k] = w < a.n;
-            e[k] = 0;
-            row[k] = a.path + w * (static_cast<uint64_t>(a.L) + 1);
-            inst[k] = a.base + static_cast<uint32_t>(w);
-            if (!live[k]) continue;
-            const uint32_t seed = a.seeds[w];
-            row[k][0] = seed;
-            if (a.L == 0) { live[k] = false; continue; }
-            const int64_t b0 = __ldg(a.rp + seed);
-            const uint32_t d0 = static_cast<uint32_t>(__ldg(a.rp + seed + 1) - b0);
-            if (d0 == 0) {   // isolated seed: the walk ends (R20)
-                for (int32_t t = 1; t <= a.L; ++t) row[k][t] = NONE;
-                live[k] = false;
-                continue;
-            }
-            e[k] = static_cast<uint64_t>(b0) + below(draw_u64(a.key, inst[k], 0u, 0u, word3(PURPOSE_EDGE, 0, 0)), d0);
-            ++steps;
-        }
-        for (int32_t t = 1; t <= a.L && (live[0] || live[1]); ++t) {
-            uint4 ra[2], rb[2], rc[2], rd[2];
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                if (live[k]) {
-                    ra[k] = __ldg(a.rec + 4 * e[k]); rb[k] = __ldg(a.rec + 4 * e[k] + 1);
-                    rc[k] = __ldg(a.rec + 4 * e[k] + 2); rd[k] = __ldg(a.rec + 4 * e[k] + 3);
-                }
-            }
-            N2xSearch q[2];
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                q[k].done = true; q[k].l = q[k].h = 0;
-                if (!live[k]) continue;
-                row[k][t] = rb[k].x;
-                if (t == a.L) continue;
-                const uint64_t U = draw_u64(a.key, inst[k], static_cast<uint32_t>(t), 0u, word3(PURPOSE_EDGE, 0, 0));
-                n2x_setup(a, ra[k], rb[k], rc[k], rd[k], U, dq1, dqp, q[k]);
-            }
-            if (t == a.L) break;
-            // both binary searches, one probe of each per round
-            while (q[0].l < q[0].h || q[1].l < q[1].h) {
-                uint32_t mid[2], p[2];
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    mid[k] = (q[k].l + q[k].h) >> 1;
-                    p[k] = q[k].l < q[k].h ? __ldg(q[k].I + mid[k]) : 0u;
-                }
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    if (q[k].l < q[k].h) {
-                        ++probes_all;
-                        if (n2x_S(wq, dq1, p[k], mid[k], q[k].sub) <= q[k].x) { q[k].l = mid[k] + 1; q[k].pos = p[k]; }
-                        else q[k].h = mid[k];
-                    }
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                if (!live[k]) continue;
-                e[k] = q[k].rs + n2x_finish(a, dq1, q[k]);
-                ++steps;
-            }
-        }
-    }
-    steps = warp_sum(steps);
-    probes_all = warp_sum(probes_all);
-    if (lane_id() == 0 && steps) {
-        atomicAdd(a.counters + 1, steps);
-        atomicAdd(a.counters + 2, probes_all);
-        atomicAdd(a.counters + 3, 32ull * (2 * steps + probes_all) + 4ull * steps);
-    }
 }
 
 // ---- TMA variant: the records (and the probed member positions) are fetched by 1-D bulk
@@ -918,138 +827,25 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
     }
 }
 
-// ---- Lane-independent variant: every lane runs its own walkers with its own mbarrier, so a
-// lane never waits for the slowest lane's probe chain (the group kernel above advances 32
-// walkers in lock step: a step costs the longest binary search of the group).  One loop
-// iteration: lanes whose record arrived (non-blocking mbarrier test) set up the step, lanes
-// searching issue one probe (vector load through L1), lanes done finish the step and request
-// the next record by a 64 B bulk copy.
-#ifndef N2X_LANE
-#define N2X_LANE 0   // A/B r02 cfg3: 16.0 ms (divergent per-lane state machine) vs 8.3 ms for the lock-step groups
-#endif
-#ifndef N2X_LANE_WARPS
-#define N2X_LANE_WARPS 8
-#endif
-#ifndef N2X_LANE_MINB
-#define N2X_LANE_MINB 4
-#endif
-__device__ __forceinline__ bool n2x_test(uint64_t* bar, uint32_t parity) {
-    uint32_t done;
-    asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(done) : "r"(n2x_smem(bar)), "r"(parity) : "memory");
-    return done != 0;
-}
-
-__global__ void __launch_bounds__(N2X_LANE_WARPS * 32, N2X_LANE_MINB) k_node2vec_lane(N2xArgs a) {
-    __shared__ __align__(128) uint4 recs[N2X_LANE_WARPS * 32][4];   // 64 B record per lane
-    __shared__ __align__(8) uint64_t bars[N2X_LANE_WARPS * 32];
-    const uint32_t wq = a.wq, w1 = a.w1, wp = a.wp;
-    const int64_t dq1 = static_cast<int64_t>(wq) - w1, dqp = static_cast<int64_t>(wq) - wp;
-    unsigned long long steps = 0, probes_all = 0;
-    const int tid = threadIdx.x;
-    uint64_t* bar = &bars[tid];
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(n2x_smem(bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + tid;   // this lane's walker
-    enum : int { WAIT = 0, PROBE = 1, FINISH = 2, START = 3, DONE = 4 };
-    int state = START;
-    uint32_t parity = 0;
-    int32_t t = 0;
-    uint64_t e = 0;
-    uint32_t* row = nullptr;
-    N2xSearch q;
-    q.l = q.h = 0;
-    auto fetch = [&]() {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        n2x_expect(bar, 64u);
-        n2x_bulk(&recs[tid][0], a.rec + 4 * e, 64u, bar);
-        state = WAIT;
-    };
-    for (;;) {
-        if (state == START) {   // the next walker: step 0 uniform (R16), then its first record
-            for (; w < a.n; w += nthreads) {
-                row = a.path + w * (static_cast<uint64_t>(a.L) + 1);
-                const uint32_t seed = a.seeds[w];
-                row[0] = seed;
-                if (a.L == 0) continue;
-                const int64_t b0 = __ldg(a.rp + seed);
-                const uint32_t d0 = static_cast<uint32_t>(__ldg(a.rp + seed + 1) - b0);
-                if (d0 == 0) {   // isolated seed: the walk ends (R20)
-                    for (int32_t tt = 1; tt <= a.L; ++tt) row[tt] = NONE;
-                    continue;
-                }
-                e = static_cast<uint64_t>(b0) + below(draw_u64(a.key, a.base + static_cast<uint32_t>(w), 0u, 0u,
-                                                               word3(PURPOSE_EDGE, 0, 0)), d0);
-                ++steps;
-                t = 1;
-                break;
-            }
-            if (w < a.n) fetch();
-            else state = DONE;
-        } else if (state == WAIT) {
-            if (n2x_test(bar, parity)) {
-                parity ^= 1u;
-                const uint4 ra = recs[tid][0], rb = recs[tid][1], rc = recs[tid][2], rd = recs[tid][3];
-                row[t] = rb.x;
-                if (t == a.L) {
-                    w += nthreads;
-                    state = START;
-                } else {
-                    const uint64_t U = draw_u64(a.key, a.base + static_cast<uint32_t>(w), static_cast<uint32_t>(t), 0u,
-                                                word3(PURPOSE_EDGE, 0, 0));
-                    n2x_setup(a, ra, rb, rc, rd, U, dq1, dqp, q);
-                    state = q.l < q.h ? PROBE : FINISH;
-                }
-            }
-        } else if (state == PROBE) {   // one probe per iteration
-            const uint32_t mid = (q.l + q.h) >> 1;
-            const uint32_t pv = __ldg(q.I + mid);
-            ++probes_all;
-            if (n2x_S(wq, dq1, pv, mid, q.sub) <= q.x) { q.l = mid + 1; q.pos = pv; }
-            else q.h = mid;
-            if (q.l >= q.h) state = FINISH;
-        }
-        if (state == FINISH) {
-            e = q.rs + n2x_finish(a, dq1, q);
-            ++steps;
-            ++t;
-            fetch();
-        }
-        if (__all_sync(FULL, state == DONE)) break;
-    }
-    steps = warp_sum(steps);
-    probes_all = warp_sum(probes_all);
-    if (lane_id() == 0 && steps) {
-        atomicAdd(a.counters + 1, steps);
-        atomicAdd(a.counters + 2, probes_all);
-        atomicAdd(a.counters + 3, 32ull * (2 * steps + probes_all) + 4ull * steps);
-    }
-}
-
-#ifndef N2X_K
-#define N2X_K 1   // walkers per thread (A/B r02 cfg3: K = 1 10.12 ms; K = 2 11.40 ms at 128 regs, 10.96 ms at 80 regs)
-#endif
 
 csaw_status launch_node2vec_index(const csaw_graph* g, const uint32_t* seeds, uint64_t n, int32_t L, uint32_t base,
                                   uint2 key, uint32_t* path, unsigned long long* counters, uint32_t wp, uint32_t w1,
                                   uint32_t wq, cudaStream_t st) {
     N2xArgs a{g->row_ptr, g->n2x_rec, g->n2x_idx, seeds, n, L, base, key, path, counters, wp, w1, wq};
     const uint64_t resident = static_cast<uint64_t>(g->num_sms) * 2048;
-    if (N2X_LANE) {
-        const uint64_t threads = std::min<uint64_t>(n, static_cast<uint64_t>(g->num_sms) * 1024);
-        const int grid = static_cast<int>(std::max<uint64_t>(1, (threads + N2X_LANE_WARPS * 32 - 1) / (N2X_LANE_WARPS * 32)));
-        k_node2vec_lane<<<grid, N2X_LANE_WARPS * 32, 0, st>>>(a);
-    } else if (N2X_TMA) {
+    if (N2X_TMA) {
+        // persistent: as many blocks as are resident at once (each warp then loops over groups)
+        static int per_sm = 0;
+        if (per_sm == 0 &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_node2vec_tma, N2X_TMA_WARPS * 32, 0) != cudaSuccess) {
+            cudaGetLastError();
+            per_sm = 1;
+        }
         const uint64_t groups = (n + 31) / 32;
-        const uint64_t resident = static_cast<uint64_t>(g->num_sms) * (2048 / (N2X_TMA_WARPS * 32)) * N2X_TMA_WARPS * N2X_TMA_K;
-        const uint64_t blocks = (std::min<uint64_t>(groups, resident) + N2X_TMA_WARPS * N2X_TMA_K - 1) / (N2X_TMA_WARPS * N2X_TMA_K);
+        const uint64_t per_block = N2X_TMA_WARPS * N2X_TMA_K;
+        const uint64_t blocks = std::min<uint64_t>((groups + per_block - 1) / per_block,
+                                                   static_cast<uint64_t>(g->num_sms) * std::max(per_sm, 1));
         k_node2vec_tma<<<static_cast<int>(std::max<uint64_t>(1, blocks)), N2X_TMA_WARPS * 32, 0, st>>>(a);
-    } else if (N2X_K == 2) {
-        const uint64_t threads = std::min<uint64_t>((n + 1) / 2, resident);
-        const int grid = static_cast<int>(std::max<uint64_t>(1, (threads + 255) / 256));
-        k_node2vec_idx2<<<grid, 256, 0, st>>>(a);
     } else {
         const uint64_t threads = std::min<uint64_t>(n, resident);
         const int grid = static_cast<int>(std::max<uint64_t>(1, (threads + 255) / 256));
