@@ -352,7 +352,7 @@ struct N2xArgs {
     uint32_t base;
     uint2 key;
     uint32_t* __restrict__ path;
-    unsigned long long* __restrict__ counters;   // [1] steps, [2] index probes, [3] sector bytes
+    unsigned long long* __restrict__ counters;   // [1] steps, [2] index probes, [3] sector bytes, [7] group ticket
     uint32_t wp, w1, wq;
 };
 
@@ -578,6 +578,9 @@ __device__ __forceinline__ uint32_t n2x_finish(const N2xArgs& a, int64_t dq1, co
 #ifndef N2X_TMA
 #define N2X_TMA 1   // node2vec index walks through the TMA kernel (A/B r02 cfg3: 8.28 ms vs 10.14 ms with vector loads)
 #endif
+#ifndef N2X_TICKET
+#define N2X_TICKET 1   // groups from a global atomic ticket (else a static grid-stride assignment)
+#endif
 #ifndef N2X_TMA_K
 #define N2X_TMA_K 1   // A/B r02 cfg3: K = 1 8.28 ms; K = 2 9.54 ms (80 regs) / 13.6 ms (64 regs + stack)
 #endif
@@ -641,8 +644,10 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
     __syncwarp();
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#if !N2X_TICKET
     const uint64_t gstride = static_cast<uint64_t>(gridDim.x) * N2X_TMA_WARPS * K;   // groups in flight grid-wide
     uint64_t next_group = (static_cast<uint64_t>(blockIdx.x) * N2X_TMA_WARPS + wib) * K;
+#endif
     N2xGroup G[K] = {};
 
     auto issue_records = [&](int k) {
@@ -657,8 +662,16 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
     // a new group: step 0 (uniform, R16) for each lane's walker, then its first record
     auto start_group = [&](int k) {
         for (;;) {
+#if N2X_TICKET
+            // the next group from a global ticket (a9: warps fetch work dynamically, so warps whose
+            // walkers sat on hubs do not leave the others waiting at the end)
+            unsigned long long tk = 0;
+            if (lane == 0) tk = atomicAdd(a.counters + 7, 1ull);
+            const uint64_t gi = __shfl_sync(FULL, tk, 0);
+#else
             const uint64_t gi = next_group;
             next_group += (gi % K == static_cast<uint64_t>(K - 1)) ? gstride - (K - 1) : 1;
+#endif
             const uint64_t w = gi * 32 + lane;
             G[k].live = gi * 32 < a.n;
             if (!G[k].live) return;
