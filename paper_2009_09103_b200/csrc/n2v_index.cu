@@ -114,13 +114,28 @@ __global__ void k_hub_cnt(const uint64_t* __restrict__ bits, uint32_t nhub, uint
 // (u -> v)).  The shorter list is walked in rows of 32; each entry's lower bound in the
 // longer list gives its position there.  Pass 1 (kList = false) writes the records'
 // C, ppos and mb; pass 2 lists the member positions into both edges' index ranges.
+// Edges are handed out in chunks of N2X_BUILD_CHUNK from a global ticket (hub-hub pairs cost
+// far more than the rest; a static split leaves a few warps with the heavy tail).
+#ifndef N2X_BUILD_CHUNK
+#define N2X_BUILD_CHUNK 16
+#endif
 template <bool kList>
 __global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col,
                       const uint32_t* __restrict__ src, int64_t E, uint4* __restrict__ rec,
-                      uint32_t* __restrict__ idx, unsigned int* __restrict__ asym, HubRank hr) {
+                      uint32_t* __restrict__ idx, unsigned int* __restrict__ asym, HubRank hr,
+                      unsigned long long* __restrict__ ticket) {
     const int lane = lane_id();
-    for (uint64_t e = global_warp_id(); e < static_cast<uint64_t>(E); e += total_warps()) {
-        const uint32_t v = src[e], u = col[e];
+    uint64_t e = 0, chunk_end = 0;
+    for (;;) {
+        if (e >= chunk_end) {
+            unsigned long long t0 = 0;
+            if (lane == 0) t0 = atomicAdd(ticket, static_cast<unsigned long long>(N2X_BUILD_CHUNK));
+            e = __shfl_sync(FULL, t0, 0);
+            chunk_end = e + N2X_BUILD_CHUNK;
+        }
+        if (e >= static_cast<uint64_t>(E)) break;
+        const uint64_t ecur = e++;
+        const uint32_t v = src[ecur], u = col[ecur];
         if (u == v) { if (lane == 0) atomicOr(asym, 1u); continue; }
         if (u < v) continue;
         const int64_t bv = rp[v], bu = rp[u];
@@ -135,7 +150,7 @@ __global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict
         uint64_t off_e = 0, off_r = 0;
         uint32_t C_all = 0;
         if (kList) {
-            const uint4 re = rec[4 * e], rr = rec[4 * r];
+            const uint4 re = rec[4 * ecur], rr = rec[4 * r];
             off_e = re.x | (static_cast<uint64_t>(re.y & 0xFFu) << 32);
             off_r = rr.x | (static_cast<uint64_t>(rr.y & 0xFFu) << 32);
             C_all = re.y >> 8;
@@ -174,7 +189,7 @@ __global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict
                         idx[off_e + rank] = pu;
                         idx[off_r + rank] = pv;
                     } else {           // inline in the records
-                        reinterpret_cast<uint32_t*>(rec + 4 * e + 2)[rank] = pu;
+                        reinterpret_cast<uint32_t*>(rec + 4 * ecur + 2)[rank] = pu;
                         reinterpret_cast<uint32_t*>(rec + 4 * r + 2)[rank] = pv;
                     }
                 }
@@ -187,9 +202,9 @@ __global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict
         }
         if (!kList && lane == 0) {
             // e = (v -> u): a walker at u that came from v; prev = v sits at position j of N(u)
-            rec[4 * e] = make_uint4(0u, cnt << 8, static_cast<uint32_t>(j), below_v);
+            rec[4 * ecur] = make_uint4(0u, cnt << 8, static_cast<uint32_t>(j), below_v);
             // r = (u -> v): a walker at v that came from u; prev = u sits at position e - bv of N(v)
-            rec[4 * r] = make_uint4(0u, cnt << 8, static_cast<uint32_t>(e - static_cast<uint64_t>(bv)), below_u);
+            rec[4 * r] = make_uint4(0u, cnt << 8, static_cast<uint32_t>(ecur - static_cast<uint64_t>(bv)), below_u);
         }
     }
 }
@@ -271,6 +286,7 @@ csaw_status build_n2v_index(csaw_graph* g, int blocks) {
         return drop();
     if (g->E >= (int64_t(1) << 40)) return drop();
     cudaMemset(asym, 0, sizeof(unsigned int));
+    cudaMemset(tot, 0, sizeof(unsigned long long));          // the count pass's edge ticket
     cudaMemset(g->n2x_rec, 0xFF, 4 * sizeof(uint4) * E);   // unused inline slots
     k_n2x_src<<<blocks, 256>>>(g->row_ptr, g->V, src);
     // hub rank bitmaps for the highest-degree rows (build scratch, freed below): at most
@@ -319,7 +335,7 @@ csaw_status build_n2v_index(csaw_graph* g, int blocks) {
             }
         }
     }
-    k_n2x<false><<<blocks * 4, 256>>>(g->row_ptr, g->col, src, E, g->n2x_rec, nullptr, asym, hr);
+    k_n2x<false><<<blocks * 4, 256>>>(g->row_ptr, g->col, src, E, g->n2x_rec, nullptr, asym, hr, tot);
     unsigned int h = 0;
     if (cudaMemcpy(&h, asym, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess || h)   // not symmetric
         return (free_hubs(), drop());
@@ -332,7 +348,8 @@ csaw_status build_n2v_index(csaw_graph* g, int blocks) {
     if (cudaMalloc(&g->n2x_idx, sizeof(uint32_t) * (total + 8)) != cudaSuccess) return (free_hubs(), drop());
     cudaMemset(g->n2x_idx + total, 0, sizeof(uint32_t) * 8);
     g->n2x_total = total;
-    k_n2x<true><<<blocks * 4, 256>>>(g->row_ptr, g->col, src, E, g->n2x_rec, g->n2x_idx, asym, hr);
+    cudaMemset(tot, 0, sizeof(unsigned long long));   // the list pass's edge ticket (the scan total was read)
+    k_n2x<true><<<blocks * 4, 256>>>(g->row_ptr, g->col, src, E, g->n2x_rec, g->n2x_idx, asym, hr, tot);
     k_n2x_dst<<<blocks * 4, 256>>>(g->row_ptr, g->col, E, g->n2x_idx, g->n2x_rec);
     const cudaError_t se = cudaDeviceSynchronize();
     free_hubs();
