@@ -35,6 +35,14 @@ struct WalkArgs {
     const uint64_t* __restrict__ ccache;          // chunk-total cache (degree pools), optional
 };
 
+// a9: warps fetch walkers from a global ticket (counters[7], zeroed per call),
+// so warps whose walkers sit on hubs do not hold up the end of the launch.
+__device__ __forceinline__ uint64_t walker_ticket(unsigned long long* c) {
+    unsigned long long t = 0;
+    if (lane_id() == 0) t = atomicAdd(c + 7, 1ull);
+    return __shfl_sync(FULL, t, 0);
+}
+
 // path[w][pi] buffered in lane (pi & 31); flushed when a 32-block completes.
 struct PathWriter {
     uint32_t* row;
@@ -59,7 +67,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_cached(WalkArgs a, 
                                                                   const uint64_t* __restrict__ nmp) {
     const int lane = lane_id();
     unsigned long long probes = 0, steps = 0;
-    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
         uint32_t cur = a.seeds[w];
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
         PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
@@ -119,7 +127,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_wix(WalkArgs a, con
     constexpr int NL = FL / 32;
     const int lane = lane_id();
     unsigned long long bytes = 0, steps = 0;
-    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
         uint32_t cur = a.seeds[w];
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
         PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
@@ -183,7 +191,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_head(WalkArgs a, co
     constexpr int NL = FL / 32;
     const uint32_t lane = static_cast<uint32_t>(lane_id());
     unsigned long long bytes = 0, steps = 0;
-    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
         uint32_t cur = a.seeds[w];
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
         PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
@@ -421,7 +429,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkArgs a) {
     uint64_t* tab = tab_all[threadIdx.x >> 5];
     const int lane = lane_id();
     unsigned long long scanned = 0, steps = 0;
-    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
         uint32_t cur = a.seeds[w];
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
         PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
@@ -461,7 +469,7 @@ template <int kKind>   // CSAW_BIAS_MH / RESTART / JUMP
 __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk_variant(WalkArgs a, uint64_t theta, int64_t V) {
     const int lane = lane_id();
     unsigned long long steps = 0;
-    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
         const uint32_t s0 = a.seeds[w];
         uint32_t cur = s0;
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
@@ -1235,7 +1243,7 @@ __global__ void __launch_bounds__(N2T_WARPS * 32, N2T_MINB) k_node2vec_tri(N2vAr
     const int lane = lane_id();
     N2tStats st;
     unsigned long long steps = 0;
-    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
         uint32_t cur = a.seeds[w], prev = NONE;
         uint64_t e_in = 0;   // CSR entry prev -> cur
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
@@ -1291,7 +1299,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 3) k_node2vec(N2vArgs na) {
     const WalkArgs& a = na.wa;
     const int lane = lane_id();
     unsigned long long scanned = 0, steps = 0;
-    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
         uint32_t cur = a.seeds[w], prev = NONE;
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
         PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
