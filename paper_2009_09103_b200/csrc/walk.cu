@@ -37,9 +37,9 @@ struct WalkArgs {
 
 // a9: warps fetch walkers from a global ticket (counters[7], zeroed per call),
 // so warps whose walkers sit on hubs do not hold up the end of the launch.
-__device__ __forceinline__ uint64_t walker_ticket(unsigned long long* c) {
+__device__ __forceinline__ uint64_t walker_ticket(unsigned long long* ticket) {
     unsigned long long t = 0;
-    if (lane_id() == 0) t = atomicAdd(c + 7, 1ull);
+    if (lane_id() == 0) t = atomicAdd(ticket, 1ull);
     return __shfl_sync(FULL, t, 0);
 }
 
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_cached(WalkArgs a, 
                                                                   const uint64_t* __restrict__ nmp) {
     const int lane = lane_id();
     unsigned long long probes = 0, steps = 0;
-    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
+    for (uint64_t w = walker_ticket(a.counters + 7); w < a.n; w = walker_ticket(a.counters + 7)) {
         uint32_t cur = a.seeds[w];
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
         PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_wix(WalkArgs a, con
     constexpr int NL = FL / 32;
     const int lane = lane_id();
     unsigned long long bytes = 0, steps = 0;
-    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
+    for (uint64_t w = walker_ticket(a.counters + 7); w < a.n; w = walker_ticket(a.counters + 7)) {
         uint32_t cur = a.seeds[w];
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
         PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_head(WalkArgs a, co
     constexpr int NL = FL / 32;
     const uint32_t lane = static_cast<uint32_t>(lane_id());
     unsigned long long bytes = 0, steps = 0;
-    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
+    for (uint64_t w = walker_ticket(a.counters + 7); w < a.n; w = walker_ticket(a.counters + 7)) {
         uint32_t cur = a.seeds[w];
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
         PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkArgs a) {
     uint64_t* tab = tab_all[threadIdx.x >> 5];
     const int lane = lane_id();
     unsigned long long scanned = 0, steps = 0;
-    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
+    for (uint64_t w = walker_ticket(a.counters + 7); w < a.n; w = walker_ticket(a.counters + 7)) {
         uint32_t cur = a.seeds[w];
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
         PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
@@ -469,7 +469,7 @@ template <int kKind>   // CSAW_BIAS_MH / RESTART / JUMP
 __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk_variant(WalkArgs a, uint64_t theta, int64_t V) {
     const int lane = lane_id();
     unsigned long long steps = 0;
-    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
+    for (uint64_t w = walker_ticket(a.counters + 7); w < a.n; w = walker_ticket(a.counters + 7)) {
         const uint32_t s0 = a.seeds[w];
         uint32_t cur = s0;
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
@@ -1243,7 +1243,7 @@ __global__ void __launch_bounds__(N2T_WARPS * 32, N2T_MINB) k_node2vec_tri(N2vAr
     const int lane = lane_id();
     N2tStats st;
     unsigned long long steps = 0;
-    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
+    for (uint64_t w = walker_ticket(a.counters + 7); w < a.n; w = walker_ticket(a.counters + 7)) {
         uint32_t cur = a.seeds[w], prev = NONE;
         uint64_t e_in = 0;   // CSR entry prev -> cur
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
@@ -1299,7 +1299,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 3) k_node2vec(N2vArgs na) {
     const WalkArgs& a = na.wa;
     const int lane = lane_id();
     unsigned long long scanned = 0, steps = 0;
-    for (uint64_t w = walker_ticket(a.counters); w < a.n; w = walker_ticket(a.counters)) {
+    for (uint64_t w = walker_ticket(a.counters + 7); w < a.n; w = walker_ticket(a.counters + 7)) {
         uint32_t cur = a.seeds[w], prev = NONE;
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
         PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
@@ -1389,6 +1389,7 @@ struct MdrwArgs {
     const uint32_t* __restrict__ colc;    // col entries [0, colc_n) on the device (k_mdrw_fast; = col in memory)
     uint64_t colc_n;
     const uint64_t* __restrict__ nmp;     // optional next-vertex metadata per entry (row << 24 | deg)
+    unsigned long long* ticket = nullptr; // k_mdrw_fast: instances from a global ticket (zeroed per call)
 };
 
 __global__ void k_mdrw(MdrwArgs a) {
@@ -1558,7 +1559,7 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 28 / MDRW_WARPS) k_mdrw_fast(
                                                                  uint64_t* __restrict__ prec, uint32_t* __restrict__ pvid) {
     const int lane = lane_id();
     const uint32_t m = static_cast<uint32_t>(a.m);
-    for (uint64_t w = global_warp_id(); w < a.n; w += total_warps()) {
+    for (uint64_t w = walker_ticket(a.ticket); w < a.n; w = walker_ticket(a.ticket)) {
         const uint32_t inst = a.base + static_cast<uint32_t>(w);
         uint4* ps = pool + w * m;
         uint64_t* pr = prec + w * m;
@@ -1852,6 +1853,7 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
             uint64_t* p8 = static_cast<uint64_t*>(pool);
             uint32_t* pv = static_cast<uint32_t*>(pvid);
             const bool narrow = g->max_deg < (int64_t(1) << 27);
+            ma.ticket = static_cast<unsigned long long*>(cnt) + 7;   // zeroed with the counters
             if (packed && narrow) k_mdrw_fast<true, true><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, p4, p8, pv);
             else if (packed) k_mdrw_fast<false, true><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, p4, p8, pv);
             else if (narrow) k_mdrw_fast<true, false><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, p4, p8, pv);
