@@ -83,6 +83,9 @@ def parse_args(argv=None):
                          "(NEXT-4(i), CSAW_GRAPH_OOM_PEER_STORE; with one GPU a same-device stand-in)")
     ap.add_argument("--oom-variant", default="partition", choices=["partition", "zerocopy"],
                     help="OOM configs: time the paper's partition scheduling (default) or the zero-copy mode")
+    ap.add_argument("--next-meta", action="store_true",
+                    help="MDRW: 8 B next-vertex metadata + col (CSAW_GRAPH_NEXT_META) instead of the 16 B "
+                         "next-vertex records (CSAW_GRAPH_NEXT_RECORD) (A/B)")
     return ap.parse_args(argv)
 
 
@@ -516,8 +519,8 @@ def main():
         use_eb = args.no_cache and not args.gather_bias and cfg.workload == "walk" and cfg.bias == "degree"
         wts = edge_weights(g, cfg.graph_seed) if cfg.bias == "weight" else None
         G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache, node2vec_tri=use_tri,
-                                 next_meta=use_meta, walk_index=use_cache, node2vec_index=use_tri, edge_bias=use_eb,
-                                 weights=wts)
+                                 next_meta=use_meta and args.next_meta, next_record=use_meta and not args.next_meta,
+                                 walk_index=use_cache, node2vec_index=use_tri, edge_bias=use_eb, weights=wts)
     ginfo = G.info()
     bias = bias_of(cs, cfg)
     stream = torch.cuda.current_stream(dev)

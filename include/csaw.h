@@ -176,6 +176,12 @@ typedef struct {
  * picked entry instead of one dependent row_ptr lookup later (degree walks on the u64
  * index, k_walk_cached, use it too).  Results are identical. */
 #define CSAW_GRAPH_NEXT_META 0x80u
+/* csaw_graph_opts.flags (in-memory graphs): next-vertex records nrec[e] = {u, deg(u),
+ * row_ptr[u] lo, hi} for u = col[e] (16 B per CSR entry, best-effort).  An MDRW step
+ * then reads the picked entry's vertex and the new pool vertex's row and
+ * VertexBias in one 16 B access instead of col[e] and nmp[e] (two random DRAM accesses).
+ * Takes precedence over CSAW_GRAPH_NEXT_META for MDRW.  Results are identical. */
+#define CSAW_GRAPH_NEXT_RECORD 0x800000u
 /* csaw_graph_opts.flags (in-memory graphs; built automatically in out-of-memory mode
  * when it fits the budget): chunk-total cache of the degree bias -- for every row of more
  * than 256 candidates, the chunk prefix sums of its CTPS (<= 256 chunks) and its count of

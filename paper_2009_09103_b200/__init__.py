@@ -100,6 +100,7 @@ CSAW_GRAPH_OOM_NO_CHUNK_CACHE = 0x20000
 CSAW_GRAPH_OOM_ZC_NO_PREFIX = 0x40000
 CSAW_GRAPH_MDRW_GENERIC = 0x80000
 CSAW_GRAPH_MDRW_ALT_RECORDS = 0x100000
+CSAW_GRAPH_NEXT_RECORD = 0x800000
 CSAW_GRAPH_OOM_PEER_STORE = 0x200000
 
 
@@ -108,7 +109,8 @@ def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, 
                       zerocopy: bool = False, batched_only: bool = False, oom_ws: bool = True,
                       oom_bal: bool = True, walk_index: bool = True, node2vec_tri: bool = False,
                       next_meta: bool = False, chunk_cache: bool = False, node2vec_index: bool = False,
-                      weights=None, edge_bias: bool = False, flags: int = 0, store_device=None) -> Graph:
+                      weights=None, edge_bias: bool = False, flags: int = 0, store_device=None,
+                      next_record: bool = False) -> Graph:
     """row_ptr int64[V+1], col_idx int32/uint32[E] (torch tensors, host or device).
     ctps_cache=True builds the static-bias CTPS cache (CSAW_GRAPH_CTPS_CACHE);
     zerocopy=True (with budget_bytes > 0) reads col_idx from pinned host memory;
@@ -122,7 +124,8 @@ def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, 
     edge weights (csaw_csr.weights, EdgeBias of the "weight" selector); edge_bias=True the materialised
     degree bias deg(col[e]) (CSAW_GRAPH_EDGE_BIAS: degree walks without the cache stream it); flags = extra
     CSAW_GRAPH_* bits (the variant selectors); store_device = GPU whose HBM holds the OOM partition store
-    (CSAW_GRAPH_OOM_PEER_STORE; == device: a same-device stand-in)."""
+    (CSAW_GRAPH_OOM_PEER_STORE; == device: a same-device stand-in); next_record=True the 16 B per-entry
+    next-vertex records MDRW reads instead of col + next_meta (CSAW_GRAPH_NEXT_RECORD)."""
     V = row_ptr.numel() - 1
     if weights is not None and weights.dtype != torch.float32:
         raise TypeError("weights must be float32")
@@ -134,6 +137,7 @@ def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, 
                           | (0 if walk_index else CSAW_GRAPH_NO_WALK_INDEX)
                           | (CSAW_GRAPH_N2V_TRI if node2vec_tri else 0)
                           | (CSAW_GRAPH_NEXT_META if next_meta else 0)
+                          | (CSAW_GRAPH_NEXT_RECORD if next_record else 0)
                           | (CSAW_GRAPH_CHUNK_CACHE if chunk_cache else 0)
                           | (CSAW_GRAPH_N2V_INDEX if node2vec_index else 0)
                           | (CSAW_GRAPH_EDGE_BIAS if edge_bias else 0) | int(flags)

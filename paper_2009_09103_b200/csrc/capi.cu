@@ -266,6 +266,18 @@ __global__ void k_build_nmp(const int64_t* __restrict__ rp, const uint32_t* __re
     }
 }
 
+// nrec[e] = {u, deg(u), row_ptr[u] lo, hi} for u = col[e]: the entry an MDRW step picks and
+// the new pool vertex's row and degree in one 16 B read (one random DRAM access, not two).
+__global__ void k_build_nrec(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col, int64_t E,
+                             uint4* __restrict__ nrec) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = col[e];
+        const int64_t a = rp[u];
+        nrec[e] = make_uint4(u, static_cast<uint32_t>(rp[u + 1] - a), static_cast<uint32_t>(a),
+                             static_cast<uint32_t>(static_cast<uint64_t>(a) >> 32));
+    }
+}
+
 __global__ void k_build_bt(const int64_t* __restrict__ rp, const uint64_t* __restrict__ cps,
                            const uint64_t* __restrict__ bt_off, int64_t V, uint64_t* __restrict__ bt) {
     const int lane = lane_id();
@@ -846,8 +858,16 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
     }
     if ((o.flags & CSAW_GRAPH_NEXT_META) && !g->oom && !g->nmp && g->max_deg < (1 << 24) && E < (int64_t(1) << 40) &&
         E > 0) {   // nmp[e] = row_ptr[col[e]] << 24 | deg(col[e]) (MDRW: k_mdrw_fast)
+        BuildTimer tm;
         if (cudaMalloc(&g->nmp, sizeof(uint64_t) * E) == cudaSuccess) k_build_nmp<<<blocks, 256>>>(g->row_ptr, g->col, E, g->nmp);
         else { cudaGetLastError(); g->nmp = nullptr; }
+        if (g->nmp) g->cache_build_ms += tm.ms();
+    }
+    if ((o.flags & CSAW_GRAPH_NEXT_RECORD) && !g->oom && !g->nrec && E > 0) {   // best-effort (MDRW: k_mdrw_fast)
+        BuildTimer tm;
+        if (cudaMalloc(&g->nrec, sizeof(uint4) * E) == cudaSuccess) k_build_nrec<<<blocks, 256>>>(g->row_ptr, g->col, E, g->nrec);
+        else { cudaGetLastError(); g->nrec = nullptr; }
+        if (g->nrec) g->cache_build_ms += tm.ms();
     }
     if ((o.flags & CSAW_GRAPH_N2V_INDEX) && !g->oom) {   // node2vec per-edge intersection index (n2v_index.cu)
         BuildTimer tm;
@@ -896,6 +916,7 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->bt) cudaFree(g->bt);
     if (g->bt_off) cudaFree(g->bt_off);
     if (g->nmp) cudaFree(g->nmp);
+    if (g->nrec) cudaFree(g->nrec);
     if (g->c32) cudaFree(g->c32);
     if (g->ccache) cudaFree(g->ccache);
     if (g->whead) cudaFree(g->whead);
@@ -944,6 +965,7 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
                         (g->tri ? static_cast<int64_t>(sizeof(uint32_t) * g->E) : 0) +
                         (g->n2x_rec ? static_cast<int64_t>(4 * sizeof(uint4) * g->E + sizeof(uint32_t) * g->n2x_total) : 0) +
                         (g->nmp ? static_cast<int64_t>(sizeof(uint64_t) * g->E) : 0) +
+                        (g->nrec ? static_cast<int64_t>(sizeof(uint4) * g->E) : 0) +
                         (g->w ? static_cast<int64_t>(sizeof(float) * (g->E + VSCAN_PAD)) : 0) +
                         (g->ebias ? static_cast<int64_t>(sizeof(uint32_t) * (g->E + VSCAN_PAD)) : 0) +
                         static_cast<int64_t>(sizeof(uint64_t) * g->ccache_entries);

@@ -54,6 +54,72 @@ __device__ __forceinline__ uint64_t draw_u64(uint2 key, uint32_t inst, uint32_t 
 // below(U, M) = floor(U * M / 2^64), uniform in [0, M).
 __device__ __forceinline__ uint64_t below(uint64_t U, uint64_t M) { return __umul64hi(U, M); }
 
+// ---------------------------------------------------------------- random single-word loads
+// An L2 miss of a lone 4 / 8 B load fetches a whole 128 B line (4 sectors) from DRAM by
+// default; the .L2::64B prefetch-size qualifier (SASS LDG.E.LTC64B) limits it to 64 B.
+// Measured on B200 (scripts/random_granule.cu, profiles/r02_random_granule.txt): 127 -> 64 DRAM
+// bytes per random 4 B read at the same ~35 G reads/s.  For the pointer-chasing loads whose
+// neighbours are never used (index probes, per-step entry + metadata reads).
+#ifndef CSAW_LD64B
+#define CSAW_LD64B 1
+#endif
+__device__ __forceinline__ uint32_t ld_rand_u32(const uint32_t* p) {
+#if CSAW_LD64B
+    uint32_t v;
+    asm("ld.global.nc.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ uint64_t ld_rand_u64(const uint64_t* p) {
+#if CSAW_LD64B
+    uint64_t v;
+    asm("ld.global.nc.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+// coherent (not .nc) variant for state the kernel itself writes
+__device__ __forceinline__ uint32_t ld_rand_rw_u32(const uint32_t* p) {
+#if CSAW_LD64B
+    uint32_t v;
+    asm volatile("ld.global.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+#else
+    return *p;
+#endif
+}
+// evict-first variants (read-once streams that should not displace reused state)
+__device__ __forceinline__ uint32_t ld_rand_cs_u32(const uint32_t* p) {
+#if CSAW_LD64B
+    uint32_t v;
+    asm("ld.global.cs.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+#else
+    return __ldcs(p);
+#endif
+}
+__device__ __forceinline__ uint64_t ld_rand_cs_u64(const uint64_t* p) {
+#if CSAW_LD64B
+    uint64_t v;
+    asm("ld.global.cs.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+#else
+    return __ldcs(p);
+#endif
+}
+__device__ __forceinline__ uint4 ld_rand_cs_v4(const uint4* p) {
+#if CSAW_LD64B
+    uint4 v;
+    asm("ld.global.cs.L2::64B.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+#else
+    return __ldcs(p);
+#endif
+}
+
 // ---------------------------------------------------------------- warp helpers
 __device__ __forceinline__ uint64_t warp_incl_scan(uint64_t v) {
     const int lane = lane_id();

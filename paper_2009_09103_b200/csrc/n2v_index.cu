@@ -828,7 +828,8 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
 #if N2X_TMA_GAP
             if (!G[k].gapping && issue_gap(k)) continue;
 #endif
-            if (me) {   // the member positions through L1 (hub lists are reused across walkers)
+            if (me) {   // the member positions through L1 (hub lists are reused across walkers; whole
+                        // 128 B lines from DRAM: .L2::64B measured 7.81 vs 7.54 ms on cfg3)
                 while (G[k].q.l < G[k].q.h) {
                     const uint32_t mid = (G[k].q.l + G[k].q.h) >> 1;
                     const uint32_t p = __ldg(G[k].q.I + mid);

@@ -1390,6 +1390,7 @@ struct MdrwArgs {
     uint64_t colc_n;
     const uint64_t* __restrict__ nmp;     // optional next-vertex metadata per entry (row << 24 | deg)
     unsigned long long* ticket = nullptr; // k_mdrw_fast: instances from a global ticket (zeroed per call)
+    const uint4* __restrict__ nrc = nullptr;   // optional next-vertex records {u, deg, row lo, hi} (k_mdrw_fast)
 };
 
 __global__ void k_mdrw(MdrwArgs a) {
@@ -1536,6 +1537,9 @@ __device__ __forceinline__ void st_keep(uint64_t* p, uint64_t v, uint64_t pol) {
     *p = v;
 #endif
 }
+#ifndef MDRW_PVV_64B
+#define MDRW_PVV_64B 1       // the slot's vertex id (output only) with a 64 B L2 fetch
+#endif
 #ifndef MDRW_STREAM_HINT
 #define MDRW_STREAM_HINT 1   // evict-first loads for the per-step random entry + metadata
 #endif   // warps per block; 28 warps / SM at 72 registers
@@ -1643,7 +1647,11 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 28 / MDRW_WARPS) k_mdrw_fast(
                 uint64_t rb;
                 if constexpr (kPacked) {
                     rb = __shfl_sync(FULL, rec, fl) >> 24;
+#if MDRW_PVV_64B
+                    v = ld_rand_rw_u32(pvv + bsel * 32 + fl);   // for the output only (not on the next step's chain)
+#else
                     v = pvv[bsel * 32 + fl];   // for the output only (not on the next step's chain)
+#endif
                 } else {
                     v = __shfl_sync(FULL, e.x, fl);
                     rb = static_cast<uint64_t>(__shfl_sync(FULL, e.w, fl)) << 32 | __shfl_sync(FULL, e.z, fl);
@@ -1657,13 +1665,17 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 28 / MDRW_WARPS) k_mdrw_fast(
                     uxb = draw_u64(a.key, inst, static_cast<uint32_t>(t + 1 + lane), 0u, word3(PURPOSE_VERTEX, 0, 0));
                     ueb = draw_u64(a.key, inst, static_cast<uint32_t>(t + 1 + lane), 0u, word3(PURPOSE_EDGE, 0, 0));
                 }
-                if (a.nmp) {   // the new vertex's row and degree come with the entry (no dependent lookup)
+                uint4 nr = make_uint4(0, 0, 0, 0);
+                if (a.nrc) {   // the entry, the new vertex's row and its degree in one 16 B read
+                    nr = ld_rand_cs_v4(a.nrc + ei);
+                    u = nr.x;
+                } else if (a.nmp) {   // the new vertex's row and degree come with the entry (no dependent lookup)
 #if MDRW_STREAM_HINT == 2
                     asm volatile("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(mt) : "l"(a.nmp + ei), "l"(pol_ef));
                     asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(u) : "l"(a.col + ei), "l"(pol_ef));
 #elif MDRW_STREAM_HINT
-                    mt = __ldcs(a.nmp + ei);   // read once: evict first, keep the pool state in L2
-                    u = __ldcs(a.col + ei);
+                    mt = ld_rand_cs_u64(a.nmp + ei);   // read once: evict first, keep the pool state in L2
+                    u = ld_rand_cs_u32(a.col + ei);
 #else
                     mt = __ldg(a.nmp + ei);
                     u = __ldg(a.col + ei);
@@ -1681,7 +1693,11 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 28 / MDRW_WARPS) k_mdrw_fast(
                 } else {
                     gsel = NONE;
                 }
-                if (a.nmp) {
+                if (a.nrc) {
+                    ru = static_cast<int64_t>(static_cast<uint64_t>(nr.w) << 32 | nr.z);
+                    du = nr.y;
+                    mt = static_cast<uint64_t>(ru) << 24 | du;
+                } else if (a.nmp) {
                     ru = static_cast<int64_t>(mt >> 24);
                     du = static_cast<uint32_t>(mt & 0xFFFFFFu);
                 } else {
@@ -1854,6 +1870,7 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
             uint32_t* pv = static_cast<uint32_t*>(pvid);
             const bool narrow = g->max_deg < (int64_t(1) << 27);
             ma.ticket = static_cast<unsigned long long*>(cnt) + 7;   // zeroed with the counters
+            ma.nrc = g->col ? g->nrec : nullptr;
             if (packed && narrow) k_mdrw_fast<true, true><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, p4, p8, pv);
             else if (packed) k_mdrw_fast<false, true><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, p4, p8, pv);
             else if (narrow) k_mdrw_fast<true, false><<<mg, MDRW_WARPS * 32, 0, st>>>(ma, p4, p8, pv);

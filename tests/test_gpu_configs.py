@@ -232,8 +232,9 @@ def test_cfg5_mdrw_full(cfg5_graph):
     g, og, host = cfg5_graph
     seeds = mdrw_seeds(g, cfg.n_instances, cfg.pool_size).to(DEV)
     sv = u32(seeds)
-    Gm = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, next_meta=True)     # in-memory bench launch
+    Gm = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, next_record=True)   # in-memory bench launch
     Gp = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0)                     # plain in-memory
+    Gn = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, next_meta=True)     # 8 B metadata + col
     bias = cs.make_bias("mdrw")
     inmem = {}
     for seed in SEEDS:
@@ -246,8 +247,11 @@ def test_cfg5_mdrw_full(cfg5_graph):
         assert first_mismatch(em, ref) is None, f"seed {seed}: instance {first_mismatch(em, ref)}"
         assert first_mismatch(ep, ref) is None, f"seed {seed}: plain instance {first_mismatch(ep, ref)}"
         check_edges_exist(og, em[:, :, 0].ravel(), em[:, :, 1].ravel())
+        if seed == SEEDS[0]:
+            en = u32(cs.csaw_walk(Gn, bias, seeds, cfg.length, rng_seed=seed))
+            assert first_mismatch(en, em) is None, "next_meta vs next_record"
         inmem[seed] = em
-    release(Gm, Gp)
+    release(Gm, Gp, Gn)
     # the config's out-of-memory launches under the 8 GB budget: identical on 100 %
     Gz = oom_graph(host, cfg, zerocopy=True)
     assert Gz.info()["oom_mode"] == 1 and Gz.info()["device_bytes"] <= cfg.oom_budget_bytes

@@ -292,7 +292,8 @@ def test_mdrw_pool_sizes(medium, m, n, L):
 
 def test_mdrw_next_meta(medium):
     """CSAW_GRAPH_NEXT_META: the new pool vertex's row and degree come with the picked CSR
-    entry (nmp) -- same edges as without it and as the oracle."""
+    entry (nmp); CSAW_GRAPH_NEXT_RECORD: entry, row and degree in one 16 B record (packed and
+    16 B slot records) -- same edges as without them and as the oracle."""
     _, og2, g2 = medium
     Gm = cs.csaw_graph_create(g2.row_ptr.to(DEV), g2.col_idx.to(DEV), next_meta=True)
     assert Gm.info()["device_bytes"] >= 8 * g2.col_idx.numel()
@@ -302,6 +303,12 @@ def test_mdrw_next_meta(medium):
         G0, _, _ = medium
         e0 = u32(cs.csaw_walk(G0, cs.make_bias("mdrw"), torch.as_tensor(s.view(np.int32)).to(DEV), L, rng_seed=17))
         assert np.array_equal(e, e0)
+        for fl in (0, cs.CSAW_GRAPH_MDRW_ALT_RECORDS):   # 16 B next-vertex records (CSAW_GRAPH_NEXT_RECORD)
+            Gr = cs.csaw_graph_create(g2.row_ptr.to(DEV), g2.col_idx.to(DEV), next_record=True, flags=fl)
+            assert Gr.info()["device_bytes"] >= 16 * g2.col_idx.numel()
+            er = u32(cs.csaw_walk(Gr, cs.make_bias("mdrw"), torch.as_tensor(s.view(np.int32)).to(DEV), L, rng_seed=17))
+            Gr.close()
+            assert np.array_equal(e, er), hex(fl)
     Gm.close()
 
 
