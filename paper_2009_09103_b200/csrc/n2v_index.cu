@@ -370,13 +370,28 @@ struct N2xArgs {
     uint2 key;
     uint32_t* __restrict__ path;
     unsigned long long* __restrict__ counters;   // [1] steps, [2] index probes, [3] sector bytes, [7] group ticket
-    uint32_t wp, w1, wq;
+    uint32_t wp, w1, wq;    // integer biases (R16), each < 2^30 (checked by the launcher)
+    int32_t wq_shift;       // log2(wq) if wq is a power of two, else -1
+    double wq_inv;          // 1 / wq (quotients of dividends < 2^53, corrected by one step)
 };
+
+// floor(a / wq) for 0 <= a < 2^53 without the 64-bit division subroutine: a shift when wq is a
+// power of two (p = 2, q = 0.5 gives wq = 4), else a double-precision estimate corrected by one
+__device__ __forceinline__ uint32_t n2x_div(int64_t a, const N2xArgs& A) {
+    if (A.wq_shift >= 0) return static_cast<uint32_t>(a >> A.wq_shift);
+    int64_t q = static_cast<int64_t>(static_cast<double>(a) * A.wq_inv);
+    const int64_t r = a - q * static_cast<int64_t>(A.wq);
+    if (r < 0) --q;
+    else if (r >= static_cast<int64_t>(A.wq)) ++q;
+    return static_cast<uint32_t>(q);
+}
 
 // S(j, p) = wq p - dq1 j - sub, exact in int64 (wq < 2^32, p, j < 2^24; dq1 may be negative):
 // the CTPS at the member of rank j and position p (sub = wq - wp after prev, else 0)
 __device__ __forceinline__ int64_t n2x_S(uint32_t wq, int64_t dq1, uint32_t p, uint32_t j, int64_t sub) {
-    return static_cast<int64_t>(static_cast<uint64_t>(wq) * p) - dq1 * static_cast<int64_t>(j) - sub;
+    // |dq1| < 2^30 and j < 2^24: 32 x 32 -> 64-bit products (IMAD.WIDE), no 64-bit multiply
+    return static_cast<int64_t>(static_cast<uint64_t>(wq) * p) -
+           static_cast<int64_t>(static_cast<int32_t>(dq1)) * static_cast<int64_t>(static_cast<int32_t>(j)) - sub;
 }
 
 // Last member rank j in [lo, hi) with S(j, I[j]) <= x (S increases with j: the predicate
@@ -503,9 +518,9 @@ __global__ void __launch_bounds__(256, N2X_MINB) k_node2vec_idx(N2xArgs a) {
                                                pos);
                 if (found) {
                     const int64_t Sm = n2x_S(wq, dq1, pos, j, sub);
-                    s = x < Sm + w1 ? pos : pos + 1 + static_cast<uint32_t>((x - Sm - w1) / wq);
+                    s = x < Sm + w1 ? pos : pos + 1 + n2x_div(x - Sm - w1, a);
                 } else {
-                    s = after ? ppos + 1 + static_cast<uint32_t>((x - Sp - wp) / wq) : static_cast<uint32_t>(x / wq);
+                    s = after ? ppos + 1 + n2x_div(x - Sp - wp, a) : n2x_div(x, a);
                 }
             }
             probes_all += probes;
@@ -577,9 +592,9 @@ __device__ __forceinline__ uint32_t n2x_finish(const N2xArgs& a, int64_t dq1, co
     const uint32_t wq = a.wq, w1 = a.w1, wp = a.wp;
     if (q.l > q.lo) {
         const int64_t Sm = n2x_S(wq, dq1, q.pos, q.l - 1, q.sub);
-        return q.x < Sm + w1 ? q.pos : q.pos + 1 + static_cast<uint32_t>((q.x - Sm - w1) / wq);
+        return q.x < Sm + w1 ? q.pos : q.pos + 1 + n2x_div(q.x - Sm - w1, a);
     }
-    return q.after ? q.ppos + 1 + static_cast<uint32_t>((q.x - q.Sp - wp) / wq) : static_cast<uint32_t>(q.x / wq);
+    return q.after ? q.ppos + 1 + n2x_div(q.x - q.Sp - wp, a) : n2x_div(q.x, a);
 }
 
 // ---- TMA variant: the records (and the probed member positions) are fetched by 1-D bulk
@@ -613,6 +628,9 @@ __device__ __forceinline__ uint32_t n2x_finish(const N2xArgs& a, int64_t dq1, co
 #ifndef N2X_TMA_WARPS
 #define N2X_TMA_WARPS 8
 #endif
+#ifndef N2X_SMEM_STRIDE
+#define N2X_SMEM_STRIDE 5   // uint4 per lane slot of the staged records (4 = unpadded)
+#endif
 __device__ __forceinline__ uint32_t n2x_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void n2x_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -644,7 +662,10 @@ struct N2xGroup {           // one group of 32 walkers (per-lane fields)
 #endif
 __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_tma(N2xArgs a) {
     constexpr int K = N2X_TMA_K;
-    __shared__ __align__(128) uint4 recs[N2X_TMA_WARPS][K][32][4];   // 64 B record per lane
+    // 64 B record per lane at an 80 B stride: a warp's uint4 reads of the records then hit 8
+    // distinct 16 B bank groups per 8-lane phase (conflict-free) -- at a 64 B stride every
+    // phase was a 4-way conflict (ncu r02: 16-way on average, 75 % excessive shared wavefronts)
+    __shared__ __align__(128) uint4 recs[N2X_TMA_WARPS][K][32][N2X_SMEM_STRIDE];
 #if N2X_TMA_PROBES
     __shared__ __align__(16) uint4 prb[N2X_TMA_WARPS][K][32];          // 16 B around the probed member
 #endif
@@ -862,7 +883,11 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
 csaw_status launch_node2vec_index(const csaw_graph* g, const uint32_t* seeds, uint64_t n, int32_t L, uint32_t base,
                                   uint2 key, uint32_t* path, unsigned long long* counters, uint32_t wp, uint32_t w1,
                                   uint32_t wq, cudaStream_t st) {
-    N2xArgs a{g->row_ptr, g->n2x_rec, g->n2x_idx, seeds, n, L, base, key, path, counters, wp, w1, wq};
+    int32_t sh = -1;
+    for (int b = 0; b < 31; ++b)
+        if (wq == (1u << b)) sh = b;
+    N2xArgs a{g->row_ptr, g->n2x_rec, g->n2x_idx, seeds, n, L, base, key, path, counters, wp, w1, wq, sh,
+              1.0 / static_cast<double>(wq)};
     const uint64_t resident = static_cast<uint64_t>(g->num_sms) * 2048;
     if (N2X_TMA) {
         // persistent: as many blocks as are resident at once (each warp then loops over groups)

@@ -1835,7 +1835,7 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         na.wf[2] = static_cast<float>(1.0 / b.q);
         na.ew = g->w;   // weighted graph: b = alpha * w(e) (R33), always the float path
         if (g->w) k_node2vec<true><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(na);
-        else if (m && g->n2x_rec)
+        else if (m && g->n2x_rec && na.wint[0] < (1u << 30) && na.wint[1] < (1u << 30) && na.wint[2] < (1u << 30))
             CSAW_TRY(launch_node2vec_index(g, d_seeds, static_cast<uint64_t>(n), length, static_cast<uint32_t>(base), key,
                                            d_path, static_cast<unsigned long long*>(cnt), na.wint[0], na.wint[1],
                                            na.wint[2], st));

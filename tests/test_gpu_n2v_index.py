@@ -32,7 +32,9 @@ def medium():
     return G, og, g
 
 
-@pytest.mark.parametrize("p,q", [(2.0, 0.5), (0.25, 4.0), (1.0, 1.0), (0.5, 2.0), (4.0, 1.0)])
+# integer scales (R16): (wp, w1, wq) = (1, 2, 4), (16, 4, 1), (1, 1, 1), (4, 2, 1), (1, 4, 4) and, with a wq
+# that is not a power of two (the quotient by fp64 estimate + correction, not a shift), (1, 3, 3), (1, 5, 10)
+@pytest.mark.parametrize("p,q", [(2.0, 0.5), (0.25, 4.0), (1.0, 1.0), (0.5, 2.0), (4.0, 1.0), (3.0, 1.0), (5.0, 0.5)])
 def test_index_medium(medium, p, q):
     G, og, g = medium
     seeds = instance_seeds(g, 256, set_id=4).numpy()
@@ -57,6 +59,7 @@ def test_index_hub():
     seeds = np.array([0, 1, 0, 1, 5, 0, 1, 17, 299_999, 20_001], dtype=np.uint32)
     check_walk(G, og, "node2vec", seeds, 30, rng_seed=9, p=2.0, q=0.5)
     check_walk(G, og, "node2vec", seeds, 30, rng_seed=10, p=0.25, q=4.0)
+    check_walk(G, og, "node2vec", seeds, 30, rng_seed=11, p=5.0, q=0.5)
     G.close()
 
 
