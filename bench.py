@@ -171,8 +171,8 @@ BYTES_MODEL = {
                           "weights, streamed) + 4 (the pick's col) + 4 (path)",
     "node2vec": "SURVEY §8(d) node2vec step: 16 + 4 d(v) + 4 (N(prev) carried from the previous step); "
                 "step 0 uniform: 16 + 4 + 4",
-    "node2vec_index": "NEXT-1-style sector model of the node2vec intersection index: 32 B sectors x (the 64 B "
-                      "record of the entry the walker arrived by (2 sectors) + the binary-search probes between its "
+    "node2vec_index": "NEXT-1-style sector model of the node2vec intersection index: 32 B sectors x (the 128 B "
+                      "record of the entry the walker arrived by (4 sectors) + the binary-search probes between its "
                       "splitters) per step + 4 (path); probes counted in the kernel",
     "mdrw": "SURVEY §8(d) MDRW step: 16 (row_ptr v) + 4 (col) + 4 (deg u) + 8 (edge out) = 32",
     "sample_degree": "SURVEY §8(d) degree-biased pool: 16 + 8 d(v) per expanded vertex + 9 per emitted edge",

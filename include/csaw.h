@@ -192,8 +192,9 @@ typedef struct {
 /* csaw_graph_opts.flags (in-memory graphs with sorted rows, max degree < 2^24; used only
  * if the graph is symmetric): node2vec per-edge intersection index.  For every CSR entry
  * e = (prev -> v): the count C of common neighbours N(v) ∩ N(prev), the position of prev in
- * N(v), and the ascending positions in N(v) of the common neighbours (16 B per entry + 4 B
- * per common neighbour pair; ~53 GB for the cfg3 graph).  Integer node2vec walks
+ * N(v), and the ascending positions in N(v) of the common neighbours (a 128 B record per
+ * entry with up to 24 of them inline, + 4 B per common-neighbour pair beyond; ~66 GB of
+ * device memory with the cfg3 graph).  Integer node2vec walks
  * (R16) then binary-search those positions for the region of the draw (the CTPS
  * is piecewise linear between them) instead of merging N(v) with N(prev): O(log C) reads
  * per step.  Picks are identical.  Best-effort: if the index does not fit, the graph is

@@ -963,7 +963,7 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
                         (g->wix_leaf ? static_cast<int64_t>(sizeof(uint32_t) * (2 * g->wleaf_entries + g->winn_entries) + sizeof(uint4) * g->V) : 0) +
                         (g->whead ? static_cast<int64_t>(sizeof(uint32_t)) * WIX_HEAD_WORDS * g->V : 0) +
                         (g->tri ? static_cast<int64_t>(sizeof(uint32_t) * g->E) : 0) +
-                        (g->n2x_rec ? static_cast<int64_t>(4 * sizeof(uint4) * g->E + sizeof(uint32_t) * g->n2x_total) : 0) +
+                        (g->n2x_rec ? static_cast<int64_t>(N2X_U4 * sizeof(uint4) * g->E + sizeof(uint32_t) * g->n2x_total) : 0) +
                         (g->nmp ? static_cast<int64_t>(sizeof(uint64_t) * g->E) : 0) +
                         (g->nrec ? static_cast<int64_t>(sizeof(uint4) * g->E) : 0) +
                         (g->w ? static_cast<int64_t>(sizeof(float) * (g->E + VSCAN_PAD)) : 0) +

@@ -25,6 +25,12 @@ csaw_status cuda_fail(cudaError_t e, const char* what, const char* file, int lin
 
 // zero padding after per-edge arrays read as 16 B vectors (vscan.cuh: one warp row = 128 entries)
 #define VSCAN_PAD 128
+// node2vec index records (n2v_index.cu): N2X_P inline member positions / splitters after a
+// 32 B header; 24 -> 128 B records (one DRAM line, what a 64 B random read moves anyway)
+#ifndef N2X_P
+#define N2X_P 24
+#endif
+constexpr int N2X_U4 = 2 + N2X_P / 4;   // record size in uint4
 
 #define CSAW_CUDA(call)                                                         \
     do {                                                                        \
@@ -145,7 +151,7 @@ struct csaw_graph {
     uint64_t ccache_entries = 0;
     uint32_t* tri = nullptr;      // [E] node2vec: |N(v) ∩ N(u)| per entry (symmetric sorted graphs, cache builds)
     // node2vec per-edge intersection index (n2v_index.cu, CSAW_GRAPH_N2V_INDEX)
-    uint4* n2x_rec = nullptr;     // [4 E] {offset lo, offset hi 8 | C << 8, ppos, mb}, {v, row lo, row hi 8 | deg << 8, 0}, P[8]
+    uint4* n2x_rec = nullptr;     // [N2X_U4 E] {offset lo, offset hi 8 | C << 8, ppos, mb}, {v, row lo, row hi 8 | deg << 8, 0}, P[N2X_P]
     uint32_t* n2x_idx = nullptr;  // member positions, n2x_total entries
     uint64_t n2x_total = 0;
     uint32_t flags = 0;           // csaw_graph_opts.flags (variant selectors are read from here)

@@ -14,20 +14,23 @@
 // of the graph, for any p and q -- so they are listed once per edge at graph creation
 // (the paper's deleted "caching transition probability", R25, applied to
 // the dynamic node2vec bias keyed by the edge the walker arrived by):
-//     rec[e] (64 B) = {index offset (40 bits) | C = |N(v) ∩ N(prev)| (24 bits), ppos, mb,
-//                      v = col[e], row start of v (40 bits) | deg(v) (24 bits), 0,
-//                      P[0..8)}
+//     rec[e] (128 B; N2X_P = 24) = {index offset (40 bits) | C = |N(v) ∩ N(prev)| (24 bits),
+//                      ppos, mb, v = col[e], row start of v (40 bits) | deg(v) (24 bits), 0,
+//                      P[0..N2X_P)}
 //         mb = members before ppos (members with value < prev: rows are sorted)
-//         P  = the member positions themselves when C <= 8, else 8 splitters
-//              P[k] = I[j_k], j_k = floor((k + 1) C / 9)
-//     idx[off .. off + C) = ascending positions I in N(v) of the members (C > 8 only).
+//         P  = the member positions themselves when C <= N2X_P, else N2X_P splitters
+//              P[k] = I[j_k], j_k = floor((k + 1) C / (N2X_P + 1))
+//     idx[off .. off + C) = ascending positions I in N(v) of the members (C > N2X_P only).
 // The record of the entry a walker arrived by carries everything the next step needs
 // (its vertex, row and degree, and the step's specials or their splitters), so a step
-// is one 64 B record and, for C > 8, a binary search of about log2(C / 9) probes
+// is one record and, for C > N2X_P, a binary search of about log2(C / (N2X_P + 1)) probes
 // between two splitters: O(log C) dependent sectors instead of a merge of N(v) with
 // N(prev).  The pick is bit-identical to the full CTPS (same integer S, same draw) and
-// to the oracle.  Memory: 64 B per CSR entry + 4 B per (edge, common neighbour) pair of
-// the edges with C > 8; built only if it fits (best-effort).
+// to the oracle.  Record size: a random read moves a whole 128 B line from HBM whether 64 or
+// 128 B are asked for (profiles/r02_random_granule.txt, r3k TMA measurement), so 128 B
+// records hold 24 inline values for the DRAM cost of 8 (A/B cfg3: 6.21 vs 6.97 ms).
+// Memory: 128 B per CSR entry + 4 B per (edge, common neighbour) pair of the edges with
+// C > N2X_P; built only if it fits (best-effort).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -37,9 +40,6 @@
 #include "internal.h"
 #include "util.cuh"
 
-#ifndef N2X_SECTOR_PROBES
-#define N2X_SECTOR_PROBES 0   // search member positions 32 B sector by sector (A/B r02 cfg3: 10.6-11.1 ms, 14.2 GB requested; per-member binary search 10.1 ms, 18.4 GB)
-#endif
 
 namespace csaw {
 
@@ -150,7 +150,7 @@ __global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict
         uint64_t off_e = 0, off_r = 0;
         uint32_t C_all = 0;
         if (kList) {
-            const uint4 re = rec[4 * ecur], rr = rec[4 * r];
+            const uint4 re = rec[N2X_U4 * ecur], rr = rec[N2X_U4 * r];
             off_e = re.x | (static_cast<uint64_t>(re.y & 0xFFu) << 32);
             off_r = rr.x | (static_cast<uint64_t>(rr.y & 0xFFu) << 32);
             C_all = re.y >> 8;
@@ -185,12 +185,12 @@ __global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict
                 if (f) {
                     const uint32_t rank = cnt + __popc(m & lanemask_lt());
                     const uint32_t pu = static_cast<uint32_t>(sv ? l : i), pv = static_cast<uint32_t>(sv ? i : l);
-                    if (C_all > 8) {   // entry e: positions in N(u); entry r: positions in N(v)
+                    if (C_all > N2X_P) {   // entry e: positions in N(u); entry r: positions in N(v)
                         idx[off_e + rank] = pu;
                         idx[off_r + rank] = pv;
                     } else {           // inline in the records
-                        reinterpret_cast<uint32_t*>(rec + 4 * ecur + 2)[rank] = pu;
-                        reinterpret_cast<uint32_t*>(rec + 4 * r + 2)[rank] = pv;
+                        reinterpret_cast<uint32_t*>(rec + N2X_U4 * ecur + 2)[rank] = pu;
+                        reinterpret_cast<uint32_t*>(rec + N2X_U4 * r + 2)[rank] = pv;
                     }
                 }
             } else {
@@ -202,49 +202,47 @@ __global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict
         }
         if (!kList && lane == 0) {
             // e = (v -> u): a walker at u that came from v; prev = v sits at position j of N(u)
-            rec[4 * ecur] = make_uint4(0u, cnt << 8, static_cast<uint32_t>(j), below_v);
+            rec[N2X_U4 * ecur] = make_uint4(0u, cnt << 8, static_cast<uint32_t>(j), below_v);
             // r = (u -> v): a walker at v that came from u; prev = u sits at position e - bv of N(v)
-            rec[4 * r] = make_uint4(0u, cnt << 8, static_cast<uint32_t>(ecur - static_cast<uint64_t>(bv)), below_u);
+            rec[N2X_U4 * r] = make_uint4(0u, cnt << 8, static_cast<uint32_t>(ecur - static_cast<uint64_t>(bv)), below_u);
         }
     }
 }
 
-// exclusive scan of the listed member counts (C > 8) into the records' 40-bit offsets
+// exclusive scan of the listed member counts (C > N2X_P) into the records' 40-bit offsets
 struct N2xCount {
     const uint4* rec;
     __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
-        const uint32_t c = rec[4 * i].y >> 8;
-        return c > 8 ? c : 0;
+        const uint32_t c = rec[N2X_U4 * i].y >> 8;
+        return c > N2X_P ? c : 0;
     }
 };
 struct N2xOffset {
     uint4* rec;
     unsigned long long* sum;
     __device__ __forceinline__ void operator()(uint64_t i, uint64_t e, uint64_t) const {
-        rec[4 * i].x = static_cast<uint32_t>(e);
-        rec[4 * i].y = static_cast<uint32_t>(e >> 32) | (rec[4 * i].y & 0xFFFFFF00u);
+        rec[N2X_U4 * i].x = static_cast<uint32_t>(e);
+        rec[N2X_U4 * i].y = static_cast<uint32_t>(e >> 32) | (rec[N2X_U4 * i].y & 0xFFFFFF00u);
     }
     __device__ __forceinline__ void total(uint64_t, uint64_t t) const { *sum = t; }
 };
 
 // rest of each record: the entry's vertex v = col[e], its row start and degree, and for
-// C > 8 the 8 splitters P[k] = I[floor((k + 1) C / 9)] (C <= 8: the list pass wrote P)
+// C > N2X_P the N2X_P splitters P[k] = I[floor((k + 1) C / (N2X_P + 1))] (C <= N2X_P: the list pass
+// wrote P)
 __global__ void k_n2x_dst(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col, int64_t E,
                           const uint32_t* __restrict__ idx, uint4* __restrict__ rec) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t v = col[e];
         const uint64_t rs = static_cast<uint64_t>(rp[v]);
         const uint32_t d = static_cast<uint32_t>(rp[v + 1] - rp[v]);
-        rec[4 * e + 1] = make_uint4(v, static_cast<uint32_t>(rs), static_cast<uint32_t>(rs >> 32) | (d << 8), 0u);
-        const uint4 q = rec[4 * e];
+        rec[N2X_U4 * e + 1] = make_uint4(v, static_cast<uint32_t>(rs), static_cast<uint32_t>(rs >> 32) | (d << 8), 0u);
+        const uint4 q = rec[N2X_U4 * e];
         const uint32_t C = q.y >> 8;
-        if (C > 8) {
+        if (C > N2X_P) {
             const uint32_t* I = idx + (q.x | (static_cast<uint64_t>(q.y & 0xFFu) << 32));
-            uint32_t P[8];
-#pragma unroll
-            for (uint32_t k = 0; k < 8; ++k) P[k] = I[((k + 1) * static_cast<uint64_t>(C)) / 9];
-            rec[4 * e + 2] = make_uint4(P[0], P[1], P[2], P[3]);
-            rec[4 * e + 3] = make_uint4(P[4], P[5], P[6], P[7]);
+            uint32_t* P = reinterpret_cast<uint32_t*>(rec + N2X_U4 * e + 2);
+            for (uint32_t k = 0; k < N2X_P; ++k) P[k] = I[((k + 1) * static_cast<uint64_t>(C)) / (N2X_P + 1)];
         }
     }
 }
@@ -282,12 +280,12 @@ csaw_status build_n2v_index(csaw_graph* g, int blocks) {
     if (cudaMalloc(&src, sizeof(uint32_t) * E) != cudaSuccess || cudaMalloc(&asym, sizeof(unsigned int)) != cudaSuccess ||
         cudaMalloc(&tot, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&part, sizeof(uint64_t) * (SCAN_MAX_GRID + 8)) != cudaSuccess ||
-        cudaMalloc(&g->n2x_rec, 4 * sizeof(uint4) * E) != cudaSuccess)
+        cudaMalloc(&g->n2x_rec, N2X_U4 * sizeof(uint4) * E) != cudaSuccess)
         return drop();
     if (g->E >= (int64_t(1) << 40)) return drop();
     cudaMemset(asym, 0, sizeof(unsigned int));
     cudaMemset(tot, 0, sizeof(unsigned long long));          // the count pass's edge ticket
-    cudaMemset(g->n2x_rec, 0xFF, 4 * sizeof(uint4) * E);   // unused inline slots
+    cudaMemset(g->n2x_rec, 0xFF, N2X_U4 * sizeof(uint4) * E);   // unused inline slots
     k_n2x_src<<<blocks, 256>>>(g->row_ptr, g->V, src);
     // hub rank bitmaps for the highest-degree rows (build scratch, freed below): at most
     // N2X_HUB_MAX_BYTES, the largest degrees first
@@ -361,7 +359,7 @@ csaw_status build_n2v_index(csaw_graph* g, int blocks) {
 // ---------------------------------------------------------------- walk
 struct N2xArgs {
     const int64_t* __restrict__ rp;
-    const uint4* __restrict__ rec;            // [4 E]: 64 B per entry
+    const uint4* __restrict__ rec;            // [N2X_U4 E]: 16 N2X_U4 B per entry
     const uint32_t* __restrict__ idx;
     const uint32_t* __restrict__ seeds;
     uint64_t n;
@@ -394,70 +392,47 @@ __device__ __forceinline__ int64_t n2x_S(uint32_t wq, int64_t dq1, uint32_t p, u
            static_cast<int64_t>(static_cast<int32_t>(dq1)) * static_cast<int64_t>(static_cast<int32_t>(j)) - sub;
 }
 
-// Last member rank j in [lo, hi) with S(j, I[j]) <= x (S increases with j: the predicate
-// holds on a prefix); found = false if none, else pos = I[j].  The record's 8 inline
-// values resolve it outright for C <= 8 and otherwise narrow [lo, hi) to the gap between
-// two splitters, searched by a plain binary search over idx (about log2(C / 9) probes).
-__device__ __forceinline__ uint32_t n2x_last_le(const uint32_t* __restrict__ I, const uint32_t (&P)[8], uint32_t C,
+// Narrow the member-rank range [lo, hi) of the draw x with the record's N2X_P inline values P:
+// the member positions themselves when C <= N2X_P (then [l, h) is resolved: h = l), else
+// splitters at ranks j_k = floor((k + 1) C / (N2X_P + 1)).  The predicate "j_k < lo, or j_k < hi
+// and S(j_k, P[k]) <= x" holds on a prefix of k (S increases with the rank), so a binary search
+// over k reads about log2(N2X_P) inline values.  On return l - 1 is the last rank known to pass
+// (pos = its position if l > lo) and h the first known to fail.
+__device__ __forceinline__ void n2x_inline(const uint32_t* P, uint32_t C, uint32_t lo, uint32_t hi, int64_t x,
+                                           uint32_t wq, int64_t dq1, int64_t sub, uint32_t& l, uint32_t& h,
+                                           uint32_t& pos) {
+    const bool in = C <= N2X_P;
+    uint32_t a0 = 0, a1 = in ? C : N2X_P;
+    l = lo;
+    h = hi;
+    while (a0 < a1) {
+        const uint32_t k = (a0 + a1) >> 1;
+        const uint32_t j = in ? k : ((k + 1) * C) / (N2X_P + 1);   // (k + 1) C < 2^29
+        bool t = j < lo;
+        if (!t && j < hi) {
+            const uint32_t pk = P[k];
+            t = n2x_S(wq, dq1, pk, j, sub) <= x;
+            if (t) { l = j + 1; pos = pk; } else h = j;
+        }
+        if (t) a0 = k + 1; else a1 = k;
+    }
+    if (in) h = l;
+}
+
+// Last member rank j in [lo, hi) with S(j, I[j]) <= x; found = false if none, else pos = I[j]:
+// the inline values, then a plain binary search over idx between two splitters (about
+// log2(C / (N2X_P + 1)) probes).
+__device__ __forceinline__ uint32_t n2x_last_le(const uint32_t* __restrict__ I, const uint32_t* P, uint32_t C,
                                                 uint32_t lo, uint32_t hi, int64_t x, uint32_t wq, int64_t dq1,
                                                 int64_t sub, uint32_t& probes, bool& found, uint32_t& pos) {
-    uint32_t l = lo, h = hi;
-    if (C <= 8) {
-#pragma unroll
-        for (uint32_t k = 0; k < 8; ++k)
-            if (k >= lo && k < hi && n2x_S(wq, dq1, P[k], k, sub) <= x) { l = k + 1; pos = P[k]; }
-        h = l;
-    } else {
-#pragma unroll
-        for (uint32_t k = 0; k < 8; ++k) {
-            const uint32_t j = static_cast<uint32_t>(((k + 1) * static_cast<uint64_t>(C)) / 9);
-            if (j >= lo && j < hi) {
-                if (n2x_S(wq, dq1, P[k], j, sub) <= x) { l = j + 1; pos = P[k]; }
-                else h = min(h, j);
-            }
-        }
-    }
-#if N2X_SECTOR_PROBES
-    // Probe whole 32 B sectors (8 members, one sector per DRAM access anyway): the predicate
-    // holds on a prefix, so one sector either holds the boundary (done) or halves the range.
-    const uintptr_t ia = reinterpret_cast<uintptr_t>(I);
-    while (l < h) {
-        const uint32_t mid = (l + h) >> 1;
-        // the aligned 8-member group holding I[mid]
-        const uint4* g = reinterpret_cast<const uint4*>((ia + 4ull * mid) & ~static_cast<uintptr_t>(31));
-        const uint4 q0 = __ldg(g), q1 = __ldg(g + 1);
-        ++probes;
-        // rank of the group's first member (negative if the group starts before I[0])
-        const int64_t gb = (static_cast<int64_t>(reinterpret_cast<uintptr_t>(g)) - static_cast<int64_t>(ia)) / 4;
-        const uint32_t pv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-        const int64_t f0 = max(static_cast<int64_t>(l), gb), f1 = min(static_cast<int64_t>(h), gb + 8);   // inside [l, h)
-        // binary search of the true prefix inside the group (the predicate is monotone)
-        uint32_t a0 = static_cast<uint32_t>(f0 - gb), a1 = static_cast<uint32_t>(f1 - gb);
-        while (a0 < a1) {
-            const uint32_t k = (a0 + a1) >> 1;
-            if (n2x_S(wq, dq1, pv[k], static_cast<uint32_t>(gb + k), sub) <= x) a0 = k + 1; else a1 = k;
-        }
-        const uint32_t nt = a0 - static_cast<uint32_t>(f0 - gb);
-        const uint32_t lastp = nt ? pv[a0 - 1] : 0;
-        if (nt == static_cast<uint32_t>(f1 - f0)) {   // all true: the boundary is to the right
-            l = static_cast<uint32_t>(f1);
-            pos = lastp;
-        } else if (nt == 0) {                         // all false: to the left
-            h = static_cast<uint32_t>(f0);
-        } else {                                      // inside the group
-            l = static_cast<uint32_t>(f0) + nt;
-            pos = lastp;
-            h = l;
-        }
-    }
-#else
+    uint32_t l, h;
+    n2x_inline(P, C, lo, hi, x, wq, dq1, sub, l, h, pos);
     while (l < h) {
         const uint32_t mid = (l + h) >> 1;
         const uint32_t p = __ldg(I + mid);
         ++probes;
         if (n2x_S(wq, dq1, p, mid, sub) <= x) { l = mid + 1; pos = p; } else h = mid;
     }
-#endif
     found = l > lo;   // l - 1 is the last true rank, pos = I[l - 1]
     return l - 1;
 }
@@ -492,8 +467,8 @@ __global__ void __launch_bounds__(256, N2X_MINB) k_node2vec_idx(N2xArgs a) {
                      below(draw_u64(a.key, inst, 0u, 0u, word3(PURPOSE_EDGE, 0, 0)), d0);
         ++steps;
         for (int32_t t = 1;; ++t) {
-            const uint4 ra = __ldg(a.rec + 4 * e), rb = __ldg(a.rec + 4 * e + 1);
-            const uint4 rc = __ldg(a.rec + 4 * e + 2), rd = __ldg(a.rec + 4 * e + 3);
+            const uint4 ra = __ldg(a.rec + N2X_U4 * e), rb = __ldg(a.rec + N2X_U4 * e + 1);
+            const uint32_t* P = reinterpret_cast<const uint32_t*>(a.rec + N2X_U4 * e + 2);
             row[t] = rb.x;                          // the vertex this entry leads to
             if (t == a.L) break;
             // step t at v = rb.x, arrived from prev by entry e (d >= 1: prev is in N(v))
@@ -513,7 +488,6 @@ __global__ void __launch_bounds__(256, N2X_MINB) k_node2vec_idx(N2xArgs a) {
                 const bool after = x >= Sp;
                 const int64_t sub = after ? dqp : 0;
                 bool found = false;
-                const uint32_t P[8] = {rc.x, rc.y, rc.z, rc.w, rd.x, rd.y, rd.z, rd.w};
                 const uint32_t j = n2x_last_le(I, P, C, after ? mb : 0, after ? C : mb, x, wq, dq1, sub, probes, found,
                                                pos);
                 if (found) {
@@ -528,14 +502,14 @@ __global__ void __launch_bounds__(256, N2X_MINB) k_node2vec_idx(N2xArgs a) {
             e = rs + s;
         }
     }
-    // sector model (32 B sectors): the 64 B edge record (2 sectors) + the probes per step,
+    // sector model (32 B sectors): the edge record (N2X_U4 / 2 sectors) + the probes per step,
     // + 4 B path (step 0: the seed's row_ptr pair instead of a record)
     steps = warp_sum(steps);
     probes_all = warp_sum(probes_all);
     if (lane_id() == 0 && steps) {
         atomicAdd(a.counters + 1, steps);
         atomicAdd(a.counters + 2, probes_all);
-        atomicAdd(a.counters + 3, 32ull * (2 * steps + probes_all) + 4ull * steps);
+        atomicAdd(a.counters + 3, 32ull * ((N2X_U4 / 2) * steps + probes_all) + 4ull * steps);
     }
 }
 
@@ -549,7 +523,7 @@ struct N2xSearch {          // one walker's step in flight
 };
 
 // record -> the step's search state (prev's own region resolves at once)
-__device__ __forceinline__ void n2x_setup(const N2xArgs& a, uint4 ra, uint4 rb, uint4 rc, uint4 rd, uint64_t U,
+__device__ __forceinline__ void n2x_setup(const N2xArgs& a, uint4 ra, uint4 rb, const uint32_t* P, uint64_t U,
                                           int64_t dq1, int64_t dqp, N2xSearch& q) {
     const uint32_t wq = a.wq, w1 = a.w1, wp = a.wp;
     q.rs = rb.y | (static_cast<uint64_t>(rb.z & 0xFFu) << 32);
@@ -565,25 +539,7 @@ __device__ __forceinline__ void n2x_setup(const N2xArgs& a, uint4 ra, uint4 rb, 
     q.after = q.x >= q.Sp;
     q.sub = q.after ? dqp : 0;
     q.lo = q.after ? q.mb : 0;
-    const uint32_t hi = q.after ? q.C : q.mb;
-    const uint32_t P[8] = {rc.x, rc.y, rc.z, rc.w, rd.x, rd.y, rd.z, rd.w};
-    uint32_t l = q.lo, h = hi;
-    if (q.C <= 8) {
-#pragma unroll
-        for (uint32_t k = 0; k < 8; ++k)
-            if (k >= q.lo && k < hi && n2x_S(wq, dq1, P[k], k, q.sub) <= q.x) { l = k + 1; q.pos = P[k]; }
-        h = l;
-    } else {
-#pragma unroll
-        for (uint32_t k = 0; k < 8; ++k) {
-            const uint32_t j = static_cast<uint32_t>(((k + 1) * static_cast<uint64_t>(q.C)) / 9);
-            if (j >= q.lo && j < hi) {
-                if (n2x_S(wq, dq1, P[k], j, q.sub) <= q.x) { l = j + 1; q.pos = P[k]; }
-                else h = min(h, j);
-            }
-        }
-    }
-    q.l = l; q.h = h;
+    n2x_inline(P, q.C, q.lo, q.after ? q.C : q.mb, q.x, wq, dq1, q.sub, q.l, q.h, q.pos);
 }
 
 // search finished: the pick's position in N(v)
@@ -629,7 +585,7 @@ __device__ __forceinline__ uint32_t n2x_finish(const N2xArgs& a, int64_t dq1, co
 #define N2X_TMA_WARPS 8
 #endif
 #ifndef N2X_SMEM_STRIDE
-#define N2X_SMEM_STRIDE 5   // uint4 per lane slot of the staged records (4 = unpadded)
+#define N2X_SMEM_STRIDE (N2X_U4 + 1)   // uint4 per lane slot of the staged records (N2X_U4 = unpadded)
 #endif
 __device__ __forceinline__ uint32_t n2x_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void n2x_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -662,9 +618,9 @@ struct N2xGroup {           // one group of 32 walkers (per-lane fields)
 #endif
 __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_tma(N2xArgs a) {
     constexpr int K = N2X_TMA_K;
-    // 64 B record per lane at an 80 B stride: a warp's uint4 reads of the records then hit 8
-    // distinct 16 B bank groups per 8-lane phase (conflict-free) -- at a 64 B stride every
-    // phase was a 4-way conflict (ncu r02: 16-way on average, 75 % excessive shared wavefronts)
+    // one record per lane at a stride of an odd number of uint4: a warp's uint4 reads of the
+    // records then hit 8 distinct 16 B bank groups per 8-lane phase (conflict-free) -- 64 B
+    // records at a 64 B stride were a 4-way conflict per phase (ncu r02: 75 % excessive wavefronts)
     __shared__ __align__(128) uint4 recs[N2X_TMA_WARPS][K][32][N2X_SMEM_STRIDE];
 #if N2X_TMA_PROBES
     __shared__ __align__(16) uint4 prb[N2X_TMA_WARPS][K][32];          // 16 B around the probed member
@@ -692,9 +648,9 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
         const bool me = G[k].w < a.n;
         const uint32_t cnt = __popc(__ballot_sync(FULL, me));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // our reads of the slot before the copy
-        if (lane == 0) n2x_expect(&bars[wib][k], cnt * 64u);
+        if (lane == 0) n2x_expect(&bars[wib][k], cnt * (16u * N2X_U4));
         __syncwarp();
-        if (me) n2x_bulk(&recs[wib][k][lane][0], a.rec + 4 * G[k].e, 64u, &bars[wib][k]);
+        if (me) n2x_bulk(&recs[wib][k][lane][0], a.rec + N2X_U4 * G[k].e, 16u * N2X_U4, &bars[wib][k]);
         G[k].probing = false;
     };
     // a new group: step 0 (uniform, R16) for each lane's walker, then its first record
@@ -804,13 +760,13 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
             if (!G[k].probing) {   // records arrived: path entry, then the step's search
                 if (me) {
                     const uint4 ra = recs[wib][k][lane][0], rb = recs[wib][k][lane][1];
-                    const uint4 rc = recs[wib][k][lane][2], rd = recs[wib][k][lane][3];
+                    const uint32_t* P = reinterpret_cast<const uint32_t*>(&recs[wib][k][lane][2]);
                     uint32_t* row = a.path + G[k].w * (static_cast<uint64_t>(a.L) + 1);
                     row[G[k].t] = rb.x;
                     if (G[k].t < a.L) {
                         const uint64_t U = draw_u64(a.key, a.base + static_cast<uint32_t>(G[k].w),
                                                     static_cast<uint32_t>(G[k].t), 0u, word3(PURPOSE_EDGE, 0, 0));
-                        n2x_setup(a, ra, rb, rc, rd, U, dq1, dqp, G[k].q);
+                        n2x_setup(a, ra, rb, P, U, dq1, dqp, G[k].q);
                     }
                 }
                 if (G[k].t == a.L) {   // the group's walks are complete
@@ -875,7 +831,7 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
     if (lane == 0 && steps) {
         atomicAdd(a.counters + 1, steps);
         atomicAdd(a.counters + 2, probes_all);
-        atomicAdd(a.counters + 3, 32ull * (2 * steps + probes_all) + 4ull * steps);
+        atomicAdd(a.counters + 3, 32ull * ((N2X_U4 / 2) * steps + probes_all) + 4ull * steps);
     }
 }
 
