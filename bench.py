@@ -83,6 +83,9 @@ def parse_args(argv=None):
                          "(NEXT-4(i), CSAW_GRAPH_OOM_PEER_STORE; with one GPU a same-device stand-in)")
     ap.add_argument("--oom-variant", default="partition", choices=["partition", "zerocopy"],
                     help="OOM configs: time the paper's partition scheduling (default) or the zero-copy mode")
+    ap.add_argument("--no-walk-buckets", action="store_true",
+                    help="degree walks: the vertex-head walk index (k_walk_head) instead of the bucketed index "
+                         "(CSAW_GRAPH_WALK_BUCKETS, k_walk_gb) (A/B)")
     ap.add_argument("--next-meta", action="store_true",
                     help="MDRW: 8 B next-vertex metadata + col (CSAW_GRAPH_NEXT_META) instead of the 16 B "
                          "next-vertex records (CSAW_GRAPH_NEXT_RECORD) (A/B)")
@@ -520,7 +523,8 @@ def main():
         wts = edge_weights(g, cfg.graph_seed) if cfg.bias == "weight" else None
         G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache, node2vec_tri=use_tri,
                                  next_meta=use_meta and args.next_meta, next_record=use_meta and not args.next_meta,
-                                 walk_index=use_cache, node2vec_index=use_tri, edge_bias=use_eb, weights=wts)
+                                 walk_index=use_cache, node2vec_index=use_tri, edge_bias=use_eb, weights=wts,
+                                 walk_buckets=use_cache and cfg.workload == "walk" and not args.no_walk_buckets)
     ginfo = G.info()
     bias = bias_of(cs, cfg)
     stream = torch.cuda.current_stream(dev)
@@ -679,7 +683,8 @@ def main():
     kname = hot_kernel_name(cfg, bool(ginfo.get("node2vec_tri") if cfg.workload == "node2vec" else ginfo.get("ctps_cache")),
                             oom and args.oom_variant != "zerocopy", int(ginfo.get("walk_index_leaf") or 0),
                             int(ginfo.get("walk_index_group") or 0), bool(ginfo.get("walk_index_heads")),
-                            bool(ginfo.get("node2vec_index")), bool(ginfo.get("edge_bias")))
+                            bool(ginfo.get("node2vec_index")), bool(ginfo.get("edge_bias")),
+                            buckets=bool(ginfo.get("walk_buckets")))
     ncu = load_ncu(variant, kname)
     if oom:
         ach = (h2d_bytes / (total_ms / 1000.0) / 1e9) if h2d_bytes else None
@@ -707,7 +712,7 @@ def main():
                 "kernel": kname, "bytes_model": BYTES_MODEL[model], "alg_bytes_per_launch": bytes_per_launch,
                 "kernel_requested_bytes_per_launch": (kbytes / max(hot_launches, 1)) if kbytes else None,
                 "hot_ms_per_launch": hot_avg_ms, "hot_share_of_step": (hot_ms / total_ms) if total_ms else None,
-                **random_gather_context(achieved),
+                **random_gather_context(achieved, ncu.get("dram_bytes_per_launch"), hot_avg_ms),
                 "peak_source": ("MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)" if "hbm_gbs" in peaks
                                 else "fallback: B200_PROFILING.md")}
 
@@ -929,12 +934,15 @@ def run_e2e(cs, G, bias, seeds, cfg, base, rng_seeds, args, kind, n, dev, world,
                                       "step (max over ranks)"}
 
 
-def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads=False, n2x=False, eb=False):
+def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads=False, n2x=False, eb=False,
+                    buckets=False):
     if cfg.workload == "walk":
         if cfg.bias == "weight":
             return "k_walk_vscan<float>"
         if cfg.bias == "degree" and not cached and eb:
             return "k_walk_vscan<uint32>"
+        if cfg.bias == "degree" and cached and buckets:
+            return "k_walk_gb"
         if cfg.bias == "degree" and wix_leaf and heads and wix_group == 32:
             return f"k_walk_head<{wix_leaf}>"
         if cfg.bias == "degree" and wix_leaf:
@@ -954,7 +962,7 @@ def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads
     return f"k_sample_fused<{mode}>"
 
 
-def random_gather_context(achieved) -> dict:
+def random_gather_context(achieved, traffic=None, hot_ms=None) -> dict:
     """The measured random-access ceiling (profiles/random_gather_peaks.json, scripts/random_roofline.cu):
     64 B records at uniformly random offsets of a 64 GiB buffer -- the access pattern of the pointer-chasing
     walk kernels -- reach ~0.95 TB/s of requested bytes, far below the streaming copy peak.  Context for
@@ -962,11 +970,19 @@ def random_gather_context(achieved) -> dict:
     practical roofline."""
     try:
         with open(os.path.join(ROOT, "profiles", "random_gather_peaks.json")) as f:
-            rg = json.load(f)["by_footprint_gib"]["64"]["64B"]
+            pk = json.load(f)
+        rg = pk["by_footprint_gib"]["64"]["64B"]
+        line = pk.get("random_line", {}).get("dram_gbs")
     except Exception:
         return {}
-    return {"random_gather_peak_gbs": rg,
-            "frac_of_random_gather_peak": (achieved / rg) if achieved else None}
+    out = {"random_gather_peak_gbs": rg, "frac_of_random_gather_peak": (achieved / rg) if achieved else None}
+    if line:
+        # the kernel's DRAM traffic (ncu) against the measured random-line ceiling: every random read moves a
+        # 128 B line, ~34 G lines/s = 4.35 TB/s (profiles/random_gather_peaks.json "random_line")
+        dram = traffic / (hot_ms / 1000.0) / 1e9 if traffic and hot_ms else None
+        out.update({"random_line_ceiling_gbs": line, "dram_gbs_ncu": dram,
+                    "dram_frac_of_random_line_ceiling": (dram / line) if dram else None})
+    return out
 
 
 def load_peaks() -> dict:

@@ -182,6 +182,17 @@ typedef struct {
  * VertexBias in one 16 B access instead of col[e] and nmp[e] (two random DRAM accesses).
  * Takes precedence over CSAW_GRAPH_NEXT_META for MDRW.  Results are identical. */
 #define CSAW_GRAPH_NEXT_RECORD 0x800000u
+/* csaw_graph_opts.flags (in-memory graphs, with CSAW_GRAPH_CTPS_CACHE; best-effort): bucketed
+ * degree-walk index.  Row v's CTPS [0, T) is cut into nb = ceil(T / 2^k) buckets of width
+ * 2^k, k = floor(log2(T / deg(v))) (deg(v) <= nb < 2 deg(v)); bucket b is one 128 B line of 8
+ * 16 B entries {S_i, u | k_u << 27, first bucket of u, T_u}, the regions [S_i, S_i + deg(u))
+ * meeting [b 2^k, (b + 1) 2^k) in order (a 9th region turns the last entry into a link to the
+ * row's CTPS cache).  A degree-walk step is then x = below(U, T), one line at bucket x >> k,
+ * the last entry with S_i <= x: the pick and the next vertex's bucket table arrive together
+ * -- one dependent DRAM round trip per step instead of two (vertex head, then leaf).  Picks
+ * are identical (same integer S, same draw).  Needs every row total < 2^32 - 2 and
+ * V < 2^27 - 1; about 128 B x (1..2) per CSR entry. */
+#define CSAW_GRAPH_WALK_BUCKETS 0x1000000u
 /* csaw_graph_opts.flags (in-memory graphs; built automatically in out-of-memory mode
  * when it fits the budget): chunk-total cache of the degree bias -- for every row of more
  * than 256 candidates, the chunk prefix sums of its CTPS (<= 256 chunks) and its count of
@@ -253,6 +264,8 @@ typedef struct {
     int32_t node2vec_index;         /* 1 if the node2vec intersection index was built (CSAW_GRAPH_N2V_INDEX) */
     int32_t has_weights;            /* 1 if the graph carries edge weights (csaw_csr.weights) */
     int32_t edge_bias;              /* 1 if the materialised degree bias was built (CSAW_GRAPH_EDGE_BIAS) */
+    int32_t walk_buckets;           /* 1 if the bucketed walk index was built (CSAW_GRAPH_WALK_BUCKETS) */
+    int32_t reserved0;
 } csaw_graph_info_t;
 
 typedef struct csaw_graph csaw_graph;  /* opaque */

@@ -101,6 +101,7 @@ CSAW_GRAPH_OOM_ZC_NO_PREFIX = 0x40000
 CSAW_GRAPH_MDRW_GENERIC = 0x80000
 CSAW_GRAPH_MDRW_ALT_RECORDS = 0x100000
 CSAW_GRAPH_NEXT_RECORD = 0x800000
+CSAW_GRAPH_WALK_BUCKETS = 0x1000000
 CSAW_GRAPH_OOM_PEER_STORE = 0x200000
 
 
@@ -110,7 +111,7 @@ def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, 
                       oom_bal: bool = True, walk_index: bool = True, node2vec_tri: bool = False,
                       next_meta: bool = False, chunk_cache: bool = False, node2vec_index: bool = False,
                       weights=None, edge_bias: bool = False, flags: int = 0, store_device=None,
-                      next_record: bool = False) -> Graph:
+                      next_record: bool = False, walk_buckets: bool = False) -> Graph:
     """row_ptr int64[V+1], col_idx int32/uint32[E] (torch tensors, host or device).
     ctps_cache=True builds the static-bias CTPS cache (CSAW_GRAPH_CTPS_CACHE);
     zerocopy=True (with budget_bytes > 0) reads col_idx from pinned host memory;
@@ -125,7 +126,8 @@ def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, 
     degree bias deg(col[e]) (CSAW_GRAPH_EDGE_BIAS: degree walks without the cache stream it); flags = extra
     CSAW_GRAPH_* bits (the variant selectors); store_device = GPU whose HBM holds the OOM partition store
     (CSAW_GRAPH_OOM_PEER_STORE; == device: a same-device stand-in); next_record=True the 16 B per-entry
-    next-vertex records MDRW reads instead of col + next_meta (CSAW_GRAPH_NEXT_RECORD)."""
+    next-vertex records MDRW reads instead of col + next_meta (CSAW_GRAPH_NEXT_RECORD); walk_buckets=True (with
+    ctps_cache) the bucketed degree-walk index (CSAW_GRAPH_WALK_BUCKETS, one DRAM round trip per step)."""
     V = row_ptr.numel() - 1
     if weights is not None and weights.dtype != torch.float32:
         raise TypeError("weights must be float32")
@@ -138,6 +140,7 @@ def csaw_graph_create(row_ptr, col_idx, device: int = 0, budget_bytes: int = 0, 
                           | (CSAW_GRAPH_N2V_TRI if node2vec_tri else 0)
                           | (CSAW_GRAPH_NEXT_META if next_meta else 0)
                           | (CSAW_GRAPH_NEXT_RECORD if next_record else 0)
+                          | (CSAW_GRAPH_WALK_BUCKETS if walk_buckets else 0)
                           | (CSAW_GRAPH_CHUNK_CACHE if chunk_cache else 0)
                           | (CSAW_GRAPH_N2V_INDEX if node2vec_index else 0)
                           | (CSAW_GRAPH_EDGE_BIAS if edge_bias else 0) | int(flags)

@@ -74,7 +74,8 @@ class csaw_graph_info_t(C.Structure):
                 ("nonisolated", C.c_int64), ("rows_sorted", C.c_int32), ("oom_mode", C.c_int32),
                 ("device_bytes", C.c_int64), ("ctps_cache", C.c_int32), ("walk_index_leaf", C.c_int32),
                 ("cache_build_ms", C.c_double), ("walk_index_group", C.c_int32), ("node2vec_tri", C.c_int32), ("walk_index_heads", C.c_int32), ("node2vec_index", C.c_int32),
-                ("has_weights", C.c_int32), ("edge_bias", C.c_int32)]
+                ("has_weights", C.c_int32), ("edge_bias", C.c_int32), ("walk_buckets", C.c_int32),
+                ("reserved0", C.c_int32)]
 
 
 class csaw_run_stats(C.Structure):

@@ -467,6 +467,137 @@ static csaw_status build_wix(csaw_graph* g, int blocks) {
     return s;
 }
 
+// ---------------------------------------------------------------- bucketed walk index
+// CSAW_GRAPH_WALK_BUCKETS (csaw.h): row v's CTPS [0, T) in buckets of width 2^k, k = floor(log2(T / d)),
+// each bucket one 128 B line of 8 entries {S_i, u | k_u << 27, first bucket of u, T_u} for the regions
+// meeting it; a 9th region turns entry 7 into {S_i, GB_LINK, CSR entry of region i lo, hi}.
+constexpr uint32_t GB_EMPTY = 0xFFFFFFFFu;   // S of an unused entry (> every draw: T < 2^32 - 2)
+constexpr uint32_t GB_LINK = 0xFFFFFFFFu;    // u field of a link entry (V < 2^27 - 1, so never u | k << 27)
+__host__ __device__ __forceinline__ uint32_t gb_shift(uint64_t T, uint64_t d) {
+    uint64_t r = T / d;   // mean region width (>= 1 unless some regions are empty)
+    uint32_t k = 0;
+    while (r > 1) { r >>= 1; ++k; }
+    return k;
+}
+struct GbSize {
+    const int64_t* rp;
+    const uint64_t* cps;
+    __device__ __forceinline__ uint64_t operator()(uint64_t v) const {
+        const int64_t b = rp[v], e = rp[v + 1];
+        if (e == b) return 0;
+        const uint64_t T = cps[e - 1];
+        if (T == 0) return 0;
+        return ((T - 1) >> gb_shift(T, static_cast<uint64_t>(e - b))) + 1;
+    }
+};
+// T < 2^32 - 2 for every row, V < 2^27 - 1 (else no bucket index)
+__global__ void k_gb_check(const int64_t* __restrict__ rp, const uint64_t* __restrict__ cps, int64_t V,
+                           unsigned int* bad) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
+        if (rp[v + 1] > rp[v] && cps[rp[v + 1] - 1] >= 0xFFFFFFFEull) atomicOr(bad, 1u);
+}
+__global__ void k_gb_meta(const int64_t* __restrict__ rp, const uint64_t* __restrict__ cps,
+                          const uint64_t* __restrict__ boff, int64_t V, uint4* __restrict__ meta) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = rp[v], e = rp[v + 1];
+        const uint64_t T = e > b ? cps[e - 1] : 0;
+        meta[v] = make_uint4(static_cast<uint32_t>(boff[v]), T ? gb_shift(T, static_cast<uint64_t>(e - b)) : 0u,
+                             static_cast<uint32_t>(T), 0u);
+    }
+}
+// one thread per bucket: its row by a binary search of the bucket offsets, its first region by
+// an upper bound of the bucket start in the row's inclusive prefix (the CTPS cache)
+__global__ void k_gb_fill(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col,
+                          const uint64_t* __restrict__ cps, const uint64_t* __restrict__ boff, int64_t V,
+                          uint64_t nbk, const uint4* __restrict__ meta, uint4* __restrict__ gbk) {
+    for (uint64_t gi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; gi < nbk; gi += (uint64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = V;   // last v with boff[v] <= gi
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (boff[mid] <= gi) lo = mid; else hi = mid;
+        }
+        const int64_t v = lo;
+        const uint64_t b = gi - boff[v];
+        const int64_t rs = rp[v];
+        const uint64_t d = static_cast<uint64_t>(rp[v + 1] - rs);
+        const uint32_t k = meta[v].y;
+        const uint64_t x0 = b << k, x1 = (b + 1) << k;
+        uint64_t l = 0, h = d;   // first region with inclusive prefix > x0
+        while (l < h) {
+            const uint64_t mid = (l + h) >> 1;
+            if (cps[rs + mid] <= x0) l = mid + 1; else h = mid;
+        }
+        uint4* out = gbk + gi * 8;
+        uint32_t slot = 0;
+        for (uint64_t i = l; i < d && slot < 8; ++i) {
+            const uint64_t sx = i ? cps[rs + i - 1] : 0;
+            if (sx >= x1) break;
+            if (cps[rs + i] == sx) continue;   // empty region: never picked
+            if (slot == 7) {   // a 9th region meets the bucket: link entry 7 to the CTPS cache
+                uint64_t j = i + 1;
+                while (j < d && cps[rs + j] == cps[rs + j - 1]) ++j;
+                if (j < d && cps[rs + j - 1] < x1) {
+                    const uint64_t ge = static_cast<uint64_t>(rs) + i;
+                    out[7] = make_uint4(static_cast<uint32_t>(sx), GB_LINK, static_cast<uint32_t>(ge),
+                                        static_cast<uint32_t>(ge >> 32));
+                    slot = 8;
+                    break;
+                }
+            }
+            const uint32_t u = col[rs + i];
+            const uint4 mu = meta[u];
+            out[slot++] = make_uint4(static_cast<uint32_t>(sx), u | (mu.y << 27), mu.x, mu.z);
+        }
+        for (; slot < 8; ++slot) out[slot] = make_uint4(GB_EMPTY, 0u, 0u, 0u);
+    }
+}
+
+static csaw_status build_gb(csaw_graph* g, int blocks) {
+    const int64_t V = g->V;
+    if (!g->cps || g->E <= 0 || V >= (int64_t(1) << 27) - 1) return CSAW_OK;
+    unsigned int* bad = nullptr;
+    uint64_t *boff = nullptr, *part = nullptr;
+    auto release = [&]() {
+        if (bad) cudaFree(bad);
+        if (boff) cudaFree(boff);
+        if (part) cudaFree(part);
+        cudaGetLastError();
+    };
+    auto drop = [&]() {   // best-effort: degree walks keep the vertex heads / walk index
+        release();
+        if (g->gbk) cudaFree(g->gbk);
+        if (g->gmeta) cudaFree(g->gmeta);
+        g->gbk = nullptr;
+        g->gmeta = nullptr;
+        g->gb_buckets = 0;
+        cudaGetLastError();
+        return CSAW_OK;
+    };
+    if (cudaMalloc(&bad, sizeof(unsigned int)) != cudaSuccess || cudaMalloc(&boff, sizeof(uint64_t) * (V + 1)) != cudaSuccess ||
+        cudaMalloc(&part, sizeof(uint64_t) * (SCAN_MAX_GRID + 8)) != cudaSuccess)
+        return drop();
+    cudaMemset(bad, 0, sizeof(unsigned int));
+    k_gb_check<<<blocks, 256>>>(g->row_ptr, g->cps, V, bad);
+    unsigned int hb = 0;
+    if (cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost) != cudaSuccess || hb) return drop();
+    if (device_scan(GbSize{g->row_ptr, g->cps}, static_cast<uint64_t>(V), ScanToArray{boff}, part, nullptr) != CSAW_OK)
+        return drop();
+    uint64_t nbk = 0;
+    if (cudaMemcpy(&nbk, boff + V, sizeof(nbk), cudaMemcpyDeviceToHost) != cudaSuccess) return drop();
+    size_t fre = 0, tot = 0;
+    if (nbk == 0 || nbk >= (uint64_t(1) << 32) || cudaMemGetInfo(&fre, &tot) != cudaSuccess ||
+        nbk * 128 + sizeof(uint4) * V > fre / 2)   // keep half of the free memory for the run
+        return drop();
+    if (cudaMalloc(&g->gbk, nbk * 128) != cudaSuccess || cudaMalloc(&g->gmeta, sizeof(uint4) * V) != cudaSuccess)
+        return drop();
+    k_gb_meta<<<blocks, 256>>>(g->row_ptr, g->cps, boff, V, g->gmeta);
+    k_gb_fill<<<blocks * 4, 256>>>(g->row_ptr, g->col, g->cps, boff, V, nbk, g->gmeta, g->gbk);
+    if (cudaDeviceSynchronize() != cudaSuccess) return drop();
+    g->gb_buckets = nbk;
+    release();
+    return CSAW_OK;
+}
+
 // ---------------------------------------------------------------- node2vec edge triangle counts
 // tri[e] = |N(v) ∩ N(u)| for the CSR entry e = (v -> u): the number of "common
 // neighbour" specials of a node2vec step that arrived at v from u (or at u from v), so
@@ -854,6 +985,10 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
             const csaw_status ws = build_wix(g, blocks);
             if (ws != CSAW_OK) return cleanup(ws);
         }
+        if (o.flags & CSAW_GRAPH_WALK_BUCKETS) {
+            const csaw_status gs = build_gb(g, blocks);
+            if (gs != CSAW_OK) return cleanup(gs);
+        }
         g->cache_build_ms = tm.ms();
     }
     if ((o.flags & CSAW_GRAPH_NEXT_META) && !g->oom && !g->nmp && g->max_deg < (1 << 24) && E < (int64_t(1) << 40) &&
@@ -917,6 +1052,8 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->bt_off) cudaFree(g->bt_off);
     if (g->nmp) cudaFree(g->nmp);
     if (g->nrec) cudaFree(g->nrec);
+    if (g->gbk) cudaFree(g->gbk);
+    if (g->gmeta) cudaFree(g->gmeta);
     if (g->c32) cudaFree(g->c32);
     if (g->ccache) cudaFree(g->ccache);
     if (g->whead) cudaFree(g->whead);
@@ -966,6 +1103,7 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
                         (g->n2x_rec ? static_cast<int64_t>(N2X_U4 * sizeof(uint4) * g->E + sizeof(uint32_t) * g->n2x_total) : 0) +
                         (g->nmp ? static_cast<int64_t>(sizeof(uint64_t) * g->E) : 0) +
                         (g->nrec ? static_cast<int64_t>(sizeof(uint4) * g->E) : 0) +
+                        (g->gbk ? static_cast<int64_t>(128 * g->gb_buckets + sizeof(uint4) * g->V) : 0) +
                         (g->w ? static_cast<int64_t>(sizeof(float) * (g->E + VSCAN_PAD)) : 0) +
                         (g->ebias ? static_cast<int64_t>(sizeof(uint32_t) * (g->E + VSCAN_PAD)) : 0) +
                         static_cast<int64_t>(sizeof(uint64_t) * g->ccache_entries);
@@ -978,6 +1116,7 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
     out->cache_build_ms = g->cache_build_ms;
     out->has_weights = g->w ? 1 : 0;
     out->edge_bias = g->ebias ? 1 : 0;
+    out->walk_buckets = g->gbk ? 1 : 0;
     return CSAW_OK;
 }
 

@@ -139,6 +139,9 @@ struct csaw_graph {
     uint64_t* bt_off = nullptr;   // [V] start of a row's index segment in bt (= row_ptr/16 + 8 v)
     uint64_t* nmp = nullptr;      // [E] next-vertex metadata row_ptr[u] << 24 | deg(u) (walks)
     uint4* nrec = nullptr;        // [E] next-vertex record {u, deg(u), row_ptr[u] lo, hi} (MDRW)
+    uint4* gbk = nullptr;         // bucketed walk index: [buckets][8] entries {S, u | k_u << 27, bucket of u, T_u}
+    uint4* gmeta = nullptr;       // [V] {first bucket, k, T, 0}
+    uint64_t gb_buckets = 0;
     // narrow walk index (wix.cuh): built with the cache when every row total T < 2^32
     uint32_t* c32 = nullptr;      // padded leaves: S_{i+1} as u32 (wix.cuh leaf_pos)
     uint32_t* wcol = nullptr;     // padded leaves: col copy

@@ -178,6 +178,75 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_wix(WalkArgs a, con
     }
 }
 
+// Degree-biased walk over the bucketed index (CSAW_GRAPH_WALK_BUCKETS, capi.cu build_gb): a step
+// is x = below(U, T), ONE 128 B line -- bucket x >> k of the current vertex, 8 entries read by
+// lanes 0..7 -- and the last entry with S_i <= x, which carries the next vertex with its own
+// bucket table, shift and T: one dependent DRAM round trip per step (k_walk_head: head, then
+// leaf).  A link entry (a bucket met by more than 8 regions, ~0.2 % of cfg2's steps) continues
+// in the row's CTPS cache 32 entries at a time, then reads the pick's col and bucket metadata.
+// Same S, same draw, same region as every other degree-walk kernel and the oracle.
+__global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_gb(WalkArgs a, const uint4* __restrict__ gbk,
+                                                              const uint4* __restrict__ gmeta,
+                                                              const uint64_t* __restrict__ cps, uint64_t E) {
+    const int lane = lane_id();
+    unsigned long long bytes = 0, steps = 0, links = 0;
+    for (uint64_t w = walker_ticket(a.counters + 7); w < a.n; w = walker_ticket(a.counters + 7)) {
+        uint32_t cur = a.seeds[w];
+        const uint32_t inst = a.base + static_cast<uint32_t>(w);
+        PathWriter pw{a.path + w * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
+        pw.put(0, cur);
+        const uint4 m0 = __ldg(gmeta + cur);
+        uint32_t B = m0.x, k = m0.y, T = m0.z;
+        uint64_t ubuf = 0;
+        for (int32_t t = 0; t < a.L; ++t) {
+            if ((t & 31) == 0)
+                ubuf = draw_u64(a.key, inst, static_cast<uint32_t>(t + lane), 0u, word3(PURPOSE_EDGE, 0, 0));
+            const uint64_t U = __shfl_sync(FULL, ubuf, t & 31);
+            uint32_t nxt = NONE;
+            if (cur != NONE && T > 0) {   // T = 0: no positive-bias neighbour, the walk ends (R20)
+                const uint32_t x = static_cast<uint32_t>(below(U, T));
+                uint4 e = make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
+                if (lane < 8) e = __ldg(gbk + (static_cast<uint64_t>(B) + (x >> k)) * 8 + lane);
+                const int fl = 31 - __clz(__ballot_sync(FULL, lane < 8 && e.x <= x));   // entry 0 always passes
+                const uint32_t uk = __shfl_sync(FULL, e.y, fl);
+                const uint32_t eb = __shfl_sync(FULL, e.z, fl), et = __shfl_sync(FULL, e.w, fl);
+                bytes += 128;
+                if (uk != 0xFFFFFFFFu) {
+                    nxt = uk & 0x7FFFFFFu;
+                    k = uk >> 27;
+                    B = eb;
+                    T = et;
+                } else {   // link: the region of x lies at or after CSR entry ge of this row
+                    ++links;
+                    uint64_t ge = static_cast<uint64_t>(et) << 32 | eb;
+                    for (;;) {   // first entry with inclusive prefix > x (exists: x < T)
+                        const uint64_t c = ge + lane < E ? __ldg(cps + ge + lane) : ~0ull;
+                        const unsigned gt = __ballot_sync(FULL, c > x);
+                        bytes += 256;
+                        if (gt) { ge += __ffs(gt) - 1; break; }
+                        ge += 32;
+                    }
+                    nxt = __ldg(a.col + ge);
+                    const uint4 mu = __ldg(gmeta + nxt);
+                    B = mu.x;
+                    k = mu.y;
+                    T = mu.z;
+                    bytes += 20;
+                }
+                ++steps;
+            }
+            cur = nxt;
+            pw.put(t + 1, nxt);
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if (bytes) atomicAdd(a.counters + 3, bytes + 4ull * steps);
+        if (steps) atomicAdd(a.counters + 1, steps);
+        if (links) atomicAdd(a.counters + 2, links);
+    }
+}
+
 // Degree-biased walk over the vertex heads (wix.cuh): a step is one coalesced 512 B head
 // read (record + top level, or the whole row when d <= 60), then K - 1 internal nodes and
 // one leaf when the row is larger -- one dependent round trip less than record + nodes.
@@ -1777,7 +1846,12 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
     const uint32_t* colp = g->col ? g->col : g->oomst.src_col;
     WalkArgs a{g->row_ptr, colp, g->deg, d_seeds, static_cast<uint64_t>(n), length,
                static_cast<uint32_t>(base), key, d_path, static_cast<unsigned long long*>(cnt), g->ccache};
-    if (b.kind == CSAW_BIAS_DEGREE && g->wix_leaf) {
+    if (b.kind == CSAW_BIAS_DEGREE && g->gbk) {
+        constexpr int hw = 2;   // warps per block: the few walkers (cfg2: 4,000 warps) spread over all SMs
+        const int64_t hwarps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 64);
+        k_walk_gb<<<static_cast<int>((hwarps + hw - 1) / hw), hw * 32, 0, st>>>(a, g->gbk, g->gmeta, g->cps,
+                                                                                     static_cast<uint64_t>(g->E));
+    } else if (b.kind == CSAW_BIAS_DEGREE && g->wix_leaf) {
         // group kernels: 2-warp blocks, so few walkers (cfg2: 1,000 warps) still spread over all SMs
         const int wpb = g->wix_group == 32 ? WALK_WARPS : 2;
         const int blk = wpb * 32;

@@ -99,9 +99,13 @@ def test_cfg2_degree_walk_full():
     Gc = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, ctps_cache=True)     # the bench's launch
     Gs = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0)                      # per-step scans (the ★ path)
     Ge = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, edge_bias=True)      # per-step scans of the streamed bias
+    Gb = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, ctps_cache=True, walk_buckets=True)   # k_walk_gb
     assert Gc.info()["walk_index_leaf"] == 128 and Gs.info()["ctps_cache"] == 0 and Ge.info()["edge_bias"] == 1
+    assert Gb.info()["walk_buckets"] == 1
     for seed in SEEDS:
         pc = u32(cs.csaw_walk(Gc, "degree", seeds, cfg.length, rng_seed=seed))
+        pb = u32(cs.csaw_walk(Gb, "degree", seeds, cfg.length, rng_seed=seed))
+        assert first_mismatch(pb, pc) is None, f"seed {seed}: bucket vs head walker {first_mismatch(pb, pc)}"
         ps = u32(cs.csaw_walk(Gs, "degree", seeds, cfg.length, rng_seed=seed))
         pe = u32(cs.csaw_walk(Ge, "degree", seeds, cfg.length, rng_seed=seed))
         assert first_mismatch(pe, ps) is None, f"seed {seed}: stream vs gather walker {first_mismatch(pe, ps)}"
@@ -113,7 +117,7 @@ def test_cfg2_degree_walk_full():
         assert first_mismatch(ps, ref) is None, f"seed {seed}: scan walker {first_mismatch(ps, ref)}"
         assert (pc != cs.NONE).all()          # symmetric graph, non-isolated seeds: exact length
         check_edges_exist(og, pc[:, :-1].ravel(), pc[:, 1:].ravel())
-    release(Gc, Gs, Ge)
+    release(Gc, Gs, Ge, Gb)
 
 
 def test_cfg2_weight_walk_full():
