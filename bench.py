@@ -170,6 +170,8 @@ BYTES_MODEL = {
     "walk_degree_cached": "SURVEY §8(f) NEXT-1 cached CTPS: 32 B sectors x (row_ptr pair + ceil(log2 d(v)) probes "
                           "+ col) per step + 4 (path)",
     "walk_uniform": "16 (row_ptr pair) + 4 (one col entry) + 4 (path) per step",
+    "walk_weight_cached": "SURVEY §8(f) NEXT-1 cached CTPS of the edge weights (fp64 prefix): 32 B sectors x (row_ptr "
+                          "pair + ceil(log2 d(v)) probes + col) per step + 4 (path)",
     "walk_weight_stream": "per-step scan of the fp32 edge weights (float path): 16 (row_ptr pair) + 4 d(v) (the pool's "
                           "weights, streamed) + 4 (the pick's col) + 4 (path)",
     "node2vec": "SURVEY §8(d) node2vec step: 16 + 4 d(v) + 4 (N(prev) carried from the previous step); "
@@ -201,8 +203,11 @@ def walk_alg_bytes(cfg, deg, out, cached, stream=False):
         return int(16 * nsteps + 4 * d[:, 1:].sum() + 4 * first + 4 * nsteps), "node2vec"
     if cfg.bias == "uniform":
         return 24 * nsteps, "walk_uniform"
-    if cfg.bias == "weight":
+    if cfg.bias == "weight" and not cached:
         return int(16 * nsteps + 4 * d.sum() + 8 * nsteps), "walk_weight_stream"
+    if cfg.bias == "weight":
+        probes = _bit_length(torch.clamp(d - 1, min=0))
+        return int(32 * (2 * nsteps + probes[valid].sum()) + 4 * nsteps), "walk_weight_cached"
     if cached:
         probes = _bit_length(torch.clamp(d - 1, min=0))
         return int(32 * (2 * nsteps + probes[valid].sum()) + 4 * nsteps), "walk_degree_cached"
@@ -524,7 +529,8 @@ def main():
         G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache, node2vec_tri=use_tri,
                                  next_meta=use_meta and args.next_meta, next_record=use_meta and not args.next_meta,
                                  walk_index=use_cache, node2vec_index=use_tri, edge_bias=use_eb, weights=wts,
-                                 walk_buckets=use_cache and cfg.workload == "walk" and not args.no_walk_buckets)
+                                 walk_buckets=(use_cache or cfg.bias == "weight") and cfg.workload == "walk"
+                                 and not args.no_walk_buckets)
     ginfo = G.info()
     bias = bias_of(cs, cfg)
     stream = torch.cuda.current_stream(dev)
@@ -625,7 +631,7 @@ def main():
     # ---------------- §8(d) algorithmic bytes of the timed launches (from the outputs, untimed re-runs)
     alg_bytes, model = 0, "oom_host"
     if not oom:
-        cached = bool(ginfo.get("ctps_cache"))
+        cached = bool(ginfo.get("ctps_cache")) or (cfg.bias == "weight" and bool(ginfo.get("walk_buckets", 0) & 2))
         for s, k in steps_per_seed.items():
             if k == 0:
                 continue
@@ -664,8 +670,9 @@ def main():
 
     # ---------------- the config's per-step scan path (no caches), reported apart
     scan_path = None
-    if args.scan_path_steps > 0 and not oom and not args.no_cache and rank == 0 and cfg.bias != "weight":
-        scan_path = run_scan_path(cs, g, cfg, deg, seeds, base, rng_seeds, n, dev, local, stream, flush, args)
+    if args.scan_path_steps > 0 and not oom and not args.no_cache and rank == 0:
+        scan_path = run_scan_path(cs, g, cfg, deg, seeds, base, rng_seeds, n, dev, local, stream, flush, args,
+                                  wts if cfg.bias == "weight" else None)
 
     # ---------------- end-to-end through the C ABI with host buffers
     e2e = None
@@ -684,7 +691,7 @@ def main():
                             oom and args.oom_variant != "zerocopy", int(ginfo.get("walk_index_leaf") or 0),
                             int(ginfo.get("walk_index_group") or 0), bool(ginfo.get("walk_index_heads")),
                             bool(ginfo.get("node2vec_index")), bool(ginfo.get("edge_bias")),
-                            buckets=bool(ginfo.get("walk_buckets")))
+                            buckets=bool(ginfo.get("walk_buckets", 0) & (2 if cfg.bias == "weight" else 1)))
     ncu = load_ncu(variant, kname)
     if oom:
         ach = (h2d_bytes / (total_ms / 1000.0) / 1e9) if h2d_bytes else None
@@ -767,7 +774,7 @@ def main():
     return 0
 
 
-def run_scan_path(cs, g, cfg, deg, seeds, base, rng_seeds, n, dev, local, stream, flush, args):
+def run_scan_path(cs, g, cfg, deg, seeds, base, rng_seeds, n, dev, local, stream, flush, args, wts=None):
     """detail.scan_path: the same workload through the per-step scan path -- no CTPS cache, no
     walk index, no node2vec index: every step evaluates its pool's biases and scans them
     (the north star's literal hot path, §4.1).  Degree walks stream the materialised per-edge
@@ -775,7 +782,7 @@ def run_scan_path(cs, g, cfg, deg, seeds, base, rng_seeds, n, dev, local, stream
     each step, CUDA events on the launching stream)."""
     try:
         eb = cfg.workload == "walk" and cfg.bias == "degree" and not args.gather_bias
-        Gs = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, edge_bias=eb)
+        Gs = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, edge_bias=eb, weights=wts)
         info = Gs.info()
         bias = bias_of(cs, cfg)
         kind = workload_of(cfg)
@@ -938,7 +945,7 @@ def hot_kernel_name(cfg, cached=False, oom=False, wix_leaf=0, wix_group=0, heads
                     buckets=False):
     if cfg.workload == "walk":
         if cfg.bias == "weight":
-            return "k_walk_vscan<float>"
+            return "k_walk_gbw" if buckets else "k_walk_vscan<float>"
         if cfg.bias == "degree" and not cached and eb:
             return "k_walk_vscan<uint32>"
         if cfg.bias == "degree" and cached and buckets:

@@ -191,7 +191,12 @@ typedef struct {
  * the last entry with S_i <= x: the pick and the next vertex's bucket table arrive together
  * -- one dependent DRAM round trip per step instead of two (vertex head, then leaf).  Picks
  * are identical (same integer S, same draw).  Needs every row total < 2^32 - 2 and
- * V < 2^27 - 1; about 128 B x (1..2) per CSR entry. */
+ * V < 2^27 - 1; about 128 B x (1..2) per CSR entry.  On a graph with edge weights the flag
+ * also builds the float-path twin for CSAW_BIAS_WEIGHT walks (no CTPS cache needed): each row's
+ * fp64 prefix of the fp32 weights summed left to right (R28 -- the oracle's sums, bit for bit),
+ * buckets of width 2^k (k = floor(log2(T / d)) in [-24, 7]) holding up to 5 candidate regions
+ * {S, T_u, u, bucket of u}; a pick is the last positive-weight region with S <= x = r T, so
+ * weighted walks match the oracle exactly instead of within the 1e-6 boundary rule. */
 #define CSAW_GRAPH_WALK_BUCKETS 0x1000000u
 /* csaw_graph_opts.flags (in-memory graphs; built automatically in out-of-memory mode
  * when it fits the budget): chunk-total cache of the degree bias -- for every row of more
@@ -264,7 +269,7 @@ typedef struct {
     int32_t node2vec_index;         /* 1 if the node2vec intersection index was built (CSAW_GRAPH_N2V_INDEX) */
     int32_t has_weights;            /* 1 if the graph carries edge weights (csaw_csr.weights) */
     int32_t edge_bias;              /* 1 if the materialised degree bias was built (CSAW_GRAPH_EDGE_BIAS) */
-    int32_t walk_buckets;           /* 1 if the bucketed walk index was built (CSAW_GRAPH_WALK_BUCKETS) */
+    int32_t walk_buckets;           /* bucketed walk indices built (CSAW_GRAPH_WALK_BUCKETS): 1 degree, 2 edge weights */
     int32_t reserved0;
 } csaw_graph_info_t;
 

@@ -598,6 +598,163 @@ static csaw_status build_gb(csaw_graph* g, int blocks) {
     return CSAW_OK;
 }
 
+// ---------------------------------------------------------------- bucketed walk index, edge weights
+// The float path (R28, EdgeBias = w(e)): S_{i+1} = S_i + (double) w_i left to right per row --
+// the oracle's order, so S, T and the draw x = r T are the oracle's bit for bit -- cut into
+// buckets of width 2^k (k = floor(log2(T / d)) in [-24, 7]); a pick is the last positive-weight
+// region with S_i <= x (R28).  A bucket (128 B) lists up to 5 candidate regions: the last
+// positive one starting at or before the bucket start, then the positive ones starting inside;
+// a 6th turns entry 4 into a link (uk = GB_LINK, T slot = its CSR entry as a u64 bit pattern).
+constexpr int GBW_CAP = 5;
+constexpr int GBW_KBIAS = 24;
+__global__ void k_gbw_prefix(const int64_t* __restrict__ rp, const float* __restrict__ w, int64_t V,
+                             double* __restrict__ cpsw, unsigned int* bad) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = rp[v], e = rp[v + 1];
+        double S = 0.0;
+        for (int64_t i = b; i < e; ++i) {
+            S += static_cast<double>(w[i]);
+            cpsw[i] = S;
+        }
+        if (e > b && S > 0.0) {
+            const int k = ilogb(S / static_cast<double>(e - b));
+            if (k < -GBW_KBIAS || k > 31 - GBW_KBIAS || S * ldexp(1.0, -k) >= 4294967295.0) atomicOr(bad, 1u);
+        }
+    }
+}
+struct GbwSize {
+    const int64_t* rp;
+    const double* cpsw;
+    __device__ __forceinline__ uint64_t operator()(uint64_t v) const {
+        const int64_t b = rp[v], e = rp[v + 1];
+        if (e == b) return 0;
+        const double T = cpsw[e - 1];
+        if (!(T > 0.0)) return 0;
+        const int k = ilogb(T / static_cast<double>(e - b));
+        return static_cast<uint64_t>(T * ldexp(1.0, -k)) + 1;   // x = r T <= T: floor(x 2^-k) < nb
+    }
+};
+__global__ void k_gbw_meta(const int64_t* __restrict__ rp, const double* __restrict__ cpsw,
+                           const uint64_t* __restrict__ boff, int64_t V, uint4* __restrict__ meta) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = rp[v], e = rp[v + 1];
+        const double T = e > b ? cpsw[e - 1] : 0.0;
+        const int k = T > 0.0 ? ilogb(T / static_cast<double>(e - b)) : 0;
+        const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(T > 0.0 ? T : 0.0));
+        meta[v] = make_uint4(static_cast<uint32_t>(boff[v]), static_cast<uint32_t>(k + GBW_KBIAS),
+                             static_cast<uint32_t>(tb), static_cast<uint32_t>(tb >> 32));
+    }
+}
+__global__ void k_gbw_fill(const int64_t* __restrict__ rp, const uint32_t* __restrict__ col, const float* __restrict__ w,
+                           const double* __restrict__ cpsw, const uint64_t* __restrict__ boff, int64_t V, uint64_t nbk,
+                           const uint4* __restrict__ meta, uint8_t* __restrict__ gbw) {
+    for (uint64_t gi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; gi < nbk; gi += (uint64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = V;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (boff[mid] <= gi) lo = mid; else hi = mid;
+        }
+        const int64_t v = lo;
+        const uint64_t b = gi - boff[v];
+        const int64_t rs = rp[v];
+        const int64_t d = rp[v + 1] - rs;
+        const int k = static_cast<int>(meta[v].y) - GBW_KBIAS;
+        const double x0 = ldexp(static_cast<double>(b), k), x1 = ldexp(static_cast<double>(b + 1), k);
+        auto sx = [&](int64_t i) { return i ? cpsw[rs + i - 1] : 0.0; };   // exclusive prefix of region i
+        int64_t l = 0, h = d;   // first i with S_excl(i) > x0
+        while (l < h) {
+            const int64_t mid = (l + h) >> 1;
+            if (sx(mid) <= x0) l = mid + 1; else h = mid;
+        }
+        int64_t r0 = l - 1;   // last positive region starting at or before x0 (exists: S_excl of the first positive one is 0)
+        while (r0 > 0 && !(w[rs + r0] > 0.0f)) --r0;
+        double* S = reinterpret_cast<double*>(gbw + gi * 128);
+        double* Tu = S + GBW_CAP;
+        uint32_t* uk = reinterpret_cast<uint32_t*>(Tu + GBW_CAP);
+        uint32_t* Bu = uk + GBW_CAP;
+        int slot = 0;
+        for (int64_t i = r0; i < d && slot < GBW_CAP; ++i) {
+            if (i > r0 && (!(w[rs + i] > 0.0f))) continue;
+            const double si = sx(i);
+            if (i > r0 && si >= x1) break;
+            if (slot == GBW_CAP - 1) {   // a further positive region starting inside: link
+                int64_t j = i + 1;
+                while (j < d && !(w[rs + j] > 0.0f)) ++j;
+                if (j < d && sx(j) < x1) {
+                    S[slot] = si;
+                    Tu[slot] = __longlong_as_double(static_cast<long long>(rs + i));
+                    uk[slot] = GB_LINK;
+                    Bu[slot] = 0u;
+                    slot = GBW_CAP;
+                    break;
+                }
+            }
+            const uint32_t u = col[rs + i];
+            const uint4 mu = meta[u];
+            S[slot] = si;
+            Tu[slot] = __longlong_as_double(static_cast<long long>(static_cast<uint64_t>(mu.w) << 32 | mu.z));
+            uk[slot] = u | (mu.y << 27);
+            Bu[slot] = mu.x;
+            ++slot;
+        }
+        for (; slot < GBW_CAP; ++slot) {
+            S[slot] = __longlong_as_double(0x7FF0000000000000ll);   // +inf: never <= x
+            Tu[slot] = 0.0;
+            uk[slot] = 0u;
+            Bu[slot] = 0u;
+        }
+    }
+}
+
+static csaw_status build_gbw(csaw_graph* g, int blocks) {
+    const int64_t V = g->V, E = g->E;
+    if (!g->w || E <= 0 || V >= (int64_t(1) << 27) - 1) return CSAW_OK;
+    unsigned int* bad = nullptr;
+    uint64_t *boff = nullptr, *part = nullptr;
+    auto release = [&]() {
+        if (bad) cudaFree(bad);
+        if (boff) cudaFree(boff);
+        if (part) cudaFree(part);
+        cudaGetLastError();
+    };
+    auto drop = [&]() {   // best-effort: weighted walks keep the per-step scan (k_walk_vscan<float>)
+        release();
+        if (g->gbw) cudaFree(g->gbw);
+        if (g->gwmeta) cudaFree(g->gwmeta);
+        if (g->cpsw) cudaFree(g->cpsw);
+        g->gbw = nullptr;
+        g->gwmeta = nullptr;
+        g->cpsw = nullptr;
+        g->gbw_buckets = 0;
+        cudaGetLastError();
+        return CSAW_OK;
+    };
+    if (cudaMalloc(&bad, sizeof(unsigned int)) != cudaSuccess || cudaMalloc(&boff, sizeof(uint64_t) * (V + 1)) != cudaSuccess ||
+        cudaMalloc(&part, sizeof(uint64_t) * (SCAN_MAX_GRID + 8)) != cudaSuccess ||
+        cudaMalloc(&g->cpsw, sizeof(double) * E) != cudaSuccess)
+        return drop();
+    cudaMemset(bad, 0, sizeof(unsigned int));
+    k_gbw_prefix<<<blocks * 4, 64>>>(g->row_ptr, g->w, V, g->cpsw, bad);
+    unsigned int hb = 0;
+    if (cudaMemcpy(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost) != cudaSuccess || hb) return drop();
+    if (device_scan(GbwSize{g->row_ptr, g->cpsw}, static_cast<uint64_t>(V), ScanToArray{boff}, part, nullptr) != CSAW_OK)
+        return drop();
+    uint64_t nbk = 0;
+    if (cudaMemcpy(&nbk, boff + V, sizeof(nbk), cudaMemcpyDeviceToHost) != cudaSuccess) return drop();
+    size_t fre = 0, tot = 0;
+    if (nbk == 0 || nbk >= (uint64_t(1) << 32) || cudaMemGetInfo(&fre, &tot) != cudaSuccess ||
+        nbk * 128 + sizeof(uint4) * V > fre / 2)
+        return drop();
+    if (cudaMalloc(&g->gbw, nbk * 128) != cudaSuccess || cudaMalloc(&g->gwmeta, sizeof(uint4) * V) != cudaSuccess)
+        return drop();
+    k_gbw_meta<<<blocks, 256>>>(g->row_ptr, g->cpsw, boff, V, g->gwmeta);
+    k_gbw_fill<<<blocks * 4, 256>>>(g->row_ptr, g->col, g->w, g->cpsw, boff, V, nbk, g->gwmeta, g->gbw);
+    if (cudaDeviceSynchronize() != cudaSuccess) return drop();
+    g->gbw_buckets = nbk;
+    release();
+    return CSAW_OK;
+}
+
 // ---------------------------------------------------------------- node2vec edge triangle counts
 // tri[e] = |N(v) ∩ N(u)| for the CSR entry e = (v -> u): the number of "common
 // neighbour" specials of a node2vec step that arrived at v from u (or at u from v), so
@@ -1030,6 +1187,13 @@ CSAW_API csaw_status csaw_graph_create(const csaw_csr* csr, const csaw_graph_opt
         const double ms = tm.ms();
         if (g->ebias) g->cache_build_ms += ms;
     }
+    if ((o.flags & CSAW_GRAPH_WALK_BUCKETS) && g->w && !g->oom) {   // weighted walks: fp64 bucketed index
+        BuildTimer tm;
+        const csaw_status ws = build_gbw(g, blocks);
+        const double ms = tm.ms();
+        if (ws != CSAW_OK) return cleanup(ws);
+        if (g->gbw) g->cache_build_ms += ms;
+    }
     CREATE_CUDA(cudaEventCreate(&g->ev0), "event");
     CREATE_CUDA(cudaEventCreate(&g->ev1), "event");
     CREATE_CUDA(cudaEventCreateWithFlags(&g->ev_done, cudaEventDisableTiming), "event");
@@ -1054,6 +1218,9 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->nrec) cudaFree(g->nrec);
     if (g->gbk) cudaFree(g->gbk);
     if (g->gmeta) cudaFree(g->gmeta);
+    if (g->gbw) cudaFree(g->gbw);
+    if (g->gwmeta) cudaFree(g->gwmeta);
+    if (g->cpsw) cudaFree(g->cpsw);
     if (g->c32) cudaFree(g->c32);
     if (g->ccache) cudaFree(g->ccache);
     if (g->whead) cudaFree(g->whead);
@@ -1078,6 +1245,8 @@ CSAW_API csaw_status csaw_graph_destroy(csaw_graph* g) {
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
     if (g->ev_done) cudaEventDestroy(g->ev_done);
+    if (g->copy_st) cudaStreamDestroy(g->copy_st);
+    for (cudaEvent_t e : g->copy_ev) if (e) cudaEventDestroy(e);
     g->scratch.release_all();
     delete g;
     return CSAW_OK;
@@ -1104,6 +1273,7 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
                         (g->nmp ? static_cast<int64_t>(sizeof(uint64_t) * g->E) : 0) +
                         (g->nrec ? static_cast<int64_t>(sizeof(uint4) * g->E) : 0) +
                         (g->gbk ? static_cast<int64_t>(128 * g->gb_buckets + sizeof(uint4) * g->V) : 0) +
+                        (g->gbw ? static_cast<int64_t>(128 * g->gbw_buckets + sizeof(uint4) * g->V + sizeof(double) * g->E) : 0) +
                         (g->w ? static_cast<int64_t>(sizeof(float) * (g->E + VSCAN_PAD)) : 0) +
                         (g->ebias ? static_cast<int64_t>(sizeof(uint32_t) * (g->E + VSCAN_PAD)) : 0) +
                         static_cast<int64_t>(sizeof(uint64_t) * g->ccache_entries);
@@ -1116,7 +1286,7 @@ CSAW_API csaw_status csaw_graph_info(const csaw_graph* g, csaw_graph_info_t* out
     out->cache_build_ms = g->cache_build_ms;
     out->has_weights = g->w ? 1 : 0;
     out->edge_bias = g->ebias ? 1 : 0;
-    out->walk_buckets = g->gbk ? 1 : 0;
+    out->walk_buckets = (g->gbk ? 1 : 0) | (g->gbw ? 2 : 0);
     return CSAW_OK;
 }
 
@@ -1252,16 +1422,20 @@ CSAW_API csaw_status csaw_walk(const csaw_graph* g, const csaw_bias* bias, int32
         d_path = static_cast<uint32_t*>(p);
     }
     csaw_status s;
+    bool copied = false;
     if (g->oom && g->oomst.zerocopy) {
         s = run_walk(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);   // every kernel reads src_col
     } else if (g->oom) {
         if (b.kind == CSAW_BIAS_MDRW) s = run_mdrw_oom(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
         else s = run_walk_oom(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
     } else {
-        s = run_walk(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st);
+        // a pinned host path the kernel cannot write directly: run_walk may copy it back itself,
+        // chunk by chunk behind the walk
+        uint32_t* h_pipe = (!path_dev && !path_pinned && kp == PtrKind::Pinned) ? path : nullptr;
+        s = run_walk(g, b, length, d_seeds, n, instance_base, rng_seed, d_path, st, h_pipe, &copied);
     }
     if (s != CSAW_OK) return s;
-    if (!path_dev && !path_pinned) {
+    if (!path_dev && !path_pinned && !copied) {
         CSAW_CUDA(cudaMemcpyAsync(path, d_path, sizeof(uint32_t) * nout, cudaMemcpyDeviceToHost, st));
     }
     if (!seeds_dev || !path_dev) CSAW_CUDA(cudaStreamSynchronize(st));

@@ -142,6 +142,12 @@ struct csaw_graph {
     uint4* gbk = nullptr;         // bucketed walk index: [buckets][8] entries {S, u | k_u << 27, bucket of u, T_u}
     uint4* gmeta = nullptr;       // [V] {first bucket, k, T, 0}
     uint64_t gb_buckets = 0;
+    // the same for edge weights (fp64 CTPS, float path R28): buckets of 5 SoA entries
+    // {S f64[5], T_u f64[5], u | (k_u + 24) << 27 [5], bucket of u [5]}, meta {bucket, k + 24, T lo, T hi}
+    uint8_t* gbw = nullptr;
+    uint4* gwmeta = nullptr;
+    double* cpsw = nullptr;       // [E] inclusive left-to-right fp64 prefix of the weights per row
+    uint64_t gbw_buckets = 0;
     // narrow walk index (wix.cuh): built with the cache when every row total T < 2^32
     uint32_t* c32 = nullptr;      // padded leaves: S_{i+1} as u32 (wix.cuh leaf_pos)
     uint32_t* wcol = nullptr;     // padded leaves: col copy
@@ -173,6 +179,10 @@ struct csaw_graph {
     // completion of the previous call's work on its stream: every call's stream waits on
     // it first, so calls on different streams never overlap on the shared scratch
     mutable cudaEvent_t ev_done = nullptr;
+    // pinned host walk outputs of the node2vec index kernel: chunks are copied back on this
+    // stream while the next chunk walks (created on first use)
+    mutable cudaStream_t copy_st = nullptr;
+    mutable cudaEvent_t copy_ev[9] = {};
     // hot-kernel timing: event pairs recorded around each selection-kernel launch
     mutable std::vector<cudaEvent_t> hot_ev;
     mutable int hot_used = 0;
@@ -233,8 +243,12 @@ csaw_status launch_walk_vscan(const csaw_graph* g, bool weights, const uint32_t*
 // false if run_walk's kernel for b writes the path with scattered per-thread stores (the
 // node2vec index kernel): a pinned host path is then staged in device memory and copied
 bool walk_path_direct_ok(const csaw_graph* g, const csaw_bias& b);
+// h_path (pinned host, optional): run_walk copies the path there itself -- the node2vec index
+// walk in chunks of walkers whose copies overlap the next chunk's walk (the caller then skips
+// its own copy); h_path is ignored (false returned in *copied) for every other kernel
 csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds,
-                     int64_t n, uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st);
+                     int64_t n, uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st,
+                     uint32_t* h_path = nullptr, bool* copied = nullptr);
 // pinned host outputs, device-mapped (the fused sampler writes them directly; the batched
 // driver's scattered writes stage through device scratch instead)
 struct PinnedOut {

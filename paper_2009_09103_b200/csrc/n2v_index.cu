@@ -562,7 +562,8 @@ __device__ __forceinline__ uint32_t n2x_finish(const N2xArgs& a, int64_t dq1, co
 // others' copies are in flight; K = 1 measured best: the register budget of one group keeps
 // 32 warps per SM); the walkers of a group advance in lock step (same t).  The member-position
 // probes stay vector loads through L1 (hub lists are reused across walkers: 45 % L1 hits),
-// unless N2X_TMA_PROBES.
+// (A/B r02: member probes by 16 B bulk copies 10.4 ms, a splitter gap fetched whole by one bulk
+// copy 9.17 ms, both against 8.16 ms through L1 -- removed).
 #ifndef N2X_TMA
 #define N2X_TMA 1   // node2vec index walks through the TMA kernel (A/B r02 cfg3: 8.28 ms vs 10.14 ms with vector loads)
 #endif
@@ -571,15 +572,6 @@ __device__ __forceinline__ uint32_t n2x_finish(const N2xArgs& a, int64_t dq1, co
 #endif
 #ifndef N2X_TMA_K
 #define N2X_TMA_K 1   // A/B r02 cfg3: K = 1 8.28 ms; K = 2 9.54 ms (80 regs) / 13.6 ms (64 regs + stack)
-#endif
-#ifndef N2X_TMA_PROBES
-#define N2X_TMA_PROBES 0   // each member probe by a 16 B bulk copy (A/B r02: slower)
-#endif
-#ifndef N2X_TMA_GAP
-#define N2X_TMA_GAP 0      // a splitter gap that fits N2X_GAP_BYTES is fetched whole by one bulk copy (A/B r02 cfg3: 9.17 ms vs 8.16 ms probing through L1)
-#endif
-#ifndef N2X_GAP_BYTES
-#define N2X_GAP_BYTES 112   // static shared memory: 8 warps x 32 lanes x 112 B + the records fit 48 KB
 #endif
 #ifndef N2X_TMA_WARPS
 #define N2X_TMA_WARPS 8
@@ -608,8 +600,6 @@ struct N2xGroup {           // one group of 32 walkers (per-lane fields)
     N2xSearch q;            // the step in flight
     int32_t t;              // step (group-uniform)
     uint32_t parity;        // mbarrier phase
-    bool probing;           // waiting for member positions (else for records)
-    bool gapping;           // ... as one splitter gap (N2X_TMA_GAP)
     bool live;              // group-uniform: the group holds walkers
 };
 
@@ -622,12 +612,6 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
     // records then hit 8 distinct 16 B bank groups per 8-lane phase (conflict-free) -- 64 B
     // records at a 64 B stride were a 4-way conflict per phase (ncu r02: 75 % excessive wavefronts)
     __shared__ __align__(128) uint4 recs[N2X_TMA_WARPS][K][32][N2X_SMEM_STRIDE];
-#if N2X_TMA_PROBES
-    __shared__ __align__(16) uint4 prb[N2X_TMA_WARPS][K][32];          // 16 B around the probed member
-#endif
-#if N2X_TMA_GAP
-    __shared__ __align__(16) uint4 gapb[N2X_TMA_WARPS][K][32][N2X_GAP_BYTES / 16];   // a splitter gap's members
-#endif
     __shared__ __align__(8) uint64_t bars[N2X_TMA_WARPS][K];
     const int lane = lane_id(), wib = threadIdx.x >> 5;
     const uint32_t wq = a.wq, w1 = a.w1, wp = a.wp;
@@ -651,7 +635,6 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
         if (lane == 0) n2x_expect(&bars[wib][k], cnt * (16u * N2X_U4));
         __syncwarp();
         if (me) n2x_bulk(&recs[wib][k][lane][0], a.rec + N2X_U4 * G[k].e, 16u * N2X_U4, &bars[wib][k]);
-        G[k].probing = false;
     };
     // a new group: step 0 (uniform, R16) for each lane's walker, then its first record
     auto start_group = [&](int k) {
@@ -692,61 +675,7 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
             // nothing to fetch in this group (all isolated / L = 0): take the next one
         }
     };
-#if N2X_TMA_PROBES
-    // member-position probes of the lanes still searching; false if none
-    auto issue_probes = [&](int k) -> bool {
-        const bool me = G[k].w < a.n && G[k].q.l < G[k].q.h;
-        const unsigned m = __ballot_sync(FULL, me);
-        if (!m) return false;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (lane == 0) n2x_expect(&bars[wib][k], __popc(m) * 16u);
-        __syncwarp();
-        if (me) {
-            const uint32_t mid = (G[k].q.l + G[k].q.h) >> 1;
-            const uintptr_t ad = reinterpret_cast<uintptr_t>(G[k].q.I + mid) & ~static_cast<uintptr_t>(15);
-            n2x_bulk(&prb[wib][k][lane], reinterpret_cast<const void*>(ad), 16u, &bars[wib][k]);
-            ++probes_all;
-        }
-        G[k].probing = true;
-        return true;
-    };
-
-#endif
-#if N2X_TMA_GAP
-    // Lanes still searching narrow their gap by vector-load probes until its members fit one
-    // bulk copy (<= N2X_GAP_BYTES, 16 B aligned), then fetch the whole gap; false if no lane does.
-    auto issue_gap = [&](int k) -> bool {
-        bool me = G[k].w < a.n && G[k].q.l < G[k].q.h;
-        uintptr_t lo = 0, hi = 0;
-        if (me) {
-            for (;;) {
-                lo = reinterpret_cast<uintptr_t>(G[k].q.I + G[k].q.l) & ~static_cast<uintptr_t>(15);
-                hi = (reinterpret_cast<uintptr_t>(G[k].q.I + G[k].q.h) + 15) & ~static_cast<uintptr_t>(15);
-                if (hi - lo <= N2X_GAP_BYTES || G[k].q.l >= G[k].q.h) break;
-                const uint32_t mid = (G[k].q.l + G[k].q.h) >> 1;
-                const uint32_t p = __ldg(G[k].q.I + mid);
-                ++probes_all;
-                if (n2x_S(wq, dq1, p, mid, G[k].q.sub) <= G[k].q.x) { G[k].q.l = mid + 1; G[k].q.pos = p; }
-                else G[k].q.h = mid;
-            }
-            me = G[k].q.l < G[k].q.h;
-        }
-        const uint32_t bytes = me ? static_cast<uint32_t>(hi - lo) : 0u;
-        const uint32_t total = __reduce_add_sync(FULL, bytes);
-        if (total == 0) return false;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (lane == 0) n2x_expect(&bars[wib][k], total);
-        __syncwarp();
-        if (me) {
-            n2x_bulk(&gapb[wib][k][lane][0], reinterpret_cast<const void*>(lo), bytes, &bars[wib][k]);
-            probes_all += bytes / 32 + 1;   // statistics: sectors requested
-        }
-        G[k].gapping = true;
-        G[k].probing = true;
-        return true;
-    };
-#endif
-    for (int k = 0; k < K; ++k) { G[k].parity = 0; G[k].live = false; G[k].gapping = false; }
+    for (int k = 0; k < K; ++k) { G[k].parity = 0; G[k].live = false; }
     for (int k = 0; k < K; ++k) start_group(k);
     for (;;) {
         bool any = false;
@@ -757,7 +686,7 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
             n2x_wait(&bars[wib][k], G[k].parity);
             G[k].parity ^= 1u;
             const bool me = G[k].w < a.n;
-            if (!G[k].probing) {   // records arrived: path entry, then the step's search
+            {   // records arrived: path entry, then the step's search
                 if (me) {
                     const uint4 ra = recs[wib][k][lane][0], rb = recs[wib][k][lane][1];
                     const uint32_t* P = reinterpret_cast<const uint32_t*>(&recs[wib][k][lane][2]);
@@ -773,38 +702,8 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
                     start_group(k);
                     continue;
                 }
-            } else if (G[k].gapping) {   // a splitter gap's members arrived: search them in shared memory
-#if N2X_TMA_GAP
-                if (me && G[k].q.l < G[k].q.h) {
-                    const uintptr_t base = reinterpret_cast<uintptr_t>(G[k].q.I + G[k].q.l) & ~static_cast<uintptr_t>(15);
-                    const uint32_t* gm = reinterpret_cast<const uint32_t*>(&gapb[wib][k][lane][0]);
-                    while (G[k].q.l < G[k].q.h) {
-                        const uint32_t mid = (G[k].q.l + G[k].q.h) >> 1;
-                        const uint32_t p = gm[(reinterpret_cast<uintptr_t>(G[k].q.I + mid) - base) >> 2];
-                        if (n2x_S(wq, dq1, p, mid, G[k].q.sub) <= G[k].q.x) { G[k].q.l = mid + 1; G[k].q.pos = p; }
-                        else G[k].q.h = mid;
-                    }
-                }
-                G[k].gapping = false;
-#endif
             }
-#if N2X_TMA_PROBES
-            else if (me && G[k].q.l < G[k].q.h) {   // a probe arrived
-                const uint32_t mid = (G[k].q.l + G[k].q.h) >> 1;
-                const uint4 pv = prb[wib][k][lane];
-                const uint32_t wsel = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(G[k].q.I + mid) >> 2) & 3u);
-                const uint32_t p = wsel == 0 ? pv.x : wsel == 1 ? pv.y : wsel == 2 ? pv.z : pv.w;
-                if (n2x_S(wq, dq1, p, mid, G[k].q.sub) <= G[k].q.x) { G[k].q.l = mid + 1; G[k].q.pos = p; }
-                else G[k].q.h = mid;
-            }
-#endif
             __syncwarp();
-#if N2X_TMA_PROBES
-            if (issue_probes(k)) continue;
-#else
-#if N2X_TMA_GAP
-            if (!G[k].gapping && issue_gap(k)) continue;
-#endif
             if (me) {   // the member positions through L1 (hub lists are reused across walkers; whole
                         // 128 B lines from DRAM: .L2::64B measured 7.81 vs 7.54 ms on cfg3)
                 while (G[k].q.l < G[k].q.h) {
@@ -815,7 +714,6 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
                     else G[k].q.h = mid;
                 }
             }
-#endif
             // every lane's region is known: finish the step, fetch the next records
             if (me) {
                 G[k].e = G[k].q.rs + n2x_finish(a, dq1, G[k].q);

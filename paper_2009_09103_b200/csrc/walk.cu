@@ -247,6 +247,92 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_gb(WalkArgs a, cons
     }
 }
 
+// Edge-weight walk (float path, R28) over the weighted bucketed index (capi.cu build_gbw): x =
+// r(U) T in fp64, bucket floor(x 2^-k), one 128 B line of 5 SoA entries read by lanes 0..4, the
+// last entry with S <= x -- it carries the next vertex, its bucket table, shift and fp64 T.  The
+// row sums are the oracle's left-to-right fp64 sums, so every pick is the oracle's (no boundary
+// excuse).  A link entry continues in the row's fp64 prefix: the last positive-weight region
+// with S_excl <= x, 32 entries at a time.
+__global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_gbw(WalkArgs a, const uint8_t* __restrict__ gbw,
+                                                               const uint4* __restrict__ meta,
+                                                               const double* __restrict__ cpsw,
+                                                               const float* __restrict__ w) {
+    constexpr int CAP = 5, KB = 24;
+    const int lane = lane_id();
+    unsigned long long bytes = 0, steps = 0, links = 0;
+    for (uint64_t wk = walker_ticket(a.counters + 7); wk < a.n; wk = walker_ticket(a.counters + 7)) {
+        uint32_t cur = a.seeds[wk];
+        const uint32_t inst = a.base + static_cast<uint32_t>(wk);
+        PathWriter pw{a.path + wk * (static_cast<uint64_t>(a.L) + 1), NONE, a.L};
+        pw.put(0, cur);
+        const uint4 m0 = __ldg(meta + cur);
+        uint32_t B = m0.x;
+        int k = static_cast<int>(m0.y) - KB;
+        double T = __longlong_as_double(static_cast<long long>(static_cast<uint64_t>(m0.w) << 32 | m0.z));
+        uint64_t ubuf = 0;
+        for (int32_t t = 0; t < a.L; ++t) {
+            if ((t & 31) == 0)
+                ubuf = draw_u64(a.key, inst, static_cast<uint32_t>(t + lane), 0u, word3(PURPOSE_EDGE, 0, 0));
+            const uint64_t U = __shfl_sync(FULL, ubuf, t & 31);
+            uint32_t nxt = NONE;
+            if (cur != NONE && T > 0.0) {   // T = 0: every weight of the row is 0, the walk ends (R20)
+                const double x = (static_cast<double>(U >> 11) * (1.0 / 9007199254740992.0)) * T;
+                const uint64_t bi = static_cast<uint64_t>(ldexp(x, -k));
+                const uint8_t* line = gbw + (static_cast<uint64_t>(B) + bi) * 128;
+                double S = __longlong_as_double(0x7FF0000000000000ll), Tu = 0.0;
+                uint32_t uk = 0, Bu = 0;
+                if (lane < CAP) {
+                    S = __ldg(reinterpret_cast<const double*>(line) + lane);
+                    Tu = __ldg(reinterpret_cast<const double*>(line) + CAP + lane);
+                    uk = __ldg(reinterpret_cast<const uint32_t*>(line + 16 * CAP) + lane);
+                    Bu = __ldg(reinterpret_cast<const uint32_t*>(line + 20 * CAP) + lane);
+                }
+                const int fl = 31 - __clz(__ballot_sync(FULL, lane < CAP && S <= x));   // entry 0 always passes
+                const uint32_t uks = __shfl_sync(FULL, uk, fl);
+                const double Ts = __shfl_sync(FULL, Tu, fl);
+                const uint32_t Bs = __shfl_sync(FULL, Bu, fl);
+                bytes += 128;
+                if (uks != 0xFFFFFFFFu) {
+                    nxt = uks & 0x7FFFFFFu;
+                    k = static_cast<int>(uks >> 27) - KB;
+                    B = Bs;
+                    T = Ts;
+                } else {   // link: the last positive region with S_excl <= x at or after CSR entry j0
+                    ++links;
+                    uint64_t j0 = static_cast<uint64_t>(__double_as_longlong(Ts));
+                    const uint64_t re = static_cast<uint64_t>(__ldg(a.rp + cur + 1));
+                    uint64_t best = j0;   // entry j0 itself qualifies (S_excl(j0) <= x, positive)
+                    for (;; j0 += 32) {
+                        const uint64_t j = j0 + lane;
+                        const bool in = j < re;
+                        const double sxj = in ? __ldg(cpsw + j - 1) : __longlong_as_double(0x7FF0000000000000ll);
+                        const bool le = sxj <= x;
+                        const unsigned ok = __ballot_sync(FULL, le && in && __ldg(w + j) > 0.0f);
+                        if (ok) best = j0 + (31 - __clz(ok));
+                        bytes += 384;
+                        if (!__shfl_sync(FULL, le, 31)) break;   // a later entry starts beyond x (or the row ended)
+                    }
+                    nxt = __ldg(a.col + best);
+                    const uint4 mu = __ldg(meta + nxt);
+                    B = mu.x;
+                    k = static_cast<int>(mu.y) - KB;
+                    T = __longlong_as_double(static_cast<long long>(static_cast<uint64_t>(mu.w) << 32 | mu.z));
+                    bytes += 20;
+                }
+                ++steps;
+            }
+            cur = nxt;
+            pw.put(t + 1, nxt);
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if (bytes) atomicAdd(a.counters + 3, bytes + 4ull * steps);
+        if (steps) atomicAdd(a.counters + 1, steps);
+        if (links) atomicAdd(a.counters + 2, links);
+    }
+}
+
 // Degree-biased walk over the vertex heads (wix.cuh): a step is one coalesced 512 B head
 // read (record + top level, or the whole row when d <= 60), then K - 1 internal nodes and
 // one leaf when the row is larger -- one dependent round trip less than record + nodes.
@@ -1824,12 +1910,14 @@ static int walk_grid(const csaw_graph* g, int64_t n) {
     return static_cast<int>(std::max<int64_t>(1, (warps + WALK_WARPS - 1) / WALK_WARPS));
 }
 
+constexpr int N2X_CHUNKS = 8;   // pipelined host copies of the node2vec index walk (copy_ev holds K + 1 events)
 bool walk_path_direct_ok(const csaw_graph* g, const csaw_bias& b) {
     return !(b.kind == CSAW_BIAS_NODE2VEC && g->n2x_rec && !g->w && !g->oom && n2v_integer_scale(b.p, b.q) != 0);
 }
 
 csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, const uint32_t* d_seeds, int64_t n,
-                     uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st) {
+                     uint64_t base, uint64_t seed, uint32_t* d_path, cudaStream_t st, uint32_t* h_path, bool* copied) {
+    if (copied) *copied = false;
     // argument checks before any statistics / timing state is recorded
     if (b.kind == CSAW_BIAS_NODE2VEC && !g->rows_sorted)
         return fail(CSAW_ERR_BAD_GRAPH, "node2vec needs sorted CSR rows (N(prev) membership)");
@@ -1846,7 +1934,11 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
     const uint32_t* colp = g->col ? g->col : g->oomst.src_col;
     WalkArgs a{g->row_ptr, colp, g->deg, d_seeds, static_cast<uint64_t>(n), length,
                static_cast<uint32_t>(base), key, d_path, static_cast<unsigned long long*>(cnt), g->ccache};
-    if (b.kind == CSAW_BIAS_DEGREE && g->gbk) {
+    if (b.kind == CSAW_BIAS_WEIGHT && g->gbw) {
+        constexpr int hw = 2;
+        const int64_t hwarps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 64);
+        k_walk_gbw<<<static_cast<int>((hwarps + hw - 1) / hw), hw * 32, 0, st>>>(a, g->gbw, g->gwmeta, g->cpsw, g->w);
+    } else if (b.kind == CSAW_BIAS_DEGREE && g->gbk) {
         constexpr int hw = 2;   // warps per block: the few walkers (cfg2: 4,000 warps) spread over all SMs
         const int64_t hwarps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 64);
         k_walk_gb<<<static_cast<int>((hwarps + hw - 1) / hw), hw * 32, 0, st>>>(a, g->gbk, g->gmeta, g->cps,
@@ -1909,10 +2001,36 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         na.wf[2] = static_cast<float>(1.0 / b.q);
         na.ew = g->w;   // weighted graph: b = alpha * w(e) (R33), always the float path
         if (g->w) k_node2vec<true><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(na);
-        else if (m && g->n2x_rec && na.wint[0] < (1u << 30) && na.wint[1] < (1u << 30) && na.wint[2] < (1u << 30))
-            CSAW_TRY(launch_node2vec_index(g, d_seeds, static_cast<uint64_t>(n), length, static_cast<uint32_t>(base), key,
-                                           d_path, static_cast<unsigned long long*>(cnt), na.wint[0], na.wint[1],
-                                           na.wint[2], st));
+        else if (m && g->n2x_rec && na.wint[0] < (1u << 30) && na.wint[1] < (1u << 30) && na.wint[2] < (1u << 30)) {
+            // a pinned host path: N2X_CHUNKS launches over consecutive walker ranges, each range's
+            // rows copied back on g->copy_st while the next range walks (the host link, not the
+            // walk, bounds an end-to-end call: cfg3 moves 618 MB of paths)
+            const bool pipe = h_path && n >= 8 * N2X_CHUNKS * 32;
+            if (pipe && !g->copy_st) {
+                CSAW_CUDA(cudaStreamCreateWithFlags(&g->copy_st, cudaStreamNonBlocking));
+                for (cudaEvent_t& e : g->copy_ev) CSAW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
+            const int K = pipe ? N2X_CHUNKS : 1;
+            const uint64_t row = static_cast<uint64_t>(length) + 1;
+            for (int c = 0; c < K; ++c) {
+                const uint64_t lo = static_cast<uint64_t>(n) * c / K, hi = static_cast<uint64_t>(n) * (c + 1) / K;
+                if (c > 0) CSAW_CUDA(cudaMemsetAsync(static_cast<unsigned long long*>(cnt) + 7, 0, 8, st));   // group ticket
+                CSAW_TRY(launch_node2vec_index(g, d_seeds + lo, hi - lo, length, static_cast<uint32_t>(base + lo), key,
+                                               d_path + lo * row, static_cast<unsigned long long*>(cnt), na.wint[0],
+                                               na.wint[1], na.wint[2], st));
+                if (pipe) {
+                    CSAW_CUDA(cudaEventRecord(g->copy_ev[c], st));
+                    CSAW_CUDA(cudaStreamWaitEvent(g->copy_st, g->copy_ev[c], 0));
+                    CSAW_CUDA(cudaMemcpyAsync(h_path + lo * row, d_path + lo * row, sizeof(uint32_t) * (hi - lo) * row,
+                                              cudaMemcpyDeviceToHost, g->copy_st));
+                }
+            }
+            if (pipe) {
+                CSAW_CUDA(cudaEventRecord(g->copy_ev[N2X_CHUNKS], g->copy_st));
+                CSAW_CUDA(cudaStreamWaitEvent(st, g->copy_ev[N2X_CHUNKS], 0));
+                if (copied) *copied = true;
+            }
+        }
         else if (m && g->tri) k_node2vec_tri<<<walk_grid(g, n), N2T_WARPS * 32, 0, st>>>(na, g->tri);
         else if (m) k_node2vec<false><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(na);
         else k_node2vec<true><<<walk_grid(g, n), WALK_WARPS * 32, 0, st>>>(na);

@@ -109,3 +109,54 @@ def test_buckets_sharding_and_seeds():
     with pytest.raises(cs.CsawError):
         cs.csaw_walk(Gb, "degree", bad, 10, rng_seed=1)
     Gb.close(); Gh.close()
+
+
+# ------------------------------------------------------------------ edge weights (float path, R28)
+def weighted(rp, col, w):
+    rpt = torch.as_tensor(np.asarray(rp, dtype=np.int64))
+    ct = torch.as_tensor(np.asarray(col).astype(np.uint32).view(np.int32))
+    wt = torch.as_tensor(np.asarray(w, dtype=np.float32))
+    G = cs.csaw_graph_create(rpt.to(DEV), ct.to(DEV), weights=wt.to(DEV), walk_buckets=True)
+    return G, O.Graph(rpt.numpy(), ct.numpy().view(np.uint32), wt.numpy())
+
+
+def check_weight_exact(G, og, seeds, length, rng_seed, walkers):
+    path = u32(cs.csaw_walk(G, "weight", torch.as_tensor(np.asarray(seeds, np.uint32).view(np.int32)).to(DEV),
+                            length, rng_seed=rng_seed))
+    for i in walkers:
+        ref = O.weight_walk(og, length, int(seeds[i]), i, rng_seed)
+        if not np.array_equal(path[i], ref):
+            t = int(np.argmax(path[i] != ref))
+            raise AssertionError(f"walker {i}: first divergence at {t}: gpu {path[i][t]} oracle {ref[t]}")
+    return path
+
+
+@pytest.mark.parametrize("zero_frac", [0.0, 0.2])
+def test_weight_buckets_exact(zero_frac):
+    """The weighted buckets sum each row left to right in fp64 like the oracle, so weighted
+    walks equal the oracle's exactly (no 1e-6 boundary excuse)."""
+    from synth import edge_weights
+    g = rmat_csr(1 << 15, 1 << 19, 5, device=DEV).to("cpu")
+    w = edge_weights(g, 3, zero_frac=zero_frac)
+    G, og = weighted(g.row_ptr, g.col_idx, w)
+    assert G.info()["walk_buckets"] & 2
+    seeds = instance_seeds(g, 512, set_id=3).numpy()
+    check_weight_exact(G, og, seeds, 300, 5, range(0, 512, 3))
+    G.close()
+
+
+def test_weight_buckets_links():
+    """Row 0: four unit-weight hubs and 2,000 leaves of weight 2^-14 -- 32 leaf regions per
+    bucket, so buckets link into the fp64 prefix; picks still equal the oracle's."""
+    rp, col = skew_csr()
+    src = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
+    w = np.ones(len(col), np.float32)
+    w[(src == 0) & (col >= 5)] = 2.0 ** -14
+    w[(col == 0) & (src >= 5)] = 0.5
+    G, og = weighted(rp, col, w)
+    assert G.info()["walk_buckets"] & 2
+    seeds = np.zeros(2048, dtype=np.uint32)
+    seeds[1::2] = 5
+    check_weight_exact(G, og, seeds, 64, 8, range(0, 2048, 7))
+    assert cs.csaw_stats(G)["cache_probes"] > 0, "no weighted bucket link was taken"
+    G.close()

@@ -131,9 +131,12 @@ def test_cfg2_weight_walk_full():
     og = O.Graph.from_torch(g, w)
     seeds = instance_seeds(g, cfg.n_instances).to(DEV)
     sv = u32(seeds)
-    G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, weights=w)
+    G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, weights=w)                       # per-step scans
+    Gb = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=0, weights=w, walk_buckets=True)   # the bench's launch
+    assert Gb.info()["walk_buckets"] & 2
     for seed in SEEDS:
         pw = u32(cs.csaw_walk(G, "weight", seeds, cfg.length, rng_seed=seed))
+        pb = u32(cs.csaw_walk(Gb, "weight", seeds, cfg.length, rng_seed=seed))
         t0 = time.time()
         ref = O.parallel_run(og, "weight_walk", sv, 0, seed, length=cfg.length)
         log(f"cfg2_weight seed {seed}: oracle over all {len(sv)} walkers in {time.time() - t0:.1f} s")
@@ -144,8 +147,11 @@ def test_cfg2_weight_walk_full():
                 assert mg[t] <= 1e-6, f"seed {seed}: walker {i} step {t} margin {mg[t]}"
                 excused += 1
         assert excused <= 4, excused
+        # the weighted buckets sum rows left to right like the oracle: every walk is the oracle's
+        bad = [i for i, (rp, _) in enumerate(ref) if not np.array_equal(pb[i], rp)]
+        assert not bad, f"seed {seed}: bucketed weighted walkers {bad[:5]} differ from the oracle"
         check_edges_exist(og, pw[:, :-1].ravel(), pw[:, 1:].ravel())
-    release(G)
+    release(G, Gb)
 
 
 # ------------------------------------------------------------------ cfg3

@@ -97,3 +97,22 @@ def test_index_equals_tri_and_merge_large_batch():
     assert torch.equal(cs.csaw_walk(Gx, b, seeds[:500], 10, rng_seed=1), cs.csaw_walk(Gm, b, seeds[:500], 10, rng_seed=1))
     for G in (Gx, Gt, Gm):
         G.close()
+
+
+def test_index_pinned_host_path_pipelined(medium):
+    """A pinned host path: the walk runs in 8 walker ranges whose rows are copied back while the
+    next range walks (g->copy_st); same rows as a device output and as the oracle."""
+    G, og, g = medium
+    seeds = instance_seeds(g, 4096, set_id=6).numpy()
+    st = torch.as_tensor(seeds.view(np.int32)).to(DEV)
+    dev = cs.csaw_walk(G, cs.make_bias("node2vec", p=2.0, q=0.5), st, 40, rng_seed=21)
+    host = torch.empty_like(dev, device="cpu").pin_memory()
+    cs.csaw_walk(G, cs.make_bias("node2vec", p=2.0, q=0.5), st.cpu().pin_memory(), 40, rng_seed=21, out=host)
+    assert torch.equal(host, dev.cpu())
+    check_walk(G, og, "node2vec", seeds, 40, rng_seed=21, p=2.0, q=0.5, walkers=range(0, 4096, 97))
+    # a second call on another stream right after (shared scratch, copy stream ordering)
+    s2 = torch.cuda.Stream(device=DEV)
+    host2 = torch.empty_like(host).pin_memory()
+    cs.csaw_walk(G, cs.make_bias("node2vec", p=2.0, q=0.5), st, 40, rng_seed=21, out=host2, stream=s2)
+    s2.synchronize()
+    assert torch.equal(host2, host)
