@@ -160,3 +160,54 @@ def test_weight_buckets_links():
     check_weight_exact(G, og, seeds, 64, 8, range(0, 2048, 7))
     assert cs.csaw_stats(G)["cache_probes"] > 0, "no weighted bucket link was taken"
     G.close()
+
+
+def directed_csr(V=3000, E=40000, seed=11):
+    """A random directed graph (sorted, deduplicated rows) where ~1/4 of the vertices have no
+    out-edges: regions of bias 0 (deg(u) = 0), rows whose every region is empty (T = 0: the walk
+    ends, R20), and isolated seeds."""
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, V, E)
+    dst = rng.integers(0, V, E)
+    sink = rng.random(V) < 0.25
+    keep = ~sink[src] & (src != dst)
+    pairs = np.unique(np.stack([src[keep], dst[keep]], 1), axis=0)
+    rp = np.zeros(V + 1, np.int64)
+    np.add.at(rp, pairs[:, 0] + 1, 1)
+    return np.cumsum(rp), pairs[:, 1].astype(np.uint32)
+
+
+def test_buckets_directed_empty_regions():
+    rp, col = directed_csr()
+    Gb, Gh, og = graphs(rp, col)
+    assert Gb.info()["walk_buckets"] == 1
+    seeds = np.arange(0, len(rp) - 1, 3, dtype=np.uint32)
+    pb = check_walk(Gb, og, "degree", seeds, 120, rng_seed=12)
+    ph = u32(cs.csaw_walk(Gh, "degree", torch.as_tensor(seeds.view(np.int32)).to(DEV), 120, rng_seed=12))
+    assert np.array_equal(pb, ph)
+    assert (pb == cs.NONE).any(), "expected walks that end (rows without positive-bias neighbours)"
+    Gb.close(); Gh.close()
+
+
+def test_weight_buckets_directed_zero_rows():
+    rp, col = directed_csr(seed=13)
+    rng = np.random.default_rng(5)
+    w = (rng.integers(1, 1 << 16, len(col)) * 2.0 ** -20).astype(np.float32)
+    w[rng.random(len(col)) < 0.3] = 0.0          # zero weights, whole zero rows
+    G, og = weighted(rp, col, w)
+    assert G.info()["walk_buckets"] & 2
+    seeds = np.arange(0, len(rp) - 1, 3, dtype=np.uint32)
+    p = check_weight_exact(G, og, seeds, 120, 14, range(len(seeds)))
+    assert (p == cs.NONE).any()
+    G.close()
+
+
+def test_buckets_short_and_empty_calls():
+    g = rmat_csr(1 << 12, 1 << 16, 3, device=DEV).to("cpu")
+    Gb, Gh, og = graphs(g.row_ptr, g.col_idx)
+    seeds = instance_seeds(g, 40, set_id=5).numpy()
+    for L in (0, 1, 31, 32, 33):
+        check_walk(Gb, og, "degree", seeds, L, rng_seed=2)
+    empty = torch.empty(0, dtype=torch.int32, device=DEV)
+    assert cs.csaw_walk(Gb, "degree", empty, 10, rng_seed=1).shape == (0, 11)
+    Gb.close(); Gh.close()
