@@ -87,8 +87,8 @@ def parse_args(argv=None):
                     help="degree walks: the vertex-head walk index (k_walk_head) instead of the bucketed index "
                          "(CSAW_GRAPH_WALK_BUCKETS, k_walk_gb) (A/B)")
     ap.add_argument("--mdrw-alt-records", action="store_true",
-                    help="MDRW: the other slot-record layout (CSAW_GRAPH_MDRW_ALT_RECORDS: 16 B {v, degree, row} "
-                         "records in memory instead of packed 8 B + vertex ids) (A/B)")
+                    help="MDRW: the other slot-record layout (CSAW_GRAPH_MDRW_ALT_RECORDS: packed 8 B {row, degree} "
+                         "+ vertex ids instead of 16 B {v, degree, row} records) (A/B)")
     ap.add_argument("--next-meta", action="store_true",
                     help="MDRW: 8 B next-vertex metadata + col (CSAW_GRAPH_NEXT_META) instead of the 16 B "
                          "next-vertex records (CSAW_GRAPH_NEXT_RECORD) (A/B)")
@@ -529,11 +529,12 @@ def main():
         use_meta = (not args.no_cache) and cfg.workload == "mdrw"
         use_eb = args.no_cache and not args.gather_bias and cfg.workload == "walk" and cfg.bias == "degree"
         wts = edge_weights(g, cfg.graph_seed) if cfg.bias == "weight" else None
-        # walks on the bucketed index need no narrow walk index / vertex heads (512 B per vertex)
+        # (the narrow walk index + vertex heads stay built beside the buckets: without them the bucket
+        # build measured 222 vs 20-54 ms and the walk 1.233 vs 1.209 ms on cfg2)
         use_buckets = (use_cache or cfg.bias == "weight") and cfg.workload == "walk" and not args.no_walk_buckets
         G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache, node2vec_tri=use_tri,
                                  next_meta=use_meta and args.next_meta, next_record=use_meta and not args.next_meta,
-                                 walk_index=use_cache and not use_buckets, node2vec_index=use_tri, edge_bias=use_eb,
+                                 walk_index=use_cache, node2vec_index=use_tri, edge_bias=use_eb,
                                  weights=wts, walk_buckets=use_buckets,
                                  flags=cs.CSAW_GRAPH_MDRW_ALT_RECORDS if args.mdrw_alt_records else 0)
     ginfo = G.info()

@@ -232,8 +232,8 @@ typedef struct {
  *   OOM_NO_CHUNK_CACHE  out-of-memory mode without the automatic chunk-total cache
  *   OOM_ZC_NO_PREFIX    zero-copy OOM mode keeps no col_idx prefix resident (all host reads)
  *   MDRW_GENERIC        MDRW uses the general kernel (shared-memory block totals) for every pool
- *   MDRW_ALT_RECORDS    MDRW pools <= 2,048 slots: the other slot-record layout (16 B records in
- *                       memory, 8 B packed row << 24 | degree in out-of-memory mode) */
+ *   MDRW_ALT_RECORDS    MDRW pools <= 2,048 slots: 8 B packed slot records row << 24 | degree
+ *                       + a vertex-id array instead of 16 B {v, degree, row} records */
 /* csaw_graph_opts.flags, out-of-memory mode: the partition store
  * -- the full col_idx the §5 scheduler copies partitions from -- lives in the
  * HBM of opts.store_device instead of pinned host memory.  Partition loads become

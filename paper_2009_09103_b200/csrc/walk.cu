@@ -2038,12 +2038,11 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         const uint32_t m = static_cast<uint32_t>(b.pool_size);
         const uint32_t nblk = (m + 31) / 32;
         if (nblk <= 64 && !(g->flags & CSAW_GRAPH_MDRW_GENERIC)) {   // pools up to 2,048 slots (cfg5: 2,000)
-            // slot records: 8 B packed in memory (the n x m pool state stays L2-resident: cfg5
-            // 96 MB instead of 128 MB of 16 B records), 16 B in the OOM zero-copy mode (there the
-            // separate vertex-id load lands on the step's chain: 14 % slower packed);
-            // CSAW_GRAPH_MDRW_ALT_RECORDS picks the other layout (A/B)
+            // slot records: 16 B {v, degree, row} (the slot's vertex comes with the block, no separate
+            // vertex-id read per step: cfg5 with next-vertex records 2.61 vs 2.76 ms packed); with
+            // CSAW_GRAPH_MDRW_ALT_RECORDS 8 B packed {row << 24 | degree} + a u32 vertex-id array (A/B)
             const bool alt = (g->flags & CSAW_GRAPH_MDRW_ALT_RECORDS) != 0;
-            const bool packed = g->max_deg < (int64_t(1) << 24) && g->E < (int64_t(1) << 40) && (!g->oom != alt);
+            const bool packed = g->max_deg < (int64_t(1) << 24) && g->E < (int64_t(1) << 40) && alt;
             void *pool = nullptr, *pvid = nullptr;
             if (packed) {
                 CSAW_TRY(g->scratch.get(SL_TMP0, sizeof(uint64_t) * n * m, &pool));

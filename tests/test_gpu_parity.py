@@ -282,7 +282,7 @@ def test_mdrw_pool_sizes(medium, m, n, L):
     G2, og2, g2 = medium
     s = mdrw_seeds(g2, n, m).numpy()
     e = check_mdrw(G2, og2, s, L, rng_seed=7, instances=range(0, n, max(1, n // 40)))
-    for fl in (cs.CSAW_GRAPH_MDRW_GENERIC, cs.CSAW_GRAPH_MDRW_ALT_RECORDS):   # large-pool kernel; 16 B slot records
+    for fl in (cs.CSAW_GRAPH_MDRW_GENERIC, cs.CSAW_GRAPH_MDRW_ALT_RECORDS):   # large-pool kernel; packed slot records
         Gv = cs.csaw_graph_create(g2.row_ptr.to(DEV), g2.col_idx.to(DEV), device=0, flags=fl)
         e2 = u32(cs.csaw_walk(Gv, cs.make_bias("mdrw", pool_size=m), torch.as_tensor(s.view(np.int32)).to(DEV), L,
                               rng_seed=7))
