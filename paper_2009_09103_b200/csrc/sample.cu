@@ -721,6 +721,12 @@ constexpr int FUSED_WARPS = 4;
 #endif
 constexpr uint32_t F_CAP = 256;
 constexpr uint32_t VIS_CAP = 512;
+// layer sampling: a level's frontier is its fanout distinct picks (<= 32), so the layer kernels
+// keep 64-entry frontiers and a 256-entry visited list -- 24 KB of shared memory per 4-warp
+// block instead of 36 KB, and 64 registers: 8 blocks (32 warps) per SM instead of 6
+// (A/B cfg4 layer: 0.109 vs 0.119 ms per step); larger visited sets overflow to the batched driver
+constexpr uint32_t F_CAP_LAYER = 64;
+constexpr uint32_t VIS_CAP_LAYER = 256;
 
 struct FusedArgs {
     const int64_t* __restrict__ rp;
@@ -845,14 +851,16 @@ struct FusedLayerEmit {
 //        4 layer (scan), 5 layer (cache), 6 edge-weight NS (float CTPS, vscan.cuh; R28)
 template <int kMode>
 // blocks / SM: forest fire (no layer prefix table, 7 KB smem per warp) 8, layer 6 (smem-bound), NS 4
-__global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB : (kMode == 4 || kMode == 5) ? 6 : FUSED_MINB)
+__global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB : (kMode == 4 || kMode == 5) ? 8 : FUSED_MINB)
     k_sample_fused(FusedArgs a) {
     __shared__ uint64_t tab_all[FUSED_WARPS][TAB];
     __shared__ uint32_t bm_all[FUSED_WARPS][BM_WORDS];
-    __shared__ uint32_t F_all[FUSED_WARPS][F_CAP];
-    __shared__ uint32_t NX_all[FUSED_WARPS][F_CAP];
-    __shared__ uint32_t VIS_all[FUSED_WARPS][VIS_CAP];
-    __shared__ uint64_t PF_all[FUSED_WARPS][(kMode == 4 || kMode == 5) ? F_CAP : 1];   // layer pools only
+    constexpr uint32_t kF = (kMode == 4 || kMode == 5) ? F_CAP_LAYER : F_CAP;
+    constexpr uint32_t kVIS = (kMode == 4 || kMode == 5) ? VIS_CAP_LAYER : VIS_CAP;
+    __shared__ uint32_t F_all[FUSED_WARPS][kF];
+    __shared__ uint32_t NX_all[FUSED_WARPS][kF];
+    __shared__ uint32_t VIS_all[FUSED_WARPS][kVIS];
+    __shared__ uint64_t PF_all[FUSED_WARPS][(kMode == 4 || kMode == 5) ? kF : 1];   // layer pools only
     const int wib = threadIdx.x >> 5;
     uint64_t* tab = tab_all[wib];
     uint32_t* bm = bm_all[wib];
@@ -964,11 +972,11 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB :
                         if (VIS[q] == u) { u = NONE; break; }
                 const unsigned bal = __ballot_sync(FULL, u != NONE);
                 const uint32_t pos = nnx + __popc(bal & lanemask_lt());
-                if (u != NONE && pos < F_CAP) NX[pos] = u;
+                if (u != NONE && pos < kF) NX[pos] = u;
                 nnx += __popc(bal);
             }
             __syncwarp();
-            if (nnx > F_CAP) { ovf = true; break; }
+            if (nnx > kF) { ovf = true; break; }
             // sort + unique (set semantics, R10)
             uint32_t P2 = 32;
             while (P2 < nnx) P2 <<= 1;
@@ -997,7 +1005,7 @@ __global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB :
             }
             __syncwarp();
             nf = w;
-            if (nv + nf > VIS_CAP) { ovf = true; break; }
+            if (nv + nf > kVIS) { ovf = true; break; }
             for (uint32_t j = lane; j < nf; j += 32) VIS[nv + j] = F[j];
             nv += nf;
             __syncwarp();
