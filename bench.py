@@ -531,7 +531,8 @@ def main():
         wts = edge_weights(g, cfg.graph_seed) if cfg.bias == "weight" else None
         # (the narrow walk index + vertex heads stay built beside the buckets: without them the bucket
         # build measured 222 vs 20-54 ms and the walk 1.233 vs 1.209 ms on cfg2)
-        use_buckets = (use_cache or cfg.bias == "weight") and cfg.workload == "walk" and not args.no_walk_buckets
+        use_buckets = ((use_cache or cfg.bias == "weight") and cfg.workload == "walk" and not args.no_walk_buckets
+                       and not args.no_cache)
         G = cs.csaw_graph_create(g.row_ptr, g.col_idx, device=local, ctps_cache=use_cache, node2vec_tri=use_tri,
                                  next_meta=use_meta and args.next_meta, next_record=use_meta and not args.next_meta,
                                  walk_index=use_cache, node2vec_index=use_tri, edge_bias=use_eb,
