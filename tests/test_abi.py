@@ -75,3 +75,18 @@ def test_host_capacity_bounds():
     assert cs.csaw_sample_capacity("uniform", [3, 1, 2], 3, 10) == 10 * (3 + 3 + 6)
     assert cs.csaw_sample_capacity("layer", [2, 2], 2, 8192) == 8192 * 4
     assert cs.csaw_sample_capacity(cs.make_bias("forest_fire", pf=0.7), [], 2, 100) > 0
+
+
+def test_graph_flags_match_header():
+    """Every CSAW_GRAPH_* macro of csaw.h equals the binding's constant of the same name, and the
+    flags are distinct single bits (graph-creation options OR together)."""
+    src = open(_lib.HEADER).read()
+    macros = {m.group(1): int(m.group(2), 16) for m in re.finditer(r"#define (CSAW_GRAPH_\w+) (0x[0-9a-fA-F]+)u", src)}
+    assert len(macros) >= 24 and "CSAW_GRAPH_WALK_BUCKETS" in macros and "CSAW_GRAPH_NEXT_RECORD" in macros
+    for name, val in macros.items():
+        assert getattr(cs, name) == val, name
+        assert val & (val - 1) == 0, name
+    assert len(set(macros.values())) == len(macros)
+    # the info struct mirror carries the fields the binding reports
+    fields = [f for f, _ in _lib.csaw_graph_info_t._fields_]
+    assert "walk_buckets" in fields and fields.index("walk_buckets") == len(fields) - 2
