@@ -16,11 +16,12 @@
 // the dynamic node2vec bias keyed by the edge the walker arrived by):
 //     rec[e] (128 B; N2X_P = 24) = {index offset (40 bits) | C = |N(v) ∩ N(prev)| (24 bits),
 //                      ppos, mb, v = col[e], row start of v (40 bits) | deg(v) (24 bits), 0,
-//                      P[0..N2X_P)}
+//                      P[0..cap)}
 //         mb = members before ppos (members with value < prev: rows are sorted)
-//         P  = the member positions themselves when C <= N2X_P, else N2X_P splitters
-//              P[k] = I[j_k], j_k = floor((k + 1) C / (N2X_P + 1))
-//     idx[off .. off + C) = ascending positions I in N(v) of the members (C > N2X_P only).
+//         cap = 48 u16 values when deg(v) <= 65,536 (every position fits 16 bits), else 24 u32
+//         P  = the member positions themselves when C <= cap, else cap splitters
+//              P[k] = I[j_k], j_k = floor((k + 1) C / (cap + 1))
+//     idx[off .. off + C) = ascending positions I in N(v) of the members (C > cap only).
 // The record of the entry a walker arrived by carries everything the next step needs
 // (its vertex, row and degree, and the step's specials or their splitters), so a step
 // is one record and, for C > N2X_P, a binary search of about log2(C / (N2X_P + 1)) probes
@@ -42,6 +43,26 @@
 
 
 namespace csaw {
+
+// Inline area of a record (96 B): the member positions / splitters in N(v) as 2 N2X_P u16 values
+// when every position of N(v) fits 16 bits (deg(v) <= 65,536: "narrow"), else N2X_P u32 values.
+#ifndef N2X_NARROW_DEG_N
+#define N2X_NARROW_DEG_N 65536   // 0: u32 inline values only (A/B)
+#endif
+constexpr uint32_t N2X_NARROW_DEG = N2X_NARROW_DEG_N;
+__host__ __device__ __forceinline__ bool n2x_narrow(uint64_t d) { return d <= N2X_NARROW_DEG; }
+__host__ __device__ __forceinline__ uint32_t n2x_cap(uint64_t d) { return n2x_narrow(d) ? 2 * N2X_P : N2X_P; }
+__device__ __forceinline__ uint32_t n2x_get(const void* P, bool narrow, uint32_t k) {
+    return narrow ? static_cast<uint32_t>(static_cast<const uint16_t*>(P)[k]) : static_cast<const uint32_t*>(P)[k];
+}
+__device__ __forceinline__ void n2x_put(void* P, bool narrow, uint32_t k, uint32_t v) {
+    if (narrow) static_cast<uint16_t*>(P)[k] = static_cast<uint16_t>(v);
+    else static_cast<uint32_t*>(P)[k] = v;
+}
+// rank of splitter k of C members: floor((k + 1) C / (cap + 1)), cap = 48 or 24 ((k + 1) C < 2^30)
+__host__ __device__ __forceinline__ uint32_t n2x_split(bool narrow, uint32_t k, uint32_t C) {
+    return narrow ? ((k + 1) * C) / (2 * N2X_P + 1) : ((k + 1) * C) / (N2X_P + 1);
+}
 
 // ---------------------------------------------------------------- build
 // Hub rank bitmaps: for the vertices of highest degree (d >= N2X_HUB_DEG, up to a memory
@@ -185,13 +206,12 @@ __global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict
                 if (f) {
                     const uint32_t rank = cnt + __popc(m & lanemask_lt());
                     const uint32_t pu = static_cast<uint32_t>(sv ? l : i), pv = static_cast<uint32_t>(sv ? i : l);
-                    if (C_all > N2X_P) {   // entry e: positions in N(u); entry r: positions in N(v)
-                        idx[off_e + rank] = pu;
-                        idx[off_r + rank] = pv;
-                    } else {           // inline in the records
-                        reinterpret_cast<uint32_t*>(rec + N2X_U4 * ecur + 2)[rank] = pu;
-                        reinterpret_cast<uint32_t*>(rec + N2X_U4 * r + 2)[rank] = pv;
-                    }
+                    // entry e (walker at u): positions in N(u); entry r (walker at v): positions in N(v);
+                    // listed in idx when C exceeds that record's inline capacity, else inline
+                    if (C_all > n2x_cap(du)) idx[off_e + rank] = pu;
+                    else n2x_put(rec + N2X_U4 * ecur + 2, n2x_narrow(du), rank, pu);
+                    if (C_all > n2x_cap(dv)) idx[off_r + rank] = pv;
+                    else n2x_put(rec + N2X_U4 * r + 2, n2x_narrow(dv), rank, pv);
                 }
             } else {
                 below_v += __popc(__ballot_sync(FULL, f && x < v));
@@ -212,9 +232,12 @@ __global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict
 // exclusive scan of the listed member counts (C > N2X_P) into the records' 40-bit offsets
 struct N2xCount {
     const uint4* rec;
+    const int64_t* rp;
+    const uint32_t* col;
     __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
         const uint32_t c = rec[N2X_U4 * i].y >> 8;
-        return c > N2X_P ? c : 0;
+        const uint32_t v = col[i];
+        return c > n2x_cap(static_cast<uint64_t>(rp[v + 1] - rp[v])) ? c : 0;
     }
 };
 struct N2xOffset {
@@ -239,10 +262,12 @@ __global__ void k_n2x_dst(const int64_t* __restrict__ rp, const uint32_t* __rest
         rec[N2X_U4 * e + 1] = make_uint4(v, static_cast<uint32_t>(rs), static_cast<uint32_t>(rs >> 32) | (d << 8), 0u);
         const uint4 q = rec[N2X_U4 * e];
         const uint32_t C = q.y >> 8;
-        if (C > N2X_P) {
+        const bool nw = n2x_narrow(d);
+        const uint32_t cap = n2x_cap(d);
+        if (C > cap) {
             const uint32_t* I = idx + (q.x | (static_cast<uint64_t>(q.y & 0xFFu) << 32));
-            uint32_t* P = reinterpret_cast<uint32_t*>(rec + N2X_U4 * e + 2);
-            for (uint32_t k = 0; k < N2X_P; ++k) P[k] = I[((k + 1) * static_cast<uint64_t>(C)) / (N2X_P + 1)];
+            void* P = rec + N2X_U4 * e + 2;
+            for (uint32_t k = 0; k < cap; ++k) n2x_put(P, nw, k, I[n2x_split(nw, k, C)]);
         }
     }
 }
@@ -337,7 +362,7 @@ csaw_status build_n2v_index(csaw_graph* g, int blocks) {
     unsigned int h = 0;
     if (cudaMemcpy(&h, asym, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess || h)   // not symmetric
         return (free_hubs(), drop());
-    if (device_scan(N2xCount{g->n2x_rec}, static_cast<uint64_t>(E), N2xOffset{g->n2x_rec, tot}, part, nullptr) != CSAW_OK)
+    if (device_scan(N2xCount{g->n2x_rec, g->row_ptr, g->col}, static_cast<uint64_t>(E), N2xOffset{g->n2x_rec, tot}, part, nullptr) != CSAW_OK)
         return (free_hubs(), drop());
     unsigned long long total = 0;
     if (cudaMemcpy(&total, tot, sizeof(total), cudaMemcpyDeviceToHost) != cudaSuccess) return (free_hubs(), drop());
@@ -398,19 +423,20 @@ __device__ __forceinline__ int64_t n2x_S(uint32_t wq, int64_t dq1, uint32_t p, u
 // and S(j_k, P[k]) <= x" holds on a prefix of k (S increases with the rank), so a binary search
 // over k reads about log2(N2X_P) inline values.  On return l - 1 is the last rank known to pass
 // (pos = its position if l > lo) and h the first known to fail.
-__device__ __forceinline__ void n2x_inline(const uint32_t* P, uint32_t C, uint32_t lo, uint32_t hi, int64_t x,
-                                           uint32_t wq, int64_t dq1, int64_t sub, uint32_t& l, uint32_t& h,
+__device__ __forceinline__ void n2x_inline(const void* P, bool narrow, uint32_t C, uint32_t lo, uint32_t hi,
+                                           int64_t x, uint32_t wq, int64_t dq1, int64_t sub, uint32_t& l, uint32_t& h,
                                            uint32_t& pos) {
-    const bool in = C <= N2X_P;
-    uint32_t a0 = 0, a1 = in ? C : N2X_P;
+    const uint32_t cap = narrow ? 2 * N2X_P : N2X_P;
+    const bool in = C <= cap;
+    uint32_t a0 = 0, a1 = in ? C : cap;
     l = lo;
     h = hi;
     while (a0 < a1) {
         const uint32_t k = (a0 + a1) >> 1;
-        const uint32_t j = in ? k : ((k + 1) * C) / (N2X_P + 1);   // (k + 1) C < 2^29
+        const uint32_t j = in ? k : n2x_split(narrow, k, C);
         bool t = j < lo;
         if (!t && j < hi) {
-            const uint32_t pk = P[k];
+            const uint32_t pk = n2x_get(P, narrow, k);
             t = n2x_S(wq, dq1, pk, j, sub) <= x;
             if (t) { l = j + 1; pos = pk; } else h = j;
         }
@@ -422,11 +448,12 @@ __device__ __forceinline__ void n2x_inline(const uint32_t* P, uint32_t C, uint32
 // Last member rank j in [lo, hi) with S(j, I[j]) <= x; found = false if none, else pos = I[j]:
 // the inline values, then a plain binary search over idx between two splitters (about
 // log2(C / (N2X_P + 1)) probes).
-__device__ __forceinline__ uint32_t n2x_last_le(const uint32_t* __restrict__ I, const uint32_t* P, uint32_t C,
-                                                uint32_t lo, uint32_t hi, int64_t x, uint32_t wq, int64_t dq1,
-                                                int64_t sub, uint32_t& probes, bool& found, uint32_t& pos) {
+__device__ __forceinline__ uint32_t n2x_last_le(const uint32_t* __restrict__ I, const void* P, bool narrow,
+                                                uint32_t C, uint32_t lo, uint32_t hi, int64_t x, uint32_t wq,
+                                                int64_t dq1, int64_t sub, uint32_t& probes, bool& found,
+                                                uint32_t& pos) {
     uint32_t l, h;
-    n2x_inline(P, C, lo, hi, x, wq, dq1, sub, l, h, pos);
+    n2x_inline(P, narrow, C, lo, hi, x, wq, dq1, sub, l, h, pos);
     while (l < h) {
         const uint32_t mid = (l + h) >> 1;
         const uint32_t p = __ldg(I + mid);
@@ -468,7 +495,7 @@ __global__ void __launch_bounds__(256, N2X_MINB) k_node2vec_idx(N2xArgs a) {
         ++steps;
         for (int32_t t = 1;; ++t) {
             const uint4 ra = __ldg(a.rec + N2X_U4 * e), rb = __ldg(a.rec + N2X_U4 * e + 1);
-            const uint32_t* P = reinterpret_cast<const uint32_t*>(a.rec + N2X_U4 * e + 2);
+            const void* P = a.rec + N2X_U4 * e + 2;
             row[t] = rb.x;                          // the vertex this entry leads to
             if (t == a.L) break;
             // step t at v = rb.x, arrived from prev by entry e (d >= 1: prev is in N(v))
@@ -488,8 +515,8 @@ __global__ void __launch_bounds__(256, N2X_MINB) k_node2vec_idx(N2xArgs a) {
                 const bool after = x >= Sp;
                 const int64_t sub = after ? dqp : 0;
                 bool found = false;
-                const uint32_t j = n2x_last_le(I, P, C, after ? mb : 0, after ? C : mb, x, wq, dq1, sub, probes, found,
-                                               pos);
+                const uint32_t j = n2x_last_le(I, P, n2x_narrow(d), C, after ? mb : 0, after ? C : mb, x, wq, dq1, sub,
+                                               probes, found, pos);
                 if (found) {
                     const int64_t Sm = n2x_S(wq, dq1, pos, j, sub);
                     s = x < Sm + w1 ? pos : pos + 1 + n2x_div(x - Sm - w1, a);
@@ -523,7 +550,7 @@ struct N2xSearch {          // one walker's step in flight
 };
 
 // record -> the step's search state (prev's own region resolves at once)
-__device__ __forceinline__ void n2x_setup(const N2xArgs& a, uint4 ra, uint4 rb, const uint32_t* P, uint64_t U,
+__device__ __forceinline__ void n2x_setup(const N2xArgs& a, uint4 ra, uint4 rb, const void* P, uint64_t U,
                                           int64_t dq1, int64_t dqp, N2xSearch& q) {
     const uint32_t wq = a.wq, w1 = a.w1, wp = a.wp;
     q.rs = rb.y | (static_cast<uint64_t>(rb.z & 0xFFu) << 32);
@@ -539,7 +566,7 @@ __device__ __forceinline__ void n2x_setup(const N2xArgs& a, uint4 ra, uint4 rb, 
     q.after = q.x >= q.Sp;
     q.sub = q.after ? dqp : 0;
     q.lo = q.after ? q.mb : 0;
-    n2x_inline(P, q.C, q.lo, q.after ? q.C : q.mb, q.x, wq, dq1, q.sub, q.l, q.h, q.pos);
+    n2x_inline(P, n2x_narrow(d), q.C, q.lo, q.after ? q.C : q.mb, q.x, wq, dq1, q.sub, q.l, q.h, q.pos);
 }
 
 // search finished: the pick's position in N(v)
@@ -689,7 +716,7 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
             {   // records arrived: path entry, then the step's search
                 if (me) {
                     const uint4 ra = recs[wib][k][lane][0], rb = recs[wib][k][lane][1];
-                    const uint32_t* P = reinterpret_cast<const uint32_t*>(&recs[wib][k][lane][2]);
+                    const void* P = &recs[wib][k][lane][2];
                     uint32_t* row = a.path + G[k].w * (static_cast<uint64_t>(a.L) + 1);
                     row[G[k].t] = rb.x;
                     if (G[k].t < a.L) {
