@@ -209,8 +209,8 @@ typedef struct {
  * if the graph is symmetric): node2vec per-edge intersection index.  For every CSR entry
  * e = (prev -> v): the count C of common neighbours N(v) ∩ N(prev), the position of prev in
  * N(v), and the ascending positions in N(v) of the common neighbours (a 128 B record per
- * entry with up to 24 of them inline, + 4 B per common-neighbour pair beyond; ~66 GB of
- * device memory with the cfg3 graph).  Integer node2vec walks
+ * entry with up to 48 u16 / 24 u32 of them inline, + 2 / 4 B per common-neighbour pair beyond;
+ * ~40 GB of device memory with the cfg3 graph).  Integer node2vec walks
  * (R16) then binary-search those positions for the region of the draw (the CTPS
  * is piecewise linear between them) instead of merging N(v) with N(prev): O(log C) reads
  * per step.  Picks are identical.  Best-effort: if the index does not fit, the graph is

@@ -21,7 +21,7 @@
 //         cap = 48 u16 values when deg(v) <= 65,536 (every position fits 16 bits), else 24 u32
 //         P  = the member positions themselves when C <= cap, else cap splitters
 //              P[k] = I[j_k], j_k = floor((k + 1) C / (cap + 1))
-//     idx[off .. off + C) = ascending positions I in N(v) of the members (C > cap only).
+//     idx[off ..) = ascending positions I in N(v) of the members (C > cap only; u16 for narrow rows).
 // The record of the entry a walker arrived by carries everything the next step needs
 // (its vertex, row and degree, and the step's specials or their splitters), so a step
 // is one record and, for C > N2X_P, a binary search of about log2(C / (N2X_P + 1)) probes
@@ -208,10 +208,10 @@ __global__ void k_n2x(const int64_t* __restrict__ rp, const uint32_t* __restrict
                     const uint32_t pu = static_cast<uint32_t>(sv ? l : i), pv = static_cast<uint32_t>(sv ? i : l);
                     // entry e (walker at u): positions in N(u); entry r (walker at v): positions in N(v);
                     // listed in idx when C exceeds that record's inline capacity, else inline
-                    if (C_all > n2x_cap(du)) idx[off_e + rank] = pu;
-                    else n2x_put(rec + N2X_U4 * ecur + 2, n2x_narrow(du), rank, pu);
-                    if (C_all > n2x_cap(dv)) idx[off_r + rank] = pv;
-                    else n2x_put(rec + N2X_U4 * r + 2, n2x_narrow(dv), rank, pv);
+                    n2x_put(C_all > n2x_cap(du) ? static_cast<void*>(idx + off_e) : static_cast<void*>(rec + N2X_U4 * ecur + 2),
+                            n2x_narrow(du), rank, pu);
+                    n2x_put(C_all > n2x_cap(dv) ? static_cast<void*>(idx + off_r) : static_cast<void*>(rec + N2X_U4 * r + 2),
+                            n2x_narrow(dv), rank, pv);
                 }
             } else {
                 below_v += __popc(__ballot_sync(FULL, f && x < v));
@@ -237,7 +237,8 @@ struct N2xCount {
     __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
         const uint32_t c = rec[N2X_U4 * i].y >> 8;
         const uint32_t v = col[i];
-        return c > n2x_cap(static_cast<uint64_t>(rp[v + 1] - rp[v])) ? c : 0;
+        const uint64_t d = static_cast<uint64_t>(rp[v + 1] - rp[v]);
+        return c > n2x_cap(d) ? (n2x_narrow(d) ? (c + 1) / 2 : c) : 0;   // u32 units (narrow rows: u16 pairs)
     }
 };
 struct N2xOffset {
@@ -267,7 +268,7 @@ __global__ void k_n2x_dst(const int64_t* __restrict__ rp, const uint32_t* __rest
         if (C > cap) {
             const uint32_t* I = idx + (q.x | (static_cast<uint64_t>(q.y & 0xFFu) << 32));
             void* P = rec + N2X_U4 * e + 2;
-            for (uint32_t k = 0; k < cap; ++k) n2x_put(P, nw, k, I[n2x_split(nw, k, C)]);
+            for (uint32_t k = 0; k < cap; ++k) n2x_put(P, nw, k, n2x_get(I, nw, n2x_split(nw, k, C)));
         }
     }
 }
@@ -456,7 +457,8 @@ __device__ __forceinline__ uint32_t n2x_last_le(const uint32_t* __restrict__ I, 
     n2x_inline(P, narrow, C, lo, hi, x, wq, dq1, sub, l, h, pos);
     while (l < h) {
         const uint32_t mid = (l + h) >> 1;
-        const uint32_t p = __ldg(I + mid);
+        const uint32_t p = narrow ? static_cast<uint32_t>(__ldg(reinterpret_cast<const unsigned short*>(I) + mid))
+                                  : __ldg(I + mid);
         ++probes;
         if (n2x_S(wq, dq1, p, mid, sub) <= x) { l = mid + 1; pos = p; } else h = mid;
     }
@@ -543,10 +545,10 @@ __global__ void __launch_bounds__(256, N2X_MINB) k_node2vec_idx(N2xArgs a) {
 // ---- A step's search state (shared by the kernels below).
 struct N2xSearch {          // one walker's step in flight
     uint64_t rs;            // row start of v
-    const uint32_t* I;      // member positions of the entry
+    const uint32_t* I;      // member positions of the entry (u16 pairs when narrow)
     int64_t x, Sp, sub;
     uint32_t C, ppos, mb, lo, l, h, pos, s;
-    bool after, done;
+    bool after, done, narrow;
 };
 
 // record -> the step's search state (prev's own region resolves at once)
@@ -557,6 +559,7 @@ __device__ __forceinline__ void n2x_setup(const N2xArgs& a, uint4 ra, uint4 rb, 
     const uint32_t d = rb.z >> 8;
     q.C = ra.y >> 8; q.ppos = ra.z; q.mb = ra.w;
     q.I = a.idx + (ra.x | (static_cast<uint64_t>(ra.y & 0xFFu) << 32));
+    q.narrow = n2x_narrow(rb.z >> 8);
     const uint64_t T = static_cast<uint64_t>(wq) * (d - q.C - 1) + static_cast<uint64_t>(w1) * q.C + wp;
     q.x = static_cast<int64_t>(below(U, T));
     q.Sp = n2x_S(wq, dq1, q.ppos, q.mb, 0);
@@ -735,7 +738,9 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
                         // 128 B lines from DRAM: .L2::64B measured 7.81 vs 7.54 ms on cfg3)
                 while (G[k].q.l < G[k].q.h) {
                     const uint32_t mid = (G[k].q.l + G[k].q.h) >> 1;
-                    const uint32_t p = __ldg(G[k].q.I + mid);
+                    const uint32_t p = G[k].q.narrow
+                                           ? static_cast<uint32_t>(__ldg(reinterpret_cast<const unsigned short*>(G[k].q.I) + mid))
+                                           : __ldg(G[k].q.I + mid);
                     ++probes_all;
                     if (n2x_S(wq, dq1, p, mid, G[k].q.sub) <= G[k].q.x) { G[k].q.l = mid + 1; G[k].q.pos = p; }
                     else G[k].q.h = mid;
