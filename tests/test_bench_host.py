@@ -122,3 +122,37 @@ def test_sample_bytes_cached_sector_model():
     # 4, 4, 2, 1, 3, 2 -> 2, 2, 1, 0, 2, 1 = 8
     b, m = bench.sample_alg_bytes(CONFIGS["cfg4_layer"], deg, seeds, offs, src, dst, dep, cached=True)
     assert m == "sample_cached" and b == 16 * 5 + 32 * (2 * 6 + 8) + 9 * 6
+
+
+def test_bucketed_walk_names_and_weight_models():
+    """The bucketed walk kernels are named in the roofline; the cached edge-weight walk uses the
+    NEXT-1 sector model (same formula as the cached degree walk), the per-step scan the stream model."""
+    assert bench.hot_kernel_name(CONFIGS["cfg2"], cached=True, wix_leaf=128, wix_group=32, heads=True,
+                                 buckets=True) == "k_walk_gb"
+    assert bench.hot_kernel_name(CONFIGS["cfg2"], cached=True, wix_leaf=128, wix_group=32,
+                                 heads=True) == "k_walk_head<128>"
+    assert bench.hot_kernel_name(CONFIGS["cfg2_weight"], buckets=True) == "k_walk_gbw"
+    assert bench.hot_kernel_name(CONFIGS["cfg2_weight"]) == "k_walk_vscan<float>"
+    deg = torch.tensor([3, 1, 2, 5], dtype=torch.int64)
+    path = torch.tensor([[0, 1, 0, 3], [2, 0, 2, 0]], dtype=torch.int32)
+    bc, mc = bench.walk_alg_bytes(CONFIGS["cfg2_weight"], deg, path, cached=True)
+    bd, _ = bench.walk_alg_bytes(CONFIGS["cfg2"], deg, path, cached=True)
+    assert mc == "walk_weight_cached" and bc == bd == 32 * (2 * 6 + 8) + 6 * 4
+    bs, ms = bench.walk_alg_bytes(CONFIGS["cfg2_weight"], deg, path, cached=False)
+    assert ms == "walk_weight_stream" and bs == 6 * 16 + 4 * 14 + 6 * 8
+
+
+def test_random_line_context():
+    """dram_frac_of_random_line_ceiling = ncu DRAM bytes / launch time / the measured random-line rate."""
+    c = bench.random_gather_context(500.0, traffic=4.35e9, hot_ms=1.0)
+    assert c["random_line_ceiling_gbs"] > 0
+    assert abs(c["dram_gbs_ncu"] - 4350.0) < 1e-6
+    assert abs(c["dram_frac_of_random_line_ceiling"] - 4350.0 / c["random_line_ceiling_gbs"]) < 1e-12
+    assert bench.random_gather_context(500.0)["dram_frac_of_random_line_ceiling"] is None
+
+
+def test_new_bench_options_parse():
+    a = bench.parse_args(["--no-walk-buckets", "--next-meta", "--mdrw-alt-records", "--config", "cfg5"])
+    assert a.no_walk_buckets and a.next_meta and a.mdrw_alt_records and a.config == "cfg5"
+    d = bench.parse_args([])
+    assert d.config == "cfg3" and not d.no_walk_buckets and d.gpus == 1
