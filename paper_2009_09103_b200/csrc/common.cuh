@@ -59,28 +59,11 @@ __device__ __forceinline__ uint64_t below(uint64_t U, uint64_t M) { return __umu
 // default; the .L2::64B prefetch-size qualifier (SASS LDG.E.LTC64B) limits it to 64 B.
 // Measured on B200 (scripts/random_granule.cu, profiles/r02_random_granule.txt): 127 -> 64 DRAM
 // bytes per random 4 B read at the same ~35 G reads/s.  For the pointer-chasing loads whose
-// neighbours are never used (index probes, per-step entry + metadata reads).
+// neighbours are never used (the MDRW per-step entry / metadata / vertex-id reads; the node2vec
+// index probes keep whole lines: .L2::64B there measured 7.81 vs 7.54 ms on cfg3).
 #ifndef CSAW_LD64B
 #define CSAW_LD64B 1
 #endif
-__device__ __forceinline__ uint32_t ld_rand_u32(const uint32_t* p) {
-#if CSAW_LD64B
-    uint32_t v;
-    asm("ld.global.nc.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-#else
-    return __ldg(p);
-#endif
-}
-__device__ __forceinline__ uint64_t ld_rand_u64(const uint64_t* p) {
-#if CSAW_LD64B
-    uint64_t v;
-    asm("ld.global.nc.L2::64B.u64 %0, [%1];" : "=l"(v) : "l"(p));
-    return v;
-#else
-    return __ldg(p);
-#endif
-}
 // coherent (not .nc) variant for state the kernel itself writes
 __device__ __forceinline__ uint32_t ld_rand_rw_u32(const uint32_t* p) {
 #if CSAW_LD64B
