@@ -211,3 +211,15 @@ def test_buckets_short_and_empty_calls():
     empty = torch.empty(0, dtype=torch.int32, device=DEV)
     assert cs.csaw_walk(Gb, "degree", empty, 10, rng_seed=1).shape == (0, 11)
     Gb.close(); Gh.close()
+
+
+def test_weight_buckets_fall_back_outside_their_range():
+    """Weights whose mean region width is below 2^-24 (here ~1e-30) cannot be bucketed (k out of
+    [-24, 7]): the graph is created without the weighted index and walks take the per-step scan."""
+    g = rmat_csr(1 << 12, 1 << 16, 3, device=DEV).to("cpu")
+    w = torch.full((g.col_idx.numel(),), 1e-30, dtype=torch.float32)
+    G, og = weighted(g.row_ptr, g.col_idx, w)
+    assert not (G.info()["walk_buckets"] & 2)
+    seeds = instance_seeds(g, 32, set_id=1).numpy()
+    check_weight_exact(G, og, seeds, 20, 3, range(32))   # equal weights: every boundary is far from the draws
+    G.close()
