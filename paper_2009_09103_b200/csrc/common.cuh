@@ -7,6 +7,9 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#ifdef CSAW_DEBUG_BOUNDS
+#include <cstdio>
+#endif
 
 namespace csaw {
 
@@ -53,6 +56,19 @@ __device__ __forceinline__ uint64_t draw_u64(uint2 key, uint32_t inst, uint32_t 
 
 // below(U, M) = floor(U * M / 2^64), uniform in [0, M).
 __device__ __forceinline__ uint64_t below(uint64_t U, uint64_t M) { return __umul64hi(U, M); }
+
+// Device bounds checks of a debug build (-DCSAW_DEBUG_BOUNDS: scripts/build_variants.sh); no code otherwise.
+#ifdef CSAW_DEBUG_BOUNDS
+#define CSAW_DASSERT(cond)                                                                      \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("CSAW_DASSERT failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);            \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define CSAW_DASSERT(cond) ((void)0)
+#endif
 
 // ---------------------------------------------------------------- random single-word loads
 // An L2 miss of a lone 4 / 8 B load fetches a whole 128 B line (4 sectors) from DRAM by

@@ -387,6 +387,7 @@ struct N2xArgs {
     const int64_t* __restrict__ rp;
     const uint4* __restrict__ rec;            // [N2X_U4 E]: 16 N2X_U4 B per entry
     const uint32_t* __restrict__ idx;
+    uint64_t idx_n;                           // u32 units of idx (debug bounds checks)
     const uint32_t* __restrict__ seeds;
     uint64_t n;
     int32_t L;
@@ -738,6 +739,7 @@ __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_t
                         // 128 B lines from DRAM: .L2::64B measured 7.81 vs 7.54 ms on cfg3)
                 while (G[k].q.l < G[k].q.h) {
                     const uint32_t mid = (G[k].q.l + G[k].q.h) >> 1;
+                    CSAW_DASSERT(static_cast<uint64_t>(G[k].q.I - a.idx) + (G[k].q.narrow ? mid / 2 : mid) < a.idx_n);
                     const uint32_t p = G[k].q.narrow
                                            ? static_cast<uint32_t>(__ldg(reinterpret_cast<const unsigned short*>(G[k].q.I) + mid))
                                            : __ldg(G[k].q.I + mid);
@@ -772,7 +774,7 @@ csaw_status launch_node2vec_index(const csaw_graph* g, const uint32_t* seeds, ui
     int32_t sh = -1;
     for (int b = 0; b < 31; ++b)
         if (wq == (1u << b)) sh = b;
-    N2xArgs a{g->row_ptr, g->n2x_rec, g->n2x_idx, seeds, n, L, base, key, path, counters, wp, w1, wq, sh,
+    N2xArgs a{g->row_ptr, g->n2x_rec, g->n2x_idx, g->n2x_total + 8, seeds, n, L, base, key, path, counters, wp, w1, wq, sh,
               1.0 / static_cast<double>(wq)};
     const uint64_t resident = static_cast<uint64_t>(g->num_sms) * 2048;
     if (N2X_TMA) {

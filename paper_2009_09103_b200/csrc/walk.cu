@@ -187,7 +187,8 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_wix(WalkArgs a, con
 // Same S, same draw, same region as every other degree-walk kernel and the oracle.
 __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_gb(WalkArgs a, const uint4* __restrict__ gbk,
                                                               const uint4* __restrict__ gmeta,
-                                                              const uint64_t* __restrict__ cps, uint64_t E) {
+                                                              const uint64_t* __restrict__ cps, uint64_t E,
+                                                              uint64_t nbk) {
     const int lane = lane_id();
     unsigned long long bytes = 0, steps = 0, links = 0;
     for (uint64_t w = walker_ticket(a.counters + 7); w < a.n; w = walker_ticket(a.counters + 7)) {
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_gb(WalkArgs a, cons
             if (cur != NONE && T > 0) {   // T = 0: no positive-bias neighbour, the walk ends (R20)
                 const uint32_t x = static_cast<uint32_t>(below(U, T));
                 uint4 e = make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
+                CSAW_DASSERT(static_cast<uint64_t>(B) + (x >> k) < nbk);
                 if (lane < 8) e = __ldg(gbk + (static_cast<uint64_t>(B) + (x >> k)) * 8 + lane);
                 const int fl = 31 - __clz(__ballot_sync(FULL, lane < 8 && e.x <= x));   // entry 0 always passes
                 const uint32_t uk = __shfl_sync(FULL, e.y, fl);
@@ -226,6 +228,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_gb(WalkArgs a, cons
                         if (gt) { ge += __ffs(gt) - 1; break; }
                         ge += 32;
                     }
+                    CSAW_DASSERT(ge < E);
                     nxt = __ldg(a.col + ge);
                     const uint4 mu = __ldg(gmeta + nxt);
                     B = mu.x;
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_gb(WalkArgs a, cons
 __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_gbw(WalkArgs a, const uint8_t* __restrict__ gbw,
                                                                const uint4* __restrict__ meta,
                                                                const double* __restrict__ cpsw,
-                                                               const float* __restrict__ w) {
+                                                               const float* __restrict__ w, uint64_t nbk) {
     constexpr int CAP = 5, KB = 24;
     const int lane = lane_id();
     unsigned long long bytes = 0, steps = 0, links = 0;
@@ -278,6 +281,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_gbw(WalkArgs a, con
             if (cur != NONE && T > 0.0) {   // T = 0: every weight of the row is 0, the walk ends (R20)
                 const double x = (static_cast<double>(U >> 11) * (1.0 / 9007199254740992.0)) * T;
                 const uint64_t bi = static_cast<uint64_t>(ldexp(x, -k));
+                CSAW_DASSERT(static_cast<uint64_t>(B) + bi < nbk);
                 const uint8_t* line = gbw + (static_cast<uint64_t>(B) + bi) * 128;
                 double S = __longlong_as_double(0x7FF0000000000000ll), Tu = 0.0;
                 uint32_t uk = 0, Bu = 0;
@@ -1812,6 +1816,7 @@ __global__ void __launch_bounds__(MDRW_WARPS * 32, 28 / MDRW_WARPS) k_mdrw_fast(
                     rb = static_cast<uint64_t>(__shfl_sync(FULL, e.w, fl)) << 32 | __shfl_sync(FULL, e.z, fl);
                 }
                 const uint64_t ei = rb + below(Ue, d);
+                CSAW_DASSERT(!a.nrc || ei < a.colc_n);
                 int64_t ru;
                 uint32_t du;
                 uint64_t mt = 0;
@@ -1937,12 +1942,13 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
     if (b.kind == CSAW_BIAS_WEIGHT && g->gbw) {
         constexpr int hw = 2;
         const int64_t hwarps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 64);
-        k_walk_gbw<<<static_cast<int>((hwarps + hw - 1) / hw), hw * 32, 0, st>>>(a, g->gbw, g->gwmeta, g->cpsw, g->w);
+        k_walk_gbw<<<static_cast<int>((hwarps + hw - 1) / hw), hw * 32, 0, st>>>(a, g->gbw, g->gwmeta, g->cpsw, g->w,
+                                                                                   g->gbw_buckets);
     } else if (b.kind == CSAW_BIAS_DEGREE && g->gbk) {
         constexpr int hw = 2;   // warps per block: the few walkers (cfg2: 4,000 warps) spread over all SMs
         const int64_t hwarps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 64);
         k_walk_gb<<<static_cast<int>((hwarps + hw - 1) / hw), hw * 32, 0, st>>>(a, g->gbk, g->gmeta, g->cps,
-                                                                                     static_cast<uint64_t>(g->E));
+                                                                                     static_cast<uint64_t>(g->E), g->gb_buckets);
     } else if (b.kind == CSAW_BIAS_DEGREE && g->wix_leaf) {
         // group kernels: 2-warp blocks, so few walkers (cfg2: 1,000 warps) still spread over all SMs
         const int wpb = g->wix_group == 32 ? WALK_WARPS : 2;
