@@ -605,7 +605,7 @@ __device__ __forceinline__ uint32_t n2x_finish(const N2xArgs& a, int64_t dq1, co
 #define N2X_TMA_K 1   // A/B r02 cfg3: K = 1 8.28 ms; K = 2 9.54 ms (80 regs) / 13.6 ms (64 regs + stack)
 #endif
 #ifndef N2X_TMA_WARPS
-#define N2X_TMA_WARPS 8
+#define N2X_TMA_WARPS 4   // 4-warp blocks, 8 per SM (A/B cfg3: 5.94 vs 6.02 ms with 8-warp blocks, 4 per SM)
 #endif
 #ifndef N2X_SMEM_STRIDE
 #define N2X_SMEM_STRIDE (N2X_U4 + 1)   // uint4 per lane slot of the staged records (N2X_U4 = unpadded)
@@ -635,7 +635,7 @@ struct N2xGroup {           // one group of 32 walkers (per-lane fields)
 };
 
 #ifndef N2X_TMA_MINB
-#define N2X_TMA_MINB 4   // <= 64 registers: 32 warps / SM (A/B r02 cfg3: 95 regs 11.45 ms, 64 regs 8.28, 48 regs + stack 9.14)
+#define N2X_TMA_MINB 8   // x 4 warps, <= 64 registers: 32 warps / SM (A/B r02 cfg3: 95 regs 11.45 ms, 64 regs 8.28, 48 regs + stack 9.14)
 #endif
 __global__ void __launch_bounds__(N2X_TMA_WARPS * 32, N2X_TMA_MINB) k_node2vec_tma(N2xArgs a) {
     constexpr int K = N2X_TMA_K;
