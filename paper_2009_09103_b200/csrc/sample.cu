@@ -712,7 +712,10 @@ __global__ void k_part_scatter(const uint32_t* __restrict__ qv, uint64_t nq, Own
 // fit (frontier > F_CAP, visited > VIS_CAP, more staged edges than ecap, or a
 // pool needing > 32 picks) raises the overflow flag and the host reruns the call
 // with the batched driver.
-constexpr int FUSED_WARPS = 4;
+#ifndef FUSED_WARPS_N
+#define FUSED_WARPS_N 4
+#endif
+constexpr int FUSED_WARPS = FUSED_WARPS_N;   // warps (instances in flight) per block
 #ifndef FUSED_MINB
 #define FUSED_MINB 4
 #endif
@@ -851,7 +854,7 @@ struct FusedLayerEmit {
 //        4 layer (scan), 5 layer (cache), 6 edge-weight NS (float CTPS, vscan.cuh; R28)
 template <int kMode>
 // blocks / SM: forest fire (no layer prefix table, 7 KB smem per warp) 8, layer 6 (smem-bound), NS 4
-__global__ void __launch_bounds__(FUSED_WARPS * 32, kMode == 3 ? FUSED_FF_MINB : (kMode == 4 || kMode == 5) ? 8 : FUSED_MINB)
+__global__ void __launch_bounds__(FUSED_WARPS * 32, (kMode == 3 ? FUSED_FF_MINB : (kMode == 4 || kMode == 5) ? 8 : FUSED_MINB) * 4 / FUSED_WARPS)
     k_sample_fused(FusedArgs a) {
     __shared__ uint64_t tab_all[FUSED_WARPS][TAB];
     __shared__ uint32_t bm_all[FUSED_WARPS][BM_WORDS];
