@@ -1,7 +1,7 @@
 #!/bin/bash
 # HEAD check: build, smoke, the whole GPU suite, default bench line
-mkdir -p gpurun_out/r3s4
-O=gpurun_out/r3s4
+mkdir -p gpurun_out/r3s5
+O=gpurun_out/r3s5
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo "build rc=$?"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 $O/smoke.log
 timeout 2400 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1; echo "pytest rc=$?"; tail -3 $O/pytest.log
