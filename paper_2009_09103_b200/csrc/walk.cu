@@ -178,6 +178,9 @@ __global__ void __launch_bounds__(WALK_WARPS * 32, 4) k_walk_wix(WalkArgs a, con
     }
 }
 
+#ifndef GB_WARPS
+#define GB_WARPS 2
+#endif
 // Degree-biased walk over the bucketed index (CSAW_GRAPH_WALK_BUCKETS, capi.cu build_gb): a step
 // is x = below(U, T), ONE 128 B line -- bucket x >> k of the current vertex, 8 entries read by
 // lanes 0..7 -- and the last entry with S_i <= x, which carries the next vertex with its own
@@ -1945,7 +1948,7 @@ csaw_status run_walk(const csaw_graph* g, const csaw_bias& b, int32_t length, co
         k_walk_gbw<<<static_cast<int>((hwarps + hw - 1) / hw), hw * 32, 0, st>>>(a, g->gbw, g->gwmeta, g->cpsw, g->w,
                                                                                    g->gbw_buckets);
     } else if (b.kind == CSAW_BIAS_DEGREE && g->gbk) {
-        constexpr int hw = 2;   // warps per block: the few walkers (cfg2: 4,000 warps) spread over all SMs
+        constexpr int hw = GB_WARPS;   // warps per block: the few walkers (cfg2: 4,000 warps) spread over all SMs
         const int64_t hwarps = std::min<int64_t>(n, static_cast<int64_t>(g->num_sms) * 64);
         k_walk_gb<<<static_cast<int>((hwarps + hw - 1) / hw), hw * 32, 0, st>>>(a, g->gbk, g->gmeta, g->cps,
                                                                                      static_cast<uint64_t>(g->E), g->gb_buckets);
